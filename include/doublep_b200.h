@@ -1,0 +1,196 @@
+/*
+ * doublep_b200.h -- C ABI of the B200-native Double-P decode path.
+ *
+ * Double-P (arxiv 2602.05191): hierarchical top-p sparse decode attention
+ * over a k-means-clustered KV cache.  This header is the drop-in boundary
+ * that replaces the reference's kernel plugin seam
+ * (/root/reference/pkg/src/doublep/kernels.py:47-96) one level higher: the
+ * reference seam is per-query and host-memory based; these entry points are
+ * batched over (sequence, kv head, q head) and take DEVICE pointers, so a
+ * whole per-layer decode step is a few stream-ordered launches with no host
+ * synchronisation (CUDA-graph capturable).
+ *
+ * Conventions
+ *   - all buffers are caller-owned device memory; nothing allocates on the
+ *     step path (workspace sized once with dp_*_workspace_bytes);
+ *   - every call is stream-ordered on the caller's cudaStream_t (passed as
+ *     void* so this header needs no CUDA include);
+ *   - return value: DP_OK or an error code; dp_last_error() gives a
+ *     thread-local message.  DP_ERR_INVALID maps to the reference's
+ *     ValueError messages (engine.py:118,162,259-261,270-274;
+ *     clustering.py:73,281);
+ *   - re-entrant across streams given distinct workspaces.
+ *
+ * Device cache layout (one layer, batch B, kv heads H, per (b,h) "head"):
+ *   rows [0, sink)                         sink tokens, position order
+ *   rows [sink, n_tokens - window)         clustered tokens, CLUSTER-CONTIGUOUS:
+ *                                          cluster c owns rows [offs[c], offs[c+1])
+ *                                          (prefill clusters in compacted k-means id
+ *                                          order, then residual singletons appended
+ *                                          by decode-time growth, clustering.py:219-229)
+ *   rows [n_tokens - window, n_tokens)     sliding window, position order
+ * keys/values [B,H,row_cap,d]; centroids/value_means fp32 [B,H,cluster_cap,d];
+ * offs int32 [B,H,cluster_cap+1]; nclusters int32 [B,H].
+ */
+#ifndef DOUBLEP_B200_H
+#define DOUBLEP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DP_OK 0
+#define DP_ERR_INVALID 1     /* bad argument / reference ValueError class */
+#define DP_ERR_CUDA 2        /* CUDA runtime error */
+#define DP_ERR_UNSUPPORTED 3 /* shape outside what the kernels were built for */
+
+#define DP_F32 0
+#define DP_BF16 1
+
+typedef struct dp_cache_view {
+  int32_t batch, kv_heads, head_dim, dtype; /* dtype: DP_F32 | DP_BF16 */
+  int32_t row_cap;     /* rows allocated per head */
+  int32_t n_tokens;    /* rows in use per head (prefill + appended) */
+  int32_t sink, window;
+  int32_t cluster_cap; /* table capacity per head */
+  int32_t _pad;
+  const void* keys;           /* [B,H,row_cap,d] */
+  const void* values;         /* [B,H,row_cap,d] */
+  const int32_t* offs;        /* [B,H,cluster_cap+1] absolute row offsets */
+  const int32_t* nclusters;   /* [B,H] */
+  const float* centroids;     /* [B,H,cluster_cap,d] fp32 (exact means rounded) */
+  const float* value_means;   /* [B,H,cluster_cap,d] fp32 */
+} dp_cache_view;
+
+/* ---------------------------------------------------------------------- */
+/* library                                                                  */
+/* ---------------------------------------------------------------------- */
+int dp_version(void);
+const char* dp_last_error(void);
+/* number of SMs / compute capability of the current device (for callers) */
+int dp_device_info(int32_t* sm_count, int32_t* cc_major, int32_t* cc_minor);
+
+/* ---------------------------------------------------------------------- */
+/* decode step                                                              */
+/* ---------------------------------------------------------------------- */
+
+/* Workspace for dp_select / dp_sparse_attention / dp_decode_step /
+ * dp_dense_attention at this geometry and GQA group size. */
+size_t dp_decode_workspace_bytes(const dp_cache_view* v, int32_t gqa_group);
+
+/* Size-weighted centroid scores, replaces estimate_cluster_distribution
+ * (engine.py:158-177; kernels.scaled_logits _kernels_cy.pyx:21-33):
+ *   log_mass[b, h*G+g, c] = (C[b,h,c] . q[b,h*G+g]) * scale + log(|c|)
+ * fp64 accumulation over fp32 centroids.  q [B, H*G, d] (q_dtype),
+ * log_mass fp64 [B, H*G, cluster_cap] (entries >= nclusters untouched). */
+int dp_score(const dp_cache_view* v, const void* q, int32_t q_dtype, int32_t gqa_group,
+             double scale, double* log_mass, void* stream);
+
+/* Two-stage top-p, replaces plan_selection + top_p_select
+ * (engine.py:180-213, selection.py:36-65).  Per q head: stage 1 keeps the
+ * minimal descending-probability prefix with cumsum/total >= p1 (ties ->
+ * lower cluster id); stage 2 keeps the minimal prefix of that set reaching
+ * p2 of its renormalised mass.  state[b,hq,c] = 2 exact, 1 approx, 0 drop.
+ * counts[b,hq,0..1] = (|C_p|, |C_exact|).  Nullable debug outputs: order
+ * [B,Hq,cluster_cap] the full descending order (estimate.order,
+ * engine.py:169; its first counts[0] entries are stage1.selected), cum_mass
+ * [B,Hq] the stage-1 normalised cumulative mass, probs [B,Hq,cluster_cap]
+ * the estimated cluster distribution (engine.py:168). */
+int dp_select(const dp_cache_view* v, int32_t gqa_group, double p1, double p2,
+              const double* log_mass, uint8_t* state, int32_t* counts, int32_t* order,
+              double* cum_mass, double* probs, void* workspace, size_t workspace_bytes,
+              void* stream);
+
+/* Mixed exact/approximate attention under one normaliser, replaces
+ * mixed_attention / sparse_attention (engine.py:216-264):
+ *   exact rows = sink + window + members of state==2 clusters,
+ *   approx pseudo-rows = (log_mass, value_mean) of state==1 clusters.
+ * out fp32 [B,Hq,d], lse fp32 [B,Hq] (log of the shared normaliser).
+ * stats (nullable) int32 [B,H,4] = (union exact rows, union approx clusters,
+ * row chunks, 0) -- the quantities the algorithmic byte count uses. */
+int dp_sparse_attention(const dp_cache_view* v, const void* q, int32_t q_dtype,
+                        int32_t gqa_group, double scale, const double* log_mass,
+                        const uint8_t* state, float* out, float* lse, int32_t* stats,
+                        void* workspace, size_t workspace_bytes, void* stream);
+
+/* score + select + sparse attention in one call (decode_step,
+ * engine.py:267-278).  log_mass/state/counts are caller buffers so the plan
+ * stays inspectable. */
+int dp_decode_step(const dp_cache_view* v, const void* q, int32_t q_dtype, int32_t gqa_group,
+                   double scale, double p1, double p2, double* log_mass, uint8_t* state,
+                   int32_t* counts, float* out, float* lse, int32_t* stats, void* workspace,
+                   size_t workspace_bytes, void* stream);
+
+/* Dense split-KV flash decoding over all n_tokens rows (the full_attention
+ * comparator, engine.py:122-144). */
+int dp_dense_attention(const dp_cache_view* v, const void* q, int32_t q_dtype,
+                       int32_t gqa_group, double scale, float* out, float* lse,
+                       void* workspace, size_t workspace_bytes, void* stream);
+
+/* Decode-time growth (ClusteredCache.append_tokens, clustering.py:182-196):
+ * writes one new token per (b,h) at row n_tokens (keys/values must have
+ * row_cap > n_tokens) and turns the row leaving the window into a residual
+ * singleton cluster (clustering.py:178-229).  The caller then uses
+ * n_tokens + 1.  new_k/new_v [B,H,d] in the cache dtype. */
+int dp_append_token(const dp_cache_view* v, const void* new_k, const void* new_v, void* stream);
+
+/* ---------------------------------------------------------------------- */
+/* prefill clustering (build_clustered_cache, clustering.py:266-314)        */
+/* ---------------------------------------------------------------------- */
+
+typedef struct dp_cluster_params {
+  int32_t batch, kv_heads, head_dim, dtype;
+  int32_t n_tokens, sink, window;
+  int32_t k;          /* requested clusters (already clamped to middle) */
+  int32_t max_iters;
+  int32_t fp64_assign; /* 1: fp64 distances (reference-exact); 0: fp32 */
+} dp_cluster_params;
+
+/* Workspace for dp_cluster_build. */
+size_t dp_cluster_workspace_bytes(const dp_cluster_params* p);
+
+/* k-means++ init (clustering.py:36-55, replaying the host RNG stream),
+ * Lloyd with empty-cluster drop (clustering.py:58-107), then the
+ * cluster-contiguous tables.
+ *   src_keys/src_values [B,H,n_tokens,d] position order (dtype)
+ *   first_pick int32 [B*H]      rng.integers(n) of each head's stream
+ *   uniforms  fp64 [B*H, k-1]   rng.random() draws of each head's stream
+ *   alt_picks int32 [B*H, k-1]  (nullable) per-step explicit picks used from
+ *                               step degenerate_from[b*H+h] on (rng.integers
+ *                               draws once the sampling mass hits 0)
+ *   degenerate_from int32 [B*H] (nullable; in/out) in: step from which
+ *                               alt_picks apply (k = never); out: first step
+ *                               whose sampling mass was 0 (k = none)
+ * Outputs (device, caller-owned):
+ *   dst_keys/dst_values [B,H,row_cap,d] cluster-ordered rows (row_cap >= n_tokens)
+ *   offs [B,H,cluster_cap+1], nclusters [B,H], centroids/value_means fp32
+ *   [B,H,cluster_cap,d] (cluster_cap >= k), perm int32 [B,H,row_cap]
+ *   (original position of every row), objective fp64 [B*H, max_iters]
+ *   (per-iteration sum of squared distances), iters int32 [B*H]. */
+int dp_cluster_build(const dp_cluster_params* p, const void* src_keys, const void* src_values,
+                     const int32_t* first_pick, const double* uniforms, const int32_t* alt_picks,
+                     int32_t* degenerate_from, void* dst_keys, void* dst_values, int32_t row_cap,
+                     int32_t* offs, int32_t* nclusters, float* centroids, float* value_means,
+                     int32_t cluster_cap, int32_t* perm, double* objective, int32_t* iters,
+                     void* workspace, size_t workspace_bytes, void* stream);
+
+/* Lower-level pieces of the above (used by the parity tests). */
+/* k-means++ picks only: picks int32 [B*H, k]. */
+int dp_kmeanspp(const dp_cluster_params* p, const void* src_keys, const int32_t* first_pick,
+                const double* uniforms, const int32_t* alt_picks, int32_t* degenerate_from,
+                int32_t* picks, void* workspace, size_t workspace_bytes, void* stream);
+
+/* nearest_centroid (_kernels_py.py:58-77, _kernels_cy.pyx:115-140): points
+ * [n,d] (dtype), centroids fp64 [k,d]; assign int32 [n], sqdist fp64 [n];
+ * ties -> lowest index. */
+int dp_nearest_centroid(const void* points, int32_t dtype, int32_t n, int32_t d,
+                        const double* centroids, int32_t k, int32_t fp64, int32_t* assign,
+                        double* sqdist, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DOUBLEP_B200_H */

@@ -1,0 +1,44 @@
+"""B200-native Double-P hierarchical top-p sparse decode attention.
+
+Drop-in for the decode path of the reference package ``doublep``
+(arxiv 2602.05191): clustered KV-cache build at prefill, then a per-step
+``sparse_attention(q, cache, p)``.  Compute runs in hand-written sm_100a
+kernels in libdoublep_b200.so (C ABI: include/doublep_b200.h), loaded with
+ctypes; this package is the host-side mirror of the reference interface.
+"""
+
+from .cache import (
+    ClusteredCache,
+    ClusteredLayer,
+    KvCache,
+    build_clustered_cache,
+    cluster_layer,
+    default_cluster_count,
+    head_seed,
+)
+from .engine import (
+    PRESETS,
+    AttentionOutput,
+    ClusterEstimate,
+    DecodeWorkspace,
+    DoublePConfig,
+    SelectionPlan,
+    TopPResult,
+    build_cache_for_config,
+    decode_step,
+    dense_attention,
+    estimate_cluster_distribution,
+    full_attention,
+    plan_selection,
+    sparse_attention,
+)
+
+__version__ = "0.1.0"
+BACKEND = "b200"
+
+__all__ = [
+    "AttentionOutput", "BACKEND", "ClusterEstimate", "ClusteredCache", "ClusteredLayer", "DecodeWorkspace",
+    "DoublePConfig", "KvCache", "PRESETS", "SelectionPlan", "TopPResult", "build_cache_for_config",
+    "build_clustered_cache", "cluster_layer", "decode_step", "default_cluster_count", "dense_attention",
+    "estimate_cluster_distribution", "full_attention", "head_seed", "plan_selection", "sparse_attention",
+]

@@ -1,0 +1,141 @@
+// extern "C" boundary of libdoublep_b200.so (declared in include/doublep_b200.h).
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <string>
+
+#include "common.cuh"
+#include "decode_internal.h"
+
+namespace {
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(DP_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+int check_view(const dp_cache_view* v, int G) {
+  if (!v) return fail(DP_ERR_INVALID, "null cache view");
+  if (v->batch < 1 || v->kv_heads < 1 || v->head_dim < 1)
+    return fail(DP_ERR_INVALID, "cache dimensions must be positive");
+  if (v->dtype != DP_F32 && v->dtype != DP_BF16) return fail(DP_ERR_INVALID, "unknown cache dtype");
+  if (v->head_dim % 8 != 0 || v->head_dim > 256)
+    return fail(DP_ERR_UNSUPPORTED, "head_dim must be a multiple of 8 and <= 256");
+  if (G < 1 || G > dp::kMaxGroup) return fail(DP_ERR_UNSUPPORTED, "gqa_group must be in [1, 8]");
+  if (v->sink < 0 || v->window < 0) return fail(DP_ERR_INVALID, "sink and window must be >= 0");
+  if (v->n_tokens > v->row_cap || v->n_tokens < 1) return fail(DP_ERR_INVALID, "n_tokens outside [1, row_cap]");
+  if (v->sink + v->window > v->n_tokens)
+    return fail(DP_ERR_INVALID, "config/cache mismatch: sink + window exceed the context");
+  if (v->cluster_cap < 1) return fail(DP_ERR_INVALID, "no clusters for this head");
+  return DP_OK;
+}
+int check_p(double p, const char* name) {
+  if (!(p > 0.0 && p <= 1.0)) return fail(DP_ERR_INVALID, std::string(name) + " must be in (0, 1]");
+  return DP_OK;
+}
+int check_q(int qdt) {
+  if (qdt != DP_F32 && qdt != DP_BF16) return fail(DP_ERR_INVALID, "unknown query dtype");
+  return DP_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int dp_version(void) { return 100; }
+
+const char* dp_last_error(void) { return g_err.c_str(); }
+
+int dp_device_info(int32_t* sm_count, int32_t* cc_major, int32_t* cc_minor) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  cudaDeviceProp p;
+  e = cudaGetDeviceProperties(&p, dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceProperties");
+  if (sm_count) *sm_count = p.multiProcessorCount;
+  if (cc_major) *cc_major = p.major;
+  if (cc_minor) *cc_minor = p.minor;
+  return DP_OK;
+}
+
+size_t dp_decode_workspace_bytes(const dp_cache_view* v, int32_t gqa_group) {
+  if (!v) return 0;
+  return dp::decode_ws_layout(v, gqa_group, nullptr, nullptr, nullptr, nullptr);
+}
+
+int dp_score(const dp_cache_view* v, const void* q, int32_t q_dtype, int32_t G, double scale,
+             double* log_mass, void* stream) {
+  int r = check_view(v, G);
+  if (r) return r;
+  if ((r = check_q(q_dtype))) return r;
+  cudaError_t e = dp::launch_score(*v, q, q_dtype, G, scale, log_mass, (cudaStream_t)stream);
+  return e == cudaSuccess ? DP_OK : cuda_fail(e, "dp_score");
+}
+
+int dp_select(const dp_cache_view* v, int32_t G, double p1, double p2, const double* log_mass,
+              uint8_t* state, int32_t* counts, int32_t* order, double* cum_mass, double* probs, void* ws,
+              size_t ws_bytes, void* stream) {
+  int r = check_view(v, G);
+  if (r) return r;
+  if ((r = check_p(p1, "p1")) || (r = check_p(p2, "p2"))) return r;
+  if (v->cluster_cap > 16384)
+    return fail(DP_ERR_UNSUPPORTED, "cluster_cap > 16384 needs the sequence-sharded select path");
+  (void)ws;
+  (void)ws_bytes;
+  cudaError_t e = dp::launch_select(*v, G, p1, p2, log_mass, state, counts, order, cum_mass, probs,
+                                    (cudaStream_t)stream);
+  return e == cudaSuccess ? DP_OK : cuda_fail(e, "dp_select");
+}
+
+int dp_sparse_attention(const dp_cache_view* v, const void* q, int32_t q_dtype, int32_t G, double scale,
+                        const double* log_mass, const uint8_t* state, float* out, float* lse, int32_t* stats,
+                        void* ws, size_t ws_bytes, void* stream) {
+  int r = check_view(v, G);
+  if (r) return r;
+  if ((r = check_q(q_dtype))) return r;
+  if (ws_bytes < dp_decode_workspace_bytes(v, G)) return fail(DP_ERR_INVALID, "workspace too small");
+  cudaError_t e = dp::launch_attention(*v, q, q_dtype, G, scale, log_mass, state, out, lse, stats, ws,
+                                       false, (cudaStream_t)stream);
+  return e == cudaSuccess ? DP_OK : cuda_fail(e, "dp_sparse_attention");
+}
+
+int dp_decode_step(const dp_cache_view* v, const void* q, int32_t q_dtype, int32_t G, double scale, double p1,
+                   double p2, double* log_mass, uint8_t* state, int32_t* counts, float* out, float* lse,
+                   int32_t* stats, void* ws, size_t ws_bytes, void* stream) {
+  int r = dp_score(v, q, q_dtype, G, scale, log_mass, stream);
+  if (r) return r;
+  r = dp_select(v, G, p1, p2, log_mass, state, counts, nullptr, nullptr, nullptr, ws, ws_bytes, stream);
+  if (r) return r;
+  return dp_sparse_attention(v, q, q_dtype, G, scale, log_mass, state, out, lse, stats, ws, ws_bytes, stream);
+}
+
+int dp_dense_attention(const dp_cache_view* v, const void* q, int32_t q_dtype, int32_t G, double scale,
+                       float* out, float* lse, void* ws, size_t ws_bytes, void* stream) {
+  int r = check_view(v, G);
+  if (r) return r;
+  if ((r = check_q(q_dtype))) return r;
+  if (ws_bytes < dp_decode_workspace_bytes(v, G)) return fail(DP_ERR_INVALID, "workspace too small");
+  cudaError_t e = dp::launch_attention(*v, q, q_dtype, G, scale, nullptr, nullptr, out, lse, nullptr, ws,
+                                       true, (cudaStream_t)stream);
+  return e == cudaSuccess ? DP_OK : cuda_fail(e, "dp_dense_attention");
+}
+
+int dp_append_token(const dp_cache_view* v, const void* new_k, const void* new_v, void* stream) {
+  int r = check_view(v, 1);
+  if (r) return r;
+  if (v->n_tokens >= v->row_cap) return fail(DP_ERR_INVALID, "row capacity exhausted");
+  cudaError_t e = dp::launch_append(*v, new_k, new_v, (cudaStream_t)stream);
+  return e == cudaSuccess ? DP_OK : cuda_fail(e, "dp_append_token");
+}
+
+}  // extern "C"
+
+// error helper used by the clustering TU
+namespace dp {
+int set_error(int code, const char* msg) { return fail(code, msg); }
+int set_cuda_error(cudaError_t e, const char* where) { return cuda_fail(e, where); }
+}  // namespace dp

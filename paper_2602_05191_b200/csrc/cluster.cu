@@ -1,0 +1,624 @@
+// Prefill k-means clustering of the keys on sm_100a (build_clustered_cache,
+// /root/reference/pkg/src/doublep/clustering.py:266-314).
+//
+//   kmeanspp   clustering.py:36-55   k-means++ seeding, replaying the host RNG
+//                                    stream (first pick + one uniform per centre,
+//                                    cdf = cumsum(dsq/total)/cdf[-1],
+//                                    searchsorted(side='right')), fp64 dsq
+//   assign     _kernels_py.py:58-77  |x|^2 - 2x.c + |c|^2 argmin, ties -> lowest id
+//   update     clustering.py:86-98   objective, empty-cluster drop with ascending
+//                                    remap (np.unique), convergence test, stable
+//                                    counting sort of members (ascending positions)
+//   means      clustering.py:100-106 fp64 means summed in member order
+//   finalize   clustering.py:298-311 cluster-contiguous rows, fp32 tables
+//
+// All heads (B*H) are processed by every launch; per-head convergence flags
+// let finished heads skip work, so the host loop never synchronises.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "common.cuh"
+#include "doublep_b200.h"
+
+namespace dp {
+
+int set_error(int code, const char* msg);
+int set_cuda_error(cudaError_t e, const char* where);
+
+struct KmWs {
+  double* dsq;    // [BH][M]
+  double* xnorm;  // [BH][M]
+  double* cent;   // [BH][k][d]
+  double* cnorm;  // [BH][k]
+  double* sqd;    // [BH][M]
+  int* assign;    // [BH][M]
+  int* prev;      // [BH][M]
+  int* sorted;    // [BH][M] member point ids, cluster-major, ascending within
+  int* counts;    // [BH][k]
+  int* remap;     // [BH][k]
+  int* start;     // [BH][k+1]
+  int* cursor;    // [BH][k]
+  int* knum;      // [BH]
+  int* done;      // [BH]
+};
+
+static size_t km_layout(const dp_cluster_params* p, KmWs* w, char* base) {
+  const size_t BH = (size_t)p->batch * p->kv_heads;
+  const size_t M = (size_t)p->n_tokens - p->sink - p->window;
+  const size_t k = p->k, d = p->head_dim;
+  size_t off = 0;
+  auto take = [&](size_t bytes) -> char* {
+    const size_t o = off;
+    off += (bytes + 255) & ~size_t(255);
+    return base ? base + o : nullptr;
+  };
+  KmWs t;
+  t.dsq = (double*)take(BH * M * 8);
+  t.xnorm = (double*)take(BH * M * 8);
+  t.cent = (double*)take(BH * k * d * 8);
+  t.cnorm = (double*)take(BH * k * 8);
+  t.sqd = (double*)take(BH * M * 8);
+  t.assign = (int*)take(BH * M * 4);
+  t.prev = (int*)take(BH * M * 4);
+  t.sorted = (int*)take(BH * M * 4);
+  t.counts = (int*)take(BH * k * 4);
+  t.remap = (int*)take(BH * k * 4);
+  t.start = (int*)take(BH * (k + 1) * 4);
+  t.cursor = (int*)take(BH * k * 4);
+  t.knum = (int*)take(BH * 4);
+  t.done = (int*)take(BH * 4);
+  if (w) *w = t;
+  return off;
+}
+
+// -------------------------------------------------------------------------
+// |x|^2 of every middle point (fp64)
+// -------------------------------------------------------------------------
+__global__ void xnorm_kernel(dp_cluster_params p, const void* __restrict__ src, KmWs w) {
+  const int bh = blockIdx.y;
+  const int M = p.n_tokens - p.sink - p.window, d = p.head_dim;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= M) return;
+  const size_t base = ((size_t)bh * p.n_tokens + p.sink + warp) * d;
+  double a = 0.0;
+  for (int j = lane; j < d; j += 32) {
+    const double x = load_elem_d(src, p.dtype, base + j);
+    a = fma(x, x, a);
+  }
+  a = warp_sum(a);
+  if (lane == 0) w.xnorm[(size_t)bh * M + warp] = a;
+}
+
+// -------------------------------------------------------------------------
+// k-means++ seeding: one CTA per head, all k-1 sequential steps in-kernel.
+// -------------------------------------------------------------------------
+constexpr int kPPThreads = 1024;
+
+__global__ void __launch_bounds__(kPPThreads) kmeanspp_kernel(dp_cluster_params p, const void* __restrict__ src,
+                                                            const int* __restrict__ first_pick,
+                                                            const double* __restrict__ uniforms,
+                                                            const int* __restrict__ alt_picks,
+                                                            int* __restrict__ degenerate_from, int* __restrict__ picks,
+                                                            KmWs w) {
+  const int bh = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+  const int M = p.n_tokens - p.sink - p.window, d = p.head_dim, k = p.k;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* c = reinterpret_cast<double*>(smem_raw);  // current centre [d]
+  __shared__ double red[33];
+  __shared__ int s_idx;
+  __shared__ int s_degen;
+  const size_t xbase = ((size_t)bh * p.n_tokens + p.sink) * d;
+  double* dsq = w.dsq + (size_t)bh * M;
+  const int degen_in = degenerate_from ? degenerate_from[bh] : k;
+  if (tid == 0) s_degen = k;
+  const int per = (M + nt - 1) / nt;
+  const int beg = min(M, tid * per), end = min(M, beg + per);
+  for (int i = 0; i < k; ++i) {
+    if (i == 0) {
+      if (tid == 0) s_idx = first_pick[bh];
+    } else {
+      // total = dsq.sum()
+      double loc = 0.0;
+      for (int j = beg; j < end; ++j) loc += dsq[j];
+      const double total = block_sum(loc, red);
+      if (total > 0.0 && i < degen_in) {
+        // cdf over p = dsq/total; idx = first j with cdf_j/cdf_last > u
+        double lp = 0.0;
+        for (int j = beg; j < end; ++j) lp += dsq[j] / total;
+        double last;
+        const double off = block_exclusive_scan(lp, red, &last);
+        const double u = uniforms[(size_t)bh * (k - 1) + (i - 1)];
+        if (tid == 0) s_idx = M;
+        __syncthreads();
+        double run = off;
+        for (int j = beg; j < end; ++j) {
+          run += dsq[j] / total;
+          if (run / last > u) {
+            atomicMin(&s_idx, j);
+            break;
+          }
+        }
+        __syncthreads();
+        if (tid == 0 && s_idx >= M) s_idx = M - 1;
+      } else {
+        if (tid == 0) {
+          if (i >= degen_in && alt_picks) {
+            s_idx = alt_picks[(size_t)bh * (k - 1) + (i - 1)];
+          } else {
+            if (s_degen == k) s_degen = i;
+            s_idx = 0;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    const int idx = s_idx;
+    if (tid == 0) picks[(size_t)bh * k + i] = idx;
+    for (int j = tid; j < d; j += nt) {
+      const double x = load_elem_d(src, p.dtype, xbase + (size_t)idx * d + j);
+      c[j] = x;
+      w.cent[((size_t)bh * k + i) * d + j] = x;
+    }
+    __syncthreads();
+    // dsq = min(dsq, |x - c|^2)
+    for (int j = tid; j < M; j += nt) {
+      double a = 0.0;
+      const size_t xb = xbase + (size_t)j * d;
+      for (int e = 0; e < d; ++e) {
+        const double df = load_elem_d(src, p.dtype, xb + e) - c[e];
+        a = fma(df, df, a);
+      }
+      dsq[j] = (i == 0) ? a : fmin(dsq[j], a);
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    if (degenerate_from) degenerate_from[bh] = s_degen;
+    w.knum[bh] = k;
+    w.done[bh] = 0;
+  }
+}
+
+// -------------------------------------------------------------------------
+// centroid norms (warp per centroid)
+// -------------------------------------------------------------------------
+__global__ void cnorm_kernel(dp_cluster_params p, KmWs w) {
+  const int bh = blockIdx.y;
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (c >= w.knum[bh] || w.done[bh]) return;
+  const double* cr = w.cent + ((size_t)bh * p.k + c) * p.head_dim;
+  double a = 0.0;
+  for (int j = lane; j < p.head_dim; j += 32) a = fma(cr[j], cr[j], a);
+  a = warp_sum(a);
+  if (lane == 0) w.cnorm[(size_t)bh * p.k + c] = a;
+}
+
+// -------------------------------------------------------------------------
+// assignment: 64 points x 64 centroids register-tiled "GEMM + argmin".
+// dist = |x|^2 - 2 x.c + |c|^2 (the NumPy backend's expansion), clamped at 0.
+// -------------------------------------------------------------------------
+constexpr int kAP = 64, kAC = 64, kAK = 32;
+
+template <typename Acc>
+__global__ void __launch_bounds__(256) assign_kernel(dp_cluster_params p, const void* __restrict__ src, KmWs w) {
+  const int bh = blockIdx.y;
+  if (w.done[bh]) return;
+  const int M = p.n_tokens - p.sink - p.window, d = p.head_dim;
+  const int kc = w.knum[bh];
+  const int p0 = blockIdx.x * kAP;
+  if (p0 >= M) return;
+  __shared__ Acc xs[kAK][kAP + 1];
+  __shared__ Acc cs[kAK][kAC + 1];
+  __shared__ Acc cn[kAC];
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const size_t xbase = ((size_t)bh * p.n_tokens + p.sink) * d;
+  const double* cent = w.cent + (size_t)bh * p.k * d;
+  double best[4];
+  int bidx[4];
+  Acc xn[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    best[i] = CUDART_INF;
+    bidx[i] = 0;
+    const int pt = p0 + ty * 4 + i;
+    xn[i] = pt < M ? (Acc)w.xnorm[(size_t)bh * M + pt] : Acc(0);
+  }
+  for (int c0 = 0; c0 < kc; c0 += kAC) {
+    Acc acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = 0;
+    for (int k0 = 0; k0 < d; k0 += kAK) {
+      for (int e = tid; e < kAP * kAK; e += 256) {
+        const int r = e / kAK, kk = e - r * kAK;
+        const int pt = p0 + r;
+        xs[kk][r] = (pt < M && k0 + kk < d) ? (Acc)load_elem_d(src, p.dtype, xbase + (size_t)pt * d + k0 + kk) : Acc(0);
+        const int cc = c0 + r;
+        cs[kk][r] = (cc < kc && k0 + kk < d) ? (Acc)cent[(size_t)cc * d + k0 + kk] : Acc(0);
+      }
+      __syncthreads();
+#pragma unroll 8
+      for (int kk = 0; kk < kAK; ++kk) {
+        Acc a[4], b[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = xs[kk][ty * 4 + i];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) b[j] = cs[kk][tx * 4 + j];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+      }
+      __syncthreads();
+    }
+    for (int e = tid; e < kAC; e += 256) cn[e] = (c0 + e < kc) ? (Acc)w.cnorm[(size_t)bh * p.k + c0 + e] : Acc(0);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int cc = c0 + tx * 4 + j;
+      if (cc < kc) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const double dist = (double)(xn[i] - Acc(2) * acc[i][j] + cn[tx * 4 + j]);
+          if (dist < best[i]) {  // strict: lowest index wins ties
+            best[i] = dist;
+            bidx[i] = cc;
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // reduce across the 16 tx lanes sharing a point row (lowest index on ties)
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    double b = best[i];
+    int bi = bidx[i];
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, b, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob < b || (ob == b && oi < bi)) {
+        b = ob;
+        bi = oi;
+      }
+    }
+    const int pt = p0 + ty * 4 + i;
+    if (tx == 0 && pt < M) {
+      w.assign[(size_t)bh * M + pt] = bi;
+      w.sqd[(size_t)bh * M + pt] = fmax(b, 0.0);
+    }
+  }
+}
+
+// -------------------------------------------------------------------------
+// update: one CTA per head.  objective, counts, drop + ascending remap,
+// convergence test, member offsets and a stable counting sort.
+// -------------------------------------------------------------------------
+constexpr int kUpdThreads = 1024;
+
+__global__ void __launch_bounds__(kUpdThreads) update_kernel(dp_cluster_params p, KmWs w, int it,
+                                                           double* __restrict__ objective,
+                                                           int* __restrict__ iters) {
+  const int bh = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+  if (w.done[bh]) return;
+  const int M = p.n_tokens - p.sink - p.window;
+  const int kc = w.knum[bh];
+  __shared__ double redd[33];
+  __shared__ int redi[33];
+  int* assign = w.assign + (size_t)bh * M;
+  int* prev = w.prev + (size_t)bh * M;
+  int* counts = w.counts + (size_t)bh * p.k;
+  int* remap = w.remap + (size_t)bh * p.k;
+  int* start = w.start + (size_t)bh * (p.k + 1);
+  int* cursor = w.cursor + (size_t)bh * p.k;
+  const double* sqd = w.sqd + (size_t)bh * M;
+
+  double loc = 0.0;
+  for (int i = tid; i < M; i += nt) loc += sqd[i];
+  const double obj = block_sum(loc, redd);
+  if (tid == 0) {
+    objective[(size_t)bh * p.max_iters + it] = obj;
+    iters[bh] = it + 1;
+  }
+  for (int c = tid; c < kc; c += nt) counts[c] = 0;
+  __syncthreads();
+  for (int i = tid; i < M; i += nt) atomicAdd(&counts[assign[i]], 1);
+  __syncthreads();
+  int base = 0, rowbase = 0;
+  for (int c0 = 0; c0 < kc; c0 += nt) {
+    const int c = c0 + tid;
+    const int cnt = c < kc ? counts[c] : 0;
+    const int used = cnt > 0;
+    int tot, totr;
+    const int ex = block_exclusive_scan(used, redi, &tot);
+    const int exr = block_exclusive_scan(cnt, redi, &totr);
+    if (c < kc) {
+      remap[c] = used ? base + ex : -1;
+      if (used) {
+        start[base + ex] = rowbase + exr;
+        cursor[base + ex] = rowbase + exr;
+      }
+    }
+    base += tot;
+    rowbase += totr;
+  }
+  const int knew = base;
+  const bool dropped = knew < kc;
+  __syncthreads();
+  int diff = 0;
+  for (int i = tid; i < M; i += nt) {
+    const int a = remap[assign[i]];
+    assign[i] = a;
+    if (it > 0 && a != prev[i]) diff = 1;
+  }
+  diff = block_sum(diff, redi);
+  if (!dropped && it > 0 && diff == 0) {
+    if (tid == 0) w.done[bh] = 1;  // sorted/start from the previous iteration stay valid
+    return;
+  }
+  for (int i = tid; i < M; i += nt) prev[i] = assign[i];
+  if (tid == 0) {
+    w.knum[bh] = knew;
+    start[knew] = M;
+  }
+  __syncthreads();
+  if (tid < 32) {
+    int* sorted = w.sorted + (size_t)bh * M;
+    const int lane = tid;
+    for (int b0 = 0; b0 < M; b0 += 32) {
+      const int i = b0 + lane;
+      const unsigned act = __ballot_sync(0xffffffffu, i < M);
+      if (i < M) {
+        const int a = assign[i];
+        const unsigned peers = __match_any_sync(act, a);
+        const int leader = __ffs(peers) - 1;
+        const int rank = __popc(peers & ((1u << lane) - 1u));
+        int pos = 0;
+        if (lane == leader) {
+          pos = cursor[a];
+          cursor[a] = pos + __popc(peers);
+        }
+        pos = __shfl_sync(peers, pos, leader);
+        sorted[pos + rank] = i;
+      }
+      __syncwarp();
+    }
+  }
+}
+
+// -------------------------------------------------------------------------
+// means: warp per cluster, fp64 sums in ascending member order (the order of
+// x64[assign == c].mean(axis=0)), then |c|^2 for the next assignment.
+// -------------------------------------------------------------------------
+__global__ void means_kernel(dp_cluster_params p, const void* __restrict__ src, KmWs w) {
+  const int bh = blockIdx.y;
+  if (w.done[bh]) return;
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (c >= w.knum[bh]) return;
+  const int M = p.n_tokens - p.sink - p.window, d = p.head_dim;
+  const int* start = w.start + (size_t)bh * (p.k + 1);
+  const int* sorted = w.sorted + (size_t)bh * M;
+  const size_t xbase = ((size_t)bh * p.n_tokens + p.sink) * d;
+  const int s = start[c], e = start[c + 1];
+  double acc[8];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) acc[t] = 0.0;
+  for (int m = s; m < e; ++m) {
+    const size_t xb = xbase + (size_t)sorted[m] * d;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int j = lane + 32 * t;
+      if (j < d) acc[t] = acc[t] + load_elem_d(src, p.dtype, xb + j);
+    }
+  }
+  const double n = (double)(e - s);
+  double nrm = 0.0;
+  double* cr = w.cent + ((size_t)bh * p.k + c) * d;
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    const int j = lane + 32 * t;
+    if (j < d) {
+      const double mu = acc[t] / n;
+      cr[j] = mu;
+      nrm = fma(mu, mu, nrm);
+    }
+  }
+  nrm = warp_sum(nrm);
+  if (lane == 0) w.cnorm[(size_t)bh * p.k + c] = nrm;
+}
+
+// -------------------------------------------------------------------------
+// finalize: cluster-contiguous rows + tables
+// -------------------------------------------------------------------------
+template <typename T>
+__global__ void permute_rows_kernel(dp_cluster_params p, const T* __restrict__ sk, const T* __restrict__ sv, KmWs w,
+                                    T* __restrict__ dk, T* __restrict__ dv, int row_cap, int* __restrict__ perm) {
+  const int bh = blockIdx.y;
+  const int N = p.n_tokens, M = N - p.sink - p.window, d = p.head_dim;
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (row >= N) return;
+  int srcpos = row;
+  if (row >= p.sink && row < p.sink + M) srcpos = p.sink + w.sorted[(size_t)bh * M + (row - p.sink)];
+  const size_t so = ((size_t)bh * N + srcpos) * d, dof = ((size_t)bh * row_cap + row) * d;
+  for (int j = lane; j < d; j += 32) {
+    dk[dof + j] = sk[so + j];
+    dv[dof + j] = sv[so + j];
+  }
+  if (lane == 0 && perm) perm[(size_t)bh * row_cap + row] = srcpos;
+}
+
+__global__ void tables_kernel(dp_cluster_params p, const void* __restrict__ sv, KmWs w, int* __restrict__ offs,
+                              int* __restrict__ ncl, float* __restrict__ cent_out, float* __restrict__ vbar,
+                              int cluster_cap) {
+  const int bh = blockIdx.y;
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int kn = w.knum[bh];
+  const int M = p.n_tokens - p.sink - p.window, d = p.head_dim;
+  const int* start = w.start + (size_t)bh * (p.k + 1);
+  if (c == 0 && lane == 0) ncl[bh] = kn;
+  if (c > kn) return;
+  if (lane == 0) offs[(size_t)bh * (cluster_cap + 1) + c] = p.sink + start[c];
+  if (c == kn) return;
+  const int* sorted = w.sorted + (size_t)bh * M;
+  const size_t vbase = ((size_t)bh * p.n_tokens + p.sink) * d;
+  const int s = start[c], e = start[c + 1];
+  double acc[8];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) acc[t] = 0.0;
+  for (int m = s; m < e; ++m) {
+    const size_t vb = vbase + (size_t)sorted[m] * d;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int j = lane + 32 * t;
+      if (j < d) acc[t] = acc[t] + load_elem_d(sv, p.dtype, vb + j);
+    }
+  }
+  const double n = (double)(e - s);
+  const double* cr = w.cent + ((size_t)bh * p.k + c) * d;
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    const int j = lane + 32 * t;
+    if (j < d) {
+      const size_t o = ((size_t)bh * cluster_cap + c) * d + j;
+      cent_out[o] = (float)cr[j];
+      vbar[o] = (float)(acc[t] / n);
+    }
+  }
+}
+
+// -------------------------------------------------------------------------
+// nearest_centroid on arbitrary points (kernel-seam parity helper)
+// -------------------------------------------------------------------------
+__global__ void nearest_kernel(const void* __restrict__ pts, int dtype, int n, int d, const double* __restrict__ cents,
+                               int k, int fp64, int* __restrict__ assign, double* __restrict__ sqdist) {
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (i >= n) return;
+  double xn = 0.0;
+  for (int j = lane; j < d; j += 32) {
+    const double x = load_elem_d(pts, dtype, (size_t)i * d + j);
+    xn = fma(x, x, xn);
+  }
+  xn = warp_sum(xn);
+  double best = CUDART_INF;
+  int bi = 0;
+  for (int c = 0; c < k; ++c) {
+    double dot = 0.0, cn = 0.0;
+    for (int j = lane; j < d; j += 32) {
+      const double x = load_elem_d(pts, dtype, (size_t)i * d + j);
+      const double cv = cents[(size_t)c * d + j];
+      if (fp64) dot = fma(x, cv, dot);
+      else dot = (double)fmaf((float)x, (float)cv, (float)dot);
+      cn = fma(cv, cv, cn);
+    }
+    dot = warp_sum(dot);
+    cn = warp_sum(cn);
+    const double dist = xn - 2.0 * dot + cn;
+    if (dist < best) {
+      best = dist;
+      bi = c;
+    }
+  }
+  if (lane == 0) {
+    assign[i] = bi;
+    sqdist[i] = fmax(best, 0.0);
+  }
+}
+
+}  // namespace dp
+
+using namespace dp;
+
+extern "C" {
+
+size_t dp_cluster_workspace_bytes(const dp_cluster_params* p) {
+  if (!p) return 0;
+  return km_layout(p, nullptr, nullptr);
+}
+
+static int check_params(const dp_cluster_params* p) {
+  if (!p) return set_error(DP_ERR_INVALID, "null params");
+  if (p->sink < 0 || p->window < 0) return set_error(DP_ERR_INVALID, "sink and window must be >= 0");
+  const int M = p->n_tokens - p->sink - p->window;
+  if (M < 1) return set_error(DP_ERR_INVALID, "no middle tokens to cluster");
+  if (p->k < 1) return set_error(DP_ERR_INVALID, "cluster count must be >= 1");
+  if (p->k > M) return set_error(DP_ERR_INVALID, "more clusters than points");
+  if (p->max_iters < 1) return set_error(DP_ERR_INVALID, "max_iters must be >= 1");
+  if (p->head_dim < 1 || p->head_dim > 256) return set_error(DP_ERR_UNSUPPORTED, "head_dim must be in [1, 256]");
+  if (p->dtype != DP_F32 && p->dtype != DP_BF16) return set_error(DP_ERR_INVALID, "unknown dtype");
+  return DP_OK;
+}
+
+int dp_kmeanspp(const dp_cluster_params* p, const void* src_keys, const int32_t* first_pick, const double* uniforms,
+                const int32_t* alt_picks, int32_t* degenerate_from, int32_t* picks, void* ws, size_t ws_bytes,
+                void* stream) {
+  int r = check_params(p);
+  if (r) return r;
+  if (ws_bytes < dp_cluster_workspace_bytes(p)) return set_error(DP_ERR_INVALID, "workspace too small");
+  KmWs w;
+  km_layout(p, &w, (char*)ws);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int BH = p->batch * p->kv_heads;
+  kmeanspp_kernel<<<BH, kPPThreads, p->head_dim * 8, st>>>(*p, src_keys, first_pick, uniforms, alt_picks,
+                                                           degenerate_from, picks, w);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? DP_OK : set_cuda_error(e, "dp_kmeanspp");
+}
+
+int dp_cluster_build(const dp_cluster_params* p, const void* src_keys, const void* src_values,
+                     const int32_t* first_pick, const double* uniforms, const int32_t* alt_picks,
+                     int32_t* degenerate_from, void* dst_keys, void* dst_values, int32_t row_cap, int32_t* offs,
+                     int32_t* nclusters, float* centroids, float* value_means, int32_t cluster_cap, int32_t* perm,
+                     double* objective, int32_t* iters, void* ws, size_t ws_bytes, void* stream) {
+  int r = check_params(p);
+  if (r) return r;
+  if (row_cap < p->n_tokens) return set_error(DP_ERR_INVALID, "row_cap < n_tokens");
+  if (cluster_cap < p->k) return set_error(DP_ERR_INVALID, "cluster_cap < k");
+  if (ws_bytes < dp_cluster_workspace_bytes(p)) return set_error(DP_ERR_INVALID, "workspace too small");
+  KmWs w;
+  km_layout(p, &w, (char*)ws);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int BH = p->batch * p->kv_heads;
+  const int M = p->n_tokens - p->sink - p->window;
+  // picks are a by-product of seeding; park them in the `sorted` scratch
+  if (M < p->k) return set_error(DP_ERR_INVALID, "more clusters than points");
+  xnorm_kernel<<<dim3((M * 32 + 255) / 256, BH), 256, 0, st>>>(*p, src_keys, w);
+  kmeanspp_kernel<<<BH, kPPThreads, p->head_dim * 8, st>>>(*p, src_keys, first_pick, uniforms, alt_picks,
+                                                           degenerate_from, w.sorted, w);
+  cnorm_kernel<<<dim3((p->k * 32 + 255) / 256, BH), 256, 0, st>>>(*p, w);
+  for (int it = 0; it < p->max_iters; ++it) {
+    if (p->fp64_assign)
+      assign_kernel<double><<<dim3((M + kAP - 1) / kAP, BH), 256, 0, st>>>(*p, src_keys, w);
+    else
+      assign_kernel<float><<<dim3((M + kAP - 1) / kAP, BH), 256, 0, st>>>(*p, src_keys, w);
+    update_kernel<<<BH, kUpdThreads, 0, st>>>(*p, w, it, objective, iters);
+    means_kernel<<<dim3((p->k * 32 + 255) / 256, BH), 256, 0, st>>>(*p, src_keys, w);
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error(e, "dp_cluster_build (lloyd)");
+  if (p->dtype == DP_F32)
+    permute_rows_kernel<float><<<dim3((p->n_tokens + 7) / 8, BH), 256, 0, st>>>(
+        *p, (const float*)src_keys, (const float*)src_values, w, (float*)dst_keys, (float*)dst_values, row_cap, perm);
+  else
+    permute_rows_kernel<__nv_bfloat16><<<dim3((p->n_tokens + 7) / 8, BH), 256, 0, st>>>(
+        *p, (const __nv_bfloat16*)src_keys, (const __nv_bfloat16*)src_values, w, (__nv_bfloat16*)dst_keys,
+        (__nv_bfloat16*)dst_values, row_cap, perm);
+  tables_kernel<<<dim3(((p->k + 1) * 32 + 255) / 256, BH), 256, 0, st>>>(*p, src_values, w, offs, nclusters,
+                                                                        centroids, value_means, cluster_cap);
+  e = cudaGetLastError();
+  return e == cudaSuccess ? DP_OK : set_cuda_error(e, "dp_cluster_build (tables)");
+}
+
+int dp_nearest_centroid(const void* points, int32_t dtype, int32_t n, int32_t d, const double* centroids, int32_t k,
+                        int32_t fp64, int32_t* assign, double* sqdist, void* stream) {
+  if (n < 1 || d < 1 || k < 1) return set_error(DP_ERR_INVALID, "empty input");
+  nearest_kernel<<<(n * 32 + 255) / 256, 256, 0, (cudaStream_t)stream>>>(points, dtype, n, d, centroids, k, fp64,
+                                                                         assign, sqdist);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? DP_OK : set_cuda_error(e, "dp_nearest_centroid");
+}
+
+}  // extern "C"

@@ -1,0 +1,616 @@
+// Double-P decode step on sm_100a: score -> select -> worklist -> split-KV
+// attention -> LSE merge.  All stages are stream-ordered with no host sync;
+// the data-dependent work lists live in device memory.
+//
+// Reference semantics (file:line into /root/reference/pkg/src/doublep):
+//   score     engine.py:158-177   log_mass = C.q * scale + log|c|
+//   select    engine.py:180-213, selection.py:36-65
+//   attention engine.py:216-252   (exact rows + approx pseudo-rows, one Z)
+//   dense     engine.py:122-144
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <string>
+
+#include "common.cuh"
+#include "decode_internal.h"
+
+namespace dp {
+
+// ---------------------------------------------------------------------------
+// score: one CTA per (tile of 128 clusters, b*h).  Centroid rows are staged
+// through shared memory with coalesced float4 loads; each thread owns one
+// cluster and accumulates the G dot products in fp64 (products of fp32
+// centroids and bf16/fp32 queries are exact in fp64, so the log-masses match
+// the fp64 oracle to ~1e-16 and selection ties are only true ties).
+// ---------------------------------------------------------------------------
+constexpr int kScoreTile = 128;
+
+__global__ void __launch_bounds__(kScoreTile) score_kernel(dp_cache_view v, const void* __restrict__ q,
+                                                         int qdt, int G, double scale,
+                                                         double* __restrict__ lm) {
+  const int bh = blockIdx.y;
+  const int K = v.nclusters[bh];
+  const int k0 = blockIdx.x * kScoreTile;
+  if (k0 >= K) return;
+  const int d = v.head_dim, tid = threadIdx.x;
+  const int stride = d + 4;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* qs = reinterpret_cast<double*>(smem_raw);
+  float* cs = reinterpret_cast<float*>(qs + G * d);
+  for (int i = tid; i < G * d; i += blockDim.x) qs[i] = load_elem_d(q, qdt, (size_t)bh * G * d + i);
+  const int n = min(kScoreTile, K - k0);
+  const int d4 = d >> 2;
+  const float4* C4 = reinterpret_cast<const float4*>(v.centroids + ((size_t)bh * v.cluster_cap + k0) * d);
+  for (int i = tid; i < n * d4; i += blockDim.x) {
+    const int r = i / d4, c = i - r * d4;
+    *reinterpret_cast<float4*>(&cs[r * stride + 4 * c]) = __ldg(&C4[(size_t)r * d4 + c]);
+  }
+  __syncthreads();
+  if (tid >= n) return;
+  double acc[kMaxGroup];
+#pragma unroll
+  for (int g = 0; g < kMaxGroup; ++g) acc[g] = 0.0;
+  const float* row = &cs[tid * stride];
+  for (int j = 0; j < d; j += 4) {
+    const float4 c4 = *reinterpret_cast<const float4*>(&row[j]);
+#pragma unroll
+    for (int g = 0; g < kMaxGroup; ++g) {
+      if (g < G) {
+        const double* qg = &qs[g * d + j];
+        double a = acc[g];
+        a = fma((double)c4.x, qg[0], a);
+        a = fma((double)c4.y, qg[1], a);
+        a = fma((double)c4.z, qg[2], a);
+        a = fma((double)c4.w, qg[3], a);
+        acc[g] = a;
+      }
+    }
+  }
+  const int k = k0 + tid;
+  const int* offs = v.offs + (size_t)bh * (v.cluster_cap + 1);
+  const double ls = log((double)(offs[k + 1] - offs[k]));
+#pragma unroll
+  for (int g = 0; g < kMaxGroup; ++g)
+    if (g < G) lm[((size_t)bh * G + g) * v.cluster_cap + k] = acc[g] * scale + ls;
+}
+
+// ---------------------------------------------------------------------------
+// select: one CTA (1024 threads) per (b, q head).  softmax in fp64, then a
+// shared-memory bitonic sort on (prob desc, cluster id asc) -- the exact
+// order of the reference's stable argsort -- then one fp64 prefix scan that
+// serves both top-p stages (stage 2 is a prefix of the same sorted order,
+// engine.py:189-194).
+// ---------------------------------------------------------------------------
+constexpr int kSelectThreads = 1024;
+
+__device__ __forceinline__ bool sel_before(double a, int ia, double b, int ib) {
+  return a > b || (a == b && ia < ib);
+}
+
+__global__ void __launch_bounds__(kSelectThreads) select_kernel(dp_cache_view v, int G, double p1,
+                                                              double p2, const double* __restrict__ lm,
+                                                              uint8_t* __restrict__ state,
+                                                              int* __restrict__ counts,
+                                                              int* __restrict__ order,
+                                                              double* __restrict__ cum_mass,
+                                                              double* __restrict__ probs, int Kp) {
+  const int bhq = blockIdx.x, bh = bhq / G;
+  const int K = v.nclusters[bh];
+  const int cap = v.cluster_cap;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* key = reinterpret_cast<double*>(smem_raw);
+  int* idx = reinterpret_cast<int*>(key + Kp);
+  __shared__ double red[33];
+  __shared__ int s_n1, s_n2;
+  const double* x = lm + (size_t)bhq * cap;
+
+  double m = -CUDART_INF;
+  for (int i = tid; i < K; i += nt) m = fmax(m, x[i]);
+  m = block_max(m, red, -CUDART_INF);
+  double s = 0.0;
+  for (int i = tid; i < K; i += nt) {
+    const double e = exp(x[i] - m);
+    key[i] = e;
+    s += e;
+  }
+  const double S = block_sum(s, red);
+  double t = 0.0;
+  for (int i = tid; i < Kp; i += nt) {
+    if (i < K) {
+      const double p = key[i] / S;
+      key[i] = p;
+      if (probs) probs[(size_t)bhq * cap + i] = p;
+      idx[i] = i;
+      t += p;
+    } else {
+      key[i] = -1.0;
+      idx[i] = 0x7fffffff;
+    }
+  }
+  const double total = block_sum(t, red);  // probs.sum(), selection.py:52
+  __syncthreads();
+
+  // bitonic sort, "ascending" in the sel_before order
+  for (int kk = 2; kk <= Kp; kk <<= 1) {
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      for (int i = tid; i < Kp; i += nt) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const double a = key[i], b = key[ixj];
+          const int ia = idx[i], ib = idx[ixj];
+          const bool up = (i & kk) == 0;
+          const bool sw = up ? sel_before(b, ib, a, ia) : sel_before(a, ia, b, ib);
+          if (sw) {
+            key[i] = b; key[ixj] = a;
+            idx[i] = ib; idx[ixj] = ia;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+
+  // inclusive prefix sums of the sorted probs (overwrites key)
+  const int per = (K + nt - 1) / nt;
+  const int beg = min(K, tid * per), end = min(K, beg + per);
+  double local = 0.0;
+  for (int i = beg; i < end; ++i) local += key[i];
+  double tot_unused;
+  double c = block_exclusive_scan(local, red, &tot_unused);
+  for (int i = beg; i < end; ++i) {
+    c += key[i];
+    key[i] = c;
+  }
+  if (tid == 0) { s_n1 = K; s_n2 = K; }
+  __syncthreads();
+  // stage 1: first i with cum_i/total >= p1 (searchsorted left + 1, clamped)
+  for (int i = tid; i < K; i += nt)
+    if (key[i] / total >= p1) atomicMin(&s_n1, i + 1);
+  __syncthreads();
+  const int n1 = s_n1;
+  const double sub_total = key[n1 - 1];  // probs[cp].sum(), engine.py:191
+  for (int i = tid; i < n1; i += nt)
+    if (key[i] / sub_total >= p2) atomicMin(&s_n2, i + 1);
+  __syncthreads();
+  const int n2 = min(s_n2, n1);
+  uint8_t* st = state + (size_t)bhq * cap;
+  for (int r = tid; r < K; r += nt) {
+    const int k = idx[r];
+    st[k] = r < n2 ? 2 : (r < n1 ? 1 : 0);
+    if (order) order[(size_t)bhq * cap + r] = k;
+  }
+  if (tid == 0) {
+    counts[2 * bhq] = n1;
+    counts[2 * bhq + 1] = n2;
+    if (cum_mass) cum_mass[bhq] = key[n1 - 1] / total;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// worklist: one CTA per (b, kv head).  Builds the GQA-union row runs
+// (sink, window, then every cluster exact for >= 1 head of the group, in
+// ascending cluster id == ascending row order) with a per-run head mask, and
+// the union of approximated clusters with their head masks.
+// ---------------------------------------------------------------------------
+constexpr int kListThreads = 1024;
+
+__global__ void __launch_bounds__(kListThreads) worklist_kernel(dp_cache_view v, int G,
+                                                              const uint8_t* __restrict__ state,
+                                                              WorkLists wl) {
+  const int bh = blockIdx.x;
+  const int K = v.nclusters[bh];
+  const int cap = v.cluster_cap, tid = threadIdx.x;
+  const int* offs = v.offs + (size_t)bh * (cap + 1);
+  int4* runs = wl.runs + (size_t)bh * (cap + 2);
+  int2* apx = wl.approx + (size_t)bh * cap;
+  __shared__ int red[33];
+  __shared__ int s_runs, s_rows, s_apx;
+  const int full = (1 << G) - 1;
+  if (tid == 0) {
+    int r = 0, rows = 0;
+    if (v.sink > 0) { runs[r++] = make_int4(0, v.sink, full, rows); rows += v.sink; }
+    if (v.window > 0) {
+      runs[r++] = make_int4(v.n_tokens - v.window, v.window, full, rows);
+      rows += v.window;
+    }
+    s_runs = r; s_rows = rows; s_apx = 0;
+  }
+  __syncthreads();
+  for (int base = 0; base < K; base += blockDim.x) {
+    const int k = base + tid;
+    int me = 0, ma = 0, len = 0;
+    if (k < K) {
+      for (int g = 0; g < G; ++g) {
+        const uint8_t s = state[((size_t)bh * G + g) * cap + k];
+        me |= (s == 2) << g;
+        ma |= (s == 1) << g;
+      }
+      if (me) len = offs[k + 1] - offs[k];
+    }
+    int tot_e, tot_a, tot_l;
+    const int pe = block_exclusive_scan<int>(me != 0, red, &tot_e);
+    const int pa = block_exclusive_scan<int>(ma != 0, red, &tot_a);
+    const int pl = block_exclusive_scan<int>(len, red, &tot_l);
+    const int rb = s_runs, rowb = s_rows, ab = s_apx;
+    if (me) runs[rb + pe] = make_int4(offs[k], len, me, rowb + pl);
+    if (ma) apx[ab + pa] = make_int2(k, ma);
+    __syncthreads();
+    if (tid == 0) { s_runs = rb + tot_e; s_rows = rowb + tot_l; s_apx = ab + tot_a; }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    wl.nruns[bh] = s_runs;
+    wl.nrows[bh] = s_rows;
+    wl.napprox[bh] = s_apx;
+    wl.nchunks[bh] = (s_rows + kChunkRows - 1) / kChunkRows;
+    if (wl.stats) {
+      wl.stats[4 * bh + 0] = s_rows;
+      wl.stats[4 * bh + 1] = s_apx;
+      wl.stats[4 * bh + 2] = (s_rows + kChunkRows - 1) / kChunkRows;
+      wl.stats[4 * bh + 3] = 0;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// attention (generic CUDA-core path): one CTA per (row chunk, b*h).  The
+// chunk's rows are gathered from the run list (cluster runs are contiguous
+// in HBM, so the 16-byte cp.async copies coalesce), logits for all G heads
+// are computed once per row and masked per head, and the chunk emits an
+// unnormalised partial (m, l, o) per head.  T = storage type, Acc = fp64 for
+// fp32 caches (1e-5 parity bar), fp32 for bf16.
+// ---------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+
+template <typename T, typename Acc, bool kDense>
+__global__ void __launch_bounds__(kAttnThreads) attn_chunk_kernel(dp_cache_view v, const void* __restrict__ q,
+                                                                 int qdt, int G, double scale, WorkLists wl,
+                                                                 Partials<Acc> pt) {
+  const int bh = blockIdx.y, c = blockIdx.x;
+  const int rows_total = kDense ? v.n_tokens : wl.nrows[bh];
+  const int nchunk = (rows_total + kChunkRows - 1) / kChunkRows;
+  if (c >= nchunk) return;
+  const int d = v.head_dim, tid = threadIdx.x, nt = blockDim.x;
+  const int v0 = c * kChunkRows;
+  const int nr = min(kChunkRows, rows_total - v0);
+  const int rowb = d * (int)sizeof(T) + 16;  // padded row stride (bytes)
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Acc* qs = reinterpret_cast<Acc*>(smem_raw);
+  Acc* sc = qs + G * d;                                   // [G][R]
+  unsigned char* ks = reinterpret_cast<unsigned char*>(sc + G * kChunkRows);
+  unsigned char* vs = ks + kChunkRows * rowb;
+  int* rphys = reinterpret_cast<int*>(vs + kChunkRows * rowb);
+  int* rmask = rphys + kChunkRows;
+
+  for (int i = tid; i < G * d; i += nt) qs[i] = (Acc)load_elem_d(q, qdt, (size_t)bh * G * d + i);
+  const int full = (1 << G) - 1;
+  for (int r = tid; r < kChunkRows; r += nt) {
+    int phys = -1, mask = 0;
+    if (r < nr) {
+      const int vr = v0 + r;
+      if (kDense) {
+        phys = vr; mask = full;
+      } else {
+        const int4* runs = wl.runs + (size_t)bh * (v.cluster_cap + 2);
+        int lo = 0, hi = wl.nruns[bh] - 1;  // last run with prefix <= vr
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (runs[mid].w <= vr) lo = mid; else hi = mid - 1;
+        }
+        const int4 ru = runs[lo];
+        phys = ru.x + (vr - ru.w);
+        mask = ru.z;
+      }
+    }
+    rphys[r] = phys;
+    rmask[r] = mask;
+  }
+  __syncthreads();
+  const size_t head_off = (size_t)bh * v.row_cap * d;
+  const T* Kg = reinterpret_cast<const T*>(v.keys) + head_off;
+  const T* Vg = reinterpret_cast<const T*>(v.values) + head_off;
+  const int ch = d * (int)sizeof(T) / 16;
+  for (int i = tid; i < kChunkRows * ch; i += nt) {
+    const int r = i / ch, cc = i - r * ch;
+    const int phys = rphys[r];
+    unsigned char* kd = ks + r * rowb + cc * 16;
+    unsigned char* vd = vs + r * rowb + cc * 16;
+    if (phys >= 0) {
+      cp_async16<T>(kd, reinterpret_cast<const unsigned char*>(Kg + (size_t)phys * d) + cc * 16);
+      cp_async16<T>(vd, reinterpret_cast<const unsigned char*>(Vg + (size_t)phys * d) + cc * 16);
+    } else {
+      *reinterpret_cast<int4*>(kd) = make_int4(0, 0, 0, 0);
+      *reinterpret_cast<int4*>(vd) = make_int4(0, 0, 0, 0);
+    }
+  }
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+  __syncthreads();
+
+  // logits: thread per (head, row); lanes share the head -> q broadcast
+  const Acc sc_scale = (Acc)scale;
+  for (int i = tid; i < G * kChunkRows; i += nt) {
+    const int g = i / kChunkRows, r = i - g * kChunkRows;
+    Acc s = -INFINITY;
+    if ((rmask[r] >> g) & 1) {
+      const T* kr = reinterpret_cast<const T*>(ks + r * rowb);
+      const Acc* qg = qs + g * d;
+      Acc a = 0;
+      for (int j = 0; j < d; ++j) {
+        if constexpr (sizeof(T) == 4) a = fma((Acc)kr[j], qg[j], a);
+        else a = fma((Acc)bf2f(kr[j]), qg[j], a);
+      }
+      s = a * sc_scale;
+    }
+    sc[g * kChunkRows + r] = s;
+  }
+  __syncthreads();
+  const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+  for (int g = warp; g < G; g += nw) {
+    Acc m = -INFINITY;
+    for (int r = lane; r < kChunkRows; r += 32) m = max(m, sc[g * kChunkRows + r]);
+    m = warp_max(m);
+    Acc l = 0;
+    for (int r = lane; r < kChunkRows; r += 32) {
+      const Acc s = sc[g * kChunkRows + r];
+      const Acc p = (m == -INFINITY || s == -INFINITY) ? Acc(0) : exp(s - m);
+      sc[g * kChunkRows + r] = p;
+      l += p;
+    }
+    l = warp_sum(l);
+    if (lane == 0) {
+      const size_t pi = ((size_t)bh * pt.max_chunks + c) * G + g;
+      pt.m[pi] = m;
+      pt.l[pi] = l;
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < G * d; i += nt) {
+    const int g = i / d, j = i - g * d;
+    const Acc* pg = sc + g * kChunkRows;
+    Acc o = 0;
+    for (int r = 0; r < nr; ++r) {
+      const T* vr = reinterpret_cast<const T*>(vs + r * rowb);
+      Acc val;
+      if constexpr (sizeof(T) == 4) val = (Acc)vr[j];
+      else val = (Acc)bf2f(vr[j]);
+      o = fma(pg[r], val, o);
+    }
+    pt.o[(((size_t)bh * pt.max_chunks + c) * G + g) * d + j] = o;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// merge: one CTA per (b, kv head).  Combines the chunk partials of every q
+// head of the group with the approx pseudo-rows (logit = log_mass, value =
+// value mean, engine.py:231-246) under one normaliser.
+// ---------------------------------------------------------------------------
+template <typename Acc, bool kDense>
+__global__ void merge_kernel(dp_cache_view v, int G, const double* __restrict__ lm, WorkLists wl,
+                             Partials<Acc> pt, float* __restrict__ out, float* __restrict__ lse) {
+  const int bh = blockIdx.x;
+  const int d = v.head_dim, tid = threadIdx.x, cap = v.cluster_cap;
+  const int rows_total = kDense ? v.n_tokens : wl.nrows[bh];
+  const int nch = (rows_total + kChunkRows - 1) / kChunkRows;
+  const int na = kDense ? 0 : wl.napprox[bh];
+  const int2* apx = wl.approx + (size_t)bh * cap;
+  const float* vbar = v.value_means + (size_t)bh * cap * d;
+  for (int g = 0; g < G; ++g) {
+    const int hq = bh * G + g;
+    const double* lmh = lm ? lm + (size_t)hq * cap : nullptr;
+    const size_t pbase = (size_t)bh * pt.max_chunks * G;
+    double M = -CUDART_INF;
+    for (int c = 0; c < nch; ++c) M = fmax(M, (double)pt.m[pbase + (size_t)c * G + g]);
+    for (int a = 0; a < na; ++a) {
+      const int2 e = apx[a];
+      if ((e.y >> g) & 1) M = fmax(M, lmh[e.x]);
+    }
+    double L = 0.0;
+    for (int c = 0; c < nch; ++c) {
+      const double mc = pt.m[pbase + (size_t)c * G + g];
+      if (mc != -CUDART_INF) L += (double)pt.l[pbase + (size_t)c * G + g] * exp(mc - M);
+    }
+    for (int a = 0; a < na; ++a) {
+      const int2 e = apx[a];
+      if ((e.y >> g) & 1) L += exp(lmh[e.x] - M);
+    }
+    for (int j = tid; j < d; j += blockDim.x) {
+      double o = 0.0;
+      for (int c = 0; c < nch; ++c) {
+        const double mc = pt.m[pbase + (size_t)c * G + g];
+        if (mc != -CUDART_INF) o += exp(mc - M) * (double)pt.o[(pbase + (size_t)c * G + g) * d + j];
+      }
+      for (int a = 0; a < na; ++a) {
+        const int2 e = apx[a];
+        if ((e.y >> g) & 1) o += exp(lmh[e.x] - M) * (double)vbar[(size_t)e.x * d + j];
+      }
+      out[(size_t)hq * d + j] = (float)(o / L);
+    }
+    if (tid == 0) lse[hq] = (float)(M + log(L));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host-side launchers
+// ---------------------------------------------------------------------------
+size_t attn_smem_bytes(int d, int G, int elem, int acc) {
+  const int rowb = d * elem + 16;
+  return (size_t)acc * (G * d + G * kChunkRows) + 2 * (size_t)kChunkRows * rowb + 2 * kChunkRows * 4;
+}
+
+int select_padded(int K) {
+  int kp = 1;
+  while (kp < K) kp <<= 1;
+  return kp;
+}
+
+size_t decode_ws_layout(const dp_cache_view* v, int G, WorkLists* wl, void** parts, size_t* part_bytes,
+                        char* base) {
+  const size_t BH = (size_t)v->batch * v->kv_heads;
+  const int cap = v->cluster_cap;
+  const int max_chunks = (v->row_cap + kChunkRows - 1) / kChunkRows;
+  const size_t acc = v->dtype == DP_F32 ? 8 : 4;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off += (bytes + 255) & ~size_t(255);
+    return base ? base + o : nullptr;
+  };
+  char* runs = take(BH * (cap + 2) * sizeof(int4));
+  char* apx = take(BH * cap * sizeof(int2));
+  char* cnt = take(BH * 4 * sizeof(int));
+  const size_t pbytes = BH * max_chunks * G * (2 + (size_t)v->head_dim) * acc;
+  char* p = take(pbytes);
+  if (wl) {
+    wl->runs = reinterpret_cast<int4*>(runs);
+    wl->approx = reinterpret_cast<int2*>(apx);
+    int* c = reinterpret_cast<int*>(cnt);
+    wl->nruns = c;
+    wl->nrows = c + BH;
+    wl->napprox = c + 2 * BH;
+    wl->nchunks = c + 3 * BH;
+    wl->stats = nullptr;
+    wl->max_chunks = max_chunks;
+  }
+  if (parts) *parts = p;
+  if (part_bytes) *part_bytes = pbytes;
+  return off;
+}
+
+template <typename Acc>
+Partials<Acc> carve_partials(void* p, size_t BH, int max_chunks, int G, int d) {
+  Partials<Acc> pt;
+  pt.max_chunks = max_chunks;
+  pt.m = reinterpret_cast<Acc*>(p);
+  pt.l = pt.m + BH * max_chunks * G;
+  pt.o = pt.l + BH * max_chunks * G;
+  return pt;
+}
+
+cudaError_t launch_score(const dp_cache_view& v, const void* q, int qdt, int G, double scale, double* lm,
+                         cudaStream_t st) {
+  const size_t smem = (size_t)G * v.head_dim * 8 + (size_t)kScoreTile * (v.head_dim + 4) * 4;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr_set = true;
+  }
+  dim3 grid((v.cluster_cap + kScoreTile - 1) / kScoreTile, v.batch * v.kv_heads);
+  score_kernel<<<grid, kScoreTile, smem, st>>>(v, q, qdt, G, scale, lm);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_select(const dp_cache_view& v, int G, double p1, double p2, const double* lm,
+                          uint8_t* state, int* counts, int* order, double* cum, double* probs,
+                          cudaStream_t st) {
+  const int Kp = select_padded(std::max(1, v.cluster_cap));
+  const size_t smem = (size_t)Kp * 12;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr_set = true;
+  }
+  select_kernel<<<v.batch * v.kv_heads * G, kSelectThreads, smem, st>>>(v, G, p1, p2, lm, state, counts,
+                                                                       order, cum, probs, Kp);
+  return cudaGetLastError();
+}
+
+template <typename T, typename Acc, bool kDense>
+cudaError_t launch_attn_t(const dp_cache_view& v, const void* q, int qdt, int G, double scale,
+                          const double* lm, WorkLists wl, void* parts, float* out, float* lse,
+                          cudaStream_t st) {
+  const size_t BH = (size_t)v.batch * v.kv_heads;
+  Partials<Acc> pt = carve_partials<Acc>(parts, BH, wl.max_chunks, G, v.head_dim);
+  const size_t smem = attn_smem_bytes(v.head_dim, G, sizeof(T), sizeof(Acc));
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(attn_chunk_kernel<T, Acc, kDense>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
+    attr_set = true;
+  }
+  const int rows = kDense ? v.n_tokens : v.row_cap;
+  dim3 grid((rows + kChunkRows - 1) / kChunkRows, (unsigned)BH);
+  attn_chunk_kernel<T, Acc, kDense><<<grid, kAttnThreads, smem, st>>>(v, q, qdt, G, scale, wl, pt);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  merge_kernel<Acc, kDense><<<(unsigned)BH, 128, 0, st>>>(v, G, lm, wl, pt, out, lse);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_attention(const dp_cache_view& v, const void* q, int qdt, int G, double scale,
+                             const double* lm, const uint8_t* state, float* out, float* lse, int* stats,
+                             void* ws, bool dense, cudaStream_t st) {
+  WorkLists wl;
+  void* parts = nullptr;
+  decode_ws_layout(&v, G, &wl, &parts, nullptr, reinterpret_cast<char*>(ws));
+  if (!dense) {
+    wl.stats = stats;
+    worklist_kernel<<<v.batch * v.kv_heads, kListThreads, 0, st>>>(v, G, state, wl);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  if (v.dtype == DP_F32) {
+    return dense ? launch_attn_t<float, double, true>(v, q, qdt, G, scale, lm, wl, parts, out, lse, st)
+                 : launch_attn_t<float, double, false>(v, q, qdt, G, scale, lm, wl, parts, out, lse, st);
+  }
+  return dense ? launch_attn_t<__nv_bfloat16, float, true>(v, q, qdt, G, scale, lm, wl, parts, out, lse, st)
+               : launch_attn_t<__nv_bfloat16, float, false>(v, q, qdt, G, scale, lm, wl, parts, out, lse, st);
+}
+
+// ---------------------------------------------------------------------------
+// decode-time growth (clustering.py:178-229): the new token lands at row
+// n_tokens; the row that leaves the window (n_tokens - window) becomes a
+// residual singleton cluster appended to the tables.  With the
+// [sink | clusters | window] row layout this is an O(d) in-place update.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void append_kernel(dp_cache_view v, const T* __restrict__ nk, const T* __restrict__ nv) {
+  const int bh = blockIdx.x, d = v.head_dim, tid = threadIdx.x;
+  const int n = v.n_tokens, leave = n - v.window;
+  T* K = const_cast<T*>(reinterpret_cast<const T*>(v.keys)) + (size_t)bh * v.row_cap * d;
+  T* V = const_cast<T*>(reinterpret_cast<const T*>(v.values)) + (size_t)bh * v.row_cap * d;
+  for (int j = tid; j < d; j += blockDim.x) {
+    K[(size_t)n * d + j] = nk[(size_t)bh * d + j];
+    V[(size_t)n * d + j] = nv[(size_t)bh * d + j];
+  }
+  int* ncl = const_cast<int*>(v.nclusters);
+  const int kc = ncl[bh];
+  __syncthreads();
+  if (kc >= v.cluster_cap || leave < v.sink) return;
+  float* C = const_cast<float*>(v.centroids) + ((size_t)bh * v.cluster_cap + kc) * d;
+  float* Vb = const_cast<float*>(v.value_means) + ((size_t)bh * v.cluster_cap + kc) * d;
+  for (int j = tid; j < d; j += blockDim.x) {
+    if constexpr (sizeof(T) == 4) {
+      C[j] = K[(size_t)leave * d + j];
+      Vb[j] = V[(size_t)leave * d + j];
+    } else {
+      C[j] = bf2f(K[(size_t)leave * d + j]);
+      Vb[j] = bf2f(V[(size_t)leave * d + j]);
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int* offs = const_cast<int*>(v.offs) + (size_t)bh * (v.cluster_cap + 1);
+    offs[kc] = leave;
+    offs[kc + 1] = leave + 1;
+    ncl[bh] = kc + 1;
+  }
+}
+
+cudaError_t launch_append(const dp_cache_view& v, const void* nk, const void* nv, cudaStream_t st) {
+  const int BH = v.batch * v.kv_heads;
+  if (v.dtype == DP_F32)
+    append_kernel<float><<<BH, 128, 0, st>>>(v, (const float*)nk, (const float*)nv);
+  else
+    append_kernel<__nv_bfloat16><<<BH, 128, 0, st>>>(v, (const __nv_bfloat16*)nk, (const __nv_bfloat16*)nv);
+  return cudaGetLastError();
+}
+
+}  // namespace dp

@@ -1,0 +1,48 @@
+// Internal declarations shared by the decode translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "doublep_b200.h"
+
+namespace dp {
+
+constexpr int kChunkRows = 128;   // rows per split-KV work item
+constexpr int kAttnThreads = 256;
+
+// Device work lists (one set per (b, kv head)), carved from the workspace.
+struct WorkLists {
+  int4* runs;     // [BH][cap+2] {row start, len, head mask, virtual row prefix}
+  int2* approx;   // [BH][cap]   {cluster id, head mask}
+  int* nruns;     // [BH]
+  int* nrows;     // [BH]  union exact rows (incl. sink/window)
+  int* napprox;   // [BH]  union approx clusters
+  int* nchunks;   // [BH]
+  int* stats;     // nullable [BH][4]
+  int max_chunks;
+};
+
+template <typename Acc>
+struct Partials {
+  Acc* m;  // [BH][max_chunks][G]
+  Acc* l;
+  Acc* o;  // [BH][max_chunks][G][d]
+  int max_chunks;
+};
+
+size_t decode_ws_layout(const dp_cache_view* v, int G, WorkLists* wl, void** parts, size_t* part_bytes,
+                        char* base);
+int select_padded(int K);
+
+cudaError_t launch_score(const dp_cache_view& v, const void* q, int qdt, int G, double scale, double* lm,
+                         cudaStream_t st);
+cudaError_t launch_select(const dp_cache_view& v, int G, double p1, double p2, const double* lm,
+                          uint8_t* state, int* counts, int* order, double* cum, double* probs,
+                          cudaStream_t st);
+cudaError_t launch_attention(const dp_cache_view& v, const void* q, int qdt, int G, double scale,
+                             const double* lm, const uint8_t* state, float* out, float* lse, int* stats,
+                             void* ws, bool dense, cudaStream_t st);
+cudaError_t launch_append(const dp_cache_view& v, const void* nk, const void* nv, cudaStream_t st);
+
+}  // namespace dp

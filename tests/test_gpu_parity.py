@@ -1,0 +1,281 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on
+the same seeded inputs.  Tolerances (BASELINE.json
+north_star): selection bit-exact except score ties within 1e-6; outputs
+rel-L2 <= 1e-5 (fp32 cache) / 2e-3 (bf16 cache)."""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import doublep_oracle as O
+from parity import compare_plan, oracle_tables
+
+pytestmark = pytest.mark.gpu
+
+TOL = {torch.float32: 1e-5, torch.bfloat16: 2e-3}
+
+
+def _workload(n, d, H, G, profile, seed, steps=1):
+    spec = O.WorkloadSpec(context_len=n, head_dim=d, num_kv_heads=H, gqa_group=G, num_steps=steps,
+                          tail_profile=profile, seed=seed)
+    return spec, *O.generate(spec)
+
+
+def _to_dev(a, dtype):
+    return torch.from_numpy(np.ascontiguousarray(a)).to("cuda").to(dtype)
+
+
+def _layer(keys, values, dtype, **kw):
+    from paper_2602_05191_b200 import cluster_layer
+
+    k = _to_dev(keys[0], dtype).unsqueeze(0)  # [1,H,N,d]
+    v = _to_dev(values[0], dtype).unsqueeze(0)
+    return cluster_layer(k, v, **kw), k, v
+
+
+def _check_decode(layer, kdev, vdev, queries, G, p1, p2, dtype, counts=None):
+    """Batched product path vs the oracle fed the GPU's tables."""
+    from paper_2602_05191_b200 import sparse_attention
+
+    H = layer.kv_heads
+    q = _to_dev(queries, dtype).unsqueeze(0)  # [1,Hq,d]
+    out, ws = sparse_attention(q, layer, p1, p2, return_plan=True)
+    out = out[0].double().cpu().numpy()
+    lse = ws.lse[0].double().cpu().numpy()
+    lm_g = ws.log_mass[0].cpu().numpy()
+    cnt = ws.counts[0].cpu().numpy()
+    # full descending order from a debug select over the same log-masses
+    from paper_2602_05191_b200 import _native as N
+
+    order = torch.zeros_like(ws.state, dtype=torch.int32)
+    st2 = torch.zeros_like(ws.state)
+    c2 = torch.zeros_like(ws.counts)
+    N.check(N.lib().dp_select(layer.view(), G, p1, p2, N.ptr(ws.log_mass), N.ptr(st2), N.ptr(c2),
+                              N.ptr(order), None, None, None, 0, torch.cuda.current_stream().cuda_stream))
+    order = order[0].cpu().numpy()
+    assert torch.equal(st2, ws.state)
+    classes = {}
+    kf = kdev[0].double().cpu().numpy()  # exact upcast of what the GPU read
+    vf = vdev[0].double().cpu().numpy()
+    for hq in range(H * G):
+        h = hq // G
+        t = oracle_tables(layer, 0, h)
+        qv = q[0, hq].double().cpu().numpy()
+        o_out, o_plan, o_est = O.decode_step(qv, kf[h], vf[h], t, p1, p2, layer.sink, layer.window)
+        K = len(t.members)
+        np.testing.assert_allclose(lm_g[hq, :K], o_est.log_masses, rtol=0, atol=1e-9)
+        c1, c2_ = compare_plan(o_est, o_plan, order[hq], int(cnt[hq, 0]), int(cnt[hq, 1]), p1, p2)
+        classes[c1] = classes.get(c1, 0) + 1
+        classes[c2_] = classes.get(c2_, 0) + 1
+        assert c1 != "real" and c2_ != "real", (hq, c1, c2_)
+        if c1 == "exact" and c2_ == "exact":
+            err = O.output_error(out[hq], o_out.output)
+            assert err <= TOL[dtype], (hq, err)
+            assert abs(lse[hq] - o_out.log_normalizer) <= 1e-4 * max(1.0, abs(o_out.log_normalizer))
+    if counts is not None:
+        counts.update(classes)
+    return classes
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("profile,n,d,H,G,seed", [
+    ("peaked", 2048, 128, 2, 4, 0),
+    ("mixed", 1536, 64, 2, 4, 1),
+    ("heavy", 1024, 128, 1, 8, 2),
+    ("uniform", 700, 32, 1, 2, 3),
+])
+def test_decode_parity(dtype, profile, n, d, H, G, seed):
+    spec, keys, values, queries = _workload(n, d, H, G, profile, seed, steps=2)
+    layer, kd, vd = _layer(keys, values, dtype)
+    for p1, p2 in [(0.95, 0.7), (0.99, 0.8), (0.9, 0.7), (1.0, 1.0), (0.5, 0.95)]:
+        for s in range(2):
+            _check_decode(layer, layer_rows(kd), layer_rows(vd), queries[s, 0], G, p1, p2, dtype)
+
+
+def layer_rows(t):
+    return t  # position-ordered source rows [1,H,N,d]
+
+
+def test_dense_parity():
+    from paper_2602_05191_b200 import dense_attention
+
+    for dtype in (torch.float32, torch.bfloat16):
+        spec, keys, values, queries = _workload(3000, 128, 2, 4, "peaked", 5)
+        layer, kd, vd = _layer(keys, values, dtype)
+        q = _to_dev(queries[0, 0], dtype).unsqueeze(0)
+        out, lse = dense_attention(q, layer, return_lse=True)
+        kf = kd[0].double().cpu().numpy()
+        vf = vd[0].double().cpu().numpy()
+        for hq in range(8):
+            ref = O.full_attention(q[0, hq].double().cpu().numpy(), kf[hq // 4], vf[hq // 4])
+            assert O.output_error(out[0, hq].double().cpu().numpy(), ref.output) <= TOL[dtype]
+            assert abs(float(lse[0, hq]) - ref.log_normalizer) <= 1e-4 * abs(ref.log_normalizer) + 1e-5
+
+
+def test_kmeanspp_picks_exact():
+    """dp_kmeanspp replays the reference's k-means++ picks bit-exactly."""
+    from paper_2602_05191_b200 import _native as N
+    from paper_2602_05191_b200.cache import head_seed, rng_stream
+
+    spec, keys, values, _ = _workload(4096, 64, 2, 1, "peaked", 7)
+    n, sink, window = 4096, 4, 64
+    M = n - sink - window
+    k = O.default_cluster_count(M)
+    for dtype in (torch.float32, torch.bfloat16):
+        kd = _to_dev(keys[0], dtype).unsqueeze(0)
+        p = N.ClusterParams()
+        p.batch, p.kv_heads, p.head_dim, p.dtype = 1, 2, 64, 0 if dtype == torch.float32 else 1
+        p.n_tokens, p.sink, p.window, p.k, p.max_iters, p.fp64_assign = n, sink, window, k, 25, 1
+        firsts, us = [], []
+        for h in range(2):
+            f, u, _ = rng_stream(head_seed(0, 0, h), M, k)
+            firsts.append(f)
+            us.append(u)
+        f_d = torch.tensor(firsts, dtype=torch.int32, device="cuda")
+        u_d = torch.from_numpy(np.stack(us)).cuda()
+        picks = torch.zeros((2, k), dtype=torch.int32, device="cuda")
+        ws = torch.empty((N.lib().dp_cluster_workspace_bytes(p),), dtype=torch.uint8, device="cuda")
+        N.check(N.lib().dp_kmeanspp(p, N.ptr(kd), N.ptr(f_d), N.ptr(u_d), None, None, N.ptr(picks),
+                                    N.ptr(ws), ws.numel(), torch.cuda.current_stream().cuda_stream))
+        kf = kd[0].double().cpu().numpy()
+        for h in range(2):
+            mid = kf[h, sink:n - window]
+            _, want = O.plusplus_init(mid, k, np.random.default_rng(head_seed(0, 0, h)))
+            np.testing.assert_array_equal(picks[h].cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("fp64", [True, False])
+def test_cluster_build_parity(fp64):
+    """Clustering parity: same init, assignment
+    agreement >= 1 - 1e-3, objective within 1e-5 (exact in fp64 mode)."""
+    spec, keys, values, _ = _workload(3072, 64, 2, 1, "mixed", 9)
+    n, sink, window = 3072, 4, 64
+    layer, kd, vd = _layer(keys, values, torch.float32, fp64_assign=fp64)
+    k = O.default_cluster_count(n - sink - window)
+    for h in range(2):
+        t_o, fit = O.build_head_tables(keys[0, h], values[0, h], k, sink, window,
+                                       seed_for_head=O.head_seed(0, 0, h))
+        t_g = layer.head_tables(0, h)
+        lab_o = np.full(n, -1)
+        lab_g = np.full(n, -1)
+        for c, m in enumerate(t_o.members):
+            lab_o[m] = c
+        for c, m in enumerate(t_g["members"]):
+            lab_g[m] = c
+        agree = np.mean(lab_o[sink:n - window] == lab_g[sink:n - window])
+        obj_g = layer.objective[h, : int(layer.iters[h])].cpu().numpy()
+        if fp64:
+            assert agree == 1.0
+            np.testing.assert_allclose(obj_g, fit.objective, rtol=1e-10)
+            np.testing.assert_allclose(t_g["centroids"], t_o.centroids, rtol=0, atol=1e-6)
+            np.testing.assert_allclose(t_g["value_means"], t_o.value_means, rtol=0, atol=1e-6)
+        else:
+            assert agree >= 1 - 1e-3
+            assert abs(obj_g[-1] - fit.objective[-1]) <= 1e-5 * fit.objective[-1]
+        # partition + contiguity invariants (SPEC.md: partition property)
+        allm = np.sort(np.concatenate(t_g["members"]))
+        np.testing.assert_array_equal(allm, np.arange(sink, n - window))
+        rows = layer.keys[0, h].float().cpu().numpy()
+        perm = layer.perm[0, h].cpu().numpy()
+        np.testing.assert_array_equal(rows[: n], keys[0, h][perm[:n]])
+
+
+def test_golden_end_to_end():
+    """GPU clustering + decode against the real reference's golden outputs."""
+    import os
+
+    from conftest import GOLDEN
+    from paper_2602_05191_b200 import sparse_attention
+
+    g = np.load(os.path.join(GOLDEN, "peaked_2048_d64.npz"))
+    spec, keys, values, queries = _workload(2048, 64, 1, 4, "peaked", 7, steps=2)
+    layer, kd, vd = _layer(keys, values, torch.float32)
+    np.testing.assert_array_equal(layer.head_tables(0, 0)["sizes"], g["L0H0_sizes"])
+    for ti, (p1, p2) in enumerate([(0.95, 0.7), (0.99, 0.8), (0.9, 0.7), (1.0, 1.0), (0.5, 0.95)]):
+        for s in range(2):
+            q = _to_dev(queries[s, 0], torch.float32).unsqueeze(0)
+            out, ws = sparse_attention(q, layer, p1, p2, return_plan=True)
+            for hq in range(4):
+                pre = f"T{ti}S{s}L0Q{hq}_"
+                assert int(ws.counts[0, hq, 0]) == g[pre + "stage1"].size
+                assert int(ws.counts[0, hq, 1]) == int(g[pre + "n_exact"])
+                err = O.output_error(out[0, hq].double().cpu().numpy(), g[pre + "output"])
+                assert err <= 1e-5, err
+
+
+def test_reference_semantics_on_gpu():
+    """Reference unit-test semantics through the reference-signature API."""
+    import paper_2602_05191_b200 as dp
+
+    rng = np.random.default_rng(0)
+    # exactness collapse with singleton clusters (test_engine.py:128-136)
+    keys = rng.normal(size=(1, 1, 40, 8)).astype(np.float32)
+    vals = rng.normal(size=(1, 1, 40, 8)).astype(np.float32)
+    cache = dp.KvCache(keys, vals)
+    cc = dp.build_clustered_cache(cache, k=40, sink=0, window=0)
+    cfg = dp.DoublePConfig(p1=1.0, p2=1.0, sink=0, window=0)
+    q = rng.normal(size=8).astype(np.float32)
+    out, plan, est = dp.decode_step(q, cache, cc, cfg, 0, 0)
+    ref = O.full_attention(q.astype(np.float64), keys[0, 0].astype(np.float64), vals[0, 0].astype(np.float64))
+    assert O.output_error(out.output, ref.output) <= 1e-5
+    assert out.normalizer == pytest.approx(ref.normalizer, rel=1e-5)
+    # two-token cluster mass 2e vs 1+e^2 (test_engine.py:113-125) -- d=8 padded
+    k2 = np.zeros((1, 1, 2, 8), np.float32)
+    k2[0, 0, 1, 0] = 2.0 * math.sqrt(8)
+    cache2 = dp.KvCache(k2, np.ones((1, 1, 2, 8), np.float32))
+    cc2 = dp.build_clustered_cache(cache2, k=1, sink=0, window=0)
+    q2 = np.zeros(8, np.float32)
+    q2[0] = 1.0
+    est2 = dp.estimate_cluster_distribution(q2, cc2, 0, 0)
+    assert math.exp(est2.log_masses[0]) == pytest.approx(2 * math.e, rel=1e-9)
+    # mixture weights sum to one (test_engine.py:151-159)
+    keys3 = rng.normal(size=(1, 1, 128, 8)).astype(np.float32)
+    cache3 = dp.KvCache(keys3, np.ones((1, 1, 128, 8), np.float32))
+    cc3 = dp.build_clustered_cache(cache3, k=9, sink=2, window=16)
+    cfg3 = dp.DoublePConfig(p1=0.9, p2=0.6, sink=2, window=16)
+    out3, plan3, _ = dp.decode_step(rng.normal(size=8).astype(np.float32) * 2, cache3, cc3, cfg3, 0, 0)
+    np.testing.assert_allclose(out3.output, np.ones(8), atol=1e-6)
+    assert out3.approx_cluster_count == plan3.approx_clusters.size
+    # p1 = p2 = 1 keeps everything (test_engine.py:115-123)
+    plan4 = dp.plan_selection(dp.estimate_cluster_distribution(q, cc3 if False else cc, 0, 0), cfg)
+    assert plan4.approx_clusters.size == 0 and plan4.exact_tokens.size == 40
+    # error messages
+    with pytest.raises(ValueError, match="config/cache mismatch"):
+        dp.decode_step(q, cache, cc, dp.DoublePConfig(0.9, 0.7, sink=4, window=0), 0, 0)
+    other = dp.KvCache(keys, vals)
+    with pytest.raises(ValueError, match="mismatch"):
+        dp.sparse_attention(q, other, cc, plan, 0, 0)
+    with pytest.raises(ValueError, match="dimension mismatch"):
+        dp.full_attention(np.ones(5, np.float32), cache, 0, 0)
+
+
+def test_growth_parity():
+    """append_tokens on the device vs the oracle's residual singleton pool."""
+    import paper_2602_05191_b200 as dp
+
+    spec, keys, values, queries = _workload(300, 16, 1, 1, "peaked", 2)
+    cache = dp.KvCache(keys, values)
+    cc = dp.build_clustered_cache(cache, sink=4, window=64, growth=8)
+    rng = np.random.default_rng(99)
+    app_k = rng.normal(size=(5, 1, 1, 16)).astype(np.float32)
+    app_v = rng.normal(size=(5, 1, 1, 16)).astype(np.float32)
+    for t in range(5):
+        cc.append_tokens(app_k[t], app_v[t])
+    assert cc.total_tokens == 305
+    base = oracle_tables(cc.layers[0], 0, 0)
+    # the first layer's tables already include the residuals; rebuild the base
+    kprefill = int(cc.layers[0]._prefill_k)
+    base = O.HeadTables(members=base.members[:kprefill], centroids=base.centroids[:kprefill],
+                        value_means=base.value_means[:kprefill])
+    kf = np.concatenate([keys[0, 0], app_k[:, 0, 0]]).astype(np.float64)
+    vf = np.concatenate([values[0, 0], app_v[:, 0, 0]]).astype(np.float64)
+    t = O.grow_tables(base, kf, vf, 300, 305, 64)
+    q = queries[0, 0, 0]
+    for p1, p2 in [(1.0, 1.0), (0.9, 0.7)]:
+        out, plan, _ = dp.decode_step(q, cache, cc, dp.DoublePConfig(p1, p2), 0, 0)
+        o_out, o_plan, _ = O.decode_step(q.astype(np.float64), kf, vf, t, p1, p2, 4, 64)
+        np.testing.assert_array_equal(plan.stage1.selected, o_plan.stage1.selected)
+        np.testing.assert_array_equal(plan.exact_tokens, o_plan.exact_tokens)
+        assert O.output_error(out.output, o_out.output) <= 1e-5
