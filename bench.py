@@ -1,0 +1,501 @@
+#!/usr/bin/env python
+"""Double-P decode-step benchmark (driver contract).
+
+Workload (BASELINE.json configs[1]): Llama-3.1-8B-shaped decode, 32 layers,
+batch 1, 32K context, 8 KV heads x 4 q heads (GQA 4), head_dim 128, bf16
+cache, (p1, p2) = (0.95, 0.7), synthetic blob KV caches with the reference's
+generator law ("peaked" queries).  One step = one decode step of every layer
+(score -> select -> worklist -> gathered split-KV attention + LSE merge),
+layers run back to back from HBM (each layer's cache is 134 MB > L2, so no
+flush is needed between steps).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Multi-GPU (torchrun): KV heads are sharded across ranks (strong scaling),
+no collective on the data path; time = max over ranks.
+"""
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--layers", type=int, default=32)
+    ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--context", type=int, default=32768)
+    ap.add_argument("--kv-heads", type=int, default=8)
+    ap.add_argument("--gqa", type=int, default=4)
+    ap.add_argument("--head-dim", type=int, default=128)
+    ap.add_argument("--p1", type=float, default=0.95)
+    ap.add_argument("--p2", type=float, default=0.7)
+    ap.add_argument("--profile", default="peaked")
+    ap.add_argument("--qsteps", type=int, default=8, help="distinct query steps cycled through")
+    ap.add_argument("--fp64-assign", type=int, default=0, help="prefill k-means distances in fp64")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--cpu-sample-heads", type=int, default=2)
+    return ap.parse_args()
+
+
+def model_name(a):
+    return "llama-3.1-8b-shape" if a.kv_heads * a.gqa == 32 else ("llama-3.1-70b-shape" if a.gqa == 8 else "custom")
+
+
+def workload_config(a, world):
+    return {
+        "workload": f"doublep-decode {model_name(a)} L{a.layers} B{a.batch} N{a.context} "
+                    f"Hq{a.kv_heads * a.gqa}/Hkv{a.kv_heads} d{a.head_dim} bf16 p=({a.p1},{a.p2}) {a.profile}",
+        "layers": a.layers, "batch": a.batch, "context": a.context, "kv_heads": a.kv_heads,
+        "q_heads": a.kv_heads * a.gqa, "head_dim": a.head_dim, "p1": a.p1, "p2": a.p2,
+        "tail_profile": a.profile, "sink": 4, "window": 64, "tokens_per_cluster": 32,
+        "parallelism": f"kv-head shard x{world}" if world > 1 else "single GPU",
+        "l2": "inputs larger than L2 (each layer's KV > 126 MB; layers cycled)",
+    }
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region (NVML)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {
+        0x0000000000000001: "gpu_idle", 0x0000000000000002: "applications_clocks_setting",
+        0x0000000000000004: "sw_power_cap", 0x0000000000000008: "hw_slowdown",
+        0x0000000000000020: "sw_thermal_slowdown", 0x0000000000000040: "hw_thermal_slowdown",
+        0x0000000000000080: "hw_power_brake_slowdown", 0x0000000000000100: "display_clock_setting",
+    }
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.ok = [], set(), False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max = None
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        return {"sm_mhz": float(statistics.median(self.samples)) if self.samples else None,
+                "sm_max_mhz": self.max, "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing
+# ---------------------------------------------------------------------------
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl" if _cuda() else "gloo")
+    return world, rank, local
+
+
+def _cuda():
+    import torch
+
+    return torch.cuda.is_available()
+
+
+def max_over_ranks(x, world, device):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (the oracle port of doublep.decode_step) -- baseline only
+# ---------------------------------------------------------------------------
+def oracle_head_from_layer(layer, h):
+    """Position-ordered keys/values + tables of one head of a GPU-built layer."""
+    from oracle import doublep_oracle as O
+
+    n = layer.n_tokens
+    rows_k = layer.keys[0, h, :n].float().cpu().numpy()
+    rows_v = layer.values[0, h, :n].float().cpu().numpy()
+    perm = layer.perm[0, h, :n].cpu().numpy()
+    kp = np.empty_like(rows_k)
+    vp = np.empty_like(rows_v)
+    kp[perm] = rows_k
+    vp[perm] = rows_v
+    t = layer.head_tables(0, h)
+    return kp, vp, O.HeadTables(members=t["members"], centroids=t["centroids"], value_means=t["value_means"])
+
+
+def cpu_decode_sample(heads, queries_for_head, a, steps):
+    """Time oracle.decode_step per (q head, step); returns per-call seconds."""
+    from oracle import doublep_oracle as O
+
+    times = []
+    for (kp, vp, tab), qs in zip(heads, queries_for_head):
+        for s in range(steps):
+            for g in range(qs.shape[1]):
+                q = qs[s % qs.shape[0], g].astype(np.float64)
+                t0 = time.perf_counter()
+                O.decode_step(q, kp, vp, tab, a.p1, a.p2, 4, 64)
+                times.append(time.perf_counter() - t0)
+    return times
+
+
+def run_reference(a):
+    """--impl reference: the reference algorithm (oracle port of doublep
+    0.1.0's NumPy path) on the host cores, same metric/config, bounded
+    sample: one KV head of one layer (host-generated with the reference law,
+    clustered with the reference k-means), G q heads per step, extrapolated
+    to all heads and layers."""
+    world, rank, _ = dist_setup()
+    if rank != 0:
+        return
+    from oracle import doublep_oracle as O
+
+    n, d, G = a.context, a.head_dim, a.gqa
+    spec = O.WorkloadSpec(context_len=n, head_dim=d, num_kv_heads=1, gqa_group=G, num_steps=max(a.qsteps, 1),
+                          tail_profile=a.profile, seed=0)
+    t0 = time.perf_counter()
+    keys, values, centers = O.generate_head(spec, 0, 0)
+    qs = np.stack([O.generate_queries(spec, 0, g, centers) for g in range(G)], axis=1)  # [S, G, d]
+    k = O.clamp_k(n, 4, 64)
+    tables, _ = O.build_head_tables(keys, values, k, 4, 64, seed_for_head=O.head_seed(0, 0, 0))
+    prefill = time.perf_counter() - t0
+    scale_up = a.kv_heads * a.layers * a.batch  # (q-head group steps) per full decode step
+    per_step = []
+    for s in range(a.warmup + a.steps):
+        t0 = time.perf_counter()
+        for g in range(G):
+            O.decode_step(qs[s % qs.shape[0], g].astype(np.float64), keys, values, tables, a.p1, a.p2, 4, 64)
+        dt = time.perf_counter() - t0
+        if s >= a.warmup:
+            per_step.append(dt * scale_up * 1e6)
+    val = float(statistics.median(per_step))
+    line = {
+        "impl": "reference", "metric": "decode_us_per_step", "value": val, "unit": "us/step",
+        "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": val / 1e3,
+        "higher_is_better": False, "scaling": "strong" if a.gpus > 1 else "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (reference generator law, host)", "config": workload_config(a, 1),
+        "cpu_baseline": {"value": val, "unit": "us/step", "cores": os.cpu_count(), "kind": "port",
+                         "sample": f"1 layer x 1 kv head x {G} q heads per step at N={n}, extrapolated "
+                                   f"x{scale_up} (kv heads x layers x batch); oracle port of doublep "
+                                   f"0.1.0 NumPy path; prefill clustering {prefill:.1f}s not timed"},
+        "e2e": {"value": val, "unit": "us/step", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# the B200 arm
+# ---------------------------------------------------------------------------
+def run_b200(a):
+    import torch
+
+    world, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    from paper_2602_05191_b200 import _native as N
+    from paper_2602_05191_b200 import cluster_layer, DecodeWorkspace, sparse_attention
+    from paper_2602_05191_b200.cache import dtype_code
+    from paper_2602_05191_b200.workload import generate_layer, generate_queries
+
+    if a.kv_heads % world:
+        raise SystemExit(f"kv heads {a.kv_heads} not divisible by {world} ranks")
+    hl = a.kv_heads // world
+    h0 = rank * hl
+    G, d, L, B = a.gqa, a.head_dim, a.layers, a.batch
+    lib = N.lib()
+    st = torch.cuda.current_stream(dev)
+
+    # ---- prefill: synthetic caches + GPU k-means (not timed) -------------
+    t0 = time.perf_counter()
+    layers, qdev = [], []
+    for li in range(L):
+        k, v, centers = generate_layer(B, a.kv_heads, a.context, d, layer=li, device=dev)
+        k, v, centers = k[:, h0:h0 + hl].contiguous(), v[:, h0:h0 + hl].contiguous(), centers[:, h0:h0 + hl]
+        lay = cluster_layer(k, v, layer=li, fp64_assign=bool(a.fp64_assign))
+        del k, v
+        q = generate_queries(centers, G, a.qsteps, profile=a.profile, layer=li)
+        layers.append(lay)
+        qdev.append(torch.from_numpy(q).to(dev).to(torch.bfloat16))  # [S,B,Hq,d]
+    torch.cuda.synchronize(dev)
+    prefill_s = time.perf_counter() - t0
+
+    wss = [DecodeWorkspace(lay, G) for lay in layers]
+    views = [lay.view() for lay in layers]
+    scale = 1.0 / math.sqrt(d)
+
+    def layer_step(li, s, stats=None, ev=None):
+        lay, ws, v = layers[li], wss[li], views[li]
+        q = qdev[li][s % a.qsteps]
+        cs = torch.cuda.current_stream(dev).cuda_stream
+        if ev is not None:
+            ev[0].record()
+        N.check(lib.dp_score(v, N.ptr(q), dtype_code(q), G, scale, N.ptr(ws.log_mass), cs))
+        if ev is not None:
+            ev[1].record()
+        N.check(lib.dp_select(v, G, a.p1, a.p2, N.ptr(ws.log_mass), N.ptr(ws.state), N.ptr(ws.counts), None,
+                              None, None, N.ptr(ws.ws), ws.ws.numel(), cs))
+        if ev is not None:
+            ev[2].record()
+        N.check(lib.dp_build_worklist(v, G, N.ptr(ws.state), N.ptr(ws.stats if stats is None else stats),
+                                      N.ptr(ws.ws), ws.ws.numel(), cs))
+        if ev is not None:
+            ev[3].record()
+        N.check(lib.dp_attend(v, N.ptr(q), dtype_code(q), G, scale, N.ptr(ws.log_mass), N.ptr(ws.out),
+                              N.ptr(ws.lse), N.ptr(ws.ws), ws.ws.numel(), cs))
+        if ev is not None:
+            ev[4].record()
+
+    def dense_step(li, s):
+        lay, ws, v = layers[li], wss[li], views[li]
+        q = qdev[li][s % a.qsteps]
+        N.check(lib.dp_dense_attention(v, N.ptr(q), dtype_code(q), G, scale, N.ptr(ws.out), N.ptr(ws.lse),
+                                       N.ptr(ws.ws), ws.ws.numel(), torch.cuda.current_stream(dev).cuda_stream))
+
+    # ---- stage timing + algorithmic bytes (eager, CUDA events) -----------
+    nstage = min(a.qsteps, 4)
+    stats_all = torch.zeros((nstage, L, B, hl, 4), dtype=torch.int32, device=dev)
+    evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(L)] for _ in range(nstage)]
+    for s in range(nstage):  # warm
+        for li in range(L):
+            layer_step(li, s, stats_all[s, li])
+    torch.cuda.synchronize(dev)
+    for s in range(nstage):
+        for li in range(L):
+            layer_step(li, s, stats_all[s, li], evs[s][li])
+    torch.cuda.synchronize(dev)
+    stage_ms = np.zeros(4)
+    for s in range(nstage):
+        for li in range(L):
+            e = evs[s][li]
+            for j in range(4):
+                stage_ms[j] += e[j].elapsed_time(e[j + 1])
+    stage_ms /= nstage * L  # per layer
+    stats_np = stats_all.cpu().numpy().astype(np.int64)  # [S,L,B,hl,4]
+    ncl = np.stack([lay.nclusters.cpu().numpy() for lay in layers]).astype(np.int64)  # [L,B,hl]
+    s_kv, s_q, s_o = 2, 2, 4
+    Hq_l = hl * G
+    qo = B * Hq_l * d * (s_q + s_o)
+    U = stats_np[..., 0]
+    A = stats_np[..., 1]
+    attend_bytes = (U * 2 * d * s_kv + A * d * 4).sum(axis=(2, 3)).mean(axis=0) + qo  # per layer [L]
+    score_bytes = (ncl * d * 4 + ncl * 4).sum(axis=(1, 2))  # [L]
+    step_bytes = float((attend_bytes + score_bytes).sum())  # all layers, one step
+    dense_bytes = float(L * (B * hl * a.context * 2 * d * s_kv + qo))
+    attend_ms = stage_ms[3]
+    attend_gbs = float(attend_bytes.mean() / (attend_ms * 1e-3) / 1e9)
+    union_frac = float(U.mean() / a.context)
+
+    # ---- CUDA graphs of the full step (one per distinct query step) -------
+    def capture(fn):
+        graphs = []
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):
+            for s in range(a.qsteps):
+                for li in range(L):
+                    fn(li, s)
+        torch.cuda.current_stream(dev).wait_stream(side)
+        torch.cuda.synchronize(dev)
+        for s in range(a.qsteps):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                for li in range(L):
+                    fn(li, s)
+            graphs.append(g)
+        return graphs
+
+    graphs = capture(layer_step)
+
+    def timed(graph_list, steps, warmup, sampler=None):
+        for s in range(warmup):
+            graph_list[s % len(graph_list)].replay()
+        torch.cuda.synchronize(dev)
+        barrier(world)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ctx = sampler if sampler is not None else _Null()
+        with ctx:
+            e0.record()
+            for s in range(steps):
+                graph_list[s % len(graph_list)].replay()
+            e1.record()
+            torch.cuda.synchronize(dev)
+        barrier(world)
+        return e0.elapsed_time(e1) / steps
+
+    sampler = ClockSampler(local)
+    ms = timed(graphs, a.steps, a.warmup, sampler)
+    ms = max_over_ranks(ms, world, dev)
+    clocks = sampler.summary()
+
+    dense_ms = None
+    if not a.no_dense:
+        dgraphs = capture(dense_step)
+        dense_ms = max_over_ranks(timed(dgraphs, a.steps, a.warmup), world, dev)
+        del dgraphs
+
+    # ---- e2e through the public API with host buffers ---------------------
+    e2e = None
+    if not a.no_e2e:
+        qh = [torch.empty((a.qsteps, B, Hq_l, d), dtype=torch.bfloat16).pin_memory() for _ in range(L)]
+        for li in range(L):
+            qh[li].copy_(qdev[li].cpu())
+        oh = torch.empty((L, B, Hq_l, d), dtype=torch.float32).pin_memory()
+        qd = [torch.empty((B, Hq_l, d), dtype=torch.bfloat16, device=dev) for _ in range(L)]
+
+        def e2e_step(s):
+            for li in range(L):
+                qd[li].copy_(qh[li][s % a.qsteps], non_blocking=True)
+            for li in range(L):
+                out = sparse_attention(qd[li], layers[li], a.p1, a.p2, workspace=wss[li])
+                oh[li].copy_(out, non_blocking=True)
+            torch.cuda.current_stream(dev).synchronize()
+
+        for s in range(a.warmup):
+            e2e_step(s)
+        barrier(world)
+        t0 = time.perf_counter()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for s in range(a.steps):
+            e2e_step(s)
+        e1.record()
+        torch.cuda.synchronize(dev)
+        wall = (time.perf_counter() - t0) / a.steps * 1e3
+        e2e_ms = max_over_ranks(max(e0.elapsed_time(e1) / a.steps, wall), world, dev)
+        e2e = {"value": e2e_ms * 1e3, "unit": "us/step", "h2d_bytes_per_step": int(L * B * Hq_l * d * 2),
+               "d2h_bytes_per_step": int(L * B * Hq_l * d * 4),
+               "path": "paper_2602_05191_b200.sparse_attention per layer, eager, pinned host q in / out back"}
+
+    # ---- CPU baseline (rank 0, N=1 only) ---------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        nh = min(a.cpu_sample_heads, hl)
+        heads = [oracle_head_from_layer(layers[0], h) for h in range(nh)]
+        qsets = [qdev[0][:, 0, h * G:(h + 1) * G].float().cpu().numpy() for h in range(nh)]
+        times = cpu_decode_sample(heads, qsets, a, steps=2)
+        per_call = statistics.median(times)
+        cpu_us = per_call * a.kv_heads * G * L * B * 1e6
+        cpu = {"value": cpu_us, "unit": "us/step", "cores": os.cpu_count(), "kind": "port",
+               "sample": f"layer 0, {nh} kv heads x {G} q heads x 2 steps of the same cache (GPU-built "
+                         f"clusters), oracle decode_step median {per_call * 1e3:.2f} ms per q-head-step, "
+                         f"extrapolated x{a.kv_heads * G * L * B} (all q heads, layers, batch); NumPy/"
+                         f"OpenBLAS threads = cores"}
+
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except Exception:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    launches = a.steps * L * 5
+    if rank == 0:
+        line = {
+            "metric": "decode_us_per_step", "value": ms * 1e3, "unit": "us/step", "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": False,
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (reference blob law on device, Philox); random-init caches, no checkpoint",
+            "config": workload_config(a, world),
+            "roofline": {"bound": "hbm", "achieved": attend_gbs, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": attend_gbs / hbm_peak, "traffic": None,
+                         "kernel": "dp_attend (attn_chunk_kernel + merge_kernel), per-layer launch",
+                         "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": float(attend_bytes.mean())},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "stage_us_per_layer": {"score": stage_ms[0] * 1e3, "select": stage_ms[1] * 1e3,
+                                   "worklist": stage_ms[2] * 1e3, "attend": stage_ms[3] * 1e3},
+            "step_algorithmic_bytes": step_bytes,
+            "step_roofline_frac": step_bytes / (ms * 1e-3) / 1e9 / hbm_peak,
+            "union_exact_rows_frac": union_frac,
+            "dense_us_per_step": None if dense_ms is None else dense_ms * 1e3,
+            "dense_roofline_frac": None if dense_ms is None else dense_bytes / (dense_ms * 1e-3) / 1e9 / hbm_peak,
+            "speedup_vs_dense": None if dense_ms is None else dense_ms / ms,
+            "prefill_s": prefill_s,
+        }
+        print(json.dumps(line), flush=True)
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_b200(a)
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        import torch.distributed as dist
+
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

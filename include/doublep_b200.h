@@ -116,6 +116,16 @@ int dp_sparse_attention(const dp_cache_view* v, const void* q, int32_t q_dtype,
                         const uint8_t* state, float* out, float* lse, int32_t* stats,
                         void* workspace, size_t workspace_bytes, void* stream);
 
+/* The two halves of dp_sparse_attention, for callers that time or overlap
+ * them separately: dp_build_worklist turns the per-head states into the
+ * GQA-union row runs / approx lists (in the workspace); dp_attend runs the
+ * gathered split-KV attention + LSE merge over them. */
+int dp_build_worklist(const dp_cache_view* v, int32_t gqa_group, const uint8_t* state,
+                      int32_t* stats, void* workspace, size_t workspace_bytes, void* stream);
+int dp_attend(const dp_cache_view* v, const void* q, int32_t q_dtype, int32_t gqa_group,
+              double scale, const double* log_mass, float* out, float* lse, void* workspace,
+              size_t workspace_bytes, void* stream);
+
 /* score + select + sparse attention in one call (decode_step,
  * engine.py:267-278).  log_mass/state/counts are caller buffers so the plan
  * stays inspectable. */

@@ -91,16 +91,31 @@ int dp_select(const dp_cache_view* v, int32_t G, double p1, double p2, const dou
   return e == cudaSuccess ? DP_OK : cuda_fail(e, "dp_select");
 }
 
-int dp_sparse_attention(const dp_cache_view* v, const void* q, int32_t q_dtype, int32_t G, double scale,
-                        const double* log_mass, const uint8_t* state, float* out, float* lse, int32_t* stats,
-                        void* ws, size_t ws_bytes, void* stream) {
+int dp_build_worklist(const dp_cache_view* v, int32_t G, const uint8_t* state, int32_t* stats, void* ws,
+                      size_t ws_bytes, void* stream) {
+  int r = check_view(v, G);
+  if (r) return r;
+  if (ws_bytes < dp_decode_workspace_bytes(v, G)) return fail(DP_ERR_INVALID, "workspace too small");
+  cudaError_t e = dp::launch_worklist(*v, G, state, stats, ws, (cudaStream_t)stream);
+  return e == cudaSuccess ? DP_OK : cuda_fail(e, "dp_build_worklist");
+}
+
+int dp_attend(const dp_cache_view* v, const void* q, int32_t q_dtype, int32_t G, double scale,
+              const double* log_mass, float* out, float* lse, void* ws, size_t ws_bytes, void* stream) {
   int r = check_view(v, G);
   if (r) return r;
   if ((r = check_q(q_dtype))) return r;
   if (ws_bytes < dp_decode_workspace_bytes(v, G)) return fail(DP_ERR_INVALID, "workspace too small");
-  cudaError_t e = dp::launch_attention(*v, q, q_dtype, G, scale, log_mass, state, out, lse, stats, ws,
-                                       false, (cudaStream_t)stream);
-  return e == cudaSuccess ? DP_OK : cuda_fail(e, "dp_sparse_attention");
+  cudaError_t e = dp::launch_attend(*v, q, q_dtype, G, scale, log_mass, out, lse, ws, false, (cudaStream_t)stream);
+  return e == cudaSuccess ? DP_OK : cuda_fail(e, "dp_attend");
+}
+
+int dp_sparse_attention(const dp_cache_view* v, const void* q, int32_t q_dtype, int32_t G, double scale,
+                        const double* log_mass, const uint8_t* state, float* out, float* lse, int32_t* stats,
+                        void* ws, size_t ws_bytes, void* stream) {
+  int r = dp_build_worklist(v, G, state, stats, ws, ws_bytes, stream);
+  if (r) return r;
+  return dp_attend(v, q, q_dtype, G, scale, log_mass, out, lse, ws, ws_bytes, stream);
 }
 
 int dp_decode_step(const dp_cache_view* v, const void* q, int32_t q_dtype, int32_t G, double scale, double p1,
@@ -119,8 +134,7 @@ int dp_dense_attention(const dp_cache_view* v, const void* q, int32_t q_dtype, i
   if (r) return r;
   if ((r = check_q(q_dtype))) return r;
   if (ws_bytes < dp_decode_workspace_bytes(v, G)) return fail(DP_ERR_INVALID, "workspace too small");
-  cudaError_t e = dp::launch_attention(*v, q, q_dtype, G, scale, nullptr, nullptr, out, lse, nullptr, ws,
-                                       true, (cudaStream_t)stream);
+  cudaError_t e = dp::launch_attend(*v, q, q_dtype, G, scale, nullptr, out, lse, ws, true, (cudaStream_t)stream);
   return e == cudaSuccess ? DP_OK : cuda_fail(e, "dp_dense_attention");
 }
 

@@ -544,18 +544,20 @@ cudaError_t launch_attn_t(const dp_cache_view& v, const void* q, int qdt, int G,
   return cudaGetLastError();
 }
 
-cudaError_t launch_attention(const dp_cache_view& v, const void* q, int qdt, int G, double scale,
-                             const double* lm, const uint8_t* state, float* out, float* lse, int* stats,
-                             void* ws, bool dense, cudaStream_t st) {
+cudaError_t launch_worklist(const dp_cache_view& v, int G, const uint8_t* state, int* stats, void* ws,
+                            cudaStream_t st) {
+  WorkLists wl;
+  decode_ws_layout(&v, G, &wl, nullptr, nullptr, reinterpret_cast<char*>(ws));
+  wl.stats = stats;
+  worklist_kernel<<<v.batch * v.kv_heads, kListThreads, 0, st>>>(v, G, state, wl);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_attend(const dp_cache_view& v, const void* q, int qdt, int G, double scale, const double* lm,
+                          float* out, float* lse, void* ws, bool dense, cudaStream_t st) {
   WorkLists wl;
   void* parts = nullptr;
   decode_ws_layout(&v, G, &wl, &parts, nullptr, reinterpret_cast<char*>(ws));
-  if (!dense) {
-    wl.stats = stats;
-    worklist_kernel<<<v.batch * v.kv_heads, kListThreads, 0, st>>>(v, G, state, wl);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-  }
   if (v.dtype == DP_F32) {
     return dense ? launch_attn_t<float, double, true>(v, q, qdt, G, scale, lm, wl, parts, out, lse, st)
                  : launch_attn_t<float, double, false>(v, q, qdt, G, scale, lm, wl, parts, out, lse, st);

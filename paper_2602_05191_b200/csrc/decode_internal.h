@@ -40,9 +40,10 @@ cudaError_t launch_score(const dp_cache_view& v, const void* q, int qdt, int G, 
 cudaError_t launch_select(const dp_cache_view& v, int G, double p1, double p2, const double* lm,
                           uint8_t* state, int* counts, int* order, double* cum, double* probs,
                           cudaStream_t st);
-cudaError_t launch_attention(const dp_cache_view& v, const void* q, int qdt, int G, double scale,
-                             const double* lm, const uint8_t* state, float* out, float* lse, int* stats,
-                             void* ws, bool dense, cudaStream_t st);
+cudaError_t launch_worklist(const dp_cache_view& v, int G, const uint8_t* state, int* stats, void* ws,
+                            cudaStream_t st);
+cudaError_t launch_attend(const dp_cache_view& v, const void* q, int qdt, int G, double scale, const double* lm,
+                          float* out, float* lse, void* ws, bool dense, cudaStream_t st);
 cudaError_t launch_append(const dp_cache_view& v, const void* nk, const void* nv, cudaStream_t st);
 
 }  // namespace dp
