@@ -316,6 +316,9 @@ def run_b200(a):
         for li in range(L):
             layer_step(li, s, stats_all[s, li])
     torch.cuda.synchronize(dev)
+    # park the GPU on a sleep kernel so every launch below is queued before
+    # it runs: the events then bracket device time, not host launch gaps
+    torch.cuda._sleep(int(2e8))
     for s in range(nstage):
         for li in range(L):
             layer_step(li, s, stats_all[s, li], evs[s][li])

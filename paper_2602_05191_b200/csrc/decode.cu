@@ -537,8 +537,18 @@ cudaError_t launch_attn_t(const dp_cache_view& v, const void* q, int qdt, int G,
   }
   const int rows = kDense ? v.n_tokens : v.row_cap;
   dim3 grid((rows + kChunkRows - 1) / kChunkRows, (unsigned)BH);
-  attn_chunk_kernel<T, Acc, kDense><<<grid, kAttnThreads, smem, st>>>(v, q, qdt, G, scale, wl, pt);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e;
+  if constexpr (sizeof(T) == 2 && sizeof(Acc) == 4) {
+    if (v.head_dim == 128) {
+      e = launch_attn_tc(v, q, qdt, G, scale, wl, *reinterpret_cast<Partials<float>*>(&pt), kDense, st);
+    } else {
+      attn_chunk_kernel<T, Acc, kDense><<<grid, kAttnThreads, smem, st>>>(v, q, qdt, G, scale, wl, pt);
+      e = cudaGetLastError();
+    }
+  } else {
+    attn_chunk_kernel<T, Acc, kDense><<<grid, kAttnThreads, smem, st>>>(v, q, qdt, G, scale, wl, pt);
+    e = cudaGetLastError();
+  }
   if (e != cudaSuccess) return e;
   merge_kernel<Acc, kDense><<<(unsigned)BH, 128, 0, st>>>(v, G, lm, wl, pt, out, lse);
   return cudaGetLastError();
