@@ -53,14 +53,13 @@ def rng_stream(seed, n, k, degenerate_from=None):
     rng.integers(n) from the first zero-mass step on."""
     rng = np.random.default_rng(seed)
     first = int(rng.integers(n))
+    stop = k if degenerate_from is None else min(int(degenerate_from), k)
     u = np.zeros(max(k - 1, 0))
     alt = np.zeros(max(k - 1, 0), dtype=np.int32)
-    stop = k if degenerate_from is None else degenerate_from
-    for i in range(1, k):
-        if i < stop:
-            u[i - 1] = rng.random()
-        else:
-            alt[i - 1] = int(rng.integers(n))
+    if stop > 1:
+        u[: stop - 1] = rng.random(stop - 1)  # same bits as stop-1 scalar draws
+    for i in range(stop, k):
+        alt[i - 1] = int(rng.integers(n))
     return first, u, alt
 
 
@@ -164,6 +163,19 @@ class ClusteredLayer:
 
     _prefill_k = 0
 
+    def split(self):
+        """One single-sequence ClusteredLayer per batch entry, sharing storage
+        (used to cluster many layers in one launch, then hand them out)."""
+        out = []
+        for b in range(self.batch):
+            sl = lambda t: None if t is None else t[b:b + 1]  # noqa: E731
+            lay = ClusteredLayer(sl(self.keys), sl(self.values), sl(self.offs), sl(self.nclusters),
+                                 sl(self.centroids), sl(self.value_means), sl(self.perm), self.n_tokens,
+                                 self.sink, self.window, prefill_tokens=self.prefill_tokens)
+            lay._prefill_k = self._prefill_k
+            out.append(lay)
+        return out
+
     # host views for parity ----------------------------------------------
     def head_tables(self, b, h):
         """Host copy of one head's tables (synchronises).  Returns dict with
@@ -188,7 +200,7 @@ class ClusteredLayer:
 
 def cluster_layer(keys, values, *, k=None, sink=4, window=64, seed=0, max_iters=DEFAULT_MAX_ITERS,
                   tokens_per_cluster=DEFAULT_TOKENS_PER_CLUSTER, layer=0, fp64_assign=True, row_cap=None,
-                  extra_clusters=0, stream=None, return_picks=False):
+                  extra_clusters=0, stream=None, head_seeds=None):
     """k-means-cluster one layer of a batch on the GPU (`build_clustered_cache`
     for one layer, clustering.py:266-314).  keys/values: CUDA [B,H,N,d] f32
     or bf16 in position order.  ``row_cap``/``extra_clusters`` reserve room
@@ -218,7 +230,8 @@ def cluster_layer(keys, values, *, k=None, sink=4, window=64, seed=0, max_iters=
         for b in range(B):
             for h in range(H):
                 i = b * H + h
-                f, u, a = rng_stream(head_seed(seed, layer, h, b), middle, k,
+                hs = head_seed(seed, layer, h, b) if head_seeds is None else int(head_seeds[b][h])
+                f, u, a = rng_stream(hs, middle, k,
                                      None if degen is None else int(degen[i]))
                 firsts[i] = f
                 us[i, :k - 1] = u

@@ -93,45 +93,135 @@ __global__ void xnorm_kernel(dp_cluster_params p, const void* __restrict__ src, 
 
 // -------------------------------------------------------------------------
 // k-means++ seeding: one CTA per head, all k-1 sequential steps in-kernel.
+// Each step streams the head's middle points through shared memory in
+// 256-point tiles (coalesced cp.async, double-buffered for bf16), computes
+// |x - c|^2 = |x|^2 - 2 x.c + |c|^2 in fp64 (products of bf16/fp32 inputs
+// are exact in fp64), folds it into dsq (global, L2-resident), then draws
+// the next centre: idx = first j with cdf_j / cdf_last > u, cdf = cumsum of
+// dsq/total over contiguous per-thread segments (Generator.choice).
 // -------------------------------------------------------------------------
-constexpr int kPPThreads = 1024;
+constexpr int kPPThreads = 256;
 
-__global__ void __launch_bounds__(kPPThreads) kmeanspp_kernel(dp_cluster_params p, const void* __restrict__ src,
+template <typename T>
+__global__ void __launch_bounds__(kPPThreads) kmeanspp_kernel(dp_cluster_params p, const T* __restrict__ src,
                                                             const int* __restrict__ first_pick,
                                                             const double* __restrict__ uniforms,
                                                             const int* __restrict__ alt_picks,
                                                             int* __restrict__ degenerate_from, int* __restrict__ picks,
                                                             KmWs w) {
+  constexpr int kStages = sizeof(T) == 2 ? 2 : 1;
   const int bh = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
   const int M = p.n_tokens - p.sink - p.window, d = p.head_dim, k = p.k;
+  const int rowb = d * (int)sizeof(T) + 16;  // padded row (bytes): conflict-free 16B LDS
+  const int chunks = d * (int)sizeof(T) / 16;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  double* c = reinterpret_cast<double*>(smem_raw);  // current centre [d]
+  double* c = reinterpret_cast<double*>(smem_raw);              // [d]
+  unsigned char* tiles = smem_raw + ((d * 8 + 127) / 128) * 128;  // kStages x [256][rowb]
   __shared__ double red[33];
-  __shared__ int s_idx;
-  __shared__ int s_degen;
-  const size_t xbase = ((size_t)bh * p.n_tokens + p.sink) * d;
+  __shared__ double s_cn;
+  __shared__ int s_idx, s_degen;
+  const T* X = src + ((size_t)bh * p.n_tokens + p.sink) * d;
+  const double* xn = w.xnorm + (size_t)bh * M;
   double* dsq = w.dsq + (size_t)bh * M;
   const int degen_in = degenerate_from ? degenerate_from[bh] : k;
-  if (tid == 0) s_degen = k;
+  const int ntiles = (M + kPPThreads - 1) / kPPThreads;
   const int per = (M + nt - 1) / nt;
   const int beg = min(M, tid * per), end = min(M, beg + per);
+  if (tid == 0) {
+    s_degen = k;
+    s_idx = first_pick[bh];
+  }
+  __syncthreads();
+
+  auto issue_tile = [&](int t, int buf) {
+    unsigned char* dst = tiles + (size_t)buf * kPPThreads * rowb;
+    const int p0 = t * kPPThreads;
+    const int np = min(kPPThreads, M - p0);
+    const unsigned char* g = reinterpret_cast<const unsigned char*>(X + (size_t)p0 * d);
+    for (int i = tid; i < np * chunks; i += nt) {
+      const int r = i / chunks, cc = i - r * chunks;
+      const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(dst + r * rowb + cc * 16));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(g + (size_t)r * d * sizeof(T) + cc * 16));
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+
   for (int i = 0; i < k; ++i) {
-    if (i == 0) {
-      if (tid == 0) s_idx = first_pick[bh];
-    } else {
-      // total = dsq.sum()
-      double loc = 0.0;
-      for (int j = beg; j < end; ++j) loc += dsq[j];
-      const double total = block_sum(loc, red);
-      if (total > 0.0 && i < degen_in) {
-        // cdf over p = dsq/total; idx = first j with cdf_j/cdf_last > u
-        double lp = 0.0;
-        for (int j = beg; j < end; ++j) lp += dsq[j] / total;
-        double last;
-        const double off = block_exclusive_scan(lp, red, &last);
-        const double u = uniforms[(size_t)bh * (k - 1) + (i - 1)];
-        if (tid == 0) s_idx = M;
-        __syncthreads();
+    const int idx = s_idx;
+    if (tid == 0) picks[(size_t)bh * k + i] = idx;
+    for (int j = tid; j < d; j += nt) {
+      const double x = (double)to_float(X[(size_t)idx * d + j]);
+      c[j] = x;
+      w.cent[((size_t)bh * k + i) * d + j] = x;
+    }
+    __syncthreads();
+    if (tid < 32) {
+      double a = 0.0;
+      for (int j = tid; j < d; j += 32) a = fma(c[j], c[j], a);
+      a = warp_sum(a);
+      if (tid == 0) s_cn = a;
+    }
+    // ---- dsq update over all tiles -------------------------------------
+    issue_tile(0, 0);
+    for (int t = 0; t < ntiles; ++t) {
+      const int buf = kStages == 2 ? (t & 1) : 0;
+      if (kStages == 2 && t + 1 < ntiles) {
+        issue_tile(t + 1, buf ^ 1);
+        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+      } else {
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      }
+      __syncthreads();
+      const int pt = t * kPPThreads + tid;
+      if (pt < M) {
+        const unsigned char* row = tiles + (size_t)buf * kPPThreads * rowb + tid * rowb;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        for (int cc = 0; cc < chunks; ++cc) {
+          const int4 raw = *reinterpret_cast<const int4*>(row + cc * 16);
+          if constexpr (sizeof(T) == 2) {
+            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+            const double* cj = c + cc * 8;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 f = __bfloat1622float2(h[e]);
+              if (e & 1) {
+                a2 = fma((double)f.x, cj[2 * e], a2);
+                a3 = fma((double)f.y, cj[2 * e + 1], a3);
+              } else {
+                a0 = fma((double)f.x, cj[2 * e], a0);
+                a1 = fma((double)f.y, cj[2 * e + 1], a1);
+              }
+            }
+          } else {
+            const float* f = reinterpret_cast<const float*>(&raw);
+            const double* cj = c + cc * 4;
+            a0 = fma((double)f[0], cj[0], a0);
+            a1 = fma((double)f[1], cj[1], a1);
+            a2 = fma((double)f[2], cj[2], a2);
+            a3 = fma((double)f[3], cj[3], a3);
+          }
+        }
+        const double dist = fmax(xn[pt] - 2.0 * ((a0 + a1) + (a2 + a3)) + s_cn, 0.0);
+        dsq[pt] = (i == 0) ? dist : fmin(dsq[pt], dist);
+      }
+      __syncthreads();  // buffer reuse
+    }
+    if (i + 1 == k) break;
+    // ---- draw centre i+1 -------------------------------------------------
+    double loc = 0.0;
+    for (int j = beg; j < end; ++j) loc += dsq[j];
+    const double total = block_sum(loc, red);
+    const int step = i + 1;
+    if (total > 0.0 && step < degen_in) {
+      double lp = 0.0;
+      for (int j = beg; j < end; ++j) lp += dsq[j] / total;
+      double last;
+      const double off = block_exclusive_scan(lp, red, &last);
+      const double u = uniforms[(size_t)bh * (k - 1) + (step - 1)];
+      if (tid == 0) s_idx = M;
+      __syncthreads();
+      {  // every segment reports its first crossing; the min is the pick (robust to
+         // the scan's rounding at segment edges)
         double run = off;
         for (int j = beg; j < end; ++j) {
           run += dsq[j] / total;
@@ -140,37 +230,16 @@ __global__ void __launch_bounds__(kPPThreads) kmeanspp_kernel(dp_cluster_params 
             break;
           }
         }
-        __syncthreads();
-        if (tid == 0 && s_idx >= M) s_idx = M - 1;
+      }
+      __syncthreads();
+      if (tid == 0 && s_idx >= M) s_idx = M - 1;
+    } else if (tid == 0) {
+      if (step >= degen_in && alt_picks) {
+        s_idx = alt_picks[(size_t)bh * (k - 1) + (step - 1)];
       } else {
-        if (tid == 0) {
-          if (i >= degen_in && alt_picks) {
-            s_idx = alt_picks[(size_t)bh * (k - 1) + (i - 1)];
-          } else {
-            if (s_degen == k) s_degen = i;
-            s_idx = 0;
-          }
-        }
+        if (s_degen == k) s_degen = step;
+        s_idx = 0;
       }
-    }
-    __syncthreads();
-    const int idx = s_idx;
-    if (tid == 0) picks[(size_t)bh * k + i] = idx;
-    for (int j = tid; j < d; j += nt) {
-      const double x = load_elem_d(src, p.dtype, xbase + (size_t)idx * d + j);
-      c[j] = x;
-      w.cent[((size_t)bh * k + i) * d + j] = x;
-    }
-    __syncthreads();
-    // dsq = min(dsq, |x - c|^2)
-    for (int j = tid; j < M; j += nt) {
-      double a = 0.0;
-      const size_t xb = xbase + (size_t)j * d;
-      for (int e = 0; e < d; ++e) {
-        const double df = load_elem_d(src, p.dtype, xb + e) - c[e];
-        a = fma(df, df, a);
-      }
-      dsq[j] = (i == 0) ? a : fmin(dsq[j], a);
     }
     __syncthreads();
   }
@@ -179,6 +248,28 @@ __global__ void __launch_bounds__(kPPThreads) kmeanspp_kernel(dp_cluster_params 
     w.knum[bh] = k;
     w.done[bh] = 0;
   }
+}
+
+static size_t pp_smem(const dp_cluster_params* p) {
+  const int es = p->dtype == DP_F32 ? 4 : 2;
+  const int stages = p->dtype == DP_F32 ? 1 : 2;
+  return ((p->head_dim * 8 + 127) / 128) * 128 + (size_t)stages * kPPThreads * (p->head_dim * es + 16);
+}
+
+static cudaError_t launch_kmeanspp(const dp_cluster_params* p, const void* src, const int* first,
+                                   const double* u, const int* alt, int* degen, int* picks, KmWs w,
+                                   cudaStream_t st) {
+  const int BH = p->batch * p->kv_heads;
+  const size_t smem = pp_smem(p);
+  if (p->dtype == DP_F32) {
+    cudaFuncSetAttribute(kmeanspp_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kmeanspp_kernel<float><<<BH, kPPThreads, smem, st>>>(*p, (const float*)src, first, u, alt, degen, picks, w);
+  } else {
+    cudaFuncSetAttribute(kmeanspp_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kmeanspp_kernel<__nv_bfloat16><<<BH, kPPThreads, smem, st>>>(*p, (const __nv_bfloat16*)src, first, u, alt,
+                                                                  degen, picks, w);
+  }
+  return cudaGetLastError();
 }
 
 // -------------------------------------------------------------------------
@@ -539,6 +630,13 @@ size_t dp_cluster_workspace_bytes(const dp_cluster_params* p) {
   return km_layout(p, nullptr, nullptr);
 }
 
+static int check_pp(const dp_cluster_params* p) {
+  const int es = p->dtype == DP_F32 ? 4 : 2;
+  if ((p->head_dim * es) % 16 != 0) return set_error(DP_ERR_UNSUPPORTED, "head_dim * elem must be a multiple of 16");
+  if (pp_smem(p) > 227 * 1024) return set_error(DP_ERR_UNSUPPORTED, "head_dim too large for the k-means++ tile");
+  return DP_OK;
+}
+
 static int check_params(const dp_cluster_params* p) {
   if (!p) return set_error(DP_ERR_INVALID, "null params");
   if (p->sink < 0 || p->window < 0) return set_error(DP_ERR_INVALID, "sink and window must be >= 0");
@@ -562,9 +660,9 @@ int dp_kmeanspp(const dp_cluster_params* p, const void* src_keys, const int32_t*
   km_layout(p, &w, (char*)ws);
   cudaStream_t st = (cudaStream_t)stream;
   const int BH = p->batch * p->kv_heads;
-  kmeanspp_kernel<<<BH, kPPThreads, p->head_dim * 8, st>>>(*p, src_keys, first_pick, uniforms, alt_picks,
-                                                           degenerate_from, picks, w);
-  cudaError_t e = cudaGetLastError();
+  if ((r = check_pp(p))) return r;
+  xnorm_kernel<<<dim3((p->n_tokens * 32 + 255) / 256, BH), 256, 0, st>>>(*p, src_keys, w);
+  cudaError_t e = launch_kmeanspp(p, src_keys, first_pick, uniforms, alt_picks, degenerate_from, picks, w, st);
   return e == cudaSuccess ? DP_OK : set_cuda_error(e, "dp_kmeanspp");
 }
 
@@ -584,10 +682,11 @@ int dp_cluster_build(const dp_cluster_params* p, const void* src_keys, const voi
   const int BH = p->batch * p->kv_heads;
   const int M = p->n_tokens - p->sink - p->window;
   // picks are a by-product of seeding; park them in the `sorted` scratch
-  if (M < p->k) return set_error(DP_ERR_INVALID, "more clusters than points");
+  cudaError_t e0;
   xnorm_kernel<<<dim3((M * 32 + 255) / 256, BH), 256, 0, st>>>(*p, src_keys, w);
-  kmeanspp_kernel<<<BH, kPPThreads, p->head_dim * 8, st>>>(*p, src_keys, first_pick, uniforms, alt_picks,
-                                                           degenerate_from, w.sorted, w);
+  if ((r = check_pp(p))) return r;
+  e0 = launch_kmeanspp(p, src_keys, first_pick, uniforms, alt_picks, degenerate_from, w.sorted, w, st);
+  if (e0 != cudaSuccess) return set_cuda_error(e0, "dp_cluster_build (kmeans++)");
   cnorm_kernel<<<dim3((p->k * 32 + 255) / 256, BH), 256, 0, st>>>(*p, w);
   for (int it = 0; it < p->max_iters; ++it) {
     if (p->fp64_assign)

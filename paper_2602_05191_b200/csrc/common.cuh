@@ -14,6 +14,9 @@ constexpr int kMaxGroup = 8;  // GQA group sizes the decode kernels are built fo
 
 __device__ __forceinline__ float bf2f(__nv_bfloat16 x) { return __bfloat162float(x); }
 
+__device__ __forceinline__ float to_float(float x) { return x; }
+__device__ __forceinline__ float to_float(__nv_bfloat16 x) { return __bfloat162float(x); }
+
 // Element loads from a raw pointer of runtime dtype (DP_F32 / DP_BF16).
 __device__ __forceinline__ double load_elem_d(const void* p, int dtype, size_t i) {
   return dtype == DP_F32 ? (double)reinterpret_cast<const float*>(p)[i]

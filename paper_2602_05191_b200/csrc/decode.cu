@@ -26,7 +26,7 @@ namespace dp {
 // centroids and bf16/fp32 queries are exact in fp64, so the log-masses match
 // the fp64 oracle to ~1e-16 and selection ties are only true ties).
 // ---------------------------------------------------------------------------
-constexpr int kScoreTile = 128;
+constexpr int kScoreTile = 64;
 
 __global__ void __launch_bounds__(kScoreTile) score_kernel(dp_cache_view v, const void* __restrict__ q,
                                                          int qdt, int G, double scale,
@@ -46,8 +46,10 @@ __global__ void __launch_bounds__(kScoreTile) score_kernel(dp_cache_view v, cons
   const float4* C4 = reinterpret_cast<const float4*>(v.centroids + ((size_t)bh * v.cluster_cap + k0) * d);
   for (int i = tid; i < n * d4; i += blockDim.x) {
     const int r = i / d4, c = i - r * d4;
-    *reinterpret_cast<float4*>(&cs[r * stride + 4 * c]) = __ldg(&C4[(size_t)r * d4 + c]);
+    const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(&cs[r * stride + 4 * c]));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(&C4[(size_t)r * d4 + c]));
   }
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
   __syncthreads();
   if (tid >= n) return;
   double acc[kMaxGroup];
@@ -168,13 +170,19 @@ __global__ void __launch_bounds__(kSelectThreads) select_kernel(dp_cache_view v,
   if (tid == 0) { s_n1 = K; s_n2 = K; }
   __syncthreads();
   // stage 1: first i with cum_i/total >= p1 (searchsorted left + 1, clamped)
-  for (int i = tid; i < K; i += nt)
-    if (key[i] / total >= p1) atomicMin(&s_n1, i + 1);
+  for (int i0 = 0; i0 < K; i0 += nt) {  // first index per warp only -> <= 32 atomics
+    const int i = i0 + tid;
+    const unsigned b = __ballot_sync(0xffffffffu, i < K && key[i] / total >= p1);
+    if (b && (tid & 31) == __ffs(b) - 1) atomicMin(&s_n1, i + 1);
+  }
   __syncthreads();
   const int n1 = s_n1;
   const double sub_total = key[n1 - 1];  // probs[cp].sum(), engine.py:191
-  for (int i = tid; i < n1; i += nt)
-    if (key[i] / sub_total >= p2) atomicMin(&s_n2, i + 1);
+  for (int i0 = 0; i0 < n1; i0 += nt) {
+    const int i = i0 + tid;
+    const unsigned b = __ballot_sync(0xffffffffu, i < n1 && key[i] / sub_total >= p2);
+    if (b && (tid & 31) == __ffs(b) - 1) atomicMin(&s_n2, i + 1);
+  }
   __syncthreads();
   const int n2 = min(s_n2, n1);
   uint8_t* st = state + (size_t)bhq * cap;
@@ -388,53 +396,85 @@ __global__ void __launch_bounds__(kAttnThreads) attn_chunk_kernel(dp_cache_view 
 }
 
 // ---------------------------------------------------------------------------
-// merge: one CTA per (b, kv head).  Combines the chunk partials of every q
-// head of the group with the approx pseudo-rows (logit = log_mass, value =
-// value mean, engine.py:231-246) under one normaliser.
+// merge: one CTA (8 warps) per (q head, b*h).  Combines the chunk partials
+// with the approx pseudo-rows (logit = log_mass, value = value mean,
+// engine.py:231-246) under one normaliser.  Chunks/approx rows are spread
+// over threads/warps so every global load is issued in parallel.
 // ---------------------------------------------------------------------------
+constexpr int kMergeThreads = 256;
+
 template <typename Acc, bool kDense>
-__global__ void merge_kernel(dp_cache_view v, int G, const double* __restrict__ lm, WorkLists wl,
-                             Partials<Acc> pt, float* __restrict__ out, float* __restrict__ lse) {
-  const int bh = blockIdx.x;
-  const int d = v.head_dim, tid = threadIdx.x, cap = v.cluster_cap;
+__global__ void __launch_bounds__(kMergeThreads) merge_kernel(dp_cache_view v, int G, const double* __restrict__ lm,
+                                                             WorkLists wl, Partials<Acc> pt, float* __restrict__ out,
+                                                             float* __restrict__ lse) {
+  const int g = blockIdx.x, bh = blockIdx.y, hq = bh * G + g;
+  const int d = v.head_dim, tid = threadIdx.x, nt = blockDim.x, cap = v.cluster_cap;
+  const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
   const int rows_total = kDense ? v.n_tokens : wl.nrows[bh];
   const int nch = (rows_total + kChunkRows - 1) / kChunkRows;
   const int na = kDense ? 0 : wl.napprox[bh];
   const int2* apx = wl.approx + (size_t)bh * cap;
   const float* vbar = v.value_means + (size_t)bh * cap * d;
-  for (int g = 0; g < G; ++g) {
-    const int hq = bh * G + g;
-    const double* lmh = lm ? lm + (size_t)hq * cap : nullptr;
-    const size_t pbase = (size_t)bh * pt.max_chunks * G;
-    double M = -CUDART_INF;
-    for (int c = 0; c < nch; ++c) M = fmax(M, (double)pt.m[pbase + (size_t)c * G + g]);
-    for (int a = 0; a < na; ++a) {
-      const int2 e = apx[a];
-      if ((e.y >> g) & 1) M = fmax(M, lmh[e.x]);
-    }
-    double L = 0.0;
-    for (int c = 0; c < nch; ++c) {
-      const double mc = pt.m[pbase + (size_t)c * G + g];
-      if (mc != -CUDART_INF) L += (double)pt.l[pbase + (size_t)c * G + g] * exp(mc - M);
-    }
-    for (int a = 0; a < na; ++a) {
-      const int2 e = apx[a];
-      if ((e.y >> g) & 1) L += exp(lmh[e.x] - M);
-    }
-    for (int j = tid; j < d; j += blockDim.x) {
-      double o = 0.0;
-      for (int c = 0; c < nch; ++c) {
-        const double mc = pt.m[pbase + (size_t)c * G + g];
-        if (mc != -CUDART_INF) o += exp(mc - M) * (double)pt.o[(pbase + (size_t)c * G + g) * d + j];
-      }
-      for (int a = 0; a < na; ++a) {
-        const int2 e = apx[a];
-        if ((e.y >> g) & 1) o += exp(lmh[e.x] - M) * (double)vbar[(size_t)e.x * d + j];
-      }
-      out[(size_t)hq * d + j] = (float)(o / L);
-    }
-    if (tid == 0) lse[hq] = (float)(M + log(L));
+  const double* lmh = lm ? lm + (size_t)hq * cap : nullptr;
+  const size_t pbase = (size_t)bh * pt.max_chunks * G;
+  __shared__ double red[33];
+  __shared__ double oacc[8][256];
+
+  double mloc = -CUDART_INF;
+  for (int c = tid; c < nch; c += nt) mloc = fmax(mloc, (double)pt.m[pbase + (size_t)c * G + g]);
+  for (int a = tid; a < na; a += nt) {
+    const int2 e = apx[a];
+    if ((e.y >> g) & 1) mloc = fmax(mloc, lmh[e.x]);
   }
+  const double M = block_max(mloc, red, -CUDART_INF);
+  double lloc = 0.0;
+  for (int c = tid; c < nch; c += nt) {
+    const double mc = pt.m[pbase + (size_t)c * G + g];
+    if (mc != -CUDART_INF) lloc += (double)pt.l[pbase + (size_t)c * G + g] * exp(mc - M);
+  }
+  for (int a = tid; a < na; a += nt) {
+    const int2 e = apx[a];
+    if ((e.y >> g) & 1) lloc += exp(lmh[e.x] - M);
+  }
+  const double L = block_sum(lloc, red);
+
+  double acc[8];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) acc[t] = 0.0;
+  for (int c = warp; c < nch; c += nw) {
+    const double mc = pt.m[pbase + (size_t)c * G + g];
+    if (mc == -CUDART_INF) continue;
+    const double w = exp(mc - M);
+    const Acc* oc = pt.o + (pbase + (size_t)c * G + g) * d;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int j = lane + 32 * t;
+      if (j < d) acc[t] += w * (double)oc[j];
+    }
+  }
+  for (int a = warp; a < na; a += nw) {
+    const int2 e = apx[a];
+    if (!((e.y >> g) & 1)) continue;
+    const double w = exp(lmh[e.x] - M);
+    const float* vb = vbar + (size_t)e.x * d;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int j = lane + 32 * t;
+      if (j < d) acc[t] += w * (double)vb[j];
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    const int j = lane + 32 * t;
+    if (j < d) oacc[warp][j] = acc[t];
+  }
+  __syncthreads();
+  for (int j = tid; j < d; j += nt) {
+    double o = 0.0;
+    for (int w = 0; w < nw; ++w) o += oacc[w][j];
+    out[(size_t)hq * d + j] = (float)(o / L);
+  }
+  if (tid == 0) lse[hq] = (float)(M + log(L));
 }
 
 // ---------------------------------------------------------------------------
@@ -550,7 +590,7 @@ cudaError_t launch_attn_t(const dp_cache_view& v, const void* q, int qdt, int G,
     e = cudaGetLastError();
   }
   if (e != cudaSuccess) return e;
-  merge_kernel<Acc, kDense><<<(unsigned)BH, 128, 0, st>>>(v, G, lm, wl, pt, out, lse);
+  merge_kernel<Acc, kDense><<<dim3(G, (unsigned)BH), kMergeThreads, 0, st>>>(v, G, lm, wl, pt, out, lse);
   return cudaGetLastError();
 }
 

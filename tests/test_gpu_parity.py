@@ -258,12 +258,13 @@ def test_reference_semantics_on_gpu():
     ref = O.full_attention(q.astype(np.float64), keys[0, 0].astype(np.float64), vals[0, 0].astype(np.float64))
     assert O.output_error(out.output, ref.output) <= 1e-5
     assert out.normalizer == pytest.approx(ref.normalizer, rel=1e-5)
-    # two-token cluster mass 2e vs 1+e^2 (test_engine.py:113-125) -- d=8 padded
-    k2 = np.zeros((1, 1, 2, 8), np.float32)
-    k2[0, 0, 1, 0] = 2.0 * math.sqrt(8)
-    cache2 = dp.KvCache(k2, np.ones((1, 1, 2, 8), np.float32))
+    # two-token cluster mass 2e vs 1+e^2 (test_engine.py:113-125), embedded in
+    # d=16 so the logits {0, 2} stay exact (sqrt(16) = 4)
+    k2 = np.zeros((1, 1, 2, 16), np.float32)
+    k2[0, 0, 1, 0] = 8.0
+    cache2 = dp.KvCache(k2, np.ones((1, 1, 2, 16), np.float32))
     cc2 = dp.build_clustered_cache(cache2, k=1, sink=0, window=0)
-    q2 = np.zeros(8, np.float32)
+    q2 = np.zeros(16, np.float32)
     q2[0] = 1.0
     est2 = dp.estimate_cluster_distribution(q2, cc2, 0, 0)
     assert math.exp(est2.log_masses[0]) == pytest.approx(2 * math.e, rel=1e-9)
