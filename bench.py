@@ -473,7 +473,7 @@ def run_b200(a):
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
-    launches = a.steps * L * 5
+    launches = a.steps * L * 4  # score, select, worklist, attn_tc (merge fused)
     if rank == 0:
         line = {
             "metric": "decode_us_per_step", "value": ms * 1e3, "unit": "us/step", "n_gpus": world,
@@ -483,7 +483,7 @@ def run_b200(a):
             "config": workload_config(a, world),
             "roofline": {"bound": "hbm", "achieved": attend_gbs, "peak": hbm_peak, "unit": "GB/s",
                          "frac": attend_gbs / hbm_peak, "traffic": None,
-                         "kernel": "dp_attend (attn_chunk_kernel + merge_kernel), per-layer launch",
+                         "kernel": "dp_attend = attn_tc_kernel (gathered split-KV attention + fused LSE merge), one launch per layer",
                          "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": float(attend_bytes.mean())},
             "cpu_baseline": cpu,

@@ -12,7 +12,8 @@
  *
  * Conventions
  *   - all buffers are caller-owned device memory; nothing allocates on the
- *     step path (workspace sized once with dp_*_workspace_bytes);
+ *     step path (workspace sized once with dp_*_workspace_bytes, ZERO-filled
+ *     once before first use; the kernels leave it reusable);
  *   - every call is stream-ordered on the caller's cudaStream_t (passed as
  *     void* so this header needs no CUDA include);
  *   - return value: DP_OK or an error code; dp_last_error() gives a

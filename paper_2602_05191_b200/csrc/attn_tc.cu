@@ -13,8 +13,11 @@
 //
 // P is split hi + lo into two bf16 operands (two MMAs), so the weights keep
 // ~2^-16 relative precision; an fp32 query is split the same way.  The chunk
-// writes an unnormalised partial (m, l, o) per head that merge_kernel folds
-// together with the approx pseudo-rows (engine.py:216-252).
+// writes an unnormalised partial (m, l, o) per head; the last chunk of a head
+// to finish (atomic counter) folds all partials together with the approx
+// pseudo-rows (engine.py:216-252), so no separate merge launch is needed.
+// CTAs are indexed by a compact work index (prefix over per-head chunk
+// counts), so active chunks are dispatched first.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -71,13 +74,49 @@ __device__ __forceinline__ void split2(float x, float y, unsigned& hi, unsigned&
 
 template <bool kDense, bool kQF32>
 __global__ void __launch_bounds__(kTcThreads) attn_tc_kernel(dp_cache_view v, const void* __restrict__ q, int G,
-                                                            float scale_log2, WorkLists wl, Partials<float> pt) {
-  const int bh = blockIdx.y, c = blockIdx.x;
-  const int rows_total = kDense ? v.n_tokens : wl.nrows[bh];
-  const int nchunk = (rows_total + kTcRows - 1) / kTcRows;
-  if (c >= nchunk) return;
+                                                            float scale_log2, const double* __restrict__ lm,
+                                                            WorkLists wl, Partials<float> pt, float* __restrict__ out,
+                                                            float* __restrict__ lse) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gq = lane >> 2, tq = lane & 3;
+  const int BH = v.batch * v.kv_heads;
+  const int w = blockIdx.x;
+  __shared__ int s_bh, s_c, s_nch, s_last;
+  __shared__ int4 sruns[kTcRows];
+  // ---- compact work index -> (head, chunk): active chunks are the first CTAs
+  if (kDense) {
+    const int per = (v.n_tokens + kTcRows - 1) / kTcRows;
+    if (tid == 0) {
+      s_bh = w / per < BH ? w / per : -1;
+      s_c = w % per;
+      s_nch = per;
+    }
+  } else if (warp == 0) {
+    int base = 0, found = 0;
+    for (int b0 = 0; b0 < BH && !found; b0 += 32) {
+      const int n = b0 + lane < BH ? wl.nchunks[b0 + lane] : 0;
+      int inc = n;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+      }
+      const bool hit = b0 + lane < BH && w >= base + inc - n && w < base + inc;
+      const unsigned bal = __ballot_sync(0xffffffffu, hit);
+      if (hit) {
+        s_bh = b0 + lane;
+        s_c = w - (base + inc - n);
+        s_nch = n;
+      }
+      found = bal != 0;
+      base += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    if (!found && lane == 0) s_bh = -1;
+  }
+  __syncthreads();
+  const int bh = s_bh, c = s_c, nchunk = s_nch;
+  if (bh < 0) return;
+  const int rows_total = kDense ? v.n_tokens : wl.nrows[bh];
   const int v0 = c * kTcRows;
   const int nr = min(kTcRows, rows_total - v0);
 
@@ -86,56 +125,54 @@ __global__ void __launch_bounds__(kTcThreads) attn_tc_kernel(dp_cache_view v, co
   __nv_bfloat16* Vs = Ks + kTcRows * kRowStride;
   float* Ps = reinterpret_cast<float*>(Vs + kTcRows * kRowStride);  // [8][kTcRows]
   int* rmask = reinterpret_cast<int*>(Ps + 8 * kTcRows);            // [kTcRows]
-  float* red = reinterpret_cast<float*>(rmask + kTcRows);           // [4][8] max, [4][8] sum
+  int* rphys = rmask + kTcRows;                                     // [kTcRows]
+  float* red = reinterpret_cast<float*>(rphys + kTcRows);           // [4][8] max, [4][8] sum
 
-  // ---- row -> physical row + head mask (thread per row) -----------------
+  // ---- row -> physical row + head mask: the chunk's runs staged in smem ---
   int phys = -1, mask = 0;
-  {
-    const int r = tid;
-    if (r < nr) {
-      const int vr = v0 + r;
-      if (kDense) {
-        phys = vr;
-        mask = (1 << G) - 1;
-      } else {
-        const int4* runs = wl.runs + (size_t)bh * (v.cluster_cap + 2);
-        int lo = 0, hi = wl.nruns[bh] - 1;
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (__ldg(&runs[mid].w) <= vr) lo = mid; else hi = mid - 1;
-        }
-        const int4 ru = runs[lo];
-        phys = ru.x + (vr - ru.w);
-        mask = ru.z;
-      }
+  if (kDense) {
+    if (tid < nr) {
+      phys = v0 + tid;
+      mask = (1 << G) - 1;
     }
-    rmask[r] = mask;
+  } else {
+    const int r0 = wl.chunk_run[(size_t)bh * wl.max_chunks + c];
+    const int nrun = min(wl.nruns[bh] - r0, nr);
+    if (tid < nrun) sruns[tid] = wl.runs[(size_t)bh * (v.cluster_cap + 2) + r0 + tid];
+    __syncthreads();
+    if (tid < nr) {
+      const int vr = v0 + tid;
+      int lo = 0, hi = nrun - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (sruns[mid].w <= vr) lo = mid; else hi = mid - 1;
+      }
+      const int4 ru = sruns[lo];
+      phys = ru.x + (vr - ru.w);
+      mask = ru.z;
+    }
   }
-  // ---- stage K (group 0) and V (group 1) --------------------------------
+  rmask[tid] = mask;
+  rphys[tid] = phys;
+  __syncthreads();
+  // ---- stage K (group 0) and V (group 1): a warp copies 2 rows = 512
+  // contiguous bytes per instruction (rows of a run are adjacent in HBM)
   const int d = 128;
   const size_t head_off = (size_t)bh * v.row_cap * d;
   const __nv_bfloat16* Kg = reinterpret_cast<const __nv_bfloat16*>(v.keys) + head_off;
   const __nv_bfloat16* Vg = reinterpret_cast<const __nv_bfloat16*>(v.values) + head_off;
-  // each thread copies its own row (16 x 16 B), rows are contiguous runs
-  {
-    const unsigned kd = smem_u32(Ks + tid * kRowStride);
-    if (phys >= 0) {
-      const __nv_bfloat16* src = Kg + (size_t)phys * d;
 #pragma unroll
-      for (int j = 0; j < 16; ++j) cp16(kd + j * 16, src + j * 8);
-    } else {
-#pragma unroll
-      for (int j = 0; j < 16; ++j) *reinterpret_cast<int4*>(Ks + tid * kRowStride + j * 8) = make_int4(0, 0, 0, 0);
-    }
-    asm volatile("cp.async.commit_group;\n" ::);
-    const unsigned vd = smem_u32(Vs + tid * kRowStride);
-    if (phys >= 0) {
-      const __nv_bfloat16* src = Vg + (size_t)phys * d;
-#pragma unroll
-      for (int j = 0; j < 16; ++j) cp16(vd + j * 16, src + j * 8);
-    } else {
-#pragma unroll
-      for (int j = 0; j < 16; ++j) *reinterpret_cast<int4*>(Vs + tid * kRowStride + j * 8) = make_int4(0, 0, 0, 0);
+  for (int pass = 0; pass < 2; ++pass) {
+    const __nv_bfloat16* G0 = pass == 0 ? Kg : Vg;
+    __nv_bfloat16* S0 = pass == 0 ? Ks : Vs;
+#pragma unroll 4
+    for (int i = 0; i < 16; ++i) {
+      const int idx = i * kTcThreads + tid;
+      const int row = idx >> 4, ch = idx & 15;
+      const int pr = rphys[row];
+      __nv_bfloat16* dst = S0 + row * kRowStride + ch * 8;
+      if (pr >= 0) cp16(smem_u32(dst), G0 + (size_t)pr * d + ch * 8);
+      else *reinterpret_cast<int4*>(dst) = make_int4(0, 0, 0, 0);
     }
     asm volatile("cp.async.commit_group;\n" ::);
   }
@@ -270,15 +307,70 @@ __global__ void __launch_bounds__(kTcThreads) attn_tc_kernel(dp_cache_view v, co
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt) *reinterpret_cast<float2*>(dst + nt * 8) = make_float2(o[nt][0], o[nt][1]);
   }
+
+  // ---- fused LSE merge: the last chunk of this head folds every partial
+  // together with the approx pseudo-rows (engine.py:231-246) -------------
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = atomicAdd(&wl.counters[bh], 1) == nchunk - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (tid == 0) wl.counters[bh] = 0;  // self-reset for the next launch
+  const int na = kDense ? 0 : wl.napprox[bh];
+  const int2* apx = wl.approx + (size_t)bh * v.cluster_cap;
+  const float* vbar = v.value_means + (size_t)bh * v.cluster_cap * d;
+  const size_t pbase = (size_t)bh * pt.max_chunks * G;
+  for (int g = warp; g < G; g += kTcThreads / 32) {
+    const int hq = bh * G + g;
+    const double* lmh = kDense ? nullptr : lm + (size_t)hq * v.cluster_cap;
+    float mloc = -INFINITY;
+    for (int cc = lane; cc < nchunk; cc += 32) mloc = fmaxf(mloc, __ldcg(&pt.m[pbase + (size_t)cc * G + g]));
+    for (int a = lane; a < na; a += 32) {
+      const int2 e = apx[a];
+      if ((e.y >> g) & 1) mloc = fmaxf(mloc, (float)lmh[e.x]);
+    }
+    const float M = warp_max(mloc);
+    float lloc = 0.f;
+    for (int cc = lane; cc < nchunk; cc += 32) {
+      const float mc = __ldcg(&pt.m[pbase + (size_t)cc * G + g]);
+      if (mc != -INFINITY) lloc += __ldcg(&pt.l[pbase + (size_t)cc * G + g]) * __expf(mc - M);
+    }
+    for (int a = lane; a < na; a += 32) {
+      const int2 e = apx[a];
+      if ((e.y >> g) & 1) lloc += __expf((float)lmh[e.x] - M);
+    }
+    const float L = warp_sum(lloc);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+    for (int cc = 0; cc < nchunk; ++cc) {
+      const float mc = __ldcg(&pt.m[pbase + (size_t)cc * G + g]);
+      const float4 oc = __ldcg(reinterpret_cast<const float4*>(pt.o + (pbase + (size_t)cc * G + g) * d) + lane);
+      const float wgt = mc == -INFINITY ? 0.f : __expf(mc - M);
+      acc.x += wgt * oc.x; acc.y += wgt * oc.y; acc.z += wgt * oc.z; acc.w += wgt * oc.w;
+    }
+#pragma unroll 4
+    for (int a = 0; a < na; ++a) {
+      const int2 e = apx[a];
+      if ((e.y >> g) & 1) {
+        const float wgt = __expf((float)lmh[e.x] - M);
+        const float4 vb = *(reinterpret_cast<const float4*>(vbar + (size_t)e.x * d) + lane);
+        acc.x += wgt * vb.x; acc.y += wgt * vb.y; acc.z += wgt * vb.z; acc.w += wgt * vb.w;
+      }
+    }
+    const float inv = 1.f / L;
+    reinterpret_cast<float4*>(out + (size_t)hq * d)[lane] = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+    if (lane == 0) lse[hq] = M + __logf(L);
+  }
 }
 
 size_t attn_tc_smem_bytes() {
-  return (size_t)2 * kTcRows * kRowStride * 2 + 8 * kTcRows * 4 + kTcRows * 4 + 64 * 4;
+  return (size_t)2 * kTcRows * kRowStride * 2 + 8 * kTcRows * 4 + 2 * kTcRows * 4 + 64 * 4;
 }
 
 template <bool kDense, bool kQF32>
-static cudaError_t launch_tc_t(const dp_cache_view& v, const void* q, int G, double scale, WorkLists wl,
-                               Partials<float> pt, cudaStream_t st) {
+static cudaError_t launch_tc_t(const dp_cache_view& v, const void* q, int G, double scale, const double* lm,
+                               WorkLists wl, Partials<float> pt, float* out, float* lse, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(attn_tc_kernel<kDense, kQF32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -286,17 +378,19 @@ static cudaError_t launch_tc_t(const dp_cache_view& v, const void* q, int G, dou
     attr = true;
   }
   const int rows = kDense ? v.n_tokens : v.row_cap;
-  dim3 grid((rows + kTcRows - 1) / kTcRows, v.batch * v.kv_heads);
+  const int grid = ((rows + kTcRows - 1) / kTcRows) * v.batch * v.kv_heads;  // upper bound; extra CTAs exit
   attn_tc_kernel<kDense, kQF32><<<grid, kTcThreads, attn_tc_smem_bytes(), st>>>(
-      v, q, G, (float)(scale * 1.4426950408889634), wl, pt);
+      v, q, G, (float)(scale * 1.4426950408889634), lm, wl, pt, out, lse);
   return cudaGetLastError();
 }
 
-cudaError_t launch_attn_tc(const dp_cache_view& v, const void* q, int qdt, int G, double scale, WorkLists wl,
-                           Partials<float> pt, bool dense, cudaStream_t st) {
+cudaError_t launch_attn_tc(const dp_cache_view& v, const void* q, int qdt, int G, double scale, const double* lm,
+                           WorkLists wl, Partials<float> pt, float* out, float* lse, bool dense, cudaStream_t st) {
   if (qdt == DP_F32)
-    return dense ? launch_tc_t<true, true>(v, q, G, scale, wl, pt, st) : launch_tc_t<false, true>(v, q, G, scale, wl, pt, st);
-  return dense ? launch_tc_t<true, false>(v, q, G, scale, wl, pt, st) : launch_tc_t<false, false>(v, q, G, scale, wl, pt, st);
+    return dense ? launch_tc_t<true, true>(v, q, G, scale, lm, wl, pt, out, lse, st)
+                 : launch_tc_t<false, true>(v, q, G, scale, lm, wl, pt, out, lse, st);
+  return dense ? launch_tc_t<true, false>(v, q, G, scale, lm, wl, pt, out, lse, st)
+               : launch_tc_t<false, false>(v, q, G, scale, lm, wl, pt, out, lse, st);
 }
 
 }  // namespace dp

@@ -169,6 +169,7 @@ __global__ void __launch_bounds__(kPPThreads) kmeanspp_kernel(dp_cluster_params 
         issue_tile(t + 1, buf ^ 1);
         asm volatile("cp.async.wait_group 1;\n" ::: "memory");
       } else {
+        if (kStages == 1 && t > 0) issue_tile(t, 0);
         asm volatile("cp.async.wait_group 0;\n" ::: "memory");
       }
       __syncthreads();

@@ -40,7 +40,16 @@ __global__ void __launch_bounds__(kScoreTile) score_kernel(dp_cache_view v, cons
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* qs = reinterpret_cast<double*>(smem_raw);
   float* cs = reinterpret_cast<float*>(qs + G * d);
-  for (int i = tid; i < G * d; i += blockDim.x) qs[i] = load_elem_d(q, qdt, (size_t)bh * G * d + i);
+  // stage the raw queries and the centroid tile with cp.async (all loads in
+  // flight at once), then widen the queries to fp64 in shared memory
+  unsigned char* qraw = smem_raw + (size_t)G * d * 8 + (size_t)kScoreTile * stride * 4;
+  const int esz = qdt == DP_F32 ? 4 : 2;
+  const int qchunks = G * d * esz / 16;
+  const unsigned char* qsrc = reinterpret_cast<const unsigned char*>(q) + (size_t)bh * G * d * esz;
+  for (int i = tid; i < qchunks; i += blockDim.x) {
+    const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(qraw + i * 16));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(qsrc + i * 16));
+  }
   const int n = min(kScoreTile, K - k0);
   const int d4 = d >> 2;
   const float4* C4 = reinterpret_cast<const float4*>(v.centroids + ((size_t)bh * v.cluster_cap + k0) * d);
@@ -50,6 +59,10 @@ __global__ void __launch_bounds__(kScoreTile) score_kernel(dp_cache_view v, cons
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(&C4[(size_t)r * d4 + c]));
   }
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+  __syncthreads();
+  for (int i = tid; i < G * d; i += blockDim.x)
+    qs[i] = esz == 4 ? (double)reinterpret_cast<const float*>(qraw)[i]
+                     : (double)bf2f(reinterpret_cast<const __nv_bfloat16*>(qraw)[i]);
   __syncthreads();
   if (tid >= n) return;
   double acc[kMaxGroup];
@@ -218,11 +231,17 @@ __global__ void __launch_bounds__(kListThreads) worklist_kernel(dp_cache_view v,
   __shared__ int red[33];
   __shared__ int s_runs, s_rows, s_apx;
   const int full = (1 << G) - 1;
+  int* crun = wl.chunk_run + (size_t)bh * wl.max_chunks;
+  // every chunk start c*R inside [prefix, prefix+len) gets this run's index
+  auto mark = [&](int r, int prefix, int len) {
+    for (int c = (prefix + kChunkRows - 1) / kChunkRows; c * kChunkRows < prefix + len; ++c) crun[c] = r;
+  };
   if (tid == 0) {
     int r = 0, rows = 0;
-    if (v.sink > 0) { runs[r++] = make_int4(0, v.sink, full, rows); rows += v.sink; }
+    if (v.sink > 0) { runs[r] = make_int4(0, v.sink, full, rows); mark(r++, rows, v.sink); rows += v.sink; }
     if (v.window > 0) {
-      runs[r++] = make_int4(v.n_tokens - v.window, v.window, full, rows);
+      runs[r] = make_int4(v.n_tokens - v.window, v.window, full, rows);
+      mark(r++, rows, v.window);
       rows += v.window;
     }
     s_runs = r; s_rows = rows; s_apx = 0;
@@ -244,7 +263,10 @@ __global__ void __launch_bounds__(kListThreads) worklist_kernel(dp_cache_view v,
     const int pa = block_exclusive_scan<int>(ma != 0, red, &tot_a);
     const int pl = block_exclusive_scan<int>(len, red, &tot_l);
     const int rb = s_runs, rowb = s_rows, ab = s_apx;
-    if (me) runs[rb + pe] = make_int4(offs[k], len, me, rowb + pl);
+    if (me) {
+      runs[rb + pe] = make_int4(offs[k], len, me, rowb + pl);
+      mark(rb + pe, rowb + pl, len);
+    }
     if (ma) apx[ab + pa] = make_int2(k, ma);
     __syncthreads();
     if (tid == 0) { s_runs = rb + tot_e; s_rows = rowb + tot_l; s_apx = ab + tot_a; }
@@ -506,6 +528,8 @@ size_t decode_ws_layout(const dp_cache_view* v, int G, WorkLists* wl, void** par
   char* runs = take(BH * (cap + 2) * sizeof(int4));
   char* apx = take(BH * cap * sizeof(int2));
   char* cnt = take(BH * 4 * sizeof(int));
+  char* crun = take(BH * max_chunks * sizeof(int));
+  char* ctr = take(BH * sizeof(int));
   const size_t pbytes = BH * max_chunks * G * (2 + (size_t)v->head_dim) * acc;
   char* p = take(pbytes);
   if (wl) {
@@ -517,6 +541,8 @@ size_t decode_ws_layout(const dp_cache_view* v, int G, WorkLists* wl, void** par
     wl->napprox = c + 2 * BH;
     wl->nchunks = c + 3 * BH;
     wl->stats = nullptr;
+    wl->chunk_run = reinterpret_cast<int*>(crun);
+    wl->counters = reinterpret_cast<int*>(ctr);
     wl->max_chunks = max_chunks;
   }
   if (parts) *parts = p;
@@ -536,7 +562,8 @@ Partials<Acc> carve_partials(void* p, size_t BH, int max_chunks, int G, int d) {
 
 cudaError_t launch_score(const dp_cache_view& v, const void* q, int qdt, int G, double scale, double* lm,
                          cudaStream_t st) {
-  const size_t smem = (size_t)G * v.head_dim * 8 + (size_t)kScoreTile * (v.head_dim + 4) * 4;
+  const size_t smem = (size_t)G * v.head_dim * 8 + (size_t)kScoreTile * (v.head_dim + 4) * 4 +
+                      (size_t)G * v.head_dim * 4;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -579,8 +606,9 @@ cudaError_t launch_attn_t(const dp_cache_view& v, const void* q, int qdt, int G,
   dim3 grid((rows + kChunkRows - 1) / kChunkRows, (unsigned)BH);
   cudaError_t e;
   if constexpr (sizeof(T) == 2 && sizeof(Acc) == 4) {
-    if (v.head_dim == 128) {
-      e = launch_attn_tc(v, q, qdt, G, scale, wl, *reinterpret_cast<Partials<float>*>(&pt), kDense, st);
+    if (v.head_dim == 128) {  // tensor-core kernel with the merge fused in (last CTA per head)
+      return launch_attn_tc(v, q, qdt, G, scale, lm, wl, *reinterpret_cast<Partials<float>*>(&pt), out, lse,
+                            kDense, st);
     } else {
       attn_chunk_kernel<T, Acc, kDense><<<grid, kAttnThreads, smem, st>>>(v, q, qdt, G, scale, wl, pt);
       e = cudaGetLastError();

@@ -20,6 +20,8 @@ struct WorkLists {
   int* napprox;   // [BH]  union approx clusters
   int* nchunks;   // [BH]
   int* stats;     // nullable [BH][4]
+  int* chunk_run; // [BH][max_chunks] first run overlapping each row chunk
+  int* counters;  // [BH] chunk-completion counters (zero between launches)
   int max_chunks;
 };
 
@@ -44,8 +46,8 @@ cudaError_t launch_worklist(const dp_cache_view& v, int G, const uint8_t* state,
                             cudaStream_t st);
 cudaError_t launch_attend(const dp_cache_view& v, const void* q, int qdt, int G, double scale, const double* lm,
                           float* out, float* lse, void* ws, bool dense, cudaStream_t st);
-cudaError_t launch_attn_tc(const dp_cache_view& v, const void* q, int qdt, int G, double scale, WorkLists wl,
-                           Partials<float> pt, bool dense, cudaStream_t st);
+cudaError_t launch_attn_tc(const dp_cache_view& v, const void* q, int qdt, int G, double scale, const double* lm,
+                           WorkLists wl, Partials<float> pt, float* out, float* lse, bool dense, cudaStream_t st);
 cudaError_t launch_append(const dp_cache_view& v, const void* nk, const void* nv, cudaStream_t st);
 
 }  // namespace dp

@@ -72,7 +72,7 @@ class DecodeWorkspace:
         self.lse = torch.zeros((B, H * G), dtype=torch.float32, device=dev)
         self.stats = torch.zeros((B, H, 4), dtype=torch.int32, device=dev)
         nbytes = N.lib().dp_decode_workspace_bytes(layer.view(), G)
-        self.ws = torch.empty((max(nbytes, 1),), dtype=torch.uint8, device=dev)
+        self.ws = torch.zeros((max(nbytes, 1),), dtype=torch.uint8, device=dev)  # counters start at 0
 
     @staticmethod
     def _key(layer, G):
@@ -271,7 +271,7 @@ def _sparse_ref(q, cache, cc, plan, layer, kv_head):
     out = torch.zeros((1, 1, lay.head_dim), dtype=torch.float32, device=lay.device)
     lse = torch.zeros((1, 1), dtype=torch.float32, device=lay.device)
     v = lay.view(0, kv_head)
-    ws = torch.empty((N.lib().dp_decode_workspace_bytes(v, 1),), dtype=torch.uint8, device=lay.device)
+    ws = torch.zeros((N.lib().dp_decode_workspace_bytes(v, 1),), dtype=torch.uint8, device=lay.device)
     st = torch.cuda.current_stream(lay.device).cuda_stream
     N.check(N.lib().dp_sparse_attention(v, N.ptr(qd), dtype_code(qd), 1, 1.0 / math.sqrt(lay.head_dim),
                                         N.ptr(bufs.lm), N.ptr(plan._state), N.ptr(out), N.ptr(lse), None,
@@ -319,7 +319,7 @@ def full_attention(q, cache, layer, kv_head, cc=None):
     qd = _head_q(q, lay)
     out = torch.zeros((1, 1, d), dtype=torch.float32, device=dev)
     lse = torch.zeros((1, 1), dtype=torch.float32, device=dev)
-    ws = torch.empty((N.lib().dp_decode_workspace_bytes(v, 1),), dtype=torch.uint8, device=dev)
+    ws = torch.zeros((N.lib().dp_decode_workspace_bytes(v, 1),), dtype=torch.uint8, device=dev)
     N.check(N.lib().dp_dense_attention(v, N.ptr(qd), dtype_code(qd), 1, 1.0 / math.sqrt(d), N.ptr(out),
                                        N.ptr(lse), N.ptr(ws), ws.numel(),
                                        torch.cuda.current_stream(dev).cuda_stream))
