@@ -1,6 +1,8 @@
 // Gathered split-KV decode attention for bf16 caches on tensor cores.
 //
-// One CTA (4 warps) per (row chunk of 128, b*h).  The chunk's rows are the
+// Each CTA (4 warps) owns `cpc` consecutive 128-row chunks of one (b, kv
+// head) and runs an online softmax over them; the next chunk's K rows are
+// fetched while the current chunk's PV runs.  The chunk's rows are the
 // GQA-union rows of the head (sink, window, members of clusters exact for
 // >= 1 q head of the group); cluster runs are contiguous in HBM, so the
 // 16-byte cp.async copies are coalesced.  K then V are staged into padded
@@ -76,25 +78,27 @@ template <bool kDense, bool kQF32>
 __global__ void __launch_bounds__(kTcThreads) attn_tc_kernel(dp_cache_view v, const void* __restrict__ q, int G,
                                                             float scale_log2, const double* __restrict__ lm,
                                                             WorkLists wl, Partials<float> pt, float* __restrict__ out,
-                                                            float* __restrict__ lse) {
+                                                            float* __restrict__ lse, int cpc) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gq = lane >> 2, tq = lane & 3;
   const int BH = v.batch * v.kv_heads;
   const int w = blockIdx.x;
-  __shared__ int s_bh, s_c, s_nch, s_last;
+  constexpr int d = 128;
+  __shared__ int s_bh, s_cta, s_ncta, s_last;
   __shared__ int4 sruns[kTcRows];
-  // ---- compact work index -> (head, chunk): active chunks are the first CTAs
+  __shared__ float red_m[32], red_l[32];
+  // ---- compact work index -> (head, CTA of that head) ---------------------
   if (kDense) {
-    const int per = (v.n_tokens + kTcRows - 1) / kTcRows;
+    const int per = ((v.n_tokens + kTcRows - 1) / kTcRows + cpc - 1) / cpc;
     if (tid == 0) {
       s_bh = w / per < BH ? w / per : -1;
-      s_c = w % per;
-      s_nch = per;
+      s_cta = w % per;
+      s_ncta = per;
     }
   } else if (warp == 0) {
     int base = 0, found = 0;
     for (int b0 = 0; b0 < BH && !found; b0 += 32) {
-      const int n = b0 + lane < BH ? wl.nchunks[b0 + lane] : 0;
+      const int n = b0 + lane < BH ? (wl.nchunks[b0 + lane] + cpc - 1) / cpc : 0;
       int inc = n;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -105,8 +109,8 @@ __global__ void __launch_bounds__(kTcThreads) attn_tc_kernel(dp_cache_view v, co
       const unsigned bal = __ballot_sync(0xffffffffu, hit);
       if (hit) {
         s_bh = b0 + lane;
-        s_c = w - (base + inc - n);
-        s_nch = n;
+        s_cta = w - (base + inc - n);
+        s_ncta = n;
       }
       found = bal != 0;
       base += __shfl_sync(0xffffffffu, inc, 31);
@@ -114,11 +118,11 @@ __global__ void __launch_bounds__(kTcThreads) attn_tc_kernel(dp_cache_view v, co
     if (!found && lane == 0) s_bh = -1;
   }
   __syncthreads();
-  const int bh = s_bh, c = s_c, nchunk = s_nch;
+  const int bh = s_bh, cta = s_cta, ncta = s_ncta;
   if (bh < 0) return;
   const int rows_total = kDense ? v.n_tokens : wl.nrows[bh];
-  const int v0 = c * kTcRows;
-  const int nr = min(kTcRows, rows_total - v0);
+  const int nch_head = (rows_total + kTcRows - 1) / kTcRows;
+  const int c_begin = cta * cpc, c_end = min(c_begin + cpc, nch_head);
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __nv_bfloat16* Ks = reinterpret_cast<__nv_bfloat16*>(smem_raw);
@@ -126,45 +130,44 @@ __global__ void __launch_bounds__(kTcThreads) attn_tc_kernel(dp_cache_view v, co
   float* Ps = reinterpret_cast<float*>(Vs + kTcRows * kRowStride);  // [8][kTcRows]
   int* rmask = reinterpret_cast<int*>(Ps + 8 * kTcRows);            // [kTcRows]
   int* rphys = rmask + kTcRows;                                     // [kTcRows]
-  float* red = reinterpret_cast<float*>(rphys + kTcRows);           // [4][8] max, [4][8] sum
 
-  // ---- row -> physical row + head mask: the chunk's runs staged in smem ---
-  int phys = -1, mask = 0;
-  if (kDense) {
-    if (tid < nr) {
-      phys = v0 + tid;
-      mask = (1 << G) - 1;
-    }
-  } else {
-    const int r0 = wl.chunk_run[(size_t)bh * wl.max_chunks + c];
-    const int nrun = min(wl.nruns[bh] - r0, nr);
-    if (tid < nrun) sruns[tid] = wl.runs[(size_t)bh * (v.cluster_cap + 2) + r0 + tid];
-    __syncthreads();
-    if (tid < nr) {
-      const int vr = v0 + tid;
-      int lo = 0, hi = nrun - 1;
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (sruns[mid].w <= vr) lo = mid; else hi = mid - 1;
-      }
-      const int4 ru = sruns[lo];
-      phys = ru.x + (vr - ru.w);
-      mask = ru.z;
-    }
-  }
-  rmask[tid] = mask;
-  rphys[tid] = phys;
-  __syncthreads();
-  // ---- stage K (group 0) and V (group 1): a warp copies 2 rows = 512
-  // contiguous bytes per instruction (rows of a run are adjacent in HBM)
-  const int d = 128;
   const size_t head_off = (size_t)bh * v.row_cap * d;
   const __nv_bfloat16* Kg = reinterpret_cast<const __nv_bfloat16*>(v.keys) + head_off;
   const __nv_bfloat16* Vg = reinterpret_cast<const __nv_bfloat16*>(v.values) + head_off;
-#pragma unroll
-  for (int pass = 0; pass < 2; ++pass) {
-    const __nv_bfloat16* G0 = pass == 0 ? Kg : Vg;
-    __nv_bfloat16* S0 = pass == 0 ? Ks : Vs;
+
+  // rows of chunk c -> (physical row, head mask) in smem; ends with a barrier
+  auto map_rows = [&](int c) {
+    const int v0 = c * kTcRows;
+    const int nr = min(kTcRows, rows_total - v0);
+    int phys = -1, mask = 0;
+    if (kDense) {
+      if (tid < nr) {
+        phys = v0 + tid;
+        mask = (1 << G) - 1;
+      }
+    } else {
+      const int r0 = wl.chunk_run[(size_t)bh * wl.max_chunks + c];
+      const int nrun = min(wl.nruns[bh] - r0, nr);
+      if (tid < nrun) sruns[tid] = wl.runs[(size_t)bh * (v.cluster_cap + 2) + r0 + tid];
+      __syncthreads();
+      if (tid < nr) {
+        const int vr = v0 + tid;
+        int lo = 0, hi = nrun - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (sruns[mid].w <= vr) lo = mid; else hi = mid - 1;
+        }
+        const int4 ru = sruns[lo];
+        phys = ru.x + (vr - ru.w);
+        mask = ru.z;
+      }
+    }
+    rmask[tid] = mask;
+    rphys[tid] = phys;
+    __syncthreads();
+  };
+  // a warp copies 2 rows = 512 contiguous bytes per instruction
+  auto issue = [&](const __nv_bfloat16* G0, __nv_bfloat16* S0) {
 #pragma unroll 4
     for (int i = 0; i < 16; ++i) {
       const int idx = i * kTcThreads + tid;
@@ -175,7 +178,11 @@ __global__ void __launch_bounds__(kTcThreads) attn_tc_kernel(dp_cache_view v, co
       else *reinterpret_cast<int4*>(dst) = make_int4(0, 0, 0, 0);
     }
     asm volatile("cp.async.commit_group;\n" ::);
-  }
+  };
+
+  map_rows(c_begin);
+  issue(Kg, Ks);
+  issue(Vg, Vs);
 
   // ---- Q fragments (registers): a0 = Q[g][k*16 + 2t..], a2 = Q[g][k*16 + 8 + 2t..]
   unsigned qa[8][2], qb[8][2];  // hi, lo
@@ -200,119 +207,144 @@ __global__ void __launch_bounds__(kTcThreads) attn_tc_kernel(dp_cache_view v, co
       }
     }
   }
-  asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-  __syncthreads();
 
-  // ---- S^T = Q K^T for this warp's 32 rows ------------------------------
-  float s[4][4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j)
-#pragma unroll
-    for (int e = 0; e < 4; ++e) s[j][e] = 0.f;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int rbase = warp * 32 + j * 8;
-    const unsigned base = smem_u32(Ks + (rbase + (lane & 7)) * kRowStride + (lane >> 3) * 8);
-#pragma unroll
-    for (int kk = 0; kk < 8; kk += 2) {
-      unsigned b0, b1, b2, b3;
-      ldsm_x4(base + kk * 32, b0, b1, b2, b3);
-      mma_bf16(s[j], qa[kk][0], qa[kk][1], b0, b1);
-      mma_bf16(s[j], qa[kk + 1][0], qa[kk + 1][1], b2, b3);
-      if (kQF32) {
-        mma_bf16(s[j], qb[kk][0], qb[kk][1], b0, b1);
-        mma_bf16(s[j], qb[kk + 1][0], qb[kk + 1][1], b2, b3);
-      }
-    }
-  }
-  // scale (log2 domain) + head mask; lane holds head gq, rows warp*32 + j*8 + 2tq + {0,1}
-  float mx = -INFINITY;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int r = warp * 32 + j * 8 + 2 * tq + e;
-      const bool ok = gq < G && ((rmask[r] >> gq) & 1);
-      const float val = ok ? s[j][e] * scale_log2 : -INFINITY;
-      s[j][e] = val;
-      mx = fmaxf(mx, val);
-    }
-  }
-  mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-  mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-  if (tq == 0 && gq < 8) red[warp * 8 + gq] = mx;
-  __syncthreads();
-  float m = -INFINITY;
-  if (gq < 8) {
-#pragma unroll
-    for (int w = 0; w < 4; ++w) m = fmaxf(m, red[w * 8 + gq]);
-  }
-  float lsum = 0.f;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const float p = (m == -INFINITY || s[j][e] == -INFINITY) ? 0.f : exp2f(s[j][e] - m);
-      lsum += p;
-      if (gq < 8) Ps[gq * kTcRows + warp * 32 + j * 8 + 2 * tq + e] = p;
-    }
-  }
-  lsum += __shfl_xor_sync(0xffffffffu, lsum, 1);
-  lsum += __shfl_xor_sync(0xffffffffu, lsum, 2);
-  if (tq == 0 && gq < 8) red[32 + warp * 8 + gq] = lsum;
-  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-  __syncthreads();
-  if (tid < G) {
-    float l = 0.f;
-#pragma unroll
-    for (int w = 0; w < 4; ++w) l += red[32 + w * 8 + tid];
-    const size_t pi = ((size_t)bh * pt.max_chunks + c) * G + tid;
-    float mm = -INFINITY;
-#pragma unroll
-    for (int w = 0; w < 4; ++w) mm = fmaxf(mm, red[w * 8 + tid]);
-    pt.m[pi] = mm == -INFINITY ? -INFINITY : mm * 0.69314718055994531f;  // back to natural log
-    pt.l[pi] = l;
-  }
-
-  // ---- O = P V for this warp's 32 head-dim columns ------------------------
   float o[4][4];
 #pragma unroll
   for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
     for (int e = 0; e < 4; ++e) o[nt][e] = 0.f;
   const int n0 = warp * 32;
-#pragma unroll 2
-  for (int ks = 0; ks < kTcRows / 16; ++ks) {
-    unsigned ah0 = 0u, al0 = 0u, ah2 = 0u, al2 = 0u;
-    if (gq < G) {
-      const float2 p0 = *reinterpret_cast<const float2*>(Ps + gq * kTcRows + ks * 16 + 2 * tq);
-      const float2 p2 = *reinterpret_cast<const float2*>(Ps + gq * kTcRows + ks * 16 + 8 + 2 * tq);
-      split2(p0.x, p0.y, ah0, al0);
-      split2(p2.x, p2.y, ah2, al2);
-    }
-    const int vrow = ks * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+  float m_run = -INFINITY;                 // running max (log2 domain) of head gq
+  float m_t = -INFINITY, l_t = 0.f;        // running max / sum of head `tid` (tid < G)
+
+  for (int c = c_begin; c < c_end; ++c) {
+    const bool has_next = c + 1 < c_end;
+    asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // K_c landed (V_c may still stream)
+    __syncthreads();
+    // ---- S^T = Q K^T for this warp's 32 rows ----------------------------
+    float s[4][4];
 #pragma unroll
-    for (int np = 0; np < 2; ++np) {
-      const unsigned addr = smem_u32(Vs + vrow * kRowStride + n0 + np * 16 + (lane >> 4) * 8);
-      unsigned b0, b1, b2, b3;
-      ldsm_x4_t(addr, b0, b1, b2, b3);
-      mma_bf16(o[2 * np], ah0, ah2, b0, b1);
-      mma_bf16(o[2 * np], al0, al2, b0, b1);
-      mma_bf16(o[2 * np + 1], ah0, ah2, b2, b3);
-      mma_bf16(o[2 * np + 1], al0, al2, b2, b3);
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) s[j][e] = 0.f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int rbase = warp * 32 + j * 8;
+      const unsigned base = smem_u32(Ks + (rbase + (lane & 7)) * kRowStride + (lane >> 3) * 8);
+#pragma unroll
+      for (int kk = 0; kk < 8; kk += 2) {
+        unsigned b0, b1, b2, b3;
+        ldsm_x4(base + kk * 32, b0, b1, b2, b3);
+        mma_bf16(s[j], qa[kk][0], qa[kk][1], b0, b1);
+        mma_bf16(s[j], qa[kk + 1][0], qa[kk + 1][1], b2, b3);
+        if (kQF32) {
+          mma_bf16(s[j], qb[kk][0], qb[kk][1], b0, b1);
+          mma_bf16(s[j], qb[kk + 1][0], qb[kk + 1][1], b2, b3);
+        }
+      }
     }
+    float mx = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int r = warp * 32 + j * 8 + 2 * tq + e;
+        const bool ok = gq < G && ((rmask[r] >> gq) & 1);
+        const float val = ok ? s[j][e] * scale_log2 : -INFINITY;
+        s[j][e] = val;
+        mx = fmaxf(mx, val);
+      }
+    }
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+    if (tq == 0) red_m[warp * 8 + gq] = mx;
+    __syncthreads();  // Ks, rmask free; chunk maxima visible
+    float cm = -INFINITY;
+#pragma unroll
+    for (int ww = 0; ww < 4; ++ww) cm = fmaxf(cm, red_m[ww * 8 + gq]);
+    const float m_new = fmaxf(m_run, cm);
+    const float alpha = m_new == -INFINITY ? 1.f : exp2f(m_run - m_new);
+    m_run = m_new;
+    float lsum = 0.f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const float pv = (s[j][e] == -INFINITY) ? 0.f : exp2f(s[j][e] - m_new);
+        lsum += pv;
+        Ps[gq * kTcRows + warp * 32 + j * 8 + 2 * tq + e] = pv;
+      }
+    }
+    lsum += __shfl_xor_sync(0xffffffffu, lsum, 1);
+    lsum += __shfl_xor_sync(0xffffffffu, lsum, 2);
+    if (tq == 0) red_l[warp * 8 + gq] = lsum;
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      o[nt][0] *= alpha;
+      o[nt][1] *= alpha;
+    }
+    if (tid < G) {  // running (m, l) of head tid
+      float cmt = -INFINITY;
+#pragma unroll
+      for (int ww = 0; ww < 4; ++ww) cmt = fmaxf(cmt, red_m[ww * 8 + tid]);
+      const float mtn = fmaxf(m_t, cmt);
+      l_t *= (mtn == -INFINITY ? 1.f : exp2f(m_t - mtn));
+      m_t = mtn;
+    }
+    if (has_next) {  // prefetch the next chunk's K while PV runs
+      map_rows(c + 1);
+      issue(Kg, Ks);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // V_c landed
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
+    __syncthreads();  // Ps / red_l / V_c visible
+    if (tid < G) {
+#pragma unroll
+      for (int ww = 0; ww < 4; ++ww) l_t += red_l[ww * 8 + tid];
+    }
+    // ---- O += P V for this warp's 32 head-dim columns ---------------------
+#pragma unroll 2
+    for (int ks = 0; ks < kTcRows / 16; ++ks) {
+      unsigned ah0 = 0u, al0 = 0u, ah2 = 0u, al2 = 0u;
+      if (gq < G) {
+        const float2 p0 = *reinterpret_cast<const float2*>(Ps + gq * kTcRows + ks * 16 + 2 * tq);
+        const float2 p2 = *reinterpret_cast<const float2*>(Ps + gq * kTcRows + ks * 16 + 8 + 2 * tq);
+        split2(p0.x, p0.y, ah0, al0);
+        split2(p2.x, p2.y, ah2, al2);
+      }
+      const int vrow = ks * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+#pragma unroll
+      for (int np = 0; np < 2; ++np) {
+        const unsigned addr = smem_u32(Vs + vrow * kRowStride + n0 + np * 16 + (lane >> 4) * 8);
+        unsigned b0, b1, b2, b3;
+        ldsm_x4_t(addr, b0, b1, b2, b3);
+        mma_bf16(o[2 * np], ah0, ah2, b0, b1);
+        mma_bf16(o[2 * np], al0, al2, b0, b1);
+        mma_bf16(o[2 * np + 1], ah0, ah2, b2, b3);
+        mma_bf16(o[2 * np + 1], al0, al2, b2, b3);
+      }
+    }
+    __syncthreads();  // Vs, Ps consumed
+    if (has_next) issue(Vg, Vs);
+  }
+
+  // ---- this CTA's partial (m natural-log, l, o) ---------------------------
+  const size_t pbase = (size_t)bh * pt.max_chunks * G;
+  if (tid < G) {
+    pt.m[pbase + (size_t)cta * G + tid] = m_t == -INFINITY ? -INFINITY : m_t * 0.69314718055994531f;
+    pt.l[pbase + (size_t)cta * G + tid] = l_t;
   }
   if (gq < G) {
-    float* dst = pt.o + (((size_t)bh * pt.max_chunks + c) * G + gq) * d + n0 + 2 * tq;
+    float* dst = pt.o + (pbase + (size_t)cta * G + gq) * d + n0 + 2 * tq;
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt) *reinterpret_cast<float2*>(dst + nt * 8) = make_float2(o[nt][0], o[nt][1]);
   }
 
-  // ---- fused LSE merge: the last chunk of this head folds every partial
-  // together with the approx pseudo-rows (engine.py:231-246) -------------
+  // ---- fused LSE merge by the last CTA of this head (engine.py:231-246) --
   __threadfence();
   __syncthreads();
-  if (tid == 0) s_last = atomicAdd(&wl.counters[bh], 1) == nchunk - 1;
+  if (tid == 0) s_last = atomicAdd(&wl.counters[bh], 1) == ncta - 1;
   __syncthreads();
   if (!s_last) return;
   __threadfence();
@@ -320,19 +352,18 @@ __global__ void __launch_bounds__(kTcThreads) attn_tc_kernel(dp_cache_view v, co
   const int na = kDense ? 0 : wl.napprox[bh];
   const int2* apx = wl.approx + (size_t)bh * v.cluster_cap;
   const float* vbar = v.value_means + (size_t)bh * v.cluster_cap * d;
-  const size_t pbase = (size_t)bh * pt.max_chunks * G;
   for (int g = warp; g < G; g += kTcThreads / 32) {
     const int hq = bh * G + g;
     const double* lmh = kDense ? nullptr : lm + (size_t)hq * v.cluster_cap;
     float mloc = -INFINITY;
-    for (int cc = lane; cc < nchunk; cc += 32) mloc = fmaxf(mloc, __ldcg(&pt.m[pbase + (size_t)cc * G + g]));
+    for (int cc = lane; cc < ncta; cc += 32) mloc = fmaxf(mloc, __ldcg(&pt.m[pbase + (size_t)cc * G + g]));
     for (int a = lane; a < na; a += 32) {
       const int2 e = apx[a];
       if ((e.y >> g) & 1) mloc = fmaxf(mloc, (float)lmh[e.x]);
     }
     const float M = warp_max(mloc);
     float lloc = 0.f;
-    for (int cc = lane; cc < nchunk; cc += 32) {
+    for (int cc = lane; cc < ncta; cc += 32) {
       const float mc = __ldcg(&pt.m[pbase + (size_t)cc * G + g]);
       if (mc != -INFINITY) lloc += __ldcg(&pt.l[pbase + (size_t)cc * G + g]) * __expf(mc - M);
     }
@@ -343,44 +374,68 @@ __global__ void __launch_bounds__(kTcThreads) attn_tc_kernel(dp_cache_view v, co
     const float L = warp_sum(lloc);
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 4
-    for (int cc = 0; cc < nchunk; ++cc) {
+    for (int cc = 0; cc < ncta; ++cc) {
       const float mc = __ldcg(&pt.m[pbase + (size_t)cc * G + g]);
       const float4 oc = __ldcg(reinterpret_cast<const float4*>(pt.o + (pbase + (size_t)cc * G + g) * d) + lane);
       const float wgt = mc == -INFINITY ? 0.f : __expf(mc - M);
       acc.x += wgt * oc.x; acc.y += wgt * oc.y; acc.z += wgt * oc.z; acc.w += wgt * oc.w;
     }
+    // approx pseudo-rows: lanes fetch (cluster, weight) 32 at a time, then the
+    // warp streams the value-mean rows with the weights broadcast by shuffle
+    for (int a0 = 0; a0 < na; a0 += 32) {
+      int k = 0;
+      float wgt = 0.f;
+      if (a0 + lane < na) {
+        const int2 e = apx[a0 + lane];
+        k = e.x;
+        if ((e.y >> g) & 1) wgt = __expf((float)lmh[e.x] - M);
+      }
+      const int nb = min(32, na - a0);
 #pragma unroll 4
-    for (int a = 0; a < na; ++a) {
-      const int2 e = apx[a];
-      if ((e.y >> g) & 1) {
-        const float wgt = __expf((float)lmh[e.x] - M);
-        const float4 vb = *(reinterpret_cast<const float4*>(vbar + (size_t)e.x * d) + lane);
-        acc.x += wgt * vb.x; acc.y += wgt * vb.y; acc.z += wgt * vb.z; acc.w += wgt * vb.w;
+      for (int b = 0; b < nb; ++b) {
+        const float wb = __shfl_sync(0xffffffffu, wgt, b);
+        const int kb = __shfl_sync(0xffffffffu, k, b);
+        if (wb != 0.f) {
+          const float4 vb = *(reinterpret_cast<const float4*>(vbar + (size_t)kb * d) + lane);
+          acc.x += wb * vb.x; acc.y += wb * vb.y; acc.z += wb * vb.z; acc.w += wb * vb.w;
+        }
       }
     }
     const float inv = 1.f / L;
-    reinterpret_cast<float4*>(out + (size_t)hq * d)[lane] = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+    reinterpret_cast<float4*>(out + (size_t)hq * d)[lane] =
+        make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
     if (lane == 0) lse[hq] = M + __logf(L);
   }
 }
 
 size_t attn_tc_smem_bytes() {
-  return (size_t)2 * kTcRows * kRowStride * 2 + 8 * kTcRows * 4 + 2 * kTcRows * 4 + 64 * 4;
+  return (size_t)2 * kTcRows * kRowStride * 2 + 8 * kTcRows * 4 + 2 * kTcRows * 4;
 }
 
 template <bool kDense, bool kQF32>
 static cudaError_t launch_tc_t(const dp_cache_view& v, const void* q, int G, double scale, const double* lm,
                                WorkLists wl, Partials<float> pt, float* out, float* lse, cudaStream_t st) {
   static bool attr = false;
+  static int sms = 148;
   if (!attr) {
     cudaFuncSetAttribute(attn_tc_kernel<kDense, kQF32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)attn_tc_smem_bytes());
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     attr = true;
   }
+  const int BH = v.batch * v.kv_heads;
   const int rows = kDense ? v.n_tokens : v.row_cap;
-  const int grid = ((rows + kTcRows - 1) / kTcRows) * v.batch * v.kv_heads;  // upper bound; extra CTAs exit
+  const int max_chunks = (rows + kTcRows - 1) / kTcRows;
+  // chunks per CTA: aim for ~3 resident CTAs per SM over the expected work
+  // (dense: every row; sparse: ~40% GQA-union rows, SURVEY.md §0 finding 4)
+  const double expect = (double)BH * max_chunks * (kDense ? 1.0 : 0.4);
+  int cpc = (int)(expect / (3.0 * sms) + 0.5);
+  cpc = cpc < 1 ? 1 : (cpc > 16 ? 16 : cpc);
+  const int grid = BH * ((max_chunks + cpc - 1) / cpc);  // upper bound; extra CTAs exit
   attn_tc_kernel<kDense, kQF32><<<grid, kTcThreads, attn_tc_smem_bytes(), st>>>(
-      v, q, G, (float)(scale * 1.4426950408889634), lm, wl, pt, out, lse);
+      v, q, G, (float)(scale * 1.4426950408889634), lm, wl, pt, out, lse, cpc);
   return cudaGetLastError();
 }
 
