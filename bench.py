@@ -310,21 +310,16 @@ def run_b200(a):
         cs = torch.cuda.current_stream(dev).cuda_stream
         if ev is not None:
             ev[0].record()
-        N.check(lib.dp_score(v, N.ptr(q), dtype_code(q), G, scale, N.ptr(ws.log_mass), cs))
+        # fused plan: score + two-stage top-p + GQA-union work list (one launch)
+        N.check(lib.dp_plan(v, N.ptr(q), dtype_code(q), G, scale, a.p1, a.p2, N.ptr(ws.log_mass), None,
+                            N.ptr(ws.counts), N.ptr(ws.stats if stats is None else stats), N.ptr(ws.ws),
+                            ws.ws.numel(), cs))
         if ev is not None:
             ev[1].record()
-        N.check(lib.dp_select(v, G, a.p1, a.p2, N.ptr(ws.log_mass), N.ptr(ws.state), N.ptr(ws.counts), None,
-                              None, None, N.ptr(ws.ws), ws.ws.numel(), cs))
-        if ev is not None:
-            ev[2].record()
-        N.check(lib.dp_build_worklist(v, G, N.ptr(ws.state), N.ptr(ws.stats if stats is None else stats),
-                                      N.ptr(ws.ws), ws.ws.numel(), cs))
-        if ev is not None:
-            ev[3].record()
         N.check(lib.dp_attend(v, N.ptr(q), dtype_code(q), G, scale, N.ptr(ws.log_mass), N.ptr(ws.out),
                               N.ptr(ws.lse), N.ptr(ws.ws), ws.ws.numel(), cs))
         if ev is not None:
-            ev[4].record()
+            ev[2].record()
 
     def dense_step(li, s):
         lay, ws, v = layers[li], wss[li], views[li]
@@ -335,7 +330,7 @@ def run_b200(a):
     # ---- stage timing + algorithmic bytes (eager, CUDA events) -----------
     nstage = min(a.qsteps, 4)
     stats_all = torch.zeros((nstage, L, B, hl, 4), dtype=torch.int32, device=dev)
-    evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(L)] for _ in range(nstage)]
+    evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(L)] for _ in range(nstage)]
     for s in range(nstage):  # warm
         for li in range(L):
             layer_step(li, s, stats_all[s, li])
@@ -347,11 +342,11 @@ def run_b200(a):
         for li in range(L):
             layer_step(li, s, stats_all[s, li], evs[s][li])
     torch.cuda.synchronize(dev)
-    stage_ms = np.zeros(4)
+    stage_ms = np.zeros(2)
     for s in range(nstage):
         for li in range(L):
             e = evs[s][li]
-            for j in range(4):
+            for j in range(2):
                 stage_ms[j] += e[j].elapsed_time(e[j + 1])
     stage_ms /= nstage * L  # per layer
     stats_np = stats_all.cpu().numpy().astype(np.int64)  # [S,L,B,hl,4]
@@ -365,7 +360,7 @@ def run_b200(a):
     score_bytes = (ncl * d * 4 + ncl * 4).sum(axis=(1, 2))  # [L]
     step_bytes = float((attend_bytes + score_bytes).sum())  # all layers, one step
     dense_bytes = float(L * (B * hl * a.context * 2 * d * s_kv + qo))
-    attend_ms = stage_ms[3]
+    attend_ms = stage_ms[1]
     attend_gbs = float(attend_bytes.mean() / (attend_ms * 1e-3) / 1e9)
     union_frac = float(U.mean() / a.context)
 
@@ -473,7 +468,7 @@ def run_b200(a):
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
-    launches = a.steps * L * 4  # score, select, worklist, attn_tc (merge fused)
+    launches = a.steps * L * 2  # plan_kernel (score+select+worklist), attn_tc_kernel (+ fused merge)
     if rank == 0:
         line = {
             "metric": "decode_us_per_step", "value": ms * 1e3, "unit": "us/step", "n_gpus": world,
@@ -490,8 +485,7 @@ def run_b200(a):
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clocks,
-            "stage_us_per_layer": {"score": stage_ms[0] * 1e3, "select": stage_ms[1] * 1e3,
-                                   "worklist": stage_ms[2] * 1e3, "attend": stage_ms[3] * 1e3},
+            "stage_us_per_layer": {"plan": stage_ms[0] * 1e3, "attend": stage_ms[1] * 1e3},
             "step_algorithmic_bytes": step_bytes,
             "step_roofline_frac": step_bytes / (ms * 1e-3) / 1e9 / hbm_peak,
             "union_exact_rows_frac": union_frac,

@@ -127,8 +127,20 @@ int dp_attend(const dp_cache_view* v, const void* q, int32_t q_dtype, int32_t gq
               double scale, const double* log_mass, float* out, float* lse, void* workspace,
               size_t workspace_bytes, void* stream);
 
+/* score + select + worklist fused into ONE launch (one 8-CTA thread-block
+ * cluster per (sequence, kv head), stages exchange data over distributed
+ * shared memory): writes log_mass, counts, state (nullable) and the
+ * workspace work lists that dp_attend consumes.  Needs cluster_cap <= 4096
+ * (contexts up to ~128K at 32 tokens per cluster) and gqa_group <= 8;
+ * stats as in dp_sparse_attention (slot 3 = union exact clusters). */
+int dp_plan(const dp_cache_view* v, const void* q, int32_t q_dtype, int32_t gqa_group,
+            double scale, double p1, double p2, double* log_mass, uint8_t* state,
+            int32_t* counts, int32_t* stats, void* workspace, size_t workspace_bytes,
+            void* stream);
+
 /* score + select + sparse attention in one call (decode_step,
- * engine.py:267-278).  log_mass/state/counts are caller buffers so the plan
+ * engine.py:267-278): dp_plan + dp_attend when supported, else the separate
+ * dp_score / dp_select / dp_sparse_attention kernels.  log_mass/state/counts are caller buffers so the plan
  * stays inspectable. */
 int dp_decode_step(const dp_cache_view* v, const void* q, int32_t q_dtype, int32_t gqa_group,
                    double scale, double p1, double p2, double* log_mass, uint8_t* state,

@@ -85,7 +85,6 @@ __global__ void __launch_bounds__(kTcThreads) attn_tc_kernel(dp_cache_view v, co
   const int w = blockIdx.x;
   constexpr int d = 128;
   __shared__ int s_bh, s_cta, s_ncta, s_last;
-  __shared__ int4 sruns[kTcRows];
   __shared__ float red_m[32], red_l[32];
   // ---- compact work index -> (head, CTA of that head) ---------------------
   if (kDense) {
@@ -146,20 +145,10 @@ __global__ void __launch_bounds__(kTcThreads) attn_tc_kernel(dp_cache_view v, co
         mask = (1 << G) - 1;
       }
     } else {
-      const int r0 = wl.chunk_run[(size_t)bh * wl.max_chunks + c];
-      const int nrun = min(wl.nruns[bh] - r0, nr);
-      if (tid < nrun) sruns[tid] = wl.runs[(size_t)bh * (v.cluster_cap + 2) + r0 + tid];
-      __syncthreads();
       if (tid < nr) {
-        const int vr = v0 + tid;
-        int lo = 0, hi = nrun - 1;
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (sruns[mid].w <= vr) lo = mid; else hi = mid - 1;
-        }
-        const int4 ru = sruns[lo];
-        phys = ru.x + (vr - ru.w);
-        mask = ru.z;
+        const unsigned e = __ldg(reinterpret_cast<const unsigned*>(wl.rowidx) + (size_t)bh * v.row_cap + v0 + tid);
+        phys = (int)(e & 0xFFFFFFu);
+        mask = (int)(e >> 24);
       }
     }
     rmask[tid] = mask;

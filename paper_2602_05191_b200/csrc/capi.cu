@@ -118,10 +118,31 @@ int dp_sparse_attention(const dp_cache_view* v, const void* q, int32_t q_dtype, 
   return dp_attend(v, q, q_dtype, G, scale, log_mass, out, lse, ws, ws_bytes, stream);
 }
 
+int dp_plan(const dp_cache_view* v, const void* q, int32_t q_dtype, int32_t G, double scale, double p1, double p2,
+            double* log_mass, uint8_t* state, int32_t* counts, int32_t* stats, void* ws, size_t ws_bytes,
+            void* stream) {
+  int r = check_view(v, G);
+  if (r) return r;
+  if ((r = check_q(q_dtype)) || (r = check_p(p1, "p1")) || (r = check_p(p2, "p2"))) return r;
+  if (ws_bytes < dp_decode_workspace_bytes(v, G)) return fail(DP_ERR_INVALID, "workspace too small");
+  if (!dp::plan_supported(*v, G))
+    return fail(DP_ERR_UNSUPPORTED, "fused plan needs cluster_cap <= 4096 and row_cap < 2^24");
+  cudaError_t e = dp::launch_plan(*v, q, q_dtype, G, scale, p1, p2, log_mass, state, counts, stats, ws,
+                                  (cudaStream_t)stream);
+  return e == cudaSuccess ? DP_OK : cuda_fail(e, "dp_plan");
+}
+
 int dp_decode_step(const dp_cache_view* v, const void* q, int32_t q_dtype, int32_t G, double scale, double p1,
                    double p2, double* log_mass, uint8_t* state, int32_t* counts, float* out, float* lse,
                    int32_t* stats, void* ws, size_t ws_bytes, void* stream) {
-  int r = dp_score(v, q, q_dtype, G, scale, log_mass, stream);
+  int r = check_view(v, G);
+  if (r) return r;
+  if (dp::plan_supported(*v, G)) {  // fused score + select + worklist (one launch) -> attend
+    r = dp_plan(v, q, q_dtype, G, scale, p1, p2, log_mass, state, counts, stats, ws, ws_bytes, stream);
+    if (r) return r;
+    return dp_attend(v, q, q_dtype, G, scale, log_mass, out, lse, ws, ws_bytes, stream);
+  }
+  r = dp_score(v, q, q_dtype, G, scale, log_mass, stream);
   if (r) return r;
   r = dp_select(v, G, p1, p2, log_mass, state, counts, nullptr, nullptr, nullptr, ws, ws_bytes, stream);
   if (r) return r;

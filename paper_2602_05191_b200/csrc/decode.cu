@@ -231,17 +231,16 @@ __global__ void __launch_bounds__(kListThreads) worklist_kernel(dp_cache_view v,
   __shared__ int red[33];
   __shared__ int s_runs, s_rows, s_apx;
   const int full = (1 << G) - 1;
-  int* crun = wl.chunk_run + (size_t)bh * wl.max_chunks;
-  // every chunk start c*R inside [prefix, prefix+len) gets this run's index
-  auto mark = [&](int r, int prefix, int len) {
-    for (int c = (prefix + kChunkRows - 1) / kChunkRows; c * kChunkRows < prefix + len; ++c) crun[c] = r;
-  };
+  unsigned* rowidx = reinterpret_cast<unsigned*>(wl.rowidx) + (size_t)bh * v.row_cap;
+  const unsigned ftag = (unsigned)full << 24;
+  // packed union rows: (head mask << 24) | physical row
+  for (int t = tid; t < v.sink; t += blockDim.x) rowidx[t] = ftag | (unsigned)t;
+  for (int t = tid; t < v.window; t += blockDim.x) rowidx[v.sink + t] = ftag | (unsigned)(v.n_tokens - v.window + t);
   if (tid == 0) {
     int r = 0, rows = 0;
-    if (v.sink > 0) { runs[r] = make_int4(0, v.sink, full, rows); mark(r++, rows, v.sink); rows += v.sink; }
+    if (v.sink > 0) { runs[r++] = make_int4(0, v.sink, full, rows); rows += v.sink; }
     if (v.window > 0) {
-      runs[r] = make_int4(v.n_tokens - v.window, v.window, full, rows);
-      mark(r++, rows, v.window);
+      runs[r++] = make_int4(v.n_tokens - v.window, v.window, full, rows);
       rows += v.window;
     }
     s_runs = r; s_rows = rows; s_apx = 0;
@@ -265,7 +264,8 @@ __global__ void __launch_bounds__(kListThreads) worklist_kernel(dp_cache_view v,
     const int rb = s_runs, rowb = s_rows, ab = s_apx;
     if (me) {
       runs[rb + pe] = make_int4(offs[k], len, me, rowb + pl);
-      mark(rb + pe, rowb + pl, len);
+      const unsigned tag = (unsigned)me << 24;
+      for (int t = 0; t < len; ++t) rowidx[rowb + pl + t] = tag | (unsigned)(offs[k] + t);
     }
     if (ma) apx[ab + pa] = make_int2(k, ma);
     __syncthreads();
@@ -528,7 +528,7 @@ size_t decode_ws_layout(const dp_cache_view* v, int G, WorkLists* wl, void** par
   char* runs = take(BH * (cap + 2) * sizeof(int4));
   char* apx = take(BH * cap * sizeof(int2));
   char* cnt = take(BH * 4 * sizeof(int));
-  char* crun = take(BH * max_chunks * sizeof(int));
+  char* crun = take(BH * (size_t)v->row_cap * sizeof(int));
   char* ctr = take(BH * sizeof(int));
   const size_t pbytes = BH * max_chunks * G * (2 + (size_t)v->head_dim) * acc;
   char* p = take(pbytes);
@@ -541,7 +541,7 @@ size_t decode_ws_layout(const dp_cache_view* v, int G, WorkLists* wl, void** par
     wl->napprox = c + 2 * BH;
     wl->nchunks = c + 3 * BH;
     wl->stats = nullptr;
-    wl->chunk_run = reinterpret_cast<int*>(crun);
+    wl->rowidx = reinterpret_cast<int*>(crun);
     wl->counters = reinterpret_cast<int*>(ctr);
     wl->max_chunks = max_chunks;
   }

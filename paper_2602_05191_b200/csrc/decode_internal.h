@@ -20,7 +20,7 @@ struct WorkLists {
   int* napprox;   // [BH]  union approx clusters
   int* nchunks;   // [BH]
   int* stats;     // nullable [BH][4]
-  int* chunk_run; // [BH][max_chunks] first run overlapping each row chunk
+  int* rowidx;    // [BH][row_cap] packed union rows: (head mask << 24) | physical row
   int* counters;  // [BH] chunk-completion counters (zero between launches)
   int max_chunks;
 };
@@ -48,6 +48,9 @@ cudaError_t launch_attend(const dp_cache_view& v, const void* q, int qdt, int G,
                           float* out, float* lse, void* ws, bool dense, cudaStream_t st);
 cudaError_t launch_attn_tc(const dp_cache_view& v, const void* q, int qdt, int G, double scale, const double* lm,
                            WorkLists wl, Partials<float> pt, float* out, float* lse, bool dense, cudaStream_t st);
+cudaError_t launch_plan(const dp_cache_view& v, const void* q, int qdt, int G, double scale, double p1, double p2,
+                        double* lm, uint8_t* state, int* counts, int* stats, void* ws, cudaStream_t st);
+bool plan_supported(const dp_cache_view& v, int G);
 cudaError_t launch_append(const dp_cache_view& v, const void* nk, const void* nv, cudaStream_t st);
 
 }  // namespace dp
