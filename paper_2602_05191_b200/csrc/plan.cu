@@ -228,7 +228,8 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT)
     }
     if (tid == 0) s_b1 = kBins;
     __syncthreads();
-    for (int b = tid; b < kBins; b += kPT) {
+    for (int b0 = 0; b0 < kBins; b0 += kPT) {
+      const int b = b0 + tid;
       const bool hit = bcnt[b] > 0 && (bcum[b] + bmass[b]) / total >= p1;
       const unsigned bal = __ballot_sync(0xffffffffu, hit);
       if (hit && lane == __ffs(bal) - 1) atomicMin(&s_b1, b);
@@ -286,8 +287,9 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT)
     // stage 2 (engine.py:191-194): same descending order, denominator = sub
     if (tid == 0) s_b2 = b1;
     __syncthreads();
-    for (int b = tid; b < min(b1, kBins); b += kPT) {
-      const bool hit = bcnt[b] > 0 && (bcum[b] + bmass[b]) / sub >= p2;
+    for (int b0 = 0; b0 < kBins; b0 += kPT) {  // uniform trip count: full-warp ballots
+      const int b = b0 + tid;
+      const bool hit = b < b1 && bcnt[b] > 0 && (bcum[b] + bmass[b]) / sub >= p2;
       const unsigned bal = __ballot_sync(0xffffffffu, hit);
       if (hit && lane == __ffs(bal) - 1) atomicMin(&s_b2, b);
     }
