@@ -200,6 +200,10 @@ int dp_cluster_build(const dp_cluster_params* p, const void* src_keys, const voi
                      int32_t cluster_cap, int32_t* perm, double* objective, int32_t* iters,
                      void* workspace, size_t workspace_bytes, void* stream);
 
+/* Profiling aid: %globaltimer stamps (ns) of the last dp_plan launch's first
+ * cluster, [8 ranks][8 phase events], copied to host memory. */
+int dp_debug_plan_timing(unsigned long long* out);
+
 /* Lower-level pieces of the above (used by the parity tests). */
 /* k-means++ picks only: picks int32 [B*H, k]. */
 int dp_kmeanspp(const dp_cluster_params* p, const void* src_keys, const int32_t* first_pick,

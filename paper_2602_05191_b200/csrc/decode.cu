@@ -329,15 +329,9 @@ __global__ void __launch_bounds__(kAttnThreads) attn_chunk_kernel(dp_cache_view 
       if (kDense) {
         phys = vr; mask = full;
       } else {
-        const int4* runs = wl.runs + (size_t)bh * (v.cluster_cap + 2);
-        int lo = 0, hi = wl.nruns[bh] - 1;  // last run with prefix <= vr
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (runs[mid].w <= vr) lo = mid; else hi = mid - 1;
-        }
-        const int4 ru = runs[lo];
-        phys = ru.x + (vr - ru.w);
-        mask = ru.z;
+        const unsigned e = reinterpret_cast<const unsigned*>(wl.rowidx)[(size_t)bh * v.row_cap + vr];
+        phys = (int)(e & 0xFFFFFFu);
+        mask = (int)(e >> 24);
       }
     }
     rphys[r] = phys;

@@ -38,6 +38,17 @@ constexpr float kBinScale = 16.f;
 constexpr int kPlanTile = 64;  // centroid rows staged per score tile
 constexpr int kPlanMaxCap = 4096;
 
+// phase timestamps (%globaltimer, ns) of cluster 0: [rank][event]; read with
+// dp_debug_plan_timing() -- profiling aid only
+__device__ unsigned long long g_plan_ts[kCl][8];
+__device__ __forceinline__ void stamp(int r, int ev) {
+  if (blockIdx.x < kCl && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_plan_ts[r][ev] = t;
+  }
+}
+
 __device__ __forceinline__ bool before(double pa, int ia, double pb, int ib) {
   return pa > pb || (pa == pb && ia < ib);
 }
@@ -129,6 +140,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT)
   __shared__ double s_lmax[kMaxGroup];
   __shared__ int s_b1, s_b2, s_nc, s_tot[3];
 
+  stamp(r, 0);
   // ---------------- phase 1: score my slice for all G heads ---------------
   for (int i = tid; i < G * d; i += kPT) qd[i] = load_elem_d(q, qdt, (size_t)bh * G * d + i);
   {
@@ -180,7 +192,9 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT)
       if (tid < 4 && tid + 4 * hh < G) s_lmax[tid + 4 * hh] = fmax(red[2 * tid], red[2 * tid + 1]);
     }
   }
+  stamp(r, 1);
   cluster.sync();  // (A) every slice scored
+  stamp(r, 2);
 
   // ---------------- phase 2: two-stage top-p for q head g = r --------------
   const bool sel = r < G;
@@ -193,6 +207,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT)
     }
   }
   cluster.sync();  // (B) gathers done (lmS no longer read remotely)
+  stamp(r, 3);
   if (sel) {
     const int g = r;
     for (int b = tid; b < kBins; b += kPT) {
@@ -348,7 +363,9 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT)
     if (state_out)
       for (int i = tid; i < K; i += kPT) state_out[((size_t)bh * G + g) * cap + i] = stS[i];
   }
+  stamp(r, 4);
   cluster.sync();  // (C) all head states ready
+  stamp(r, 5);
 
   // ---------------- phase 3: GQA-union work list for my slice ------------
   const int full_mask = (1 << G) - 1;
@@ -433,8 +450,18 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT)
       wl.stats[4 * bh + 3] = all_e;
     }
   }
+  stamp(r, 6);
   cluster.sync();  // (E) keep smem alive until every remote read is done
+  stamp(r, 7);
 }
+
+}  // namespace dp
+
+extern "C" int dp_debug_plan_timing(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, dp::g_plan_ts, sizeof(dp::g_plan_ts)) == cudaSuccess ? 0 : 2;
+}
+
+namespace dp {
 
 size_t plan_smem_bytes(int d, int cap) { return plan_layout(d, cap).total; }
 

@@ -1,0 +1,37 @@
+"""Print the per-phase timing of one dp_plan launch (cluster 0) at the bench
+shape: python tools/plan_timing.py [context] [G]"""
+import ctypes
+import math
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2602_05191_b200 import DecodeWorkspace, cluster_layer  # noqa: E402
+from paper_2602_05191_b200 import _native as N  # noqa: E402
+from paper_2602_05191_b200.workload import generate_layer, generate_queries  # noqa: E402
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
+G = int(sys.argv[2]) if len(sys.argv) > 2 else 4
+k, v, c = generate_layer(1, 8, n, 128)
+lay = cluster_layer(k, v)
+q = torch.from_numpy(generate_queries(c, G, 1)[0]).cuda().to(torch.bfloat16)
+ws = DecodeWorkspace(lay, G)
+lib = N.lib()
+view = lay.view()
+for it in range(3):
+    N.check(lib.dp_plan(view, N.ptr(q), 1, G, 1 / math.sqrt(128), 0.95, 0.7, N.ptr(ws.log_mass), None,
+                        N.ptr(ws.counts), N.ptr(ws.stats), N.ptr(ws.ws), ws.ws.numel(),
+                        torch.cuda.current_stream().cuda_stream))
+torch.cuda.synchronize()
+buf = (ctypes.c_ulonglong * 64)()
+lib.dp_debug_plan_timing(ctypes.cast(buf, ctypes.c_void_p))
+t = np.array(buf[:], dtype=np.float64).reshape(8, 8)
+t0 = t[:, 0].min()
+names = ["start", "p1 done", "syncA", "syncB", "p2 done", "syncC", "p3 done", "end"]
+print("rank " + " ".join(f"{x:>8s}" for x in names))
+for r in range(8):
+    print(f"{r:4d} " + " ".join(f"{(x - t0) / 1e3:8.2f}" for x in t[r]))
+print("counts", ws.counts[0, :G].tolist(), "stats", ws.stats[0, 0].tolist())
