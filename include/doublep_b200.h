@@ -202,7 +202,7 @@ int dp_cluster_build(const dp_cluster_params* p, const void* src_keys, const voi
 
 /* Profiling aid: %globaltimer stamps (ns) of the last dp_plan launch's first
  * cluster, [8 ranks][8 phase events], copied to host memory. */
-int dp_debug_plan_timing(unsigned long long* out);
+int dp_debug_plan_timing(unsigned long long* out); /* [8][16] */
 
 /* Lower-level pieces of the above (used by the parity tests). */
 /* k-means++ picks only: picks int32 [B*H, k]. */

@@ -98,3 +98,4 @@ __device__ __forceinline__ T block_exclusive_scan(T v, T* red, T* total) {
 }
 
 }  // namespace dp
+

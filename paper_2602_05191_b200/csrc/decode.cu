@@ -277,6 +277,7 @@ __global__ void __launch_bounds__(kListThreads) worklist_kernel(dp_cache_view v,
     wl.nrows[bh] = s_rows;
     wl.napprox[bh] = s_apx;
     wl.nchunks[bh] = (s_rows + kChunkRows - 1) / kChunkRows;
+    publish_chunk_prefix(wl, v.batch * v.kv_heads);
     if (wl.stats) {
       wl.stats[4 * bh + 0] = s_rows;
       wl.stats[4 * bh + 1] = s_apx;
@@ -524,6 +525,8 @@ size_t decode_ws_layout(const dp_cache_view* v, int G, WorkLists* wl, void** par
   char* cnt = take(BH * 4 * sizeof(int));
   char* crun = take(BH * (size_t)v->row_cap * sizeof(int));
   char* ctr = take(BH * sizeof(int));
+  char* cpre = take((BH + 1) * sizeof(int));
+  char* dn = take(sizeof(int));
   const size_t pbytes = BH * max_chunks * G * (2 + (size_t)v->head_dim) * acc;
   char* p = take(pbytes);
   if (wl) {
@@ -537,6 +540,8 @@ size_t decode_ws_layout(const dp_cache_view* v, int G, WorkLists* wl, void** par
     wl->stats = nullptr;
     wl->rowidx = reinterpret_cast<int*>(crun);
     wl->counters = reinterpret_cast<int*>(ctr);
+    wl->chunk_prefix = reinterpret_cast<int*>(cpre);
+    wl->done = reinterpret_cast<int*>(dn);
     wl->max_chunks = max_chunks;
   }
   if (parts) *parts = p;

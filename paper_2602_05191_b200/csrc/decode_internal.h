@@ -21,7 +21,9 @@ struct WorkLists {
   int* nchunks;   // [BH]
   int* stats;     // nullable [BH][4]
   int* rowidx;    // [BH][row_cap] packed union rows: (head mask << 24) | physical row
-  int* counters;  // [BH] chunk-completion counters (zero between launches)
+  int* counters;  // [BH] partial-completion counters (zero between launches)
+  int* chunk_prefix;  // [BH+1] exclusive prefix of nchunks over heads (+ total)
+  int* done;      // [1] producer-completion counter (zero between launches)
   int max_chunks;
 };
 
@@ -32,6 +34,23 @@ struct Partials {
   Acc* o;  // [BH][max_chunks][G][d]
   int max_chunks;
 };
+
+// Called by ONE thread of every producer block (one per head) after its
+// nchunks entry is written: the last producer to finish writes the exclusive
+// prefix of nchunks over all heads (and the total) and re-arms the counter.
+__device__ __forceinline__ void publish_chunk_prefix(const WorkLists& wl, int BH) {
+  __threadfence();
+  if (atomicAdd(wl.done, 1) != BH - 1) return;
+  __threadfence();
+  int acc = 0;
+  for (int b = 0; b < BH; ++b) {
+    wl.chunk_prefix[b] = acc;
+    acc += *((volatile int*)&wl.nchunks[b]);
+  }
+  wl.chunk_prefix[BH] = acc;
+  *wl.done = 0;
+  __threadfence();
+}
 
 size_t decode_ws_layout(const dp_cache_view* v, int G, WorkLists* wl, void** parts, size_t* part_bytes,
                         char* base);

@@ -40,7 +40,7 @@ constexpr int kPlanMaxCap = 4096;
 
 // phase timestamps (%globaltimer, ns) of cluster 0: [rank][event]; read with
 // dp_debug_plan_timing() -- profiling aid only
-__device__ unsigned long long g_plan_ts[kCl][8];
+__device__ unsigned long long g_plan_ts[kCl][16];
 __device__ __forceinline__ void stamp(int r, int ev) {
   if (blockIdx.x < kCl && threadIdx.x == 0) {
     unsigned long long t;
@@ -230,6 +230,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT)
       t += p;
     }
     const double total = block_sum(t, red);  // probs.sum(), selection.py:52
+    stamp(r, 8);
     {
       constexpr int bp = kBins / kPT;
       double loc = 0.0;
@@ -251,6 +252,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT)
     }
     __syncthreads();
     const int b1 = s_b1;  // kBins: p1 never reached (rounding at p1 = 1) -> keep all
+    stamp(r, 9);
 
     // gather + rank-sort the elements of bin `bin` into candidate slots [base, base+n)
     auto sort_bin = [&](int bin, int base) -> int {
@@ -299,6 +301,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT)
       (void)loc;
     }
     __syncthreads();
+    stamp(r, 10);
     // stage 2 (engine.py:191-194): same descending order, denominator = sub
     if (tid == 0) s_b2 = b1;
     __syncthreads();
@@ -331,6 +334,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT)
       cut2 = s_nc;
     }
     __syncthreads();
+    stamp(r, 11);
     // states: 2 exact, 1 approx, 0 dropped
     for (int i = tid; i < K; i += kPT) {
       const int b = bin16[i];
@@ -400,7 +404,9 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT)
     s_tot[1] = tot_a;
     s_tot[2] = tot_r;
   }
+  stamp(r, 12);
   cluster.sync();  // (D) slice totals visible
+  stamp(r, 13);
   int off_e = 0, off_a = 0, off_r = sw_rows, all_e = 0, all_a = 0, all_r = sw_rows;
   for (int rr = 0; rr < kCl; ++rr) {
     const int* t3 = cluster.map_shared_rank(s_tot, rr);
@@ -443,6 +449,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT)
     wl.napprox[bh] = all_a;
     wl.nruns[bh] = all_e + (v.sink > 0) + (v.window > 0);
     wl.nchunks[bh] = (all_r + kChunkRows - 1) / kChunkRows;
+    publish_chunk_prefix(wl, v.batch * v.kv_heads);
     if (wl.stats) {
       wl.stats[4 * bh + 0] = all_r;
       wl.stats[4 * bh + 1] = all_a;
@@ -458,7 +465,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT)
 }  // namespace dp
 
 extern "C" int dp_debug_plan_timing(unsigned long long* out) {
-  return cudaMemcpyFromSymbol(out, dp::g_plan_ts, sizeof(dp::g_plan_ts)) == cudaSuccess ? 0 : 2;
+  return cudaMemcpyFromSymbol(out, dp::g_plan_ts, sizeof(dp::g_plan_ts)) == cudaSuccess ? 0 : 2;  // [8][16]
 }
 
 namespace dp {

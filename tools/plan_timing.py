@@ -26,12 +26,12 @@ for it in range(3):
                         N.ptr(ws.counts), N.ptr(ws.stats), N.ptr(ws.ws), ws.ws.numel(),
                         torch.cuda.current_stream().cuda_stream))
 torch.cuda.synchronize()
-buf = (ctypes.c_ulonglong * 64)()
+buf = (ctypes.c_ulonglong * 128)()
 lib.dp_debug_plan_timing(ctypes.cast(buf, ctypes.c_void_p))
-t = np.array(buf[:], dtype=np.float64).reshape(8, 8)
+t = np.array(buf[:], dtype=np.float64).reshape(8, 16)[:, [0, 1, 2, 3, 8, 9, 10, 11, 4, 5, 12, 13, 6, 7]]
 t0 = t[:, 0].min()
-names = ["start", "p1 done", "syncA", "syncB", "p2 done", "syncC", "p3 done", "end"]
-print("rank " + " ".join(f"{x:>8s}" for x in names))
+names = ["start", "p1", "syncA", "syncB", "softmx", "b1", "cut1", "st2", "p2", "syncC", "3scan", "syncD", "p3", "end"]
+print("rank " + " ".join(f"{x:>6s}" for x in names))
 for r in range(8):
-    print(f"{r:4d} " + " ".join(f"{(x - t0) / 1e3:8.2f}" for x in t[r]))
+    print(f"{r:4d} " + " ".join(f"{(x - t0) / 1e3:6.2f}" if x > 0 else "     -" for x in t[r]))
 print("counts", ws.counts[0, :G].tolist(), "stats", ws.stats[0, 0].tolist())
