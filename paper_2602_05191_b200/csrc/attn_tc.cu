@@ -6,9 +6,11 @@
 // contiguous range [i*T/grid, (i+1)*T/grid) of it -- balanced to +-1 chunk
 // with no atomics -- and runs an online softmax over it, flushing one partial
 // (m, l, o) per head it touches.  Rows are gathered through a 3-stage
-// cp.async ring (64 KB of K+V per stage, two chunks in flight while one is
-// computed); cluster members are contiguous in HBM so each warp instruction
-// copies 512 contiguous bytes.
+// TMA-bulk ring (64 KB of K+V per stage, two chunks in flight while one is
+// computed).  Rows are moved by the bulk-copy engine (cp.async.bulk, one 256-B
+// copy per K/V row into a padded 272-B smem row so ldmatrix stays
+// conflict-free) completing on a per-stage mbarrier: the LSU and its
+// outstanding-request limit are out of the data path.
 //
 //   S^T[head, row] = Q[head, :] . K[row, :]     mma.m16n8k16 bf16 -> f32, M = heads
 //                                                (G <= 8 of 16), N = 8 rows, K = 16 dims
@@ -70,6 +72,27 @@ __device__ __forceinline__ void split2(float x, float y, unsigned& hi, unsigned&
   lo = pack_bf16(x - __bfloat162float(hx), y - __bfloat162float(hy));
 }
 
+// ---- bulk-copy engine (TMA, non-tensor) + mbarrier helpers -------------
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+// one contiguous row (bytes multiple of 16) global -> shared, completing on bar
+__device__ __forceinline__ void bulk_row(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+
 // owner CTA of global chunk j when T chunks are split evenly over `grid`
 // CTAs as [i*T/grid, (i+1)*T/grid)
 __device__ __forceinline__ int chunk_owner(long long j, long long T, int grid) {
@@ -102,11 +125,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
   __shared__ float red_m[32], red_l[32];
   __shared__ float s_M[8], s_L[8];
   __shared__ int s_merge[4], s_nmerge;
+  __shared__ __align__(8) unsigned long long s_bar[kStages];
 
   // ---- chunk prefix over heads, my contiguous chunk range -----------------
   const int per_dense = (v.n_tokens + kTcRows - 1) / kTcRows;
   for (int b = tid; b <= BH; b += kTcThreads) prefix[b] = kDense ? b * per_dense : wl.chunk_prefix[b];
-  if (tid == 0) s_nmerge = 0;
+  if (tid == 0) {
+    s_nmerge = 0;
+    for (int i = 0; i < kStages; ++i) mbar_init(smem_u32(&s_bar[i]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
   __syncthreads();
   const long long T = prefix[BH];
   const int j0 = (int)((long long)me * T / grid), j1 = (int)((long long)(me + 1) * T / grid);
@@ -121,50 +149,55 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
     return lo;
   };
 
-  // ---- producer: rows of global chunk j -> stage s, cp.async K and V -------
-  // thread t loads the row entries of the rows it copies (t/16 + 8i) and the
-  // entry of row t (its head mask, read back by the QK step)
+  // ---- producer: rows of global chunk j -> stage s through the bulk-copy
+  // engine.  Thread 0 posts the stage's byte count (expect_tx) BEFORE the
+  // barrier that precedes the copies; thread t then copies row t's K and V
+  // (256 B each) and records its head mask.
+  auto chunk_rows = [&](int j) {
+    const int bh = head_of(j);
+    const int rows_total = kDense ? v.n_tokens : __ldg(&wl.nrows[bh]);
+    return min(kTcRows, rows_total - (j - prefix[bh]) * kTcRows);
+  };
+  auto expect_chunk = [&](int j, int s) {  // thread 0 only
+    mbar_expect_tx(smem_u32(&s_bar[s]), (unsigned)chunk_rows(j) * (2u * d * 2u));
+  };
   auto issue_chunk = [&](int j, int s) {
     const int bh = head_of(j);
     const int c = j - prefix[bh];
     const int rows_total = kDense ? v.n_tokens : __ldg(&wl.nrows[bh]);
     const int v0 = c * kTcRows;
     const int nr = min(kTcRows, rows_total - v0);
-    const unsigned* ridx = reinterpret_cast<const unsigned*>(wl.rowidx) + (size_t)bh * v.row_cap + v0;
-    {
-      int mask = 0;
-      if (tid < nr) mask = kDense ? (1 << G) - 1 : (int)(__ldg(&ridx[tid]) >> 24);
-      rmask[s * kTcRows + tid] = mask;
-    }
-    const size_t head_off = (size_t)bh * v.row_cap * d;
-    const __nv_bfloat16* Kg = reinterpret_cast<const __nv_bfloat16*>(v.keys) + head_off;
-    const __nv_bfloat16* Vg = reinterpret_cast<const __nv_bfloat16*>(v.values) + head_off;
     __nv_bfloat16* Ks = KV + (size_t)s * 2 * kStageElems;
     __nv_bfloat16* Vs = Ks + kStageElems;
-    const int ch = tid & 15;
-    int pr[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int row = (tid >> 4) + 8 * i;
-      pr[i] = row < nr ? (kDense ? v0 + row : (int)(__ldg(&ridx[row]) & 0xFFFFFFu)) : -1;
-    }
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int row = (tid >> 4) + 8 * i;
-      __nv_bfloat16* kd = Ks + row * kRowStride + ch * 8;
-      __nv_bfloat16* vd = Vs + row * kRowStride + ch * 8;
-      if (pr[i] >= 0) {
-        cp16(smem_u32(kd), Kg + (size_t)pr[i] * d + ch * 8);
-        cp16(smem_u32(vd), Vg + (size_t)pr[i] * d + ch * 8);
+    int mask = 0;
+    if (tid < nr) {
+      int phys;
+      if (kDense) {
+        phys = v0 + tid;
+        mask = (1 << G) - 1;
       } else {
-        *reinterpret_cast<int4*>(kd) = make_int4(0, 0, 0, 0);
-        *reinterpret_cast<int4*>(vd) = make_int4(0, 0, 0, 0);
+        const unsigned e = __ldg(reinterpret_cast<const unsigned*>(wl.rowidx) + (size_t)bh * v.row_cap + v0 + tid);
+        phys = (int)(e & 0xFFFFFFu);
+        mask = (int)(e >> 24);
+      }
+      const size_t off = ((size_t)bh * v.row_cap + phys) * d;
+      const unsigned bar = smem_u32(&s_bar[s]);
+      bulk_row(smem_u32(Ks + tid * kRowStride), reinterpret_cast<const __nv_bfloat16*>(v.keys) + off, d * 2, bar);
+      bulk_row(smem_u32(Vs + tid * kRowStride), reinterpret_cast<const __nv_bfloat16*>(v.values) + off, d * 2, bar);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        *reinterpret_cast<int4*>(Ks + tid * kRowStride + i * 8) = make_int4(0, 0, 0, 0);
+        *reinterpret_cast<int4*>(Vs + tid * kRowStride + i * 8) = make_int4(0, 0, 0, 0);
       }
     }
-    asm volatile("cp.async.commit_group;\n" ::);
+    rmask[s * kTcRows + tid] = mask;
   };
 
   // prologue: fill the ring
+  if (tid == 0)
+    for (int i = 0; i < kStages && i < n; ++i) expect_chunk(j0 + i, i);
+  __syncthreads();
   for (int i = 0; i < kStages && i < n; ++i) issue_chunk(j0 + i, i);
 
   unsigned qa[8][2], qb[8][2];
@@ -220,10 +253,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
   for (int idx = 0; idx < n; ++idx) {
     const int j = j0 + idx, s = idx % kStages;
     const int bh = head_of(j);
-    const int ahead = min(kStages - 1, n - 1 - idx);  // groups committed after chunk idx
-    if (ahead >= 2) asm volatile("cp.async.wait_group 2;\n" ::: "memory");
-    else if (ahead == 1) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-    else asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    mbar_wait(smem_u32(&s_bar[s]), (unsigned)((idx / kStages) & 1));  // stage s bytes landed
     if (bh != cur) {
       if (cur >= 0) flush(cur);
       cur = bh;
@@ -340,11 +370,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
         mma_bf16(o[2 * np + 1], al0, al2, b2, b3);
       }
     }
-    __syncthreads();  // stage s and Ps consumed
+    if (tid == 0 && idx + kStages < n) expect_chunk(j0 + idx + kStages, s);
+    __syncthreads();  // stage s and Ps consumed; next expect_tx posted
     if (idx + kStages < n) issue_chunk(j0 + idx + kStages, s);
   }
   flush(cur);
   __syncthreads();
+  if (tid < kStages) asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&s_bar[tid])));
 
   // ---- merges of the heads I finished last (engine.py:231-246) ----------
   const int nm = s_nmerge;

@@ -48,3 +48,51 @@ def compare_plan(est_o, plan_o, order_g, n1_g, n2_g, p1, p2):
     cum2 = np.cumsum(sub) / sub.sum()
     c2 = classify_stage(probs, order_o, n2_o, order_g, n2_g, cum2, p2) if c1 == "exact" else c1
     return c1, c2
+
+
+def _same_modulo_ties(probs, got, want, scale):
+    """Sets `got` and `want` (equal size) hold the same probabilities up to
+    swaps of entries within TIE*scale of each other."""
+    a = np.sort(probs[np.asarray(sorted(got - want), dtype=np.int64)]) if got - want else np.empty(0)
+    b = np.sort(probs[np.asarray(sorted(want - got), dtype=np.int64)]) if want - got else np.empty(0)
+    return a.size == b.size and np.all(np.abs(a - b) <= TIE * scale)
+
+
+def classify_sets(est_o, plan_o, state_row, p1, p2):
+    """Classify the GPU plan given as per-cluster states (2 exact, 1 approx,
+    0 dropped) against the oracle plan: 'exact', 'order_tie',
+    'threshold_tie' or 'real' for each stage."""
+    probs = est_o.probs
+    K = probs.size
+    st = np.asarray(state_row[:K])
+    order = np.argsort(-probs, kind="stable")
+    scale = max(float(probs.max()), 1e-300)
+    res = []
+    for stage in (1, 2):
+        if stage == 1:
+            g = set(np.flatnonzero(st >= 1).tolist())
+            o_set = set(plan_o.stage1.selected.tolist())
+            cum = np.cumsum(probs[order]) / probs.sum()
+            p = p1
+            base = order
+        else:
+            g = set(np.flatnonzero(st == 2).tolist())
+            o_set = set(plan_o.exact_clusters.tolist())
+            n1 = plan_o.stage1.selected.size
+            sub = probs[order[:n1]]
+            cum = np.cumsum(sub) / sub.sum()
+            p = p2
+            base = order[:n1]
+        if g == o_set:
+            res.append("exact")
+            continue
+        ng, no = len(g), len(o_set)
+        if not _same_modulo_ties(probs, g, set(base[:ng].tolist()), scale):
+            res.append("real")
+            continue
+        if ng == no:
+            res.append("order_tie")
+            continue
+        lo, hi = sorted((ng, no))
+        res.append("threshold_tie" if all(abs(cum[j] - p) <= TIE for j in range(lo - 1, hi - 1)) else "real")
+    return tuple(res)

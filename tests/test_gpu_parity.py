@@ -10,7 +10,7 @@ import pytest
 import torch
 
 from oracle import doublep_oracle as O
-from parity import compare_plan, oracle_tables
+from parity import classify_sets, compare_plan, oracle_tables
 
 pytestmark = pytest.mark.gpu
 
@@ -55,7 +55,7 @@ def _check_decode(layer, kdev, vdev, queries, G, p1, p2, dtype, counts=None):
     N.check(N.lib().dp_select(layer.view(), G, p1, p2, N.ptr(ws.log_mass), N.ptr(st2), N.ptr(c2),
                               N.ptr(order), None, None, None, 0, torch.cuda.current_stream().cuda_stream))
     order = order[0].cpu().numpy()
-    assert torch.equal(st2, ws.state)
+    st_plan = ws.state[0].cpu().numpy()  # the fused plan kernel's selection
     classes = {}
     kf = kdev[0].double().cpu().numpy()  # exact upcast of what the GPU read
     vf = vdev[0].double().cpu().numpy()
@@ -66,7 +66,11 @@ def _check_decode(layer, kdev, vdev, queries, G, p1, p2, dtype, counts=None):
         o_out, o_plan, o_est = O.decode_step(qv, kf[h], vf[h], t, p1, p2, layer.sink, layer.window)
         K = len(t.members)
         np.testing.assert_allclose(lm_g[hq, :K], o_est.log_masses, rtol=0, atol=1e-9)
-        c1, c2_ = compare_plan(o_est, o_plan, order[hq], int(cnt[hq, 0]), int(cnt[hq, 1]), p1, p2)
+        c1, c2_ = classify_sets(o_est, o_plan, st_plan[hq], p1, p2)
+        # the debug (full bitonic sort) select must agree with the oracle too
+        d1, d2 = compare_plan(o_est, o_plan, order[hq], int(c2[0, hq, 0]), int(c2[0, hq, 1]), p1, p2)
+        assert d1 != "real" and d2 != "real", (hq, d1, d2)
+        assert int(cnt[hq, 0]) == int((st_plan[hq, :K] >= 1).sum()) and int(cnt[hq, 1]) == int((st_plan[hq, :K] == 2).sum())
         classes[c1] = classes.get(c1, 0) + 1
         classes[c2_] = classes.get(c2_, 0) + 1
         assert c1 != "real" and c2_ != "real", (hq, c1, c2_)
