@@ -1,20 +1,21 @@
 // Gathered split-KV decode attention for bf16 caches on tensor cores.
 //
-// Persistent: one CTA (4 warps) per SM.  The GQA-union rows of every
+// Persistent: one CTA (8 warps) per SM.  The GQA-union rows of every
 // (sequence, kv head) form a global sequence of 128-row chunks (the plan /
 // worklist kernel publishes the per-head chunk prefix); CTA i owns the
 // contiguous range [i*T/grid, (i+1)*T/grid) of it -- balanced to +-1 chunk
 // with no atomics -- and runs an online softmax over it, flushing one partial
 // (m, l, o) per head it touches.  Rows are gathered through a 3-stage
 // TMA-bulk ring (64 KB of K+V per stage, two chunks in flight while one is
-// computed).  Rows are moved by the bulk-copy engine (cp.async.bulk, one 256-B
-// copy per K/V row into a padded 272-B smem row so ldmatrix stays
-// conflict-free) completing on a per-stage mbarrier: the LSU and its
-// outstanding-request limit are out of the data path.
+// computed): 16-byte cp.async copies, a warp moving 2 rows = 512 contiguous
+// bytes per instruction into padded 272-B smem rows (conflict-free ldmatrix).
+// (tools/bw_probe.cu: this ring streams at ~5.4 TB/s on B200; per-row
+// cp.async.bulk reached 4.6 TB/s.)
 //
-//   S^T[head, row] = Q[head, :] . K[row, :]     mma.m16n8k16 bf16 -> f32, M = heads
-//                                                (G <= 8 of 16), N = 8 rows, K = 16 dims
-//   O[head, d]    += P[head, row] . V[row, d]   M = heads, N = 8 dims, K = 16 rows
+//   S[row, head]  = K[row, :] . Q[head, :]     mma.m16n8k16 bf16 -> f32, M = 16 rows,
+//                                                N = 8 heads (G <= 8), K = 16 dims
+//   O^T[d, head] += V^T[d, row] . P[row, head]  M = 16 dims, N = 8 heads, K = 16 rows
+// (heads on N keeps M dense: 24 MMAs per warp per 128-row chunk)
 //
 // P is split hi + lo into two bf16 operands (two MMAs) so the weights keep
 // ~2^-16 relative precision; an fp32 query is split the same way.  The last
@@ -29,7 +30,7 @@
 namespace dp {
 
 constexpr int kTcRows = kChunkRows;  // 128
-constexpr int kTcThreads = 128;
+constexpr int kTcThreads = 256;  // 8 warps
 constexpr int kRowStride = 136;      // bf16 elements per staged row (272 B: conflict-free ldmatrix)
 constexpr int kStages = 3;
 constexpr int kStageElems = kTcRows * kRowStride;  // one K (or V) tile
@@ -112,29 +113,25 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
                                                                WorkLists wl, Partials<float> pt,
                                                                float* __restrict__ out, float* __restrict__ lse) {
   constexpr int d = 128;
+  constexpr int kWarps = kTcThreads / 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int gq = lane >> 2, tq = lane & 3;
+  const int g8 = lane >> 2, tq = lane & 3;  // fragment row / column-pair
   const int BH = v.batch * v.kv_heads;
   const int grid = gridDim.x, me = blockIdx.x;
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __nv_bfloat16* KV = reinterpret_cast<__nv_bfloat16*>(smem_raw);  // [stage][K|V][rows][stride]
-  float* Ps = reinterpret_cast<float*>(smem_raw + TcSmem::kv);      // [8][rows]
+  float* Ps = reinterpret_cast<float*>(smem_raw + TcSmem::kv);      // [8 heads][rows]
   int* rmask = reinterpret_cast<int*>(smem_raw + TcSmem::kv + TcSmem::ps);  // [stage][rows]
   int* prefix = reinterpret_cast<int*>(smem_raw + TcSmem::fixed);           // [BH+1]
-  __shared__ float red_m[32], red_l[32];
+  __shared__ float red_m[kWarps][8], red_l[kWarps][8];
   __shared__ float s_M[8], s_L[8];
   __shared__ int s_merge[4], s_nmerge;
-  __shared__ __align__(8) unsigned long long s_bar[kStages];
 
   // ---- chunk prefix over heads, my contiguous chunk range -----------------
   const int per_dense = (v.n_tokens + kTcRows - 1) / kTcRows;
   for (int b = tid; b <= BH; b += kTcThreads) prefix[b] = kDense ? b * per_dense : wl.chunk_prefix[b];
-  if (tid == 0) {
-    s_nmerge = 0;
-    for (int i = 0; i < kStages; ++i) mbar_init(smem_u32(&s_bar[i]), 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
+  if (tid == 0) s_nmerge = 0;
   __syncthreads();
   const long long T = prefix[BH];
   const int j0 = (int)((long long)me * T / grid), j1 = (int)((long long)(me + 1) * T / grid);
@@ -149,61 +146,54 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
     return lo;
   };
 
-  // ---- producer: rows of global chunk j -> stage s through the bulk-copy
-  // engine.  Thread 0 posts the stage's byte count (expect_tx) BEFORE the
-  // barrier that precedes the copies; thread t then copies row t's K and V
-  // (256 B each) and records its head mask.
-  auto chunk_rows = [&](int j) {
-    const int bh = head_of(j);
-    const int rows_total = kDense ? v.n_tokens : __ldg(&wl.nrows[bh]);
-    return min(kTcRows, rows_total - (j - prefix[bh]) * kTcRows);
-  };
-  auto expect_chunk = [&](int j, int s) {  // thread 0 only
-    mbar_expect_tx(smem_u32(&s_bar[s]), (unsigned)chunk_rows(j) * (2u * d * 2u));
-  };
+  // ---- producer: rows of global chunk j -> stage s (one cp.async group) ---
+  // thread t copies 16-B column `t & 15` of rows (t >> 4) + 16 i, i < 8, of
+  // both K and V; the ch == 0 thread of a row records its head mask
   auto issue_chunk = [&](int j, int s) {
     const int bh = head_of(j);
     const int c = j - prefix[bh];
     const int rows_total = kDense ? v.n_tokens : __ldg(&wl.nrows[bh]);
     const int v0 = c * kTcRows;
     const int nr = min(kTcRows, rows_total - v0);
+    const unsigned* ridx = reinterpret_cast<const unsigned*>(wl.rowidx) + (size_t)bh * v.row_cap + v0;
+    const size_t head_off = (size_t)bh * v.row_cap * d;
+    const __nv_bfloat16* Kg = reinterpret_cast<const __nv_bfloat16*>(v.keys) + head_off;
+    const __nv_bfloat16* Vg = reinterpret_cast<const __nv_bfloat16*>(v.values) + head_off;
     __nv_bfloat16* Ks = KV + (size_t)s * 2 * kStageElems;
     __nv_bfloat16* Vs = Ks + kStageElems;
-    int mask = 0;
-    if (tid < nr) {
-      int phys;
-      if (kDense) {
-        phys = v0 + tid;
-        mask = (1 << G) - 1;
-      } else {
-        const unsigned e = __ldg(reinterpret_cast<const unsigned*>(wl.rowidx) + (size_t)bh * v.row_cap + v0 + tid);
-        phys = (int)(e & 0xFFFFFFu);
-        mask = (int)(e >> 24);
-      }
-      const size_t off = ((size_t)bh * v.row_cap + phys) * d;
-      const unsigned bar = smem_u32(&s_bar[s]);
-      bulk_row(smem_u32(Ks + tid * kRowStride), reinterpret_cast<const __nv_bfloat16*>(v.keys) + off, d * 2, bar);
-      bulk_row(smem_u32(Vs + tid * kRowStride), reinterpret_cast<const __nv_bfloat16*>(v.values) + off, d * 2, bar);
-    } else {
+    const int ch = tid & 15;
+    unsigned e[8];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        *reinterpret_cast<int4*>(Ks + tid * kRowStride + i * 8) = make_int4(0, 0, 0, 0);
-        *reinterpret_cast<int4*>(Vs + tid * kRowStride + i * 8) = make_int4(0, 0, 0, 0);
-      }
+    for (int i = 0; i < 8; ++i) {
+      const int row = (tid >> 4) + 16 * i;
+      e[i] = row < nr ? (kDense ? (((unsigned)((1 << G) - 1)) << 24) | (unsigned)(v0 + row) : __ldg(&ridx[row]))
+                      : 0xFFFFFFFFu;
     }
-    rmask[s * kTcRows + tid] = mask;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int row = (tid >> 4) + 16 * i;
+      __nv_bfloat16* kd = Ks + row * kRowStride + ch * 8;
+      __nv_bfloat16* vd = Vs + row * kRowStride + ch * 8;
+      if (e[i] != 0xFFFFFFFFu) {
+        const size_t off = (size_t)(e[i] & 0xFFFFFFu) * d + ch * 8;
+        cp16(smem_u32(kd), Kg + off);
+        cp16(smem_u32(vd), Vg + off);
+      } else {
+        *reinterpret_cast<int4*>(kd) = make_int4(0, 0, 0, 0);
+        *reinterpret_cast<int4*>(vd) = make_int4(0, 0, 0, 0);
+      }
+      if (ch == 0) rmask[s * kTcRows + row] = e[i] == 0xFFFFFFFFu ? 0 : (int)(e[i] >> 24);
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
   };
 
-  // prologue: fill the ring
-  if (tid == 0)
-    for (int i = 0; i < kStages && i < n; ++i) expect_chunk(j0 + i, i);
-  __syncthreads();
-  for (int i = 0; i < kStages && i < n; ++i) issue_chunk(j0 + i, i);
+  for (int i = 0; i < kStages && i < n; ++i) issue_chunk(j0 + i, i);  // fill the ring
 
-  unsigned qa[8][2], qb[8][2];
+  // Q^T B-fragments (registers): b0 = Q[head g8][k*16 + 2tq ..], b1 = Q[head g8][k*16 + 8 + 2tq ..]
+  unsigned qa[8][2], qb[8][2];  // hi, lo
   auto load_q = [&](int bh) {
-    const bool valid = gq < G;
-    const size_t qoff = ((size_t)bh * G + (valid ? gq : 0)) * d;
+    const bool valid = g8 < G;
+    const size_t qoff = ((size_t)bh * G + (valid ? g8 : 0)) * d;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
 #pragma unroll
@@ -223,14 +213,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
     }
   };
 
-  float o[4][4];
-  float m_run = -INFINITY;                // running max (log2 domain) of head gq
-  float m_t = -INFINITY, l_t = 0.f;       // running max / sum of head `tid` (tid < G)
-  const int n0 = warp * 32;
+  // O^T accumulator of this warp: dims [16w, 16w+16) x heads; lane holds
+  // (dim 16w+g8, heads 2tq, 2tq+1) in o[0..1] and dim +8 in o[2..3]
+  float o[4];
+  float m_run[2];                       // running max (log2) of heads 2tq, 2tq+1
+  float m_t = -INFINITY, l_t = 0.f;     // running max / sum of head `tid` (tid < G)
+  const int dim0 = warp * 16;
   int cur = -1;
 
-  // flush the running state of head `bh` as my partial, count it, remember
-  // the head if I am its last contributor
   auto flush = [&](int bh) {
     const int first = chunk_owner(prefix[bh], T, grid);
     const int nparts = chunk_owner(prefix[bh + 1] - 1, T, grid) - first + 1;
@@ -240,10 +230,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
       pt.m[pbase + (size_t)slot * G + tid] = m_t == -INFINITY ? -INFINITY : m_t * 0.69314718055994531f;
       pt.l[pbase + (size_t)slot * G + tid] = l_t;
     }
-    if (gq < G) {
-      float* dst = pt.o + (pbase + (size_t)slot * G + gq) * d + n0 + 2 * tq;
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt) *reinterpret_cast<float2*>(dst + nt * 8) = make_float2(o[nt][0], o[nt][1]);
+    for (int e = 0; e < 4; ++e) {
+      const int h = 2 * tq + (e & 1), dd = dim0 + g8 + (e >> 1) * 8;
+      if (h < G) pt.o[(pbase + (size_t)slot * G + h) * d + dd] = o[e];
     }
     __threadfence();
     __syncthreads();
@@ -253,16 +243,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
   for (int idx = 0; idx < n; ++idx) {
     const int j = j0 + idx, s = idx % kStages;
     const int bh = head_of(j);
-    mbar_wait(smem_u32(&s_bar[s]), (unsigned)((idx / kStages) & 1));  // stage s bytes landed
+    const int ahead = min(kStages - 1, n - 1 - idx);  // groups committed after chunk idx
+    if (ahead >= 2) asm volatile("cp.async.wait_group 2;\n" ::: "memory");
+    else if (ahead == 1) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    else asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     if (bh != cur) {
       if (cur >= 0) flush(cur);
       cur = bh;
       load_q(bh);
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) o[nt][e] = 0.f;
-      m_run = -INFINITY;
+      for (int e = 0; e < 4; ++e) o[e] = 0.f;
+      m_run[0] = m_run[1] = -INFINITY;
       m_t = -INFINITY;
       l_t = 0.f;
     }
@@ -270,73 +261,85 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
     const __nv_bfloat16* Ks = KV + (size_t)s * 2 * kStageElems;
     const __nv_bfloat16* Vs = Ks + kStageElems;
     const int* rm = rmask + s * kTcRows;
-    // ---- S^T = Q K^T for this warp's 32 rows ------------------------------
-    float sc[4][4];
+    // ---- S = K Q^T for this warp's 16 rows --------------------------------
+    const int r0 = warp * 16;
+    float sc[4] = {0.f, 0.f, 0.f, 0.f};
+    {
+      const unsigned base =
+          smem_u32(Ks + (r0 + (lane & 7) + ((lane >> 3) & 1) * 8) * kRowStride + (lane >> 4) * 8);
 #pragma unroll
-    for (int jj = 0; jj < 4; ++jj)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) sc[jj][e] = 0.f;
-#pragma unroll
-    for (int jj = 0; jj < 4; ++jj) {
-      const int rbase = warp * 32 + jj * 8;
-      const unsigned base = smem_u32(Ks + (rbase + (lane & 7)) * kRowStride + (lane >> 3) * 8);
-#pragma unroll
-      for (int kk = 0; kk < 8; kk += 2) {
-        unsigned b0, b1, b2, b3;
-        ldsm_x4(base + kk * 32, b0, b1, b2, b3);
-        mma_bf16(sc[jj], qa[kk][0], qa[kk][1], b0, b1);
-        mma_bf16(sc[jj], qa[kk + 1][0], qa[kk + 1][1], b2, b3);
-        if (kQF32) {
-          mma_bf16(sc[jj], qb[kk][0], qb[kk][1], b0, b1);
-          mma_bf16(sc[jj], qb[kk + 1][0], qb[kk + 1][1], b2, b3);
-        }
+      for (int k = 0; k < 8; ++k) {
+        unsigned a0, a1, a2, a3;
+        ldsm_x4(base + k * 32, a0, a1, a2, a3);
+        asm volatile(
+            "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+            "{%0,%1,%2,%3};\n"
+            : "+f"(sc[0]), "+f"(sc[1]), "+f"(sc[2]), "+f"(sc[3])
+            : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(qa[k][0]), "r"(qa[k][1]));
+        if (kQF32)
+          asm volatile(
+              "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+              "{%0,%1,%2,%3};\n"
+              : "+f"(sc[0]), "+f"(sc[1]), "+f"(sc[2]), "+f"(sc[3])
+              : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(qb[k][0]), "r"(qb[k][1]));
       }
     }
-    float mx = -INFINITY;
+    // sc[e]: row r0 + g8 + (e>>1)*8, head 2tq + (e&1)
+    float mx[2] = {-INFINITY, -INFINITY};
 #pragma unroll
-    for (int jj = 0; jj < 4; ++jj) {
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int r = warp * 32 + jj * 8 + 2 * tq + e;
-        const bool ok = gq < G && ((rm[r] >> gq) & 1);
-        const float val = ok ? sc[jj][e] * scale_log2 : -INFINITY;
-        sc[jj][e] = val;
-        mx = fmaxf(mx, val);
-      }
+    for (int e = 0; e < 4; ++e) {
+      const int h = 2 * tq + (e & 1), r = r0 + g8 + (e >> 1) * 8;
+      const bool ok = h < G && ((rm[r] >> h) & 1);
+      const float val = ok ? sc[e] * scale_log2 : -INFINITY;
+      sc[e] = val;
+      mx[e & 1] = fmaxf(mx[e & 1], val);
     }
-    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-    if (tq == 0) red_m[warp * 8 + gq] = mx;
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+#pragma unroll
+      for (int off = 4; off < 32; off <<= 1) mx[hh] = fmaxf(mx[hh], __shfl_xor_sync(0xffffffffu, mx[hh], off));
+    }
+    if (g8 == 0) {
+      red_m[warp][2 * tq] = mx[0];
+      red_m[warp][2 * tq + 1] = mx[1];
+    }
     __syncthreads();
-    float cm = -INFINITY;
+    float alpha[2];
 #pragma unroll
-    for (int ww = 0; ww < 4; ++ww) cm = fmaxf(cm, red_m[ww * 8 + gq]);
-    const float m_new = fmaxf(m_run, cm);
-    const float alpha = m_new == -INFINITY ? 1.f : exp2f(m_run - m_new);
-    m_run = m_new;
-    float lsum = 0.f;
+    for (int hh = 0; hh < 2; ++hh) {
+      float cm = -INFINITY;
 #pragma unroll
-    for (int jj = 0; jj < 4; ++jj) {
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const float pv = (sc[jj][e] == -INFINITY) ? 0.f : exp2f(sc[jj][e] - m_new);
-        lsum += pv;
-        Ps[gq * kTcRows + warp * 32 + jj * 8 + 2 * tq + e] = pv;
-      }
+      for (int ww = 0; ww < kWarps; ++ww) cm = fmaxf(cm, red_m[ww][2 * tq + hh]);
+      const float mn = fmaxf(m_run[hh], cm);
+      alpha[hh] = mn == -INFINITY ? 1.f : exp2f(m_run[hh] - mn);
+      m_run[hh] = mn;
     }
-    lsum += __shfl_xor_sync(0xffffffffu, lsum, 1);
-    lsum += __shfl_xor_sync(0xffffffffu, lsum, 2);
-    if (tq == 0) red_l[warp * 8 + gq] = lsum;
+    float ls[2] = {0.f, 0.f};
 #pragma unroll
-    for (int nt = 0; nt < 4; ++nt) {
-      o[nt][0] *= alpha;
-      o[nt][1] *= alpha;
+    for (int e = 0; e < 4; ++e) {
+      const int h = 2 * tq + (e & 1), r = r0 + g8 + (e >> 1) * 8;
+      const float pv = sc[e] == -INFINITY ? 0.f : exp2f(sc[e] - m_run[e & 1]);
+      ls[e & 1] += pv;
+      Ps[h * kTcRows + r] = pv;
     }
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+#pragma unroll
+      for (int off = 4; off < 32; off <<= 1) ls[hh] += __shfl_xor_sync(0xffffffffu, ls[hh], off);
+    }
+    if (g8 == 0) {
+      red_l[warp][2 * tq] = ls[0];
+      red_l[warp][2 * tq + 1] = ls[1];
+    }
+    o[0] *= alpha[0];
+    o[1] *= alpha[1];
+    o[2] *= alpha[0];
+    o[3] *= alpha[1];
     float alpha_t = 1.f;
     if (tid < G) {
       float cmt = -INFINITY;
 #pragma unroll
-      for (int ww = 0; ww < 4; ++ww) cmt = fmaxf(cmt, red_m[ww * 8 + tid]);
+      for (int ww = 0; ww < kWarps; ++ww) cmt = fmaxf(cmt, red_m[ww][tid]);
       const float mtn = fmaxf(m_t, cmt);
       alpha_t = mtn == -INFINITY ? 1.f : exp2f(m_t - mtn);
       m_t = mtn;
@@ -345,44 +348,47 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
     if (tid < G) {
       float cl = 0.f;
 #pragma unroll
-      for (int ww = 0; ww < 4; ++ww) cl += red_l[ww * 8 + tid];
+      for (int ww = 0; ww < kWarps; ++ww) cl += red_l[ww][tid];
       l_t = l_t * alpha_t + cl;
     }
-    // ---- O += P V for this warp's 32 head-dim columns ---------------------
-#pragma unroll 2
-    for (int ks = 0; ks < kTcRows / 16; ++ks) {
-      unsigned ah0 = 0u, al0 = 0u, ah2 = 0u, al2 = 0u;
-      if (gq < G) {
-        const float2 p0 = *reinterpret_cast<const float2*>(Ps + gq * kTcRows + ks * 16 + 2 * tq);
-        const float2 p2 = *reinterpret_cast<const float2*>(Ps + gq * kTcRows + ks * 16 + 8 + 2 * tq);
-        split2(p0.x, p0.y, ah0, al0);
-        split2(p2.x, p2.y, ah2, al2);
-      }
-      const int vrow = ks * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+    // ---- O^T += V^T P for this warp's 16 dims --------------------------------
+    {
+      const unsigned vbase =
+          smem_u32(Vs + ((lane & 7) + ((lane >> 4) & 1) * 8) * kRowStride + dim0 + ((lane >> 3) & 1) * 8);
 #pragma unroll
-      for (int np = 0; np < 2; ++np) {
-        const unsigned addr = smem_u32(Vs + vrow * kRowStride + n0 + np * 16 + (lane >> 4) * 8);
-        unsigned b0, b1, b2, b3;
-        ldsm_x4_t(addr, b0, b1, b2, b3);
-        mma_bf16(o[2 * np], ah0, ah2, b0, b1);
-        mma_bf16(o[2 * np], al0, al2, b0, b1);
-        mma_bf16(o[2 * np + 1], ah0, ah2, b2, b3);
-        mma_bf16(o[2 * np + 1], al0, al2, b2, b3);
+      for (int ks = 0; ks < kTcRows / 16; ++ks) {
+        unsigned a0, a1, a2, a3;
+        ldsm_x4_t(vbase + ks * 16 * kRowStride * 2, a0, a1, a2, a3);
+        unsigned bh0 = 0u, bl0 = 0u, bh1 = 0u, bl1 = 0u;
+        if (g8 < G) {
+          const float2 p0 = *reinterpret_cast<const float2*>(Ps + g8 * kTcRows + ks * 16 + 2 * tq);
+          const float2 p1 = *reinterpret_cast<const float2*>(Ps + g8 * kTcRows + ks * 16 + 8 + 2 * tq);
+          split2(p0.x, p0.y, bh0, bl0);
+          split2(p1.x, p1.y, bh1, bl1);
+        }
+        asm volatile(
+            "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+            "{%0,%1,%2,%3};\n"
+            : "+f"(o[0]), "+f"(o[1]), "+f"(o[2]), "+f"(o[3])
+            : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(bh0), "r"(bh1));
+        asm volatile(
+            "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+            "{%0,%1,%2,%3};\n"
+            : "+f"(o[0]), "+f"(o[1]), "+f"(o[2]), "+f"(o[3])
+            : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(bl0), "r"(bl1));
       }
     }
-    if (tid == 0 && idx + kStages < n) expect_chunk(j0 + idx + kStages, s);
-    __syncthreads();  // stage s and Ps consumed; next expect_tx posted
+    __syncthreads();  // stage s and Ps consumed
     if (idx + kStages < n) issue_chunk(j0 + idx + kStages, s);
   }
   flush(cur);
   __syncthreads();
-  if (tid < kStages) asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&s_bar[tid])));
 
   // ---- merges of the heads I finished last (engine.py:231-246) ----------
   const int nm = s_nmerge;
   if (nm == 0) return;
   __threadfence();
-  float* ored = reinterpret_cast<float*>(KV);  // [4 warps][8 heads][128] scratch
+  float* ored = reinterpret_cast<float*>(KV);  // [warps][8 heads][128] scratch
   for (int mi = 0; mi < nm; ++mi) {
     const int bh = s_merge[mi];
     const int first = chunk_owner(prefix[bh], T, grid);
@@ -393,7 +399,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
     const float* vbar = v.value_means + (size_t)bh * v.cluster_cap * d;
     if (tid == 0) wl.counters[bh] = 0;  // self-reset for the next launch
     // (1) per head: max and normaliser over partials + approx pseudo-rows
-    for (int g = warp; g < G; g += 4) {
+    for (int g = warp; g < G; g += kWarps) {
       const double* lmh = kDense ? nullptr : lm + ((size_t)bh * G + g) * v.cluster_cap;
       float mloc = -INFINITY;
       for (int p = lane; p < nparts; p += 32) mloc = fmaxf(mloc, __ldcg(&pt.m[pbase + (size_t)p * G + g]));
@@ -422,7 +428,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
     float4 acc[8];
 #pragma unroll
     for (int g = 0; g < 8; ++g) acc[g] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int p = warp; p < nparts; p += 4) {
+    for (int p = warp; p < nparts; p += kWarps) {
 #pragma unroll
       for (int g = 0; g < 8; ++g) {
         if (g < G) {
@@ -433,7 +439,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
         }
       }
     }
-    for (int a = warp; a < na; a += 4) {
+    for (int a = warp; a < na; a += kWarps) {
       const int2 e = apx[a];
       const float4 vb = *(reinterpret_cast<const float4*>(vbar + (size_t)e.x * d) + lane);
       float lmv = 0.f;  // lane g fetches head g's log-mass, broadcast below
@@ -453,8 +459,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
     __syncthreads();
     for (int i = tid; i < G * d; i += kTcThreads) {
       const int g = i / d, c = i - g * d;
-      const float sum = ored[(0 * 8 + g) * d + c] + ored[(1 * 8 + g) * d + c] + ored[(2 * 8 + g) * d + c] +
-                        ored[(3 * 8 + g) * d + c];
+      float sum = 0.f;
+#pragma unroll
+      for (int ww = 0; ww < kWarps; ++ww) sum += ored[(ww * 8 + g) * d + c];
       out[((size_t)bh * G + g) * d + c] = sum / s_L[g];
     }
     if (tid < G) lse[(size_t)bh * G + tid] = s_M[tid] + __logf(s_L[tid]);
