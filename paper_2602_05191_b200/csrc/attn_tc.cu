@@ -1,6 +1,7 @@
 // Gathered split-KV decode attention for bf16 caches on tensor cores.
 //
-// Persistent: one CTA (8 warps) per SM.  The GQA-union rows of every
+// Persistent, warp-specialised: one CTA per SM = 8 compute warps + 1
+// producer warp.  The GQA-union rows of every
 // (sequence, kv head) form a global sequence of 128-row chunks (the plan /
 // worklist kernel publishes the per-head chunk prefix); CTA i owns the
 // contiguous range [i*T/grid, (i+1)*T/grid) of it -- balanced to +-1 chunk
@@ -30,7 +31,8 @@
 namespace dp {
 
 constexpr int kTcRows = kChunkRows;  // 128
-constexpr int kTcThreads = 256;  // 8 warps
+constexpr int kConsumers = 256;  // 8 compute warps
+constexpr int kTcThreads = kConsumers + 32;  // + 1 producer warp
 constexpr int kRowStride = 136;      // bf16 elements per staged row (272 B: conflict-free ldmatrix)
 constexpr int kStages = 3;
 constexpr int kStageElems = kTcRows * kRowStride;  // one K (or V) tile
@@ -80,6 +82,20 @@ __device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
 __device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(unsigned bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+// the mbarrier tracks completion of this thread's prior cp.async copies
+__device__ __forceinline__ void cp_async_arrive(unsigned bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
+}
+// 16-byte cp.async that writes zeros (src-size 0)
+__device__ __forceinline__ void cp16_zero(unsigned dst, const void* any) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, 0;\n" ::"r"(dst), "l"(any));
+}
+// barrier over the 8 compute warps only (the producer warp never joins)
+__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;\n" ::"n"(kConsumers) : "memory"); }
+
 __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
   asm volatile(
       "{\n .reg .pred p;\n"
@@ -113,7 +129,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
                                                                WorkLists wl, Partials<float> pt,
                                                                float* __restrict__ out, float* __restrict__ lse) {
   constexpr int d = 128;
-  constexpr int kWarps = kTcThreads / 32;
+  constexpr int kWarps = kConsumers / 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g8 = lane >> 2, tq = lane & 3;  // fragment row / column-pair
   const int BH = v.batch * v.kv_heads;
@@ -127,11 +143,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
   __shared__ float red_m[kWarps][8], red_l[kWarps][8];
   __shared__ float s_M[8], s_L[8];
   __shared__ int s_merge[4], s_nmerge;
+  __shared__ __align__(8) unsigned long long full_bar[kStages], empty_bar[kStages];
 
   // ---- chunk prefix over heads, my contiguous chunk range -----------------
   const int per_dense = (v.n_tokens + kTcRows - 1) / kTcRows;
   for (int b = tid; b <= BH; b += kTcThreads) prefix[b] = kDense ? b * per_dense : wl.chunk_prefix[b];
-  if (tid == 0) s_nmerge = 0;
+  if (tid == 0) {
+    s_nmerge = 0;
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(smem_u32(&full_bar[i]), 33);  // 32 async (cp.async) + 1 release arrive
+      mbar_init(smem_u32(&empty_bar[i]), kWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
   __syncthreads();
   const long long T = prefix[BH];
   const int j0 = (int)((long long)me * T / grid), j1 = (int)((long long)(me + 1) * T / grid);
@@ -146,48 +170,58 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
     return lo;
   };
 
-  // ---- producer: rows of global chunk j -> stage s (one cp.async group) ---
-  // thread t copies 16-B column `t & 15` of rows (t >> 4) + 16 i, i < 8, of
-  // both K and V; the ch == 0 thread of a row records its head mask
-  auto issue_chunk = [&](int j, int s) {
-    const int bh = head_of(j);
-    const int c = j - prefix[bh];
-    const int rows_total = kDense ? v.n_tokens : __ldg(&wl.nrows[bh]);
-    const int v0 = c * kTcRows;
-    const int nr = min(kTcRows, rows_total - v0);
-    const unsigned* ridx = reinterpret_cast<const unsigned*>(wl.rowidx) + (size_t)bh * v.row_cap + v0;
-    const size_t head_off = (size_t)bh * v.row_cap * d;
-    const __nv_bfloat16* Kg = reinterpret_cast<const __nv_bfloat16*>(v.keys) + head_off;
-    const __nv_bfloat16* Vg = reinterpret_cast<const __nv_bfloat16*>(v.values) + head_off;
-    __nv_bfloat16* Ks = KV + (size_t)s * 2 * kStageElems;
-    __nv_bfloat16* Vs = Ks + kStageElems;
-    const int ch = tid & 15;
-    unsigned e[8];
+  // ---- producer warp: runs up to kStages chunks ahead ---------------------
+  if (warp == kWarps) {
+    const int ch = lane & 15;
+    for (int idx = 0; idx < n; ++idx) {
+      const int s = idx % kStages;
+      if (idx >= kStages) mbar_wait(smem_u32(&empty_bar[s]), (unsigned)(((idx / kStages) + 1) & 1));
+      const int j = j0 + idx;
+      const int bh = head_of(j);
+      const int c = j - prefix[bh];
+      const int rows_total = kDense ? v.n_tokens : __ldg(&wl.nrows[bh]);
+      const int v0 = c * kTcRows;
+      const int nr = min(kTcRows, rows_total - v0);
+      const unsigned* ridx = reinterpret_cast<const unsigned*>(wl.rowidx) + (size_t)bh * v.row_cap + v0;
+      unsigned e[4];  // row entries of rows lane + 32 i
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int row = (tid >> 4) + 16 * i;
-      e[i] = row < nr ? (kDense ? (((unsigned)((1 << G) - 1)) << 24) | (unsigned)(v0 + row) : __ldg(&ridx[row]))
-                      : 0xFFFFFFFFu;
-    }
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int row = (tid >> 4) + 16 * i;
-      __nv_bfloat16* kd = Ks + row * kRowStride + ch * 8;
-      __nv_bfloat16* vd = Vs + row * kRowStride + ch * 8;
-      if (e[i] != 0xFFFFFFFFu) {
-        const size_t off = (size_t)(e[i] & 0xFFFFFFu) * d + ch * 8;
-        cp16(smem_u32(kd), Kg + off);
-        cp16(smem_u32(vd), Vg + off);
-      } else {
-        *reinterpret_cast<int4*>(kd) = make_int4(0, 0, 0, 0);
-        *reinterpret_cast<int4*>(vd) = make_int4(0, 0, 0, 0);
+      for (int i = 0; i < 4; ++i) {
+        const int row = lane + 32 * i;
+        e[i] = row < nr ? (kDense ? (((unsigned)((1 << G) - 1)) << 24) | (unsigned)(v0 + row) : __ldg(&ridx[row]))
+                        : 0xFFFFFFFFu;
+        rmask[s * kTcRows + row] = e[i] == 0xFFFFFFFFu ? 0 : (int)(e[i] >> 24);
       }
-      if (ch == 0) rmask[s * kTcRows + row] = e[i] == 0xFFFFFFFFu ? 0 : (int)(e[i] >> 24);
+      const size_t head_off = (size_t)bh * v.row_cap * d;
+      const __nv_bfloat16* Kg = reinterpret_cast<const __nv_bfloat16*>(v.keys) + head_off;
+      const __nv_bfloat16* Vg = reinterpret_cast<const __nv_bfloat16*>(v.values) + head_off;
+      __nv_bfloat16* Ks = KV + (size_t)s * 2 * kStageElems;
+      __nv_bfloat16* Vs = Ks + kStageElems;
+      // lane copies 16-B column `ch` of rows (lane >> 4) + 2 r: a warp
+      // instruction moves 2 rows = 512 contiguous bytes
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+#pragma unroll 4
+        for (int r = 0; r < 16; ++r) {
+          const int row = (lane >> 4) + 2 * (16 * i + r);
+          const unsigned er = __shfl_sync(0xffffffffu, e[i], ((lane >> 4) + 2 * r) & 31);
+          const unsigned kd = smem_u32(Ks + row * kRowStride + ch * 8);
+          const unsigned vd = smem_u32(Vs + row * kRowStride + ch * 8);
+          if (er != 0xFFFFFFFFu) {
+            const size_t off = (size_t)(er & 0xFFFFFFu) * d + ch * 8;
+            cp16(kd, Kg + off);
+            cp16(vd, Vg + off);
+          } else {
+            cp16_zero(kd, Kg);
+            cp16_zero(vd, Vg);
+          }
+        }
+      }
+      cp_async_arrive(smem_u32(&full_bar[s]));  // completes when this lane's copies land
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&full_bar[s]));  // releases the rmask stores
     }
-    asm volatile("cp.async.commit_group;\n" ::);
-  };
-
-  for (int i = 0; i < kStages && i < n; ++i) issue_chunk(j0 + i, i);  // fill the ring
+    return;
+  }
 
   // Q^T B-fragments (registers): b0 = Q[head g8][k*16 + 2tq ..], b1 = Q[head g8][k*16 + 8 + 2tq ..]
   unsigned qa[8][2], qb[8][2];  // hi, lo
@@ -236,17 +270,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
       if (h < G) pt.o[(pbase + (size_t)slot * G + h) * d + dd] = o[e];
     }
     __threadfence();
-    __syncthreads();
+    consumers_sync();
     if (tid == 0 && atomicAdd(&wl.counters[bh], 1) == nparts - 1) s_merge[s_nmerge++] = bh;
   };
 
   for (int idx = 0; idx < n; ++idx) {
     const int j = j0 + idx, s = idx % kStages;
     const int bh = head_of(j);
-    const int ahead = min(kStages - 1, n - 1 - idx);  // groups committed after chunk idx
-    if (ahead >= 2) asm volatile("cp.async.wait_group 2;\n" ::: "memory");
-    else if (ahead == 1) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-    else asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     if (bh != cur) {
       if (cur >= 0) flush(cur);
       cur = bh;
@@ -257,7 +287,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
       m_t = -INFINITY;
       l_t = 0.f;
     }
-    __syncthreads();  // stage s landed for every thread
+    mbar_wait(smem_u32(&full_bar[s]), (unsigned)((idx / kStages) & 1));  // stage s landed
     const __nv_bfloat16* Ks = KV + (size_t)s * 2 * kStageElems;
     const __nv_bfloat16* Vs = Ks + kStageElems;
     const int* rm = rmask + s * kTcRows;
@@ -303,7 +333,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
       red_m[warp][2 * tq] = mx[0];
       red_m[warp][2 * tq + 1] = mx[1];
     }
-    __syncthreads();
+    consumers_sync();
     float alpha[2];
 #pragma unroll
     for (int hh = 0; hh < 2; ++hh) {
@@ -344,7 +374,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
       alpha_t = mtn == -INFINITY ? 1.f : exp2f(m_t - mtn);
       m_t = mtn;
     }
-    __syncthreads();  // Ps, red_l visible
+    consumers_sync();  // Ps, red_l visible
     if (tid < G) {
       float cl = 0.f;
 #pragma unroll
@@ -378,11 +408,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
             : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(bl0), "r"(bl1));
       }
     }
-    __syncthreads();  // stage s and Ps consumed
-    if (idx + kStages < n) issue_chunk(j0 + idx + kStages, s);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(smem_u32(&empty_bar[s]));  // stage s free for the producer
   }
   flush(cur);
-  __syncthreads();
+  consumers_sync();
 
   // ---- merges of the heads I finished last (engine.py:231-246) ----------
   const int nm = s_nmerge;
@@ -423,7 +453,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
         s_L[g] = L;
       }
     }
-    __syncthreads();
+    consumers_sync();
     // (2) weighted sums: warps stride over partials and approx rows, lanes over d
     float4 acc[8];
 #pragma unroll
@@ -456,8 +486,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
 #pragma unroll
     for (int g = 0; g < 8; ++g)
       if (g < G) reinterpret_cast<float4*>(ored + ((size_t)warp * 8 + g) * d)[lane] = acc[g];
-    __syncthreads();
-    for (int i = tid; i < G * d; i += kTcThreads) {
+    consumers_sync();
+    for (int i = tid; i < G * d; i += kConsumers) {
       const int g = i / d, c = i - g * d;
       float sum = 0.f;
 #pragma unroll
@@ -465,7 +495,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
       out[((size_t)bh * G + g) * d + c] = sum / s_L[g];
     }
     if (tid < G) lse[(size_t)bh * G + tid] = s_M[tid] + __logf(s_L[tid]);
-    __syncthreads();
+    consumers_sync();
   }
 }
 
