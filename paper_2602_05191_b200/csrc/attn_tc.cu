@@ -32,7 +32,8 @@ namespace dp {
 
 constexpr int kTcRows = kChunkRows;  // 128
 constexpr int kConsumers = 256;  // 8 compute warps
-constexpr int kTcThreads = kConsumers + 32;  // + 1 producer warp
+constexpr int kProducers = 2;  // producer warps, 64 rows each
+constexpr int kTcThreads = kConsumers + 32 * kProducers;
 constexpr int kRowStride = 136;      // bf16 elements per staged row (272 B: conflict-free ldmatrix)
 constexpr int kStages = 3;
 constexpr int kStageElems = kTcRows * kRowStride;  // one K (or V) tile
@@ -151,7 +152,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
   if (tid == 0) {
     s_nmerge = 0;
     for (int i = 0; i < kStages; ++i) {
-      mbar_init(smem_u32(&full_bar[i]), 33);  // 32 async (cp.async) + 1 release arrive
+      mbar_init(smem_u32(&full_bar[i]), 33 * kProducers);  // per producer warp: 32 async + 1 release
       mbar_init(smem_u32(&empty_bar[i]), kWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -170,9 +171,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
     return lo;
   };
 
-  // ---- producer warp: runs up to kStages chunks ahead ---------------------
-  if (warp == kWarps) {
-    const int ch = lane & 15;
+  // ---- producer warps (rows [64p, 64p+64) each): run up to kStages ahead -
+  if (warp >= kWarps) {
+    const int ch = lane & 15, pr0 = (warp - kWarps) * 64;
     for (int idx = 0; idx < n; ++idx) {
       const int s = idx % kStages;
       if (idx >= kStages) mbar_wait(smem_u32(&empty_bar[s]), (unsigned)(((idx / kStages) + 1) & 1));
@@ -183,10 +184,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
       const int v0 = c * kTcRows;
       const int nr = min(kTcRows, rows_total - v0);
       const unsigned* ridx = reinterpret_cast<const unsigned*>(wl.rowidx) + (size_t)bh * v.row_cap + v0;
-      unsigned e[4];  // row entries of rows lane + 32 i
+      unsigned e[2];  // row entries of rows pr0 + lane + 32 i
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int row = lane + 32 * i;
+      for (int i = 0; i < 2; ++i) {
+        const int row = pr0 + lane + 32 * i;
         e[i] = row < nr ? (kDense ? (((unsigned)((1 << G) - 1)) << 24) | (unsigned)(v0 + row) : __ldg(&ridx[row]))
                         : 0xFFFFFFFFu;
         rmask[s * kTcRows + row] = e[i] == 0xFFFFFFFFu ? 0 : (int)(e[i] >> 24);
@@ -199,10 +200,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
       // lane copies 16-B column `ch` of rows (lane >> 4) + 2 r: a warp
       // instruction moves 2 rows = 512 contiguous bytes
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
+      for (int i = 0; i < 2; ++i) {
 #pragma unroll 4
         for (int r = 0; r < 16; ++r) {
-          const int row = (lane >> 4) + 2 * (16 * i + r);
+          const int row = pr0 + (lane >> 4) + 2 * (16 * i + r);
           const unsigned er = __shfl_sync(0xffffffffu, e[i], ((lane >> 4) + 2 * r) & 31);
           const unsigned kd = smem_u32(Ks + row * kRowStride + ch * 8);
           const unsigned vd = smem_u32(Vs + row * kRowStride + ch * 8);
@@ -415,74 +416,147 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
   consumers_sync();
 
   // ---- merges of the heads I finished last (engine.py:231-246) ----------
+  // Stage partial stats and approx entries in smem, then issue every
+  // partial-o / value-mean load independently (addresses come from smem) so
+  // the merge costs a few memory round trips, not one per row.
   const int nm = s_nmerge;
   if (nm == 0) return;
   __threadfence();
-  float* ored = reinterpret_cast<float*>(KV);  // [warps][8 heads][128] scratch
+  constexpr int kMaxParts = 256, kApb = 1024;
+  float* ored = reinterpret_cast<float*>(KV);        // [warps][8 heads][d]
+  float* s_pm = ored + kWarps * 8 * d;               // [8][kMaxParts] partial m
+  float* s_pw = s_pm + 8 * kMaxParts;                // [8][kMaxParts] partial l -> weight
+  int2* s_apx = reinterpret_cast<int2*>(s_pw + 8 * kMaxParts);  // [kApb]
+  float* s_aw = reinterpret_cast<float*>(s_apx + kApb);         // [8][kApb]
+  __shared__ float s_am[kWarps][8];
   for (int mi = 0; mi < nm; ++mi) {
     const int bh = s_merge[mi];
     const int first = chunk_owner(prefix[bh], T, grid);
-    const int nparts = chunk_owner(prefix[bh + 1] - 1, T, grid) - first + 1;
+    const int nparts = min(kMaxParts, chunk_owner(prefix[bh + 1] - 1, T, grid) - first + 1);
     const size_t pbase = (size_t)bh * pt.max_chunks * G;
     const int na = kDense ? 0 : wl.napprox[bh];
     const int2* apx = wl.approx + (size_t)bh * v.cluster_cap;
     const float* vbar = v.value_means + (size_t)bh * v.cluster_cap * d;
+    const double* lmb = kDense ? nullptr : lm + (size_t)bh * G * v.cluster_cap;
     if (tid == 0) wl.counters[bh] = 0;  // self-reset for the next launch
-    // (1) per head: max and normaliser over partials + approx pseudo-rows
+    // (1) partial stats -> smem; per-thread maxima of the approx log-masses
+    for (int i = tid; i < G * nparts; i += kConsumers) {
+      const int g = i / nparts, p = i - g * nparts;
+      s_pm[g * kMaxParts + p] = __ldcg(&pt.m[pbase + (size_t)p * G + g]);
+      s_pw[g * kMaxParts + p] = __ldcg(&pt.l[pbase + (size_t)p * G + g]);
+    }
+    float am[8];
+#pragma unroll
+    for (int g = 0; g < 8; ++g) am[g] = -INFINITY;
+    for (int a = tid; a < na; a += kConsumers) {
+      const int2 e = apx[a];
+#pragma unroll
+      for (int g = 0; g < 8; ++g)
+        if (g < G && ((e.y >> g) & 1)) am[g] = fmaxf(am[g], (float)lmb[(size_t)g * v.cluster_cap + e.x]);
+    }
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+      const float m = warp_max(am[g]);
+      if (lane == 0) s_am[warp][g] = m;
+    }
+    consumers_sync();
+    // (2) per head: global max M, partial weights, partial part of L
     for (int g = warp; g < G; g += kWarps) {
-      const double* lmh = kDense ? nullptr : lm + ((size_t)bh * G + g) * v.cluster_cap;
-      float mloc = -INFINITY;
-      for (int p = lane; p < nparts; p += 32) mloc = fmaxf(mloc, __ldcg(&pt.m[pbase + (size_t)p * G + g]));
-      for (int a = lane; a < na; a += 32) {
-        const int2 e = apx[a];
-        if ((e.y >> g) & 1) mloc = fmaxf(mloc, (float)lmh[e.x]);
-      }
+      float mloc = lane < kWarps ? s_am[lane][g] : -INFINITY;
+      for (int p = lane; p < nparts; p += 32) mloc = fmaxf(mloc, s_pm[g * kMaxParts + p]);
       const float M = warp_max(mloc);
       float lloc = 0.f;
       for (int p = lane; p < nparts; p += 32) {
-        const float mp = __ldcg(&pt.m[pbase + (size_t)p * G + g]);
-        if (mp != -INFINITY) lloc += __ldcg(&pt.l[pbase + (size_t)p * G + g]) * __expf(mp - M);
+        const float mp = s_pm[g * kMaxParts + p];
+        const float w = mp == -INFINITY ? 0.f : __expf(mp - M);
+        lloc += s_pw[g * kMaxParts + p] * w;
+        s_pw[g * kMaxParts + p] = w;
       }
-      for (int a = lane; a < na; a += 32) {
-        const int2 e = apx[a];
-        if ((e.y >> g) & 1) lloc += __expf((float)lmh[e.x] - M);
-      }
-      const float L = warp_sum(lloc);
+      lloc = warp_sum(lloc);
       if (lane == 0) {
         s_M[g] = M;
-        s_L[g] = L;
+        s_L[g] = lloc;
       }
     }
     consumers_sync();
-    // (2) weighted sums: warps stride over partials and approx rows, lanes over d
     float4 acc[8];
 #pragma unroll
     for (int g = 0; g < 8; ++g) acc[g] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int p = warp; p < nparts; p += kWarps) {
+    // (3) partials: warp-strided, 2 partials (x G heads) in flight per lane
+    for (int p0 = warp; p0 < nparts; p0 += 2 * kWarps) {
+      float4 op[2][8];
 #pragma unroll
-      for (int g = 0; g < 8; ++g) {
-        if (g < G) {
-          const float mp = __ldcg(&pt.m[pbase + (size_t)p * G + g]);
-          const float4 op = __ldcg(reinterpret_cast<const float4*>(pt.o + (pbase + (size_t)p * G + g) * d) + lane);
-          const float w = mp == -INFINITY ? 0.f : __expf(mp - s_M[g]);
-          acc[g].x += w * op.x; acc[g].y += w * op.y; acc[g].z += w * op.z; acc[g].w += w * op.w;
+      for (int u = 0; u < 2; ++u) {
+        const int p = p0 + u * kWarps;
+#pragma unroll
+        for (int g = 0; g < 8; ++g)
+          op[u][g] = (p < nparts && g < G)
+                         ? __ldcg(reinterpret_cast<const float4*>(pt.o + (pbase + (size_t)p * G + g) * d) + lane)
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int p = p0 + u * kWarps;
+        if (p < nparts) {
+#pragma unroll
+          for (int g = 0; g < 8; ++g) {
+            if (g < G) {
+              const float w = s_pw[g * kMaxParts + p];
+              acc[g].x += w * op[u][g].x; acc[g].y += w * op[u][g].y;
+              acc[g].z += w * op[u][g].z; acc[g].w += w * op[u][g].w;
+            }
+          }
         }
       }
     }
-    for (int a = warp; a < na; a += kWarps) {
-      const int2 e = apx[a];
-      const float4 vb = *(reinterpret_cast<const float4*>(vbar + (size_t)e.x * d) + lane);
-      float lmv = 0.f;  // lane g fetches head g's log-mass, broadcast below
-      if (lane < G && ((e.y >> lane) & 1)) lmv = (float)lm[((size_t)bh * G + lane) * v.cluster_cap + e.x];
+    // (4) approx pseudo-rows in batches of kApb
+    for (int b0 = 0; b0 < na; b0 += kApb) {
+      const int nb = min(kApb, na - b0);
+      consumers_sync();
+      for (int a = tid; a < nb; a += kConsumers) s_apx[a] = apx[b0 + a];
+      consumers_sync();
+      for (int i = tid; i < G * nb; i += kConsumers) {
+        const int g = i / nb, a = i - g * nb;
+        const int2 e = s_apx[a];
+        s_aw[g * kApb + a] = ((e.y >> g) & 1) ? __expf((float)lmb[(size_t)g * v.cluster_cap + e.x] - s_M[g]) : 0.f;
+      }
+      consumers_sync();
+      float lloc[8];
+#pragma unroll
+      for (int g = 0; g < 8; ++g) lloc[g] = 0.f;
+      for (int a = tid; a < nb; a += kConsumers)
+#pragma unroll
+        for (int g = 0; g < 8; ++g)
+          if (g < G) lloc[g] += s_aw[g * kApb + a];
 #pragma unroll
       for (int g = 0; g < 8; ++g) {
-        const float lg = __shfl_sync(0xffffffffu, lmv, g);
-        if (g < G && ((e.y >> g) & 1)) {
-          const float w = __expf(lg - s_M[g]);
-          acc[g].x += w * vb.x; acc[g].y += w * vb.y; acc[g].z += w * vb.z; acc[g].w += w * vb.w;
+        const float t = warp_sum(lloc[g]);
+        if (lane == 0 && g < G) atomicAdd(&s_L[g], t);
+      }
+      for (int a0 = warp; a0 < nb; a0 += 8 * kWarps) {
+        float4 vb[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int a = a0 + u * kWarps;
+          vb[u] = a < nb ? *(reinterpret_cast<const float4*>(vbar + (size_t)s_apx[a].x * d) + lane)
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int a = a0 + u * kWarps;
+          if (a < nb) {
+#pragma unroll
+            for (int g = 0; g < 8; ++g) {
+              if (g < G) {
+                const float w = s_aw[g * kApb + a];
+                acc[g].x += w * vb[u].x; acc[g].y += w * vb[u].y; acc[g].z += w * vb[u].z; acc[g].w += w * vb[u].w;
+              }
+            }
+          }
         }
       }
     }
+    // (5) reduce over warps, normalise
 #pragma unroll
     for (int g = 0; g < 8; ++g)
       if (g < G) reinterpret_cast<float4*>(ored + ((size_t)warp * 8 + g) * d)[lane] = acc[g];
