@@ -119,10 +119,12 @@ int dp_sparse_attention(const dp_cache_view* v, const void* q, int32_t q_dtype,
 
 /* The two halves of dp_sparse_attention, for callers that time or overlap
  * them separately: dp_build_worklist turns the per-head states into the
- * GQA-union row runs / approx lists (in the workspace); dp_attend runs the
+ * GQA-union rows / approx lists and each q head's approx partial (in the
+ * workspace); dp_attend runs the
  * gathered split-KV attention + LSE merge over them. */
-int dp_build_worklist(const dp_cache_view* v, int32_t gqa_group, const uint8_t* state,
-                      int32_t* stats, void* workspace, size_t workspace_bytes, void* stream);
+int dp_build_worklist(const dp_cache_view* v, int32_t gqa_group, const double* log_mass,
+                      const uint8_t* state, int32_t* stats, void* workspace,
+                      size_t workspace_bytes, void* stream);
 int dp_attend(const dp_cache_view* v, const void* q, int32_t q_dtype, int32_t gqa_group,
               double scale, const double* log_mass, float* out, float* lse, void* workspace,
               size_t workspace_bytes, void* stream);
@@ -203,6 +205,10 @@ int dp_cluster_build(const dp_cluster_params* p, const void* src_keys, const voi
 /* Profiling aid: %globaltimer stamps (ns) of the last dp_plan launch's first
  * cluster, [8 ranks][8 phase events], copied to host memory. */
 int dp_debug_plan_timing(unsigned long long* out); /* [8][16] */
+/* Profiling aid: per-CTA %globaltimer stamps of the last bf16 attention
+ * launch, [512 CTAs][8 events]: start, prefix loaded, first stage landed,
+ * main loop done, flushed, exit. */
+int dp_debug_attn_timing(unsigned long long* out);
 
 /* Lower-level pieces of the above (used by the parity tests). */
 /* k-means++ picks only: picks int32 [B*H, k]. */

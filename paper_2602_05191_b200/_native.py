@@ -56,13 +56,14 @@ _SIGS = {
     "dp_sparse_attention": (ctypes.c_int, [ctypes.POINTER(CacheView), _vp, ctypes.c_int32,
                                            ctypes.c_int32, ctypes.c_double, _vp, _vp, _vp, _vp, _vp,
                                            _vp, ctypes.c_size_t, _vp]),
-    "dp_build_worklist": (ctypes.c_int, [ctypes.POINTER(CacheView), ctypes.c_int32, _vp, _vp, _vp,
+    "dp_build_worklist": (ctypes.c_int, [ctypes.POINTER(CacheView), ctypes.c_int32, _vp, _vp, _vp, _vp,
                                          ctypes.c_size_t, _vp]),
     "dp_attend": (ctypes.c_int, [ctypes.POINTER(CacheView), _vp, ctypes.c_int32, ctypes.c_int32,
                                  ctypes.c_double, _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp]),
     "dp_plan": (ctypes.c_int, [ctypes.POINTER(CacheView), _vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_double,
                                ctypes.c_double, ctypes.c_double, _vp, _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp]),
     "dp_debug_plan_timing": (ctypes.c_int, [_vp]),
+    "dp_debug_attn_timing": (ctypes.c_int, [_vp]),
     "dp_decode_step": (ctypes.c_int, [ctypes.POINTER(CacheView), _vp, ctypes.c_int32, ctypes.c_int32,
                                       ctypes.c_double, ctypes.c_double, ctypes.c_double, _vp, _vp,
                                       _vp, _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp]),

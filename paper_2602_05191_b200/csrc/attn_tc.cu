@@ -111,6 +111,17 @@ __device__ __forceinline__ void bulk_row(unsigned dst, const void* src, unsigned
                : "memory");
 }
 
+// per-CTA phase stamps (%globaltimer ns) of the last launch; profiling aid,
+// read with dp_debug_attn_timing()
+__device__ unsigned long long g_attn_ts[512][8];
+__device__ __forceinline__ void astamp(int ev) {
+  if (threadIdx.x == 0 && blockIdx.x < 512) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_attn_ts[blockIdx.x][ev] = t;
+  }
+}
+
 // owner CTA of global chunk j when T chunks are split evenly over `grid`
 // CTAs as [i*T/grid, (i+1)*T/grid)
 __device__ __forceinline__ int chunk_owner(long long j, long long T, int grid) {
@@ -147,6 +158,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
   __shared__ __align__(8) unsigned long long full_bar[kStages], empty_bar[kStages];
 
   // ---- chunk prefix over heads, my contiguous chunk range -----------------
+  astamp(0);
   const int per_dense = (v.n_tokens + kTcRows - 1) / kTcRows;
   for (int b = tid; b <= BH; b += kTcThreads) prefix[b] = kDense ? b * per_dense : wl.chunk_prefix[b];
   if (tid == 0) {
@@ -158,6 +170,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
+  astamp(1);
   const long long T = prefix[BH];
   const int j0 = (int)((long long)me * T / grid), j1 = (int)((long long)(me + 1) * T / grid);
   const int n = j1 - j0;
@@ -289,6 +302,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
       l_t = 0.f;
     }
     mbar_wait(smem_u32(&full_bar[s]), (unsigned)((idx / kStages) & 1));  // stage s landed
+    if (idx == 0) astamp(2);
     const __nv_bfloat16* Ks = KV + (size_t)s * 2 * kStageElems;
     const __nv_bfloat16* Vs = Ks + kStageElems;
     const int* rm = rmask + s * kTcRows;
@@ -412,57 +426,38 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
     __syncwarp();
     if (lane == 0) mbar_arrive(smem_u32(&empty_bar[s]));  // stage s free for the producer
   }
+  astamp(3);
   flush(cur);
   consumers_sync();
+  astamp(4);
 
   // ---- merges of the heads I finished last (engine.py:231-246) ----------
-  // Stage partial stats and approx entries in smem, then issue every
-  // partial-o / value-mean load independently (addresses come from smem) so
-  // the merge costs a few memory round trips, not one per row.
+  // partials of every CTA that touched the head + the plan's approx partial
+  // (approximated clusters: logit = log-mass, value = value mean)
   const int nm = s_nmerge;
   if (nm == 0) return;
   __threadfence();
-  constexpr int kMaxParts = 256, kApb = 1024;
+  constexpr int kMaxParts = 256;
   float* ored = reinterpret_cast<float*>(KV);        // [warps][8 heads][d]
   float* s_pm = ored + kWarps * 8 * d;               // [8][kMaxParts] partial m
   float* s_pw = s_pm + 8 * kMaxParts;                // [8][kMaxParts] partial l -> weight
-  int2* s_apx = reinterpret_cast<int2*>(s_pw + 8 * kMaxParts);  // [kApb]
-  float* s_aw = reinterpret_cast<float*>(s_apx + kApb);         // [8][kApb]
-  __shared__ float s_am[kWarps][8];
+  __shared__ float s_aw[8];
   for (int mi = 0; mi < nm; ++mi) {
     const int bh = s_merge[mi];
     const int first = chunk_owner(prefix[bh], T, grid);
     const int nparts = min(kMaxParts, chunk_owner(prefix[bh + 1] - 1, T, grid) - first + 1);
     const size_t pbase = (size_t)bh * pt.max_chunks * G;
-    const int na = kDense ? 0 : wl.napprox[bh];
-    const int2* apx = wl.approx + (size_t)bh * v.cluster_cap;
-    const float* vbar = v.value_means + (size_t)bh * v.cluster_cap * d;
-    const double* lmb = kDense ? nullptr : lm + (size_t)bh * G * v.cluster_cap;
     if (tid == 0) wl.counters[bh] = 0;  // self-reset for the next launch
-    // (1) partial stats -> smem; per-thread maxima of the approx log-masses
     for (int i = tid; i < G * nparts; i += kConsumers) {
       const int g = i / nparts, p = i - g * nparts;
       s_pm[g * kMaxParts + p] = __ldcg(&pt.m[pbase + (size_t)p * G + g]);
       s_pw[g * kMaxParts + p] = __ldcg(&pt.l[pbase + (size_t)p * G + g]);
     }
-    float am[8];
-#pragma unroll
-    for (int g = 0; g < 8; ++g) am[g] = -INFINITY;
-    for (int a = tid; a < na; a += kConsumers) {
-      const int2 e = apx[a];
-#pragma unroll
-      for (int g = 0; g < 8; ++g)
-        if (g < G && ((e.y >> g) & 1)) am[g] = fmaxf(am[g], (float)lmb[(size_t)g * v.cluster_cap + e.x]);
-    }
-#pragma unroll
-    for (int g = 0; g < 8; ++g) {
-      const float m = warp_max(am[g]);
-      if (lane == 0) s_am[warp][g] = m;
-    }
     consumers_sync();
-    // (2) per head: global max M, partial weights, partial part of L
     for (int g = warp; g < G; g += kWarps) {
-      float mloc = lane < kWarps ? s_am[lane][g] : -INFINITY;
+      const float* ap = wl.apart + ((size_t)bh * G + g) * (2 + d);
+      const float ma = kDense ? -INFINITY : __ldcg(&ap[0]);
+      float mloc = ma;
       for (int p = lane; p < nparts; p += 32) mloc = fmaxf(mloc, s_pm[g * kMaxParts + p]);
       const float M = warp_max(mloc);
       float lloc = 0.f;
@@ -474,15 +469,25 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
       }
       lloc = warp_sum(lloc);
       if (lane == 0) {
+        const float wa = ma == -INFINITY ? 0.f : __expf(ma - M);
+        s_aw[g] = wa;
         s_M[g] = M;
-        s_L[g] = lloc;
+        s_L[g] = lloc + (wa > 0.f ? wa * __ldcg(&ap[1]) : 0.f);
       }
     }
     consumers_sync();
     float4 acc[8];
 #pragma unroll
     for (int g = 0; g < 8; ++g) acc[g] = make_float4(0.f, 0.f, 0.f, 0.f);
-    // (3) partials: warp-strided, 2 partials (x G heads) in flight per lane
+    if (!kDense && warp == 0) {  // the approx partial
+#pragma unroll
+      for (int g = 0; g < 8; ++g)
+        if (g < G && s_aw[g] > 0.f) {
+          const float4 oa = __ldcg(reinterpret_cast<const float4*>(wl.apart + ((size_t)bh * G + g) * (2 + d) + 2) + lane);
+          acc[g].x = s_aw[g] * oa.x; acc[g].y = s_aw[g] * oa.y; acc[g].z = s_aw[g] * oa.z; acc[g].w = s_aw[g] * oa.w;
+        }
+    }
+    // partials: warp-strided, 2 partials (x G heads) in flight per lane
     for (int p0 = warp; p0 < nparts; p0 += 2 * kWarps) {
       float4 op[2][8];
 #pragma unroll
@@ -509,54 +514,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
         }
       }
     }
-    // (4) approx pseudo-rows in batches of kApb
-    for (int b0 = 0; b0 < na; b0 += kApb) {
-      const int nb = min(kApb, na - b0);
-      consumers_sync();
-      for (int a = tid; a < nb; a += kConsumers) s_apx[a] = apx[b0 + a];
-      consumers_sync();
-      for (int i = tid; i < G * nb; i += kConsumers) {
-        const int g = i / nb, a = i - g * nb;
-        const int2 e = s_apx[a];
-        s_aw[g * kApb + a] = ((e.y >> g) & 1) ? __expf((float)lmb[(size_t)g * v.cluster_cap + e.x] - s_M[g]) : 0.f;
-      }
-      consumers_sync();
-      float lloc[8];
-#pragma unroll
-      for (int g = 0; g < 8; ++g) lloc[g] = 0.f;
-      for (int a = tid; a < nb; a += kConsumers)
-#pragma unroll
-        for (int g = 0; g < 8; ++g)
-          if (g < G) lloc[g] += s_aw[g * kApb + a];
-#pragma unroll
-      for (int g = 0; g < 8; ++g) {
-        const float t = warp_sum(lloc[g]);
-        if (lane == 0 && g < G) atomicAdd(&s_L[g], t);
-      }
-      for (int a0 = warp; a0 < nb; a0 += 8 * kWarps) {
-        float4 vb[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int a = a0 + u * kWarps;
-          vb[u] = a < nb ? *(reinterpret_cast<const float4*>(vbar + (size_t)s_apx[a].x * d) + lane)
-                         : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int a = a0 + u * kWarps;
-          if (a < nb) {
-#pragma unroll
-            for (int g = 0; g < 8; ++g) {
-              if (g < G) {
-                const float w = s_aw[g * kApb + a];
-                acc[g].x += w * vb[u].x; acc[g].y += w * vb[u].y; acc[g].z += w * vb[u].z; acc[g].w += w * vb[u].w;
-              }
-            }
-          }
-        }
-      }
-    }
-    // (5) reduce over warps, normalise
 #pragma unroll
     for (int g = 0; g < 8; ++g)
       if (g < G) reinterpret_cast<float4*>(ored + ((size_t)warp * 8 + g) * d)[lane] = acc[g];
@@ -571,8 +528,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
     if (tid < G) lse[(size_t)bh * G + tid] = s_M[tid] + __logf(s_L[tid]);
     consumers_sync();
   }
+  astamp(5);
 }
 
+}  // namespace dp
+extern "C" int dp_debug_attn_timing(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, dp::g_attn_ts, sizeof(dp::g_attn_ts)) == cudaSuccess ? 0 : 2;  // [512][8]
+}
+namespace dp {
 size_t attn_tc_smem_bytes(int BH) { return TcSmem::fixed + (size_t)(BH + 1) * 4; }
 
 template <bool kDense, bool kQF32>

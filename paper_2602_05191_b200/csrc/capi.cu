@@ -91,12 +91,12 @@ int dp_select(const dp_cache_view* v, int32_t G, double p1, double p2, const dou
   return e == cudaSuccess ? DP_OK : cuda_fail(e, "dp_select");
 }
 
-int dp_build_worklist(const dp_cache_view* v, int32_t G, const uint8_t* state, int32_t* stats, void* ws,
-                      size_t ws_bytes, void* stream) {
+int dp_build_worklist(const dp_cache_view* v, int32_t G, const double* log_mass, const uint8_t* state,
+                      int32_t* stats, void* ws, size_t ws_bytes, void* stream) {
   int r = check_view(v, G);
   if (r) return r;
   if (ws_bytes < dp_decode_workspace_bytes(v, G)) return fail(DP_ERR_INVALID, "workspace too small");
-  cudaError_t e = dp::launch_worklist(*v, G, state, stats, ws, (cudaStream_t)stream);
+  cudaError_t e = dp::launch_worklist(*v, G, state, stats, ws, (cudaStream_t)stream, log_mass);
   return e == cudaSuccess ? DP_OK : cuda_fail(e, "dp_build_worklist");
 }
 
@@ -113,7 +113,7 @@ int dp_attend(const dp_cache_view* v, const void* q, int32_t q_dtype, int32_t G,
 int dp_sparse_attention(const dp_cache_view* v, const void* q, int32_t q_dtype, int32_t G, double scale,
                         const double* log_mass, const uint8_t* state, float* out, float* lse, int32_t* stats,
                         void* ws, size_t ws_bytes, void* stream) {
-  int r = dp_build_worklist(v, G, state, stats, ws, ws_bytes, stream);
+  int r = dp_build_worklist(v, G, log_mass, state, stats, ws, ws_bytes, stream);
   if (r) return r;
   return dp_attend(v, q, q_dtype, G, scale, log_mass, out, lse, ws, ws_bytes, stream);
 }

@@ -527,6 +527,7 @@ size_t decode_ws_layout(const dp_cache_view* v, int G, WorkLists* wl, void** par
   char* ctr = take(BH * sizeof(int));
   char* cpre = take((BH + 1) * sizeof(int));
   char* dn = take(sizeof(int));
+  char* ap = take(BH * (size_t)G * (2 + (size_t)v->head_dim) * sizeof(float));
   const size_t pbytes = BH * max_chunks * G * (2 + (size_t)v->head_dim) * acc;
   char* p = take(pbytes);
   if (wl) {
@@ -542,6 +543,7 @@ size_t decode_ws_layout(const dp_cache_view* v, int G, WorkLists* wl, void** par
     wl->counters = reinterpret_cast<int*>(ctr);
     wl->chunk_prefix = reinterpret_cast<int*>(cpre);
     wl->done = reinterpret_cast<int*>(dn);
+    wl->apart = reinterpret_cast<float*>(ap);
     wl->max_chunks = max_chunks;
   }
   if (parts) *parts = p;
@@ -621,12 +623,58 @@ cudaError_t launch_attn_t(const dp_cache_view& v, const void* q, int qdt, int G,
   return cudaGetLastError();
 }
 
+// approx partial per q head for the separate-kernel path (the fused plan
+// computes it in-cluster): over state==1 clusters, m = max log-mass,
+// l = sum e^(lm - m), o = sum e^(lm - m) * value_mean (engine.py:231-246)
+__global__ void __launch_bounds__(256) approx_partial_kernel(dp_cache_view v, int G, const double* __restrict__ lm,
+                                                            const uint8_t* __restrict__ state, WorkLists wl) {
+  const int hq = blockIdx.x, bh = hq / G, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int K = v.nclusters[bh], cap = v.cluster_cap, d = v.head_dim;
+  const double* x = lm + (size_t)hq * cap;
+  const uint8_t* st = state + (size_t)hq * cap;
+  __shared__ double red[33];
+  __shared__ float part[8][256];
+  double m = -CUDART_INF;
+  for (int k = tid; k < K; k += blockDim.x)
+    if (st[k] == 1) m = fmax(m, x[k]);
+  const double M = block_max(m, red, -CUDART_INF);
+  const float* vbar = v.value_means + (size_t)bh * cap * d;
+  float acc[8];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) acc[t] = 0.f;
+  double l = 0.0;
+  for (int k = warp; k < K; k += blockDim.x / 32) {
+    if (st[k] != 1) continue;
+    const double e = exp(x[k] - M);
+    if (lane == 0) l += e;
+#pragma unroll
+    for (int t = 0; t < 8; ++t)
+      if (lane + 32 * t < d) acc[t] += (float)e * vbar[(size_t)k * d + lane + 32 * t];
+  }
+#pragma unroll
+  for (int t = 0; t < 8; ++t)
+    if (lane + 32 * t < d) part[warp][lane + 32 * t] = acc[t];
+  const double L = block_sum(l, red);
+  float* ap = wl.apart + (size_t)hq * (2 + d);
+  for (int c = tid; c < d; c += blockDim.x) {
+    float sum = 0.f;
+    for (int w = 0; w < 8; ++w) sum += part[w][c];
+    ap[2 + c] = sum;
+  }
+  if (tid == 0) {
+    ap[0] = M == -CUDART_INF ? -INFINITY : (float)M;
+    ap[1] = (float)L;
+  }
+}
+
 cudaError_t launch_worklist(const dp_cache_view& v, int G, const uint8_t* state, int* stats, void* ws,
-                            cudaStream_t st) {
+                            cudaStream_t st, const double* lm) {
   WorkLists wl;
   decode_ws_layout(&v, G, &wl, nullptr, nullptr, reinterpret_cast<char*>(ws));
   wl.stats = stats;
   worklist_kernel<<<v.batch * v.kv_heads, kListThreads, 0, st>>>(v, G, state, wl);
+  if (lm && v.head_dim <= 256)
+    approx_partial_kernel<<<v.batch * v.kv_heads * G, 256, 0, st>>>(v, G, lm, state, wl);
   return cudaGetLastError();
 }
 

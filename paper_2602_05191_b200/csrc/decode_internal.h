@@ -24,6 +24,7 @@ struct WorkLists {
   int* counters;  // [BH] partial-completion counters (zero between launches)
   int* chunk_prefix;  // [BH+1] exclusive prefix of nchunks over heads (+ total)
   int* done;      // [1] producer-completion counter (zero between launches)
+  float* apart;   // [BH][G][2+d] approx pseudo-row partial per q head (m, l, o); m = -inf: none
   int max_chunks;
 };
 
@@ -62,7 +63,7 @@ cudaError_t launch_select(const dp_cache_view& v, int G, double p1, double p2, c
                           uint8_t* state, int* counts, int* order, double* cum, double* probs,
                           cudaStream_t st);
 cudaError_t launch_worklist(const dp_cache_view& v, int G, const uint8_t* state, int* stats, void* ws,
-                            cudaStream_t st);
+                            cudaStream_t st, const double* lm);
 cudaError_t launch_attend(const dp_cache_view& v, const void* q, int qdt, int G, double scale, const double* lm,
                           float* out, float* lse, void* ws, bool dense, cudaStream_t st);
 cudaError_t launch_attn_tc(const dp_cache_view& v, const void* q, int qdt, int G, double scale, const double* lm,

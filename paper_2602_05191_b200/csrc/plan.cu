@@ -1,22 +1,25 @@
 // Fused per-layer "plan": size-weighted centroid scoring + two-stage top-p +
-// GQA-union work list, one launch, one 8-CTA thread-block cluster per
-// (sequence, kv head); stages hand data over through distributed shared
-// memory instead of HBM round trips.
+// approx partial + GQA-union work list, one launch, one 8-CTA thread-block
+// cluster per (sequence, kv head); stages hand data over through distributed
+// shared memory instead of HBM round trips.
 //
 //   phase 1  score   (engine.py:158-177)  CTA r scores clusters [r*per, (r+1)*per)
-//                    for every q head of the group: fp64 dot of fp32 centroids
-//                    with the query, + log|c|.
+//                    for every q head of the group: 8 lanes per centroid row,
+//                    fp32 query/centroid products accumulated in fp64 (exact
+//                    products, so log-masses match the fp64 oracle to ~1e-15).
 //   phase 2  select  (engine.py:180-213, selection.py:36-65)  CTA g (g < G) owns
-//                    q head g: gathers its K log-masses over DSMEM, softmax in
-//                    fp64, then a mass histogram over 1/16-nat log bins finds the
-//                    bin where the cumulative mass crosses p1 (and p2 of the
+//                    q head g: gathers its K log-masses over DSMEM, e = exp(lm -
+//                    max), a mass histogram over 1/16-nat log bins finds the bin
+//                    where the cumulative mass crosses p1 (then p2 of the
 //                    retained mass); only those boundary bins are sorted (prob
 //                    desc, cluster id asc == the stable argsort order) to place
-//                    the exact cuts.  No full sort.
-//   phase 3  worklist  every CTA turns its cluster slice into GQA-union rows:
-//                    packed row entries (head mask << 24 | physical row) for
-//                    sink, window and members of clusters exact for >= 1 head,
-//                    and (cluster, mask) entries for approximated clusters.
+//                    the exact cuts.  It then folds the head's approximated
+//                    clusters (logit = log-mass, value = value mean,
+//                    engine.py:231-246) into one (m, l, o) partial.
+//   phase 3  worklist  every CTA reads all head states over DSMEM, computes
+//                    the GQA-union prefix itself (no extra cluster barrier) and
+//                    writes its slice's packed row entries (head mask << 24 |
+//                    physical row) and (cluster, mask) approx entries.
 //
 // Cut semantics follow the reference: the first prefix whose cumsum/total
 // >= p (searchsorted left + 1, clamped to n); ties -> lower cluster id.
@@ -35,7 +38,7 @@ constexpr int kCl = 8;         // CTAs per cluster (portable size)
 constexpr int kPT = 256;       // threads per CTA
 constexpr int kBins = 1024;    // log-mass bins of width 1/16 nat (span 64 nats)
 constexpr float kBinScale = 16.f;
-constexpr int kPlanTile = 64;  // centroid rows staged per score tile
+constexpr int kTile = 32;      // centroid rows per score tile (8 lanes per row)
 constexpr int kPlanMaxCap = 4096;
 
 // phase timestamps (%globaltimer, ns) of cluster 0: [rank][event]; read with
@@ -55,7 +58,7 @@ __device__ __forceinline__ bool before(double pa, int ia, double pb, int ib) {
 
 struct PlanLayout {
   int per;
-  size_t qd, lmS, full, bin, st, bins, cand, ctile, total;
+  size_t qf, lmS, full, bin, st, bins, cand, ctile, total;
 };
 
 __host__ __device__ inline PlanLayout plan_layout(int d, int cap) {
@@ -67,22 +70,78 @@ __host__ __device__ inline PlanLayout plan_layout(int d, int cap) {
     o += (bytes + 15) & ~size_t(15);
     return r;
   };
-  L.qd = take((size_t)kMaxGroup * d * 8);
+  L.qf = take((size_t)kMaxGroup * d * 4);
   L.lmS = take((size_t)kMaxGroup * L.per * 8);
   L.full = take((size_t)cap * 8);
   L.bin = take((size_t)cap * 2);
   L.st = take((size_t)cap);
-  L.bins = take((size_t)kBins * 20);
-  L.cand = take((size_t)cap * 16);  // (prob f64, id i32, sorted slot i32)
-  L.ctile = take((size_t)kPlanTile * (d + 4) * 4);
+  L.bins = take((size_t)kBins * 12 > (size_t)cap * 4 ? (size_t)kBins * 12 : (size_t)cap * 4);  // bins | approx ids
+  L.cand = take((size_t)cap * 16 > (size_t)kMaxGroup * cap ? (size_t)cap * 16 : (size_t)kMaxGroup * cap);
+  L.ctile = take((size_t)2 * kTile * (d + 4) * 4 > (size_t)8 * 256 * 4 ? (size_t)2 * kTile * (d + 4) * 4
+                                                                        : (size_t)8 * 256 * 4);
   L.total = o;
   return L;
 }
 
-// warp 0: first j in [0, n) with (base + sum_{t<=j} p[order[t]]) / denom >= pthr
-// (n if never); *at receives the inclusive sum at the cut (or the full sum).
-__device__ int warp_cut(const double* cp, const int* order, int n, double base, double denom, double pthr,
-                        double* at) {
+// warp-level search over the bins: first non-empty bin b < limit at which
+// the running mass reaches thresh; *before_mass / *before_cnt receive the mass
+// and count of the bins before it (limit if never reached)
+__device__ int bin_search(const double* bmass, const int* bcnt, int limit, double thresh, double* before_mass,
+                          int* before_cnt) {
+  const int lane = threadIdx.x & 31;
+  constexpr int per = kBins / 32;
+  double ms = 0.0;
+  int cs = 0;
+#pragma unroll 8
+  for (int j = 0; j < per; ++j) {
+    const int b = lane * per + j;
+    if (b < limit) {
+      ms += bmass[b];
+      cs += bcnt[b];
+    }
+  }
+  double inc = ms;
+  int ci = cs;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double t = __shfl_up_sync(0xffffffffu, inc, o);
+    const int tc = __shfl_up_sync(0xffffffffu, ci, o);
+    if (lane >= o) {
+      inc += t;
+      ci += tc;
+    }
+  }
+  const unsigned hit = __ballot_sync(0xffffffffu, inc >= thresh && cs > 0);
+  if (!hit) {
+    *before_mass = __shfl_sync(0xffffffffu, inc, 31);
+    *before_cnt = __shfl_sync(0xffffffffu, ci, 31);
+    return limit;
+  }
+  const int f = __ffs(hit) - 1;
+  double run = __shfl_sync(0xffffffffu, inc - ms, f);
+  int crun = __shfl_sync(0xffffffffu, ci - cs, f);
+  int res = limit;
+  if (lane == f) {
+    for (int j = 0; j < per; ++j) {
+      const int b = f * per + j;
+      if (b >= limit) break;
+      if (bcnt[b] > 0 && run + bmass[b] >= thresh) {
+        res = b;
+        break;
+      }
+      run += bmass[b];
+      crun += bcnt[b];
+    }
+  }
+  res = __shfl_sync(0xffffffffu, res, f);
+  *before_mass = __shfl_sync(0xffffffffu, run, f);
+  *before_cnt = __shfl_sync(0xffffffffu, crun, f);
+  return res;
+}
+
+// warp: first j in [0, n) with (base + sum_{t<=j} p[order[t]]) >= thresh
+// (n if never); *at receives the inclusive sum at the cut (or the full sum)
+__device__ int warp_cut(const double* cp, const int* order, int n, double base, double thresh, double* at) {
   const int lane = threadIdx.x & 31;
   for (int j0 = 0; j0 < n; j0 += 32) {
     const int j = j0 + lane;
@@ -94,7 +153,7 @@ __device__ int warp_cut(const double* cp, const int* order, int n, double base, 
       if (lane >= o) inc += t;
     }
     const double cum = base + inc;
-    const unsigned hit = __ballot_sync(0xffffffffu, j < n && cum / denom >= pthr);
+    const unsigned hit = __ballot_sync(0xffffffffu, j < n && cum >= thresh);
     if (hit) {
       const int f = __ffs(hit) - 1;
       *at = __shfl_sync(0xffffffffu, cum, f);
@@ -106,7 +165,7 @@ __device__ int warp_cut(const double* cp, const int* order, int n, double base, 
   return n;
 }
 
-__global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT)
+__global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT, 1)
     plan_kernel(dp_cache_view v, const void* __restrict__ q, int qdt, int G, double scale, double p1, double p2,
                 double* __restrict__ lm_out, uint8_t* __restrict__ state_out, int* __restrict__ counts,
                 WorkLists wl) {
@@ -123,137 +182,141 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT)
   const int* offs = v.offs + (size_t)bh * (cap + 1);
 
   extern __shared__ __align__(16) unsigned char smem[];
-  double* qd = reinterpret_cast<double*>(smem + L.qd);
-  double* lmS = reinterpret_cast<double*>(smem + L.lmS);  // [kMaxGroup][per]
+  float* qf = reinterpret_cast<float*>(smem + L.qf);       // [8][d]
+  double* lmS = reinterpret_cast<double*>(smem + L.lmS);  // [8][per]
   double* full = reinterpret_cast<double*>(smem + L.full);
   uint16_t* bin16 = reinterpret_cast<uint16_t*>(smem + L.bin);
   uint8_t* stS = reinterpret_cast<uint8_t*>(smem + L.st);
   double* bmass = reinterpret_cast<double*>(smem + L.bins);
-  double* bcum = bmass + kBins;
-  int* bcnt = reinterpret_cast<int*>(bcum + kBins);
+  int* bcnt = reinterpret_cast<int*>(bmass + kBins);
+  int* alist = reinterpret_cast<int*>(smem + L.bins);      // phase 2 tail: approx ids
   double* cp_ = reinterpret_cast<double*>(smem + L.cand);  // candidate probs
   int* cid = reinterpret_cast<int*>(cp_ + cap);             // candidate ids
   int* cord = cid + cap;                                    // sorted order (slots)
+  uint8_t* stall = reinterpret_cast<uint8_t*>(smem + L.cand);  // phase 3: [G][K] states
   float* ctile = reinterpret_cast<float*>(smem + L.ctile);
+  float* ared = ctile;                                      // phase 2 tail: [8 warps][256]
   __shared__ double red[33];
   __shared__ int redi[33];
   __shared__ double s_lmax[kMaxGroup];
-  __shared__ int s_b1, s_b2, s_nc, s_tot[3];
+  __shared__ int s_b1, s_b2, s_nc, s_c1, s_c2;
+  __shared__ double s_sub;
 
   stamp(r, 0);
   // ---------------- phase 1: score my slice for all G heads ---------------
-  for (int i = tid; i < G * d; i += kPT) qd[i] = load_elem_d(q, qdt, (size_t)bh * G * d + i);
-  {
-    double lmax0 = -CUDART_INF, lmax1 = -CUDART_INF;
-    const float4* C4 = reinterpret_cast<const float4*>(v.centroids + ((size_t)bh * cap + k0) * d);
-    const int d4 = d >> 2, stride = d + 4;
-    const int row = tid & (kPlanTile - 1), slot = tid >> 6;  // 64 rows x 4 head slots
-    for (int t0 = 0; t0 < nloc; t0 += kPlanTile) {
-      const int n = min(kPlanTile, nloc - t0);
-      __syncthreads();
-      for (int i = tid; i < n * d4; i += kPT) {
-        const int rr = i / d4, c = i - rr * d4;
-        const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(&ctile[rr * stride + 4 * c]));
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(&C4[(size_t)(t0 + rr) * d4 + c]));
-      }
-      asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
-      __syncthreads();
-      if (row < n) {
-        const int k = k0 + t0 + row;
-        const double ls = log((double)(offs[k + 1] - offs[k]));
-        const float* crow = &ctile[row * stride];
+  const int d4 = d >> 2, stride = d + 4;
+  const float4* C4 = reinterpret_cast<const float4*>(v.centroids + ((size_t)bh * cap + k0) * d);
+  const int ntiles = (nloc + kTile - 1) / kTile;
+  auto issue_tile = [&](int t, int buf) {
+    const int n = min(kTile, nloc - t * kTile);
+    for (int i = tid; i < n * d4; i += kPT) {
+      const int rr = i / d4, c = i - rr * d4;
+      const unsigned dst =
+          static_cast<unsigned>(__cvta_generic_to_shared(&ctile[(buf * kTile + rr) * stride + 4 * c]));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(&C4[(size_t)(t * kTile + rr) * d4 + c]));
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  if (ntiles > 0) issue_tile(0, 0);
+  for (int i = tid; i < G * d; i += kPT) qf[i] = load_elem_f(q, qdt, (size_t)bh * G * d + i);
+  __syncthreads();
+  // 8 lanes per centroid row, each over d/8 dims; G independent fp64 chains
+  const int part = tid & 7, row = tid >> 3;
+  const int dpp = d / 8;
+  double lmax[kMaxGroup];
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          const int g = slot + 4 * hh;
-          if (g < G) {
-            const double* qg = qd + g * d;
-            double a0 = 0.0, a1 = 0.0;
-            for (int j = 0; j < d; j += 4) {
-              const float4 c4 = *reinterpret_cast<const float4*>(&crow[j]);
-              a0 = fma((double)c4.x, qg[j], a0);
-              a1 = fma((double)c4.y, qg[j + 1], a1);
-              a0 = fma((double)c4.z, qg[j + 2], a0);
-              a1 = fma((double)c4.w, qg[j + 3], a1);
-            }
-            const double val = (a0 + a1) * scale + ls;
-            lmS[g * per + t0 + row] = val;
-            if (hh == 0) lmax0 = fmax(lmax0, val); else lmax1 = fmax(lmax1, val);
-            lm_out[((size_t)bh * G + g) * cap + k] = val;
-          }
+  for (int g = 0; g < kMaxGroup; ++g) lmax[g] = -CUDART_INF;
+  for (int t = 0; t < ntiles; ++t) {
+    const int buf = t & 1;
+    if (t + 1 < ntiles) {
+      issue_tile(t + 1, buf ^ 1);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
+    __syncthreads();
+    const int n = min(kTile, nloc - t * kTile);
+    double acc[kMaxGroup];
+#pragma unroll
+    for (int g = 0; g < kMaxGroup; ++g) acc[g] = 0.0;
+    const float* crow = &ctile[(buf * kTile + row) * stride + part * dpp];
+    for (int j = 0; j < dpp; j += 4) {
+      const float4 c4 = *reinterpret_cast<const float4*>(crow + j);
+#pragma unroll
+      for (int g = 0; g < kMaxGroup; ++g) {
+        if (g < G) {
+          const float4 q4 = *reinterpret_cast<const float4*>(qf + g * d + part * dpp + j);
+          double a = acc[g];
+          a = fma((double)c4.x, (double)q4.x, a);
+          a = fma((double)c4.y, (double)q4.y, a);
+          a = fma((double)c4.z, (double)q4.z, a);
+          a = fma((double)c4.w, (double)q4.w, a);
+          acc[g] = a;
         }
       }
     }
 #pragma unroll
-    for (int hh = 0; hh < 2; ++hh) {
-      const double m = warp_max(hh == 0 ? lmax0 : lmax1);
-      __syncthreads();
-      if (lane == 0) red[warp] = m;
-      __syncthreads();
-      if (tid < 4 && tid + 4 * hh < G) s_lmax[tid + 4 * hh] = fmax(red[2 * tid], red[2 * tid + 1]);
+    for (int g = 0; g < kMaxGroup; ++g) {
+      acc[g] += __shfl_xor_sync(0xffffffffu, acc[g], 1);
+      acc[g] += __shfl_xor_sync(0xffffffffu, acc[g], 2);
+      acc[g] += __shfl_xor_sync(0xffffffffu, acc[g], 4);
     }
+    if (row < n) {
+      const int k = k0 + t * kTile + row;
+      const double ls = log((double)(offs[k + 1] - offs[k]));
+#pragma unroll
+      for (int g = 0; g < kMaxGroup; ++g) {
+        if (g < G && part == g) {
+          const double val = acc[g] * scale + ls;
+          lmS[g * per + t * kTile + row] = val;
+          lm_out[((size_t)bh * G + g) * cap + k] = val;
+          lmax[g] = fmax(lmax[g], val);
+        }
+      }
+    }
+    __syncthreads();  // tile buffer reuse
+  }
+#pragma unroll
+  for (int g = 0; g < kMaxGroup; ++g) {
+    const double m = warp_max(lmax[g]);
+    if (lane == 0) red[warp] = m;
+    __syncthreads();
+    if (tid == 0 && g < G) {
+      double mm = -CUDART_INF;
+      for (int w = 0; w < kPT / 32; ++w) mm = fmax(mm, red[w]);
+      s_lmax[g] = mm;
+    }
+    __syncthreads();
   }
   stamp(r, 1);
   cluster.sync();  // (A) every slice scored
   stamp(r, 2);
 
   // ---------------- phase 2: two-stage top-p for q head g = r --------------
-  const bool sel = r < G;
-  double M = -CUDART_INF;
-  if (sel) {
-    for (int rr = 0; rr < kCl; ++rr) M = fmax(M, cluster.map_shared_rank(s_lmax, rr)[r]);
-    for (int i = tid; i < K; i += kPT) {
-      const int rr = i / per;
-      full[i] = cluster.map_shared_rank(lmS, rr)[r * per + (i - rr * per)];
-    }
-  }
-  cluster.sync();  // (B) gathers done (lmS no longer read remotely)
-  stamp(r, 3);
-  if (sel) {
+  if (r < G) {
     const int g = r;
+    double M = -CUDART_INF;
+    for (int rr = 0; rr < kCl; ++rr) M = fmax(M, cluster.map_shared_rank(s_lmax, rr)[g]);
     for (int b = tid; b < kBins; b += kPT) {
       bmass[b] = 0.0;
       bcnt[b] = 0;
     }
+    __syncthreads();
     double s = 0.0;
-    for (int i = tid; i < K; i += kPT) s += exp(full[i] - M);
-    const double S = block_sum(s, red);  // also orders the bin zeroing
-    double t = 0.0;
     for (int i = tid; i < K; i += kPT) {
-      const double lmv = full[i];
-      const double p = exp(lmv - M) / S;  // softmax, engine.py:168
+      const int rr = i / per;
+      const double lmv = cluster.map_shared_rank(lmS, rr)[g * per + (i - rr * per)];
+      const double e = exp(lmv - M);  // unnormalised softmax (engine.py:168); ratios are scale-free
       int b = (int)((float)(M - lmv) * kBinScale);
       b = b < 0 ? 0 : (b >= kBins ? kBins - 1 : b);
-      full[i] = p;
+      full[i] = e;
       bin16[i] = (uint16_t)b;
-      atomicAdd(&bmass[b], p);
+      atomicAdd(&bmass[b], e);
       atomicAdd(&bcnt[b], 1);
-      t += p;
+      s += e;
     }
-    const double total = block_sum(t, red);  // probs.sum(), selection.py:52
+    const double total = block_sum(s, red);  // also orders the histogram
     stamp(r, 8);
-    {
-      constexpr int bp = kBins / kPT;
-      double loc = 0.0;
-      for (int j = 0; j < bp; ++j) loc += bmass[tid * bp + j];
-      double tot;
-      double off = block_exclusive_scan(loc, red, &tot);
-      for (int j = 0; j < bp; ++j) {
-        bcum[tid * bp + j] = off;
-        off += bmass[tid * bp + j];
-      }
-    }
-    if (tid == 0) s_b1 = kBins;
-    __syncthreads();
-    for (int b0 = 0; b0 < kBins; b0 += kPT) {
-      const int b = b0 + tid;
-      const bool hit = bcnt[b] > 0 && (bcum[b] + bmass[b]) / total >= p1;
-      const unsigned bal = __ballot_sync(0xffffffffu, hit);
-      if (hit && lane == __ffs(bal) - 1) atomicMin(&s_b1, b);
-    }
-    __syncthreads();
-    const int b1 = s_b1;  // kBins: p1 never reached (rounding at p1 = 1) -> keep all
-    stamp(r, 9);
-
     // gather + rank-sort the elements of bin `bin` into candidate slots [base, base+n)
     auto sort_bin = [&](int bin, int base) -> int {
       if (tid == 0) s_nc = 0;
@@ -277,49 +340,61 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT)
       __syncthreads();
       return n;
     };
-
+    // stage 1: bin holding the crossing of p1 * total
+    if (warp == 0) {
+      double bm;
+      int bc;
+      const int b1 = bin_search(bmass, bcnt, kBins, p1 * total, &bm, &bc);
+      if (lane == 0) {
+        s_b1 = b1;
+        s_c1 = bc;
+        red[1] = bm;
+      }
+    }
+    __syncthreads();
+    const int b1 = s_b1, c1 = s_c1;
+    const double before1 = red[1];
+    stamp(r, 9);
     int n1c = 0, cut1 = 0;
-    double sub = total;  // retained (stage-1) mass = probs[cp].sum(), engine.py:191
     if (b1 < kBins) {
       n1c = sort_bin(b1, 0);
       if (warp == 0) {
         double at;
-        const int j = warp_cut(cp_, cord, n1c, bcum[b1], total, p1, &at);
+        const int j = warp_cut(cp_, cord, n1c, before1, p1 * total, &at);
         if (lane == 0) {
-          s_nc = j < n1c ? j + 1 : n1c;  // cut inside the boundary bin
-          red[0] = j < n1c ? at : bcum[b1] + bmass[b1];
+          s_nc = j < n1c ? j + 1 : n1c;
+          s_sub = j < n1c ? at : before1 + bmass[b1];
         }
       }
-      __syncthreads();
-      cut1 = s_nc;
-      sub = red[0];
-    } else {
-      double loc = 0.0;  // every bin retained
-      if (tid == 0) red[0] = bcum[kBins - 1] + bmass[kBins - 1];
-      __syncthreads();
-      sub = red[0];
-      (void)loc;
+    } else if (tid == 0) {
+      s_sub = before1;  // p1 never reached (rounding at p1 = 1): keep everything
     }
     __syncthreads();
+    if (b1 < kBins) cut1 = s_nc;
+    const double sub = s_sub;  // retained mass, probs[cp].sum() (engine.py:191)
     stamp(r, 10);
-    // stage 2 (engine.py:191-194): same descending order, denominator = sub
-    if (tid == 0) s_b2 = b1;
-    __syncthreads();
-    for (int b0 = 0; b0 < kBins; b0 += kPT) {  // uniform trip count: full-warp ballots
-      const int b = b0 + tid;
-      const bool hit = b < b1 && bcnt[b] > 0 && (bcum[b] + bmass[b]) / sub >= p2;
-      const unsigned bal = __ballot_sync(0xffffffffu, hit);
-      if (hit && lane == __ffs(bal) - 1) atomicMin(&s_b2, b);
+    // stage 2 (engine.py:191-194): same descending order, threshold p2 * sub
+    if (warp == 0) {
+      double bm;
+      int bc;
+      const int b2 = bin_search(bmass, bcnt, b1 < kBins ? b1 : kBins, p2 * sub, &bm, &bc);
+      if (lane == 0) {
+        s_b2 = b2;
+        s_c2 = bc;
+        red[2] = bm;
+      }
     }
     __syncthreads();
-    const int b2 = s_b2;
-    int cut2 = 0, n2c = 0, base2 = 0;
+    const int b2 = s_b2 < b1 ? s_b2 : b1;
+    const int c2 = s_b2 < b1 ? s_c2 : c1;
+    const double before2 = s_b2 < b1 ? red[2] : before1;
+    int cut2 = 0, n2c = 0;
+    const int base2 = n1c;
     if (b2 < b1) {
-      base2 = n1c;
       n2c = sort_bin(b2, base2);
       if (warp == 0) {
         double at;
-        const int j = warp_cut(cp_, cord + base2, n2c, bcum[b2], sub, p2, &at);
+        const int j = warp_cut(cp_, cord + base2, n2c, before2, p2 * sub, &at);
         if (lane == 0) s_nc = j < n2c ? j + 1 : n2c;
       }
       __syncthreads();
@@ -327,13 +402,12 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT)
     } else if (b1 < kBins) {
       if (warp == 0) {
         double at;
-        const int j = warp_cut(cp_, cord, cut1, bcum[b1], sub, p2, &at);
+        const int j = warp_cut(cp_, cord, cut1, before1, p2 * sub, &at);
         if (lane == 0) s_nc = j < cut1 ? j + 1 : cut1;
       }
       __syncthreads();
       cut2 = s_nc;
     }
-    __syncthreads();
     stamp(r, 11);
     // states: 2 exact, 1 approx, 0 dropped
     for (int i = tid; i < K; i += kPT) {
@@ -341,140 +415,159 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT)
       stS[i] = (uint8_t)(b < b2 ? 2 : (b < b1 ? 1 : 0));
     }
     __syncthreads();
-    if (b1 < kBins) {
-      for (int j = tid; j < n1c; j += kPT) {
-        const int id = cid[cord[j]];
-        stS[id] = (uint8_t)(j < cut1 ? (b2 == b1 && j < cut2 ? 2 : 1) : 0);
-      }
-    }
-    if (b2 < b1) {
+    if (b1 < kBins)
+      for (int j = tid; j < n1c; j += kPT)
+        stS[cid[cord[j]]] = (uint8_t)(j < cut1 ? (b2 == b1 && j < cut2 ? 2 : 1) : 0);
+    if (b2 < b1)
       for (int j = tid; j < n2c; j += kPT) stS[cid[cord[base2 + j]]] = (uint8_t)(j < cut2 ? 2 : 1);
-    }
-    // counts: elements of bins strictly above the boundary + the cuts
-    int c1 = 0, c2 = 0;
-    for (int b = tid; b < kBins; b += kPT) {
-      if (b < b1) c1 += bcnt[b];
-      if (b < b2) c2 += bcnt[b];
-    }
-    c1 = block_sum(c1, redi);
-    c2 = block_sum(c2, redi);
+    __syncthreads();
+    const int hq = bh * G + g;
     if (tid == 0) {
-      const int hq = bh * G + g;
       counts[2 * hq] = b1 < kBins ? c1 + cut1 : K;
       counts[2 * hq + 1] = c2 + cut2;
     }
-    __syncthreads();
     if (state_out)
-      for (int i = tid; i < K; i += kPT) state_out[((size_t)bh * G + g) * cap + i] = stS[i];
+      for (int i = tid; i < K; i += kPT) state_out[(size_t)hq * cap + i] = stS[i];
+    // approx partial: m = M, l = sum e, o = sum e * value_mean over state==1
+    int na = 0;
+    {
+      int cnt = 0;
+      const int per_t = (K + kPT - 1) / kPT;
+      const int beg = min(K, tid * per_t), end = min(K, beg + per_t);
+      for (int i = beg; i < end; ++i) cnt += stS[i] == 1;
+      int tot;
+      int off = block_exclusive_scan(cnt, redi, &tot);
+      for (int i = beg; i < end; ++i)
+        if (stS[i] == 1) alist[off++] = i;
+      na = tot;
+      __syncthreads();
+    }
+    const float* vbar = v.value_means + (size_t)bh * cap * d;
+    const int nq = d / 4;  // float4 columns (d <= 128 -> at most one per lane)
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    double lsum = 0.0;
+    for (int a0 = warp; a0 < na; a0 += 4 * (kPT / 32)) {
+      float4 vb[4];
+      float wt[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int a = a0 + u * (kPT / 32);
+        const int k = a < na ? alist[a] : 0;
+        wt[u] = a < na ? (float)full[k] : 0.f;
+        vb[u] = (a < na && lane < nq) ? *(reinterpret_cast<const float4*>(vbar + (size_t)k * d) + lane)
+                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+        if (lane == 0 && a < na) lsum += full[k];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        acc.x += wt[u] * vb[u].x; acc.y += wt[u] * vb[u].y; acc.z += wt[u] * vb[u].z; acc.w += wt[u] * vb[u].w;
+      }
+    }
+    reinterpret_cast<float4*>(ared + warp * 256)[lane] = acc;
+    if (lane == 0) red[warp] = lsum;
+    __syncthreads();
+    float* ap = wl.apart + (size_t)hq * (2 + d);
+    for (int c = tid; c < d; c += kPT) {
+      float sum = 0.f;
+      for (int w = 0; w < kPT / 32; ++w) sum += ared[w * 256 + c];
+      ap[2 + c] = sum;
+    }
+    if (tid == 0) {
+      double l = 0.0;
+      for (int w = 0; w < kPT / 32; ++w) l += red[w];
+      ap[0] = na > 0 ? (float)M : -INFINITY;  // natural-log domain, like the attention partials
+      ap[1] = (float)l;
+    }
   }
   stamp(r, 4);
   cluster.sync();  // (C) all head states ready
   stamp(r, 5);
 
-  // ---------------- phase 3: GQA-union work list for my slice ------------
+  // ---------------- phase 3: GQA-union work list --------------------------
+  // every CTA copies all G state arrays (16-byte DSMEM loads), computes the
+  // union prefix over all clusters itself and writes its own slice
+  {
+    const int kq = (K + 15) / 16;
+    for (int i = tid; i < G * kq; i += kPT) {
+      const int gg = i / kq, c = i - gg * kq;
+      *reinterpret_cast<int4*>(stall + (size_t)gg * cap + c * 16) =
+          *reinterpret_cast<const int4*>(cluster.map_shared_rank(stS, gg) + c * 16);
+    }
+  }
+  // done with remote smem: arrive now, wait at the very end
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+  __syncthreads();
   const int full_mask = (1 << G) - 1;
   const int sw_rows = v.sink + v.window;
-  int me_l[2] = {0, 0}, ma_l[2] = {0, 0}, len_l[2] = {0, 0};
-  int e_loc = 0, a_loc = 0, r_loc = 0;
-#pragma unroll
-  for (int u = 0; u < 2; ++u) {  // per <= 512 -> 2 clusters per thread
-    const int li = tid * 2 + u;
-    if (li < nloc) {
-      const int k = k0 + li;
-      int me = 0, ma = 0;
-      for (int gg = 0; gg < G; ++gg) {
-        const uint8_t s = cluster.map_shared_rank(stS, gg)[k];
-        me |= (s == 2) << gg;
-        ma |= (s == 1) << gg;
-      }
-      me_l[u] = me;
-      ma_l[u] = ma;
-      len_l[u] = me ? offs[k + 1] - offs[k] : 0;
-      e_loc += me != 0;
-      a_loc += ma != 0;
-      r_loc += len_l[u];
+  const int per_t = (K + kPT - 1) / kPT;
+  const int beg = min(K, tid * per_t), end = min(K, beg + per_t);
+  int e_cnt = 0, a_cnt = 0, r_cnt = 0;
+  for (int k = beg; k < end; ++k) {
+    int me = 0, ma = 0;
+    for (int gg = 0; gg < G; ++gg) {
+      const uint8_t s = stall[(size_t)gg * cap + k];
+      me |= (s == 2) << gg;
+      ma |= (s == 1) << gg;
     }
+    e_cnt += me != 0;
+    a_cnt += ma != 0;
+    if (me) r_cnt += offs[k + 1] - offs[k];
   }
-  int tot_e, tot_a, tot_r;
-  const int pe = block_exclusive_scan(e_loc, redi, &tot_e);
-  const int pa = block_exclusive_scan(a_loc, redi, &tot_a);
-  const int pr = block_exclusive_scan(r_loc, redi, &tot_r);
-  if (tid == 0) {
-    s_tot[0] = tot_e;
-    s_tot[1] = tot_a;
-    s_tot[2] = tot_r;
-  }
-  stamp(r, 12);
-  cluster.sync();  // (D) slice totals visible
-  stamp(r, 13);
-  int off_e = 0, off_a = 0, off_r = sw_rows, all_e = 0, all_a = 0, all_r = sw_rows;
-  for (int rr = 0; rr < kCl; ++rr) {
-    const int* t3 = cluster.map_shared_rank(s_tot, rr);
-    if (rr < r) {
-      off_e += t3[0];
-      off_a += t3[1];
-      off_r += t3[2];
-    }
-    all_e += t3[0];
-    all_a += t3[1];
-    all_r += t3[2];
-  }
+  int tot_a, tot_r, tot_e;
+  int off_a = block_exclusive_scan(a_cnt, redi, &tot_a);
+  int off_r = block_exclusive_scan(r_cnt, redi, &tot_r) + sw_rows;
+  (void)block_exclusive_scan(e_cnt, redi, &tot_e);
   unsigned* rowidx = reinterpret_cast<unsigned*>(wl.rowidx) + (size_t)bh * v.row_cap;
   int2* apx = wl.approx + (size_t)bh * cap;
-  {
-    int ea = off_a + pa, er = off_r + pr;
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int li = tid * 2 + u;
-      if (li < nloc) {
-        const int k = k0 + li;
-        if (ma_l[u]) apx[ea++] = make_int2(k, ma_l[u]);
-        if (me_l[u]) {
-          const unsigned tag = (unsigned)me_l[u] << 24;
-          const int o0 = offs[k];
-          for (int t = 0; t < len_l[u]; ++t) rowidx[er + t] = tag | (unsigned)(o0 + t);
-          er += len_l[u];
-        }
+  // entries of my cluster slice [k0, k0 + nloc) only
+  for (int k = beg; k < end; ++k) {
+    int me = 0, ma = 0;
+    for (int gg = 0; gg < G; ++gg) {
+      const uint8_t s = stall[(size_t)gg * cap + k];
+      me |= (s == 2) << gg;
+      ma |= (s == 1) << gg;
+    }
+    const int len = me ? offs[k + 1] - offs[k] : 0;
+    if (k >= k0 && k < k0 + nloc) {
+      if (ma) apx[off_a] = make_int2(k, ma);
+      if (me) {
+        const unsigned tag = (unsigned)me << 24;
+        const int o0 = offs[k];
+        for (int t = 0; t < len; ++t) rowidx[off_r + t] = tag | (unsigned)(o0 + t);
       }
     }
+    off_a += ma != 0;
+    off_r += len;
   }
-  (void)pe;
   if (r == 0) {
     const unsigned tag = (unsigned)full_mask << 24;
     for (int t = tid; t < v.sink; t += kPT) rowidx[t] = tag | (unsigned)t;
     for (int t = tid; t < v.window; t += kPT) rowidx[v.sink + t] = tag | (unsigned)(v.n_tokens - v.window + t);
-  }
-  if (r == kCl - 1 && tid == 0) {
-    wl.nrows[bh] = all_r;
-    wl.napprox[bh] = all_a;
-    wl.nruns[bh] = all_e + (v.sink > 0) + (v.window > 0);
-    wl.nchunks[bh] = (all_r + kChunkRows - 1) / kChunkRows;
-    publish_chunk_prefix(wl, v.batch * v.kv_heads);
-    if (wl.stats) {
-      wl.stats[4 * bh + 0] = all_r;
-      wl.stats[4 * bh + 1] = all_a;
-      wl.stats[4 * bh + 2] = (all_r + kChunkRows - 1) / kChunkRows;
-      wl.stats[4 * bh + 3] = all_e;
+    if (tid == 0) {
+      const int all_r = tot_r + sw_rows;
+      wl.nrows[bh] = all_r;
+      wl.napprox[bh] = tot_a;
+      wl.nruns[bh] = tot_e + (v.sink > 0) + (v.window > 0);
+      wl.nchunks[bh] = (all_r + kChunkRows - 1) / kChunkRows;
+      if (wl.stats) {
+        wl.stats[4 * bh + 0] = all_r;
+        wl.stats[4 * bh + 1] = tot_a;
+        wl.stats[4 * bh + 2] = (all_r + kChunkRows - 1) / kChunkRows;
+        wl.stats[4 * bh + 3] = tot_e;
+      }
+      publish_chunk_prefix(wl, v.batch * v.kv_heads);
     }
   }
   stamp(r, 6);
-  cluster.sync();  // (E) keep smem alive until every remote read is done
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");  // (E) remote smem lifetime
   stamp(r, 7);
 }
-
-}  // namespace dp
-
-extern "C" int dp_debug_plan_timing(unsigned long long* out) {
-  return cudaMemcpyFromSymbol(out, dp::g_plan_ts, sizeof(dp::g_plan_ts)) == cudaSuccess ? 0 : 2;  // [8][16]
-}
-
-namespace dp {
 
 size_t plan_smem_bytes(int d, int cap) { return plan_layout(d, cap).total; }
 
 bool plan_supported(const dp_cache_view& v, int G) {
-  return v.cluster_cap <= kPlanMaxCap && G <= kCl && v.head_dim <= 256 && v.row_cap < (1 << 24) &&
-         plan_smem_bytes(v.head_dim, v.cluster_cap) <= 227 * 1024;
+  return v.cluster_cap <= kPlanMaxCap && G <= kCl && v.head_dim <= 128 && v.head_dim % 32 == 0 &&
+         v.row_cap < (1 << 24) && plan_smem_bytes(v.head_dim, v.cluster_cap) <= 227 * 1024;
 }
 
 cudaError_t launch_plan(const dp_cache_view& v, const void* q, int qdt, int G, double scale, double p1, double p2,
@@ -493,3 +586,7 @@ cudaError_t launch_plan(const dp_cache_view& v, const void* q, int qdt, int G, d
 }
 
 }  // namespace dp
+
+extern "C" int dp_debug_plan_timing(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, dp::g_plan_ts, sizeof(dp::g_plan_ts)) == cudaSuccess ? 0 : 2;  // [8][16]
+}

@@ -77,10 +77,13 @@ def classify_sets(est_o, plan_o, state_row, p1, p2):
             base = order
         else:
             g = set(np.flatnonzero(st == 2).tolist())
-            o_set = set(plan_o.exact_clusters.tolist())
-            n1 = plan_o.stage1.selected.size
+            # stage 2 runs on the stage-1 set actually selected; after a
+            # stage-1 tie that is the GPU's set, so re-derive the oracle cut
+            n1 = plan_o.stage1.selected.size if res[0] == "exact" else int((st >= 1).sum())
             sub = probs[order[:n1]]
             cum = np.cumsum(sub) / sub.sum()
+            n2 = min(int(np.searchsorted(cum, p2, side="left")) + 1, n1)
+            o_set = set(order[:n2].tolist())
             p = p2
             base = order[:n1]
         if g == o_set:

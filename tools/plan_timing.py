@@ -35,3 +35,24 @@ print("rank " + " ".join(f"{x:>6s}" for x in names))
 for r in range(8):
     print(f"{r:4d} " + " ".join(f"{(x - t0) / 1e3:6.2f}" if x > 0 else "     -" for x in t[r]))
 print("counts", ws.counts[0, :G].tolist(), "stats", ws.stats[0, 0].tolist())
+
+# attention phases (sparse launch after the plan)
+N.check(lib.dp_attend(view, N.ptr(q), 1, G, 1 / math.sqrt(128), N.ptr(ws.log_mass), N.ptr(ws.out), N.ptr(ws.lse),
+                      N.ptr(ws.ws), ws.ws.numel(), torch.cuda.current_stream().cuda_stream))
+torch.cuda.synchronize()
+for it in range(2):
+    N.check(lib.dp_plan(view, N.ptr(q), 1, G, 1 / math.sqrt(128), 0.95, 0.7, N.ptr(ws.log_mass), None,
+                        N.ptr(ws.counts), N.ptr(ws.stats), N.ptr(ws.ws), ws.ws.numel(),
+                        torch.cuda.current_stream().cuda_stream))
+    N.check(lib.dp_attend(view, N.ptr(q), 1, G, 1 / math.sqrt(128), N.ptr(ws.log_mass), N.ptr(ws.out),
+                          N.ptr(ws.lse), N.ptr(ws.ws), ws.ws.numel(), torch.cuda.current_stream().cuda_stream))
+torch.cuda.synchronize()
+abuf = (ctypes.c_ulonglong * (512 * 8))()
+lib.dp_debug_attn_timing(ctypes.cast(abuf, ctypes.c_void_p))
+a = np.array(abuf[:], dtype=np.float64).reshape(512, 8)[:148]
+a0 = a[:, 0].min()
+rel = (a - a0) / 1e3
+print("attn phases (us, rel. to first CTA start): start, prefix, first data, loop done, flushed, exit")
+for name, col in (("start", 0), ("prefix", 1), ("data0", 2), ("loop", 3), ("flush", 4), ("exit", 5)):
+    x = rel[:, col]
+    print(f"  {name:7s} min {x.min():7.2f} med {np.median(x):7.2f} max {x.max():7.2f}")
