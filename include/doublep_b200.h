@@ -209,6 +209,9 @@ int dp_debug_plan_timing(unsigned long long* out); /* [8][16] */
  * launch, [512 CTAs][8 events]: start, prefix loaded, first stage landed,
  * main loop done, flushed, exit. */
 int dp_debug_attn_timing(unsigned long long* out);
+/* Profiling switches: key 0 = attention flags (bit 0: skip the math, stream
+ * K/V only).  Never set on the product path. */
+int dp_debug_set(int key, int value);
 
 /* Lower-level pieces of the above (used by the parity tests). */
 /* k-means++ picks only: picks int32 [B*H, k]. */

@@ -32,11 +32,12 @@ namespace dp {
 
 constexpr int kTcRows = kChunkRows;  // 128
 constexpr int kConsumers = 256;  // 8 compute warps
-constexpr int kProducers = 2;  // producer warps, 64 rows each
+constexpr int kProducers = 4;  // producer warps, 32 rows each
 constexpr int kTcThreads = kConsumers + 32 * kProducers;
 constexpr int kRowStride = 136;      // bf16 elements per staged row (272 B: conflict-free ldmatrix)
 constexpr int kStages = 3;
 constexpr int kStageElems = kTcRows * kRowStride;  // one K (or V) tile
+int g_attn_debug = 0;  // profiling switches (dp_debug_set)
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
@@ -139,7 +140,8 @@ template <bool kDense, bool kQF32>
 __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v, const void* __restrict__ q, int G,
                                                                float scale_log2, const double* __restrict__ lm,
                                                                WorkLists wl, Partials<float> pt,
-                                                               float* __restrict__ out, float* __restrict__ lse) {
+                                                               float* __restrict__ out, float* __restrict__ lse,
+                                                               int dbg) {
   constexpr int d = 128;
   constexpr int kWarps = kConsumers / 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -160,7 +162,28 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
   // ---- chunk prefix over heads, my contiguous chunk range -----------------
   astamp(0);
   const int per_dense = (v.n_tokens + kTcRows - 1) / kTcRows;
-  for (int b = tid; b <= BH; b += kTcThreads) prefix[b] = kDense ? b * per_dense : wl.chunk_prefix[b];
+  int* nrows_s = prefix + BH + 1;  // [BH] union rows per head (sparse)
+  if (kDense) {
+    for (int b = tid; b <= BH; b += kTcThreads) prefix[b] = b * per_dense;
+  } else {
+    // exclusive prefix of the per-head chunk counts (warp 0, 32 heads per step)
+    for (int b = tid; b < BH; b += kTcThreads) nrows_s[b] = __ldcg(&wl.nrows[b]);
+    if (warp == 0) {
+      int base = 0;
+      for (int b0 = 0; b0 < BH; b0 += 32) {
+        const int nch = b0 + lane < BH ? (__ldcg(&wl.nrows[b0 + lane]) + kTcRows - 1) / kTcRows : 0;
+        int inc = nch;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(0xffffffffu, inc, o);
+          if (lane >= o) inc += t;
+        }
+        if (b0 + lane < BH) prefix[b0 + lane] = base + inc - nch;
+        base += __shfl_sync(0xffffffffu, inc, 31);
+      }
+      if (lane == 0) prefix[BH] = base;
+    }
+  }
   if (tid == 0) {
     s_nmerge = 0;
     for (int i = 0; i < kStages; ++i) {
@@ -184,50 +207,50 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
     return lo;
   };
 
-  // ---- producer warps (rows [64p, 64p+64) each): run up to kStages ahead -
+  // ---- producer warps (rows [32p, 32p+32) each): run up to kStages ahead;
+  // the next chunk's row entries are fetched while this chunk's copies issue
   if (warp >= kWarps) {
-    const int ch = lane & 15, pr0 = (warp - kWarps) * 64;
+    const int ch = lane & 15, pr0 = (warp - kWarps) * 32;
+    auto fetch = [&](int idx, unsigned& e, int& bh, int& v0) {
+      const int j = j0 + idx;
+      bh = head_of(j);
+      v0 = (j - prefix[bh]) * kTcRows;
+      const int nr = min(kTcRows, (kDense ? v.n_tokens : nrows_s[bh]) - v0);
+      const int row = pr0 + lane;
+      e = row < nr ? (kDense ? (((unsigned)((1 << G) - 1)) << 24) | (unsigned)(v0 + row)
+                             : __ldg(reinterpret_cast<const unsigned*>(wl.rowidx) + (size_t)bh * v.row_cap + v0 + row))
+                   : 0xFFFFFFFFu;
+    };
+    unsigned e_nx;
+    int bh_nx, v0_nx;
+    fetch(0, e_nx, bh_nx, v0_nx);
     for (int idx = 0; idx < n; ++idx) {
       const int s = idx % kStages;
+      const unsigned e = e_nx;
+      const int bh = bh_nx;
+      if (idx + 1 < n) fetch(idx + 1, e_nx, bh_nx, v0_nx);
       if (idx >= kStages) mbar_wait(smem_u32(&empty_bar[s]), (unsigned)(((idx / kStages) + 1) & 1));
-      const int j = j0 + idx;
-      const int bh = head_of(j);
-      const int c = j - prefix[bh];
-      const int rows_total = kDense ? v.n_tokens : __ldg(&wl.nrows[bh]);
-      const int v0 = c * kTcRows;
-      const int nr = min(kTcRows, rows_total - v0);
-      const unsigned* ridx = reinterpret_cast<const unsigned*>(wl.rowidx) + (size_t)bh * v.row_cap + v0;
-      unsigned e[2];  // row entries of rows pr0 + lane + 32 i
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int row = pr0 + lane + 32 * i;
-        e[i] = row < nr ? (kDense ? (((unsigned)((1 << G) - 1)) << 24) | (unsigned)(v0 + row) : __ldg(&ridx[row]))
-                        : 0xFFFFFFFFu;
-        rmask[s * kTcRows + row] = e[i] == 0xFFFFFFFFu ? 0 : (int)(e[i] >> 24);
-      }
+      rmask[s * kTcRows + pr0 + lane] = e == 0xFFFFFFFFu ? 0 : (int)(e >> 24);
       const size_t head_off = (size_t)bh * v.row_cap * d;
       const __nv_bfloat16* Kg = reinterpret_cast<const __nv_bfloat16*>(v.keys) + head_off;
       const __nv_bfloat16* Vg = reinterpret_cast<const __nv_bfloat16*>(v.values) + head_off;
       __nv_bfloat16* Ks = KV + (size_t)s * 2 * kStageElems;
       __nv_bfloat16* Vs = Ks + kStageElems;
-      // lane copies 16-B column `ch` of rows (lane >> 4) + 2 r: a warp
+      // lane copies 16-B column `ch` of rows pr0 + (lane >> 4) + 2 r: a warp
       // instruction moves 2 rows = 512 contiguous bytes
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
 #pragma unroll 4
-        for (int r = 0; r < 16; ++r) {
-          const int row = pr0 + (lane >> 4) + 2 * (16 * i + r);
-          const unsigned er = __shfl_sync(0xffffffffu, e[i], ((lane >> 4) + 2 * r) & 31);
-          const unsigned kd = smem_u32(Ks + row * kRowStride + ch * 8);
-          const unsigned vd = smem_u32(Vs + row * kRowStride + ch * 8);
-          if (er != 0xFFFFFFFFu) {
-            const size_t off = (size_t)(er & 0xFFFFFFu) * d + ch * 8;
-            cp16(kd, Kg + off);
-            cp16(vd, Vg + off);
-          } else {
-            cp16_zero(kd, Kg);
-            cp16_zero(vd, Vg);
-          }
+      for (int r = 0; r < 16; ++r) {
+        const int row = pr0 + (lane >> 4) + 2 * r;
+        const unsigned er = __shfl_sync(0xffffffffu, e, (lane >> 4) + 2 * r);
+        const unsigned kd = smem_u32(Ks + row * kRowStride + ch * 8);
+        const unsigned vd = smem_u32(Vs + row * kRowStride + ch * 8);
+        if (er != 0xFFFFFFFFu) {
+          const size_t off = (size_t)(er & 0xFFFFFFu) * d + ch * 8;
+          cp16(kd, Kg + off);
+          cp16(vd, Vg + off);
+        } else {
+          cp16_zero(kd, Kg);
+          cp16_zero(vd, Vg);
         }
       }
       cp_async_arrive(smem_u32(&full_bar[s]));  // completes when this lane's copies land
@@ -306,6 +329,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
     const __nv_bfloat16* Ks = KV + (size_t)s * 2 * kStageElems;
     const __nv_bfloat16* Vs = Ks + kStageElems;
     const int* rm = rmask + s * kTcRows;
+    if (dbg & 1) {  // profiling: stream only, no math
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&empty_bar[s]));
+      continue;
+    }
     // ---- S = K Q^T for this warp's 16 rows --------------------------------
     const int r0 = warp * 16;
     float sc[4] = {0.f, 0.f, 0.f, 0.f};
@@ -455,7 +483,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
     }
     consumers_sync();
     for (int g = warp; g < G; g += kWarps) {
-      const float* ap = wl.apart + ((size_t)bh * G + g) * (2 + d);
+      const float* ap = wl.apart + ((size_t)bh * G + g) * (4 + d);
       const float ma = kDense ? -INFINITY : __ldcg(&ap[0]);
       float mloc = ma;
       for (int p = lane; p < nparts; p += 32) mloc = fmaxf(mloc, s_pm[g * kMaxParts + p]);
@@ -483,7 +511,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
 #pragma unroll
       for (int g = 0; g < 8; ++g)
         if (g < G && s_aw[g] > 0.f) {
-          const float4 oa = __ldcg(reinterpret_cast<const float4*>(wl.apart + ((size_t)bh * G + g) * (2 + d) + 2) + lane);
+          const float4 oa = __ldcg(reinterpret_cast<const float4*>(wl.apart + ((size_t)bh * G + g) * (4 + d) + 4) + lane);
           acc[g].x = s_aw[g] * oa.x; acc[g].y = s_aw[g] * oa.y; acc[g].z = s_aw[g] * oa.z; acc[g].w = s_aw[g] * oa.w;
         }
     }
@@ -532,11 +560,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
 }
 
 }  // namespace dp
+extern "C" int dp_debug_set(int key, int value) {
+  if (key == 0) dp::g_attn_debug = value;
+  return 0;
+}
 extern "C" int dp_debug_attn_timing(unsigned long long* out) {
   return cudaMemcpyFromSymbol(out, dp::g_attn_ts, sizeof(dp::g_attn_ts)) == cudaSuccess ? 0 : 2;  // [512][8]
 }
 namespace dp {
-size_t attn_tc_smem_bytes(int BH) { return TcSmem::fixed + (size_t)(BH + 1) * 4; }
+
+
+size_t attn_tc_smem_bytes(int BH) { return TcSmem::fixed + (size_t)(2 * BH + 1) * 4; }
 
 template <bool kDense, bool kQF32>
 static cudaError_t launch_tc_t(const dp_cache_view& v, const void* q, int G, double scale, const double* lm,
@@ -559,13 +593,13 @@ static cudaError_t launch_tc_t(const dp_cache_view& v, const void* q, int G, dou
   const long long cap_chunks = (long long)BH * ((rows + kTcRows - 1) / kTcRows);
   const int grid = (int)(cap_chunks < sms ? cap_chunks : sms);
   attn_tc_kernel<kDense, kQF32><<<grid, kTcThreads, smem, st>>>(v, q, G, (float)(scale * 1.4426950408889634), lm,
-                                                               wl, pt, out, lse);
+                                                               wl, pt, out, lse, g_attn_debug);
   return cudaGetLastError();
 }
 
 cudaError_t launch_attn_tc(const dp_cache_view& v, const void* q, int qdt, int G, double scale, const double* lm,
                            WorkLists wl, Partials<float> pt, float* out, float* lse, bool dense, cudaStream_t st) {
-  if ((size_t)(v.batch * v.kv_heads + 1) * 4 + TcSmem::fixed > 227 * 1024) return cudaErrorInvalidConfiguration;
+  if (attn_tc_smem_bytes(v.batch * v.kv_heads) > 227 * 1024) return cudaErrorInvalidConfiguration;
   if (qdt == DP_F32)
     return dense ? launch_tc_t<true, true>(v, q, G, scale, lm, wl, pt, out, lse, st)
                  : launch_tc_t<false, true>(v, q, G, scale, lm, wl, pt, out, lse, st);

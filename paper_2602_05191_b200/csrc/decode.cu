@@ -277,7 +277,6 @@ __global__ void __launch_bounds__(kListThreads) worklist_kernel(dp_cache_view v,
     wl.nrows[bh] = s_rows;
     wl.napprox[bh] = s_apx;
     wl.nchunks[bh] = (s_rows + kChunkRows - 1) / kChunkRows;
-    publish_chunk_prefix(wl, v.batch * v.kv_heads);
     if (wl.stats) {
       wl.stats[4 * bh + 0] = s_rows;
       wl.stats[4 * bh + 1] = s_apx;
@@ -527,7 +526,7 @@ size_t decode_ws_layout(const dp_cache_view* v, int G, WorkLists* wl, void** par
   char* ctr = take(BH * sizeof(int));
   char* cpre = take((BH + 1) * sizeof(int));
   char* dn = take(sizeof(int));
-  char* ap = take(BH * (size_t)G * (2 + (size_t)v->head_dim) * sizeof(float));
+  char* ap = take(BH * (size_t)G * (4 + (size_t)v->head_dim) * sizeof(float));  // [m, l, -, -, o]
   const size_t pbytes = BH * max_chunks * G * (2 + (size_t)v->head_dim) * acc;
   char* p = take(pbytes);
   if (wl) {
@@ -655,11 +654,11 @@ __global__ void __launch_bounds__(256) approx_partial_kernel(dp_cache_view v, in
   for (int t = 0; t < 8; ++t)
     if (lane + 32 * t < d) part[warp][lane + 32 * t] = acc[t];
   const double L = block_sum(l, red);
-  float* ap = wl.apart + (size_t)hq * (2 + d);
+  float* ap = wl.apart + (size_t)hq * (4 + d);
   for (int c = tid; c < d; c += blockDim.x) {
     float sum = 0.f;
     for (int w = 0; w < 8; ++w) sum += part[w][c];
-    ap[2 + c] = sum;
+    ap[4 + c] = sum;
   }
   if (tid == 0) {
     ap[0] = M == -CUDART_INF ? -INFINITY : (float)M;

@@ -24,7 +24,7 @@ struct WorkLists {
   int* counters;  // [BH] partial-completion counters (zero between launches)
   int* chunk_prefix;  // [BH+1] exclusive prefix of nchunks over heads (+ total)
   int* done;      // [1] producer-completion counter (zero between launches)
-  float* apart;   // [BH][G][2+d] approx pseudo-row partial per q head (m, l, o); m = -inf: none
+  float* apart;   // [BH][G][4+d] approx pseudo-row partial per q head (m, l, -, -, o[d]); m = -inf: none
   int max_chunks;
 };
 

@@ -58,7 +58,7 @@ __device__ __forceinline__ bool before(double pa, int ia, double pb, int ib) {
 
 struct PlanLayout {
   int per;
-  size_t qf, lmS, full, bin, st, bins, cand, ctile, total;
+  size_t qf, lmS, full, bin, st, bins, cand, ctile, offs, total;
 };
 
 __host__ __device__ inline PlanLayout plan_layout(int d, int cap) {
@@ -76,9 +76,11 @@ __host__ __device__ inline PlanLayout plan_layout(int d, int cap) {
   L.bin = take((size_t)cap * 2);
   L.st = take((size_t)cap);
   L.bins = take((size_t)kBins * 12 > (size_t)cap * 4 ? (size_t)kBins * 12 : (size_t)cap * 4);  // bins | approx ids
-  L.cand = take((size_t)cap * 16 > (size_t)kMaxGroup * cap ? (size_t)cap * 16 : (size_t)kMaxGroup * cap);
+  const size_t capP = (size_t)(cap + 15) & ~size_t(15);  // 16-B aligned state rows
+  L.cand = take((size_t)cap * 16 > (size_t)kMaxGroup * capP ? (size_t)cap * 16 : (size_t)kMaxGroup * capP);
   L.ctile = take((size_t)2 * kTile * (d + 4) * 4 > (size_t)8 * 256 * 4 ? (size_t)2 * kTile * (d + 4) * 4
                                                                         : (size_t)8 * 256 * 4);
+  L.offs = take((size_t)(cap + 1) * 4);  // the head's cluster row offsets
   L.total = o;
   return L;
 }
@@ -165,6 +167,7 @@ __device__ int warp_cut(const double* cp, const int* order, int n, double base, 
   return n;
 }
 
+template <int kG>  // compile-time bound on the GQA group (G <= kG), keeps the head loops branch-free
 __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT, 1)
     plan_kernel(dp_cache_view v, const void* __restrict__ q, int qdt, int G, double scale, double p1, double p2,
                 double* __restrict__ lm_out, uint8_t* __restrict__ state_out, int* __restrict__ counts,
@@ -179,9 +182,8 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT, 1)
   const int per = L.per;
   const int k0 = r * per;
   const int nloc = max(0, min(per, K - k0));
-  const int* offs = v.offs + (size_t)bh * (cap + 1);
-
   extern __shared__ __align__(16) unsigned char smem[];
+  int* offs = reinterpret_cast<int*>(smem + L.offs);  // staged copy of v.offs[bh]
   float* qf = reinterpret_cast<float*>(smem + L.qf);       // [8][d]
   double* lmS = reinterpret_cast<double*>(smem + L.lmS);  // [8][per]
   double* full = reinterpret_cast<double*>(smem + L.full);
@@ -204,89 +206,92 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT, 1)
 
   stamp(r, 0);
   // ---------------- phase 1: score my slice for all G heads ---------------
-  const int d4 = d >> 2, stride = d + 4;
+  // 8 lanes per centroid row (a warp reads 4 rows = 2 KB contiguous with
+  // float4 loads straight into registers, one tile of 32 rows ahead); each
+  // lane runs G independent fp64 chains over its d/8 dims, then the 8 lanes
+  // combine with shuffles.  No shared-memory staging, no barriers.
+  const int part = tid & 7, row = tid >> 3;
+  const int dpp = d / 8;       // dims per lane (16 at d = 128)
+  const int nv = dpp / 4;      // float4 per lane per row (<= 4)
   const float4* C4 = reinterpret_cast<const float4*>(v.centroids + ((size_t)bh * cap + k0) * d);
   const int ntiles = (nloc + kTile - 1) / kTile;
-  auto issue_tile = [&](int t, int buf) {
-    const int n = min(kTile, nloc - t * kTile);
-    for (int i = tid; i < n * d4; i += kPT) {
-      const int rr = i / d4, c = i - rr * d4;
-      const unsigned dst =
-          static_cast<unsigned>(__cvta_generic_to_shared(&ctile[(buf * kTile + rr) * stride + 4 * c]));
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(&C4[(size_t)(t * kTile + rr) * d4 + c]));
-    }
-    asm volatile("cp.async.commit_group;\n" ::);
+  float4 cur[4], nxt[4];
+  // lane `part` of a row reads float4 j*8 + part (j < nv): 8 lanes cover
+  // 128 contiguous bytes per step
+  auto load_row = [&](int t, float4 (&dst)[4]) {
+    const int rr = t * kTile + row;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      dst[j] = (rr < nloc && j < nv) ? __ldg(&C4[(size_t)rr * (d / 4) + j * 8 + part]) : make_float4(0.f, 0.f, 0.f, 0.f);
   };
-  if (ntiles > 0) issue_tile(0, 0);
-  for (int i = tid; i < G * d; i += kPT) qf[i] = load_elem_f(q, qdt, (size_t)bh * G * d + i);
+  if (ntiles > 0) load_row(0, cur);
+  {
+    const int* goffs = v.offs + (size_t)bh * (cap + 1);
+    for (int i = tid; i <= K; i += kPT) offs[i] = __ldg(&goffs[i]);
+    for (int i = tid; i < kG * d; i += kPT) qf[i] = i < G * d ? load_elem_f(q, qdt, (size_t)bh * G * d + i) : 0.f;
+  }
   __syncthreads();
-  // 8 lanes per centroid row, each over d/8 dims; G independent fp64 chains
-  const int part = tid & 7, row = tid >> 3;
-  const int dpp = d / 8;
-  double lmax[kMaxGroup];
+  stamp(r, 12);
+  double lmax[kG];
 #pragma unroll
-  for (int g = 0; g < kMaxGroup; ++g) lmax[g] = -CUDART_INF;
+  for (int g = 0; g < kG; ++g) lmax[g] = -CUDART_INF;
   for (int t = 0; t < ntiles; ++t) {
-    const int buf = t & 1;
-    if (t + 1 < ntiles) {
-      issue_tile(t + 1, buf ^ 1);
-      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-    } else {
-      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-    }
-    __syncthreads();
-    const int n = min(kTile, nloc - t * kTile);
-    double acc[kMaxGroup];
+    if (t + 1 < ntiles) load_row(t + 1, nxt);
+    double acc[kG];
 #pragma unroll
-    for (int g = 0; g < kMaxGroup; ++g) acc[g] = 0.0;
-    const float* crow = &ctile[(buf * kTile + row) * stride + part * dpp];
-    for (int j = 0; j < dpp; j += 4) {
-      const float4 c4 = *reinterpret_cast<const float4*>(crow + j);
+    for (int g = 0; g < kG; ++g) acc[g] = 0.0;
 #pragma unroll
-      for (int g = 0; g < kMaxGroup; ++g) {
-        if (g < G) {
-          const float4 q4 = *reinterpret_cast<const float4*>(qf + g * d + part * dpp + j);
-          double a = acc[g];
-          a = fma((double)c4.x, (double)q4.x, a);
-          a = fma((double)c4.y, (double)q4.y, a);
-          a = fma((double)c4.z, (double)q4.z, a);
-          a = fma((double)c4.w, (double)q4.w, a);
-          acc[g] = a;
+    for (int j = 0; j < 4; ++j) {
+      if (j < nv) {
+        const float4 c4 = cur[j];
+#pragma unroll
+        for (int g = 0; g < kG; ++g) {
+          const float4 q4 = *reinterpret_cast<const float4*>(qf + g * d + 4 * (j * 8 + part));
+          acc[g] = fma((double)c4.x, (double)q4.x, acc[g]);
+          acc[g] = fma((double)c4.y, (double)q4.y, acc[g]);
+          acc[g] = fma((double)c4.z, (double)q4.z, acc[g]);
+          acc[g] = fma((double)c4.w, (double)q4.w, acc[g]);
         }
       }
     }
 #pragma unroll
-    for (int g = 0; g < kMaxGroup; ++g) {
+    for (int g = 0; g < kG; ++g) {
       acc[g] += __shfl_xor_sync(0xffffffffu, acc[g], 1);
       acc[g] += __shfl_xor_sync(0xffffffffu, acc[g], 2);
       acc[g] += __shfl_xor_sync(0xffffffffu, acc[g], 4);
     }
-    if (row < n) {
-      const int k = k0 + t * kTile + row;
+    const int rr = t * kTile + row;
+    if (rr < nloc) {
+      const int k = k0 + rr;
       const double ls = log((double)(offs[k + 1] - offs[k]));
 #pragma unroll
-      for (int g = 0; g < kMaxGroup; ++g) {
+      for (int g = 0; g < kG; ++g) {
         if (g < G && part == g) {
           const double val = acc[g] * scale + ls;
-          lmS[g * per + t * kTile + row] = val;
+          lmS[g * per + rr] = val;
           lm_out[((size_t)bh * G + g) * cap + k] = val;
           lmax[g] = fmax(lmax[g], val);
         }
       }
     }
-    __syncthreads();  // tile buffer reuse
-  }
 #pragma unroll
-  for (int g = 0; g < kMaxGroup; ++g) {
-    const double m = warp_max(lmax[g]);
-    if (lane == 0) red[warp] = m;
-    __syncthreads();
-    if (tid == 0 && g < G) {
-      double mm = -CUDART_INF;
-      for (int w = 0; w < kPT / 32; ++w) mm = fmax(mm, red[w]);
-      s_lmax[g] = mm;
+    for (int j = 0; j < 4; ++j) cur[j] = nxt[j];
+  }
+  stamp(r, 13);
+  {  // per-head max of my slice: one barrier
+    __shared__ double s_wm[kPT / 32][kG];
+#pragma unroll
+    for (int g = 0; g < kG; ++g) {
+      const double m = warp_max(lmax[g]);
+      if (lane == 0) s_wm[warp][g] = m;
     }
     __syncthreads();
+    if (tid < G) {
+      double mm = -CUDART_INF;
+#pragma unroll
+      for (int w = 0; w < kPT / 32; ++w) mm = fmax(mm, s_wm[w][tid]);
+      s_lmax[tid] = mm;
+    }
   }
   stamp(r, 1);
   cluster.sync();  // (A) every slice scored
@@ -466,11 +471,11 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT, 1)
     reinterpret_cast<float4*>(ared + warp * 256)[lane] = acc;
     if (lane == 0) red[warp] = lsum;
     __syncthreads();
-    float* ap = wl.apart + (size_t)hq * (2 + d);
+    float* ap = wl.apart + (size_t)hq * (4 + d);
     for (int c = tid; c < d; c += kPT) {
       float sum = 0.f;
       for (int w = 0; w < kPT / 32; ++w) sum += ared[w * 256 + c];
-      ap[2 + c] = sum;
+      ap[4 + c] = sum;
     }
     if (tid == 0) {
       double l = 0.0;
@@ -486,11 +491,12 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT, 1)
   // ---------------- phase 3: GQA-union work list --------------------------
   // every CTA copies all G state arrays (16-byte DSMEM loads), computes the
   // union prefix over all clusters itself and writes its own slice
+  const int capP = (cap + 15) & ~15;
   {
     const int kq = (K + 15) / 16;
     for (int i = tid; i < G * kq; i += kPT) {
       const int gg = i / kq, c = i - gg * kq;
-      *reinterpret_cast<int4*>(stall + (size_t)gg * cap + c * 16) =
+      *reinterpret_cast<int4*>(stall + (size_t)gg * capP + c * 16) =
           *reinterpret_cast<const int4*>(cluster.map_shared_rank(stS, gg) + c * 16);
     }
   }
@@ -505,7 +511,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT, 1)
   for (int k = beg; k < end; ++k) {
     int me = 0, ma = 0;
     for (int gg = 0; gg < G; ++gg) {
-      const uint8_t s = stall[(size_t)gg * cap + k];
+      const uint8_t s = stall[(size_t)gg * capP + k];
       me |= (s == 2) << gg;
       ma |= (s == 1) << gg;
     }
@@ -523,7 +529,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT, 1)
   for (int k = beg; k < end; ++k) {
     int me = 0, ma = 0;
     for (int gg = 0; gg < G; ++gg) {
-      const uint8_t s = stall[(size_t)gg * cap + k];
+      const uint8_t s = stall[(size_t)gg * capP + k];
       me |= (s == 2) << gg;
       ma |= (s == 1) << gg;
     }
@@ -555,7 +561,6 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT, 1)
         wl.stats[4 * bh + 2] = (all_r + kChunkRows - 1) / kChunkRows;
         wl.stats[4 * bh + 3] = tot_e;
       }
-      publish_chunk_prefix(wl, v.batch * v.kv_heads);
     }
   }
   stamp(r, 6);
@@ -576,12 +581,15 @@ cudaError_t launch_plan(const dp_cache_view& v, const void* q, int qdt, int G, d
   decode_ws_layout(&v, G, &wl, nullptr, nullptr, reinterpret_cast<char*>(ws));
   wl.stats = stats;
   const size_t smem = plan_smem_bytes(v.head_dim, v.cluster_cap);
-  static size_t attr = 0;
-  if (attr < smem) {
-    cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = smem;
-  }
-  plan_kernel<<<v.batch * v.kv_heads * kCl, kPT, smem, st>>>(v, q, qdt, G, scale, p1, p2, lm, state, counts, wl);
+  const int grid = v.batch * v.kv_heads * kCl;
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<grid, kPT, smem, st>>>(v, q, qdt, G, scale, p1, p2, lm, state, counts, wl);
+  };
+  if (G <= 1) go(plan_kernel<1>);
+  else if (G <= 2) go(plan_kernel<2>);
+  else if (G <= 4) go(plan_kernel<4>);
+  else go(plan_kernel<8>);
   return cudaGetLastError();
 }
 

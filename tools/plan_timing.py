@@ -12,6 +12,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2602_05191_b200 import DecodeWorkspace, cluster_layer  # noqa: E402
 from paper_2602_05191_b200 import _native as N  # noqa: E402
 from paper_2602_05191_b200.workload import generate_layer, generate_queries  # noqa: E402
+from tools.gpu_warm import clocks, warm  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
 G = int(sys.argv[2]) if len(sys.argv) > 2 else 4
@@ -21,6 +22,8 @@ q = torch.from_numpy(generate_queries(c, G, 1)[0]).cuda().to(torch.bfloat16)
 ws = DecodeWorkspace(lay, G)
 lib = N.lib()
 view = lay.view()
+warm()
+print('clocks after warm-up:', clocks())
 for it in range(3):
     N.check(lib.dp_plan(view, N.ptr(q), 1, G, 1 / math.sqrt(128), 0.95, 0.7, N.ptr(ws.log_mass), None,
                         N.ptr(ws.counts), N.ptr(ws.stats), N.ptr(ws.ws), ws.ws.numel(),
@@ -28,9 +31,9 @@ for it in range(3):
 torch.cuda.synchronize()
 buf = (ctypes.c_ulonglong * 128)()
 lib.dp_debug_plan_timing(ctypes.cast(buf, ctypes.c_void_p))
-t = np.array(buf[:], dtype=np.float64).reshape(8, 16)[:, [0, 1, 2, 3, 8, 9, 10, 11, 4, 5, 12, 13, 6, 7]]
+t = np.array(buf[:], dtype=np.float64).reshape(8, 16)[:, [0, 12, 13, 1, 2, 8, 9, 10, 11, 4, 5, 6, 7]]
 t0 = t[:, 0].min()
-names = ["start", "p1", "syncA", "syncB", "softmx", "b1", "cut1", "st2", "p2", "syncC", "3scan", "syncD", "p3", "end"]
+names = ["start", "loads", "tiles", "p1", "syncA", "softmx", "b1", "cut1", "st2", "p2", "syncC", "p3", "end"]
 print("rank " + " ".join(f"{x:>6s}" for x in names))
 for r in range(8):
     print(f"{r:4d} " + " ".join(f"{(x - t0) / 1e3:6.2f}" if x > 0 else "     -" for x in t[r]))
@@ -46,6 +49,7 @@ for it in range(2):
                         torch.cuda.current_stream().cuda_stream))
     N.check(lib.dp_attend(view, N.ptr(q), 1, G, 1 / math.sqrt(128), N.ptr(ws.log_mass), N.ptr(ws.out),
                           N.ptr(ws.lse), N.ptr(ws.ws), ws.ws.numel(), torch.cuda.current_stream().cuda_stream))
+warm(0.3)
 torch.cuda.synchronize()
 abuf = (ctypes.c_ulonglong * (512 * 8))()
 lib.dp_debug_attn_timing(ctypes.cast(abuf, ctypes.c_void_p))
