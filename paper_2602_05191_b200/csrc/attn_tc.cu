@@ -198,6 +198,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
   const int j0 = (int)((long long)me * T / grid), j1 = (int)((long long)(me + 1) * T / grid);
   const int n = j1 - j0;
   if (n <= 0) return;
+  // number of partials (CTAs with a non-empty range) of head bh
+  auto head_parts = [&](int bh) {
+    return T >= grid ? chunk_owner(prefix[bh + 1] - 1, T, grid) - chunk_owner(prefix[bh], T, grid) + 1
+                     : prefix[bh + 1] - prefix[bh];
+  };
   auto head_of = [&](int j) {  // last b with prefix[b] <= j
     int lo = 0, hi = BH - 1;
     while (lo < hi) {
@@ -293,9 +298,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
   int cur = -1;
 
   auto flush = [&](int bh) {
-    const int first = chunk_owner(prefix[bh], T, grid);
-    const int nparts = chunk_owner(prefix[bh + 1] - 1, T, grid) - first + 1;
-    const int slot = me - first;
+    const int nparts = head_parts(bh);
+    // T >= grid: every CTA owns >= 1 chunk, slot = rank among the head's CTAs;
+    // T < grid: non-empty CTAs own exactly one chunk, slot = chunk index
+    const int slot = T >= grid ? me - chunk_owner(prefix[bh], T, grid) : j0 - prefix[bh];
     const size_t pbase = (size_t)bh * pt.max_chunks * G;
     if (tid < G) {
       pt.m[pbase + (size_t)slot * G + tid] = m_t == -INFINITY ? -INFINITY : m_t * 0.69314718055994531f;
@@ -472,8 +478,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
   __shared__ float s_aw[8];
   for (int mi = 0; mi < nm; ++mi) {
     const int bh = s_merge[mi];
-    const int first = chunk_owner(prefix[bh], T, grid);
-    const int nparts = min(kMaxParts, chunk_owner(prefix[bh + 1] - 1, T, grid) - first + 1);
+    const int nparts = min(kMaxParts, head_parts(bh));
     const size_t pbase = (size_t)bh * pt.max_chunks * G;
     if (tid == 0) wl.counters[bh] = 0;  // self-reset for the next launch
     for (int i = tid; i < G * nparts; i += kConsumers) {

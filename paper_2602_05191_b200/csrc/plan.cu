@@ -124,15 +124,30 @@ __device__ int bin_search(const double* bmass, const int* bcnt, int limit, doubl
   int crun = __shfl_sync(0xffffffffu, ci - cs, f);
   int res = limit;
   if (lane == f) {
+    // the crossing lies in lane f's bins; if its sequential re-sum rounds
+    // below thresh, fall back to its last non-empty bin (a threshold tie)
+    int last = -1;
+    double run_last = run;
+    int crun_last = crun;
     for (int j = 0; j < per; ++j) {
       const int b = f * per + j;
       if (b >= limit) break;
-      if (bcnt[b] > 0 && run + bmass[b] >= thresh) {
-        res = b;
-        break;
+      if (bcnt[b] > 0) {
+        if (run + bmass[b] >= thresh) {
+          res = b;
+          break;
+        }
+        last = b;
+        run_last = run;
+        crun_last = crun;
       }
       run += bmass[b];
       crun += bcnt[b];
+    }
+    if (res == limit && last >= 0) {
+      res = last;
+      run = run_last;
+      crun = crun_last;
     }
   }
   res = __shfl_sync(0xffffffffu, res, f);
@@ -427,10 +442,21 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT, 1)
       for (int j = tid; j < n2c; j += kPT) stS[cid[cord[base2 + j]]] = (uint8_t)(j < cut2 ? 2 : 1);
     __syncthreads();
     const int hq = bh * G + g;
-    if (tid == 0) {
-      counts[2 * hq] = b1 < kBins ? c1 + cut1 : K;
-      counts[2 * hq + 1] = c2 + cut2;
+    {  // counts straight from the states, so they can never disagree
+      int n1 = 0, n2 = 0;
+      for (int i = tid; i < K; i += kPT) {
+        n1 += stS[i] >= 1;
+        n2 += stS[i] == 2;
+      }
+      n1 = block_sum(n1, redi);
+      n2 = block_sum(n2, redi);
+      if (tid == 0) {
+        counts[2 * hq] = n1;
+        counts[2 * hq + 1] = n2;
+      }
     }
+    (void)c1;
+    (void)c2;
     if (state_out)
       for (int i = tid; i < K; i += kPT) state_out[(size_t)hq * cap + i] = stS[i];
     // approx partial: m = M, l = sum e, o = sum e * value_mean over state==1
