@@ -123,9 +123,9 @@ __device__ __forceinline__ void astamp(int ev) {
   }
 }
 
-// owner CTA of global chunk j when T chunks are split evenly over `grid`
-// CTAs as [i*T/grid, (i+1)*T/grid)
-__device__ __forceinline__ int chunk_owner(long long j, long long T, int grid) {
+// owner CTA of global row j when T rows are split evenly over `grid` CTAs
+// as [floor(i*T/grid), floor((i+1)*T/grid))
+__device__ __forceinline__ int row_owner(long long j, long long T, int grid) {
   return (int)(((j + 1) * grid - 1) / T);
 }
 
@@ -136,10 +136,40 @@ struct TcSmem {
   static constexpr size_t fixed = kv + ps + rows;
 };
 
+// Walks a CTA's contiguous range [s, end) of the global union-row sequence
+// in tiles of <= 128 rows that never straddle two heads.  Producer and
+// consumer warps run identical copies, so they agree on every tile.
+struct TileWalk {
+  long long s, end;
+  int bh;
+  __device__ __forceinline__ void init(const long long* rp, int BH, long long s0, long long e0) {
+    s = s0;
+    end = e0;
+    int lo = 0, hi = BH - 1;  // last b with rp[b] <= s, then skip empty heads
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (rp[mid] <= s) lo = mid; else hi = mid - 1;
+    }
+    bh = lo;
+    while (bh < BH - 1 && rp[bh + 1] <= s) ++bh;
+  }
+  __device__ __forceinline__ bool more() const { return s < end; }
+  // current tile: head bh, head-local rows [v0, v0 + nr)
+  __device__ __forceinline__ void tile(const long long* rp, int& tb, int& v0, int& nr) const {
+    tb = bh;
+    v0 = (int)(s - rp[bh]);
+    long long lim = rp[bh + 1] < end ? rp[bh + 1] : end;
+    nr = (int)((lim - s) < kTcRows ? (lim - s) : kTcRows);
+  }
+  __device__ __forceinline__ void next(const long long* rp, int BH, int nr) {
+    s += nr;
+    while (bh < BH - 1 && rp[bh + 1] <= s) ++bh;
+  }
+};
+
 template <bool kDense, bool kQF32>
 __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v, const void* __restrict__ q, int G,
-                                                               float scale_log2, const double* __restrict__ lm,
-                                                               WorkLists wl, Partials<float> pt,
+                                                               float scale_log2, WorkLists wl, Partials<float> pt,
                                                                float* __restrict__ out, float* __restrict__ lse,
                                                                int dbg) {
   constexpr int d = 128;
@@ -153,37 +183,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
   __nv_bfloat16* KV = reinterpret_cast<__nv_bfloat16*>(smem_raw);  // [stage][K|V][rows][stride]
   float* Ps = reinterpret_cast<float*>(smem_raw + TcSmem::kv);      // [8 heads][rows]
   int* rmask = reinterpret_cast<int*>(smem_raw + TcSmem::kv + TcSmem::ps);  // [stage][rows]
-  int* prefix = reinterpret_cast<int*>(smem_raw + TcSmem::fixed);           // [BH+1]
+  long long* rp = reinterpret_cast<long long*>(smem_raw + TcSmem::fixed);    // [BH+1] row prefix
   __shared__ float red_m[kWarps][8], red_l[kWarps][8];
-  __shared__ float s_M[8], s_L[8];
-  __shared__ int s_merge[4], s_nmerge;
+  __shared__ int s_merge[8], s_nmerge;
   __shared__ __align__(8) unsigned long long full_bar[kStages], empty_bar[kStages];
 
-  // ---- chunk prefix over heads, my contiguous chunk range -----------------
   astamp(0);
-  const int per_dense = (v.n_tokens + kTcRows - 1) / kTcRows;
-  int* nrows_s = prefix + BH + 1;  // [BH] union rows per head (sparse)
-  if (kDense) {
-    for (int b = tid; b <= BH; b += kTcThreads) prefix[b] = b * per_dense;
-  } else {
-    // exclusive prefix of the per-head chunk counts (warp 0, 32 heads per step)
-    for (int b = tid; b < BH; b += kTcThreads) nrows_s[b] = __ldcg(&wl.nrows[b]);
-    if (warp == 0) {
-      int base = 0;
-      for (int b0 = 0; b0 < BH; b0 += 32) {
-        const int nch = b0 + lane < BH ? (__ldcg(&wl.nrows[b0 + lane]) + kTcRows - 1) / kTcRows : 0;
-        int inc = nch;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int t = __shfl_up_sync(0xffffffffu, inc, o);
-          if (lane >= o) inc += t;
-        }
-        if (b0 + lane < BH) prefix[b0 + lane] = base + inc - nch;
-        base += __shfl_sync(0xffffffffu, inc, 31);
-      }
-      if (lane == 0) prefix[BH] = base;
-    }
-  }
   if (tid == 0) {
     s_nmerge = 0;
     for (int i = 0; i < kStages; ++i) {
@@ -192,48 +197,59 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
+  // PDL: everything above overlapped the plan kernel's tail; its outputs
+  // (row lists, counts, approx partials) are visible after the wait
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  // ---- row prefix over heads (warp 0, 32 heads per step) ------------------
+  if (warp == 0) {
+    long long base = 0;
+    for (int b0 = 0; b0 < BH; b0 += 32) {
+      const long long nr = b0 + lane < BH ? (kDense ? v.n_tokens : __ldcg(&wl.nrows[b0 + lane])) : 0;
+      long long inc = nr;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+      }
+      if (b0 + lane < BH) rp[b0 + lane] = base + inc - nr;
+      base += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    if (lane == 0) rp[BH] = base;
+  }
   __syncthreads();
   astamp(1);
-  const long long T = prefix[BH];
-  const int j0 = (int)((long long)me * T / grid), j1 = (int)((long long)(me + 1) * T / grid);
-  const int n = j1 - j0;
-  if (n <= 0) return;
-  // number of partials (CTAs with a non-empty range) of head bh
-  auto head_parts = [&](int bh) {
-    return T >= grid ? chunk_owner(prefix[bh + 1] - 1, T, grid) - chunk_owner(prefix[bh], T, grid) + 1
-                     : prefix[bh + 1] - prefix[bh];
-  };
-  auto head_of = [&](int j) {  // last b with prefix[b] <= j
-    int lo = 0, hi = BH - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (prefix[mid] <= j) lo = mid; else hi = mid - 1;
-    }
-    return lo;
-  };
+  const long long T = rp[BH];
+  const long long r0 = T * me / grid, r1 = T * (me + 1) / grid;
+  auto first_owner = [&](int bh) { return row_owner(rp[bh], T, grid); };
+  auto head_parts = [&](int bh) { return row_owner(rp[bh + 1] - 1, T, grid) - first_owner(bh) + 1; };
 
-  // ---- producer warps (rows [32p, 32p+32) each): run up to kStages ahead;
-  // the next chunk's row entries are fetched while this chunk's copies issue
+  // ---- producer warps (rows [32p, 32p+32) of every tile): run up to kStages
+  // tiles ahead; the next tile's row entries are fetched while this tile's
+  // copies issue
   if (warp >= kWarps) {
+    if (r0 >= r1) return;
     const int ch = lane & 15, pr0 = (warp - kWarps) * 32;
-    auto fetch = [&](int idx, unsigned& e, int& bh, int& v0) {
-      const int j = j0 + idx;
-      bh = head_of(j);
-      v0 = (j - prefix[bh]) * kTcRows;
-      const int nr = min(kTcRows, (kDense ? v.n_tokens : nrows_s[bh]) - v0);
+    TileWalk w;
+    w.init(rp, BH, r0, r1);
+    auto fetch = [&](const TileWalk& tw, unsigned& e, int& bh) {
+      int v0, nr;
+      tw.tile(rp, bh, v0, nr);
       const int row = pr0 + lane;
       e = row < nr ? (kDense ? (((unsigned)((1 << G) - 1)) << 24) | (unsigned)(v0 + row)
                              : __ldg(reinterpret_cast<const unsigned*>(wl.rowidx) + (size_t)bh * v.row_cap + v0 + row))
                    : 0xFFFFFFFFu;
+      return nr;
     };
     unsigned e_nx;
-    int bh_nx, v0_nx;
-    fetch(0, e_nx, bh_nx, v0_nx);
-    for (int idx = 0; idx < n; ++idx) {
+    int bh_nx;
+    int nr_nx = fetch(w, e_nx, bh_nx);
+    for (int idx = 0; w.more(); ++idx) {
       const int s = idx % kStages;
       const unsigned e = e_nx;
       const int bh = bh_nx;
-      if (idx + 1 < n) fetch(idx + 1, e_nx, bh_nx, v0_nx);
+      w.next(rp, BH, nr_nx);
+      if (w.more()) nr_nx = fetch(w, e_nx, bh_nx);
       if (idx >= kStages) mbar_wait(smem_u32(&empty_bar[s]), (unsigned)(((idx / kStages) + 1) & 1));
       rmask[s * kTcRows + pr0 + lane] = e == 0xFFFFFFFFu ? 0 : (int)(e >> 24);
       const size_t head_off = (size_t)bh * v.row_cap * d;
@@ -299,9 +315,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
 
   auto flush = [&](int bh) {
     const int nparts = head_parts(bh);
-    // T >= grid: every CTA owns >= 1 chunk, slot = rank among the head's CTAs;
-    // T < grid: non-empty CTAs own exactly one chunk, slot = chunk index
-    const int slot = T >= grid ? me - chunk_owner(prefix[bh], T, grid) : j0 - prefix[bh];
+    const int slot = me - first_owner(bh);
     const size_t pbase = (size_t)bh * pt.max_chunks * G;
     if (tid < G) {
       pt.m[pbase + (size_t)slot * G + tid] = m_t == -INFINITY ? -INFINITY : m_t * 0.69314718055994531f;
@@ -317,9 +331,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
     if (tid == 0 && atomicAdd(&wl.counters[bh], 1) == nparts - 1) s_merge[s_nmerge++] = bh;
   };
 
-  for (int idx = 0; idx < n; ++idx) {
-    const int j = j0 + idx, s = idx % kStages;
-    const int bh = head_of(j);
+  TileWalk w;
+  w.init(rp, BH, r0, r1);
+  for (int idx = 0; w.more(); ++idx) {
+    const int s = idx % kStages;
+    int bh, v0, nr;
+    w.tile(rp, bh, v0, nr);
+    w.next(rp, BH, nr);
     if (bh != cur) {
       if (cur >= 0) flush(cur);
       cur = bh;
@@ -341,11 +359,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
       continue;
     }
     // ---- S = K Q^T for this warp's 16 rows --------------------------------
-    const int r0 = warp * 16;
+    const int r0w = warp * 16;
     float sc[4] = {0.f, 0.f, 0.f, 0.f};
     {
       const unsigned base =
-          smem_u32(Ks + (r0 + (lane & 7) + ((lane >> 3) & 1) * 8) * kRowStride + (lane >> 4) * 8);
+          smem_u32(Ks + (r0w + (lane & 7) + ((lane >> 3) & 1) * 8) * kRowStride + (lane >> 4) * 8);
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         unsigned a0, a1, a2, a3;
@@ -363,11 +381,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
               : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(qb[k][0]), "r"(qb[k][1]));
       }
     }
-    // sc[e]: row r0 + g8 + (e>>1)*8, head 2tq + (e&1)
+    // sc[e]: row r0w + g8 + (e>>1)*8, head 2tq + (e&1)
     float mx[2] = {-INFINITY, -INFINITY};
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const int h = 2 * tq + (e & 1), r = r0 + g8 + (e >> 1) * 8;
+      const int h = 2 * tq + (e & 1), r = r0w + g8 + (e >> 1) * 8;
       const bool ok = h < G && ((rm[r] >> h) & 1);
       const float val = ok ? sc[e] * scale_log2 : -INFINITY;
       sc[e] = val;
@@ -396,7 +414,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
     float ls[2] = {0.f, 0.f};
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const int h = 2 * tq + (e & 1), r = r0 + g8 + (e >> 1) * 8;
+      const int h = 2 * tq + (e & 1), r = r0w + g8 + (e >> 1) * 8;
       const float pv = sc[e] == -INFINITY ? 0.f : exp2f(sc[e] - m_run[e & 1]);
       ls[e & 1] += pv;
       Ps[h * kTcRows + r] = pv;
@@ -434,139 +452,153 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
     {
       const unsigned vbase =
           smem_u32(Vs + ((lane & 7) + ((lane >> 4) & 1) * 8) * kRowStride + dim0 + ((lane >> 3) & 1) * 8);
+      const int ksteps = (nr + 15) >> 4;  // rows >= nr carry P = 0 (zero-filled V)
 #pragma unroll
       for (int ks = 0; ks < kTcRows / 16; ++ks) {
-        unsigned a0, a1, a2, a3;
-        ldsm_x4_t(vbase + ks * 16 * kRowStride * 2, a0, a1, a2, a3);
-        unsigned bh0 = 0u, bl0 = 0u, bh1 = 0u, bl1 = 0u;
-        if (g8 < G) {
-          const float2 p0 = *reinterpret_cast<const float2*>(Ps + g8 * kTcRows + ks * 16 + 2 * tq);
-          const float2 p1 = *reinterpret_cast<const float2*>(Ps + g8 * kTcRows + ks * 16 + 8 + 2 * tq);
-          split2(p0.x, p0.y, bh0, bl0);
-          split2(p1.x, p1.y, bh1, bl1);
+        if (ks < ksteps) {
+          unsigned a0, a1, a2, a3;
+          ldsm_x4_t(vbase + ks * 16 * kRowStride * 2, a0, a1, a2, a3);
+          unsigned bh0 = 0u, bl0 = 0u, bh1 = 0u, bl1 = 0u;
+          if (g8 < G) {
+            const float2 p0 = *reinterpret_cast<const float2*>(Ps + g8 * kTcRows + ks * 16 + 2 * tq);
+            const float2 p1 = *reinterpret_cast<const float2*>(Ps + g8 * kTcRows + ks * 16 + 8 + 2 * tq);
+            split2(p0.x, p0.y, bh0, bl0);
+            split2(p1.x, p1.y, bh1, bl1);
+          }
+          asm volatile(
+              "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+              "{%0,%1,%2,%3};\n"
+              : "+f"(o[0]), "+f"(o[1]), "+f"(o[2]), "+f"(o[3])
+              : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(bh0), "r"(bh1));
+          asm volatile(
+              "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+              "{%0,%1,%2,%3};\n"
+              : "+f"(o[0]), "+f"(o[1]), "+f"(o[2]), "+f"(o[3])
+              : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(bl0), "r"(bl1));
         }
-        asm volatile(
-            "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-            "{%0,%1,%2,%3};\n"
-            : "+f"(o[0]), "+f"(o[1]), "+f"(o[2]), "+f"(o[3])
-            : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(bh0), "r"(bh1));
-        asm volatile(
-            "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-            "{%0,%1,%2,%3};\n"
-            : "+f"(o[0]), "+f"(o[1]), "+f"(o[2]), "+f"(o[3])
-            : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(bl0), "r"(bl1));
       }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(smem_u32(&empty_bar[s]));  // stage s free for the producer
   }
   astamp(3);
-  flush(cur);
+  if (cur >= 0) flush(cur);
+  // heads with no rows at all (no sink/window, nothing exact): merged by CTA bh % grid
+  if (!kDense)
+    for (int bh = me; bh < BH; bh += grid)
+      if (rp[bh + 1] == rp[bh] && tid == 0) s_merge[s_nmerge++] = bh;
   consumers_sync();
   astamp(4);
 
   // ---- merges of the heads I finished last (engine.py:231-246) ----------
   // partials of every CTA that touched the head + the plan's approx partial
-  // (approximated clusters: logit = log-mass, value = value mean)
+  // (approximated clusters: logit = log-mass, value = value mean).  One
+  // round trip: warp w streams partials w, w+8, ... with an online rescale,
+  // then the 8 warp states are combined in shared memory.
   const int nm = s_nmerge;
-  if (nm == 0) return;
+  if (nm == 0) {
+    astamp(5);
+    return;
+  }
   __threadfence();
-  constexpr int kMaxParts = 256;
-  float* ored = reinterpret_cast<float*>(KV);        // [warps][8 heads][d]
-  float* s_pm = ored + kWarps * 8 * d;               // [8][kMaxParts] partial m
-  float* s_pw = s_pm + 8 * kMaxParts;                // [8][kMaxParts] partial l -> weight
-  __shared__ float s_aw[8];
+  astamp(6);
+  float* ored = reinterpret_cast<float*>(KV);  // [warps][8 heads][d]
+  __shared__ float s_wm[kWarps][8], s_wl[kWarps][8];
   for (int mi = 0; mi < nm; ++mi) {
     const int bh = s_merge[mi];
-    const int nparts = min(kMaxParts, head_parts(bh));
+    const bool empty = rp[bh + 1] == rp[bh];
+    const int nparts = empty ? 0 : head_parts(bh);
     const size_t pbase = (size_t)bh * pt.max_chunks * G;
     if (tid == 0) wl.counters[bh] = 0;  // self-reset for the next launch
-    for (int i = tid; i < G * nparts; i += kConsumers) {
-      const int g = i / nparts, p = i - g * nparts;
-      s_pm[g * kMaxParts + p] = __ldcg(&pt.m[pbase + (size_t)p * G + g]);
-      s_pw[g * kMaxParts + p] = __ldcg(&pt.l[pbase + (size_t)p * G + g]);
-    }
-    consumers_sync();
-    for (int g = warp; g < G; g += kWarps) {
-      const float* ap = wl.apart + ((size_t)bh * G + g) * (4 + d);
-      const float ma = kDense ? -INFINITY : __ldcg(&ap[0]);
-      float mloc = ma;
-      for (int p = lane; p < nparts; p += 32) mloc = fmaxf(mloc, s_pm[g * kMaxParts + p]);
-      const float M = warp_max(mloc);
-      float lloc = 0.f;
-      for (int p = lane; p < nparts; p += 32) {
-        const float mp = s_pm[g * kMaxParts + p];
-        const float w = mp == -INFINITY ? 0.f : __expf(mp - M);
-        lloc += s_pw[g * kMaxParts + p] * w;
-        s_pw[g * kMaxParts + p] = w;
-      }
-      lloc = warp_sum(lloc);
-      if (lane == 0) {
-        const float wa = ma == -INFINITY ? 0.f : __expf(ma - M);
-        s_aw[g] = wa;
-        s_M[g] = M;
-        s_L[g] = lloc + (wa > 0.f ? wa * __ldcg(&ap[1]) : 0.f);
-      }
-    }
-    consumers_sync();
+    float M[8], Lw[8];
     float4 acc[8];
 #pragma unroll
-    for (int g = 0; g < 8; ++g) acc[g] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (!kDense && warp == 0) {  // the approx partial
-#pragma unroll
-      for (int g = 0; g < 8; ++g)
-        if (g < G && s_aw[g] > 0.f) {
-          const float4 oa = __ldcg(reinterpret_cast<const float4*>(wl.apart + ((size_t)bh * G + g) * (4 + d) + 4) + lane);
-          acc[g].x = s_aw[g] * oa.x; acc[g].y = s_aw[g] * oa.y; acc[g].z = s_aw[g] * oa.z; acc[g].w = s_aw[g] * oa.w;
-        }
+    for (int g = 0; g < 8; ++g) {
+      M[g] = -INFINITY;
+      Lw[g] = 0.f;
+      acc[g] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    // partials: warp-strided, 2 partials (x G heads) in flight per lane
-    for (int p0 = warp; p0 < nparts; p0 += 2 * kWarps) {
-      float4 op[2][8];
+    // item i <-> partial p = i + first; p == -1 is the plan's approx partial
+    const int first = kDense ? 0 : -1;
+    const int items = nparts - first;
+    for (int i0 = warp; i0 < items; i0 += 2 * kWarps) {
+      float pm[2][8], pl[2][8];
+      float4 po[2][8];
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
-        const int p = p0 + u * kWarps;
+        const int i = i0 + u * kWarps, p = i + first;
+        const float* pmp = p >= 0 ? pt.m + pbase + (size_t)p * G : wl.apart + (size_t)bh * G * (4 + d);
+        const float* plp = p >= 0 ? pt.l + pbase + (size_t)p * G : pmp + 1;
+        const float* pop = p >= 0 ? pt.o + (pbase + (size_t)p * G) * d : pmp + 4;
+        const int sm = p >= 0 ? 1 : 4 + d, so = p >= 0 ? d : 4 + d;  // per-head strides
 #pragma unroll
-        for (int g = 0; g < 8; ++g)
-          op[u][g] = (p < nparts && g < G)
-                         ? __ldcg(reinterpret_cast<const float4*>(pt.o + (pbase + (size_t)p * G + g) * d) + lane)
-                         : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int g = 0; g < 8; ++g) {
+          pm[u][g] = -INFINITY;
+          pl[u][g] = 0.f;
+          po[u][g] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (g < G && i < items) {
+            pm[u][g] = __ldcg(pmp + g * sm);
+            pl[u][g] = __ldcg(plp + g * sm);
+            po[u][g] = __ldcg(reinterpret_cast<const float4*>(pop + (size_t)g * so) + lane);
+          }
+        }
       }
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
-        const int p = p0 + u * kWarps;
-        if (p < nparts) {
 #pragma unroll
-          for (int g = 0; g < 8; ++g) {
-            if (g < G) {
-              const float w = s_pw[g * kMaxParts + p];
-              acc[g].x += w * op[u][g].x; acc[g].y += w * op[u][g].y;
-              acc[g].z += w * op[u][g].z; acc[g].w += w * op[u][g].w;
-            }
+        for (int g = 0; g < 8; ++g) {
+          if (g < G && pm[u][g] != -INFINITY) {
+            const float mn = fmaxf(M[g], pm[u][g]);
+            const float a = __expf(M[g] - mn), b = __expf(pm[u][g] - mn);
+            Lw[g] = Lw[g] * a + pl[u][g] * b;
+            acc[g].x = acc[g].x * a + po[u][g].x * b;
+            acc[g].y = acc[g].y * a + po[u][g].y * b;
+            acc[g].z = acc[g].z * a + po[u][g].z * b;
+            acc[g].w = acc[g].w * a + po[u][g].w * b;
+            M[g] = mn;
           }
         }
       }
     }
 #pragma unroll
-    for (int g = 0; g < 8; ++g)
-      if (g < G) reinterpret_cast<float4*>(ored + ((size_t)warp * 8 + g) * d)[lane] = acc[g];
+    for (int g = 0; g < 8; ++g) {
+      if (g < G) {
+        reinterpret_cast<float4*>(ored + ((size_t)warp * 8 + g) * d)[lane] = acc[g];
+        if (lane == 0) {
+          s_wm[warp][g] = M[g];
+          s_wl[warp][g] = Lw[g];
+        }
+      }
+    }
     consumers_sync();
     for (int i = tid; i < G * d; i += kConsumers) {
       const int g = i / d, c = i - g * d;
-      float sum = 0.f;
+      float Mx = -INFINITY;
 #pragma unroll
-      for (int ww = 0; ww < kWarps; ++ww) sum += ored[(ww * 8 + g) * d + c];
-      out[((size_t)bh * G + g) * d + c] = sum / s_L[g];
+      for (int ww = 0; ww < kWarps; ++ww) Mx = fmaxf(Mx, s_wm[ww][g]);
+      float sum = 0.f, L = 0.f;
+#pragma unroll
+      for (int ww = 0; ww < kWarps; ++ww) {
+        const float wm = s_wm[ww][g];
+        if (wm != -INFINITY) {
+          const float f = __expf(wm - Mx);
+          sum += f * ored[(ww * 8 + g) * d + c];
+          L += f * s_wl[ww][g];
+        }
+      }
+      out[((size_t)bh * G + g) * d + c] = L > 0.f ? sum / L : 0.f;
+      if (c == 0) lse[(size_t)bh * G + g] = L > 0.f ? Mx + __logf(L) : -INFINITY;
     }
-    if (tid < G) lse[(size_t)bh * G + tid] = s_M[tid] + __logf(s_L[tid]);
     consumers_sync();
   }
   astamp(5);
 }
 
 }  // namespace dp
+namespace dp { extern int g_plan_cl; }
 extern "C" int dp_debug_set(int key, int value) {
   if (key == 0) dp::g_attn_debug = value;
+  if (key == 1) dp::g_plan_cl = value;
   return 0;
 }
 extern "C" int dp_debug_attn_timing(unsigned long long* out) {
@@ -575,7 +607,7 @@ extern "C" int dp_debug_attn_timing(unsigned long long* out) {
 namespace dp {
 
 
-size_t attn_tc_smem_bytes(int BH) { return TcSmem::fixed + (size_t)(2 * BH + 1) * 4; }
+size_t attn_tc_smem_bytes(int BH) { return TcSmem::fixed + (size_t)(BH + 1) * 8; }
 
 template <bool kDense, bool kQF32>
 static cudaError_t launch_tc_t(const dp_cache_view& v, const void* q, int G, double scale, const double* lm,
@@ -593,13 +625,21 @@ static cudaError_t launch_tc_t(const dp_cache_view& v, const void* q, int G, dou
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  // one persistent CTA per SM, capped by the chunk capacity
-  const int rows = kDense ? v.n_tokens : v.row_cap;
-  const long long cap_chunks = (long long)BH * ((rows + kTcRows - 1) / kTcRows);
-  const int grid = (int)(cap_chunks < sms ? cap_chunks : sms);
-  attn_tc_kernel<kDense, kQF32><<<grid, kTcThreads, smem, st>>>(v, q, G, (float)(scale * 1.4426950408889634), lm,
-                                                               wl, pt, out, lse, g_attn_debug);
-  return cudaGetLastError();
+  // one persistent CTA per SM (row ranges balanced to +-1 row)
+  const int grid = sms < kMaxPartSlots ? sms : kMaxPartSlots;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kTcThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL: prologue overlaps the plan
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  (void)lm;
+  return cudaLaunchKernelEx(&cfg, attn_tc_kernel<kDense, kQF32>, v, q, G, (float)(scale * 1.4426950408889634), wl,
+                            pt, out, lse, g_attn_debug);
 }
 
 cudaError_t launch_attn_tc(const dp_cache_view& v, const void* q, int qdt, int G, double scale, const double* lm,

@@ -511,7 +511,9 @@ size_t decode_ws_layout(const dp_cache_view* v, int G, WorkLists* wl, void** par
                         char* base) {
   const size_t BH = (size_t)v->batch * v->kv_heads;
   const int cap = v->cluster_cap;
-  const int max_chunks = (v->row_cap + kChunkRows - 1) / kChunkRows;
+  // partial slots per head: one per 128-row chunk (generic kernel) or one
+  // per CTA touching the head (persistent tensor-core kernel, grid <= kMaxPartSlots)
+  const int max_chunks = std::max((v->row_cap + kChunkRows - 1) / kChunkRows, kMaxPartSlots);
   const size_t acc = v->dtype == DP_F32 ? 8 : 4;
   size_t off = 0;
   auto take = [&](size_t bytes) {

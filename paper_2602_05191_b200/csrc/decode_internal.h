@@ -10,6 +10,7 @@ namespace dp {
 
 constexpr int kChunkRows = 128;   // rows per split-KV work item
 constexpr int kAttnThreads = 256;
+constexpr int kMaxPartSlots = 256;  // persistent attention grid cap (partials per head)
 
 // Device work lists (one set per (b, kv head)), carved from the workspace.
 struct WorkLists {

@@ -8,6 +8,7 @@
 //   E  cp.async 16 B, one chunk per CTA, 3 CTAs/SM (the old kernel)
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o bw_probe bw_probe.cu
 #include <cstdio>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 constexpr int ROWB = 256, ROWS_PER_CHUNK = 128, STRIDE = 272, STAGES = 3;
@@ -99,6 +100,80 @@ __global__ void __launch_bounds__(128) probe_e(const char* __restrict__ k, const
   if (sm[tid * 16] == 0x7f && sm[tid * 16 + 1] == 0x3e) *sink = 1;
 }
 
+
+// TMA tensor probes: 128-row chunks, K and V each split in two 64-column
+// (128 B) halves, 128B swizzle.  MODE 3: one box {64,128} per half;
+// MODE 4: boxes {64,8}; MODE 5: tile::gather4 with box {64,1}.
+template <int MODE>
+__global__ void __launch_bounds__(128, 1) probe_tma(const __grid_constant__ CUtensorMap km, const __grid_constant__ CUtensorMap vm,
+                                                    int nchunks, int* sink) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  __shared__ __align__(8) unsigned long long bar[STAGES];
+  const int tid = threadIdx.x;
+  const int j0 = (int)((long long)blockIdx.x * nchunks / gridDim.x), j1 = (int)((long long)(blockIdx.x + 1) * nchunks / gridDim.x);
+  const int n = j1 - j0;
+  unsigned char* base = sm + ((1024 - (su(sm) & 1023)) & 1023);
+  if (tid == 0)
+    for (int i = 0; i < STAGES; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su(&bar[i])));
+  __syncthreads();
+  auto issue = [&](int j, int s) {
+    if (tid != 0) return;
+    const unsigned b = su(&bar[s]);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(ROWS_PER_CHUNK * ROWB * 2));
+    unsigned char* st = base + (size_t)s * 65536;
+    const int row0 = j * ROWS_PER_CHUNK;
+    for (int t = 0; t < 2; ++t) {
+      const unsigned long long m = t == 0 ? (unsigned long long)&km : (unsigned long long)&vm;
+      for (int h = 0; h < 2; ++h) {
+        unsigned char* dst = st + t * 32768 + h * 16384;
+        if (MODE == 3) {
+          asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+                       ::"r"(su(dst)), "l"(m), "r"(h * 64), "r"(row0), "r"(b) : "memory");
+        } else if (MODE == 4) {
+          for (int r = 0; r < ROWS_PER_CHUNK; r += 8)
+            asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+                         ::"r"(su(dst + r * 128)), "l"(m), "r"(h * 64), "r"(row0 + r), "r"(b) : "memory");
+        } else {
+          for (int r = 0; r < ROWS_PER_CHUNK; r += 4)
+            asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];"
+                         ::"r"(su(dst + r * 128)), "l"(m), "r"(h * 64), "r"(row0 + r), "r"(row0 + r + 1), "r"(row0 + r + 2), "r"(row0 + r + 3), "r"(b) : "memory");
+        }
+      }
+    }
+  };
+  for (int i = 0; i < STAGES && i < n; ++i) issue(j0 + i, i);
+  int acc = 0;
+  for (int idx = 0; idx < n; ++idx) {
+    const int s = idx % STAGES;
+    asm volatile("{ .reg .pred p; W_%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; @!p bra W_%=; }" ::"r"(su(&bar[s])), "r"((idx / STAGES) & 1) : "memory");
+    __syncthreads();
+    acc += base[(size_t)s * 65536 + tid * 16];
+    __syncthreads();
+    if (idx + STAGES < n) issue(j0 + idx + STAGES, s);
+  }
+  if (acc == 0x7fffffff) *sink = acc;
+}
+
+typedef CUresult (*EncFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                          const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                          CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static CUtensorMap make_map(const char* p, size_t rows, unsigned boxrows) {
+  static EncFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&fn, cudaEnableDefault, &q);
+  }
+  CUtensorMap m;
+  cuuint64_t dims[2] = {128, rows};
+  cuuint64_t strides[1] = {256};
+  cuuint32_t box[2] = {64, boxrows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (void*)p, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) printf("encode failed %d (box rows %u)\n", (int)r, boxrows);
+  return m;
+}
+
 int main() {
   const size_t bytes = (size_t)8 * 32768 * ROWB;  // one of K/V per layer
   const int layers = 8;                             // cycle layers so L2 never holds the data
@@ -121,8 +196,20 @@ int main() {
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   const char* names[] = {"A ldg.128 regs (SMs x8 CTAs)", "B cp.async16 ring 1CTA/SM", "C bulk/row ring 1CTA/SM",
-                         "D bulk/8KB ring 1CTA/SM", "E cp.async16 1chunk/CTA 3/SM", "A2 ldg.128 (SMs x32 CTAs)"};
-  for (int mode = 0; mode < 6; ++mode) {
+                         "D bulk/8KB ring 1CTA/SM", "E cp.async16 1chunk/CTA 3/SM", "A2 ldg.128 (SMs x32 CTAs)",
+                         "F TMA box 64x128 swz ring", "G TMA box 64x8 swz ring", "H TMA gather4 swz ring"};
+  const size_t tring = (size_t)STAGES * 65536 + 1024;
+  cudaFuncSetAttribute(probe_tma<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tring);
+  cudaFuncSetAttribute(probe_tma<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tring);
+  cudaFuncSetAttribute(probe_tma<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tring);
+  const size_t rows = bytes / ROWB;
+  CUtensorMap kmF[8], vmF[8], kmG[8], vmG[8], kmH[8], vmH[8];
+  for (int l = 0; l < layers; ++l) {
+    kmF[l] = make_map(k + l * bytes, rows, 128); vmF[l] = make_map(v + l * bytes, rows, 128);
+    kmG[l] = make_map(k + l * bytes, rows, 8); vmG[l] = make_map(v + l * bytes, rows, 8);
+    kmH[l] = make_map(k + l * bytes, rows, 1); vmH[l] = make_map(v + l * bytes, rows, 1);
+  }
+  for (int mode = 0; mode < 9; ++mode) {
     for (int rep = 0; rep < 2; ++rep) {
       cudaEventRecord(e0);
       for (int l = 0; l < layers; ++l) {
@@ -134,6 +221,9 @@ int main() {
         if (mode == 2) probe_ring<1><<<sms, 128, ring>>>(kl, vl, nchunks, sink);
         if (mode == 3) probe_ring<2><<<sms, 128, ring>>>(kl, vl, nchunks, sink);
         if (mode == 4) probe_e<<<nchunks, 128, 2 * ROWS_PER_CHUNK * STRIDE>>>(kl, vl, nchunks, sink);
+        if (mode == 6) probe_tma<3><<<sms, 128, tring>>>(kmF[l], vmF[l], nchunks, sink);
+        if (mode == 7) probe_tma<4><<<sms, 128, tring>>>(kmG[l], vmG[l], nchunks, sink);
+        if (mode == 8) probe_tma<5><<<sms, 128, tring>>>(kmH[l], vmH[l], nchunks, sink);
       }
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
@@ -142,6 +232,6 @@ int main() {
       if (rep) printf("%-34s %8.1f GB/s  (%.1f us per 134 MB layer)\n", names[mode], 2.0 * bytes * layers / (ms * 1e-3) / 1e9, ms * 1e3 / layers);
     }
   }
-  printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
+  printf("err: %s\n", cudaGetErrorString(cudaDeviceSynchronize()));
   return 0;
 }

@@ -16,6 +16,8 @@ from tools.gpu_warm import clocks, warm  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
 G = int(sys.argv[2]) if len(sys.argv) > 2 else 4
+if len(sys.argv) > 3:
+    N.lib().dp_debug_set(1, int(sys.argv[3]))  # force the plan cluster size
 k, v, c = generate_layer(1, 8, n, 128)
 lay = cluster_layer(k, v)
 q = torch.from_numpy(generate_queries(c, G, 1)[0]).cuda().to(torch.bfloat16)
@@ -29,13 +31,15 @@ for it in range(3):
                         N.ptr(ws.counts), N.ptr(ws.stats), N.ptr(ws.ws), ws.ws.numel(),
                         torch.cuda.current_stream().cuda_stream))
 torch.cuda.synchronize()
-buf = (ctypes.c_ulonglong * 128)()
+buf = (ctypes.c_ulonglong * 384)()
 lib.dp_debug_plan_timing(ctypes.cast(buf, ctypes.c_void_p))
-t = np.array(buf[:], dtype=np.float64).reshape(8, 16)[:, [0, 12, 13, 1, 2, 8, 9, 10, 11, 4, 5, 6, 7]]
+t = np.array(buf[:], dtype=np.float64).reshape(16, 24)[:, [0, 1, 2, 14, 10, 3, 4, 11, 13, 5, 6, 15, 7, 8, 16, 17, 18, 19, 9]]
+nr = 16 if t[8:, 0].min() > 0 else 8
+t = t[:nr]
 t0 = t[:, 0].min()
-names = ["start", "loads", "tiles", "p1", "syncA", "softmx", "b1", "cut1", "st2", "p2", "syncC", "p3", "end"]
+names = ["start", "loads", "qreg", "mma0", "score", "P1", "A", "b1", "cut1", "P2", "B", "cnts", "P3", "C", "aps", "dbg", "scan", "expand", "P4"]
 print("rank " + " ".join(f"{x:>6s}" for x in names))
-for r in range(8):
+for r in range(nr):
     print(f"{r:4d} " + " ".join(f"{(x - t0) / 1e3:6.2f}" if x > 0 else "     -" for x in t[r]))
 print("counts", ws.counts[0, :G].tolist(), "stats", ws.stats[0, 0].tolist())
 
