@@ -203,15 +203,19 @@ int dp_cluster_build(const dp_cluster_params* p, const void* src_keys, const voi
                      void* workspace, size_t workspace_bytes, void* stream);
 
 /* Profiling aid: %globaltimer stamps (ns) of the last dp_plan launch's first
- * cluster, [8 ranks][8 phase events], copied to host memory. */
-int dp_debug_plan_timing(unsigned long long* out); /* [8][16] */
+ * cluster, [16 ranks][24 phase events], copied to host memory. */
+int dp_debug_plan_timing(unsigned long long* out); /* [16][24] */
 /* Profiling aid: per-CTA %globaltimer stamps of the last bf16 attention
  * launch, [512 CTAs][8 events]: start, prefix loaded, first stage landed,
  * main loop done, flushed, exit. */
 int dp_debug_attn_timing(unsigned long long* out);
 /* Profiling switches: key 0 = attention flags (bit 0: skip the math, stream
- * K/V only).  Never set on the product path. */
+ * K/V only); key 1 = force the plan cluster size (8 or 16; 0 = auto).
+ * Never set on the product path. */
 int dp_debug_set(int key, int value);
+/* Profiling aid: co-resident plan clusters at this geometry for cluster size
+ * cl (cudaOccupancyMaxActiveClusters). */
+int dp_debug_plan_occupancy(const dp_cache_view* v, int G, int cl);
 
 /* Lower-level pieces of the above (used by the parity tests). */
 /* k-means++ picks only: picks int32 [B*H, k]. */
