@@ -205,8 +205,10 @@ int dp_cluster_build(const dp_cluster_params* p, const void* src_keys, const voi
 /* Profiling aid: %globaltimer stamps (ns) of the last dp_plan launch's first
  * cluster, [16 ranks][24 phase events], copied to host memory. */
 int dp_debug_plan_timing(unsigned long long* out); /* [16][24] */
+/* Profiling aid: clock64 at the first / last stamp of the same launch [16][2]. */
+int dp_debug_plan_clock(unsigned long long* out);
 /* Profiling aid: per-CTA %globaltimer stamps of the last bf16 attention
- * launch, [512 CTAs][8 events]: start, prefix loaded, first stage landed,
+ * launch, [512 CTAs][12 events]: start, prefix loaded, first stage landed,
  * main loop done, flushed, exit. */
 int dp_debug_attn_timing(unsigned long long* out);
 /* Profiling switches: key 0 = attention flags (bit 0: skip the math, stream

@@ -63,6 +63,7 @@ _SIGS = {
     "dp_plan": (ctypes.c_int, [ctypes.POINTER(CacheView), _vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_double,
                                ctypes.c_double, ctypes.c_double, _vp, _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp]),
     "dp_debug_plan_timing": (ctypes.c_int, [_vp]),
+    "dp_debug_plan_clock": (ctypes.c_int, [_vp]),
     "dp_debug_attn_timing": (ctypes.c_int, [_vp]),
     "dp_debug_set": (ctypes.c_int, [ctypes.c_int, ctypes.c_int]),
     "dp_debug_plan_occupancy": (ctypes.c_int, [ctypes.POINTER(CacheView), ctypes.c_int, ctypes.c_int]),

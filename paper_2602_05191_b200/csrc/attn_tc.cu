@@ -42,8 +42,15 @@ int g_attn_debug = 0;  // profiling switches (dp_debug_set)
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void cp16(unsigned dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src));
+// K/V rows are read once per step: evict-first in L2, so the streamed cache
+// does not push out what is reused (code, work lists, partials, tables)
+__device__ __forceinline__ unsigned long long evict_first_policy() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void cp16(unsigned dst, const void* src, unsigned long long pol) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "l"(pol));
 }
 __device__ __forceinline__ void ldsm_x4(unsigned addr, unsigned& r0, unsigned& r1, unsigned& r2, unsigned& r3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
@@ -114,7 +121,7 @@ __device__ __forceinline__ void bulk_row(unsigned dst, const void* src, unsigned
 
 // per-CTA phase stamps (%globaltimer ns) of the last launch; profiling aid,
 // read with dp_debug_attn_timing()
-__device__ unsigned long long g_attn_ts[512][8];
+__device__ unsigned long long g_attn_ts[512][12];
 __device__ __forceinline__ void astamp(int ev) {
   if (threadIdx.x == 0 && blockIdx.x < 512) {
     unsigned long long t;
@@ -181,11 +188,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __nv_bfloat16* KV = reinterpret_cast<__nv_bfloat16*>(smem_raw);  // [stage][K|V][rows][stride]
-  float* Ps = reinterpret_cast<float*>(smem_raw + TcSmem::kv);      // [8 heads][rows]
+  float* Pbuf = reinterpret_cast<float*>(smem_raw + TcSmem::kv);    // [8 warps][16 rows][8 heads]
   int* rmask = reinterpret_cast<int*>(smem_raw + TcSmem::kv + TcSmem::ps);  // [stage][rows]
   long long* rp = reinterpret_cast<long long*>(smem_raw + TcSmem::fixed);    // [BH+1] row prefix
-  __shared__ float red_m[kWarps][8], red_l[kWarps][8];
-  __shared__ int s_merge[8], s_nmerge;
+  __shared__ float s_wm[kWarps][8], s_wl[kWarps][8];  // warp states (flush / merge)
+  __shared__ int s_merge[32], s_nmerge;
   __shared__ __align__(8) unsigned long long full_bar[kStages], empty_bar[kStages];
 
   astamp(0);
@@ -230,6 +237,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
   if (warp >= kWarps) {
     if (r0 >= r1) return;
     const int ch = lane & 15, pr0 = (warp - kWarps) * 32;
+    const unsigned long long pol = evict_first_policy();
     TileWalk w;
     w.init(rp, BH, r0, r1);
     auto fetch = [&](const TileWalk& tw, unsigned& e, int& bh) {
@@ -267,8 +275,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
         const unsigned vd = smem_u32(Vs + row * kRowStride + ch * 8);
         if (er != 0xFFFFFFFFu) {
           const size_t off = (size_t)(er & 0xFFFFFFu) * d + ch * 8;
-          cp16(kd, Kg + off);
-          cp16(vd, Vg + off);
+          cp16(kd, Kg + off, pol);
+          cp16(vd, Vg + off, pol);
         } else {
           cp16_zero(kd, Kg);
           cp16_zero(vd, Vg);
@@ -305,30 +313,76 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
     }
   };
 
-  // O^T accumulator of this warp: dims [16w, 16w+16) x heads; lane holds
-  // (dim 16w+g8, heads 2tq, 2tq+1) in o[0..1] and dim +8 in o[2..3]
-  float o[4];
-  float m_run[2];                       // running max (log2) of heads 2tq, 2tq+1
-  float m_t = -INFINITY, l_t = 0.f;     // running max / sum of head `tid` (tid < G)
-  const int dim0 = warp * 16;
+  // Every consumer warp owns rows [16w, 16w+16) of each tile end to end:
+  // S = K Q^T for its rows, its own online softmax, and O^T += V^T P over
+  // all 128 dims -- no CTA-wide barrier per tile.  The 8 warp states are
+  // combined once per head segment (flush), in the K buffer of the segment's
+  // last tile before that stage is released to the producer.
+  float o[8][4];       // O^T block mb: dims 16mb + g8 (+8) x heads 2tq, 2tq+1
+  float m_run[2];      // running max (log2 units) of heads 2tq + hh over this warp's rows
+  float l_run[2];      // this lane's share (rows g8, g8+8) of the running sum of heads 2tq + hh
+  float* Pw = Pbuf + warp * 128;  // [16 rows][8 heads] P transpose buffer of this warp
+  const int r0w = warp * 16;
   int cur = -1;
 
-  auto flush = [&](int bh) {
-    const int nparts = head_parts(bh);
+  // partial (m, l, o) of a finished head segment; the completion counters are
+  // bumped once, after the loop, behind a single fence (no mid-loop stall)
+  int flushed[2] = {-1, -1}, nflushed = 0;  // a CTA range touches <= 2 heads unless heads are tiny
+  auto flush = [&](int bh, float* scratch) {
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      l_run[hh] += __shfl_xor_sync(0xffffffffu, l_run[hh], 4);
+      l_run[hh] += __shfl_xor_sync(0xffffffffu, l_run[hh], 8);
+      l_run[hh] += __shfl_xor_sync(0xffffffffu, l_run[hh], 16);
+    }
+    consumers_sync();  // every warp is done reading this stage
+#pragma unroll
+    for (int mb = 0; mb < 8; ++mb)
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        scratch[((size_t)warp * 8 + 2 * tq + (e & 1)) * d + mb * 16 + g8 + (e >> 1) * 8] = o[mb][e];
+    if (g8 == 0) {
+      s_wm[warp][2 * tq] = m_run[0];
+      s_wm[warp][2 * tq + 1] = m_run[1];
+      s_wl[warp][2 * tq] = l_run[0];
+      s_wl[warp][2 * tq + 1] = l_run[1];
+    }
+    consumers_sync();
     const int slot = me - first_owner(bh);
     const size_t pbase = (size_t)bh * pt.max_chunks * G;
-    if (tid < G) {
-      pt.m[pbase + (size_t)slot * G + tid] = m_t == -INFINITY ? -INFINITY : m_t * 0.69314718055994531f;
-      pt.l[pbase + (size_t)slot * G + tid] = l_t;
-    }
+#pragma unroll 1
+    for (int i = tid; i < G * d; i += kConsumers) {
+      const int h = i / d, c = i - h * d;
+      float Mx = -INFINITY;
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int h = 2 * tq + (e & 1), dd = dim0 + g8 + (e >> 1) * 8;
-      if (h < G) pt.o[(pbase + (size_t)slot * G + h) * d + dd] = o[e];
+      for (int ww = 0; ww < kWarps; ++ww) Mx = fmaxf(Mx, s_wm[ww][h]);
+      float sum = 0.f, L = 0.f;
+#pragma unroll
+      for (int ww = 0; ww < kWarps; ++ww) {
+        const float wm = s_wm[ww][h];
+        if (wm != -INFINITY) {
+          const float f = exp2f(wm - Mx);
+          sum += f * scratch[((size_t)ww * 8 + h) * d + c];
+          L += f * s_wl[ww][h];
+        }
+      }
+      pt.o[(pbase + (size_t)slot * G + h) * d + c] = sum;
+      if (c == 0) {
+        pt.m[pbase + (size_t)slot * G + h] = Mx == -INFINITY ? -INFINITY : Mx * 0.69314718055994531f;
+        pt.l[pbase + (size_t)slot * G + h] = L;
+      }
     }
-    __threadfence();
-    consumers_sync();
-    if (tid == 0 && atomicAdd(&wl.counters[bh], 1) == nparts - 1) s_merge[s_nmerge++] = bh;
+    consumers_sync();  // scratch (this stage) and s_wm/s_wl free again
+    if (nflushed < 2) {
+      flushed[nflushed++] = bh;
+    } else {  // many tiny heads in one range: publish the oldest now
+      if (tid == 0) {
+        __threadfence();
+        if (atomicAdd(&wl.counters[flushed[0]], 1) == head_parts(flushed[0]) - 1) s_merge[s_nmerge++] = flushed[0];
+      }
+      flushed[0] = flushed[1];
+      flushed[1] = bh;
+    }
   };
 
   TileWalk w;
@@ -338,155 +392,122 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
     int bh, v0, nr;
     w.tile(rp, bh, v0, nr);
     w.next(rp, BH, nr);
+    const bool seg_end = !w.more() || w.bh != bh;
     if (bh != cur) {
-      if (cur >= 0) flush(cur);
       cur = bh;
       load_q(bh);
 #pragma unroll
-      for (int e = 0; e < 4; ++e) o[e] = 0.f;
+      for (int mb = 0; mb < 8; ++mb)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) o[mb][e] = 0.f;
       m_run[0] = m_run[1] = -INFINITY;
-      m_t = -INFINITY;
-      l_t = 0.f;
+      l_run[0] = l_run[1] = 0.f;
     }
     mbar_wait(smem_u32(&full_bar[s]), (unsigned)((idx / kStages) & 1));  // stage s landed
     if (idx == 0) astamp(2);
-    const __nv_bfloat16* Ks = KV + (size_t)s * 2 * kStageElems;
+    __nv_bfloat16* Ks = KV + (size_t)s * 2 * kStageElems;
     const __nv_bfloat16* Vs = Ks + kStageElems;
-    const int* rm = rmask + s * kTcRows;
-    if (dbg & 1) {  // profiling: stream only, no math
-      __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&empty_bar[s]));
-      continue;
-    }
-    // ---- S = K Q^T for this warp's 16 rows --------------------------------
-    const int r0w = warp * 16;
-    float sc[4] = {0.f, 0.f, 0.f, 0.f};
-    {
-      const unsigned base =
-          smem_u32(Ks + (r0w + (lane & 7) + ((lane >> 3) & 1) * 8) * kRowStride + (lane >> 4) * 8);
+    if (!(dbg & 1) && r0w < nr) {
+      // ---- S = K Q^T for this warp's 16 rows (two accumulators: short chains)
+      float sa[4] = {0.f, 0.f, 0.f, 0.f}, sb[4] = {0.f, 0.f, 0.f, 0.f};
+      {
+        const unsigned base =
+            smem_u32(Ks + (r0w + (lane & 7) + ((lane >> 3) & 1) * 8) * kRowStride + (lane >> 4) * 8);
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
+        for (int k = 0; k < 8; ++k) {
+          unsigned a0, a1, a2, a3;
+          ldsm_x4(base + k * 32, a0, a1, a2, a3);
+          float* acc = (k & 1) ? sb : sa;
+          asm volatile(
+              "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+              "{%0,%1,%2,%3};\n"
+              : "+f"(acc[0]), "+f"(acc[1]), "+f"(acc[2]), "+f"(acc[3])
+              : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(qa[k][0]), "r"(qa[k][1]));
+          if (kQF32)
+            asm volatile(
+                "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                "{%0,%1,%2,%3};\n"
+                : "+f"(acc[0]), "+f"(acc[1]), "+f"(acc[2]), "+f"(acc[3])
+                : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(qb[k][0]), "r"(qb[k][1]));
+        }
+      }
+      // sc[e]: row r0w + g8 + (e>>1)*8, head 2tq + (e&1); masked by the row's head set
+      const int* rm = rmask + s * kTcRows + r0w + g8;
+      const int mlo = rm[0], mhi = rm[8];
+      float sc[4], mx[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int h = 2 * tq + (e & 1);
+        const bool ok = h < G && (((e >> 1) ? mhi : mlo) >> h & 1);
+        sc[e] = ok ? (sa[e] + sb[e]) * scale_log2 : -INFINITY;
+        mx[e & 1] = fmaxf(mx[e & 1], sc[e]);
+      }
+      float alpha[2];
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        mx[hh] = fmaxf(mx[hh], __shfl_xor_sync(0xffffffffu, mx[hh], 4));
+        mx[hh] = fmaxf(mx[hh], __shfl_xor_sync(0xffffffffu, mx[hh], 8));
+        mx[hh] = fmaxf(mx[hh], __shfl_xor_sync(0xffffffffu, mx[hh], 16));
+        const float mn = fmaxf(m_run[hh], mx[hh]);
+        alpha[hh] = mn == -INFINITY ? 1.f : exp2f(m_run[hh] - mn);
+        m_run[hh] = mn;
+        l_run[hh] *= alpha[hh];
+      }
+      float pv[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        pv[e] = sc[e] == -INFINITY ? 0.f : exp2f(sc[e] - m_run[e & 1]);
+        l_run[e & 1] += pv[e];
+      }
+#pragma unroll
+      for (int mb = 0; mb < 8; ++mb) {
+        o[mb][0] *= alpha[0];
+        o[mb][1] *= alpha[1];
+        o[mb][2] *= alpha[0];
+        o[mb][3] *= alpha[1];
+      }
+      // P (rows x heads) -> B fragment (k = row, n = head) through the warp's buffer
+      *reinterpret_cast<float2*>(Pw + g8 * 8 + 2 * tq) = make_float2(pv[0], pv[1]);
+      *reinterpret_cast<float2*>(Pw + (g8 + 8) * 8 + 2 * tq) = make_float2(pv[2], pv[3]);
+      __syncwarp();
+      unsigned bh0, bl0, bh1, bl1;
+      split2(Pw[(2 * tq) * 8 + g8], Pw[(2 * tq + 1) * 8 + g8], bh0, bl0);
+      split2(Pw[(2 * tq + 8) * 8 + g8], Pw[(2 * tq + 9) * 8 + g8], bh1, bl1);
+      __syncwarp();
+      // ---- O^T += V^T P over all 128 dims (8 independent m-blocks)
+      const unsigned vbase =
+          smem_u32(Vs + (r0w + (lane & 7) + ((lane >> 4) & 1) * 8) * kRowStride + ((lane >> 3) & 1) * 8);
+#pragma unroll
+      for (int mb = 0; mb < 8; ++mb) {
         unsigned a0, a1, a2, a3;
-        ldsm_x4(base + k * 32, a0, a1, a2, a3);
+        ldsm_x4_t(vbase + mb * 32, a0, a1, a2, a3);
         asm volatile(
             "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
             "{%0,%1,%2,%3};\n"
-            : "+f"(sc[0]), "+f"(sc[1]), "+f"(sc[2]), "+f"(sc[3])
-            : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(qa[k][0]), "r"(qa[k][1]));
-        if (kQF32)
-          asm volatile(
-              "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-              "{%0,%1,%2,%3};\n"
-              : "+f"(sc[0]), "+f"(sc[1]), "+f"(sc[2]), "+f"(sc[3])
-              : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(qb[k][0]), "r"(qb[k][1]));
+            : "+f"(o[mb][0]), "+f"(o[mb][1]), "+f"(o[mb][2]), "+f"(o[mb][3])
+            : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(bh0), "r"(bh1));
+        asm volatile(
+            "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+            "{%0,%1,%2,%3};\n"
+            : "+f"(o[mb][0]), "+f"(o[mb][1]), "+f"(o[mb][2]), "+f"(o[mb][3])
+            : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(bl0), "r"(bl1));
       }
     }
-    // sc[e]: row r0w + g8 + (e>>1)*8, head 2tq + (e&1)
-    float mx[2] = {-INFINITY, -INFINITY};
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int h = 2 * tq + (e & 1), r = r0w + g8 + (e >> 1) * 8;
-      const bool ok = h < G && ((rm[r] >> h) & 1);
-      const float val = ok ? sc[e] * scale_log2 : -INFINITY;
-      sc[e] = val;
-      mx[e & 1] = fmaxf(mx[e & 1], val);
-    }
-#pragma unroll
-    for (int hh = 0; hh < 2; ++hh) {
-#pragma unroll
-      for (int off = 4; off < 32; off <<= 1) mx[hh] = fmaxf(mx[hh], __shfl_xor_sync(0xffffffffu, mx[hh], off));
-    }
-    if (g8 == 0) {
-      red_m[warp][2 * tq] = mx[0];
-      red_m[warp][2 * tq + 1] = mx[1];
-    }
-    consumers_sync();
-    float alpha[2];
-#pragma unroll
-    for (int hh = 0; hh < 2; ++hh) {
-      float cm = -INFINITY;
-#pragma unroll
-      for (int ww = 0; ww < kWarps; ++ww) cm = fmaxf(cm, red_m[ww][2 * tq + hh]);
-      const float mn = fmaxf(m_run[hh], cm);
-      alpha[hh] = mn == -INFINITY ? 1.f : exp2f(m_run[hh] - mn);
-      m_run[hh] = mn;
-    }
-    float ls[2] = {0.f, 0.f};
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int h = 2 * tq + (e & 1), r = r0w + g8 + (e >> 1) * 8;
-      const float pv = sc[e] == -INFINITY ? 0.f : exp2f(sc[e] - m_run[e & 1]);
-      ls[e & 1] += pv;
-      Ps[h * kTcRows + r] = pv;
-    }
-#pragma unroll
-    for (int hh = 0; hh < 2; ++hh) {
-#pragma unroll
-      for (int off = 4; off < 32; off <<= 1) ls[hh] += __shfl_xor_sync(0xffffffffu, ls[hh], off);
-    }
-    if (g8 == 0) {
-      red_l[warp][2 * tq] = ls[0];
-      red_l[warp][2 * tq + 1] = ls[1];
-    }
-    o[0] *= alpha[0];
-    o[1] *= alpha[1];
-    o[2] *= alpha[0];
-    o[3] *= alpha[1];
-    float alpha_t = 1.f;
-    if (tid < G) {
-      float cmt = -INFINITY;
-#pragma unroll
-      for (int ww = 0; ww < kWarps; ++ww) cmt = fmaxf(cmt, red_m[ww][tid]);
-      const float mtn = fmaxf(m_t, cmt);
-      alpha_t = mtn == -INFINITY ? 1.f : exp2f(m_t - mtn);
-      m_t = mtn;
-    }
-    consumers_sync();  // Ps, red_l visible
-    if (tid < G) {
-      float cl = 0.f;
-#pragma unroll
-      for (int ww = 0; ww < kWarps; ++ww) cl += red_l[ww][tid];
-      l_t = l_t * alpha_t + cl;
-    }
-    // ---- O^T += V^T P for this warp's 16 dims --------------------------------
-    {
-      const unsigned vbase =
-          smem_u32(Vs + ((lane & 7) + ((lane >> 4) & 1) * 8) * kRowStride + dim0 + ((lane >> 3) & 1) * 8);
-      const int ksteps = (nr + 15) >> 4;  // rows >= nr carry P = 0 (zero-filled V)
-#pragma unroll
-      for (int ks = 0; ks < kTcRows / 16; ++ks) {
-        if (ks < ksteps) {
-          unsigned a0, a1, a2, a3;
-          ldsm_x4_t(vbase + ks * 16 * kRowStride * 2, a0, a1, a2, a3);
-          unsigned bh0 = 0u, bl0 = 0u, bh1 = 0u, bl1 = 0u;
-          if (g8 < G) {
-            const float2 p0 = *reinterpret_cast<const float2*>(Ps + g8 * kTcRows + ks * 16 + 2 * tq);
-            const float2 p1 = *reinterpret_cast<const float2*>(Ps + g8 * kTcRows + ks * 16 + 8 + 2 * tq);
-            split2(p0.x, p0.y, bh0, bl0);
-            split2(p1.x, p1.y, bh1, bl1);
-          }
-          asm volatile(
-              "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-              "{%0,%1,%2,%3};\n"
-              : "+f"(o[0]), "+f"(o[1]), "+f"(o[2]), "+f"(o[3])
-              : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(bh0), "r"(bh1));
-          asm volatile(
-              "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-              "{%0,%1,%2,%3};\n"
-              : "+f"(o[0]), "+f"(o[1]), "+f"(o[2]), "+f"(o[3])
-              : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(bl0), "r"(bl1));
-        }
-      }
-    }
+    if (seg_end) flush(bh, reinterpret_cast<float*>(Ks));  // this stage's K buffer is the scratch
     __syncwarp();
     if (lane == 0) mbar_arrive(smem_u32(&empty_bar[s]));  // stage s free for the producer
   }
   astamp(3);
-  if (cur >= 0) flush(cur);
-  // heads with no rows at all (no sink/window, nothing exact): merged by CTA bh % grid
-  if (!kDense)
-    for (int bh = me; bh < BH; bh += grid)
-      if (rp[bh + 1] == rp[bh] && tid == 0) s_merge[s_nmerge++] = bh;
+  consumers_sync();  // every partial of this CTA is written (CTA scope)
+  if (tid == 0) {
+    __threadfence();  // ... and visible at gpu scope before the counters move (cumulativity)
+    for (int i = 0; i < nflushed; ++i)
+      if (atomicAdd(&wl.counters[flushed[i]], 1) == head_parts(flushed[i]) - 1) s_merge[s_nmerge++] = flushed[i];
+    // heads with no rows at all (no sink/window, nothing exact): merged by CTA bh % grid
+    if (!kDense)
+      for (int bh = me; bh < BH; bh += grid)
+        if (rp[bh + 1] == rp[bh]) s_merge[s_nmerge++] = bh;
+  }
   consumers_sync();
   astamp(4);
 
@@ -503,93 +524,99 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
   __threadfence();
   astamp(6);
   float* ored = reinterpret_cast<float*>(KV);  // [warps][8 heads][d]
-  __shared__ float s_wm[kWarps][8], s_wl[kWarps][8];
   for (int mi = 0; mi < nm; ++mi) {
     const int bh = s_merge[mi];
     const bool empty = rp[bh + 1] == rp[bh];
     const int nparts = empty ? 0 : head_parts(bh);
     const size_t pbase = (size_t)bh * pt.max_chunks * G;
     if (tid == 0) wl.counters[bh] = 0;  // self-reset for the next launch
-    float M[8], Lw[8];
-    float4 acc[8];
-#pragma unroll
-    for (int g = 0; g < 8; ++g) {
-      M[g] = -INFINITY;
-      Lw[g] = 0.f;
-      acc[g] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (mi == 0 && tid == 0 && blockIdx.x < 512) {  // profiling: one dependent L2 round trip
+      unsigned long long ta, tb;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ta));
+      const float probe = __ldcg(pt.m + pbase);
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tb) : "f"(probe));
+      g_attn_ts[blockIdx.x][11] = (tb - ta) + (probe == 12345.f);
     }
-    // item i <-> partial p = i + first; p == -1 is the plan's approx partial
+    // warp w merges head g = w % G over partials p = first + w / G, + 8/G, ...
+    // (p == -1 is the plan's approx partial); each round issues kU loads
+    // before using any
     const int first = kDense ? 0 : -1;
-    const int items = nparts - first;
-    for (int i0 = warp; i0 < items; i0 += 2 * kWarps) {
-      float pm[2][8], pl[2][8];
-      float4 po[2][8];
+    const int wpg = kWarps / G;  // warps per head (G in {1, 2, 4, 8})
+    const int g = warp % G;
+    float M = -INFINITY, Lw = 0.f;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (warp < wpg * G) {
+      constexpr int kU = 16;
+      for (int p0 = first + warp / G; p0 < nparts; p0 += kU * wpg) {
+        float pm[kU], pl[kU];
+        float4 po[kU];
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int i = i0 + u * kWarps, p = i + first;
-        const float* pmp = p >= 0 ? pt.m + pbase + (size_t)p * G : wl.apart + (size_t)bh * G * (4 + d);
-        const float* plp = p >= 0 ? pt.l + pbase + (size_t)p * G : pmp + 1;
-        const float* pop = p >= 0 ? pt.o + (pbase + (size_t)p * G) * d : pmp + 4;
-        const int sm = p >= 0 ? 1 : 4 + d, so = p >= 0 ? d : 4 + d;  // per-head strides
-#pragma unroll
-        for (int g = 0; g < 8; ++g) {
-          pm[u][g] = -INFINITY;
-          pl[u][g] = 0.f;
-          po[u][g] = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (g < G && i < items) {
-            pm[u][g] = __ldcg(pmp + g * sm);
-            pl[u][g] = __ldcg(plp + g * sm);
-            po[u][g] = __ldcg(reinterpret_cast<const float4*>(pop + (size_t)g * so) + lane);
+        for (int u = 0; u < kU; ++u) {
+          const int p = p0 + u * wpg;
+          pm[u] = -INFINITY;
+          pl[u] = 0.f;
+          po[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (p < nparts) {
+            if (p >= 0) {
+              pm[u] = __ldcg(pt.m + pbase + (size_t)p * G + g);
+              pl[u] = __ldcg(pt.l + pbase + (size_t)p * G + g);
+              po[u] = __ldcg(reinterpret_cast<const float4*>(pt.o + (pbase + (size_t)p * G + g) * d) + lane);
+            } else {
+              const float* ap = wl.apart + ((size_t)bh * G + g) * (4 + d);
+              pm[u] = __ldcg(ap);
+              pl[u] = __ldcg(ap + 1);
+              po[u] = __ldcg(reinterpret_cast<const float4*>(ap + 4) + lane);
+            }
           }
         }
-      }
+        float mx = M;
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < kU; ++u) mx = fmaxf(mx, pm[u]);
+        if (mx != -INFINITY) {
+          const float a = __expf(M - mx);
+          Lw *= a;
+          acc.x *= a; acc.y *= a; acc.z *= a; acc.w *= a;
 #pragma unroll
-        for (int g = 0; g < 8; ++g) {
-          if (g < G && pm[u][g] != -INFINITY) {
-            const float mn = fmaxf(M[g], pm[u][g]);
-            const float a = __expf(M[g] - mn), b = __expf(pm[u][g] - mn);
-            Lw[g] = Lw[g] * a + pl[u][g] * b;
-            acc[g].x = acc[g].x * a + po[u][g].x * b;
-            acc[g].y = acc[g].y * a + po[u][g].y * b;
-            acc[g].z = acc[g].z * a + po[u][g].z * b;
-            acc[g].w = acc[g].w * a + po[u][g].w * b;
-            M[g] = mn;
+          for (int u = 0; u < kU; ++u) {
+            const float b = pm[u] == -INFINITY ? 0.f : __expf(pm[u] - mx);
+            Lw += pl[u] * b;
+            acc.x += po[u].x * b; acc.y += po[u].y * b; acc.z += po[u].z * b; acc.w += po[u].w * b;
           }
+          M = mx;
         }
       }
     }
-#pragma unroll
-    for (int g = 0; g < 8; ++g) {
-      if (g < G) {
-        reinterpret_cast<float4*>(ored + ((size_t)warp * 8 + g) * d)[lane] = acc[g];
-        if (lane == 0) {
-          s_wm[warp][g] = M[g];
-          s_wl[warp][g] = Lw[g];
-        }
+    if (mi == 0) {
+      astamp(7);
+      if (tid == 0 && blockIdx.x < 512) {
+        g_attn_ts[blockIdx.x][9] = nm;
+        g_attn_ts[blockIdx.x][10] = nparts;
       }
+    }
+    reinterpret_cast<float4*>(ored + (size_t)warp * d)[lane] = acc;
+    if (lane == 0) {
+      s_wm[warp][0] = M;
+      s_wl[warp][0] = Lw;
     }
     consumers_sync();
     for (int i = tid; i < G * d; i += kConsumers) {
-      const int g = i / d, c = i - g * d;
+      const int gg = i / d, c = i - gg * d;
       float Mx = -INFINITY;
-#pragma unroll
-      for (int ww = 0; ww < kWarps; ++ww) Mx = fmaxf(Mx, s_wm[ww][g]);
+      for (int ww = gg; ww < wpg * G; ww += G) Mx = fmaxf(Mx, s_wm[ww][0]);
       float sum = 0.f, L = 0.f;
-#pragma unroll
-      for (int ww = 0; ww < kWarps; ++ww) {
-        const float wm = s_wm[ww][g];
+      for (int ww = gg; ww < wpg * G; ww += G) {
+        const float wm = s_wm[ww][0];
         if (wm != -INFINITY) {
           const float f = __expf(wm - Mx);
-          sum += f * ored[(ww * 8 + g) * d + c];
-          L += f * s_wl[ww][g];
+          sum += f * ored[(size_t)ww * d + c];
+          L += f * s_wl[ww][0];
         }
       }
-      out[((size_t)bh * G + g) * d + c] = L > 0.f ? sum / L : 0.f;
-      if (c == 0) lse[(size_t)bh * G + g] = L > 0.f ? Mx + __logf(L) : -INFINITY;
+      out[((size_t)bh * G + gg) * d + c] = L > 0.f ? sum / L : 0.f;
+      if (c == 0) lse[(size_t)bh * G + gg] = L > 0.f ? Mx + __logf(L) : -INFINITY;
     }
     consumers_sync();
+    if (mi == 0) astamp(8);
   }
   astamp(5);
 }
@@ -602,7 +629,7 @@ extern "C" int dp_debug_set(int key, int value) {
   return 0;
 }
 extern "C" int dp_debug_attn_timing(unsigned long long* out) {
-  return cudaMemcpyFromSymbol(out, dp::g_attn_ts, sizeof(dp::g_attn_ts)) == cudaSuccess ? 0 : 2;  // [512][8]
+  return cudaMemcpyFromSymbol(out, dp::g_attn_ts, sizeof(dp::g_attn_ts)) == cudaSuccess ? 0 : 2;  // [512][12]
 }
 namespace dp {
 

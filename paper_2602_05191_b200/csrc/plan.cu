@@ -52,16 +52,19 @@ constexpr double kFix = 549755813888.0;  // 2^39 fixed-point scale of e = exp(lm
 constexpr int kPlanMaxCap = 4096;
 constexpr int kCh = 128;
 constexpr int kTileBytes = kCh * 128 * 4;  // one tile: kCh rows x 128 fp32 (4 swizzled column blocks)
-constexpr int kMaxPer = 512;      // clusters per CTA slice (cap 4096 / 8)          // centroid rows per shared-memory tile (P1)
+constexpr int kMaxPer = 512;
+constexpr int kApx = 96;          // approximated clusters staged per P3 round      // clusters per CTA slice (cap 4096 / 8)          // centroid rows per shared-memory tile (P1)
 
 // phase timestamps (%globaltimer, ns) of cluster 0: [rank][event]; read with
 // dp_debug_plan_timing() -- profiling aid only
 __device__ unsigned long long g_plan_ts[16][24];
+__device__ unsigned long long g_plan_clk[16][2];
 __device__ __forceinline__ void stamp(int r, int ev) {
   if (blockIdx.x < 16 && threadIdx.x == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     g_plan_ts[r][ev] = t;
+    if (ev == 0 || ev == 9) g_plan_clk[r][ev == 9] = clock64();
   }
 }
 
@@ -81,6 +84,7 @@ struct PlanLayout {
   size_t um, bin, hm, hc, clist, cord;  // P2 arrays (inside the cs region)
   size_t lmall;            // [cap] fp64 log-masses of my head (owners; pushed by every CTA)
   size_t lml;              // [kG][per] fp64 log-masses of my slice
+  size_t qd;               // [8][d + 4] fp64 queries (padded rows)
   size_t stl;              // [kG][per] u8 states of my slice (pushed by the owners)
   size_t aps;              // [CL][d + 4] fp32 approx partials of my head (owners; pushed by every CTA)
   size_t offs;             // [per + 1] int row offsets of my slice
@@ -109,13 +113,14 @@ __host__ __device__ inline PlanLayout plan_layout(int CL, int kG, int d, int cap
   L.clist = take2((size_t)cap * 4);
   L.cord = take2((size_t)cap * 4);
   const size_t csb = (size_t)2 * kTileBytes;  // two TMA tiles (128B swizzle) to d + 4 floats (conflict-free A loads)
-  const size_t redb = (size_t)kPW * kG * (d + 4) * 4;  // P3 cross-warp scratch
+  const size_t redb = ((size_t)kApx * (d + 8) + (size_t)kPW * kG * (d + 4)) * 4;  // P3: value means, weights, sums
   size_t big = csb > p2 ? csb : p2;
   big = big > redb ? big : redb;
   L.cs = take(big);
   L.um += L.cs; L.bin += L.cs; L.hm += L.cs; L.hc += L.cs; L.clist += L.cs; L.cord += L.cs;
   L.lmall = take((size_t)cap * 8);
-  L.lml = take((size_t)kG * L.per * 8 > (size_t)8 * (d + 4) * 4 ? (size_t)kG * L.per * 8 : (size_t)8 * (d + 4) * 4);
+  L.lml = take((size_t)kG * L.per * 8);
+  L.qd = take((size_t)8 * (d + 4) * 8);
   L.stl = take((size_t)kG * L.per);
   L.aps = take((size_t)CL * (d + 4) * 4);
   L.offs = take((size_t)(L.per + 1) * 4);
@@ -172,6 +177,113 @@ __device__ __forceinline__ void scan_pair(unsigned long long m, int c, unsigned 
   ct = cbt;
 }
 
+// ---------------------------------------------------------------------------
+// P2 pieces, one copy each (__noinline__): this code runs once per launch on
+// a cold instruction cache, so its footprint -- not its instruction count --
+// is what costs time.  All threads of the CTA call them.
+// ---------------------------------------------------------------------------
+struct SelShared {
+  unsigned long long before, at;
+  int b, n, nc, cbefore;
+};
+
+// first bin (< limit) whose inclusive mass reaches thr; before / cbefore =
+// mass / count of the bins ahead of it.  bm/bc: this thread's kBinsPT bins.
+__device__ __noinline__ int sel_find_bin(SelShared* sh, const unsigned long long* bm, const int* bc,
+                                         unsigned long long mbase, int cbase, double thr, int limit) {
+  const int tid = threadIdx.x;
+  if (tid == 0) sh->b = kBins;
+  __syncthreads();
+  unsigned long long m = mbase, hmass = 0;
+  int c = cbase, hit = -1, hcnt = 0;
+#pragma unroll
+  for (int j = 0; j < kBinsPT; ++j) {
+    const int b = tid * kBinsPT + j;
+    if (hit < 0 && b < limit && bm[j] && (double)(m + bm[j]) >= thr) {
+      hit = b;
+      hmass = m;
+      hcnt = c;
+    }
+    m += bm[j];
+    c += bc[j];
+  }
+  if (hit >= 0) atomicMin(&sh->b, hit);
+  __syncthreads();
+  const int bb = sh->b;
+  if (hit == bb) {
+    sh->before = hmass;
+    sh->cbefore = hcnt;
+  }
+  __syncthreads();
+  return bb;
+}
+
+// members of bin b -> clist (any order), then cord[rank] = member with the
+// exact (log-mass desc, cluster id asc) rank; returns the member count
+__device__ __noinline__ int sel_rank_bin(SelShared* sh, const uint16_t* binI, const double* lmall, int* clist,
+                                         int* cord, int K, int b) {
+  const int tid = threadIdx.x;
+  if (tid == 0) sh->nc = 0;
+  __syncthreads();
+#pragma unroll 1
+  for (int i = tid; i < K; i += kPT)
+    if (binI[i] == b) clist[atomicAdd(&sh->nc, 1)] = i;
+  __syncthreads();
+  const int n = sh->nc;
+#pragma unroll 1
+  for (int a = tid; a < n; a += kPT) {
+    const int ia = clist[a];
+    const double la = lmall[ia];
+    int rk = 0;
+#pragma unroll 1
+    for (int j = 0; j < n; ++j) {
+      const int ij = clist[j];
+      const double lj = lmall[ij];
+      rk += lj > la || (lj == la && ij < ia);
+    }
+    cord[rk] = ia;
+  }
+  __syncthreads();
+  return n;
+}
+
+// warp 0: first j < n with base + sum_{t<=j} u[cord[t]] >= thr (n if none);
+// sh->at = that inclusive sum
+__device__ __noinline__ int sel_cut(SelShared* sh, const unsigned long long* um, const int* cord, int n,
+                                    unsigned long long base, double thr) {
+  const int lane = threadIdx.x & 31;
+  if ((threadIdx.x >> 5) == 0) {
+    int res = n;
+    unsigned long long at = base;
+#pragma unroll 1
+    for (int j0 = 0; j0 < n; j0 += 32) {
+      const int j = j0 + lane;
+      unsigned long long inc = j < n ? um[cord[j]] : 0ull;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+      }
+      const unsigned long long cum = base + inc;
+      const unsigned hit = __ballot_sync(0xffffffffu, j < n && (double)cum >= thr);
+      if (hit) {
+        const int f = __ffs(hit) - 1;
+        res = j0 + f;
+        at = __shfl_sync(0xffffffffu, cum, f);
+        break;
+      }
+      base += __shfl_sync(0xffffffffu, inc, 31);
+      at = base;
+    }
+    if (lane == 0) {
+      sh->n = res;
+      sh->at = at;
+    }
+  }
+  __syncthreads();
+  return sh->n;
+}
+
 template <int CL, int kG>
 __global__ void __launch_bounds__(kPT, 1)
     plan_kernel(const __grid_constant__ CUtensorMap tmC, dp_cache_view v, const void* __restrict__ q, int qdt, int G,
@@ -189,6 +301,7 @@ __global__ void __launch_bounds__(kPT, 1)
   float* Cs = reinterpret_cast<float*>(smem + L.cs);
   double* lmall = reinterpret_cast<double*>(smem + L.lmall);
   double* lml = reinterpret_cast<double*>(smem + L.lml);
+  double* qd = reinterpret_cast<double*>(smem + L.qd);
   uint8_t* stl = reinterpret_cast<uint8_t*>(smem + L.stl);
   float* aps = reinterpret_cast<float*>(smem + L.aps);
   int* offs = reinterpret_cast<int*>(smem + L.offs);
@@ -200,13 +313,14 @@ __global__ void __launch_bounds__(kPT, 1)
   __shared__ double s_wm[kPW][kG];
   __shared__ unsigned long long s_redu[kPW];
   __shared__ int s_redi[kPW * 4];
-  __shared__ int s_b, s_n, s_nc;
-  __shared__ unsigned long long s_before, s_at;
-  __shared__ int s_cbefore;
-  __shared__ int s_alist[kMaxPer];          // approx clusters of my slice (local id | head mask << 16), P3
+  __shared__ SelShared s_sel;
+  __shared__ int s_alist[kMaxPer];      // approx clusters of my slice (local id | head mask << 16), P3
   __shared__ int s_na;
 
   asm volatile("griddepcontrol.wait;\n" ::: "memory");  // PDL: inputs of the previous grid are visible
+  // let the attention grid become resident on the SMs this launch leaves free
+  // (its CTAs wait for our completion before reading anything we write)
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   cl_arrive_relaxed();  // (S) every CTA of the cluster has started before DSMEM is touched
   stamp(r, 0);
 
@@ -216,60 +330,54 @@ __global__ void __launch_bounds__(kPT, 1)
   const int nloc = max(0, min(per, K - k0));
 
   // ---------------- P1: score my centroid slice ---------------------------
-  // The slice streams through a shared-memory tile of kCh rows padded to
-  // d + 4 floats (conflict-free MMA A-fragment loads) with 128-bit loads;
-  // the next tile is fetched into registers while this one is multiplied.
+  // Tiles of kCh centroid rows arrive by TMA (two in flight, 128B swizzle).
   // S[row, head] = sum_k C[row, k] q[head, k] on the fp64 tensor pipe:
   // mma.m8n8k4.f64 with M = 8 centroid rows, N = 8 heads (G <= 8, the rest
-  // zero), K = 4 dims; each lane feeds one fp32 centroid element (exact in
-  // fp64) per MMA, the query B-fragments stay in registers.
-  const int qP = d + 4;  // padded query rows (conflict-free fragment loads)
-  float* qs = reinterpret_cast<float*>(smem + L.lml);  // staging for q (lml is written only after)
+  // zero), K = 4 dims; fp32 centroids and queries are exact in fp64.
+  const int qP = d + 4;  // padded fp64 query rows: conflict-free B-fragment loads
   const unsigned bar0 = (unsigned)__cvta_generic_to_shared(&s_tbar[0]);
   const int ntile = (nloc + kCh - 1) / kCh;
   const int ncb = d / 32;  // 128-B column blocks per row
-  // TMA: tile t -> buffer t & 1, one 2-D box (32 floats x kCh rows, 128B
-  // swizzle) per column block, completing on s_tbar[t & 1]
-  auto issue_tile = [&](int t) {
-    const unsigned b = bar0 + (unsigned)(t & 1) * 8;
-    const unsigned dst = (unsigned)__cvta_generic_to_shared(Cs) + (unsigned)(t & 1) * kTileBytes;
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(b), "r"((unsigned)(ncb * kCh * 128))
-                 : "memory");
-    for (int cb = 0; cb < ncb; ++cb)
-      asm volatile(
-          "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
-              dst + (unsigned)cb * kCh * 128),
-          "l"(reinterpret_cast<unsigned long long>(&tmC)), "r"(cb * 32), "r"(bh * cap + k0 + t * kCh), "r"(b)
-          : "memory");
-  };
   if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar0));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar0 + 8));
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    if (ntile > 0) issue_tile(0);
-    if (ntile > 1) issue_tile(1);
+  }
+  // TMA: tile t -> buffer t & 1, one 2-D box (32 floats x kCh rows) per column block
+#pragma unroll 1
+  for (int t = 0; t < 2 && t < ntile; ++t) {
+    if (tid == 0) {
+      const unsigned b = bar0 + (unsigned)(t & 1) * 8;
+      const unsigned dst = (unsigned)__cvta_generic_to_shared(Cs) + (unsigned)(t & 1) * kTileBytes;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(b), "r"((unsigned)(ncb * kCh * 128))
+                   : "memory");
+#pragma unroll 1
+      for (int cb = 0; cb < ncb; ++cb)
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+                dst + (unsigned)cb * kCh * 128),
+            "l"(reinterpret_cast<unsigned long long>(&tmC)), "r"(cb * 32), "r"(bh * cap + k0 + t * kCh), "r"(b)
+            : "memory");
+    }
   }
   {
     const int* goffs = v.offs + (size_t)bh * (cap + 1) + k0;
+#pragma unroll 1
     for (int i = tid; i <= nloc; i += kPT) offs[i] = __ldg(&goffs[i]);
+#pragma unroll 1
     for (int i = tid; i < 8 * d; i += kPT) {
       const int h = i / d, c = i - h * d;
-      qs[h * qP + c] = h < G ? load_elem_f(q, qdt, ((size_t)bh * G + h) * d + c) : 0.f;
+      qd[h * qP + c] = h < G ? (double)load_elem_f(q, qdt, ((size_t)bh * G + h) * d + c) : 0.0;
     }
-    if (tid == 0) {
-      s_nc = 0;
-      s_na = 0;
-    }
+    if (tid == 0) s_na = 0;
   }
-  __syncthreads();  // qs, offs, barrier init
+  __syncthreads();  // qd, offs, barrier init
   stamp(r, 1);
-  double qreg[32];  // lane l: q[head l/4][4 kk + l%4]
-#pragma unroll
-  for (int kk = 0; kk < 32; ++kk) qreg[kk] = kk * 4 < d ? (double)qs[(lane >> 2) * qP + kk * 4 + (lane & 3)] : 0.0;
-  stamp(r, 2);
   cl_wait();  // (S)
-  stamp(r, 12);
+  stamp(r, 2);
   double lmax[2] = {-CUDART_INF, -CUDART_INF};  // heads 2(l%4), 2(l%4)+1
+  const double* qrow = qd + (lane >> 2) * qP + (lane & 3);  // B fragment: q[head l/4][4 kk + l%4]
+#pragma unroll 1
   for (int t = 0; t < ntile; ++t) {
     const int row0 = t * kCh;
     {
@@ -284,29 +392,27 @@ __global__ void __launch_bounds__(kPT, 1)
     }
     const unsigned char* tileC = reinterpret_cast<const unsigned char*>(Cs) + (size_t)(t & 1) * kTileBytes;
     const int nrb = (min(kCh, nloc - row0) + 7) >> 3;
+#pragma unroll 1
     for (int rb = warp; rb < nrb; rb += kPW) {
-      // row i = rb*8 + lane/4, dim = 4 kk + lane%4: column block kk/8, 16-B chunk
-      // kk%8 stored at chunk (kk%8) ^ (i%8) (128B swizzle) -> 32 distinct banks
+      // row i = rb*8 + lane/4, dim = 4 kk + lane%4: column block kk/8, 16-B
+      // chunk kk%8 stored at chunk (kk%8) ^ (i%8) (128B swizzle) -> 32 banks
       const int ia = rb * 8 + (lane >> 2);
       const unsigned char* arow = tileC + (size_t)ia * 128 + (lane & 3) * 4;
       const int sw = ia & 7;
       double c[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
-#pragma unroll
-      for (int kk = 0; kk < 32; kk += 4) {
+#pragma unroll 1
+      for (int kk = 0; kk < d / 4; kk += 4) {
 #pragma unroll
         for (int tt = 0; tt < 4; ++tt) {
-          if ((kk + tt) * 4 < d) {
-            const int kq = kk + tt;
-            const double a = (double)*reinterpret_cast<const float*>(
-                arow + (size_t)(kq >> 3) * kCh * 128 + (((kq & 7) ^ sw) << 4));
-            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-                         : "+d"(c[tt][0]), "+d"(c[tt][1])
-                         : "d"(a), "d"(qreg[kk + tt]));
-          }
+          const int kq = kk + tt;
+          const double a =
+              (double)*reinterpret_cast<const float*>(arow + (size_t)(kq >> 3) * kCh * 128 + (((kq & 7) ^ sw) << 4));
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                       : "+d"(c[tt][0]), "+d"(c[tt][1])
+                       : "d"(a), "d"(qrow[kq * 4]));
         }
       }
-      const int row = row0 + rb * 8 + (lane >> 2);
-      if (t == 0 && rb == 0) stamp(r, 14);
+      const int row = row0 + ia;
       if (row < nloc) {
         const double ls = log((double)(offs[row + 1] - offs[row]));
 #pragma unroll
@@ -325,7 +431,18 @@ __global__ void __launch_bounds__(kPT, 1)
       __syncthreads();
       if (tid == 0) {
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        issue_tile(t + 2);
+        const unsigned b = bar0 + (unsigned)(t & 1) * 8;
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(Cs) + (unsigned)(t & 1) * kTileBytes;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(b),
+                     "r"((unsigned)(ncb * kCh * 128))
+                     : "memory");
+#pragma unroll 1
+        for (int cb = 0; cb < ncb; ++cb)
+          asm volatile(
+              "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+                  dst + (unsigned)cb * kCh * 128),
+              "l"(reinterpret_cast<unsigned long long>(&tmC)), "r"(cb * 32), "r"(bh * cap + k0 + (t + 2) * kCh), "r"(b)
+              : "memory");
       }
     }
   }
@@ -342,7 +459,7 @@ __global__ void __launch_bounds__(kPT, 1)
   __syncthreads();
   if (tid < G) {
     double mm = -CUDART_INF;
-#pragma unroll
+#pragma unroll 1
     for (int w = 0; w < kPW; ++w) mm = fmax(mm, s_wm[w][tid]);
     remote(cluster, &s_max[0][0], tid)[r * kG + tid] = mm;
   }
@@ -356,15 +473,14 @@ __global__ void __launch_bounds__(kPT, 1)
     const int hq = bh * G + g;
     unsigned long long* um = reinterpret_cast<unsigned long long*>(smem + L.um);
     uint16_t* binI = reinterpret_cast<uint16_t*>(smem + L.bin);
-    unsigned long long* hm = reinterpret_cast<unsigned long long*>(smem + L.hm);
+    unsigned* hmh = reinterpret_cast<unsigned*>(smem + L.hm);  // [kBins] high 19 bits of the mass
+    unsigned* hml = hmh + kBins;                               // [kBins] low 20 bits
     int* hc = reinterpret_cast<int*>(smem + L.hc);
     int* clist = reinterpret_cast<int*>(smem + L.clist);
     int* cord = reinterpret_cast<int*>(smem + L.cord);
     double M = -CUDART_INF;
-#pragma unroll
+#pragma unroll 1
     for (int rr = 0; rr < CL; ++rr) M = fmax(M, s_max[rr][g]);
-    unsigned* hmh = reinterpret_cast<unsigned*>(hm);  // [kBins] high parts
-    unsigned* hml = hmh + kBins;                         // [kBins] low parts
 #pragma unroll
     for (int j = 0; j < kBinsPT; ++j) {
       hmh[tid * kBinsPT + j] = 0u;
@@ -372,6 +488,8 @@ __global__ void __launch_bounds__(kPT, 1)
       hc[tid * kBinsPT + j] = 0;
     }
     __syncthreads();
+    stamp(r, 20);
+#pragma unroll 1
     for (int i = tid; i < K; i += kPT) {
       const float xf = (float)(M - lmall[i]);  // >= 0
       const unsigned long long u = __float2ull_rn(__expf(-xf) * (float)kFix);
@@ -379,14 +497,14 @@ __global__ void __launch_bounds__(kPT, 1)
       b = b < 0 ? 0 : (b >= kBins ? kBins - 1 : b);
       um[i] = u;
       binI[i] = (uint16_t)b;
-      if (u) {  // native 32-bit shared atomics (a 64-bit add is a CAS loop): 19 + 20 bit halves
+      if (u) {  // native 32-bit shared atomics (a 64-bit add is a CAS loop)
         atomicAdd(&hmh[b], (unsigned)(u >> 20));
         atomicAdd(&hml[b], (unsigned)(u & 0xFFFFFu));
       }
       atomicAdd(&hc[b], 1);
     }
     __syncthreads();
-    // my 4 bins [4 tid, 4 tid + 4): exclusive (mass, count) bases
+    stamp(r, 21);
     unsigned long long bm[kBinsPT];
     int bc[kBinsPT];
     unsigned long long msum = 0;
@@ -400,142 +518,76 @@ __global__ void __launch_bounds__(kPT, 1)
     }
     unsigned long long mbase, total;
     int cbase, ctot;
-    if (tid == 0) s_b = kBins;
     scan_pair(msum, csum, s_redu, s_redi, mbase, cbase, total, ctot);
-    // first bin (< limit) whose inclusive mass reaches thr; s_before / s_cbefore
-    auto find_bin = [&](double thr, int limit) {
-      unsigned long long m = mbase;
-      int c = cbase, hit = -1;
-      unsigned long long hm_ = 0;
-      int hc_ = 0;
-#pragma unroll
-      for (int j = 0; j < kBinsPT; ++j) {
-        const int b = tid * kBinsPT + j;
-        if (hit < 0 && b < limit && bm[j] && (double)(m + bm[j]) >= thr) {
-          hit = b;
-          hm_ = m;
-          hc_ = c;
-        }
-        m += bm[j];
-        c += bc[j];
-      }
-      if (hit >= 0) atomicMin(&s_b, hit);
-      __syncthreads();
-      const int bb = s_b;
-      if (hit == bb) {
-        s_before = hm_;
-        s_cbefore = hc_;
-      }
-      __syncthreads();
-      return bb;
-    };
-    // members of bin b (any order) -> clist; exact rank by (lm desc, id asc) -> cord
-    auto rank_bin = [&](int b) {
-      for (int i = tid; i < K; i += kPT)
-        if (binI[i] == b) clist[atomicAdd(&s_nc, 1)] = i;
-      __syncthreads();
-      const int n = s_nc;
-      for (int a = tid; a < n; a += kPT) {
-        const int ia = clist[a];
-        const double la = lmall[ia];
-        int rk = 0;
-        for (int j = 0; j < n; ++j) {
-          const int ij = clist[j];
-          rk += before(lmall[ij], ij, la, ia);
-        }
-        cord[rk] = ia;
-      }
-      __syncthreads();
-      if (tid == 0) s_nc = 0;  // ready for the next bin (read again only after a barrier)
-      return n;
-    };
-    // warp 0: first j < n with base + sum_{t<=j} u[cord[t]] >= thr (n if none);
-    // s_at = that inclusive sum
-    auto cut_in = [&](int n, unsigned long long base, double thr) {
-      if (warp == 0) {
-        int res = n;
-        unsigned long long at = base;
-        for (int j0 = 0; j0 < n; j0 += 32) {
-          const int j = j0 + lane;
-          const unsigned long long val = j < n ? um[cord[j]] : 0ull;
-          unsigned long long inc = val;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const unsigned long long t = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc += t;
-          }
-          const unsigned long long cum = base + inc;
-          const unsigned hit = __ballot_sync(0xffffffffu, j < n && (double)cum >= thr);
-          if (hit) {
-            const int f = __ffs(hit) - 1;
-            res = j0 + f;
-            at = __shfl_sync(0xffffffffu, cum, f);
-            break;
-          }
-          base += __shfl_sync(0xffffffffu, inc, 31);
-          at = base;
-        }
-        if (lane == 0) {
-          s_n = res;
-          s_at = at;
-        }
-      }
-      __syncthreads();
-      return s_n;
-    };
-    // cluster i's state byte goes to the CTA owning its slice
-    auto push_state = [&](int i, int s) {
-      const int rr = i / per;
-      remote(cluster, stl, rr)[g * L.per + (i - rr * per)] = (uint8_t)s;
-    };
-
+    stamp(r, 22);
+    int b1 = kBins, cut1 = 0, n1c = 0, cbefore1 = 0, b2 = kBins, cut2 = 0, n2 = 0;
+    unsigned long long before1 = 0;
     if (K > 0) {
-      // stage 1 (selection.py:57-58): crossing of p1 * total
-      const double thr1 = p1 * (double)total;
-      const int b1 = find_bin(thr1, kBins);  // always found: total reaches thr1
-      const unsigned long long before1 = s_before;
-      const int cbefore1 = s_cbefore;
-      stamp(r, 11);
-      const int n1c = rank_bin(b1);
-      const int j1 = cut_in(n1c, before1, thr1);
-      const int cut1 = j1 < n1c ? j1 + 1 : n1c;
-      stamp(r, 13);
-      const unsigned long long sub = s_at;  // retained mass (engine.py:191); j1 < n1c always
-      // stage 2 (engine.py:191-194): same order, threshold p2 * sub
-      const double thr2 = p2 * (double)sub;
-      int b2 = b1, cut2 = 0, n2 = 0;
-      if ((double)before1 >= thr2 && cbefore1 > 0) {  // crossing strictly below bin b1
-        if (tid == 0) s_b = kBins;
-        __syncthreads();
-        b2 = find_bin(thr2, b1);
-        const unsigned long long before2 = s_before;
-        const int cbefore2 = s_cbefore;
-        // bin b1's order lives in cord; emit its states before re-ranking
-        for (int j = tid; j < n1c; j += kPT) push_state(cord[j], j < cut1 ? 1 : 0);
-        __syncthreads();
-        const int n2c = rank_bin(b2);
-        const int j2 = cut_in(n2c, before2, thr2);
-        cut2 = j2 < n2c ? j2 + 1 : n2c;
-        for (int j = tid; j < n2c; j += kPT) push_state(cord[j], j < cut2 ? 2 : 1);
-        n2 = cbefore2 + cut2;
-      } else {
-        const int j2 = cut_in(cut1, before1, thr2);
-        cut2 = j2 < cut1 ? j2 + 1 : cut1;
-        for (int j = tid; j < n1c; j += kPT) push_state(cord[j], j < cut2 ? 2 : (j < cut1 ? 1 : 0));
-        n2 = cbefore1 + cut2;
+      // stage 1 (selection.py:57-58): crossing of p1 * total, then stage 2
+      // (engine.py:191-194): same order, crossing of p2 * (retained mass)
+      double thr = p1 * (double)total;
+      int limit = kBins;
+#pragma unroll 1
+      for (int stage = 0; stage < 2; ++stage) {
+        const bool inb1 = stage == 1 && !((double)before1 >= thr && cbefore1 > 0);
+        int b, n, cb;
+        unsigned long long base;
+        if (inb1) {  // stage-2 crossing inside bin b1's already-ranked prefix
+          b = b1;
+          n = cut1;
+          base = before1;
+          cb = cbefore1;
+        } else {
+          b = sel_find_bin(&s_sel, bm, bc, mbase, cbase, thr, limit);
+          if (stage == 0) stamp(r, 23);
+          base = s_sel.before;
+          cb = s_sel.cbefore;
+          if (stage == 1)  // bin b1's order is about to be overwritten: emit its states
+#pragma unroll 1
+            for (int j = tid; j < n1c; j += kPT) {
+              const int i = cord[j], rr = i / per;
+              remote(cluster, stl, rr)[g * L.per + (i - rr * per)] = (uint8_t)(j < cut1 ? 1 : 0);
+            }
+          n = sel_rank_bin(&s_sel, binI, lmall, clist, cord, K, b);
+        }
+        const int jj = sel_cut(&s_sel, um, cord, n, base, thr);
+        const int cut = jj < n ? jj + 1 : n;
+        if (stage == 0) {
+          b1 = b;
+          n1c = n;
+          cut1 = cut;
+          before1 = base;
+          cbefore1 = cb;
+          thr = p2 * (double)s_sel.at;  // retained mass (engine.py:191)
+          limit = b1;
+          stamp(r, 11);
+        } else {
+          b2 = b;
+          cut2 = cut;
+          n2 = cb + cut;
+          // boundary-bin members follow their exact rank
+#pragma unroll 1
+          for (int j = tid; j < (inb1 ? n1c : n); j += kPT) {
+            const int i = cord[j], rr = i / per;
+            const int sv = inb1 ? (j < cut2 ? 2 : (j < cut1 ? 1 : 0)) : (j < cut2 ? 2 : 1);
+            remote(cluster, stl, rr)[g * L.per + (i - rr * per)] = (uint8_t)sv;
+          }
+        }
       }
+      stamp(r, 13);
       // everything outside the boundary bins: bins < b2 exact, [b2, b1) approx, > b1 dropped
+#pragma unroll 1
       for (int i = tid; i < K; i += kPT) {
         const int b = binI[i];
-        if (b != b1 && b != b2) push_state(i, b < b2 ? 2 : (b < b1 ? 1 : 0));
+        if (b != b1 && b != b2) {
+          const int rr = i / per;
+          remote(cluster, stl, rr)[g * L.per + (i - rr * per)] = (uint8_t)(b < b2 ? 2 : (b < b1 ? 1 : 0));
+        }
       }
-      if (tid == 0) {
-        counts[2 * hq] = cbefore1 + cut1;
-        counts[2 * hq + 1] = n2;
-      }
-    } else if (tid == 0) {  // no clusters (engine.py:162 raises on the host side): empty plan
-      counts[2 * hq] = 0;
-      counts[2 * hq + 1] = 0;
+    }
+    if (tid == 0) {
+      counts[2 * hq] = K > 0 ? cbefore1 + cut1 : 0;
+      counts[2 * hq + 1] = K > 0 ? n2 : 0;
     }
     if (tid < CL) remote(cluster, s_Mg, tid)[g] = K > 0 ? M : 0.0;
   }
@@ -545,15 +597,14 @@ __global__ void __launch_bounds__(kPT, 1)
 
   // ---------------- P3: union counts + approx partial of my slice --------
   int e_rows = 0, e_cl = 0, a_cl = 0;
+#pragma unroll 1
   for (int i = tid; i < nloc; i += kPT) {
     int me = 0, ma = 0;
-#pragma unroll
-    for (int g = 0; g < kG; ++g) {
-      if (g < G) {
-        const uint8_t s = stl[g * L.per + i];
-        me |= (s == 2) << g;
-        ma |= (s == 1) << g;
-      }
+#pragma unroll 1
+    for (int g = 0; g < G; ++g) {
+      const uint8_t s = stl[g * L.per + i];
+      me |= (s == 2) << g;
+      ma |= (s == 1) << g;
     }
     if (me) {
       e_rows += offs[i + 1] - offs[i];
@@ -561,8 +612,7 @@ __global__ void __launch_bounds__(kPT, 1)
     }
     if (ma) {
       a_cl += 1;
-      const int slot = atomicAdd(&s_na, 1);
-      if (slot < kMaxPer) s_alist[slot] = i | (ma << 16);
+      s_alist[atomicAdd(&s_na, 1)] = i | (ma << 16);
     }
   }
   {  // (rows, exact clusters, approx clusters) of my slice -> every CTA
@@ -577,7 +627,7 @@ __global__ void __launch_bounds__(kPT, 1)
   stamp(r, 15);
   if (tid < CL) {
     int t0 = 0, t1 = 0, t2 = 0;
-#pragma unroll
+#pragma unroll 1
     for (int w = 0; w < kPW; ++w) {
       t0 += s_redi[w * 4 + 0];
       t1 += s_redi[w * 4 + 1];
@@ -589,59 +639,66 @@ __global__ void __launch_bounds__(kPT, 1)
     dst[2] = t2;
   }
   {
-    // warp w folds approx clusters w, w + 16, ...: all the Vbar rows it needs
-    // are loaded before any is used (one HBM round trip)
-    const int na = min(s_na, kMaxPer);
+    // approximated clusters (engine.py:231-246): their value means stream into
+    // the dead tile buffers by cp.async (all in flight at once), weights
+    // w = exp(lm - M_g) go to shared memory, then column-parallel sums
+    const int na = s_na;
     const float* vbar = v.value_means + ((size_t)bh * cap + k0) * d;
-    constexpr int kU = 4;
-    float4 acc[kG];
-    float lsum[kG];
-#pragma unroll
-    for (int g = 0; g < kG; ++g) {
-      acc[g] = make_float4(0.f, 0.f, 0.f, 0.f);
-      lsum[g] = 0.f;
-    }
-    for (int a0 = warp; a0 < na; a0 += kU * kPW) {
-      float4 vb[kU];
-      int ent[kU];
-#pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const int a = a0 + u * kPW;
-        ent[u] = a < na ? s_alist[a] : -1;
-        vb[u] = (ent[u] >= 0 && lane * 4 < d)
-                    ? __ldg(reinterpret_cast<const float4*>(vbar + (size_t)(ent[u] & 0xFFFF) * d) + lane)
-                    : make_float4(0.f, 0.f, 0.f, 0.f);
+    float* vb = Cs;                                   // [kApx][d] value means
+    float* ws = Cs + (size_t)kApx * d;                // [kApx][8] weights
+    float* red = ws + (size_t)kApx * 8;               // [groups][G][d + 4] partial sums
+    const int ncol = G * (d / 4);                     // float4 columns (head, 4 dims)
+    const int ngrp = kPT / ncol;                      // >= 2 (G * d <= 1024)
+    const int col = tid % ncol, grp = tid / ncol;
+    const int cg_ = col / (d / 4), c4 = col - cg_ * (d / 4);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    float lsum = 0.f;
+#pragma unroll 1
+    for (int a0 = 0; a0 < na; a0 += kApx) {
+      const int cnt = min(kApx, na - a0);
+      __syncthreads();  // previous chunk consumed
+#pragma unroll 1
+      for (int e = tid; e < cnt * (d / 4); e += kPT) {
+        const int a = e / (d / 4), cc = e - a * (d / 4);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(
+                         (unsigned)__cvta_generic_to_shared(vb + (size_t)a * d + cc * 4)),
+                     "l"(vbar + (size_t)(s_alist[a0 + a] & 0xFFFF) * d + cc * 4));
       }
-#pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        if (ent[u] < 0) continue;
-        const int i = ent[u] & 0xFFFF, ma = ent[u] >> 16;
-#pragma unroll
-        for (int g = 0; g < kG; ++g) {
-          if ((ma >> g) & 1) {
-            const float w = __expf((float)(lml[g * L.per + i] - s_Mg[g]));
-            lsum[g] += w;
-            acc[g].x += w * vb[u].x; acc[g].y += w * vb[u].y; acc[g].z += w * vb[u].z; acc[g].w += w * vb[u].w;
-          }
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+#pragma unroll 1
+      for (int e = tid; e < cnt * 8; e += kPT) {
+        const int a = e >> 3, g = e & 7;
+        const int ent = s_alist[a0 + a], i = ent & 0xFFFF;
+        ws[e] = (g < G && ((ent >> (16 + g)) & 1)) ? __expf((float)(lml[g * L.per + i] - s_Mg[g])) : 0.f;
+      }
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      __syncthreads();
+      if (grp < ngrp) {
+#pragma unroll 1
+        for (int a = grp; a < cnt; a += ngrp) {
+          const float w = ws[a * 8 + cg_];
+          const float4 x = *reinterpret_cast<const float4*>(vb + (size_t)a * d + c4 * 4);
+          acc.x += w * x.x; acc.y += w * x.y; acc.z += w * x.z; acc.w += w * x.w;
+          lsum += w;
         }
       }
     }
-    float* red = Cs;  // [warps][kG][d + 4] (the centroid slice is dead)
-#pragma unroll
-    for (int g = 0; g < kG; ++g) {
-      float* rw = red + ((size_t)warp * kG + g) * (d + 4);
-      if (lane * 4 < d) reinterpret_cast<float4*>(rw + 4)[lane] = acc[g];
-      if (lane == 0) rw[0] = lsum[g];
+    __syncthreads();
+    if (grp < ngrp) {
+      float* rw = red + ((size_t)grp * G + cg_) * (d + 4);
+      *reinterpret_cast<float4*>(rw + 4 + c4 * 4) = acc;
+      if (c4 == 0) rw[0] = lsum;
     }
     __syncthreads();
-    // sum over warps; push my slice's (l, o) for head g into owner g's slot r
+    // sum over groups; push my slice's (l, o) for head g into owner g's slot r
+#pragma unroll 1
     for (int i = tid; i < G * (d + 4); i += kPT) {
       const int g = i / (d + 4), c = i - g * (d + 4);
       if (c == 1 || c == 2 || c == 3) continue;
-      float s = 0.f;
-#pragma unroll
-      for (int w = 0; w < kPW; ++w) s += red[((size_t)w * kG + g) * (d + 4) + c];
-      remote(cluster, aps, g)[r * (d + 4) + c] = s;
+      float sm = 0.f;
+#pragma unroll 1
+      for (int q2 = 0; q2 < ngrp; ++q2) sm += red[((size_t)q2 * G + g) * (d + 4) + c];
+      remote(cluster, aps, g)[r * (d + 4) + c] = sm;
     }
   }
   stamp(r, 7);
@@ -651,7 +708,7 @@ __global__ void __launch_bounds__(kPT, 1)
   // ---------------- P4: work lists -----------------------------------------
   const int sw_rows = v.sink + v.window;
   int row_base = sw_rows, apx_base = 0, tot_r = 0, tot_e = 0, tot_a = 0;
-#pragma unroll
+#pragma unroll 1
   for (int rr = 0; rr < CL; ++rr) {
     if (rr < r) {
       row_base += s_cnt[rr][0];
@@ -664,27 +721,30 @@ __global__ void __launch_bounds__(kPT, 1)
   if (r < G) {  // owner: the head's approx partial = sum of the CL slice partials
     const int g = r;
     float* ap = wl.apart + ((size_t)bh * G + g) * (4 + d);
+#pragma unroll 1
     for (int c = tid; c < d + 4; c += kPT) {
       if (c == 1 || c == 2 || c == 3) continue;
-      float s = 0.f;
-#pragma unroll
-      for (int rr = 0; rr < CL; ++rr) s += aps[rr * (d + 4) + c];
+      float sm = 0.f;
+#pragma unroll 1
+      for (int rr = 0; rr < CL; ++rr) sm += aps[rr * (d + 4) + c];
       if (c == 0) {
-        ap[0] = s > 0.f ? (float)s_Mg[g] : -INFINITY;  // natural-log domain, like the attention partials
-        ap[1] = s;
+        ap[0] = sm > 0.f ? (float)s_Mg[g] : -INFINITY;  // natural-log domain, like the attention partials
+        ap[1] = sm;
       } else {
-        ap[c] = s;
+        ap[c] = sm;
       }
     }
   }
   stamp(r, 16);
   // debug / parity outputs of my slice (kept off the barrier-release paths above)
   if (lm_out)
+#pragma unroll 1
     for (int i = tid; i < G * nloc; i += kPT) {
       const int g = i / nloc, k = i - g * nloc;
       lm_out[((size_t)bh * G + g) * cap + k0 + k] = lml[g * L.per + k];
     }
   if (state_out)
+#pragma unroll 1
     for (int i = tid; i < G * nloc; i += kPT) {
       const int g = i / nloc, k = i - g * nloc;
       state_out[((size_t)bh * G + g) * cap + k0 + k] = stl[g * L.per + k];
@@ -692,17 +752,16 @@ __global__ void __launch_bounds__(kPT, 1)
   stamp(r, 17);
   unsigned* rowidx = reinterpret_cast<unsigned*>(wl.rowidx) + (size_t)bh * v.row_cap;
   int2* apx = wl.approx + (size_t)bh * cap;
+#pragma unroll 1
   for (int i0 = 0; i0 < nloc; i0 += kPT) {
     const int i = i0 + tid;
     int me = 0, ma = 0, len = 0, st0 = 0;
     if (i < nloc) {
-#pragma unroll
-      for (int g = 0; g < kG; ++g) {
-        if (g < G) {
-          const uint8_t s = stl[g * L.per + i];
-          me |= (s == 2) << g;
-          ma |= (s == 1) << g;
-        }
+#pragma unroll 1
+      for (int g = 0; g < G; ++g) {
+        const uint8_t s = stl[g * L.per + i];
+        me |= (s == 2) << g;
+        ma |= (s == 1) << g;
       }
       st0 = offs[i];
       len = me ? offs[i + 1] - st0 : 0;
@@ -715,6 +774,7 @@ __global__ void __launch_bounds__(kPT, 1)
     if (ma) apx[ao + apx_base] = make_int2(k0 + i, ma);
     // warp-cooperative expansion of the warp's 32 clusters: lanes write consecutive rows
     unsigned todo = __ballot_sync(0xffffffffu, len > 0);
+#pragma unroll 1
     while (todo) {
       const int t = __ffs(todo) - 1;
       todo &= todo - 1;
@@ -722,6 +782,7 @@ __global__ void __launch_bounds__(kPT, 1)
       const int to = __shfl_sync(0xffffffffu, ro, t);
       const unsigned tag = (unsigned)__shfl_sync(0xffffffffu, me, t) << 24;
       const int ts = __shfl_sync(0xffffffffu, st0, t);
+#pragma unroll 1
       for (int x = lane; x < tl; x += 32) rowidx[to + x] = tag | (unsigned)(ts + x);
     }
     row_base += (int)trr64;
@@ -731,8 +792,9 @@ __global__ void __launch_bounds__(kPT, 1)
   }
   if (r == 0) {
     const unsigned tag = (unsigned)((1 << G) - 1) << 24;
-    for (int t = tid; t < v.sink; t += kPT) rowidx[t] = tag | (unsigned)t;
-    for (int t = tid; t < v.window; t += kPT) rowidx[v.sink + t] = tag | (unsigned)(v.n_tokens - v.window + t);
+#pragma unroll 1
+    for (int t = tid; t < sw_rows; t += kPT)
+      rowidx[t] = tag | (unsigned)(t < v.sink ? t : v.n_tokens - v.window + (t - v.sink));
     if (tid == 0) {
       const int all_r = tot_r + sw_rows;
       wl.nrows[bh] = all_r;
@@ -748,7 +810,6 @@ __global__ void __launch_bounds__(kPT, 1)
     }
   }
   stamp(r, 9);
-  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 }
 
 int g_plan_cl = 0;  // 0: auto; 8 / 16 forces the cluster size (dp_debug_set(1, .))
@@ -851,6 +912,9 @@ cudaError_t launch_plan(const dp_cache_view& v, const void* q, int qdt, int G, d
 
 }  // namespace dp
 
+extern "C" int dp_debug_plan_clock(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, dp::g_plan_clk, sizeof(dp::g_plan_clk)) == cudaSuccess ? 0 : 2;  // [16][2]
+}
 extern "C" int dp_debug_plan_timing(unsigned long long* out) {
   return cudaMemcpyFromSymbol(out, dp::g_plan_ts, sizeof(dp::g_plan_ts)) == cudaSuccess ? 0 : 2;  // [16][24]
 }

@@ -33,34 +33,18 @@ for it in range(3):
 torch.cuda.synchronize()
 buf = (ctypes.c_ulonglong * 384)()
 lib.dp_debug_plan_timing(ctypes.cast(buf, ctypes.c_void_p))
-t = np.array(buf[:], dtype=np.float64).reshape(16, 24)[:, [0, 1, 2, 14, 10, 3, 4, 11, 13, 5, 6, 15, 7, 8, 16, 17, 18, 19, 9]]
+t = np.array(buf[:], dtype=np.float64).reshape(16, 24)[:, [0, 1, 2, 10, 3, 4, 20, 21, 22, 23, 11, 13, 5, 6, 15, 7, 8, 9]]
 nr = 16 if t[8:, 0].min() > 0 else 8
 t = t[:nr]
 t0 = t[:, 0].min()
-names = ["start", "loads", "qreg", "mma0", "score", "P1", "A", "b1", "cut1", "P2", "B", "cnts", "P3", "C", "aps", "dbg", "scan", "expand", "P4"]
+names = ["start", "loads", "S", "score", "P1", "A", "zero", "hist", "scan", "find", "stage1", "stage2", "P2", "B", "cnts", "P3", "C", "P4"]
 print("rank " + " ".join(f"{x:>6s}" for x in names))
 for r in range(nr):
     print(f"{r:4d} " + " ".join(f"{(x - t0) / 1e3:6.2f}" if x > 0 else "     -" for x in t[r]))
+cbuf = (ctypes.c_ulonglong * 32)()
+lib.dp_debug_plan_clock(ctypes.cast(cbuf, ctypes.c_void_p))
+cl = np.array(cbuf[:], dtype=np.float64).reshape(16, 2)
+tt = np.array(buf[:], dtype=np.float64).reshape(16, 24)
+print("SM clock inside the kernel (MHz):", [round((cl[r, 1] - cl[r, 0]) / (tt[r, 9] - tt[r, 0]) * 1e3) for r in range(nr)])
 print("counts", ws.counts[0, :G].tolist(), "stats", ws.stats[0, 0].tolist())
 
-# attention phases (sparse launch after the plan)
-N.check(lib.dp_attend(view, N.ptr(q), 1, G, 1 / math.sqrt(128), N.ptr(ws.log_mass), N.ptr(ws.out), N.ptr(ws.lse),
-                      N.ptr(ws.ws), ws.ws.numel(), torch.cuda.current_stream().cuda_stream))
-torch.cuda.synchronize()
-for it in range(2):
-    N.check(lib.dp_plan(view, N.ptr(q), 1, G, 1 / math.sqrt(128), 0.95, 0.7, N.ptr(ws.log_mass), None,
-                        N.ptr(ws.counts), N.ptr(ws.stats), N.ptr(ws.ws), ws.ws.numel(),
-                        torch.cuda.current_stream().cuda_stream))
-    N.check(lib.dp_attend(view, N.ptr(q), 1, G, 1 / math.sqrt(128), N.ptr(ws.log_mass), N.ptr(ws.out),
-                          N.ptr(ws.lse), N.ptr(ws.ws), ws.ws.numel(), torch.cuda.current_stream().cuda_stream))
-warm(0.3)
-torch.cuda.synchronize()
-abuf = (ctypes.c_ulonglong * (512 * 8))()
-lib.dp_debug_attn_timing(ctypes.cast(abuf, ctypes.c_void_p))
-a = np.array(abuf[:], dtype=np.float64).reshape(512, 8)[:148]
-a0 = a[:, 0].min()
-rel = (a - a0) / 1e3
-print("attn phases (us, rel. to first CTA start): start, prefix, first data, loop done, flushed, exit")
-for name, col in (("start", 0), ("prefix", 1), ("data0", 2), ("loop", 3), ("flush", 4), ("exit", 5)):
-    x = rel[:, col]
-    print(f"  {name:7s} min {x.min():7.2f} med {np.median(x):7.2f} max {x.max():7.2f}")

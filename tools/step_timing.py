@@ -94,6 +94,10 @@ print(f"  plan (layers cycled)  {timed(lambda: [plan(j) for j in range(L)]):8.2f
 print(f"  attend (cycled)       {timed(lambda: [attend(j) for j in range(L)]):8.2f}")
 print(f"  plan+attend (cycled)  {timed(lambda: [(plan(j), attend(j)) for j in range(L)]):8.2f}")
 print(f"  dense (cycled)        {timed(lambda: [dense(j) for j in range(L)]):8.2f}")
+lib.dp_debug_set(0, 1)
+print(f"  attend stream-only    {timed(lambda: [attend(j) for j in range(L)]):8.2f}")
+print(f"  dense stream-only     {timed(lambda: [dense(j) for j in range(L)]):8.2f}")
+lib.dp_debug_set(0, 0)
 st = wss[0].stats[0].cpu().tolist()
 print("  stats (rows, approx, chunks, exact clusters) of layer 0:", st)
 
@@ -102,14 +106,20 @@ import ctypes  # noqa: E402
 import numpy as np  # noqa: E402
 
 timed(lambda: [(plan(j), attend(j)) for j in range(L)], reps=1)
-abuf = (ctypes.c_ulonglong * (512 * 8))()
+abuf = (ctypes.c_ulonglong * (512 * 12))()
 lib.dp_debug_attn_timing(ctypes.cast(abuf, ctypes.c_void_p))
-a = np.array(abuf[:], dtype=np.float64).reshape(512, 8)[:148]
+a = np.array(abuf[:], dtype=np.float64).reshape(512, 12)[:148]
+nmg = a[:, 9].copy(); npt = a[:, 10].copy(); rtt = a[:, 11].copy(); a = a[:, :9]
 a0 = a[:, 0].min()
 rel = (a - a0) / 1e3
 print("attn phases of the last step (us, rel. to first CTA start): start, prefix, first data, loop done, flushed, exit")
-for name, col in (("start", 0), ("prefix", 1), ("data0", 2), ("loop", 3), ("flush", 4), ("merge0", 6), ("exit", 5)):
+for name, col in (("start", 0), ("prefix", 1), ("data0", 2), ("loop", 3), ("flush", 4), ("merge0", 6),
+                  ("mload", 7), ("mdone", 8), ("exit", 5)):
     x = rel[:, col]
     x = x[(x > -1e6) & (x < 1e6)]
     if x.size:
         print(f"  {name:7s} min {x.min():7.2f} med {np.median(x):7.2f} max {x.max():7.2f}  (n={x.size})")
+mer = np.where((rel[:, 6] > 0) & (rel[:, 6] < 1e3))[0]
+for c in mer:
+    print(f"  merging CTA {c}: nm={int(nmg[c])} nparts={int(npt[c])} loop {rel[c,3]:.2f} flush {rel[c,4]:.2f} "
+          f"merge0 {rel[c,6]:.2f} loads {rel[c,7]:.2f} done {rel[c,8]:.2f} exit {rel[c,5]:.2f} rtt {rtt[c]/1e3:.2f}")
