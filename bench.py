@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--cpu-sample-heads", type=int, default=2)
+    ap.add_argument("--long-context", type=int, default=131072,
+                    help="secondary workload context (0: off); reported under long_context")
+    ap.add_argument("--long-layers", type=int, default=4)
     return ap.parse_args()
 
 
@@ -243,32 +246,29 @@ def run_reference(a):
 # ---------------------------------------------------------------------------
 # the B200 arm
 # ---------------------------------------------------------------------------
-def run_b200(a):
+def _measure(a, context, L, dev, world, rank, sampler=None):
+    """Build L synthetic layers at `context` (GPU k-means prefill, not timed)
+    and time CUDA graphs of the full sparse decode step (plan + attend per
+    layer) and of the dense comparator over the same caches."""
     import torch
 
-    world, rank, local = dist_setup()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
     from paper_2602_05191_b200 import _native as N
-    from paper_2602_05191_b200 import cluster_layer, DecodeWorkspace, sparse_attention
-    from paper_2602_05191_b200.cache import dtype_code
+    from paper_2602_05191_b200 import cluster_layer, DecodeWorkspace, ClusteredLayer
+    from paper_2602_05191_b200.cache import dtype_code, head_seed
     from paper_2602_05191_b200.workload import generate_layer, generate_queries
 
-    if a.kv_heads % world:
-        raise SystemExit(f"kv heads {a.kv_heads} not divisible by {world} ranks")
     hl = a.kv_heads // world
     h0 = rank * hl
-    G, d, L, B = a.gqa, a.head_dim, a.layers, a.batch
+    G, d, B = a.gqa, a.head_dim, a.batch
     lib = N.lib()
-    st = torch.cuda.current_stream(dev)
 
     # ---- prefill: synthetic caches + GPU k-means (not timed) -------------
     t0 = time.perf_counter()
     qdev = []
-    ks = torch.empty((L * B, hl, a.context, d), dtype=torch.bfloat16, device=dev)
+    ks = torch.empty((L * B, hl, context, d), dtype=torch.bfloat16, device=dev)
     vs = torch.empty_like(ks)
     for li in range(L):
-        k, v, centers = generate_layer(B, a.kv_heads, a.context, d, layer=li, device=dev)
+        k, v, centers = generate_layer(B, a.kv_heads, context, d, layer=li, device=dev)
         ks[li * B:(li + 1) * B] = k[:, h0:h0 + hl]
         vs[li * B:(li + 1) * B] = v[:, h0:h0 + hl]
         del k, v
@@ -278,8 +278,6 @@ def run_b200(a):
     gen_s = time.perf_counter() - t0
     # every (layer, sequence, kv head) of the model clustered in ONE batched
     # GPU k-means (seeds as build_clustered_cache: SeedSequence([0, layer, head]))
-    from paper_2602_05191_b200.cache import head_seed
-
     seeds = [[head_seed(0, li, h0 + h, b) for h in range(hl)] for li in range(L) for b in range(B)]
     big = cluster_layer(ks, vs, fp64_assign=bool(a.fp64_assign), head_seeds=seeds)
     del ks, vs
@@ -292,8 +290,6 @@ def run_b200(a):
             layers.append(per_seq[li])
         else:  # re-slice [L*B] -> per layer [B]
             sl = lambda t: t[li * B:(li + 1) * B]  # noqa: E731
-            from paper_2602_05191_b200 import ClusteredLayer
-
             lay = ClusteredLayer(sl(big.keys), sl(big.values), sl(big.offs), sl(big.nclusters),
                                  sl(big.centroids), sl(big.value_means), sl(big.perm), big.n_tokens,
                                  big.sink, big.window)
@@ -305,7 +301,7 @@ def run_b200(a):
     scale = 1.0 / math.sqrt(d)
 
     def layer_step(li, s, stats=None, ev=None):
-        lay, ws, v = layers[li], wss[li], views[li]
+        ws, v = wss[li], views[li]
         q = qdev[li][s % a.qsteps]
         cs = torch.cuda.current_stream(dev).cuda_stream
         if ev is not None:
@@ -321,16 +317,21 @@ def run_b200(a):
         if ev is not None:
             ev[2].record()
 
-    def dense_step(li, s):
-        lay, ws, v = layers[li], wss[li], views[li]
+    def dense_step(li, s, ev=None):
+        ws, v = wss[li], views[li]
         q = qdev[li][s % a.qsteps]
+        if ev is not None:
+            ev[0].record()
         N.check(lib.dp_dense_attention(v, N.ptr(q), dtype_code(q), G, scale, N.ptr(ws.out), N.ptr(ws.lse),
                                        N.ptr(ws.ws), ws.ws.numel(), torch.cuda.current_stream(dev).cuda_stream))
+        if ev is not None:
+            ev[1].record()
 
     # ---- stage timing + algorithmic bytes (eager, CUDA events) -----------
     nstage = min(a.qsteps, 4)
     stats_all = torch.zeros((nstage, L, B, hl, 4), dtype=torch.int32, device=dev)
     evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(L)] for _ in range(nstage)]
+    devs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(L)]
     for s in range(nstage):  # warm
         for li in range(L):
             layer_step(li, s, stats_all[s, li])
@@ -341,6 +342,8 @@ def run_b200(a):
     for s in range(nstage):
         for li in range(L):
             layer_step(li, s, stats_all[s, li], evs[s][li])
+    for li in range(L):
+        dense_step(li, 0, devs[li])
     torch.cuda.synchronize(dev)
     stage_ms = np.zeros(2)
     for s in range(nstage):
@@ -349,6 +352,7 @@ def run_b200(a):
             for j in range(2):
                 stage_ms[j] += e[j].elapsed_time(e[j + 1])
     stage_ms /= nstage * L  # per layer
+    dense_kernel_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in devs]))
     stats_np = stats_all.cpu().numpy().astype(np.int64)  # [S,L,B,hl,4]
     ncl = np.stack([lay.nclusters.cpu().numpy() for lay in layers]).astype(np.int64)  # [L,B,hl]
     s_kv, s_q, s_o = 2, 2, 4
@@ -359,10 +363,7 @@ def run_b200(a):
     attend_bytes = (U * 2 * d * s_kv + A * d * 4).sum(axis=(2, 3)).mean(axis=0) + qo  # per layer [L]
     score_bytes = (ncl * d * 4 + ncl * 4).sum(axis=(1, 2))  # [L]
     step_bytes = float((attend_bytes + score_bytes).sum())  # all layers, one step
-    dense_bytes = float(L * (B * hl * a.context * 2 * d * s_kv + qo))
-    attend_ms = stage_ms[1]
-    attend_gbs = float(attend_bytes.mean() / (attend_ms * 1e-3) / 1e9)
-    union_frac = float(U.mean() / a.context)
+    dense_bytes = float(L * (B * hl * context * 2 * d * s_kv + qo))
 
     # ---- CUDA graphs of the full step (one per distinct query step) -------
     def capture(fn):
@@ -383,15 +384,13 @@ def run_b200(a):
             graphs.append(g)
         return graphs
 
-    graphs = capture(layer_step)
-
-    def timed(graph_list, steps, warmup, sampler=None):
+    def timed(graph_list, steps, warmup, smp=None):
         for s in range(warmup):
             graph_list[s % len(graph_list)].replay()
         torch.cuda.synchronize(dev)
         barrier(world)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ctx = sampler if sampler is not None else _Null()
+        ctx = smp if smp is not None else _Null()
         with ctx:
             e0.record()
             for s in range(steps):
@@ -401,16 +400,41 @@ def run_b200(a):
         barrier(world)
         return e0.elapsed_time(e1) / steps
 
-    sampler = ClockSampler(local)
-    ms = timed(graphs, a.steps, a.warmup, sampler)
-    ms = max_over_ranks(ms, world, dev)
-    clocks = sampler.summary()
-
+    graphs = capture(layer_step)
+    ms = max_over_ranks(timed(graphs, a.steps, a.warmup, sampler), world, dev)
+    del graphs
     dense_ms = None
     if not a.no_dense:
         dgraphs = capture(dense_step)
         dense_ms = max_over_ranks(timed(dgraphs, a.steps, a.warmup), world, dev)
         del dgraphs
+    return dict(layers=layers, wss=wss, qdev=qdev, ms=ms, dense_ms=dense_ms, stage_ms=stage_ms,
+                dense_kernel_ms=dense_kernel_ms, attend_bytes=attend_bytes, step_bytes=step_bytes,
+                dense_bytes=dense_bytes, union_frac=float(U.mean() / context), prefill_s=prefill_s, gen_s=gen_s,
+                hl=hl, Hq_l=Hq_l)
+
+
+def run_b200(a):
+    import torch
+
+    world, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    from paper_2602_05191_b200 import sparse_attention
+
+    if a.kv_heads % world:
+        raise SystemExit(f"kv heads {a.kv_heads} not divisible by {world} ranks")
+    G, d, L, B = a.gqa, a.head_dim, a.layers, a.batch
+    sampler = ClockSampler(local)
+    res = _measure(a, a.context, L, dev, world, rank, sampler)
+    clocks = sampler.summary()
+    layers, wss, qdev, ms, dense_ms = res["layers"], res["wss"], res["qdev"], res["ms"], res["dense_ms"]
+    hl, Hq_l = res["hl"], res["Hq_l"]
+    stage_ms, attend_bytes = res["stage_ms"], res["attend_bytes"]
+    step_bytes, dense_bytes, union_frac = res["step_bytes"], res["dense_bytes"], res["union_frac"]
+    prefill_s, gen_s = res["prefill_s"], res["gen_s"]
+    attend_ms = stage_ms[1]
+    attend_gbs = float(attend_bytes.mean() / (attend_ms * 1e-3) / 1e9)
 
     # ---- e2e through the public API with host buffers ---------------------
     e2e = None
@@ -460,6 +484,26 @@ def run_b200(a):
                          f"extrapolated x{a.kv_heads * G * L * B} (all q heads, layers, batch); NumPy/"
                          f"OpenBLAS threads = cores"}
 
+    # ---- secondary workload: the same step at 128K context (fewer layers) --
+    long_ctx = None
+    if a.long_context and a.long_context != a.context:
+        del layers, wss, qdev, res
+        torch.cuda.empty_cache()
+        r2 = _measure(a, a.long_context, a.long_layers, dev, world, rank)
+        a_ms = r2["stage_ms"][1]
+        long_ctx = {
+            "context": a.long_context, "layers_timed": a.long_layers,
+            "us_per_layer": r2["ms"] * 1e3 / a.long_layers,
+            "us_per_step_32_layers": r2["ms"] * 1e3 / a.long_layers * 32,
+            "dense_us_per_layer": None if r2["dense_ms"] is None else r2["dense_ms"] * 1e3 / a.long_layers,
+            "speedup_vs_dense": None if r2["dense_ms"] is None else r2["dense_ms"] / r2["ms"],
+            "stage_us_per_layer": {"plan": r2["stage_ms"][0] * 1e3, "attend": a_ms * 1e3},
+            "attend_algorithmic_bytes": float(r2["attend_bytes"].mean()),
+            "attend_gbs": float(r2["attend_bytes"].mean() / (a_ms * 1e-3) / 1e9),
+            "dense_kernel_gbs": r2["dense_bytes"] / a.long_layers / (r2["dense_kernel_ms"] * 1e-3) / 1e9,
+            "union_exact_rows_frac": r2["union_frac"],
+        }
+
     peaks = {}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -493,7 +537,11 @@ def run_b200(a):
             "dense_roofline_frac": None if dense_ms is None else dense_bytes / (dense_ms * 1e-3) / 1e9 / hbm_peak,
             "speedup_vs_dense": None if dense_ms is None else dense_ms / ms,
             "prefill_s": prefill_s, "generate_s": gen_s,
+            "long_context": long_ctx,
         }
+        if long_ctx is not None:
+            long_ctx["attend_roofline_frac"] = long_ctx["attend_gbs"] / hbm_peak
+            long_ctx["dense_kernel_roofline_frac"] = long_ctx["dense_kernel_gbs"] / hbm_peak
         print(json.dumps(line), flush=True)
 
 

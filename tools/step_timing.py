@@ -114,12 +114,12 @@ a0 = a[:, 0].min()
 rel = (a - a0) / 1e3
 print("attn phases of the last step (us, rel. to first CTA start): start, prefix, first data, loop done, flushed, exit")
 for name, col in (("start", 0), ("prefix", 1), ("data0", 2), ("loop", 3), ("flush", 4), ("merge0", 6),
-                  ("mload", 7), ("mdone", 8), ("exit", 5)):
+                  ("exit", 5)):
     x = rel[:, col]
     x = x[(x > -1e6) & (x < 1e6)]
     if x.size:
         print(f"  {name:7s} min {x.min():7.2f} med {np.median(x):7.2f} max {x.max():7.2f}  (n={x.size})")
 mer = np.where((rel[:, 6] > 0) & (rel[:, 6] < 1e3))[0]
 for c in mer:
-    print(f"  merging CTA {c}: nm={int(nmg[c])} nparts={int(npt[c])} loop {rel[c,3]:.2f} flush {rel[c,4]:.2f} "
-          f"merge0 {rel[c,6]:.2f} loads {rel[c,7]:.2f} done {rel[c,8]:.2f} exit {rel[c,5]:.2f} rtt {rtt[c]/1e3:.2f}")
+    print(f"  merging CTA {c}: loop {rel[c,3]:.2f} flush {rel[c,4]:.2f} "
+          f"merge0 {rel[c,6]:.2f} exit {rel[c,5]:.2f}")
