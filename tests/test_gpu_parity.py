@@ -320,3 +320,61 @@ def test_growth_parity():
         np.testing.assert_array_equal(plan.stage1.selected, o_plan.stage1.selected)
         np.testing.assert_array_equal(plan.exact_tokens, o_plan.exact_tokens)
         assert O.output_error(out.output, o_out.output) <= 1e-5
+
+
+@pytest.mark.parametrize("cl", [8, 16])
+def test_plan_cluster_sizes_and_multi_tile(cl):
+    """The fused plan at both cluster sizes, with slices longer than one
+    128-row centroid tile (n = 40K -> ~1250 clusters)."""
+    from paper_2602_05191_b200 import _native as N
+
+    N.lib().dp_debug_set(1, cl)
+    try:
+        spec, keys, values, queries = _workload(40000, 128, 1, 4, "peaked", 11)
+        layer, kd, vd = _layer(keys, values, torch.bfloat16, fp64_assign=False)
+        for p1, p2 in [(0.95, 0.7), (0.99, 0.8)]:
+            _check_decode(layer, kd, vd, queries[0, 0], 4, p1, p2, torch.bfloat16)
+    finally:
+        N.lib().dp_debug_set(1, 0)
+
+
+def test_full_size_exact_collapse_matches_dense():
+    """Size-independent property at the bench shape (32K, 8 kv heads, G=4):
+    with p1 = p2 = 1 every cluster is exact, so the sparse step must equal the
+    dense kernel (engine.py:128-136 exactness collapse)."""
+    from paper_2602_05191_b200 import cluster_layer, dense_attention, sparse_attention
+    from paper_2602_05191_b200.workload import generate_layer, generate_queries
+
+    k, v, c = generate_layer(1, 8, 32768, 128)
+    layer = cluster_layer(k, v, fp64_assign=False)
+    q = torch.from_numpy(generate_queries(c, 4, 1)[0]).cuda().to(torch.bfloat16)
+    sp = sparse_attention(q, layer, 1.0, 1.0).clone()
+    de = dense_attention(q, layer).clone()
+    err = ((sp - de).norm(dim=-1) / de.norm(dim=-1)).max().item()
+    assert err <= 2e-3, err
+    # and at the default thresholds the kept mass is large: the output stays close to dense
+    sp95 = sparse_attention(q, layer, 0.95, 0.7).clone()
+    assert torch.isfinite(sp95).all()
+
+
+def test_sequence_sharded_merge_on_gpu():
+    """Config-5 exchange math on one GPU: two sequence shards, dense attention
+    per shard (kernel lse), LSE merge == dense attention over all tokens."""
+    from paper_2602_05191_b200 import cluster_layer, dense_attention
+    from paper_2602_05191_b200.sharding import lse_merge
+
+    spec, keys, values, queries = _workload(4096, 128, 2, 4, "peaked", 7)
+    kd = _to_dev(keys[0], torch.bfloat16).unsqueeze(0)
+    vd = _to_dev(values[0], torch.bfloat16).unsqueeze(0)
+    q = _to_dev(queries[0, 0], torch.bfloat16).unsqueeze(0)
+    full = cluster_layer(kd, vd, fp64_assign=False)
+    ref = dense_attention(q, full).clone()
+    half = 2048
+    a = cluster_layer(kd[:, :, :half].contiguous(), vd[:, :, :half].contiguous(), fp64_assign=False, window=0)
+    b = cluster_layer(kd[:, :, half:].contiguous(), vd[:, :, half:].contiguous(), fp64_assign=False, sink=0)
+    oa, la = dense_attention(q, a, return_lse=True)
+    oa, la = oa.clone(), la.clone()
+    ob, lb = dense_attention(q, b, return_lse=True)
+    out, _ = lse_merge(torch.stack([oa, ob.clone()]), torch.stack([la, lb.clone()]))
+    err = ((out - ref).norm(dim=-1) / ref.norm(dim=-1)).max().item()
+    assert err <= 1e-4, err
