@@ -176,7 +176,8 @@ struct TileWalk {
 
 template <bool kDense, bool kQF32>
 __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v, const void* __restrict__ q, int G,
-                                                               float scale_log2, WorkLists wl, Partials<float> pt,
+                                                               float scale_log2, const double* __restrict__ lm,
+                                                               WorkLists wl, Partials<float> pt,
                                                                float* __restrict__ out, float* __restrict__ lse,
                                                                int dbg) {
   constexpr int d = 128;
@@ -402,6 +403,75 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
         for (int e = 0; e < 4; ++e) o[mb][e] = 0.f;
       m_run[0] = m_run[1] = -INFINITY;
       l_run[0] = l_run[1] = 0.f;
+      // approximated clusters of this head (engine.py:231-246): pseudo-rows
+      // with logit = log-mass, value = value mean.  The head's CTAs split the
+      // plan's approx list evenly and start their online softmax from their
+      // share -- this runs while the segment's first tile is in flight, and
+      // the merge needs no separate approx partial.
+      if (!kDense) {
+        const int na = __ldcg(&wl.napprox[bh]);
+        const int part = me - first_owner(bh), np = head_parts(bh);
+        const int j0 = (int)((long long)na * part / np), j1 = (int)((long long)na * (part + 1) / np);
+        // warp w: entries [a0, a1) of the CTA's share; batches of 4 whose
+        // loads (one 128-bit value-mean slice per lane per entry, one
+        // log-mass per (entry, head) lane) are all in flight together
+        const int a0 = j0 + (j1 - j0) * warp / kWarps, a1 = j0 + (j1 - j0) * (warp + 1) / kWarps;
+        const int2* apx = wl.approx + (size_t)bh * v.cluster_cap;
+        const float* vbar = v.value_means + (size_t)bh * v.cluster_cap * d;
+#pragma unroll 1
+        for (int b0 = a0; b0 < a1; b0 += 4) {
+          const int nb = min(4, a1 - b0);
+          const int2 el = lane < nb ? __ldcg(&apx[b0 + lane]) : make_int2(0, 0);
+          int ex[4], ey[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            ex[u] = __shfl_sync(0xffffffffu, el.x, u);
+            ey[u] = __shfl_sync(0xffffffffu, el.y, u);
+          }
+          float4 vrow[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            vrow[u] = u < nb ? __ldg(reinterpret_cast<const float4*>(vbar + (size_t)ex[u] * d) + lane)
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+          const int lu = lane >> 3, lh = lane & 7;  // this lane fetches entry lu's head-lh log-mass
+          const int eyu = __shfl_sync(0xffffffffu, el.y, lu), exu = __shfl_sync(0xffffffffu, el.x, lu);
+          const float xl = (lu < nb && lh < G && ((eyu >> lh) & 1))
+                               ? (float)(__ldcg(lm + ((size_t)bh * G + lh) * v.cluster_cap + exu) * 1.4426950408889634)
+                               : -INFINITY;
+#pragma unroll 1
+          for (int u = 0; u < nb; ++u) {
+            float x[2];
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) x[hh] = __shfl_sync(0xffffffffu, xl, u * 8 + 2 * tq + hh);
+            // value mean row -> fragment layout through the warp's P buffer
+            float4 vr = vrow[0];
+            if (u == 1) vr = vrow[1];
+            if (u == 2) vr = vrow[2];
+            if (u == 3) vr = vrow[3];
+            __syncwarp();
+            reinterpret_cast<float4*>(Pw)[lane] = vr;
+            __syncwarp();
+            float pa[2], al[2];
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              const float mn = fmaxf(m_run[hh], x[hh]);
+              al[hh] = mn == -INFINITY ? 1.f : exp2f(m_run[hh] - mn);
+              pa[hh] = x[hh] == -INFINITY ? 0.f : exp2f(x[hh] - mn);
+              m_run[hh] = mn;
+              l_run[hh] = l_run[hh] * al[hh] + (g8 == 0 ? pa[hh] : 0.f);  // one lane per head counts it
+            }
+#pragma unroll
+            for (int mb = 0; mb < 8; ++mb) {
+              const float v0 = Pw[mb * 16 + g8], v1 = Pw[mb * 16 + g8 + 8];
+              o[mb][0] = o[mb][0] * al[0] + pa[0] * v0;
+              o[mb][1] = o[mb][1] * al[1] + pa[1] * v0;
+              o[mb][2] = o[mb][2] * al[0] + pa[0] * v1;
+              o[mb][3] = o[mb][3] * al[1] + pa[1] * v1;
+            }
+          }
+        }
+        __syncwarp();
+      }
     }
     mbar_wait(smem_u32(&full_bar[s]), (unsigned)((idx / kStages) & 1));  // stage s landed
     if (idx == 0) astamp(2);
@@ -537,17 +607,34 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tb) : "f"(probe));
       g_attn_ts[blockIdx.x][11] = (tb - ta) + (probe == 12345.f);
     }
-    // warp w merges head g = w % G over partials p = first + w / G, + 8/G, ...
-    // (p == -1 is the plan's approx partial); each round issues kU loads
-    // before using any
-    const int first = kDense ? 0 : -1;
+    // warp w merges head g = w % G over partials p = w / G, + 8/G, ... (the
+    // approx pseudo-rows already live inside the CTA partials); a head with no
+    // rows at all folds its approx list here (p == -1, slow path)
+    const int first = (kDense || !empty) ? 0 : -1;
     const int wpg = kWarps / G;  // warps per head (G in {1, 2, 4, 8})
     const int g = warp % G;
     float M = -INFINITY, Lw = 0.f;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (first < 0 && warp < G) {
+      const int na = __ldcg(&wl.napprox[bh]);
+      const int2* apx = wl.approx + (size_t)bh * v.cluster_cap;
+      const float* vbar = v.value_means + (size_t)bh * v.cluster_cap * d;
+#pragma unroll 1
+      for (int j = 0; j < na; ++j) {
+        const int2 e = __ldcg(&apx[j]);
+        if (!((e.y >> g) & 1)) continue;
+        const float x = (float)__ldcg(lm + ((size_t)bh * G + g) * v.cluster_cap + e.x);
+        const float4 vv = __ldg(reinterpret_cast<const float4*>(vbar + (size_t)e.x * d) + lane);
+        const float mn = fmaxf(M, x), a = __expf(M - mn), b = __expf(x - mn);
+        Lw = Lw * a + b;
+        acc.x = acc.x * a + b * vv.x; acc.y = acc.y * a + b * vv.y;
+        acc.z = acc.z * a + b * vv.z; acc.w = acc.w * a + b * vv.w;
+        M = mn;
+      }
+    }
     if (warp < wpg * G) {
       constexpr int kU = 16;
-      for (int p0 = first + warp / G; p0 < nparts; p0 += kU * wpg) {
+      for (int p0 = warp / G; p0 < nparts; p0 += kU * wpg) {
         float pm[kU], pl[kU];
         float4 po[kU];
 #pragma unroll
@@ -557,16 +644,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
           pl[u] = 0.f;
           po[u] = make_float4(0.f, 0.f, 0.f, 0.f);
           if (p < nparts) {
-            if (p >= 0) {
-              pm[u] = __ldcg(pt.m + pbase + (size_t)p * G + g);
-              pl[u] = __ldcg(pt.l + pbase + (size_t)p * G + g);
-              po[u] = __ldcg(reinterpret_cast<const float4*>(pt.o + (pbase + (size_t)p * G + g) * d) + lane);
-            } else {
-              const float* ap = wl.apart + ((size_t)bh * G + g) * (4 + d);
-              pm[u] = __ldcg(ap);
-              pl[u] = __ldcg(ap + 1);
-              po[u] = __ldcg(reinterpret_cast<const float4*>(ap + 4) + lane);
-            }
+            pm[u] = __ldcg(pt.m + pbase + (size_t)p * G + g);
+            pl[u] = __ldcg(pt.l + pbase + (size_t)p * G + g);
+            po[u] = __ldcg(reinterpret_cast<const float4*>(pt.o + (pbase + (size_t)p * G + g) * d) + lane);
           }
         }
         float mx = M;
@@ -664,9 +744,8 @@ static cudaError_t launch_tc_t(const dp_cache_view& v, const void* q, int G, dou
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  (void)lm;
-  return cudaLaunchKernelEx(&cfg, attn_tc_kernel<kDense, kQF32>, v, q, G, (float)(scale * 1.4426950408889634), wl,
-                            pt, out, lse, g_attn_debug);
+  return cudaLaunchKernelEx(&cfg, attn_tc_kernel<kDense, kQF32>, v, q, G, (float)(scale * 1.4426950408889634), lm,
+                            wl, pt, out, lse, g_attn_debug);
 }
 
 cudaError_t launch_attn_tc(const dp_cache_view& v, const void* q, int qdt, int G, double scale, const double* lm,

@@ -20,13 +20,14 @@
 //              mass); only the boundary bins are ranked exactly (log-mass
 //              desc, cluster id asc == the reference's stable argsort order).
 //              States go back to the CTAs owning each cluster slice.  -> B
-//   P3 union   every CTA counts its slice's union rows / clusters and folds
-//              its approximated clusters (logit = log-mass, value = value
-//              mean, engine.py:231-246) into per-head (l, o) partials, pushed
-//              to the head owners; slice counts pushed to all.      -> C
+//   P3 union   every CTA counts its slice's union rows / exact clusters /
+//              approximated clusters and pushes the counts to all.  -> C
 //   P4 lists   exclusive offsets from the pushed counts; coalesced packed
-//              row entries ((head mask << 24) | physical row); owners sum the
-//              approx partials of their head.  No remote access after C.
+//              row entries ((head mask << 24) | physical row), the approx
+//              cluster list and the log-masses.  No remote access after C.
+//              (The approximated clusters' pseudo-rows -- logit = log-mass,
+//              value = value mean, engine.py:231-246 -- are folded in by the
+//              attention kernel while its first tiles are in flight.)
 //
 // Cut semantics follow the reference: the first prefix whose cumsum/total
 // >= p (searchsorted left + 1, clamped to n); ties -> lower cluster id.
@@ -50,10 +51,9 @@ constexpr int kBinsPT = kBins / kPT;  // 4 bins per thread
 constexpr double kFix = 549755813888.0;  // 2^39 fixed-point scale of e = exp(lm - max) <= 1
 // (mass below 2^-39 of the max rounds to zero: <= 4096 * 2^-39 < 1e-8 of the total)
 constexpr int kPlanMaxCap = 4096;
-constexpr int kCh = 128;
+constexpr int kCh = 128;          // centroid rows per shared-memory tile (P1)
 constexpr int kTileBytes = kCh * 128 * 4;  // one tile: kCh rows x 128 fp32 (4 swizzled column blocks)
-constexpr int kMaxPer = 512;
-constexpr int kApx = 96;          // approximated clusters staged per P3 round      // clusters per CTA slice (cap 4096 / 8)          // centroid rows per shared-memory tile (P1)
+constexpr int kMaxPer = 512;      // clusters per CTA slice (cap 4096 / 8)
 
 // phase timestamps (%globaltimer, ns) of cluster 0: [rank][event]; read with
 // dp_debug_plan_timing() -- profiling aid only
@@ -86,7 +86,6 @@ struct PlanLayout {
   size_t lml;              // [kG][per] fp64 log-masses of my slice
   size_t qd;               // [8][d + 4] fp64 queries (padded rows)
   size_t stl;              // [kG][per] u8 states of my slice (pushed by the owners)
-  size_t aps;              // [CL][d + 4] fp32 approx partials of my head (owners; pushed by every CTA)
   size_t offs;             // [per + 1] int row offsets of my slice
   size_t total;
 };
@@ -113,16 +112,13 @@ __host__ __device__ inline PlanLayout plan_layout(int CL, int kG, int d, int cap
   L.clist = take2((size_t)cap * 4);
   L.cord = take2((size_t)cap * 4);
   const size_t csb = (size_t)2 * kTileBytes;  // two TMA tiles (128B swizzle) to d + 4 floats (conflict-free A loads)
-  const size_t redb = ((size_t)kApx * (d + 8) + (size_t)kPW * kG * (d + 4)) * 4;  // P3: value means, weights, sums
-  size_t big = csb > p2 ? csb : p2;
-  big = big > redb ? big : redb;
+  const size_t big = csb > p2 ? csb : p2;
   L.cs = take(big);
   L.um += L.cs; L.bin += L.cs; L.hm += L.cs; L.hc += L.cs; L.clist += L.cs; L.cord += L.cs;
   L.lmall = take((size_t)cap * 8);
   L.lml = take((size_t)kG * L.per * 8);
   L.qd = take((size_t)8 * (d + 4) * 8);
   L.stl = take((size_t)kG * L.per);
-  L.aps = take((size_t)CL * (d + 4) * 4);
   L.offs = take((size_t)(L.per + 1) * 4);
   L.total = o;
   return L;
@@ -303,7 +299,6 @@ __global__ void __launch_bounds__(kPT, 1)
   double* lml = reinterpret_cast<double*>(smem + L.lml);
   double* qd = reinterpret_cast<double*>(smem + L.qd);
   uint8_t* stl = reinterpret_cast<uint8_t*>(smem + L.stl);
-  float* aps = reinterpret_cast<float*>(smem + L.aps);
   int* offs = reinterpret_cast<int*>(smem + L.offs);
 
   __shared__ __align__(8) unsigned long long s_tbar[2];  // TMA tile barriers
@@ -314,8 +309,6 @@ __global__ void __launch_bounds__(kPT, 1)
   __shared__ unsigned long long s_redu[kPW];
   __shared__ int s_redi[kPW * 4];
   __shared__ SelShared s_sel;
-  __shared__ int s_alist[kMaxPer];      // approx clusters of my slice (local id | head mask << 16), P3
-  __shared__ int s_na;
 
   asm volatile("griddepcontrol.wait;\n" ::: "memory");  // PDL: inputs of the previous grid are visible
   // let the attention grid become resident on the SMs this launch leaves free
@@ -369,7 +362,6 @@ __global__ void __launch_bounds__(kPT, 1)
       const int h = i / d, c = i - h * d;
       qd[h * qP + c] = h < G ? (double)load_elem_f(q, qdt, ((size_t)bh * G + h) * d + c) : 0.0;
     }
-    if (tid == 0) s_na = 0;
   }
   __syncthreads();  // qd, offs, barrier init
   stamp(r, 1);
@@ -610,10 +602,7 @@ __global__ void __launch_bounds__(kPT, 1)
       e_rows += offs[i + 1] - offs[i];
       e_cl += 1;
     }
-    if (ma) {
-      a_cl += 1;
-      s_alist[atomicAdd(&s_na, 1)] = i | (ma << 16);
-    }
+    a_cl += ma != 0;
   }
   {  // (rows, exact clusters, approx clusters) of my slice -> every CTA
     const int v0 = warp_sum(e_rows), v1 = warp_sum(e_cl), v2 = warp_sum(a_cl);
@@ -638,71 +627,8 @@ __global__ void __launch_bounds__(kPT, 1)
     dst[1] = t1;
     dst[2] = t2;
   }
-  {
-    // approximated clusters (engine.py:231-246): their value means stream into
-    // the dead tile buffers by cp.async (all in flight at once), weights
-    // w = exp(lm - M_g) go to shared memory, then column-parallel sums
-    const int na = s_na;
-    const float* vbar = v.value_means + ((size_t)bh * cap + k0) * d;
-    float* vb = Cs;                                   // [kApx][d] value means
-    float* ws = Cs + (size_t)kApx * d;                // [kApx][8] weights
-    float* red = ws + (size_t)kApx * 8;               // [groups][G][d + 4] partial sums
-    const int ncol = G * (d / 4);                     // float4 columns (head, 4 dims)
-    const int ngrp = kPT / ncol;                      // >= 2 (G * d <= 1024)
-    const int col = tid % ncol, grp = tid / ncol;
-    const int cg_ = col / (d / 4), c4 = col - cg_ * (d / 4);
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    float lsum = 0.f;
-#pragma unroll 1
-    for (int a0 = 0; a0 < na; a0 += kApx) {
-      const int cnt = min(kApx, na - a0);
-      __syncthreads();  // previous chunk consumed
-#pragma unroll 1
-      for (int e = tid; e < cnt * (d / 4); e += kPT) {
-        const int a = e / (d / 4), cc = e - a * (d / 4);
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(
-                         (unsigned)__cvta_generic_to_shared(vb + (size_t)a * d + cc * 4)),
-                     "l"(vbar + (size_t)(s_alist[a0 + a] & 0xFFFF) * d + cc * 4));
-      }
-      asm volatile("cp.async.commit_group;\n" ::: "memory");
-#pragma unroll 1
-      for (int e = tid; e < cnt * 8; e += kPT) {
-        const int a = e >> 3, g = e & 7;
-        const int ent = s_alist[a0 + a], i = ent & 0xFFFF;
-        ws[e] = (g < G && ((ent >> (16 + g)) & 1)) ? __expf((float)(lml[g * L.per + i] - s_Mg[g])) : 0.f;
-      }
-      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-      __syncthreads();
-      if (grp < ngrp) {
-#pragma unroll 1
-        for (int a = grp; a < cnt; a += ngrp) {
-          const float w = ws[a * 8 + cg_];
-          const float4 x = *reinterpret_cast<const float4*>(vb + (size_t)a * d + c4 * 4);
-          acc.x += w * x.x; acc.y += w * x.y; acc.z += w * x.z; acc.w += w * x.w;
-          lsum += w;
-        }
-      }
-    }
-    __syncthreads();
-    if (grp < ngrp) {
-      float* rw = red + ((size_t)grp * G + cg_) * (d + 4);
-      *reinterpret_cast<float4*>(rw + 4 + c4 * 4) = acc;
-      if (c4 == 0) rw[0] = lsum;
-    }
-    __syncthreads();
-    // sum over groups; push my slice's (l, o) for head g into owner g's slot r
-#pragma unroll 1
-    for (int i = tid; i < G * (d + 4); i += kPT) {
-      const int g = i / (d + 4), c = i - g * (d + 4);
-      if (c == 1 || c == 2 || c == 3) continue;
-      float sm = 0.f;
-#pragma unroll 1
-      for (int q2 = 0; q2 < ngrp; ++q2) sm += red[((size_t)q2 * G + g) * (d + 4) + c];
-      remote(cluster, aps, g)[r * (d + 4) + c] = sm;
-    }
-  }
   stamp(r, 7);
-  cl_sync();  // (C) slice counts + approx partials published; no remote access after this
+  cl_sync();  // (C) slice counts published; no remote access after this
   stamp(r, 8);
 
   // ---------------- P4: work lists -----------------------------------------
@@ -718,25 +644,9 @@ __global__ void __launch_bounds__(kPT, 1)
     tot_e += s_cnt[rr][1];
     tot_a += s_cnt[rr][2];
   }
-  if (r < G) {  // owner: the head's approx partial = sum of the CL slice partials
-    const int g = r;
-    float* ap = wl.apart + ((size_t)bh * G + g) * (4 + d);
-#pragma unroll 1
-    for (int c = tid; c < d + 4; c += kPT) {
-      if (c == 1 || c == 2 || c == 3) continue;
-      float sm = 0.f;
-#pragma unroll 1
-      for (int rr = 0; rr < CL; ++rr) sm += aps[rr * (d + 4) + c];
-      if (c == 0) {
-        ap[0] = sm > 0.f ? (float)s_Mg[g] : -INFINITY;  // natural-log domain, like the attention partials
-        ap[1] = sm;
-      } else {
-        ap[c] = sm;
-      }
-    }
-  }
   stamp(r, 16);
-  // debug / parity outputs of my slice (kept off the barrier-release paths above)
+  // log-masses (the attention kernel reads the approximated clusters' ones)
+  // and the debug states of my slice, kept off the barrier-release paths above
   if (lm_out)
 #pragma unroll 1
     for (int i = tid; i < G * nloc; i += kPT) {
@@ -894,6 +804,7 @@ cudaError_t launch_plan(const dp_cache_view& v, const void* q, int qdt, int G, d
   decode_ws_layout(&v, G, &wl, nullptr, nullptr, reinterpret_cast<char*>(ws));
   wl.stats = stats;
   const int kG = group_bound(G);
+  if (!lm) return cudaErrorInvalidValue;  // the attention kernel reads the approx clusters' log-masses
   if (pick_cl(v) == 16) {
     switch (kG) {
       case 1: return launch_plan_t<16, 1>(v, q, qdt, G, scale, p1, p2, lm, state, counts, wl, st);
