@@ -329,7 +329,64 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
   // partial (m, l, o) of a finished head segment; the completion counters are
   // bumped once, after the loop, behind a single fence (no mid-loop stall)
   int flushed[2] = {-1, -1}, nflushed = 0;  // a CTA range touches <= 2 heads unless heads are tiny
+  // approx pseudo-row pipeline state (warp-uniform)
+  int ap_base = 0, ap_n = 0, ap_k = 0;
+  bool ap_ready = false;
+  int2 ap_desc = make_int2(0, 0);  // lane i: descriptor of entry ap_base + i (i < 32)
+  float4 ap_v = make_float4(0.f, 0.f, 0.f, 0.f);  // value-mean slice [4 lane, 4 lane + 4)
+  float ap_x = -INFINITY;          // lanes 0..7: log2-mass of head `lane` (or -inf)
+  auto ap_issue = [&](int bh) {    // start the loads of entry ap_k
+    int2 e;
+    if (ap_k < 32) {
+      e.x = __shfl_sync(0xffffffffu, ap_desc.x, ap_k);
+      e.y = __shfl_sync(0xffffffffu, ap_desc.y, ap_k);
+    } else {
+      e = __ldcg(&wl.approx[(size_t)bh * v.cluster_cap + ap_base + ap_k]);
+    }
+    ap_v = __ldg(reinterpret_cast<const float4*>(v.value_means + ((size_t)bh * v.cluster_cap + e.x) * d) + lane);
+    ap_x = (lane < G && ((e.y >> lane) & 1))
+               ? (float)(__ldcg(lm + ((size_t)bh * G + lane) * v.cluster_cap + e.x) * 1.4426950408889634)
+               : -INFINITY;
+    ++ap_k;
+    ap_ready = true;
+  };
+  auto ap_fold = [&]() {  // fold the loaded entry into this warp's online softmax
+    float x[2];
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) x[hh] = __shfl_sync(0xffffffffu, ap_x, 2 * tq + hh);
+    __syncwarp();
+    reinterpret_cast<float4*>(Pw)[lane] = ap_v;  // value row -> fragment layout via the P buffer
+    __syncwarp();
+    float pa[2], al[2];
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      const float mn = fmaxf(m_run[hh], x[hh]);
+      al[hh] = mn == -INFINITY ? 1.f : exp2f(m_run[hh] - mn);
+      pa[hh] = x[hh] == -INFINITY ? 0.f : exp2f(x[hh] - mn);
+      m_run[hh] = mn;
+      l_run[hh] = l_run[hh] * al[hh] + (g8 == 0 ? pa[hh] : 0.f);  // one lane per head counts it
+    }
+#pragma unroll
+    for (int mb = 0; mb < 8; ++mb) {
+      const float v0 = Pw[mb * 16 + g8], v1 = Pw[mb * 16 + g8 + 8];
+      o[mb][0] = o[mb][0] * al[0] + pa[0] * v0;
+      o[mb][1] = o[mb][1] * al[1] + pa[1] * v0;
+      o[mb][2] = o[mb][2] * al[0] + pa[0] * v1;
+      o[mb][3] = o[mb][3] * al[1] + pa[1] * v1;
+    }
+    __syncwarp();
+    ap_ready = false;
+  };
+
   auto flush = [&](int bh, float* scratch) {
+    if (!kDense) {  // drain this warp's remaining approx entries
+      if (ap_ready) ap_fold();
+#pragma unroll 1
+      while (ap_k < ap_n) {
+        ap_issue(bh);
+        ap_fold();
+      }
+    }
 #pragma unroll
     for (int hh = 0; hh < 2; ++hh) {
       l_run[hh] += __shfl_xor_sync(0xffffffffu, l_run[hh], 4);
@@ -405,72 +462,21 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
       l_run[0] = l_run[1] = 0.f;
       // approximated clusters of this head (engine.py:231-246): pseudo-rows
       // with logit = log-mass, value = value mean.  The head's CTAs split the
-      // plan's approx list evenly and start their online softmax from their
-      // share -- this runs while the segment's first tile is in flight, and
-      // the merge needs no separate approx partial.
+      // plan's approx list, each warp takes a share and trickles it into its
+      // online softmax one entry per tile, loads issued a tile ahead (so the
+      // fold never waits on memory); the flush drains what is left.
       if (!kDense) {
-        const int na = __ldcg(&wl.napprox[bh]);
-        const int part = me - first_owner(bh), np = head_parts(bh);
-        const int j0 = (int)((long long)na * part / np), j1 = (int)((long long)na * (part + 1) / np);
-        // warp w: entries [a0, a1) of the CTA's share; batches of 4 whose
-        // loads (one 128-bit value-mean slice per lane per entry, one
-        // log-mass per (entry, head) lane) are all in flight together
-        const int a0 = j0 + (j1 - j0) * warp / kWarps, a1 = j0 + (j1 - j0) * (warp + 1) / kWarps;
-        const int2* apx = wl.approx + (size_t)bh * v.cluster_cap;
-        const float* vbar = v.value_means + (size_t)bh * v.cluster_cap * d;
-#pragma unroll 1
-        for (int b0 = a0; b0 < a1; b0 += 4) {
-          const int nb = min(4, a1 - b0);
-          const int2 el = lane < nb ? __ldcg(&apx[b0 + lane]) : make_int2(0, 0);
-          int ex[4], ey[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            ex[u] = __shfl_sync(0xffffffffu, el.x, u);
-            ey[u] = __shfl_sync(0xffffffffu, el.y, u);
-          }
-          float4 vrow[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            vrow[u] = u < nb ? __ldg(reinterpret_cast<const float4*>(vbar + (size_t)ex[u] * d) + lane)
-                             : make_float4(0.f, 0.f, 0.f, 0.f);
-          const int lu = lane >> 3, lh = lane & 7;  // this lane fetches entry lu's head-lh log-mass
-          const int eyu = __shfl_sync(0xffffffffu, el.y, lu), exu = __shfl_sync(0xffffffffu, el.x, lu);
-          const float xl = (lu < nb && lh < G && ((eyu >> lh) & 1))
-                               ? (float)(__ldcg(lm + ((size_t)bh * G + lh) * v.cluster_cap + exu) * 1.4426950408889634)
-                               : -INFINITY;
-#pragma unroll 1
-          for (int u = 0; u < nb; ++u) {
-            float x[2];
-#pragma unroll
-            for (int hh = 0; hh < 2; ++hh) x[hh] = __shfl_sync(0xffffffffu, xl, u * 8 + 2 * tq + hh);
-            // value mean row -> fragment layout through the warp's P buffer
-            float4 vr = vrow[0];
-            if (u == 1) vr = vrow[1];
-            if (u == 2) vr = vrow[2];
-            if (u == 3) vr = vrow[3];
-            __syncwarp();
-            reinterpret_cast<float4*>(Pw)[lane] = vr;
-            __syncwarp();
-            float pa[2], al[2];
-#pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-              const float mn = fmaxf(m_run[hh], x[hh]);
-              al[hh] = mn == -INFINITY ? 1.f : exp2f(m_run[hh] - mn);
-              pa[hh] = x[hh] == -INFINITY ? 0.f : exp2f(x[hh] - mn);
-              m_run[hh] = mn;
-              l_run[hh] = l_run[hh] * al[hh] + (g8 == 0 ? pa[hh] : 0.f);  // one lane per head counts it
-            }
-#pragma unroll
-            for (int mb = 0; mb < 8; ++mb) {
-              const float v0 = Pw[mb * 16 + g8], v1 = Pw[mb * 16 + g8 + 8];
-              o[mb][0] = o[mb][0] * al[0] + pa[0] * v0;
-              o[mb][1] = o[mb][1] * al[1] + pa[1] * v0;
-              o[mb][2] = o[mb][2] * al[0] + pa[0] * v1;
-              o[mb][3] = o[mb][3] * al[1] + pa[1] * v1;
-            }
-          }
-        }
-        __syncwarp();
+        // this CTA's share of the head's approx list is proportional to the
+        // rows of the head it covers (a short head segment gets few entries)
+        const long long na = __ldcg(&wl.napprox[bh]);
+        const long long hr = rp[bh + 1] - rp[bh];
+        const long long lo = (r0 > rp[bh] ? r0 : rp[bh]) - rp[bh], hi = (r1 < rp[bh + 1] ? r1 : rp[bh + 1]) - rp[bh];
+        const int j0 = (int)(na * lo / hr), j1 = (int)(na * hi / hr);
+        ap_base = j0 + (j1 - j0) * warp / kWarps;
+        ap_n = j0 + (j1 - j0) * (warp + 1) / kWarps - ap_base;
+        ap_desc = lane < ap_n ? __ldcg(&wl.approx[(size_t)bh * v.cluster_cap + ap_base + lane]) : make_int2(0, 0);
+        ap_k = 0;
+        ap_ready = false;
       }
     }
     mbar_wait(smem_u32(&full_bar[s]), (unsigned)((idx / kStages) & 1));  // stage s landed
@@ -563,11 +569,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
             : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(bl0), "r"(bl1));
       }
     }
+    if (!kDense) {  // one approx pseudo-row per tile: fold the loaded one, issue the next
+      if (ap_ready) ap_fold();
+      if (ap_k < ap_n) ap_issue(bh);
+    }
     if (seg_end) flush(bh, reinterpret_cast<float*>(Ks));  // this stage's K buffer is the scratch
     __syncwarp();
     if (lane == 0) mbar_arrive(smem_u32(&empty_bar[s]));  // stage s free for the producer
   }
   astamp(3);
+  if (tid == 0 && blockIdx.x < 512) {  // profiling: rows and head segments of this CTA
+    g_attn_ts[blockIdx.x][7] = (unsigned long long)(r1 - r0);
+    g_attn_ts[blockIdx.x][8] = (unsigned long long)nflushed;
+  }
   consumers_sync();  // every partial of this CTA is written (CTA scope)
   if (tid == 0) {
     __threadfence();  // ... and visible at gpu scope before the counters move (cumulativity)
@@ -594,28 +608,25 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
   __threadfence();
   astamp(6);
   float* ored = reinterpret_cast<float*>(KV);  // [warps][8 heads][d]
-  for (int mi = 0; mi < nm; ++mi) {
+  if (tid < nm) wl.counters[s_merge[tid]] = 0;  // self-reset for the next launch
+  // (merged head, q head) pairs are spread over all 8 warps, so a CTA that
+  // closes two heads merges them side by side.  Warp w takes pair
+  // w % npr of the round and partials w / npr, + wpp, ...; a head with no rows
+  // at all folds its approx list here instead (slow path).
+  const int pairs = nm * G;
+#pragma unroll 1
+  for (int base = 0; base < pairs; base += kWarps) {
+    const int npr = min(kWarps, pairs - base);
+    const int wpp = kWarps / npr;  // warps per pair
+    const int pr = warp % npr;
+    const int mi = (base + pr) / G, g = (base + pr) % G;
     const int bh = s_merge[mi];
     const bool empty = rp[bh + 1] == rp[bh];
     const int nparts = empty ? 0 : head_parts(bh);
     const size_t pbase = (size_t)bh * pt.max_chunks * G;
-    if (tid == 0) wl.counters[bh] = 0;  // self-reset for the next launch
-    if (mi == 0 && tid == 0 && blockIdx.x < 512) {  // profiling: one dependent L2 round trip
-      unsigned long long ta, tb;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ta));
-      const float probe = __ldcg(pt.m + pbase);
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tb) : "f"(probe));
-      g_attn_ts[blockIdx.x][11] = (tb - ta) + (probe == 12345.f);
-    }
-    // warp w merges head g = w % G over partials p = w / G, + 8/G, ... (the
-    // approx pseudo-rows already live inside the CTA partials); a head with no
-    // rows at all folds its approx list here (p == -1, slow path)
-    const int first = (kDense || !empty) ? 0 : -1;
-    const int wpg = kWarps / G;  // warps per head (G in {1, 2, 4, 8})
-    const int g = warp % G;
     float M = -INFINITY, Lw = 0.f;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (first < 0 && warp < G) {
+    if (!kDense && empty && warp < npr) {
       const int na = __ldcg(&wl.napprox[bh]);
       const int2* apx = wl.approx + (size_t)bh * v.cluster_cap;
       const float* vbar = v.value_means + (size_t)bh * v.cluster_cap * d;
@@ -632,14 +643,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
         M = mn;
       }
     }
-    if (warp < wpg * G) {
+    if (warp < wpp * npr) {
       constexpr int kU = 16;
-      for (int p0 = warp / G; p0 < nparts; p0 += kU * wpg) {
+#pragma unroll 1
+      for (int p0 = warp / npr; p0 < nparts; p0 += kU * wpp) {
         float pm[kU], pl[kU];
         float4 po[kU];
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
-          const int p = p0 + u * wpg;
+          const int p = p0 + u * wpp;
           pm[u] = -INFINITY;
           pl[u] = 0.f;
           po[u] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -666,25 +678,20 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
         }
       }
     }
-    if (mi == 0) {
-      astamp(7);
-      if (tid == 0 && blockIdx.x < 512) {
-        g_attn_ts[blockIdx.x][9] = nm;
-        g_attn_ts[blockIdx.x][10] = nparts;
-      }
-    }
     reinterpret_cast<float4*>(ored + (size_t)warp * d)[lane] = acc;
     if (lane == 0) {
       s_wm[warp][0] = M;
       s_wl[warp][0] = Lw;
     }
     consumers_sync();
-    for (int i = tid; i < G * d; i += kConsumers) {
-      const int gg = i / d, c = i - gg * d;
+#pragma unroll 1
+    for (int i = tid; i < npr * d; i += kConsumers) {
+      const int q2 = i / d, c = i - q2 * d;
+      const int mi2 = (base + q2) / G, g2 = (base + q2) % G, bh2 = s_merge[mi2];
       float Mx = -INFINITY;
-      for (int ww = gg; ww < wpg * G; ww += G) Mx = fmaxf(Mx, s_wm[ww][0]);
+      for (int ww = q2; ww < wpp * npr; ww += npr) Mx = fmaxf(Mx, s_wm[ww][0]);
       float sum = 0.f, L = 0.f;
-      for (int ww = gg; ww < wpg * G; ww += G) {
+      for (int ww = q2; ww < wpp * npr; ww += npr) {
         const float wm = s_wm[ww][0];
         if (wm != -INFINITY) {
           const float f = __expf(wm - Mx);
@@ -692,11 +699,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
           L += f * s_wl[ww][0];
         }
       }
-      out[((size_t)bh * G + gg) * d + c] = L > 0.f ? sum / L : 0.f;
-      if (c == 0) lse[(size_t)bh * G + gg] = L > 0.f ? Mx + __logf(L) : -INFINITY;
+      out[((size_t)bh2 * G + g2) * d + c] = L > 0.f ? sum / L : 0.f;
+      if (c == 0) lse[(size_t)bh2 * G + g2] = L > 0.f ? Mx + __logf(L) : -INFINITY;
     }
     consumers_sync();
-    if (mi == 0) astamp(8);
   }
   astamp(5);
 }

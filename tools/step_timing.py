@@ -109,7 +109,7 @@ timed(lambda: [(plan(j), attend(j)) for j in range(L)], reps=1)
 abuf = (ctypes.c_ulonglong * (512 * 12))()
 lib.dp_debug_attn_timing(ctypes.cast(abuf, ctypes.c_void_p))
 a = np.array(abuf[:], dtype=np.float64).reshape(512, 12)[:148]
-nmg = a[:, 9].copy(); npt = a[:, 10].copy(); rtt = a[:, 11].copy(); a = a[:, :9]
+rows = a[:, 7].copy(); segs = a[:, 8].copy(); a = a[:, :7]
 a0 = a[:, 0].min()
 rel = (a - a0) / 1e3
 print("attn phases of the last step (us, rel. to first CTA start): start, prefix, first data, loop done, flushed, exit")
@@ -119,6 +119,15 @@ for name, col in (("start", 0), ("prefix", 1), ("data0", 2), ("loop", 3), ("flus
     x = x[(x > -1e6) & (x < 1e6)]
     if x.size:
         print(f"  {name:7s} min {x.min():7.2f} med {np.median(x):7.2f} max {x.max():7.2f}  (n={x.size})")
+loop_end = rel[:, 3] - rel[:, 2]
+for sg in (1, 2):
+    sel = segs == sg
+    if sel.any():
+        print(f"  CTAs with {sg} head segment(s): n={int(sel.sum())} rows med {np.median(rows[sel]):.0f} "
+              f"loop(data0->done) med {np.median(loop_end[sel]):.2f} max {loop_end[sel].max():.2f} us")
+slow = np.argsort(-rel[:, 3])[:6]
+print("  slowest CTAs (id, segments, rows, data0, loop done):",
+      [(int(c), int(segs[c]), int(rows[c]), round(rel[c, 2], 2), round(rel[c, 3], 2)) for c in slow])
 mer = np.where((rel[:, 6] > 0) & (rel[:, 6] < 1e3))[0]
 for c in mer:
     print(f"  merging CTA {c}: loop {rel[c,3]:.2f} flush {rel[c,4]:.2f} "
