@@ -54,6 +54,7 @@ constexpr int kPlanMaxCap = 4096;
 constexpr int kCh = 128;          // centroid rows per shared-memory tile (P1)
 constexpr int kTileBytes = kCh * 128 * 4;  // one tile: kCh rows x 128 fp32 (4 swizzled column blocks)
 constexpr int kMaxPer = 512;      // clusters per CTA slice (cap 4096 / 8)
+constexpr int kMaxCL = 16;        // cluster size is chosen at launch (<= 16, non-portable above 8)
 
 // phase timestamps (%globaltimer, ns) of cluster 0: [rank][event]; read with
 // dp_debug_plan_timing() -- profiling aid only
@@ -280,11 +281,11 @@ __device__ __noinline__ int sel_cut(SelShared* sh, const unsigned long long* um,
   return sh->n;
 }
 
-template <int CL, int kG>
+template <int kG>
 __global__ void __launch_bounds__(kPT, 1)
     plan_kernel(const __grid_constant__ CUtensorMap tmC, dp_cache_view v, const void* __restrict__ q, int qdt, int G,
                 double scale, double p1, double p2, double* __restrict__ lm_out, uint8_t* __restrict__ state_out,
-                int* __restrict__ counts, WorkLists wl) {
+                int* __restrict__ counts, WorkLists wl, int CL) {
   cg::cluster_group cluster = cg::this_cluster();
   const int r = (int)cluster.block_rank();
   const int bh = blockIdx.x / CL;
@@ -302,8 +303,8 @@ __global__ void __launch_bounds__(kPT, 1)
   int* offs = reinterpret_cast<int*>(smem + L.offs);
 
   __shared__ __align__(8) unsigned long long s_tbar[2];  // TMA tile barriers
-  __shared__ double s_max[CL][kG];      // pushed slice maxima (owners)
-  __shared__ int s_cnt[CL][4];          // pushed slice counts (rows, exact clusters, approx clusters)
+  __shared__ double s_max[kMaxCL][kG];  // pushed slice maxima (owners)
+  __shared__ int s_cnt[kMaxCL][4];      // pushed slice counts (rows, exact clusters, approx clusters)
   __shared__ double s_Mg[kG];           // pushed head maxima (every CTA)
   __shared__ double s_wm[kPW][kG];
   __shared__ unsigned long long s_redu[kPW];
@@ -392,8 +393,9 @@ __global__ void __launch_bounds__(kPT, 1)
       const unsigned char* arow = tileC + (size_t)ia * 128 + (lane & 3) * 4;
       const int sw = ia & 7;
       double c[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
-#pragma unroll 1
-      for (int kk = 0; kk < d / 4; kk += 4) {
+#pragma unroll
+      for (int kk = 0; kk < 32; kk += 4) {
+        if (kk * 4 >= d) break;
 #pragma unroll
         for (int tt = 0; tt < 4; ++tt) {
           const int kq = kk + tt;
@@ -722,14 +724,7 @@ __global__ void __launch_bounds__(kPT, 1)
   stamp(r, 9);
 }
 
-int g_plan_cl = 0;  // 0: auto; 8 / 16 forces the cluster size (dp_debug_set(1, .))
-// 8-CTA clusters: on B200 at most 7 sixteen-CTA clusters are co-resident
-// (GPC shapes), so 8 kv heads of 16-CTA clusters would run in two waves
-static int pick_cl(const dp_cache_view& v) {
-  if (g_plan_cl == 8 || g_plan_cl == 16) return g_plan_cl;
-  return 8;
-}
-
+int g_plan_cl = 0;  // 0: auto; 2..16 forces the cluster size (dp_debug_set(1, .))
 size_t plan_smem_bytes(int d, int cap, int CL, int kG) { return plan_layout(CL, kG, d, cap).total + 1024; }
 
 // 2-D tensor map over all centroid rows [B*H*cap, d] fp32: 32-float x kCh-row
@@ -758,25 +753,84 @@ static cudaError_t centroid_tmap(const dp_cache_view& v, CUtensorMap* m) {
 
 static int group_bound(int G) { return G <= 1 ? 1 : (G <= 2 ? 2 : (G <= 4 ? 4 : 8)); }
 
-bool plan_supported(const dp_cache_view& v, int G) {
-  const int CL = pick_cl(v);
-  const int per = (v.cluster_cap + CL - 1) / CL;
-  return v.cluster_cap <= kPlanMaxCap && G <= 8 && G <= CL && v.head_dim <= 128 && v.head_dim % 32 == 0 &&
-         per <= kMaxPer && v.row_cap < (1 << 24) &&
-         plan_smem_bytes(v.head_dim, v.cluster_cap, CL, group_bound(G)) <= 227 * 1024;
+template <int kG>
+static void* plan_fn() {
+  return reinterpret_cast<void*>(plan_kernel<kG>);
+}
+static void* plan_fn_for(int kG) {
+  return kG == 1 ? plan_fn<1>() : kG == 2 ? plan_fn<2>() : kG == 4 ? plan_fn<4>() : plan_fn<8>();
 }
 
-template <int CL, int kG>
-static cudaError_t launch_plan_t(const dp_cache_view& v, const void* q, int qdt, int G, double scale, double p1,
-                                 double p2, double* lm, uint8_t* state, int* counts, const WorkLists& wl,
-                                 cudaStream_t st) {
-  auto kern = plan_kernel<CL, kG>;
+// co-resident clusters of size cl at this shared-memory footprint
+static int max_active_clusters(int kG, int cl, size_t smem) {
+  static int cache[9][17] = {};
+  static size_t cache_smem[9][17] = {};
+  if (cache_smem[kG][cl] == smem) return cache[kG][cl];
+  void* fn = plan_fn_for(kG);
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)cl);
+  cfg.blockDim = dim3(kPT);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cl;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
+  }
+  cache[kG][cl] = n;
+  cache_smem[kG][cl] = smem;
+  return n;
+}
+
+static bool cl_fits(const dp_cache_view& v, int G, int cl) {
+  const int per = (v.cluster_cap + cl - 1) / cl;
+  return G <= cl && per <= kMaxPer && plan_smem_bytes(v.head_dim, v.cluster_cap, cl, group_bound(G)) <= 227 * 1024;
+}
+
+// Cluster size: the widest (<= 16) for which every (sequence, kv head) cluster
+// is co-resident in one wave -- more CTAs per head shorten the per-CTA slice;
+// a second wave would double the latency.  (B200: 7 sixteen-CTA clusters fit,
+// so 8 kv heads use 12-14.)  Batches with more heads than one wave holds at
+// any size use 8.
+static int pick_cl(const dp_cache_view& v, int G) {
+  if (g_plan_cl >= 2 && g_plan_cl <= kMaxCL && cl_fits(v, G, g_plan_cl)) return g_plan_cl;
+  const int units = v.batch * v.kv_heads;
+  const int kG = group_bound(G);
+  for (int cl = kMaxCL; cl > 8; --cl)
+    if (cl_fits(v, G, cl) &&
+        max_active_clusters(kG, cl, plan_smem_bytes(v.head_dim, v.cluster_cap, cl, kG)) >= units)
+      return cl;
+  return 8;
+}
+
+bool plan_supported(const dp_cache_view& v, int G) {
+  return v.cluster_cap <= kPlanMaxCap && G <= 8 && v.head_dim <= 128 && v.head_dim % 32 == 0 &&
+         v.row_cap < (1 << 24) && cl_fits(v, G, 8);
+}
+
+cudaError_t launch_plan(const dp_cache_view& v, const void* q, int qdt, int G, double scale, double p1, double p2,
+                        double* lm, uint8_t* state, int* counts, int* stats, void* ws, cudaStream_t st) {
+  WorkLists wl;
+  decode_ws_layout(&v, G, &wl, nullptr, nullptr, reinterpret_cast<char*>(ws));
+  wl.stats = stats;
+  if (!lm) return cudaErrorInvalidValue;  // the attention kernel reads the approx clusters' log-masses
+  const int kG = group_bound(G);
+  const int CL = pick_cl(v, G);
   const size_t smem = plan_smem_bytes(v.head_dim, v.cluster_cap, CL, kG);
-  static size_t attr = 0;
-  if (attr < smem) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (CL > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    attr = smem;
+  void* fn = plan_fn_for(kG);
+  static size_t attr[9] = {};
+  if (attr[kG] < smem) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    attr[kG] = smem;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(v.batch * v.kv_heads * CL));
@@ -795,31 +849,15 @@ static cudaError_t launch_plan_t(const dp_cache_view& v, const void* q, int qdt,
   CUtensorMap tm;
   const cudaError_t e = centroid_tmap(v, &tm);
   if (e != cudaSuccess) return e;
-  return cudaLaunchKernelEx(&cfg, kern, tm, v, q, qdt, G, scale, p1, p2, lm, state, counts, wl);
+  switch (kG) {
+    case 1: return cudaLaunchKernelEx(&cfg, plan_kernel<1>, tm, v, q, qdt, G, scale, p1, p2, lm, state, counts, wl, CL);
+    case 2: return cudaLaunchKernelEx(&cfg, plan_kernel<2>, tm, v, q, qdt, G, scale, p1, p2, lm, state, counts, wl, CL);
+    case 4: return cudaLaunchKernelEx(&cfg, plan_kernel<4>, tm, v, q, qdt, G, scale, p1, p2, lm, state, counts, wl, CL);
+    default: return cudaLaunchKernelEx(&cfg, plan_kernel<8>, tm, v, q, qdt, G, scale, p1, p2, lm, state, counts, wl, CL);
+  }
 }
 
-cudaError_t launch_plan(const dp_cache_view& v, const void* q, int qdt, int G, double scale, double p1, double p2,
-                        double* lm, uint8_t* state, int* counts, int* stats, void* ws, cudaStream_t st) {
-  WorkLists wl;
-  decode_ws_layout(&v, G, &wl, nullptr, nullptr, reinterpret_cast<char*>(ws));
-  wl.stats = stats;
-  const int kG = group_bound(G);
-  if (!lm) return cudaErrorInvalidValue;  // the attention kernel reads the approx clusters' log-masses
-  if (pick_cl(v) == 16) {
-    switch (kG) {
-      case 1: return launch_plan_t<16, 1>(v, q, qdt, G, scale, p1, p2, lm, state, counts, wl, st);
-      case 2: return launch_plan_t<16, 2>(v, q, qdt, G, scale, p1, p2, lm, state, counts, wl, st);
-      case 4: return launch_plan_t<16, 4>(v, q, qdt, G, scale, p1, p2, lm, state, counts, wl, st);
-      default: return launch_plan_t<16, 8>(v, q, qdt, G, scale, p1, p2, lm, state, counts, wl, st);
-    }
-  }
-  switch (kG) {
-    case 1: return launch_plan_t<8, 1>(v, q, qdt, G, scale, p1, p2, lm, state, counts, wl, st);
-    case 2: return launch_plan_t<8, 2>(v, q, qdt, G, scale, p1, p2, lm, state, counts, wl, st);
-    case 4: return launch_plan_t<8, 4>(v, q, qdt, G, scale, p1, p2, lm, state, counts, wl, st);
-    default: return launch_plan_t<8, 8>(v, q, qdt, G, scale, p1, p2, lm, state, counts, wl, st);
-  }
-}
+int plan_cluster_size(const dp_cache_view& v, int G) { return pick_cl(v, G); }
 
 }  // namespace dp
 
@@ -831,31 +869,13 @@ extern "C" int dp_debug_plan_timing(unsigned long long* out) {
 }
 
 // max co-resident clusters of the plan kernel at this geometry (profiling aid)
+namespace dp {
+int plan_occupancy(const dp_cache_view& v, int G, int cl) {
+  const int kG = group_bound(G);
+  return max_active_clusters(kG, cl, plan_smem_bytes(v.head_dim, v.cluster_cap, cl, kG));
+}
+}  // namespace dp
 extern "C" int dp_debug_plan_occupancy(const dp_cache_view* v, int G, int cl) {
-  const int kG = dp::group_bound(G);
-  const size_t smem = dp::plan_smem_bytes(v->head_dim, v->cluster_cap, cl, kG);
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(v->batch * v->kv_heads * cl));
-  cfg.blockDim = dim3(dp::kPT);
-  cfg.dynamicSmemBytes = smem;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = cl;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  int n = -1;
-  cudaError_t e;
-  if (cl == 16) {
-    auto k = dp::plan_kernel<16, 4>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    e = cudaOccupancyMaxActiveClusters(&n, k, &cfg);
-  } else {
-    auto k = dp::plan_kernel<8, 4>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    e = cudaOccupancyMaxActiveClusters(&n, k, &cfg);
-  }
-  return e == cudaSuccess ? n : -(int)e;
+  if (cl == 0) return dp::plan_cluster_size(*v, G);  // the size launch_plan picks
+  return dp::plan_occupancy(*v, G, cl);
 }

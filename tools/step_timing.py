@@ -84,8 +84,8 @@ for j in range(L):
     plan(j)
     attend(j)
 torch.cuda.synchronize()
-print("max active plan clusters: CL16", lib.dp_debug_plan_occupancy(views[0], G, 16), "CL8",
-      lib.dp_debug_plan_occupancy(views[0], G, 8))
+print("max active plan clusters by size:", {c: lib.dp_debug_plan_occupancy(views[0], G, c) for c in (8, 10, 12, 14, 16)},
+      "picked:", lib.dp_debug_plan_occupancy(views[0], G, 0))
 if len(sys.argv) > 4:
     lib.dp_debug_set(1, int(sys.argv[4]))
 print(f"context {n}, layers {L}, G {G}: us per layer")
