@@ -36,6 +36,7 @@ constexpr int kProducers = 4;  // producer warps, 32 rows each
 constexpr int kTcThreads = kConsumers + 32 * kProducers;
 constexpr int kRowStride = 136;      // bf16 elements per staged row (272 B: conflict-free ldmatrix)
 constexpr int kStages = 3;
+constexpr int kSegCost = 256;  // rows' worth of time a head segment start costs a CTA (range balancing)
 constexpr int kStageElems = kTcRows * kRowStride;  // one K (or V) tile
 int g_attn_debug = 0;  // profiling switches (dp_debug_set)
 
@@ -227,10 +228,24 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
   }
   __syncthreads();
   astamp(1);
-  const long long T = rp[BH];
-  const long long r0 = T * me / grid, r1 = T * (me + 1) / grid;
-  auto first_owner = [&](int bh) { return row_owner(rp[bh], T, grid); };
-  auto head_parts = [&](int bh) { return row_owner(rp[bh + 1] - 1, T, grid) - first_owner(bh) + 1; };
+  // Ranges are balanced in a virtual row space where every head is preceded
+  // by kSegCost empty rows: a CTA whose range starts a head segment (q load,
+  // approx list, one more flush) gets correspondingly fewer real rows.
+  // virtual(j) = j + (b + 1) * kSegCost for real row j of head b.
+  const long long TV = rp[BH] + (long long)BH * kSegCost;
+  auto real_of = [&](long long vv) {  // first real row at or after virtual row vv
+    int lo = 0, hi = BH - 1;           // last head b with rp[b] + b * kSegCost <= vv
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (rp[mid] + (long long)mid * kSegCost <= vv) lo = mid; else hi = mid - 1;
+    }
+    const long long o = vv - (rp[lo] + (long long)(lo + 1) * kSegCost);
+    return o <= 0 ? rp[lo] : (rp[lo] + o < rp[lo + 1] ? rp[lo] + o : rp[lo + 1]);
+  };
+  const long long r0 = real_of(TV * me / grid), r1 = me + 1 == grid ? rp[BH] : real_of(TV * (me + 1) / grid);
+  auto owner = [&](long long j, int b) { return row_owner(j + (long long)(b + 1) * kSegCost, TV, grid); };
+  auto first_owner = [&](int bh) { return owner(rp[bh], bh); };
+  auto head_parts = [&](int bh) { return owner(rp[bh + 1] - 1, bh) - first_owner(bh) + 1; };
 
   // ---- producer warps (rows [32p, 32p+32) of every tile): run up to kStages
   // tiles ahead; the next tile's row entries are fetched while this tile's
@@ -411,23 +426,34 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
 #pragma unroll 1
     for (int i = tid; i < G * d; i += kConsumers) {
       const int h = i / d, c = i - h * d;
-      float Mx = -INFINITY;
+      // sparse: scale to the plan's reference max and add into the head's
+      // accumulators (fire-and-forget reductions; the merge then reads one
+      // (o, l) per q head instead of every CTA's partial).  Dense: partials.
+      const float Mx = kDense ? -INFINITY : __ldcg(&wl.refm[(size_t)bh * G + h]);
+      float Mw = -INFINITY;
 #pragma unroll
-      for (int ww = 0; ww < kWarps; ++ww) Mx = fmaxf(Mx, s_wm[ww][h]);
+      for (int ww = 0; ww < kWarps; ++ww) Mw = fmaxf(Mw, s_wm[ww][h]);
+      const float Mr = kDense ? Mw : Mx;
       float sum = 0.f, L = 0.f;
 #pragma unroll
       for (int ww = 0; ww < kWarps; ++ww) {
         const float wm = s_wm[ww][h];
         if (wm != -INFINITY) {
-          const float f = exp2f(wm - Mx);
+          const float f = exp2f(wm - Mr);
           sum += f * scratch[((size_t)ww * 8 + h) * d + c];
           L += f * s_wl[ww][h];
         }
       }
-      pt.o[(pbase + (size_t)slot * G + h) * d + c] = sum;
-      if (c == 0) {
-        pt.m[pbase + (size_t)slot * G + h] = Mx == -INFINITY ? -INFINITY : Mx * 0.69314718055994531f;
-        pt.l[pbase + (size_t)slot * G + h] = L;
+      if (kDense) {
+        pt.o[(pbase + (size_t)slot * G + h) * d + c] = sum;
+        if (c == 0) {
+          pt.m[pbase + (size_t)slot * G + h] = Mw == -INFINITY ? -INFINITY : Mw * 0.69314718055994531f;
+          pt.l[pbase + (size_t)slot * G + h] = L;
+        }
+      } else if (Mw != -INFINITY) {
+        float* ac = wl.acc + ((size_t)bh * G + h) * (d + 1);
+        atomicAdd(ac + c, sum);
+        if (c == 0) atomicAdd(ac + d, L);
       }
     }
     consumers_sync();  // scratch (this stage) and s_wm/s_wl free again
@@ -609,11 +635,43 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
   astamp(6);
   float* ored = reinterpret_cast<float*>(KV);  // [warps][8 heads][d]
   if (tid < nm) wl.counters[s_merge[tid]] = 0;  // self-reset for the next launch
+  if (!kDense) {
+    // sparse heads with rows: out = o / l from the accumulators (one round
+    // trip), which are zeroed again for the next launch
+    const int nq = nm * G;
+#pragma unroll 1
+    for (int i = tid; i < nq * d; i += kConsumers) {
+      const int qi = i / d, c = i - qi * d, mi = qi / G, g = qi - mi * G, bh = s_merge[mi];
+      if (rp[bh + 1] == rp[bh]) continue;  // no rows: slow path below
+      float* ac = wl.acc + ((size_t)bh * G + g) * (d + 1);
+      const float o_ = __ldcg(ac + c), l_ = __ldcg(ac + d);
+      out[((size_t)bh * G + g) * d + c] = l_ > 0.f ? o_ / l_ : 0.f;
+      if (c == 0)
+        lse[(size_t)bh * G + g] =
+            l_ > 0.f ? __ldcg(&wl.refm[(size_t)bh * G + g]) * 0.69314718055994531f + __logf(l_) : -INFINITY;
+    }
+    consumers_sync();  // every accumulator read before any is cleared
+#pragma unroll 1
+    for (int i = tid; i < nq * (d + 1); i += kConsumers) {
+      const int qi = i / (d + 1), c = i - qi * (d + 1), mi = qi / G, g = qi - mi * G;
+      wl.acc[((size_t)s_merge[mi] * G + g) * (d + 1) + c] = 0.f;
+    }
+    // keep only the row-less heads for the slow path
+    consumers_sync();
+    if (tid == 0) {
+      int k = 0;
+      for (int mi = 0; mi < nm; ++mi)
+        if (rp[s_merge[mi] + 1] == rp[s_merge[mi]]) s_merge[k++] = s_merge[mi];
+      s_nmerge = k;
+    }
+    consumers_sync();
+  }
+  const int nm2 = s_nmerge;
   // (merged head, q head) pairs are spread over all 8 warps, so a CTA that
   // closes two heads merges them side by side.  Warp w takes pair
   // w % npr of the round and partials w / npr, + wpp, ...; a head with no rows
   // at all folds its approx list here instead (slow path).
-  const int pairs = nm * G;
+  const int pairs = nm2 * G;
 #pragma unroll 1
   for (int base = 0; base < pairs; base += kWarps) {
     const int npr = min(kWarps, pairs - base);

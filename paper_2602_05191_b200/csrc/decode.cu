@@ -529,6 +529,8 @@ size_t decode_ws_layout(const dp_cache_view* v, int G, WorkLists* wl, void** par
   char* cpre = take((BH + 1) * sizeof(int));
   char* dn = take(sizeof(int));
   char* ap = take(BH * (size_t)G * (4 + (size_t)v->head_dim) * sizeof(float));  // [m, l, -, -, o]
+  char* ac = take(BH * (size_t)G * (1 + (size_t)v->head_dim) * sizeof(float));  // [o, l]
+  char* rm = take(BH * (size_t)G * sizeof(float));
   const size_t pbytes = BH * max_chunks * G * (2 + (size_t)v->head_dim) * acc;
   char* p = take(pbytes);
   if (wl) {
@@ -545,6 +547,8 @@ size_t decode_ws_layout(const dp_cache_view* v, int G, WorkLists* wl, void** par
     wl->chunk_prefix = reinterpret_cast<int*>(cpre);
     wl->done = reinterpret_cast<int*>(dn);
     wl->apart = reinterpret_cast<float*>(ap);
+    wl->acc = reinterpret_cast<float*>(ac);
+    wl->refm = reinterpret_cast<float*>(rm);
     wl->max_chunks = max_chunks;
   }
   if (parts) *parts = p;
@@ -635,10 +639,15 @@ __global__ void __launch_bounds__(256) approx_partial_kernel(dp_cache_view v, in
   const uint8_t* st = state + (size_t)hq * cap;
   __shared__ double red[33];
   __shared__ float part[8][256];
-  double m = -CUDART_INF;
-  for (int k = tid; k < K; k += blockDim.x)
+  double m = -CUDART_INF, mall = -CUDART_INF;
+  for (int k = tid; k < K; k += blockDim.x) {
     if (st[k] == 1) m = fmax(m, x[k]);
+    mall = fmax(mall, x[k]);
+  }
   const double M = block_max(m, red, -CUDART_INF);
+  const double Mall = block_max(mall, red, -CUDART_INF);
+  // reference max of the tensor-core attention's accumulators (log2 units), as dp_plan writes it
+  if (tid == 0) wl.refm[hq] = K > 0 ? (float)(Mall * 1.4426950408889634) : 0.f;
   const float* vbar = v.value_means + (size_t)bh * cap * d;
   float acc[8];
 #pragma unroll

@@ -26,6 +26,8 @@ struct WorkLists {
   int* chunk_prefix;  // [BH+1] exclusive prefix of nchunks over heads (+ total)
   int* done;      // [1] producer-completion counter (zero between launches)
   float* apart;   // [BH][G][4+d] approx pseudo-row partial per q head (m, l, -, -, o[d]); m = -inf: none
+  float* acc;     // [BH][G][d+1] sparse attention accumulators (o[d], l) scaled by 2^-ref (zero between launches)
+  float* refm;    // [BH][G] reference max (log2 units) of those accumulators, written by the plan
   int max_chunks;
 };
 

@@ -707,6 +707,8 @@ __global__ void __launch_bounds__(kPT, 1)
 #pragma unroll 1
     for (int t = tid; t < sw_rows; t += kPT)
       rowidx[t] = tag | (unsigned)(t < v.sink ? t : v.n_tokens - v.window + (t - v.sink));
+    if (tid < G)  // reference max of the attention accumulators: the head's top log-mass (log2 units)
+      wl.refm[(size_t)bh * G + tid] = (float)(s_Mg[tid] * 1.4426950408889634);
     if (tid == 0) {
       const int all_r = tot_r + sw_rows;
       wl.nrows[bh] = all_r;
