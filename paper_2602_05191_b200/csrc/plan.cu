@@ -54,7 +54,8 @@ constexpr int kPlanMaxCap = 4096;
 constexpr int kCh = 128;          // centroid rows per shared-memory tile (P1)
 constexpr int kTileBytes = kCh * 128 * 4;  // one tile: kCh rows x 128 fp32 (4 swizzled column blocks)
 constexpr int kMaxPer = 512;      // clusters per CTA slice (cap 4096 / 8)
-constexpr int kMaxCL = 16;        // cluster size is chosen at launch (<= 16, non-portable above 8)
+constexpr int kMaxCL = 16;
+constexpr int kCandBins = 8;      // stage-2 candidate bins ranked together with the stage-1 bin        // cluster size is chosen at launch (<= 16, non-portable above 8)
 
 // phase timestamps (%globaltimer, ns) of cluster 0: [rank][event]; read with
 // dp_debug_plan_timing() -- profiling aid only
@@ -310,6 +311,9 @@ __global__ void __launch_bounds__(kPT, 1)
   __shared__ unsigned long long s_redu[kPW];
   __shared__ int s_redi[kPW * 4];
   __shared__ SelShared s_sel;
+  __shared__ int s_lo, s_hi, s_bcnt[kCandBins + 1], s_boff[kCandBins + 1];
+  __shared__ unsigned long long s_pre_m[kCandBins];
+  __shared__ int s_pre_c[kCandBins];
 
   asm volatile("griddepcontrol.wait;\n" ::: "memory");  // PDL: inputs of the previous grid are visible
   // let the attention grid become resident on the SMs this launch leaves free
@@ -457,6 +461,15 @@ __global__ void __launch_bounds__(kPT, 1)
     for (int w = 0; w < kPW; ++w) mm = fmax(mm, s_wm[w][tid]);
     remote(cluster, &s_max[0][0], tid)[r * kG + tid] = mm;
   }
+  if (r < G) {  // owners: zero the histogram now (the tile buffers it overlays are consumed)
+    unsigned* hz = reinterpret_cast<unsigned*>(smem + L.hm);
+#pragma unroll
+    for (int j = 0; j < kBinsPT; ++j) {
+      hz[tid * kBinsPT + j] = 0u;
+      hz[kBins + tid * kBinsPT + j] = 0u;
+      reinterpret_cast<int*>(smem + L.hc)[tid * kBinsPT + j] = 0;
+    }
+  }
   stamp(r, 3);
   cl_sync();  // (A) every score is in its owner's shared memory
   stamp(r, 4);
@@ -475,13 +488,6 @@ __global__ void __launch_bounds__(kPT, 1)
     double M = -CUDART_INF;
 #pragma unroll 1
     for (int rr = 0; rr < CL; ++rr) M = fmax(M, s_max[rr][g]);
-#pragma unroll
-    for (int j = 0; j < kBinsPT; ++j) {
-      hmh[tid * kBinsPT + j] = 0u;
-      hml[tid * kBinsPT + j] = 0u;
-      hc[tid * kBinsPT + j] = 0;
-    }
-    __syncthreads();
     stamp(r, 20);
 #pragma unroll 1
     for (int i = tid; i < K; i += kPT) {
@@ -494,8 +500,8 @@ __global__ void __launch_bounds__(kPT, 1)
       if (u) {  // native 32-bit shared atomics (a 64-bit add is a CAS loop)
         atomicAdd(&hmh[b], (unsigned)(u >> 20));
         atomicAdd(&hml[b], (unsigned)(u & 0xFFFFFu));
+        atomicAdd(&hc[b], 1);  // zero-mass members only ever sit at or past the stage-1 bin
       }
-      atomicAdd(&hc[b], 1);
     }
     __syncthreads();
     stamp(r, 21);
@@ -514,61 +520,163 @@ __global__ void __launch_bounds__(kPT, 1)
     int cbase, ctot;
     scan_pair(msum, csum, s_redu, s_redi, mbase, cbase, total, ctot);
     stamp(r, 22);
-    int b1 = kBins, cut1 = 0, n1c = 0, cbefore1 = 0, b2 = kBins, cut2 = 0, n2 = 0;
-    unsigned long long before1 = 0;
+    int cut1 = 0, cbefore1 = 0, n2 = 0;
     if (K > 0) {
-      // stage 1 (selection.py:57-58): crossing of p1 * total, then stage 2
-      // (engine.py:191-194): same order, crossing of p2 * (retained mass)
-      double thr = p1 * (double)total;
-      int limit = kBins;
-#pragma unroll 1
-      for (int stage = 0; stage < 2; ++stage) {
-        const bool inb1 = stage == 1 && !((double)before1 >= thr && cbefore1 > 0);
-        int b, n, cb;
-        unsigned long long base;
-        if (inb1) {  // stage-2 crossing inside bin b1's already-ranked prefix
-          b = b1;
-          n = cut1;
-          base = before1;
-          cb = cbefore1;
-        } else {
-          b = sel_find_bin(&s_sel, bm, bc, mbase, cbase, thr, limit);
-          if (stage == 0) stamp(r, 23);
-          base = s_sel.before;
-          cb = s_sel.cbefore;
-          if (stage == 1)  // bin b1's order is about to be overwritten: emit its states
-#pragma unroll 1
-            for (int j = tid; j < n1c; j += kPT) {
-              const int i = cord[j], rr = i / per;
-              remote(cluster, stl, rr)[g * L.per + (i - rr * per)] = (uint8_t)(j < cut1 ? 1 : 0);
-            }
-          n = sel_rank_bin(&s_sel, binI, lmall, clist, cord, K, b);
-        }
-        const int jj = sel_cut(&s_sel, um, cord, n, base, thr);
-        const int cut = jj < n ? jj + 1 : n;
-        if (stage == 0) {
-          b1 = b;
-          n1c = n;
-          cut1 = cut;
-          before1 = base;
-          cbefore1 = cb;
-          thr = p2 * (double)s_sel.at;  // retained mass (engine.py:191)
-          limit = b1;
-          stamp(r, 11);
-        } else {
-          b2 = b;
-          cut2 = cut;
-          n2 = cb + cut;
-          // boundary-bin members follow their exact rank
-#pragma unroll 1
-          for (int j = tid; j < (inb1 ? n1c : n); j += kPT) {
-            const int i = cord[j], rr = i / per;
-            const int sv = inb1 ? (j < cut2 ? 2 : (j < cut1 ? 1 : 0)) : (j < cut2 ? 2 : 1);
-            remote(cluster, stl, rr)[g * L.per + (i - rr * per)] = (uint8_t)sv;
+      // stage 1 (selection.py:57-58): the bin where the mass crosses p1 * total
+      const double thr1 = p1 * (double)total;
+      const int b1 = sel_find_bin(&s_sel, bm, bc, mbase, cbase, thr1, kBins);  // always found
+      const unsigned long long before1 = s_sel.before;
+      cbefore1 = s_sel.cbefore;
+      stamp(r, 23);
+      // stage 2 (engine.py:191-194) crosses p2 * sub with sub in [before1, before1 + mass(b1)]:
+      // its bin lies in [blo, bhi] (or inside b1), so every candidate bin is ranked in ONE pass
+      const unsigned long long mb1 = ((unsigned long long)hmh[b1] << 20) + hml[b1];
+      if (tid == 0) {
+        s_lo = kBins;
+        s_hi = kBins;
+      }
+      __syncthreads();
+      {
+        const double tlo = p2 * (double)before1, thi = p2 * (double)(before1 + mb1);
+        unsigned long long m = mbase;
+        int hlo = -1, hhi = -1;
+#pragma unroll
+        for (int j = 0; j < kBinsPT; ++j) {
+          const int b = tid * kBinsPT + j;
+          if (b < b1 && bm[j]) {
+            if (hlo < 0 && (double)(m + bm[j]) >= tlo) hlo = b;
+            if (hhi < 0 && (double)(m + bm[j]) >= thi) hhi = b;
           }
+          m += bm[j];
+        }
+        if (hlo >= 0) atomicMin(&s_lo, hlo);
+        if (hhi >= 0) atomicMin(&s_hi, hhi);
+      }
+      __syncthreads();
+      const int blo = s_lo;                              // kBins: every stage-2 crossing is inside b1
+      const int bhi = min(s_hi, b1 - 1);                 // s_hi = kBins: up to the bin before b1
+      const int nrange = blo <= bhi ? bhi - blo + 1 : 0;  // candidate bins below b1
+      const bool wide = nrange > kCandBins;             // rare: fall back to ranking b2 separately
+      const int rlo = wide ? kBins : blo, rhi = wide ? -1 : bhi;
+      {  // exclusive (mass, count) prefix of the candidate range bins
+        unsigned long long m = mbase;
+        int c = cbase;
+#pragma unroll
+        for (int j = 0; j < kBinsPT; ++j) {
+          const int b = tid * kBinsPT + j;
+          if (b >= blo && b < blo + kCandBins) {
+            s_pre_m[b - blo] = m;
+            s_pre_c[b - blo] = c;
+          }
+          m += bm[j];
+          c += bc[j];
         }
       }
+      // compaction: members of b1 and of [rlo, rhi]; per-bin counts -> segment offsets
+      if (tid <= kCandBins) s_bcnt[tid] = 0;
+      if (tid == 0) s_sel.nc = 0;
+      __syncthreads();
+#pragma unroll 1
+      for (int i = tid; i < K; i += kPT) {
+        const int b = binI[i];
+        if (b == b1 || (b >= rlo && b <= rhi)) {
+          clist[atomicAdd(&s_sel.nc, 1)] = i;
+          atomicAdd(&s_bcnt[b == b1 ? kCandBins : b - rlo], 1);
+        }
+      }
+      __syncthreads();
+      if (tid == 0) {  // segment offsets in rank order: range bins ascending, then b1
+        int o = 0;
+        for (int j = 0; j <= kCandBins; ++j) {
+          const int c = s_bcnt[j];
+          s_boff[j] = o;
+          o += c;
+        }
+      }
+      __syncthreads();
+      const int ncand = s_sel.nc;
+#pragma unroll 1
+      for (int a = tid; a < ncand; a += kPT) {  // exact rank (log-mass desc, id asc) within the bin
+        const int ia = clist[a], ba = binI[ia];
+        const double la = lmall[ia];
+        int rk = 0;
+#pragma unroll 1
+        for (int j = 0; j < ncand; ++j) {
+          const int ij = clist[j];
+          if (binI[ij] != ba) continue;
+          const double lj = lmall[ij];
+          rk += lj > la || (lj == la && ij < ia);
+        }
+        cord[s_boff[ba == b1 ? kCandBins : ba - rlo] + rk] = ia;
+      }
+      __syncthreads();
+      const int o1 = s_boff[kCandBins], n1c = s_bcnt[kCandBins];
+      const int j1 = sel_cut(&s_sel, um, cord + o1, n1c, before1, thr1);
+      cut1 = j1 < n1c ? j1 + 1 : n1c;
+      const double thr2 = p2 * (double)s_sel.at;  // retained mass (engine.py:191)
       stamp(r, 13);
+      int b2 = b1, cut2;
+      if ((double)before1 >= thr2 && cbefore1 > 0) {  // crossing strictly below bin b1
+        if (!wide) {
+          // first range bin whose inclusive mass reaches thr2 (it exists: thr2 in [tlo, thi])
+          if (tid == 0) {
+            int bb = bhi;
+            for (int b = blo; b <= bhi; ++b) {
+              const unsigned long long mm = ((unsigned long long)hmh[b] << 20) + hml[b];
+              if (mm && (double)(s_pre_m[b - blo] + mm) >= thr2) {
+                bb = b;
+                break;
+              }
+            }
+            s_lo = bb;
+          }
+          __syncthreads();
+          b2 = s_lo;
+          const int n2c = s_bcnt[b2 - rlo], o2 = s_boff[b2 - rlo];
+          const int j2 = sel_cut(&s_sel, um, cord + o2, n2c, s_pre_m[b2 - blo], thr2);
+          cut2 = j2 < n2c ? j2 + 1 : n2c;
+          n2 = s_pre_c[b2 - blo] + cut2;
+#pragma unroll 1
+          for (int j = tid; j < n2c; j += kPT) {
+            const int i = cord[o2 + j], rr = i / per;
+            remote(cluster, stl, rr)[g * L.per + (i - rr * per)] = (uint8_t)(j < cut2 ? 2 : 1);
+          }
+        } else {  // wide range: rank b2 on its own after emitting b1's states
+          b2 = sel_find_bin(&s_sel, bm, bc, mbase, cbase, thr2, b1);
+          const unsigned long long before2 = s_sel.before;
+          const int cbefore2 = s_sel.cbefore;
+#pragma unroll 1
+          for (int j = tid; j < n1c; j += kPT) {
+            const int i = cord[o1 + j], rr = i / per;
+            remote(cluster, stl, rr)[g * L.per + (i - rr * per)] = (uint8_t)(j < cut1 ? 1 : 0);
+          }
+          __syncthreads();
+          const int n2c = sel_rank_bin(&s_sel, binI, lmall, clist, cord, K, b2);
+          const int j2 = sel_cut(&s_sel, um, cord, n2c, before2, thr2);
+          cut2 = j2 < n2c ? j2 + 1 : n2c;
+          n2 = cbefore2 + cut2;
+#pragma unroll 1
+          for (int j = tid; j < n2c; j += kPT) {
+            const int i = cord[j], rr = i / per;
+            remote(cluster, stl, rr)[g * L.per + (i - rr * per)] = (uint8_t)(j < cut2 ? 2 : 1);
+          }
+        }
+        if (!wide)
+#pragma unroll 1
+          for (int j = tid; j < n1c; j += kPT) {
+            const int i = cord[o1 + j], rr = i / per;
+            remote(cluster, stl, rr)[g * L.per + (i - rr * per)] = (uint8_t)(j < cut1 ? 1 : 0);
+          }
+      } else {  // crossing inside b1's ranked prefix
+        const int j2 = sel_cut(&s_sel, um, cord + o1, cut1, before1, thr2);
+        cut2 = j2 < cut1 ? j2 + 1 : cut1;
+        n2 = cbefore1 + cut2;
+#pragma unroll 1
+        for (int j = tid; j < n1c; j += kPT) {
+          const int i = cord[o1 + j], rr = i / per;
+          remote(cluster, stl, rr)[g * L.per + (i - rr * per)] = (uint8_t)(j < cut2 ? 2 : (j < cut1 ? 1 : 0));
+        }
+      }
       // everything outside the boundary bins: bins < b2 exact, [b2, b1) approx, > b1 dropped
 #pragma unroll 1
       for (int i = tid; i < K; i += kPT) {
@@ -583,6 +691,7 @@ __global__ void __launch_bounds__(kPT, 1)
       counts[2 * hq] = K > 0 ? cbefore1 + cut1 : 0;
       counts[2 * hq + 1] = K > 0 ? n2 : 0;
     }
+    (void)ctot;
     if (tid < CL) remote(cluster, s_Mg, tid)[g] = K > 0 ? M : 0.0;
   }
   stamp(r, 5);
