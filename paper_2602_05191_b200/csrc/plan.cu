@@ -53,7 +53,7 @@ constexpr double kFix = 549755813888.0;  // 2^39 fixed-point scale of e = exp(lm
 constexpr int kPlanMaxCap = 4096;
 constexpr int kCh = 128;          // centroid rows per shared-memory tile (P1)
 constexpr int kTileBytes = kCh * 128 * 4;  // one tile: kCh rows x 128 fp32 (4 swizzled column blocks)
-constexpr int kMaxPer = 512;      // clusters per CTA slice (cap 4096 / 8)
+constexpr int kMaxPer = 1024;     // clusters per CTA slice (cap 4096 / 4)
 constexpr int kMaxCL = 16;
 constexpr int kCandBins = 8;      // stage-2 candidate bins ranked together with the stage-1 bin        // cluster size is chosen at launch (<= 16, non-portable above 8)
 
@@ -915,10 +915,15 @@ static int pick_cl(const dp_cache_view& v, int G) {
   if (g_plan_cl >= 2 && g_plan_cl <= kMaxCL && cl_fits(v, G, g_plan_cl)) return g_plan_cl;
   const int units = v.batch * v.kv_heads;
   const int kG = group_bound(G);
-  for (int cl = kMaxCL; cl > 8; --cl)
+  for (int cl = kMaxCL; cl >= 8; --cl)
     if (cl_fits(v, G, cl) &&
         max_active_clusters(kG, cl, plan_smem_bytes(v.head_dim, v.cluster_cap, cl, kG)) >= units)
       return cl;
+  // more heads than one wave holds: the phases are latency-bound, so a CTA's
+  // time grows slowly with its slice -- the narrowest cluster costs the
+  // fewest SM-microseconds per head
+  for (int cl = max(4, G); cl < 8; ++cl)
+    if (cl_fits(v, G, cl)) return cl;
   return 8;
 }
 

@@ -322,7 +322,7 @@ def test_growth_parity():
         assert O.output_error(out.output, o_out.output) <= 1e-5
 
 
-@pytest.mark.parametrize("cl", [8, 16])
+@pytest.mark.parametrize("cl", [4, 8, 10, 12, 16])
 def test_plan_cluster_sizes_and_multi_tile(cl):
     """The fused plan at both cluster sizes, with slices longer than one
     128-row centroid tile (n = 40K -> ~1250 clusters)."""
