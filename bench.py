@@ -511,6 +511,14 @@ def run_b200(a):
     except Exception:
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    traffic = None  # ncu-measured DRAM bytes per attention launch, when profiled at this workload
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            tj = json.load(f)
+        if a.context == 32768 and a.batch == 1 and a.gqa == 4 and a.kv_heads == 8 and world == 1:
+            traffic = float(tj["attn_tc_kernel_sparse_32k_b1_g4"])
+    except Exception:
+        pass
     peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
     launches = a.steps * L * 2  # plan_kernel (score+select+worklist), attn_tc_kernel (+ fused merge)
     if rank == 0:
@@ -521,7 +529,8 @@ def run_b200(a):
             "data": "synthetic (reference blob law on device, Philox); random-init caches, no checkpoint",
             "config": workload_config(a, world),
             "roofline": {"bound": "hbm", "achieved": attend_gbs, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": attend_gbs / hbm_peak, "traffic": None,
+                         "frac": attend_gbs / hbm_peak, "traffic": traffic,
+                         "traffic_source": "profiles/traffic.json (ncu --set full, dram read+write per launch)",
                          "kernel": "dp_attend = attn_tc_kernel (gathered split-KV attention + fused LSE merge), one launch per layer",
                          "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": float(attend_bytes.mean())},
