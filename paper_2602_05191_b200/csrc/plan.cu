@@ -315,10 +315,11 @@ __global__ void __launch_bounds__(kPT, 1)
   __shared__ unsigned long long s_pre_m[kCandBins];
   __shared__ int s_pre_c[kCandBins];
 
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");  // PDL: inputs of the previous grid are visible
-  // let the attention grid become resident on the SMs this launch leaves free
-  // (its CTAs wait for our completion before reading anything we write)
-  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  // Before griddepcontrol.wait only the cache tables are touched (centroid
+  // tiles, offsets): the previous grid in the stream (the last layer's
+  // attention) never writes them, and anything that does (dp_append_token,
+  // prefill) completed before that grid started.  So the centroid TMA and the
+  // offset loads overlap the previous layer's tail; q and every output wait.
   cl_arrive_relaxed();  // (S) every CTA of the cluster has started before DSMEM is touched
   stamp(r, 0);
 
@@ -362,6 +363,10 @@ __global__ void __launch_bounds__(kPT, 1)
     const int* goffs = v.offs + (size_t)bh * (cap + 1) + k0;
 #pragma unroll 1
     for (int i = tid; i <= nloc; i += kPT) offs[i] = __ldg(&goffs[i]);
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");  // PDL: inputs of the previous grid are visible
+    // let the attention grid become resident on the SMs this launch leaves free
+    // (its CTAs wait for our completion before reading anything we write)
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 #pragma unroll 1
     for (int i = tid; i < 8 * d; i += kPT) {
       const int h = i / d, c = i - h * d;
