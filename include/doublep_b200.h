@@ -149,6 +149,18 @@ int dp_decode_step(const dp_cache_view* v, const void* q, int32_t q_dtype, int32
                    int32_t* counts, float* out, float* lse, int32_t* stats, void* workspace,
                    size_t workspace_bytes, void* stream);
 
+/* Fixed cluster-budget baseline, replaces baseline_cluster_topk
+ * (engine.py:318-338, the RetroInfer-style comparator of PAPER.md:505): the
+ * `budget` clusters with the largest estimated mass are attended exactly
+ * (plus sink and window), every other cluster through its centroid
+ * approximation, under one normaliser.  budget >= 1; a head with fewer
+ * clusters keeps all of them exact.  order [B,Hq,cluster_cap] receives the
+ * full descending cluster order; counts [B,Hq,2] = (clusters, exact). */
+int dp_cluster_topk(const dp_cache_view* v, const void* q, int32_t q_dtype, int32_t gqa_group, double scale,
+                    int32_t budget, double* log_mass, uint8_t* state, int32_t* order, int32_t* counts,
+                    float* out, float* lse, int32_t* stats, void* workspace, size_t workspace_bytes,
+                    void* stream);
+
 /* Dense split-KV flash decoding over all n_tokens rows (the full_attention
  * comparator, engine.py:122-144). */
 int dp_dense_attention(const dp_cache_view* v, const void* q, int32_t q_dtype,

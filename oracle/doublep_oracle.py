@@ -565,6 +565,22 @@ def decode_step(q, keys_h, values_h, tables, p1, p2, sink, window):
     return out, pl, est
 
 
+def cluster_topk(q, keys_h, values_h, tables, budget, sink, window):
+    """Fixed cluster-budget baseline -- `engine.py:318-338`: the `budget`
+    clusters of largest estimated mass exact (plus sink and window), every
+    other cluster approximated, one normaliser."""
+    n = keys_h.shape[0]
+    est = estimate(q, tables, keys_h.shape[1])
+    if not 1 <= budget <= est.probs.size:
+        raise ValueError(f"cluster budget must be in [1, {est.probs.size}], got {budget}")
+    chosen = est.order[:budget]
+    rest = est.order[budget:]
+    tokens = np.concatenate([np.arange(sink, dtype=np.int64), np.arange(n - window, n, dtype=np.int64),
+                             *[tables.members[int(i)] for i in chosen]])
+    tokens.sort()
+    return mixed_attention(q, keys_h, values_h, tables, tokens, rest, est)
+
+
 def full_attention(q, keys_h, values_h):
     """Dense oracle -- `engine.py:122-144`."""
     d = keys_h.shape[1]

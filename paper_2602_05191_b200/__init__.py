@@ -25,6 +25,7 @@ from .engine import (
     SelectionPlan,
     TopPResult,
     build_cache_for_config,
+    cluster_topk_attention,
     decode_step,
     dense_attention,
     estimate_cluster_distribution,
@@ -39,6 +40,6 @@ BACKEND = "b200"
 __all__ = [
     "AttentionOutput", "BACKEND", "ClusterEstimate", "ClusteredCache", "ClusteredLayer", "DecodeWorkspace",
     "DoublePConfig", "KvCache", "PRESETS", "SelectionPlan", "TopPResult", "build_cache_for_config",
-    "build_clustered_cache", "cluster_layer", "decode_step", "default_cluster_count", "dense_attention",
+    "build_clustered_cache", "cluster_layer", "cluster_topk_attention", "decode_step", "default_cluster_count", "dense_attention",
     "estimate_cluster_distribution", "full_attention", "head_seed", "plan_selection", "sparse_attention",
 ]

@@ -70,6 +70,9 @@ _SIGS = {
     "dp_decode_step": (ctypes.c_int, [ctypes.POINTER(CacheView), _vp, ctypes.c_int32, ctypes.c_int32,
                                       ctypes.c_double, ctypes.c_double, ctypes.c_double, _vp, _vp,
                                       _vp, _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp]),
+    "dp_cluster_topk": (ctypes.c_int, [ctypes.POINTER(CacheView), _vp, ctypes.c_int32, ctypes.c_int32,
+                                       ctypes.c_double, ctypes.c_int32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                       ctypes.c_size_t, _vp]),
     "dp_dense_attention": (ctypes.c_int, [ctypes.POINTER(CacheView), _vp, ctypes.c_int32,
                                           ctypes.c_int32, ctypes.c_double, _vp, _vp, _vp,
                                           ctypes.c_size_t, _vp]),

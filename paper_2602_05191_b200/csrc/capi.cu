@@ -149,6 +149,21 @@ int dp_decode_step(const dp_cache_view* v, const void* q, int32_t q_dtype, int32
   return dp_sparse_attention(v, q, q_dtype, G, scale, log_mass, state, out, lse, stats, ws, ws_bytes, stream);
 }
 
+int dp_cluster_topk(const dp_cache_view* v, const void* q, int32_t q_dtype, int32_t G, double scale,
+                    int32_t budget, double* log_mass, uint8_t* state, int32_t* order, int32_t* counts, float* out,
+                    float* lse, int32_t* stats, void* ws, size_t ws_bytes, void* stream) {
+  int r = check_view(v, G);
+  if (r) return r;
+  if (budget < 1) return fail(DP_ERR_INVALID, "cluster budget must be >= 1");
+  if (!log_mass || !state || !order) return fail(DP_ERR_INVALID, "log_mass, state and order are required");
+  if ((r = dp_score(v, q, q_dtype, G, scale, log_mass, stream))) return r;
+  if ((r = dp_select(v, G, 1.0, 1.0, log_mass, state, counts, order, nullptr, nullptr, ws, ws_bytes, stream)))
+    return r;
+  cudaError_t e = dp::launch_topk_state(*v, G, budget, order, state, counts, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "dp_cluster_topk");
+  return dp_sparse_attention(v, q, q_dtype, G, scale, log_mass, state, out, lse, stats, ws, ws_bytes, stream);
+}
+
 int dp_dense_attention(const dp_cache_view* v, const void* q, int32_t q_dtype, int32_t G, double scale,
                        float* out, float* lse, void* ws, size_t ws_bytes, void* stream) {
   int r = check_view(v, G);

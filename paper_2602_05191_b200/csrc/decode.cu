@@ -580,6 +580,30 @@ cudaError_t launch_score(const dp_cache_view& v, const void* q, int qdt, int G, 
   return cudaGetLastError();
 }
 
+// Fixed cluster-budget baseline (engine.py:318-338, RetroInfer-style): the
+// `budget` clusters of largest estimated mass (the select kernel's full
+// descending order) are exact, every other cluster is approximated; nothing
+// is dropped.  Heads with fewer clusters keep all of them exact.
+__global__ void __launch_bounds__(256) topk_state_kernel(dp_cache_view v, int G, int budget,
+                                                         const int* __restrict__ order, uint8_t* __restrict__ state,
+                                                         int* __restrict__ counts) {
+  const int hq = blockIdx.x, bh = hq / G;
+  const int K = v.nclusters[bh], cap = v.cluster_cap;
+  const int k = budget < K ? budget : K;
+  for (int i = threadIdx.x; i < K; i += blockDim.x)
+    state[(size_t)hq * cap + order[(size_t)hq * cap + i]] = (uint8_t)(i < k ? 2 : 1);
+  if (threadIdx.x == 0 && counts) {
+    counts[2 * hq] = K;
+    counts[2 * hq + 1] = k;
+  }
+}
+
+cudaError_t launch_topk_state(const dp_cache_view& v, int G, int budget, const int* order, uint8_t* state,
+                              int* counts, cudaStream_t st) {
+  topk_state_kernel<<<v.batch * v.kv_heads * G, 256, 0, st>>>(v, G, budget, order, state, counts);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_select(const dp_cache_view& v, int G, double p1, double p2, const double* lm,
                           uint8_t* state, int* counts, int* order, double* cum, double* probs,
                           cudaStream_t st) {

@@ -74,6 +74,8 @@ cudaError_t launch_attn_tc(const dp_cache_view& v, const void* q, int qdt, int G
 cudaError_t launch_plan(const dp_cache_view& v, const void* q, int qdt, int G, double scale, double p1, double p2,
                         double* lm, uint8_t* state, int* counts, int* stats, void* ws, cudaStream_t st);
 bool plan_supported(const dp_cache_view& v, int G);
+cudaError_t launch_topk_state(const dp_cache_view& v, int G, int budget, const int* order, uint8_t* state,
+                              int* counts, cudaStream_t st);
 cudaError_t launch_append(const dp_cache_view& v, const void* nk, const void* nv, cudaStream_t st);
 
 }  // namespace dp

@@ -124,6 +124,27 @@ def _sparse_layer(q, layer, p1=0.95, p2=0.7, *, workspace=None, return_plan=Fals
     return (ws.out, ws) if return_plan else ws.out
 
 
+def cluster_topk_attention(q, layer, budget, *, workspace=None, stream=None, scale=None, return_plan=False):
+    """Fixed cluster-budget baseline on the device (baseline_cluster_topk,
+    engine.py:318-338): the `budget` clusters of largest estimated mass are
+    exact, every other cluster is approximated -- the RetroInfer-style
+    comparator of PAPER.md:505.  Returns out fp32 [B,Hq,d] (and the
+    workspace with log_mass/state/order/counts if return_plan)."""
+    if int(budget) < 1:
+        raise ValueError(f"cluster budget must be >= 1, got {budget}")
+    G = _group(q, layer)
+    ws = workspace if workspace is not None and workspace.fits(layer, G) else DecodeWorkspace(layer, G)
+    if getattr(ws, "order", None) is None:
+        ws.order = torch.zeros(ws.state.shape, dtype=torch.int32, device=ws.state.device)
+    q = q.contiguous()
+    sc = 1.0 / math.sqrt(layer.head_dim) if scale is None else scale
+    N.check(N.lib().dp_cluster_topk(
+        layer.view(), N.ptr(q), dtype_code(q), G, sc, int(budget), N.ptr(ws.log_mass), N.ptr(ws.state),
+        N.ptr(ws.order), N.ptr(ws.counts), N.ptr(ws.out), N.ptr(ws.lse), N.ptr(ws.stats), N.ptr(ws.ws),
+        ws.ws.numel(), _stream(layer, stream)))
+    return (ws.out, ws) if return_plan else ws.out
+
+
 def dense_attention(q, layer, *, workspace=None, stream=None, scale=None, return_lse=False):
     """Dense split-KV flash decoding over every cached row (full_attention,
     engine.py:122-144) -- the comparator the sparse step must beat."""

@@ -378,3 +378,27 @@ def test_sequence_sharded_merge_on_gpu():
     out, _ = lse_merge(torch.stack([oa, ob.clone()]), torch.stack([la, lb.clone()]))
     err = ((out - ref).norm(dim=-1) / ref.norm(dim=-1)).max().item()
     assert err <= 1e-4, err
+
+
+@pytest.mark.parametrize("budget", [1, 7, 40])
+def test_cluster_topk_baseline_parity(budget):
+    """GPU fixed cluster-budget baseline (engine.py:318-338) vs the oracle fed
+    the GPU's tables."""
+    from paper_2602_05191_b200 import cluster_topk_attention
+
+    spec, keys, values, queries = _workload(2048, 128, 2, 4, "peaked", 13)
+    for dtype in (torch.float32, torch.bfloat16):
+        layer, kd, vd = _layer(keys, values, dtype)
+        q = _to_dev(queries[0, 0], dtype).unsqueeze(0)
+        out, ws = cluster_topk_attention(q, layer, budget, return_plan=True)
+        out = out[0].double().cpu().numpy()
+        kf = kd[0].double().cpu().numpy()
+        vf = vd[0].double().cpu().numpy()
+        for hq in range(8):
+            h = hq // 4
+            t = oracle_tables(layer, 0, h)
+            K = len(t.members)
+            ref = O.cluster_topk(q[0, hq].double().cpu().numpy(), kf[h], vf[h], t, min(budget, K), layer.sink,
+                                 layer.window)
+            assert int(ws.counts[0, hq, 1]) == min(budget, K)
+            assert O.output_error(out[hq], ref.output) <= TOL[dtype], (hq, budget)
