@@ -402,3 +402,38 @@ def test_cluster_topk_baseline_parity(budget):
                                  layer.window)
             assert int(ws.counts[0, hq, 1]) == min(budget, K)
             assert O.output_error(out[hq], ref.output) <= TOL[dtype], (hq, budget)
+
+
+@pytest.mark.parametrize("G", [3, 4])
+def test_batched_sequences_parity(G):
+    """Batch > 1 (config 3 layout): two sequences with different caches in one
+    layer, one decode step; every (sequence, q head) against the oracle fed
+    that sequence's GPU tables.  G = 3 exercises a non-power-of-two group."""
+    from paper_2602_05191_b200 import cluster_layer, sparse_attention
+
+    B, H, n, d = 2, 2, 1500, 128
+    ks, vs, qs = [], [], []
+    for b in range(B):
+        spec, keys, values, queries = _workload(n, d, H, G, "peaked", 20 + b)
+        ks.append(keys[0])
+        vs.append(values[0])
+        qs.append(queries[0, 0])
+    kd = _to_dev(np.stack(ks), torch.bfloat16)  # [B,H,N,d]
+    vd = _to_dev(np.stack(vs), torch.bfloat16)
+    q = _to_dev(np.stack(qs), torch.bfloat16)    # [B,Hq,d]
+    layer = cluster_layer(kd, vd, fp64_assign=False)
+    out, ws = sparse_attention(q, layer, 0.95, 0.7, return_plan=True)
+    out = out.double().cpu().numpy()
+    st = ws.state.cpu().numpy()
+    for b in range(B):
+        kf = kd[b].double().cpu().numpy()
+        vf = vd[b].double().cpu().numpy()
+        for hq in range(H * G):
+            h = hq // G
+            t = oracle_tables(layer, b, h)
+            o_out, o_plan, o_est = O.decode_step(q[b, hq].double().cpu().numpy(), kf[h], vf[h], t, 0.95, 0.7,
+                                                 layer.sink, layer.window)
+            c1, c2 = classify_sets(o_est, o_plan, st[b, hq], 0.95, 0.7)
+            assert c1 != "real" and c2 != "real", (b, hq, c1, c2)
+            if c1 == "exact" and c2 == "exact":
+                assert O.output_error(out[b, hq], o_out.output) <= TOL[torch.bfloat16], (b, hq)
