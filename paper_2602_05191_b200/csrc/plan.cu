@@ -136,7 +136,9 @@ __device__ __forceinline__ T* remote(cg::cluster_group& c, T* p, int rank) {
 }
 
 // block-wide exclusive scan of (mass u64, count int) pairs; totals to mt / ct.
-// Callers separate consecutive uses with a barrier (sm/sc are reused).
+// Warp scans, then warp 0 scans the 16 warp totals (so no thread reads all
+// of them).  sm/sc need 2 * kPW + 1 slots; callers separate consecutive uses
+// with a barrier.
 __device__ __forceinline__ void scan_pair(unsigned long long m, int c, unsigned long long* sm, int* sc,
                                           unsigned long long& mex, int& cex, unsigned long long& mt, int& ct) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -156,23 +158,34 @@ __device__ __forceinline__ void scan_pair(unsigned long long m, int c, unsigned 
     sc[warp] = ci;
   }
   __syncthreads();
-  unsigned long long wb = 0, wt = 0;
-  int cb = 0, cbt = 0;
+  if (warp == 0) {
+    const unsigned long long wv = lane < kPW ? sm[lane] : 0ull;
+    const int wc = lane < kPW ? sc[lane] : 0;
+    unsigned long long wi = wv;
+    int wci = wc;
 #pragma unroll
-  for (int w = 0; w < kPW; ++w) {
-    const unsigned long long a = sm[w];
-    const int b = sc[w];
-    if (w < warp) {
-      wb += a;
-      cb += b;
+    for (int o = 1; o < kPW; o <<= 1) {
+      const unsigned long long tm = __shfl_up_sync(0xffffffffu, wi, o);
+      const int tc = __shfl_up_sync(0xffffffffu, wci, o);
+      if (lane >= o) {
+        wi += tm;
+        wci += tc;
+      }
     }
-    wt += a;
-    cbt += b;
+    if (lane < kPW) {
+      sm[kPW + lane] = wi - wv;
+      sc[kPW + lane] = wci - wc;
+    }
+    if (lane == kPW - 1) {
+      sm[2 * kPW] = wi;
+      sc[2 * kPW] = wci;
+    }
   }
-  mex = wb + mi - m;
-  cex = cb + ci - c;
-  mt = wt;
-  ct = cbt;
+  __syncthreads();
+  mex = sm[kPW + warp] + mi - m;
+  cex = sc[kPW + warp] + ci - c;
+  mt = sm[2 * kPW];
+  ct = sc[2 * kPW];
 }
 
 // ---------------------------------------------------------------------------
@@ -308,7 +321,7 @@ __global__ void __launch_bounds__(kPT, 1)
   __shared__ int s_cnt[kMaxCL][4];      // pushed slice counts (rows, exact clusters, approx clusters)
   __shared__ double s_Mg[kG];           // pushed head maxima (every CTA)
   __shared__ double s_wm[kPW][kG];
-  __shared__ unsigned long long s_redu[kPW];
+  __shared__ unsigned long long s_redu[2 * kPW + 1];
   __shared__ int s_redi[kPW * 4];
   __shared__ SelShared s_sel;
   __shared__ int s_lo, s_hi, s_bcnt[kCandBins + 1], s_boff[kCandBins + 1];
