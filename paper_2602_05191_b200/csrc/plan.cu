@@ -83,7 +83,7 @@ __device__ __forceinline__ void cl_sync() {
 struct PlanLayout {
   int per;                 // centroid rows per CTA (capacity)
   size_t cs;               // P1: [per][d + 4] fp32 centroid slice | P2 (owners): select arrays | P3 scratch
-  size_t um, bin, hm, hc, clist, cord;  // P2 arrays (inside the cs region)
+  size_t um, bin, hm, hc, clist, cord, stown;  // P2 arrays (inside the cs region)
   size_t lmall;            // [cap] fp64 log-masses of my head (owners; pushed by every CTA)
   size_t lml;              // [kG][per] fp64 log-masses of my slice
   size_t qd;               // [8][d + 4] fp64 queries (padded rows)
@@ -94,7 +94,7 @@ struct PlanLayout {
 
 __host__ __device__ inline PlanLayout plan_layout(int CL, int kG, int d, int cap) {
   PlanLayout L;
-  L.per = (cap + CL - 1) / CL;
+  L.per = ((cap + CL - 1) / CL + 3) & ~3;  // multiple of 4: states travel as packed words
   size_t o = 0;
   auto take = [&](size_t bytes) {
     const size_t r = o;
@@ -113,10 +113,11 @@ __host__ __device__ inline PlanLayout plan_layout(int CL, int kG, int d, int cap
   L.hc = take2((size_t)kBins * 4);
   L.clist = take2((size_t)cap * 4);
   L.cord = take2((size_t)cap * 4);
+  L.stown = take2((size_t)cap + 4);
   const size_t csb = (size_t)2 * kTileBytes;  // two TMA tiles (128B swizzle) to d + 4 floats (conflict-free A loads)
   const size_t big = csb > p2 ? csb : p2;
   L.cs = take(big);
-  L.um += L.cs; L.bin += L.cs; L.hm += L.cs; L.hc += L.cs; L.clist += L.cs; L.cord += L.cs;
+  L.um += L.cs; L.bin += L.cs; L.hm += L.cs; L.hc += L.cs; L.clist += L.cs; L.cord += L.cs; L.stown += L.cs;
   L.lmall = take((size_t)cap * 8);
   L.lml = take((size_t)kG * L.per * 8);
   L.qd = take((size_t)8 * (d + 4) * 8);
@@ -337,7 +338,7 @@ __global__ void __launch_bounds__(kPT, 1)
   stamp(r, 0);
 
   const int K = __ldg(&v.nclusters[bh]);
-  const int per = (K + CL - 1) / CL;
+  const int per = ((K + CL - 1) / CL + 3) & ~3;
   const int k0 = min(K, r * per);
   const int nloc = max(0, min(per, K - k0));
 
@@ -497,6 +498,7 @@ __global__ void __launch_bounds__(kPT, 1)
     const int g = r;
     const int hq = bh * G + g;
     unsigned long long* um = reinterpret_cast<unsigned long long*>(smem + L.um);
+    uint8_t* stown = reinterpret_cast<uint8_t*>(smem + L.stown);  // this head's states, then packed out
     uint16_t* binI = reinterpret_cast<uint16_t*>(smem + L.bin);
     unsigned* hmh = reinterpret_cast<unsigned*>(smem + L.hm);  // [kBins] high 19 bits of the mass
     unsigned* hml = hmh + kBins;                               // [kBins] low 20 bits
@@ -656,8 +658,8 @@ __global__ void __launch_bounds__(kPT, 1)
           n2 = s_pre_c[b2 - blo] + cut2;
 #pragma unroll 1
           for (int j = tid; j < n2c; j += kPT) {
-            const int i = cord[o2 + j], rr = i / per;
-            remote(cluster, stl, rr)[g * L.per + (i - rr * per)] = (uint8_t)(j < cut2 ? 2 : 1);
+            const int i = cord[o2 + j];
+            stown[i] = (uint8_t)(j < cut2 ? 2 : 1);
           }
         } else {  // wide range: rank b2 on its own after emitting b1's states
           b2 = sel_find_bin(&s_sel, bm, bc, mbase, cbase, thr2, b1);
@@ -665,8 +667,8 @@ __global__ void __launch_bounds__(kPT, 1)
           const int cbefore2 = s_sel.cbefore;
 #pragma unroll 1
           for (int j = tid; j < n1c; j += kPT) {
-            const int i = cord[o1 + j], rr = i / per;
-            remote(cluster, stl, rr)[g * L.per + (i - rr * per)] = (uint8_t)(j < cut1 ? 1 : 0);
+            const int i = cord[o1 + j];
+            stown[i] = (uint8_t)(j < cut1 ? 1 : 0);
           }
           __syncthreads();
           const int n2c = sel_rank_bin(&s_sel, binI, lmall, clist, cord, K, b2);
@@ -675,15 +677,15 @@ __global__ void __launch_bounds__(kPT, 1)
           n2 = cbefore2 + cut2;
 #pragma unroll 1
           for (int j = tid; j < n2c; j += kPT) {
-            const int i = cord[j], rr = i / per;
-            remote(cluster, stl, rr)[g * L.per + (i - rr * per)] = (uint8_t)(j < cut2 ? 2 : 1);
+            const int i = cord[j];
+            stown[i] = (uint8_t)(j < cut2 ? 2 : 1);
           }
         }
         if (!wide)
 #pragma unroll 1
           for (int j = tid; j < n1c; j += kPT) {
-            const int i = cord[o1 + j], rr = i / per;
-            remote(cluster, stl, rr)[g * L.per + (i - rr * per)] = (uint8_t)(j < cut1 ? 1 : 0);
+            const int i = cord[o1 + j];
+            stown[i] = (uint8_t)(j < cut1 ? 1 : 0);
           }
       } else {  // crossing inside b1's ranked prefix
         const int j2 = sel_cut(&s_sel, um, cord + o1, cut1, before1, thr2);
@@ -691,8 +693,8 @@ __global__ void __launch_bounds__(kPT, 1)
         n2 = cbefore1 + cut2;
 #pragma unroll 1
         for (int j = tid; j < n1c; j += kPT) {
-          const int i = cord[o1 + j], rr = i / per;
-          remote(cluster, stl, rr)[g * L.per + (i - rr * per)] = (uint8_t)(j < cut2 ? 2 : (j < cut1 ? 1 : 0));
+          const int i = cord[o1 + j];
+          stown[i] = (uint8_t)(j < cut2 ? 2 : (j < cut1 ? 1 : 0));
         }
       }
       // everything outside the boundary bins: bins < b2 exact, [b2, b1) approx, > b1 dropped
@@ -700,9 +702,19 @@ __global__ void __launch_bounds__(kPT, 1)
       for (int i = tid; i < K; i += kPT) {
         const int b = binI[i];
         if (b != b1 && b != b2) {
-          const int rr = i / per;
-          remote(cluster, stl, rr)[g * L.per + (i - rr * per)] = (uint8_t)(b < b2 ? 2 : (b < b1 ? 1 : 0));
+          stown[i] = (uint8_t)(b < b2 ? 2 : (b < b1 ? 1 : 0));
         }
+      }
+      __syncthreads();
+      // states travel to the slice owners as packed 4-byte words (slices are 4-aligned)
+#pragma unroll 1
+      for (int i = 4 * tid; i < K; i += 4 * kPT) {
+        unsigned w = 0;
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+          if (i + t < K) w |= (unsigned)stown[i + t] << (8 * t);
+        const int rr = i / per;
+        *reinterpret_cast<unsigned*>(remote(cluster, stl, rr) + g * L.per + (i - rr * per)) = w;
       }
     }
     if (tid == 0) {
