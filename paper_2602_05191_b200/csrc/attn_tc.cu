@@ -207,7 +207,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   // PDL: everything above overlapped the plan kernel's tail; its outputs
-  // (row lists, counts, approx partials) are visible after the wait
+  // (row lists, counts, approx lists) are visible after the wait.  q is not
+  // written by the plan and its producers finished before the plan started,
+  // so it is pulled into L2 now (load_q then hits L2 on the critical path).
+  {
+    const size_t qbytes = (size_t)BH * G * d * (kQF32 ? 4 : 2);
+    const char* qc = reinterpret_cast<const char*>(q);
+    for (size_t off = (size_t)tid * 128; off < qbytes; off += (size_t)kTcThreads * 128)
+      asm volatile("prefetch.global.L2 [%0];\n" ::"l"(qc + off));
+  }
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
   // ---- row prefix over heads (warp 0, 32 heads per step) ------------------

@@ -381,6 +381,13 @@ __global__ void __launch_bounds__(kPT, 1)
     // let the attention grid become resident on the SMs this launch leaves free
     // (its CTAs wait for our completion before reading anything we write)
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    if (r == 0) {  // sink and window rows open every head's union list (plan-independent)
+      const unsigned tag = (unsigned)((1 << G) - 1) << 24;
+      unsigned* rw = reinterpret_cast<unsigned*>(wl.rowidx) + (size_t)bh * v.row_cap;
+#pragma unroll 1
+      for (int t = tid; t < v.sink + v.window; t += kPT)
+        rw[t] = tag | (unsigned)(t < v.sink ? t : v.n_tokens - v.window + (t - v.sink));
+    }
 #pragma unroll 1
     for (int i = tid; i < 8 * d; i += kPT) {
       const int h = i / d, c = i - h * d;
@@ -842,10 +849,6 @@ __global__ void __launch_bounds__(kPT, 1)
     __syncthreads();  // s_redu / s_redi reuse
   }
   if (r == 0) {
-    const unsigned tag = (unsigned)((1 << G) - 1) << 24;
-#pragma unroll 1
-    for (int t = tid; t < sw_rows; t += kPT)
-      rowidx[t] = tag | (unsigned)(t < v.sink ? t : v.n_tokens - v.window + (t - v.sink));
     if (tid < G)  // reference max of the attention accumulators: the head's top log-mass (log2 units)
       wl.refm[(size_t)bh * G + tid] = (float)(s_Mg[tid] * 1.4426950408889634);
     if (tid == 0) {
