@@ -284,6 +284,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
       if (w.more()) nr_nx = fetch(w, e_nx, bh_nx);
       if (idx >= kStages) mbar_wait(smem_u32(&empty_bar[s]), (unsigned)(((idx / kStages) + 1) & 1));
       rmask[s * kTcRows + pr0 + lane] = e == 0xFFFFFFFFu ? 0 : (int)(e >> 24);
+      if (idx == 0 && warp == kWarps && lane == 0 && blockIdx.x < 512) {  // profiling: first row entries in hand
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t) : "r"(e));
+        g_attn_ts[blockIdx.x][9] = t;
+      }
       const size_t head_off = (size_t)bh * v.row_cap * d;
       const __nv_bfloat16* Kg = reinterpret_cast<const __nv_bfloat16*>(v.keys) + head_off;
       const __nv_bfloat16* Vg = reinterpret_cast<const __nv_bfloat16*>(v.values) + head_off;
@@ -305,6 +310,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
           cp16_zero(kd, Kg);
           cp16_zero(vd, Vg);
         }
+      }
+      if (idx == 0 && warp == kWarps && lane == 0 && blockIdx.x < 512) {  // profiling: first tile issued
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_attn_ts[blockIdx.x][10] = t;
       }
       cp_async_arrive(smem_u32(&full_bar[s]));  // completes when this lane's copies land
       __syncwarp();

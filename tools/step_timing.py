@@ -109,7 +109,7 @@ timed(lambda: [(plan(j), attend(j)) for j in range(L)], reps=1)
 abuf = (ctypes.c_ulonglong * (512 * 12))()
 lib.dp_debug_attn_timing(ctypes.cast(abuf, ctypes.c_void_p))
 a = np.array(abuf[:], dtype=np.float64).reshape(512, 12)[:148]
-rows = a[:, 7].copy(); segs = a[:, 8].copy(); a = a[:, :7]
+rows = a[:, 7].copy(); segs = a[:, 8].copy(); pe = a[:, 9].copy(); pi = a[:, 10].copy(); a = a[:, :7]
 a0 = a[:, 0].min()
 rel = (a - a0) / 1e3
 print("attn phases of the last step (us, rel. to first CTA start): start, prefix, first data, loop done, flushed, exit")
@@ -119,6 +119,9 @@ for name, col in (("start", 0), ("prefix", 1), ("data0", 2), ("loop", 3), ("flus
     x = x[(x > -1e6) & (x < 1e6)]
     if x.size:
         print(f"  {name:7s} min {x.min():7.2f} med {np.median(x):7.2f} max {x.max():7.2f}  (n={x.size})")
+pe_rel = (pe - a0) / 1e3
+pi_rel = (pi - a0) / 1e3
+print(f"  producer: first row entries med {np.median(pe_rel):.2f}, first tile issued med {np.median(pi_rel):.2f}")
 loop_end = rel[:, 3] - rel[:, 2]
 for sg in (1, 2):
     sel = segs == sg
