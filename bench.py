@@ -296,7 +296,10 @@ def _measure(a, context, L, dev, world, rank, sampler=None):
             lay._prefill_k = big._prefill_k
             layers.append(lay)
 
-    wss = [DecodeWorkspace(lay, G) for lay in layers]
+    # one workspace reused by every layer, as a serving engine holds it (all
+    # layers share the geometry; each plan waits for the previous attention)
+    ws0 = DecodeWorkspace(layers[0], G)
+    wss = [ws0] * L
     views = [lay.view() for lay in layers]
     scale = 1.0 / math.sqrt(d)
 

@@ -34,6 +34,8 @@ big = cluster_layer(ks, vs, fp64_assign=False)
 del ks, vs
 layers = big.split()
 wss = [DecodeWorkspace(lay, G) for lay in layers]
+if os.environ.get("DP_SHARED_WS"):  # one workspace reused by every layer (a serving engine's layout)
+    wss = [wss[0]] * L
 views = [lay.view() for lay in layers]
 lib = N.lib()
 sc = 1.0 / math.sqrt(d)
