@@ -15,6 +15,7 @@ int fail(int code, const std::string& msg) {
   return code;
 }
 int cuda_fail(cudaError_t e, const char* where) {
+  cudaGetLastError();  // a failed launch must not leave its (non-sticky) error for the caller's next CUDA call
   return fail(DP_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
 

@@ -300,7 +300,7 @@ template <int kG>
 __global__ void __launch_bounds__(kPT, 1)
     plan_kernel(const __grid_constant__ CUtensorMap tmC, dp_cache_view v, const void* __restrict__ q, int qdt, int G,
                 double scale, double p1, double p2, double* __restrict__ lm_out, uint8_t* __restrict__ state_out,
-                int* __restrict__ counts, WorkLists wl, int CL) {
+                int* __restrict__ counts, WorkLists wl, int CL, int boxr) {
   cg::cluster_group cluster = cg::this_cluster();
   const int r = (int)cluster.block_rank();
   const int bh = blockIdx.x / CL;
@@ -362,7 +362,7 @@ __global__ void __launch_bounds__(kPT, 1)
     if (tid == 0) {
       const unsigned b = bar0 + (unsigned)(t & 1) * 8;
       const unsigned dst = (unsigned)__cvta_generic_to_shared(Cs) + (unsigned)(t & 1) * kTileBytes;
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(b), "r"((unsigned)(ncb * kCh * 128))
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(b), "r"((unsigned)(ncb * boxr * 128))
                    : "memory");
 #pragma unroll 1
       for (int cb = 0; cb < ncb; ++cb)
@@ -458,7 +458,7 @@ __global__ void __launch_bounds__(kPT, 1)
         const unsigned b = bar0 + (unsigned)(t & 1) * 8;
         const unsigned dst = (unsigned)__cvta_generic_to_shared(Cs) + (unsigned)(t & 1) * kTileBytes;
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(b),
-                     "r"((unsigned)(ncb * kCh * 128))
+                     "r"((unsigned)(ncb * boxr * 128))
                      : "memory");
 #pragma unroll 1
         for (int cb = 0; cb < ncb; ++cb)
@@ -887,7 +887,8 @@ static cudaError_t centroid_tmap(const dp_cache_view& v, CUtensorMap* m) {
   }
   const cuuint64_t dims[2] = {(cuuint64_t)v.head_dim, (cuuint64_t)v.batch * v.kv_heads * v.cluster_cap};
   const cuuint64_t strides[1] = {(cuuint64_t)v.head_dim * 4};
-  const cuuint32_t box[2] = {32, (cuuint32_t)kCh};
+  const cuuint64_t rows = (cuuint64_t)v.batch * v.kv_heads * v.cluster_cap;
+  const cuuint32_t box[2] = {32, (cuuint32_t)(rows < (cuuint64_t)kCh ? rows : kCh)};  // a box may not exceed the tensor
   const cuuint32_t es[2] = {1, 1};
   const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(v.centroids), dims, strides, box, es,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -905,14 +906,25 @@ static void* plan_fn_for(int kG) {
   return kG == 1 ? plan_fn<1>() : kG == 2 ? plan_fn<2>() : kG == 4 ? plan_fn<4>() : plan_fn<8>();
 }
 
+// the kernel's dynamic shared-memory limit only ever grows (the occupancy
+// queries below and the launches share it; lowering it for a query would
+// make a later, larger launch fail)
+static void ensure_smem_attr(int kG, size_t smem) {
+  static size_t cur[9] = {};
+  if (cur[kG] >= smem) return;
+  void* fn = plan_fn_for(kG);
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cur[kG] = smem;
+}
+
 // co-resident clusters of size cl at this shared-memory footprint
 static int max_active_clusters(int kG, int cl, size_t smem) {
   static int cache[9][17] = {};
   static size_t cache_smem[9][17] = {};
   if (cache_smem[kG][cl] == smem) return cache[kG][cl];
   void* fn = plan_fn_for(kG);
-  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  ensure_smem_attr(kG, smem);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)cl);
   cfg.blockDim = dim3(kPT);
@@ -974,13 +986,7 @@ cudaError_t launch_plan(const dp_cache_view& v, const void* q, int qdt, int G, d
   const int kG = group_bound(G);
   const int CL = pick_cl(v, G);
   const size_t smem = plan_smem_bytes(v.head_dim, v.cluster_cap, CL, kG);
-  void* fn = plan_fn_for(kG);
-  static size_t attr[9] = {};
-  if (attr[kG] < smem) {
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    attr[kG] = smem;
-  }
+  ensure_smem_attr(kG, smem);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(v.batch * v.kv_heads * CL));
   cfg.blockDim = dim3(kPT);
@@ -998,11 +1004,13 @@ cudaError_t launch_plan(const dp_cache_view& v, const void* q, int qdt, int G, d
   CUtensorMap tm;
   const cudaError_t e = centroid_tmap(v, &tm);
   if (e != cudaSuccess) return e;
+  const long long rows = (long long)v.batch * v.kv_heads * v.cluster_cap;
+  const int boxr = rows < kCh ? (int)rows : kCh;  // rows per TMA box (the tile is never fuller than that)
   switch (kG) {
-    case 1: return cudaLaunchKernelEx(&cfg, plan_kernel<1>, tm, v, q, qdt, G, scale, p1, p2, lm, state, counts, wl, CL);
-    case 2: return cudaLaunchKernelEx(&cfg, plan_kernel<2>, tm, v, q, qdt, G, scale, p1, p2, lm, state, counts, wl, CL);
-    case 4: return cudaLaunchKernelEx(&cfg, plan_kernel<4>, tm, v, q, qdt, G, scale, p1, p2, lm, state, counts, wl, CL);
-    default: return cudaLaunchKernelEx(&cfg, plan_kernel<8>, tm, v, q, qdt, G, scale, p1, p2, lm, state, counts, wl, CL);
+    case 1: return cudaLaunchKernelEx(&cfg, plan_kernel<1>, tm, v, q, qdt, G, scale, p1, p2, lm, state, counts, wl, CL, boxr);
+    case 2: return cudaLaunchKernelEx(&cfg, plan_kernel<2>, tm, v, q, qdt, G, scale, p1, p2, lm, state, counts, wl, CL, boxr);
+    case 4: return cudaLaunchKernelEx(&cfg, plan_kernel<4>, tm, v, q, qdt, G, scale, p1, p2, lm, state, counts, wl, CL, boxr);
+    default: return cudaLaunchKernelEx(&cfg, plan_kernel<8>, tm, v, q, qdt, G, scale, p1, p2, lm, state, counts, wl, CL, boxr);
   }
 }
 
