@@ -37,7 +37,7 @@ def main():
     worst = {torch.float32: 0.0, torch.bfloat16: 0.0}
     t0 = time.time()
     for c in range(cases):
-        n = int(rng.choice([300, 700, 1500, 3000, 6000, 12000]))
+        n = int(rng.choice([300, 700, 1500, 3000, 6000, 12000, 24000, 40000]))
         H = int(rng.choice([1, 2, 3]))
         G = int(rng.choice([1, 2, 3, 4, 6, 8]))
         d = int(rng.choice([32, 64, 128, 128]))
