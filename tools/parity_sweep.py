@@ -47,15 +47,22 @@ def main():
         p2 = float(rng.choice([0.3, 0.7, 0.8, 0.95, 1.0]))
         cl = int(rng.choice([0, 0, 4, 8, 12, 16]))
         seed = int(rng.integers(1 << 30))
-        spec = O.WorkloadSpec(context_len=n, head_dim=d, num_kv_heads=H, gqa_group=G, num_steps=1,
-                              tail_profile=prof, seed=seed)
-        keys, values, queries = O.generate(spec)
-        kd = torch.from_numpy(np.ascontiguousarray(keys[0])).cuda().to(dtype).unsqueeze(0)
-        vd = torch.from_numpy(np.ascontiguousarray(values[0])).cuda().to(dtype).unsqueeze(0)
-        q = torch.from_numpy(np.ascontiguousarray(queries[0, 0])).cuda().to(dtype).unsqueeze(0)
+        B = int(rng.choice([1, 1, 2, 3]))
+        qdt = torch.float32 if rng.random() < 0.3 else dtype  # fp32 queries over bf16 caches too
+        ks, vs, qs = [], [], []
+        for b in range(B):
+            spec = O.WorkloadSpec(context_len=n, head_dim=d, num_kv_heads=H, gqa_group=G, num_steps=1,
+                                  tail_profile=prof, seed=seed + b)
+            keys, values, queries = O.generate(spec)
+            ks.append(keys[0])
+            vs.append(values[0])
+            qs.append(queries[0, 0])
+        kd = torch.from_numpy(np.ascontiguousarray(np.stack(ks))).cuda().to(dtype)
+        vd = torch.from_numpy(np.ascontiguousarray(np.stack(vs))).cuda().to(dtype)
+        q = torch.from_numpy(np.ascontiguousarray(np.stack(qs))).cuda().to(dtype).to(qdt)
         N.lib().dp_debug_set(1, cl if cl >= G else 0)
-        tag = (f"case {c:3d}: n={n:5d} H={H} G={G} d={d:3d} {str(dtype)[6:]:8s} {prof:7s} p=({p1},{p2}) "
-               f"cl={cl or 'auto'}")
+        tag = (f"case {c:3d}: B={B} n={n:5d} H={H} G={G} d={d:3d} {str(dtype)[6:]:8s} q {str(qdt)[6:]:8s} "
+               f"{prof:7s} p=({p1},{p2}) cl={cl or 'auto'}")
         layer = cluster_layer(kd, vd, fp64_assign=False)
         try:
             out, ws = sparse_attention(q, layer, p1, p2, return_plan=True)
@@ -63,16 +70,17 @@ def main():
             totals.setdefault("errors", []).append(tag)
             print(tag + f": ERROR {e} (K={layer.nclusters.tolist()}, cap={layer.cluster_cap})", flush=True)
             continue
-        out = out[0].double().cpu().numpy()
-        lm = ws.log_mass[0].cpu().numpy()
-        st = ws.state[0].cpu().numpy()
-        kf = kd[0].double().cpu().numpy()
-        vf = vd[0].double().cpu().numpy()
+        outs = out.double().cpu().numpy()
+        lms = ws.log_mass.cpu().numpy()
+        sts = ws.state.cpu().numpy()
         cls = {}
-        for hq in range(H * G):
+        for b, hq in [(b, hq) for b in range(B) for hq in range(H * G)]:
+            out, lm, st = outs[b], lms[b], sts[b]
+            kf = kd[b].double().cpu().numpy()
+            vf = vd[b].double().cpu().numpy()
             h = hq // G
-            t = oracle_tables(layer, 0, h)
-            o_out, o_plan, o_est = O.decode_step(q[0, hq].double().cpu().numpy(), kf[h], vf[h], t, p1, p2,
+            t = oracle_tables(layer, b, h)
+            o_out, o_plan, o_est = O.decode_step(q[b, hq].double().cpu().numpy(), kf[h], vf[h], t, p1, p2,
                                                  layer.sink, layer.window)
             K = len(t.members)
             if K and np.max(np.abs(lm[hq, :K] - o_est.log_masses)) > 1e-9:
