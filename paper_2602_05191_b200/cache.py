@@ -126,7 +126,18 @@ class ClusteredLayer:
         return self.keys.device
 
     def view(self, b=None, h=None):
-        """dp_cache_view over the whole layer, or over one (b, h) head."""
+        """dp_cache_view over the whole layer, or over one (b, h) head.  The
+        whole-layer view is cached (the step path calls this every layer) and
+        rebuilt when the token count changes."""
+        if b is None:
+            cv = self.__dict__.get("_view")
+            if cv is not None and cv.n_tokens == self.n_tokens:
+                return cv
+            self.__dict__["_view"] = cv = self._make_view(None, None)
+            return cv
+        return self._make_view(b, h)
+
+    def _make_view(self, b, h):
         v = N.CacheView()
         v.batch, v.kv_heads = self.batch, self.kv_heads
         v.head_dim, v.dtype = self.head_dim, dtype_code(self.keys)

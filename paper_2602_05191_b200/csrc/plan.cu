@@ -876,7 +876,32 @@ size_t plan_smem_bytes(int d, int cap, int CL, int kG) { return plan_layout(CL, 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static cudaError_t centroid_tmap_encode(const dp_cache_view& v, CUtensorMap* m);
+// a few recent maps, keyed by (centroid pointer, rows, d): encoding costs host
+// microseconds on every layer of every step otherwise
 static cudaError_t centroid_tmap(const dp_cache_view& v, CUtensorMap* m) {
+  struct Entry {
+    const void* ptr;
+    long long rows;
+    int d;
+    CUtensorMap map;
+  };
+  static Entry cache[64];
+  static int next = 0;
+  const long long rows = (long long)v.batch * v.kv_heads * v.cluster_cap;
+  for (const Entry& e : cache)
+    if (e.ptr == v.centroids && e.rows == rows && e.d == v.head_dim) {
+      *m = e.map;
+      return cudaSuccess;
+    }
+  const cudaError_t err = centroid_tmap_encode(v, m);
+  if (err == cudaSuccess) {
+    cache[next] = Entry{v.centroids, rows, v.head_dim, *m};
+    next = (next + 1) % 64;
+  }
+  return err;
+}
+static cudaError_t centroid_tmap_encode(const dp_cache_view& v, CUtensorMap* m) {
   static EncodeTiledFn fn = nullptr;
   if (!fn) {
     cudaDriverEntryPointQueryResult qr;
