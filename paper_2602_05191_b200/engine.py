@@ -106,22 +106,28 @@ def sparse_attention(q, cache, *args, **kw):
 
 
 def _sparse_layer(q, layer, p1=0.95, p2=0.7, *, workspace=None, return_plan=False, stream=None,
-                  scale=None):
+                  scale=None, out=None):
     """One decode step over a whole layer: score -> two-stage top-p ->
     mixed exact/approx attention.  Returns out fp32 [B,Hq,d] (and the
-    workspace holding log_mass/state/counts/lse/stats if return_plan)."""
+    workspace holding log_mass/state/counts/lse/stats if return_plan).
+    `out`, if given, is a contiguous fp32 CUDA tensor [B,Hq,d] written in
+    place (lets one workspace serve every layer while outputs accumulate)."""
     for name, val in (("p1", p1), ("p2", p2)):
         if not 0.0 < val <= 1.0:
             raise ValueError(f"{name} must be in (0, 1], got {val}")
     G = _group(q, layer)
     ws = workspace if workspace is not None and workspace.fits(layer, G) else DecodeWorkspace(layer, G)
+    if out is None:
+        out = ws.out
+    elif out.dtype != torch.float32 or tuple(out.shape) != tuple(ws.out.shape) or not out.is_contiguous():
+        raise ValueError(f"out must be a contiguous float32 tensor of shape {tuple(ws.out.shape)}")
     q = q.contiguous()
     sc = 1.0 / math.sqrt(layer.head_dim) if scale is None else scale
     N.check(N.lib().dp_decode_step(
         layer.view(), N.ptr(q), dtype_code(q), G, sc, p1, p2, N.ptr(ws.log_mass), N.ptr(ws.state),
-        N.ptr(ws.counts), N.ptr(ws.out), N.ptr(ws.lse), N.ptr(ws.stats), N.ptr(ws.ws), ws.ws.numel(),
+        N.ptr(ws.counts), N.ptr(out), N.ptr(ws.lse), N.ptr(ws.stats), N.ptr(ws.ws), ws.ws.numel(),
         _stream(layer, stream)))
-    return (ws.out, ws) if return_plan else ws.out
+    return (out, ws) if return_plan else out
 
 
 def cluster_topk_attention(q, layer, budget, *, workspace=None, stream=None, scale=None, return_plan=False):
