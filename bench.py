@@ -406,6 +406,26 @@ def _measure(a, context, L, dev, world, rank, sampler=None):
     graphs = capture(layer_step)
     ms = max_over_ranks(timed(graphs, a.steps, a.warmup, sampler), world, dev)
     del graphs
+
+    # the attention kernel alone, back to back in a graph (PDL-chained as in
+    # the step): per-layer workspaces hold each layer's plan
+    wsl = [DecodeWorkspace(lay, G) for lay in layers]
+    for li in range(L):
+        q = qdev[li][0]
+        N.check(lib.dp_plan(views[li], N.ptr(q), dtype_code(q), G, scale, a.p1, a.p2, N.ptr(wsl[li].log_mass), None,
+                            N.ptr(wsl[li].counts), N.ptr(wsl[li].stats), N.ptr(wsl[li].ws), wsl[li].ws.numel(),
+                            torch.cuda.current_stream(dev).cuda_stream))
+
+    def attend_only(li, s):
+        w, q = wsl[li], qdev[li][0]
+        N.check(lib.dp_attend(views[li], N.ptr(q), dtype_code(q), G, scale, N.ptr(w.log_mass), N.ptr(w.out),
+                              N.ptr(w.lse), N.ptr(w.ws), w.ws.numel(), torch.cuda.current_stream(dev).cuda_stream))
+
+    agraphs = capture(attend_only)
+    attend_graph_ms = max_over_ranks(timed(agraphs, a.steps, a.warmup), world, dev) / L
+    attend_graph_bytes = float((((stats_np[0, :, :, :, 0] * 2 * d * s_kv + stats_np[0, :, :, :, 1] * d * 4)
+                                 .sum(axis=(1, 2))) + qo).mean())
+    del agraphs, wsl
     dense_ms = None
     if not a.no_dense:
         dgraphs = capture(dense_step)
@@ -414,7 +434,7 @@ def _measure(a, context, L, dev, world, rank, sampler=None):
     return dict(layers=layers, wss=wss, qdev=qdev, ms=ms, dense_ms=dense_ms, stage_ms=stage_ms,
                 dense_kernel_ms=dense_kernel_ms, attend_bytes=attend_bytes, step_bytes=step_bytes,
                 dense_bytes=dense_bytes, union_frac=float(U.mean() / context), prefill_s=prefill_s, gen_s=gen_s,
-                hl=hl, Hq_l=Hq_l)
+                hl=hl, Hq_l=Hq_l, attend_graph_ms=attend_graph_ms, attend_graph_bytes=attend_graph_bytes)
 
 
 def run_b200(a):
@@ -438,6 +458,7 @@ def run_b200(a):
     prefill_s, gen_s = res["prefill_s"], res["gen_s"]
     attend_ms = stage_ms[1]
     attend_gbs = float(attend_bytes.mean() / (attend_ms * 1e-3) / 1e9)
+    res_attend_graph_ms, res_attend_graph_bytes = res["attend_graph_ms"], res["attend_graph_bytes"]
 
     # ---- e2e through the public API with host buffers ---------------------
     e2e = None
@@ -544,6 +565,13 @@ def run_b200(a):
             "gpu_launches": launches,
             "clocks": clocks,
             "stage_us_per_layer": {"plan": stage_ms[0] * 1e3, "attend": stage_ms[1] * 1e3},
+            "attend_in_graph": {"us_per_launch": res_attend_graph_ms * 1e3,
+                                "algorithmic_bytes_per_launch": res_attend_graph_bytes,
+                                "gbs": res_attend_graph_bytes / (res_attend_graph_ms * 1e-3) / 1e9,
+                                "frac": res_attend_graph_bytes / (res_attend_graph_ms * 1e-3) / 1e9 / hbm_peak,
+                                "note": "attn_tc_kernel launches back to back in a CUDA graph (PDL-chained), per-layer "
+                                        "work lists from one plan each; the roofline object above times each launch "
+                                        "between CUDA events (no PDL overlap)"},
             "step_algorithmic_bytes": step_bytes,
             "step_roofline_frac": step_bytes / (ms * 1e-3) / 1e9 / hbm_peak,
             "union_exact_rows_frac": union_frac,
