@@ -528,6 +528,8 @@ def run_b200(a):
             "attend_gbs": float(r2["attend_bytes"].mean() / (a_ms * 1e-3) / 1e9),
             "dense_kernel_gbs": r2["dense_bytes"] / a.long_layers / (r2["dense_kernel_ms"] * 1e-3) / 1e9,
             "union_exact_rows_frac": r2["union_frac"],
+            "attend_in_graph": {"us_per_launch": r2["attend_graph_ms"] * 1e3,
+                                "gbs": r2["attend_graph_bytes"] / (r2["attend_graph_ms"] * 1e-3) / 1e9},
         }
 
     peaks = {}
@@ -583,6 +585,7 @@ def run_b200(a):
         }
         if long_ctx is not None:
             long_ctx["attend_roofline_frac"] = long_ctx["attend_gbs"] / hbm_peak
+            long_ctx["attend_in_graph"]["frac"] = long_ctx["attend_in_graph"]["gbs"] / hbm_peak
             long_ctx["dense_kernel_roofline_frac"] = long_ctx["dense_kernel_gbs"] / hbm_peak
         print(json.dumps(line), flush=True)
 
