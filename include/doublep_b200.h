@@ -175,6 +175,48 @@ int dp_dense_attention(const dp_cache_view* v, const void* q, int32_t q_dtype,
 int dp_append_token(const dp_cache_view* v, const void* new_k, const void* new_v, void* stream);
 
 /* ---------------------------------------------------------------------- */
+/* measurement side: true distribution, token top-k baseline, metrics       */
+/* (fp64 like the reference; not on the decode path)    */
+/* ---------------------------------------------------------------------- */
+
+/* True token distribution, replaces full_attention_weights / true_token_weights
+ * (engine.py:122-132, :147-155): logits = (k . q) * scale in fp64 over all
+ * n_tokens rows, lse = m + log(sum(exp(x - m))) (kernels.logsumexp,
+ * _kernels_py.py:29-35), weights = exp(logits - lse).  weights fp64
+ * [B,Hq,row_cap] in PHYSICAL row order (the clustered layout); lse fp64 [B,Hq]. */
+int dp_token_weights(const dp_cache_view* v, const void* q, int32_t q_dtype, int32_t gqa_group, double scale,
+                     double* weights, double* lse, void* stream);
+
+/* Idealised fixed-budget baseline, replaces baseline_token_topk
+ * (engine.py:293-315) with top_k_select (selection.py:85-92): the `budget`
+ * rows of largest true weight (ties -> lower token position; perm int32
+ * [B,H,row_cap] maps rows < perm_rows to positions, NULL = identity), then
+ * out = sum (w / captured) v in fp64.  out fp64 [B,Hq,d]; captured fp64
+ * [B,Hq] (the true mass of the subset; normalizer = exp(lse) * captured);
+ * selected (nullable) uint8 [B,Hq,row_cap].  budget outside [1, n_tokens]
+ * -> DP_ERR_INVALID with the reference message. */
+int dp_token_topk(const dp_cache_view* v, const int32_t* perm, int32_t perm_rows, int32_t gqa_group,
+                  int32_t budget, const double* weights, double* out, double* captured, uint8_t* selected,
+                  void* stream);
+
+/* recovered_mass (metrics.py:26-39): true mass of a plan's exact tokens
+ * (sink + window + members of state==2 clusters).  recovered fp64 [B,Hq]. */
+int dp_recovered_mass(const dp_cache_view* v, int32_t gqa_group, const double* weights, const uint8_t* state,
+                      double* recovered, void* stream);
+
+/* cluster_approx_error (metrics.py:61-76): |true cluster mass -
+ * exp(log_mass - lse)| for the cluster at each estimated rank (order from
+ * dp_select).  errors fp64 [B,Hq,cluster_cap], rank order. */
+int dp_cluster_approx_error(const dp_cache_view* v, int32_t gqa_group, const double* weights, const double* lse,
+                            const double* log_mass, const int32_t* order, double* errors, void* stream);
+
+/* adaptive_token_budget (metrics.py:41-50): the minimal number of tokens
+ * whose true mass reaches p (searchsorted(cumsum(sorted desc), p, 'left')
+ * + 1; n_tokens + 1 when the total never reaches p).  budget int32 [B,Hq]. */
+int dp_adaptive_token_budget(const dp_cache_view* v, int32_t gqa_group, const double* weights, double p,
+                             int32_t* budget, void* stream);
+
+/* ---------------------------------------------------------------------- */
 /* prefill clustering (build_clustered_cache, clustering.py:266-314)        */
 /* ---------------------------------------------------------------------- */
 

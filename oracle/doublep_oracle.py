@@ -593,6 +593,62 @@ def full_attention(q, keys_h, values_h):
 
 
 # ----------------------------------------------------------------------------
+# Measurement side: token top-k baseline and metrics (engine.py:293-315,
+# metrics.py:26-76)
+# ----------------------------------------------------------------------------
+
+
+def full_attention_weights(q, keys_h):
+    """`engine.py:122-132`: (weights f64[N], lse)."""
+    logits = scaled_logits(keys_h, q, 1.0 / np.sqrt(keys_h.shape[1]))
+    lse = logsumexp(logits)
+    return np.exp(logits - lse), lse
+
+
+def token_topk(q, keys_h, values_h, budget):
+    """`engine.py:293-315` baseline_token_topk: exact attention over the
+    `budget` tokens of largest true weight, renormalised over the subset.
+    Returns (AttentionOutput, captured, idx)."""
+    n = keys_h.shape[0]
+    if not 1 <= budget <= n:
+        raise ValueError(f"budget must be in [1, {n}], got {budget}")
+    w, lse = full_attention_weights(q, keys_h)
+    idx = top_k_select(w, budget)
+    captured = float(w[idx].sum())
+    out = weighted_sum(w[idx] / captured, values_h[idx])
+    return (AttentionOutput(output=out, normalizer=float(np.exp(lse)) * captured, exact_token_count=int(budget),
+                            approx_cluster_count=0, log_normalizer=lse + math.log(captured)), captured, idx)
+
+
+def recovered_mass(w, exact_tokens):
+    """`metrics.py:26-39`: true mass of a plan's exact tokens."""
+    return float(w[np.asarray(exact_tokens, dtype=np.int64)].sum())
+
+
+def adaptive_token_budget(w, p):
+    """`metrics.py:41-50`: minimal token count whose true mass reaches p."""
+    order = np.argsort(-w, kind="stable")
+    cum = np.cumsum(w[order])
+    return int(np.searchsorted(cum, p, side="left") + 1)
+
+
+def violation_rate(recovered, p):
+    """`metrics.py:53-58`."""
+    arr = np.asarray(recovered, dtype=np.float64)
+    if arr.size == 0:
+        raise ValueError("no recovered masses given")
+    return float(np.mean(arr < p))
+
+
+def cluster_approx_error(w, lse, est, tables):
+    """`metrics.py:61-76`: |true mass - exp(log_mass - lse)| per cluster, in
+    estimated-rank order.  Returns (errors, order)."""
+    true_mass = np.array([w[m].sum() for m in tables.members], dtype=np.float64)
+    errors = np.abs(true_mass - np.exp(est.log_masses - lse))
+    return errors[est.order], est.order
+
+
+# ----------------------------------------------------------------------------
 # Decode-time growth (clustering.py:170-229) and split-KV merge
 # ----------------------------------------------------------------------------
 

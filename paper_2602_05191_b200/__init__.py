@@ -33,6 +33,18 @@ from .engine import (
     plan_selection,
     sparse_attention,
 )
+from .metrics import (
+    adaptive_token_budget,
+    baseline_token_topk,
+    cluster_approx_error,
+    full_attention_weights,
+    output_error,
+    recovered_mass,
+    token_topk_attention,
+    token_weights,
+    true_token_weights,
+    violation_rate,
+)
 
 __version__ = "0.1.0"
 BACKEND = "b200"
@@ -42,4 +54,7 @@ __all__ = [
     "DoublePConfig", "KvCache", "PRESETS", "SelectionPlan", "TopPResult", "build_cache_for_config",
     "build_clustered_cache", "cluster_layer", "cluster_topk_attention", "decode_step", "default_cluster_count", "dense_attention",
     "estimate_cluster_distribution", "full_attention", "head_seed", "plan_selection", "sparse_attention",
+    "adaptive_token_budget", "baseline_token_topk", "cluster_approx_error", "full_attention_weights",
+    "output_error", "recovered_mass", "token_topk_attention", "token_weights", "true_token_weights",
+    "violation_rate",
 ]

@@ -183,6 +183,59 @@ int dp_append_token(const dp_cache_view* v, const void* new_k, const void* new_v
   return e == cudaSuccess ? DP_OK : cuda_fail(e, "dp_append_token");
 }
 
+/* ---- measurement side (metrics.cu) ---------------------------------- */
+
+int dp_token_weights(const dp_cache_view* v, const void* q, int32_t q_dtype, int32_t G, double scale,
+                     double* weights, double* lse, void* stream) {
+  int r = check_view(v, G);
+  if (r) return r;
+  if ((r = check_q(q_dtype))) return r;
+  if (!weights || !lse) return fail(DP_ERR_INVALID, "weights and lse are required");
+  cudaError_t e = dp::launch_token_weights(*v, q, q_dtype, G, scale, weights, lse, (cudaStream_t)stream);
+  return e == cudaSuccess ? DP_OK : cuda_fail(e, "dp_token_weights");
+}
+
+int dp_token_topk(const dp_cache_view* v, const int32_t* perm, int32_t perm_rows, int32_t G, int32_t budget,
+                  const double* weights, double* out, double* captured, uint8_t* selected, void* stream) {
+  int r = check_view(v, G);
+  if (r) return r;
+  if (budget < 1 || budget > v->n_tokens)
+    return fail(DP_ERR_INVALID, "budget must be in [1, " + std::to_string(v->n_tokens) + "], got " +
+                                    std::to_string(budget));
+  if (!weights || !out || !captured) return fail(DP_ERR_INVALID, "weights, out and captured are required");
+  cudaError_t e = dp::launch_token_topk(*v, perm, perm_rows, G, budget, weights, out, captured, selected,
+                                        (cudaStream_t)stream);
+  return e == cudaSuccess ? DP_OK : cuda_fail(e, "dp_token_topk");
+}
+
+int dp_recovered_mass(const dp_cache_view* v, int32_t G, const double* weights, const uint8_t* state,
+                      double* recovered, void* stream) {
+  int r = check_view(v, G);
+  if (r) return r;
+  if (!weights || !state || !recovered) return fail(DP_ERR_INVALID, "weights, state and recovered are required");
+  cudaError_t e = dp::launch_recovered_mass(*v, G, weights, state, recovered, (cudaStream_t)stream);
+  return e == cudaSuccess ? DP_OK : cuda_fail(e, "dp_recovered_mass");
+}
+
+int dp_cluster_approx_error(const dp_cache_view* v, int32_t G, const double* weights, const double* lse,
+                            const double* log_mass, const int32_t* order, double* errors, void* stream) {
+  int r = check_view(v, G);
+  if (r) return r;
+  if (!weights || !lse || !log_mass || !order || !errors)
+    return fail(DP_ERR_INVALID, "weights, lse, log_mass, order and errors are required");
+  cudaError_t e = dp::launch_cluster_error(*v, G, weights, lse, log_mass, order, errors, (cudaStream_t)stream);
+  return e == cudaSuccess ? DP_OK : cuda_fail(e, "dp_cluster_approx_error");
+}
+
+int dp_adaptive_token_budget(const dp_cache_view* v, int32_t G, const double* weights, double p, int32_t* budget,
+                             void* stream) {
+  int r = check_view(v, G);
+  if (r) return r;
+  if (!weights || !budget) return fail(DP_ERR_INVALID, "weights and budget are required");
+  cudaError_t e = dp::launch_adaptive_budget(*v, G, weights, p, budget, (cudaStream_t)stream);
+  return e == cudaSuccess ? DP_OK : cuda_fail(e, "dp_adaptive_token_budget");
+}
+
 }  // extern "C"
 
 // error helper used by the clustering TU

@@ -12,7 +12,8 @@ Reference: /root/reference/pkg/src/doublep/engine.py.  Two entry styles:
       decode_step(q, cache, cc, cfg, layer, kv_head) -> (AttentionOutput,
           SelectionPlan, ClusterEstimate)
       estimate_cluster_distribution, plan_selection, sparse_attention(q,
-      cache, cc, plan, layer, kv_head), full_attention, full_attention_weights
+      cache, cc, plan, layer, kv_head), full_attention (the token-level
+      baselines and metrics.py quantities live in metrics.py)
 
 Every result is computed by libdoublep_b200.so; there is no CPU fallback.
 """
