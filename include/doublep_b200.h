@@ -194,9 +194,13 @@ int dp_token_weights(const dp_cache_view* v, const void* q, int32_t q_dtype, int
  * out = sum (w / captured) v in fp64.  out fp64 [B,Hq,d]; captured fp64
  * [B,Hq] (the true mass of the subset; normalizer = exp(lse) * captured);
  * selected (nullable) uint8 [B,Hq,row_cap].  budget outside [1, n_tokens]
- * -> DP_ERR_INVALID with the reference message. */
+ * -> DP_ERR_INVALID with the reference message.  budgets (nullable) int32
+ * [B,Hq] caps each q head's budget (min(budget, budgets[hq])): with the
+ * output of dp_adaptive_token_budget this is
+ * baseline_token_topp_fixed_budget (engine.py:340-370), the top-p prefix of
+ * the top-`budget` candidates (selection.py:68-82). */
 int dp_token_topk(const dp_cache_view* v, const int32_t* perm, int32_t perm_rows, int32_t gqa_group,
-                  int32_t budget, const double* weights, double* out, double* captured, uint8_t* selected,
+                  int32_t budget, const int32_t* budgets, const double* weights, double* out, double* captured, uint8_t* selected,
                   void* stream);
 
 /* recovered_mass (metrics.py:26-39): true mass of a plan's exact tokens
@@ -215,6 +219,15 @@ int dp_cluster_approx_error(const dp_cache_view* v, int32_t gqa_group, const dou
  * + 1; n_tokens + 1 when the total never reaches p).  budget int32 [B,Hq]. */
 int dp_adaptive_token_budget(const dp_cache_view* v, int32_t gqa_group, const double* weights, double p,
                              int32_t* budget, void* stream);
+
+/* Mixed exact/approximate attention in fp64 (mixed_attention,
+ * engine.py:216-252) with the same row/pseudo-row sets as
+ * dp_sparse_attention, one CTA per q head, deterministic: the evaluation
+ * path of the experiment runner (cli.py), not the decode hot path.
+ * state == NULL treats every cluster as exact (full attention over all
+ * rows).  out fp64 [B,Hq,d]; lse (nullable) fp64 [B,Hq]. */
+int dp_mixed_attention_f64(const dp_cache_view* v, const void* q, int32_t q_dtype, int32_t gqa_group, double scale,
+                           const double* log_mass, const uint8_t* state, double* out, double* lse, void* stream);
 
 /* ---------------------------------------------------------------------- */
 /* prefill clustering (build_clustered_cache, clustering.py:266-314)        */

@@ -79,12 +79,14 @@ _SIGS = {
     "dp_token_weights": (ctypes.c_int, [ctypes.POINTER(CacheView), _vp, ctypes.c_int32, ctypes.c_int32,
                                         ctypes.c_double, _vp, _vp, _vp]),
     "dp_token_topk": (ctypes.c_int, [ctypes.POINTER(CacheView), _vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
-                                     _vp, _vp, _vp, _vp, _vp]),
+                                     _vp, _vp, _vp, _vp, _vp, _vp]),
     "dp_recovered_mass": (ctypes.c_int, [ctypes.POINTER(CacheView), ctypes.c_int32, _vp, _vp, _vp, _vp]),
     "dp_cluster_approx_error": (ctypes.c_int, [ctypes.POINTER(CacheView), ctypes.c_int32, _vp, _vp, _vp, _vp, _vp,
                                                _vp]),
     "dp_adaptive_token_budget": (ctypes.c_int, [ctypes.POINTER(CacheView), ctypes.c_int32, _vp, ctypes.c_double,
                                                 _vp, _vp]),
+    "dp_mixed_attention_f64": (ctypes.c_int, [ctypes.POINTER(CacheView), _vp, ctypes.c_int32, ctypes.c_int32,
+                                              ctypes.c_double, _vp, _vp, _vp, _vp, _vp]),
     "dp_append_token": (ctypes.c_int, [ctypes.POINTER(CacheView), _vp, _vp, _vp]),
     "dp_cluster_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(ClusterParams)]),
     "dp_cluster_build": (ctypes.c_int, [ctypes.POINTER(ClusterParams), _vp, _vp, _vp, _vp, _vp, _vp,

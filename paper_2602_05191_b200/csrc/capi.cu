@@ -196,14 +196,14 @@ int dp_token_weights(const dp_cache_view* v, const void* q, int32_t q_dtype, int
 }
 
 int dp_token_topk(const dp_cache_view* v, const int32_t* perm, int32_t perm_rows, int32_t G, int32_t budget,
-                  const double* weights, double* out, double* captured, uint8_t* selected, void* stream) {
+                  const int32_t* budgets, const double* weights, double* out, double* captured, uint8_t* selected, void* stream) {
   int r = check_view(v, G);
   if (r) return r;
   if (budget < 1 || budget > v->n_tokens)
     return fail(DP_ERR_INVALID, "budget must be in [1, " + std::to_string(v->n_tokens) + "], got " +
                                     std::to_string(budget));
   if (!weights || !out || !captured) return fail(DP_ERR_INVALID, "weights, out and captured are required");
-  cudaError_t e = dp::launch_token_topk(*v, perm, perm_rows, G, budget, weights, out, captured, selected,
+  cudaError_t e = dp::launch_token_topk(*v, perm, perm_rows, G, budget, budgets, weights, out, captured, selected,
                                         (cudaStream_t)stream);
   return e == cudaSuccess ? DP_OK : cuda_fail(e, "dp_token_topk");
 }
@@ -234,6 +234,17 @@ int dp_adaptive_token_budget(const dp_cache_view* v, int32_t G, const double* we
   if (!weights || !budget) return fail(DP_ERR_INVALID, "weights and budget are required");
   cudaError_t e = dp::launch_adaptive_budget(*v, G, weights, p, budget, (cudaStream_t)stream);
   return e == cudaSuccess ? DP_OK : cuda_fail(e, "dp_adaptive_token_budget");
+}
+
+int dp_mixed_attention_f64(const dp_cache_view* v, const void* q, int32_t q_dtype, int32_t G, double scale,
+                           const double* log_mass, const uint8_t* state, double* out, double* lse, void* stream) {
+  int r = check_view(v, G);
+  if (r) return r;
+  if ((r = check_q(q_dtype))) return r;
+  if (!out) return fail(DP_ERR_INVALID, "out is required");
+  if (state && !log_mass) return fail(DP_ERR_INVALID, "log_mass is required with a state");
+  cudaError_t e = dp::launch_mixed_f64(*v, q, q_dtype, G, scale, log_mass, state, out, lse, (cudaStream_t)stream);
+  return e == cudaSuccess ? DP_OK : cuda_fail(e, "dp_mixed_attention_f64");
 }
 
 }  // extern "C"

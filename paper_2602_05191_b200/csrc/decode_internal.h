@@ -81,11 +81,13 @@ cudaError_t launch_append(const dp_cache_view& v, const void* nk, const void* nv
 cudaError_t launch_token_weights(const dp_cache_view& v, const void* q, int qdt, int G, double scale, double* w,
                                  double* lse, cudaStream_t st);
 cudaError_t launch_token_topk(const dp_cache_view& v, const int* perm, int perm_rows, int G, int budget,
-                              const double* w, double* out, double* captured, uint8_t* selected, cudaStream_t st);
+                              const int* budgets, const double* w, double* out, double* captured, uint8_t* selected, cudaStream_t st);
 cudaError_t launch_recovered_mass(const dp_cache_view& v, int G, const double* w, const uint8_t* state,
                                   double* recovered, cudaStream_t st);
 cudaError_t launch_cluster_error(const dp_cache_view& v, int G, const double* w, const double* lse,
                                  const double* lm, const int* order, double* errors, cudaStream_t st);
+cudaError_t launch_mixed_f64(const dp_cache_view& v, const void* q, int qdt, int G, double scale, const double* lm,
+                             const uint8_t* state, double* out, double* lse, cudaStream_t st);
 cudaError_t launch_adaptive_budget(const dp_cache_view& v, int G, const double* w, double p, int* budget,
                                    cudaStream_t st);
 

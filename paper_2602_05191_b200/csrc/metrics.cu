@@ -12,6 +12,8 @@
 //   recovered_mass       metrics.py:26-39
 //   adaptive_budget      metrics.py:41-50
 //   cluster_approx_error metrics.py:61-76
+//   mixed_f64            engine.py:216-252 mixed_attention in fp64 (deterministic
+//                        evaluation path for the experiment runner)
 //
 // All of these read the fp64 weight rows [B, Hq, row_cap] written by
 // token_weights (physical row order of the clustered layout; `perm` maps a
@@ -111,6 +113,7 @@ __device__ unsigned long long kth_largest_key(const double* x, int n, int k, int
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kMetThreads) token_topk_kernel(dp_cache_view v, const int* __restrict__ perm,
                                                                  int perm_rows, int G, int budget,
+                                                                 const int* __restrict__ budgets,
                                                                  const double* __restrict__ w,
                                                                  double* __restrict__ out,
                                                                  double* __restrict__ captured,
@@ -119,7 +122,8 @@ __global__ void __launch_bounds__(kMetThreads) token_topk_kernel(dp_cache_view v
   __shared__ int ired[33];
   __shared__ double dred[33];
   const int hq = blockIdx.x, Hq = v.kv_heads * G, b = hq / Hq, h = (hq - b * Hq) / G;
-  const int n = v.n_tokens, d = v.head_dim, k = min(budget, n);
+  const int n = v.n_tokens, d = v.head_dim;
+  const int k = max(1, min(min(budget, n), budgets ? budgets[hq] : n));
   const double* x = w + (size_t)hq * v.row_cap;
   const int* pm = perm ? perm + (size_t)(b * v.kv_heads + h) * v.row_cap : nullptr;
   const unsigned long long T = kth_largest_key(x, n, k, ired);
@@ -283,6 +287,99 @@ __global__ void __launch_bounds__(kMetThreads) adaptive_budget_kernel(dp_cache_v
 }
 
 // ---------------------------------------------------------------------------
+// mixed exact/approximate attention in fp64, one CTA per q head
+// (mixed_attention, engine.py:216-252): exact rows = sink + window + rows of
+// state==2 clusters, approx pseudo-rows = (log_mass, value_mean) of state==1
+// clusters; state == NULL makes every cluster exact (full_attention over the
+// clustered rows).  Deterministic (fixed work split and combine order), so
+// experiment tables reproduce byte for byte; the decode hot path is the
+// fp32 attn_tc_kernel.
+// ---------------------------------------------------------------------------
+constexpr int kMixWarps = 8;
+
+__global__ void __launch_bounds__(kMixWarps * 32) mixed_f64_kernel(dp_cache_view v, const void* __restrict__ q,
+                                                                   int qdt, int G, double scale,
+                                                                   const double* __restrict__ lm,
+                                                                   const uint8_t* __restrict__ state,
+                                                                   double* __restrict__ out, double* __restrict__ lse) {
+  __shared__ double sm[kMixWarps], sl[kMixWarps];
+  __shared__ double so[kMixWarps][256];
+  const int hq = blockIdx.x, Hq = v.kv_heads * G, b = hq / Hq, h = (hq - b * Hq) / G;
+  const int bh = b * v.kv_heads + h, n = v.n_tokens, d = v.head_dim;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ne = d / 32 + (d % 32 ? 1 : 0);  // elements per lane (<= 8)
+  double qr[8], o[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const int j = lane + 32 * e;
+    qr[e] = (e < ne && j < d) ? load_elem_d(q, qdt, (size_t)hq * d + j) : 0.0;
+    o[e] = 0.0;
+  }
+  double m = -CUDART_INF, l = 0.0;
+  const size_t rb = (size_t)bh * v.row_cap * d;
+  auto fold = [&](double x, const double* vv) {  // online softmax update with one (logit, value row)
+    const double mn = fmax(m, x);
+    const double a = exp(m - mn), p = exp(x - mn);
+    l = l * a + p;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) o[e] = o[e] * a + p * vv[e];
+    m = mn;
+  };
+  auto row = [&](int r) {
+    double s = 0.0, vv[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int j = lane + 32 * e;
+      const bool ok = e < ne && j < d;
+      s = fma(ok ? load_elem_d(v.keys, v.dtype, rb + (size_t)r * d + j) : 0.0, qr[e], s);
+      vv[e] = ok ? load_elem_d(v.values, v.dtype, rb + (size_t)r * d + j) : 0.0;
+    }
+    fold(warp_sum(s) * scale, vv);
+  };
+  for (int r = warp; r < v.sink; r += kMixWarps) row(r);
+  for (int r = n - v.window + warp; r < n; r += kMixWarps) row(r);
+  const int K = v.nclusters[bh];
+  const int* offs = v.offs + (size_t)bh * (v.cluster_cap + 1);
+  const size_t cb = (size_t)hq * v.cluster_cap;
+  for (int c = warp; c < K; c += kMixWarps) {
+    const int st = state ? state[cb + c] : 2;
+    if (st == 2) {
+      for (int r = offs[c]; r < offs[c + 1]; ++r) row(r);
+    } else if (st == 1) {
+      double vv[8];
+      const float* vm = v.value_means + ((size_t)bh * v.cluster_cap + c) * d;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int j = lane + 32 * e;
+        vv[e] = (e < ne && j < d) ? (double)vm[j] : 0.0;
+      }
+      fold(lm[cb + c], vv);
+    }
+  }
+  if (lane == 0) {
+    sm[warp] = m;
+    sl[warp] = l;
+  }
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const int j = lane + 32 * e;
+    if (e < ne && j < d) so[warp][j] = o[e];
+  }
+  __syncthreads();
+  double M = -CUDART_INF;
+  for (int i = 0; i < kMixWarps; ++i) M = fmax(M, sm[i]);
+  double L = 0.0;
+  for (int i = 0; i < kMixWarps; ++i) L += sm[i] == -CUDART_INF ? 0.0 : sl[i] * exp(sm[i] - M);
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    double acc = 0.0;
+    for (int i = 0; i < kMixWarps; ++i)
+      if (sm[i] != -CUDART_INF) acc += so[i][j] * exp(sm[i] - M);
+    out[(size_t)hq * d + j] = L > 0.0 ? acc / L : 0.0;
+  }
+  if (threadIdx.x == 0 && lse) lse[hq] = L > 0.0 ? M + log(L) : -CUDART_INF;
+}
+
+// ---------------------------------------------------------------------------
 // host launchers
 // ---------------------------------------------------------------------------
 cudaError_t launch_token_weights(const dp_cache_view& v, const void* q, int qdt, int G, double scale, double* w,
@@ -294,11 +391,12 @@ cudaError_t launch_token_weights(const dp_cache_view& v, const void* q, int qdt,
 }
 
 cudaError_t launch_token_topk(const dp_cache_view& v, const int* perm, int perm_rows, int G, int budget,
-                              const double* w, double* out, double* captured, uint8_t* selected, cudaStream_t st) {
+                              const int* budgets, const double* w, double* out, double* captured, uint8_t* selected, cudaStream_t st) {
   const int HQ = v.batch * v.kv_heads * G;
   const size_t smem = (size_t)(kMetThreads / 32) * v.head_dim * sizeof(double);
   cudaFuncSetAttribute(token_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  token_topk_kernel<<<HQ, kMetThreads, smem, st>>>(v, perm, perm_rows, G, budget, w, out, captured, selected);
+  token_topk_kernel<<<HQ, kMetThreads, smem, st>>>(v, perm, perm_rows, G, budget, budgets, w, out, captured,
+                                                          selected);
   return cudaGetLastError();
 }
 
@@ -311,6 +409,12 @@ cudaError_t launch_recovered_mass(const dp_cache_view& v, int G, const double* w
 cudaError_t launch_cluster_error(const dp_cache_view& v, int G, const double* w, const double* lse,
                                  const double* lm, const int* order, double* errors, cudaStream_t st) {
   cluster_error_kernel<<<v.batch * v.kv_heads * G, 256, 0, st>>>(v, G, w, lse, lm, order, errors);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mixed_f64(const dp_cache_view& v, const void* q, int qdt, int G, double scale, const double* lm,
+                             const uint8_t* state, double* out, double* lse, cudaStream_t st) {
+  mixed_f64_kernel<<<v.batch * v.kv_heads * G, kMixWarps * 32, 0, st>>>(v, q, qdt, G, scale, lm, state, out, lse);
   return cudaGetLastError();
 }
 

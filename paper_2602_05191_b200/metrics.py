@@ -9,6 +9,7 @@ engine.py:293-338.  Two entry styles, as in engine.py:
       recovered_mass_batched(layer, w, state)                  # per q head
       cluster_approx_error_batched(layer, w, lse, log_mass, order)
       adaptive_token_budget_batched(layer, w, p)
+      mixed_attention_f64(q, layer, state, log_mass)           # fp64 evaluation path
 * reference signatures (per (layer, kv head), single query vector):
       recovered_mass(plan, q, cache), adaptive_token_budget(q, cache, p, layer,
       kv_head), violation_rate(recovered, p), cluster_approx_error(q, cache,
@@ -58,11 +59,13 @@ def _perm_args(layer):
     return N.ptr(layer.perm), layer.prefill_tokens - layer.window
 
 
-def token_topk_attention(q, layer, budget, *, weights=None, scale=None, stream=None, return_selected=False):
+def token_topk_attention(q, layer, budget, *, weights=None, budgets=None, scale=None, stream=None,
+                         return_selected=False):
     """Idealised fixed-budget baseline (baseline_token_topk, engine.py:293-315)
     for every q head: the `budget` tokens of largest true weight (ties ->
     lower position), renormalised.  Returns (out fp64 [B,Hq,d], captured fp64
-    [B,Hq]) and, with return_selected, the uint8 [B,Hq,row_cap] row mask."""
+    [B,Hq]) and, with return_selected, the uint8 [B,Hq,row_cap] row mask.
+    ``budgets`` (int32 [B,Hq], optional) caps each head's budget."""
     G = _group(q, layer)
     if not 1 <= int(budget) <= layer.n_tokens:
         raise ValueError(f"budget must be in [1, {layer.n_tokens}], got {budget}")
@@ -73,7 +76,7 @@ def token_topk_attention(q, layer, budget, *, weights=None, scale=None, stream=N
     cap = torch.zeros((B, Hq), dtype=torch.float64, device=layer.device)
     sel = torch.zeros((B, Hq, layer.row_cap), dtype=torch.uint8, device=layer.device) if return_selected else None
     perm, perm_rows = _perm_args(layer)
-    N.check(N.lib().dp_token_topk(layer.view(), perm, perm_rows, G, int(budget), N.ptr(weights), N.ptr(out),
+    N.check(N.lib().dp_token_topk(layer.view(), perm, perm_rows, G, int(budget), N.ptr(budgets), N.ptr(weights), N.ptr(out),
                                   N.ptr(cap), N.ptr(sel), _stream(layer, stream)))
     return (out, cap, sel) if return_selected else (out, cap)
 
@@ -113,6 +116,24 @@ def adaptive_token_budget_batched(layer, weights, p, *, stream=None):
     N.check(N.lib().dp_adaptive_token_budget(layer.view(), G, N.ptr(weights), float(p), N.ptr(out),
                                              _stream(layer, stream)))
     return out
+
+
+def mixed_attention_f64(q, layer, state=None, log_mass=None, *, scale=None, stream=None):
+    """mixed_attention (engine.py:216-252) in fp64 for every q head with the
+    plan given as per-cluster states (2 exact, 1 approx, 0 dropped); no state
+    = every cluster exact, i.e. full attention.  Deterministic -- the
+    experiment runner's evaluation path.  Returns (out fp64 [B,Hq,d], lse
+    fp64 [B,Hq])."""
+    G = _group(q, layer)
+    q = q.contiguous()
+    B, Hq = q.shape[0], q.shape[1]
+    out = torch.zeros((B, Hq, layer.head_dim), dtype=torch.float64, device=layer.device)
+    lse = torch.zeros((B, Hq), dtype=torch.float64, device=layer.device)
+    sc = 1.0 / math.sqrt(layer.head_dim) if scale is None else scale
+    N.check(N.lib().dp_mixed_attention_f64(layer.view(), N.ptr(q), dtype_code(q), G, sc, N.ptr(log_mass),
+                                           N.ptr(None if state is None else state.contiguous()), N.ptr(out),
+                                           N.ptr(lse), _stream(layer, stream)))
+    return out, lse
 
 
 def to_positions(layer, rows, b=0, h=0):
@@ -192,7 +213,7 @@ def baseline_token_topk(q, cache, budget, layer, kv_head):
     v, w, lse = _head_weights(q, lay, 0)
     out = torch.zeros((1, 1, lay.head_dim), dtype=torch.float64, device=lay.device)
     cap = torch.zeros((1, 1), dtype=torch.float64, device=lay.device)
-    N.check(N.lib().dp_token_topk(v, None, 0, 1, int(budget), N.ptr(w), N.ptr(out), N.ptr(cap), None,
+    N.check(N.lib().dp_token_topk(v, None, 0, 1, int(budget), None, N.ptr(w), N.ptr(out), N.ptr(cap), None,
                                   torch.cuda.current_stream(lay.device).cuda_stream))
     captured = float(cap.item())
     lz = float(lse.item())

@@ -1,0 +1,113 @@
+"""The experiment runner (paper_2602_05191_b200.cli)
+against the REAL reference CLI's tables on the same reference-generated
+workload (tests/golden/cli_w.dpkv and cli_*.csv, made by
+oracle/gen_golden_cli.py).  Same header and row keys; integer columns equal
+(selection counts, exact tokens, budgets); float columns within the fp32
+table tolerance (centroids/value means are stored fp32 on the device, the
+reference keeps fp64).  Also: repeated runs are byte-identical, and gen ->
+run --input equals the inline run."""
+
+import csv
+import io
+import os
+
+import pytest
+
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+DUMP = os.path.join(GOLDEN, "cli_w.dpkv")
+RUNS = [
+    ("cli_run_doublep", ["run", "--method", "doublep", "--window", "32"]),
+    ("cli_run_doublep_qwen", ["run", "--method", "doublep", "--window", "32", "--preset", "qwen-default"]),
+    ("cli_run_full", ["run", "--method", "full", "--window", "32"]),
+    ("cli_run_token_topk", ["run", "--method", "token_topk", "--k", "40", "--window", "32"]),
+    ("cli_run_cluster_topk", ["run", "--method", "cluster_topk", "--m", "3", "--window", "32"]),
+    ("cli_run_token_topp_fixed", ["run", "--method", "token_topp_fixed", "--B", "64", "--window", "32"]),
+    ("cli_sweep", ["sweep", "--methods", "doublep,token_topk,cluster_topk,token_topp_fixed,full",
+                   "--p1-grid", "0.9,0.95,0.99", "--k-grid", "16,128", "--m-grid", "2,5", "--B-grid", "32",
+                   "--window", "32"]),
+    ("cli_figs_budgets", ["figs", "--table", "budgets", "--k-list", "8,64", "--window", "32"]),
+    ("cli_figs_recovery", ["figs", "--table", "recovery", "--window", "32"]),
+    ("cli_figs_cluster_error", ["figs", "--table", "cluster-error", "--window", "32"]),
+    ("cli_figs_tracking", ["figs", "--table", "tracking", "--window", "32"]),
+]
+INT_COLS = {"layer", "head", "step", "kv_head", "rank", "k", "m", "B", "clusters_total", "clusters_selected",
+            "clusters_exact", "exact_tokens", "records", "budget", "violation", "attained", "min_clusters"}
+# float tolerance (abs, rel) per column: fp32 tables move log-masses by ~1e-6 relative
+FTOL = {"rel_err": (2e-5, 1e-3), "mean_rel_err": (2e-5, 1e-3), "p50_rel_err": (2e-5, 1e-3),
+        "p90_rel_err": (2e-5, 1e-3), "est_mass": (1e-5, 0), "recovered_mass": (1e-9, 0), "recovered": (1e-9, 0),
+        "captured": (1e-9, 0), "mean_exact_tokens": (1e-9, 0), "violation_rate": (1e-9, 0),
+        "mean_error": (1e-5, 1e-3), "max_error": (1e-5, 1e-3), "ratio": (1e-9, 0), "p1": (0, 0), "p2": (0, 0)}
+
+
+def _rows(text):
+    return list(csv.reader(io.StringIO(text)))
+
+
+def _run(argv, tmp_path, name):
+    from paper_2602_05191_b200.cli import main
+
+    out = tmp_path / (name + ".csv")
+    assert main([argv[0], "--input", DUMP, *argv[1:], "--out", str(out)]) == 0
+    return out.read_text()
+
+
+@pytest.mark.parametrize("name,argv", RUNS, ids=[r[0] for r in RUNS])
+def test_cli_tables_match_reference(name, argv, tmp_path):
+    got = _rows(_run(argv, tmp_path, name))
+    with open(os.path.join(GOLDEN, name + ".csv")) as f:
+        want = _rows(f.read())
+    assert got[0] == want[0]  # identical header / schema
+    assert len(got) == len(want)
+    cols = want[0]
+    mism = []
+    for g, w in zip(got[1:], want[1:]):
+        for c, a, b in zip(cols, g, w):
+            if c == "method" or c == "selector" or a == b:
+                assert a == b, (name, c, a, b)
+                continue
+            if c in INT_COLS:
+                mism.append((c, a, b))
+                continue
+            assert a != "" and b != "", (name, c, a, b)
+            tol_abs, tol_rel = FTOL[c]
+            assert abs(float(a) - float(b)) <= tol_abs + tol_rel * abs(float(b)), (name, g[:3], c, a, b)
+    # integer columns are exact; the tracking table's minimal counts sit on an
+    # error threshold (eps = the step's own rel_err) and may move by a tie
+    if name == "cli_figs_tracking":
+        assert all(c in ("min_clusters", "attained") for c, _, _ in mism) and len(mism) <= 2, mism
+    else:
+        assert not mism, (name, mism)
+
+
+def test_cli_deterministic_and_gen_roundtrip(tmp_path):
+    from paper_2602_05191_b200.cli import main
+
+    flags = ["--n", "600", "--d", "32", "--kv-heads", "2", "--gqa-group", "2", "--steps", "2", "--profile",
+             "mixed", "--seed", "3"]
+    run = ["--method", "doublep", "--window", "32"]
+    a, b, c = (tmp_path / x for x in ("a.csv", "b.csv", "c.csv"))
+    assert main(["run", *flags, *run, "--out", str(a)]) == 0
+    assert main(["run", *flags, *run, "--out", str(b)]) == 0
+    assert a.read_bytes() == b.read_bytes()
+    dump = tmp_path / "w.dpkv"
+    assert main(["gen", *flags, "--out", str(dump)]) == 0
+    assert main(["run", "--input", str(dump), *run, "--seed", "3", "--out", str(c)]) == 0
+    assert a.read_bytes() == c.read_bytes()
+    j = tmp_path / "a.json"
+    assert main(["run", *flags, *run, "--format", "json", "--out", str(j)]) == 0
+    import json
+
+    rows = json.loads(j.read_text())
+    assert len(rows) == len(_rows(a.read_text())) - 1
+
+
+def test_cli_errors(capsys):
+    from paper_2602_05191_b200.cli import main
+
+    assert main(["run", "--input", DUMP, "--method", "token_topk", "--window", "32"]) == 1
+    assert "requires k" in capsys.readouterr().err
+    assert main(["run", "--input", DUMP, "--method", "cluster_topk", "--m", "999", "--window", "32"]) == 1
+    assert "cluster budget must be in" in capsys.readouterr().err
