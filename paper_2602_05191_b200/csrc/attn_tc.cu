@@ -123,6 +123,17 @@ __device__ __forceinline__ void bulk_row(unsigned dst, const void* src, unsigned
 // per-CTA phase stamps (%globaltimer ns) of the last launch; profiling aid,
 // read with dp_debug_attn_timing()
 __device__ unsigned long long g_attn_ts[512][12];
+__device__ __forceinline__ void red_add_v4(float* p, float4 v) {  // p 16-B aligned
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+
+__device__ __forceinline__ int atom_add_acq_rel(int* p, int v) {
+  int old;
+  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;\n" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
 __device__ __forceinline__ void astamp(int ev) {
   if (threadIdx.x == 0 && blockIdx.x < 512) {
     unsigned long long t;
@@ -441,47 +452,69 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
     consumers_sync();
     const int slot = me - first_owner(bh);
     const size_t pbase = (size_t)bh * pt.max_chunks * G;
+    if (kDense) {
 #pragma unroll 1
-    for (int i = tid; i < G * d; i += kConsumers) {
-      const int h = i / d, c = i - h * d;
-      // sparse: scale to the plan's reference max and add into the head's
-      // accumulators (fire-and-forget reductions; the merge then reads one
-      // (o, l) per q head instead of every CTA's partial).  Dense: partials.
-      const float Mx = kDense ? -INFINITY : __ldcg(&wl.refm[(size_t)bh * G + h]);
-      float Mw = -INFINITY;
+      for (int i = tid; i < G * d; i += kConsumers) {
+        const int h = i / d, c = i - h * d;
+        float Mw = -INFINITY;
 #pragma unroll
-      for (int ww = 0; ww < kWarps; ++ww) Mw = fmaxf(Mw, s_wm[ww][h]);
-      const float Mr = kDense ? Mw : Mx;
-      float sum = 0.f, L = 0.f;
+        for (int ww = 0; ww < kWarps; ++ww) Mw = fmaxf(Mw, s_wm[ww][h]);
+        float sum = 0.f, L = 0.f;
 #pragma unroll
-      for (int ww = 0; ww < kWarps; ++ww) {
-        const float wm = s_wm[ww][h];
-        if (wm != -INFINITY) {
-          const float f = exp2f(wm - Mr);
-          sum += f * scratch[((size_t)ww * 8 + h) * d + c];
-          L += f * s_wl[ww][h];
+        for (int ww = 0; ww < kWarps; ++ww) {
+          const float wm = s_wm[ww][h];
+          if (wm != -INFINITY) {
+            const float f = exp2f(wm - Mw);
+            sum += f * scratch[((size_t)ww * 8 + h) * d + c];
+            L += f * s_wl[ww][h];
+          }
         }
-      }
-      if (kDense) {
         pt.o[(pbase + (size_t)slot * G + h) * d + c] = sum;
         if (c == 0) {
           pt.m[pbase + (size_t)slot * G + h] = Mw == -INFINITY ? -INFINITY : Mw * 0.69314718055994531f;
           pt.l[pbase + (size_t)slot * G + h] = L;
         }
-      } else if (Mw != -INFINITY) {
-        float* ac = wl.acc + ((size_t)bh * G + h) * (d + 1);
-        atomicAdd(ac + c, sum);
-        if (c == 0) atomicAdd(ac + d, L);
+      }
+    } else {
+      // sparse: scale to the plan's reference max and add into the head's
+      // accumulators with 4-wide fire-and-forget reductions (the merge then
+      // reads one (o, l) per q head instead of every CTA's partial)
+      const int d4 = d >> 2;
+#pragma unroll 1
+      for (int i = tid; i < G * d4; i += kConsumers) {
+        const int h = i / d4, c = (i - h * d4) * 4;
+        const float Mr = __ldcg(&wl.refm[(size_t)bh * G + h]);
+        bool any = false;
+        float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+        float L = 0.f;
+#pragma unroll
+        for (int ww = 0; ww < kWarps; ++ww) {
+          const float wm = s_wm[ww][h];
+          if (wm != -INFINITY) {
+            any = true;
+            const float f = exp2f(wm - Mr);
+            const float4 x = *reinterpret_cast<const float4*>(scratch + ((size_t)ww * 8 + h) * d + c);
+            sum.x += f * x.x;
+            sum.y += f * x.y;
+            sum.z += f * x.z;
+            sum.w += f * x.w;
+            L += f * s_wl[ww][h];
+          }
+        }
+        if (any) {
+          float* ac = wl.acc + ((size_t)bh * G + h) * acc_stride(d);
+          red_add_v4(ac + c, sum);
+          if (c == 0) atomicAdd(ac + d, L);
+        }
       }
     }
     consumers_sync();  // scratch (this stage) and s_wm/s_wl free again
     if (nflushed < 2) {
       flushed[nflushed++] = bh;
     } else {  // many tiny heads in one range: publish the oldest now
-      if (tid == 0) {
-        __threadfence();
-        if (atomicAdd(&wl.counters[flushed[0]], 1) == head_parts(flushed[0]) - 1) s_merge[s_nmerge++] = flushed[0];
-      }
+      if (tid == 0)
+        if (atom_add_acq_rel(&wl.counters[flushed[0]], 1) == head_parts(flushed[0]) - 1)
+          s_merge[s_nmerge++] = flushed[0];
       flushed[0] = flushed[1];
       flushed[1] = bh;
     }
@@ -628,9 +661,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
   }
   consumers_sync();  // every partial of this CTA is written (CTA scope)
   if (tid == 0) {
-    __threadfence();  // ... and visible at gpu scope before the counters move (cumulativity)
+    // release: this CTA's reductions (observed through the barrier) are visible
+    // at gpu scope before its count; acquire: the last CTA's merge reads, ordered
+    // after the barrier below, see every other CTA's reductions
     for (int i = 0; i < nflushed; ++i)
-      if (atomicAdd(&wl.counters[flushed[i]], 1) == head_parts(flushed[i]) - 1) s_merge[s_nmerge++] = flushed[i];
+      if (atom_add_acq_rel(&wl.counters[flushed[i]], 1) == head_parts(flushed[i]) - 1)
+        s_merge[s_nmerge++] = flushed[i];
     // heads with no rows at all (no sink/window, nothing exact): merged by CTA bh % grid
     if (!kDense)
       for (int bh = me; bh < BH; bh += grid)
@@ -649,7 +685,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
     astamp(5);
     return;
   }
-  __threadfence();
   astamp(6);
   float* ored = reinterpret_cast<float*>(KV);  // [warps][8 heads][d]
   if (tid < nm) wl.counters[s_merge[tid]] = 0;  // self-reset for the next launch
@@ -661,7 +696,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
     for (int i = tid; i < nq * d; i += kConsumers) {
       const int qi = i / d, c = i - qi * d, mi = qi / G, g = qi - mi * G, bh = s_merge[mi];
       if (rp[bh + 1] == rp[bh]) continue;  // no rows: slow path below
-      float* ac = wl.acc + ((size_t)bh * G + g) * (d + 1);
+      float* ac = wl.acc + ((size_t)bh * G + g) * acc_stride(d);
       const float o_ = __ldcg(ac + c), l_ = __ldcg(ac + d);
       out[((size_t)bh * G + g) * d + c] = l_ > 0.f ? o_ / l_ : 0.f;
       if (c == 0)
@@ -672,7 +707,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
 #pragma unroll 1
     for (int i = tid; i < nq * (d + 1); i += kConsumers) {
       const int qi = i / (d + 1), c = i - qi * (d + 1), mi = qi / G, g = qi - mi * G;
-      wl.acc[((size_t)s_merge[mi] * G + g) * (d + 1) + c] = 0.f;
+      wl.acc[((size_t)s_merge[mi] * G + g) * acc_stride(d) + c] = 0.f;
     }
     // keep only the row-less heads for the slow path
     consumers_sync();

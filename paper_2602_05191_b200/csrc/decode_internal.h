@@ -12,6 +12,10 @@ constexpr int kChunkRows = 128;   // rows per split-KV work item
 constexpr int kAttnThreads = 256;
 constexpr int kMaxPartSlots = 256;  // persistent attention grid cap (partials per head)
 
+// Row stride of the sparse accumulators: o[d], l, 3 pad floats (16-B aligned rows
+// for vector reductions).
+__host__ __device__ constexpr int acc_stride(int d) { return d + 4; }
+
 // Device work lists (one set per (b, kv head)), carved from the workspace.
 struct WorkLists {
   int4* runs;     // [BH][cap+2] {row start, len, head mask, virtual row prefix}
@@ -26,7 +30,7 @@ struct WorkLists {
   int* chunk_prefix;  // [BH+1] exclusive prefix of nchunks over heads (+ total)
   int* done;      // [1] producer-completion counter (zero between launches)
   float* apart;   // [BH][G][4+d] approx pseudo-row partial per q head (m, l, -, -, o[d]); m = -inf: none
-  float* acc;     // [BH][G][d+1] sparse attention accumulators (o[d], l) scaled by 2^-ref (zero between launches)
+  float* acc;     // [BH][G][acc_stride(d)] sparse attention accumulators (o[d], l, pad) scaled by 2^-ref (zero between launches)
   float* refm;    // [BH][G] reference max (log2 units) of those accumulators, written by the plan
   int max_chunks;
 };
