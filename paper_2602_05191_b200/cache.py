@@ -211,7 +211,7 @@ class ClusteredLayer:
 
 def cluster_layer(keys, values, *, k=None, sink=4, window=64, seed=0, max_iters=DEFAULT_MAX_ITERS,
                   tokens_per_cluster=DEFAULT_TOKENS_PER_CLUSTER, layer=0, fp64_assign=True, row_cap=None,
-                  extra_clusters=0, stream=None, head_seeds=None):
+                  extra_clusters=0, stream=None, head_seeds=None, tensor_cores=False):
     """k-means-cluster one layer of a batch on the GPU (`build_clustered_cache`
     for one layer, clustering.py:266-314).  keys/values: CUDA [B,H,N,d] f32
     or bf16 in position order.  ``row_cap``/``extra_clusters`` reserve room
@@ -232,7 +232,7 @@ def cluster_layer(keys, values, *, k=None, sink=4, window=64, seed=0, max_iters=
     p = N.ClusterParams()
     p.batch, p.kv_heads, p.head_dim, p.dtype = B, H, d, dtype_code(keys)
     p.n_tokens, p.sink, p.window, p.k = n, sink, window, k
-    p.max_iters, p.fp64_assign = max_iters, int(bool(fp64_assign))
+    p.max_iters, p.fp64_assign = max_iters, 2 if tensor_cores else int(bool(fp64_assign))
 
     def streams(degen=None):
         firsts = np.zeros(B * H, dtype=np.int32)

@@ -17,6 +17,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cuda.h>
+
 #include <string>
 
 #include "common.cuh"
@@ -42,6 +44,7 @@ struct KmWs {
   int* cursor;    // [BH][k]
   int* knum;      // [BH]
   int* done;      // [BH]
+  __nv_bfloat16* csplit;  // [3][BH][k][d] centroids as bf16 hi + mid + lo (tensor-core assignment)
 };
 
 static size_t km_layout(const dp_cluster_params* p, KmWs* w, char* base) {
@@ -69,6 +72,7 @@ static size_t km_layout(const dp_cluster_params* p, KmWs* w, char* base) {
   t.cursor = (int*)take(BH * k * 4);
   t.knum = (int*)take(BH * 4);
   t.done = (int*)take(BH * 4);
+  t.csplit = (__nv_bfloat16*)take(p->fp64_assign == 2 ? 3 * BH * k * d * 2 : 0);
   if (w) *w = t;
   return off;
 }
@@ -387,6 +391,336 @@ __global__ void __launch_bounds__(256) assign_kernel(dp_cluster_params p, const 
 }
 
 // -------------------------------------------------------------------------
+// assignment on the 5th-gen tensor cores (fp64_assign == 2; bf16 keys,
+// d in {64, 128}, k <= kTcMaxK).  dot(x, c) for 128 points x 128 centroids
+// per accumulator tile with tcgen05.mma (kind::f16, bf16 in, fp32 in TMEM):
+// the keys are exact in bf16 and every centroid is split into three bf16
+// terms (hi + mid + lo carry 24 mantissa bits, i.e. the fp32 path's
+// precision), accumulated into the same TMEM tile.  Warp roles: warp 0 issues
+// TMA (keys tile once, then one (centroid tile, split term) per ring stage),
+// warp 1 owns TMEM and issues the MMAs from one lane, warps 4-7 drain the
+// double-buffered accumulator with tcgen05.ld and keep the running argmin
+// (dist = |x|^2 - 2 x.c + |c|^2, ties -> lowest index) for their 32 points;
+// when the runner-up is within the tensor-core error band the two candidates
+// are re-scored in fp64, so near-ties resolve like the fp64 path.
+// -------------------------------------------------------------------------
+constexpr int kTcRows = 128;                   // points per CTA = centroids per tile = TMEM lanes
+constexpr int kTcStages = 2;                   // ring of (tile, term) stages (2 CTAs per SM hide each other's tails)
+constexpr int kTcHalf = kTcRows * 128;         // one 64-column swizzle half: 128 rows x 128 B
+constexpr int kTcMaxK = 4096;
+constexpr int kTcThreads = 256;
+
+__device__ __forceinline__ unsigned tc_smem(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void tc_bar_init(unsigned b, unsigned n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(b), "r"(n));
+}
+__device__ __forceinline__ void tc_bar_tx(unsigned b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(b), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tc_bar_arrive(unsigned b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(b) : "memory");
+}
+__device__ __forceinline__ void tc_bar_wait(unsigned b, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "TCW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra TCW_%=;\n}\n" ::"r"(b), "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tc_tma2d(unsigned dst, const CUtensorMap* m, int x, int y, unsigned bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          dst),
+      "l"(reinterpret_cast<unsigned long long>(m)), "r"(x), "r"(y), "r"(bar)
+      : "memory");
+}
+// UMMA shared-memory descriptor: K-major, 128-byte swizzle, 8-row atoms 1024 B apart
+__device__ __forceinline__ unsigned long long tc_desc(unsigned saddr) {
+  return (unsigned long long)((saddr >> 4) & 0x3FFF) | (1ull << 16) | ((unsigned long long)(1024 >> 4) << 32) |
+         (1ull << 46) | (2ull << 61);
+}
+
+__global__ void __launch_bounds__(kTcThreads, 1)
+    assign_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmC,
+                     dp_cluster_params p, KmWs w, const __nv_bfloat16* __restrict__ tc_keys) {
+  const int bh = blockIdx.y;
+  if (w.done[bh]) return;
+  const int M = p.n_tokens - p.sink - p.window, d = p.head_dim;
+  const int p0 = blockIdx.x * kTcRows;
+  if (p0 >= M) return;
+  const int kc = w.knum[bh];
+  const int halves = d / 64;
+  const int ntile = (kc + kTcRows - 1) / kTcRows, nsteps = ntile * 3;
+  const unsigned stage_bytes = (unsigned)halves * kTcHalf;
+  extern __shared__ unsigned char tc_raw[];
+  unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tc_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* As = base;                                      // keys tile [halves][128 x 128 B]
+  unsigned char* Bs = As + 2 * kTcHalf;                          // ring [stages][halves][128 x 128 B]
+  float* cn = reinterpret_cast<float*>(Bs + kTcStages * 2 * kTcHalf);  // [kTcMaxK] centroid norms
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(cn + kTcMaxK);
+  // bars: full[4], empty[4], afull, accf[2], acce[2]
+  unsigned* tslot = reinterpret_cast<unsigned*>(bars + 16);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const unsigned b0 = tc_smem(bars);
+  auto FULL = [&](int s) { return b0 + 8u * s; };
+  auto EMPTY = [&](int s) { return b0 + 8u * (kTcStages + s); };
+  const unsigned AFULL = b0 + 8u * (2 * kTcStages);
+  auto ACCF = [&](int b) { return b0 + 8u * (2 * kTcStages + 1 + b); };
+  auto ACCE = [&](int b) { return b0 + 8u * (2 * kTcStages + 3 + b); };
+  if (tid == 0) {
+    for (int s = 0; s < kTcStages; ++s) {
+      tc_bar_init(FULL(s), 1);
+      tc_bar_init(EMPTY(s), 1);
+    }
+    tc_bar_init(AFULL, 1);
+    for (int b = 0; b < 2; ++b) {
+      tc_bar_init(ACCF(b), 1);
+      tc_bar_init(ACCE(b), 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) {  // 2 x 128 fp32 accumulator columns
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;\n" ::"r"(tc_smem(tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (tid >= 128)
+    for (int c = tid - 128; c < kc; c += 128) cn[c] = (float)w.cnorm[(size_t)bh * p.k + c];
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const unsigned tmem = *tslot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer
+      const int xrow = bh * p.n_tokens + p.sink + p0;
+      tc_bar_tx(AFULL, (unsigned)halves * kTcHalf);
+      for (int hf = 0; hf < halves; ++hf) tc_tma2d(tc_smem(As + hf * kTcHalf), &tmX, hf * 64, xrow, AFULL);
+      const int BHk = p.batch * p.kv_heads * p.k;
+      for (int i = 0; i < nsteps; ++i) {
+        const int s = i % kTcStages, j = i / 3, t = i - 3 * j;
+        if (i >= kTcStages) tc_bar_wait(EMPTY(s), ((i / kTcStages) - 1) & 1);
+        const int crow = t * BHk + bh * p.k + j * kTcRows;
+        tc_bar_tx(FULL(s), stage_bytes);
+        for (int hf = 0; hf < halves; ++hf)
+          tc_tma2d(tc_smem(Bs + (s * 2 + hf) * kTcHalf), &tmC, hf * 64, crow, FULL(s));
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer: D[128 x 128] (+)= A[128 x 16] . B[128 x 16]^T per instruction
+      const unsigned idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((unsigned)(kTcRows >> 3) << 17) |
+                             ((unsigned)(kTcRows >> 4) << 24);
+      tc_bar_wait(AFULL, 0);
+      for (int i = 0; i < nsteps; ++i) {
+        const int s = i % kTcStages, j = i / 3, t = i - 3 * j, b = j & 1;
+        if (t == 0 && j >= 2) tc_bar_wait(ACCE(b), ((j >> 1) - 1) & 1);
+        tc_bar_wait(FULL(s), (i / kTcStages) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        const unsigned dt = tmem + (unsigned)(b * kTcRows);
+        for (int kk = 0; kk < halves * 4; ++kk) {
+          const unsigned off = (unsigned)((kk >> 2) * kTcHalf + (kk & 3) * 32);
+          const unsigned long long da = tc_desc(tc_smem(As) + off);
+          const unsigned long long db = tc_desc(tc_smem(Bs + s * 2 * kTcHalf) + off);
+          const unsigned acc = (t > 0 || kk > 0) ? 1u : 0u;
+          asm volatile(
+              "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+              " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(dt),
+              "l"(da), "l"(db), "r"(idesc), "r"(acc)
+              : "memory");
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(EMPTY(s))
+                     : "memory");
+        if (t == 2)
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(ACCF(b))
+                       : "memory");
+      }
+    }
+  } else if (warp >= 4) {  // epilogue: TMEM lanes 32*(warp-4) .. +31 = my points
+    const int ew = warp - 4, row = ew * 32 + lane, pt = p0 + row;
+    const float xn = pt < M ? (float)w.xnorm[(size_t)bh * M + pt] : 0.f;
+    // four independent (best, runner-up) trackers over columns q % 4: the
+    // compare chain is the epilogue's critical path, so it gets ILP
+    float tb[4], tb2[4];
+    int ti[4], ti2[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      tb[u] = tb2[u] = CUDART_INF_F;
+      ti[u] = 0x7fffffff;
+      ti2[u] = -1;
+    }
+    for (int j = 0; j < ntile; ++j) {
+      const int b = j & 1;
+      tc_bar_wait(ACCF(b), (j >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+#pragma unroll 1
+      for (int c0 = 0; c0 < kTcRows; c0 += 32) {
+        unsigned v[32];
+        const unsigned ta = tmem + ((unsigned)(ew * 32) << 16) + (unsigned)(b * kTcRows + c0);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+              "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]),
+              "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
+              "=r"(v[30]), "=r"(v[31])
+            : "r"(ta));
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        const int cb = j * kTcRows + c0;
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+          const int col = cb + q, u = q & 3;
+          const float dist = col < kc ? fmaf(-2.f, __uint_as_float(v[q]), xn + cn[col]) : CUDART_INF_F;
+          if (dist < tb[u]) {  // strict: within a tracker columns arrive in increasing order
+            tb2[u] = tb[u];
+            ti2[u] = ti[u];
+            tb[u] = dist;
+            ti[u] = col;
+          } else if (dist < tb2[u]) {
+            tb2[u] = dist;
+            ti2[u] = col;
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      tc_bar_arrive(ACCE(b));
+    }
+    // merge the trackers (static indexing only): lowest (dist, index) wins; the
+    // runner-up of a merged pair is min(loser's best, winner's runner-up)
+    float best = tb[0], best2 = tb2[0];
+    int bi = ti[0], bi2 = ti2[0];
+#pragma unroll
+    for (int u = 1; u < 4; ++u) {
+      if (tb[u] < best || (tb[u] == best && ti[u] < bi)) {
+        if (best < tb2[u] || (best == tb2[u] && bi < ti2[u])) {
+          best2 = best;
+          bi2 = bi;
+        } else {
+          best2 = tb2[u];
+          bi2 = ti2[u];
+        }
+        best = tb[u];
+        bi = ti[u];
+      } else if (tb[u] < best2 || (tb[u] == best2 && ti[u] < bi2)) {
+        best2 = tb[u];
+        bi2 = ti[u];
+      }
+    }
+    if (bi == 0x7fffffff) bi = 0;
+    if (pt < M) {
+      // the winner is re-scored in fp64 (exact objective, the fp64 path's
+      // formula); near-ties -- the runner-up within the tensor-core error
+      // band (~1e-6 relative) -- are resolved the same way
+      const bool tie = bi2 >= 0 && best2 - best <= 2e-5f * (xn + cn[bi]);
+      const double* c1 = w.cent + ((size_t)bh * p.k + bi) * d;
+      const double* c2 = w.cent + ((size_t)bh * p.k + (tie ? bi2 : bi)) * d;
+      const __nv_bfloat16* xrow = tc_keys + ((size_t)bh * p.n_tokens + p.sink + pt) * d;
+      double a1 = 0.0, a2 = 0.0, b1 = 0.0, b2 = 0.0;
+#pragma unroll 4
+      for (int e0 = 0; e0 < d; e0 += 8) {  // 16-B key loads, independent chains (latency, not flops)
+        const uint4 raw = *reinterpret_cast<const uint4*>(xrow + e0);
+        const __nv_bfloat162* xh = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const float2 xf = __bfloat1622float2(xh[t]);
+          const double2 u = *reinterpret_cast<const double2*>(c1 + e0 + 2 * t);
+          a1 = fma((double)xf.x, u.x, a1);
+          b1 = fma((double)xf.y, u.y, b1);
+          if (tie) {
+            const double2 z = *reinterpret_cast<const double2*>(c2 + e0 + 2 * t);
+            a2 = fma((double)xf.x, z.x, a2);
+            b2 = fma((double)xf.y, z.y, b2);
+          }
+        }
+      }
+      a1 += b1;
+      a2 += b2;
+      const double xnd = w.xnorm[(size_t)bh * M + pt];
+      double dbest = xnd - 2.0 * a1 + w.cnorm[(size_t)bh * p.k + bi];
+      if (tie) {
+        const double d2 = xnd - 2.0 * a2 + w.cnorm[(size_t)bh * p.k + bi2];
+        if (d2 < dbest || (d2 == dbest && bi2 < bi)) {
+          bi = bi2;
+          dbest = d2;
+        }
+      }
+      w.assign[(size_t)bh * M + pt] = bi;
+      w.sqd[(size_t)bh * M + pt] = fmax(dbest, 0.0);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;\n" ::"r"(tmem));
+}
+
+// centroids (fp64) -> three bf16 terms: hi = bf16(c), mid = bf16(c - hi), lo = bf16(c - hi - mid)
+__global__ void csplit_kernel(dp_cluster_params p, KmWs w) {
+  const int bh = blockIdx.y;
+  if (w.done[bh]) return;
+  const int d = p.head_dim, kc = w.knum[bh];
+  const size_t BHk = (size_t)p.batch * p.kv_heads * p.k;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < kc * d; i += gridDim.x * blockDim.x) {
+    const size_t o = (size_t)bh * p.k * d + i;
+    const double c = w.cent[o];
+    const __nv_bfloat16 hi = __double2bfloat16(c);
+    const double r1 = c - (double)__bfloat162float(hi);
+    const __nv_bfloat16 mid = __double2bfloat16(r1);
+    const double r2 = r1 - (double)__bfloat162float(mid);
+    w.csplit[o] = hi;
+    w.csplit[BHk * d + o] = mid;
+    w.csplit[2 * BHk * d + o] = __double2bfloat16(r2);
+  }
+}
+
+typedef CUresult (*TcEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static cudaError_t tc_map(CUtensorMap* m, const void* ptr, unsigned long long rows, int d) {
+  static TcEncodeFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&fn), cudaEnableDefault, &qr) !=
+            cudaSuccess ||
+        qr != cudaDriverEntryPointSuccess || !fn)
+      return cudaErrorNotSupported;
+  }
+  const cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)d * 2};
+  const cuuint32_t box[2] = {64, (cuuint32_t)(rows < (unsigned long long)kTcRows ? rows : kTcRows)};
+  const cuuint32_t es[2] = {1, 1};
+  const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+static size_t tc_smem_bytes() {
+  return 1024 + 2 * kTcHalf + (size_t)kTcStages * 2 * kTcHalf + kTcMaxK * 4 + 16 * 8 + 16;
+}
+
+static bool tc_supported(const dp_cluster_params* p) {
+  return p->dtype == DP_BF16 && (p->head_dim == 64 || p->head_dim == 128) && p->k <= kTcMaxK &&
+         p->n_tokens - p->sink - p->window >= kTcRows;
+}
+
+static cudaError_t launch_assign_tc(const dp_cluster_params* p, const void* src, KmWs w, cudaStream_t st) {
+  const int BH = p->batch * p->kv_heads;
+  const int M = p->n_tokens - p->sink - p->window;
+  CUtensorMap mx, mc;
+  cudaError_t e = tc_map(&mx, src, (unsigned long long)BH * p->n_tokens, p->head_dim);
+  if (e != cudaSuccess) return e;
+  e = tc_map(&mc, w.csplit, 3ull * BH * p->k, p->head_dim);
+  if (e != cudaSuccess) return e;
+  csplit_kernel<<<dim3((p->k * p->head_dim + 255) / 256, BH), 256, 0, st>>>(*p, w);
+  const size_t smem = tc_smem_bytes();
+  cudaFuncSetAttribute(assign_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  assign_tc_kernel<<<dim3((M + kTcRows - 1) / kTcRows, BH), kTcThreads, smem, st>>>(
+      mx, mc, *p, w, static_cast<const __nv_bfloat16*>(src));
+  return cudaGetLastError();
+}
+
+// -------------------------------------------------------------------------
 // update: one CTA per head.  objective, counts, drop + ascending remap,
 // convergence test, member offsets and a stable counting sort.
 // -------------------------------------------------------------------------
@@ -648,6 +982,8 @@ static int check_params(const dp_cluster_params* p) {
   if (p->max_iters < 1) return set_error(DP_ERR_INVALID, "max_iters must be >= 1");
   if (p->head_dim < 1 || p->head_dim > 256) return set_error(DP_ERR_UNSUPPORTED, "head_dim must be in [1, 256]");
   if (p->dtype != DP_F32 && p->dtype != DP_BF16) return set_error(DP_ERR_INVALID, "unknown dtype");
+  if (p->fp64_assign == 2 && !tc_supported(p))
+    return set_error(DP_ERR_UNSUPPORTED, "tensor-core assignment needs bf16 keys, head_dim 64/128, k <= 4096");
   return DP_OK;
 }
 
@@ -690,7 +1026,10 @@ int dp_cluster_build(const dp_cluster_params* p, const void* src_keys, const voi
   if (e0 != cudaSuccess) return set_cuda_error(e0, "dp_cluster_build (kmeans++)");
   cnorm_kernel<<<dim3((p->k * 32 + 255) / 256, BH), 256, 0, st>>>(*p, w);
   for (int it = 0; it < p->max_iters; ++it) {
-    if (p->fp64_assign)
+    if (p->fp64_assign == 2) {
+      const cudaError_t ea = launch_assign_tc(p, src_keys, w, st);
+      if (ea != cudaSuccess) return set_cuda_error(ea, "dp_cluster_build (tensor-core assign)");
+    } else if (p->fp64_assign)
       assign_kernel<double><<<dim3((M + kAP - 1) / kAP, BH), 256, 0, st>>>(*p, src_keys, w);
     else
       assign_kernel<float><<<dim3((M + kAP - 1) / kAP, BH), 256, 0, st>>>(*p, src_keys, w);

@@ -186,6 +186,35 @@ def test_cluster_build_parity(fp64):
         np.testing.assert_array_equal(rows[: n], keys[0, h][perm[:n]])
 
 
+@pytest.mark.parametrize("d", [64, 128])
+def test_cluster_build_parity_tensor_cores(d):
+    """Lloyd assignment on tcgen05 (bf16 keys exact, centroids as three bf16
+    terms, fp32 TMEM accumulation) against the oracle on the same bf16 keys:
+    assignment agreement >= 1 - 1e-3, final objective within 1e-5."""
+    spec, keys, values, _ = _workload(3072, d, 2, 1, "mixed", 9)
+    n, sink, window = 3072, 4, 64
+    kb = torch.from_numpy(keys[0]).to(torch.bfloat16)
+    keys_b = kb.double().numpy()[None]  # the values the GPU clusters (exact upcast)
+    layer, kd, vd = _layer(keys_b, values, torch.bfloat16, fp64_assign=False, tensor_cores=True)
+    k = O.default_cluster_count(n - sink - window)
+    for h in range(2):
+        t_o, fit = O.build_head_tables(keys_b[0, h], values[0, h], k, sink, window,
+                                       seed_for_head=O.head_seed(0, 0, h))
+        t_g = layer.head_tables(0, h)
+        lab_o = np.full(n, -1)
+        lab_g = np.full(n, -1)
+        for c, m in enumerate(t_o.members):
+            lab_o[m] = c
+        for c, m in enumerate(t_g["members"]):
+            lab_g[m] = c
+        agree = np.mean(lab_o[sink:n - window] == lab_g[sink:n - window])
+        obj_g = layer.objective[h, : int(layer.iters[h])].cpu().numpy()
+        assert agree >= 1 - 1e-3, agree
+        assert abs(obj_g[-1] - fit.objective[-1]) <= 1e-5 * fit.objective[-1]
+        allm = np.sort(np.concatenate(t_g["members"]))
+        np.testing.assert_array_equal(allm, np.arange(sink, n - window))
+
+
 def _gpu_order(layer, ws, G, p1, p2):
     """Full descending order from a debug dp_select over the same log-masses."""
     from paper_2602_05191_b200 import _native as N
