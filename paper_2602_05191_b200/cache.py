@@ -211,11 +211,14 @@ class ClusteredLayer:
 
 def cluster_layer(keys, values, *, k=None, sink=4, window=64, seed=0, max_iters=DEFAULT_MAX_ITERS,
                   tokens_per_cluster=DEFAULT_TOKENS_PER_CLUSTER, layer=0, fp64_assign=True, row_cap=None,
-                  extra_clusters=0, stream=None, head_seeds=None, tensor_cores=False):
+                  extra_clusters=0, stream=None, head_seeds=None, tensor_cores=None):
     """k-means-cluster one layer of a batch on the GPU (`build_clustered_cache`
     for one layer, clustering.py:266-314).  keys/values: CUDA [B,H,N,d] f32
     or bf16 in position order.  ``row_cap``/``extra_clusters`` reserve room
-    for decode-time growth."""
+    for decode-time growth.  ``tensor_cores`` (default: wherever it applies --
+    bf16 keys, d 64/128, k <= 4096, not fp64 mode) runs the Lloyd assignment
+    on tcgen05 with an fp64 re-score of each winner, which reproduces the fp64
+    path's assignments and objective."""
     if keys.dim() != 4 or keys.shape != values.shape:
         raise ValueError("keys/values must have shape (batch, kv_heads, context, dim)")
     if keys.dtype != values.dtype:
@@ -232,6 +235,9 @@ def cluster_layer(keys, values, *, k=None, sink=4, window=64, seed=0, max_iters=
     p = N.ClusterParams()
     p.batch, p.kv_heads, p.head_dim, p.dtype = B, H, d, dtype_code(keys)
     p.n_tokens, p.sink, p.window, p.k = n, sink, window, k
+    if tensor_cores is None:  # the fast path wherever it applies (fp64 mode stays on DFMA)
+        tensor_cores = (not fp64_assign and keys.dtype == torch.bfloat16 and d in (64, 128) and k <= 4096
+                        and middle >= 128)
     p.max_iters, p.fp64_assign = max_iters, 2 if tensor_cores else int(bool(fp64_assign))
 
     def streams(degen=None):
