@@ -819,10 +819,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
 }
 
 }  // namespace dp
-namespace dp { extern int g_plan_cl; }
+namespace dp { extern int g_plan_cl, g_pp_single; }
 extern "C" int dp_debug_set(int key, int value) {
   if (key == 0) dp::g_attn_debug = value;
   if (key == 1) dp::g_plan_cl = value;
+  if (key == 3) dp::g_pp_single = value;
   return 0;
 }
 extern "C" int dp_debug_attn_timing(unsigned long long* out) {

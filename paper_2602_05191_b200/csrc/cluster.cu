@@ -17,12 +17,15 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cooperative_groups.h>
 #include <cuda.h>
 
 #include <string>
 
 #include "common.cuh"
 #include "doublep_b200.h"
+
+namespace cg = cooperative_groups;
 
 namespace dp {
 
@@ -255,16 +258,188 @@ __global__ void __launch_bounds__(kPPThreads) kmeanspp_kernel(dp_cluster_params 
   }
 }
 
+// -------------------------------------------------------------------------
+// k-means++ seeding with one 16-CTA thread-block cluster per head: CTA r owns
+// a contiguous chunk of the points, each thread a contiguous segment of it.
+// Per step: dsq update of my segment (16-B key loads, the single-CTA
+// kernel's fp64 arithmetic), CTA sums pushed to every CTA over DSMEM
+// (barrier 1, everybody forms the same total T in the same order), then the
+// first point whose running dsq sum exceeds u * T -- the sampling draw of
+// Generator.choice(p = dsq / T) in unnormalised form -- found per CTA and
+// pushed (barrier 2); the minimum is the next centre.  ~2 cluster barriers
+// per centre instead of one SM streaming every point.
+// -------------------------------------------------------------------------
+constexpr int kPPCL = 16;          // CTAs per head (non-portable cluster size)
+constexpr int kPPCThreads = 1024;
+
+template <typename T>
+__global__ void __launch_bounds__(kPPCThreads) kmeanspp_cluster_kernel(
+    dp_cluster_params p, const T* __restrict__ src, const int* __restrict__ first_pick,
+    const double* __restrict__ uniforms, const int* __restrict__ alt_picks, int* __restrict__ degenerate_from,
+    int* __restrict__ picks, KmWs w) {
+  cg::cluster_group cluster = cg::this_cluster();
+  const int r = (int)cluster.block_rank();
+  const int bh = blockIdx.x / kPPCL;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int M = p.n_tokens - p.sink - p.window, d = p.head_dim, k = p.k;
+  const int chunk = (M + kPPCL - 1) / kPPCL;
+  const int c0 = min(M, r * chunk), c1 = min(M, c0 + chunk);
+  const int per = (c1 - c0 + nt - 1) / nt;
+  const int beg = min(c1, c0 + tid * per), end = min(c1, beg + per);
+  const int chunks = d * (int)sizeof(T) / 16;
+  __shared__ double c[256];
+  __shared__ double red[33];
+  __shared__ double s_sum[kPPCL];
+  __shared__ int s_cand[kPPCL];
+  __shared__ double s_cn;
+  __shared__ int s_idx, s_degen, s_mine;
+  const T* X = src + ((size_t)bh * p.n_tokens + p.sink) * d;
+  const double* xn = w.xnorm + (size_t)bh * M;
+  double* dsq = w.dsq + (size_t)bh * M;
+  const int degen_in = degenerate_from ? degenerate_from[bh] : k;
+  if (tid == 0) {
+    s_degen = k;
+    s_idx = first_pick[bh];
+  }
+  __syncthreads();
+  for (int i = 0; i < k; ++i) {
+    const int idx = s_idx;
+    if (r == 0 && tid == 0) picks[(size_t)bh * k + i] = idx;
+    for (int j = tid; j < d; j += nt) {
+      const double x = (double)to_float(X[(size_t)idx * d + j]);
+      c[j] = x;
+      if (r == 0) w.cent[((size_t)bh * k + i) * d + j] = x;
+    }
+    __syncthreads();
+    if (tid < 32) {
+      double a = 0.0;
+      for (int j = tid; j < d; j += 32) a = fma(c[j], c[j], a);
+      a = warp_sum(a);
+      if (tid == 0) s_cn = a;
+    }
+    __syncthreads();
+    const double cn = s_cn;
+    double loc = 0.0;
+#pragma unroll 1
+    for (int pt = beg; pt < end; ++pt) {
+      const int4* row = reinterpret_cast<const int4*>(X + (size_t)pt * d);
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll 4
+      for (int cc = 0; cc < chunks; ++cc) {
+        const int4 raw = __ldg(row + cc);
+        if constexpr (sizeof(T) == 2) {
+          const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+          const double* cj = c + cc * 8;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 f = __bfloat1622float2(h[e]);
+            if (e & 1) {
+              a2 = fma((double)f.x, cj[2 * e], a2);
+              a3 = fma((double)f.y, cj[2 * e + 1], a3);
+            } else {
+              a0 = fma((double)f.x, cj[2 * e], a0);
+              a1 = fma((double)f.y, cj[2 * e + 1], a1);
+            }
+          }
+        } else {
+          const float* f = reinterpret_cast<const float*>(&raw);
+          const double* cj = c + cc * 4;
+          a0 = fma((double)f[0], cj[0], a0);
+          a1 = fma((double)f[1], cj[1], a1);
+          a2 = fma((double)f[2], cj[2], a2);
+          a3 = fma((double)f[3], cj[3], a3);
+        }
+      }
+      const double dist = fmax(xn[pt] - 2.0 * ((a0 + a1) + (a2 + a3)) + cn, 0.0);
+      const double nd = (i == 0) ? dist : fmin(dsq[pt], dist);
+      dsq[pt] = nd;
+      loc += nd;
+    }
+    if (i + 1 == k) break;
+    // ---- draw centre i+1 ------------------------------------------------
+    const double mine = block_sum(loc, red);
+    if (tid < kPPCL) *cluster.map_shared_rank(&s_sum[r], tid) = mine;
+    cluster.sync();  // (1) every CTA holds every chunk sum
+    double total = 0.0, before = 0.0;
+    for (int q = 0; q < kPPCL; ++q) {
+      if (q < r) before += s_sum[q];
+      total += s_sum[q];
+    }
+    const int step = i + 1;
+    if (total > 0.0 && step < degen_in) {
+      double last;
+      const double off = block_exclusive_scan(loc, red, &last);
+      const double thr = uniforms[(size_t)bh * (k - 1) + (step - 1)] * total;
+      if (tid == 0) s_mine = M;
+      __syncthreads();
+      double run = before + off;
+      for (int j = beg; j < end; ++j) {
+        run += dsq[j];
+        if (run > thr) {
+          atomicMin(&s_mine, j);
+          break;
+        }
+      }
+      __syncthreads();
+      if (tid < kPPCL) *cluster.map_shared_rank(&s_cand[r], tid) = s_mine;
+      cluster.sync();  // (2) every CTA's first crossing
+      if (tid == 0) {
+        int pick = M;
+        for (int q = 0; q < kPPCL; ++q) pick = min(pick, s_cand[q]);
+        s_idx = pick >= M ? M - 1 : pick;
+      }
+    } else if (tid == 0) {
+      if (step >= degen_in && alt_picks) {
+        s_idx = alt_picks[(size_t)bh * (k - 1) + (step - 1)];
+      } else {
+        if (s_degen == k) s_degen = step;
+        s_idx = 0;
+      }
+    }
+    __syncthreads();
+  }
+  if (r == 0 && tid == 0) {
+    if (degenerate_from) degenerate_from[bh] = s_degen;
+    w.knum[bh] = k;
+    w.done[bh] = 0;
+  }
+  cluster.sync();  // no CTA exits while a peer may still push into its shared memory
+}
+
 static size_t pp_smem(const dp_cluster_params* p) {
   const int es = p->dtype == DP_F32 ? 4 : 2;
   const int stages = p->dtype == DP_F32 ? 1 : 2;
   return ((p->head_dim * 8 + 127) / 128) * 128 + (size_t)stages * kPPThreads * (p->head_dim * es + 16);
 }
 
+int g_pp_single = 0;  // 1: the one-CTA-per-head seeding kernel (dp_debug_set(3, 1))
+
+template <typename T>
+static cudaError_t launch_pp_cluster(const dp_cluster_params* p, const T* src, const int* first, const double* u,
+                                     const int* alt, int* degen, int* picks, KmWs w, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(p->batch * p->kv_heads * kPPCL));
+  cfg.blockDim = dim3(kPPCThreads);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = kPPCL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaFuncSetAttribute(kmeanspp_cluster_kernel<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  return cudaLaunchKernelEx(&cfg, kmeanspp_cluster_kernel<T>, *p, src, first, u, alt, degen, picks, w);
+}
+
 static cudaError_t launch_kmeanspp(const dp_cluster_params* p, const void* src, const int* first,
                                    const double* u, const int* alt, int* degen, int* picks, KmWs w,
                                    cudaStream_t st) {
   const int BH = p->batch * p->kv_heads;
+  if (!g_pp_single && p->head_dim <= 256) {
+    if (p->dtype == DP_F32) return launch_pp_cluster(p, (const float*)src, first, u, alt, degen, picks, w, st);
+    return launch_pp_cluster(p, (const __nv_bfloat16*)src, first, u, alt, degen, picks, w, st);
+  }
   const size_t smem = pp_smem(p);
   if (p->dtype == DP_F32) {
     cudaFuncSetAttribute(kmeanspp_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
