@@ -612,6 +612,7 @@ __global__ void __launch_bounds__(kPT, 1)
         }
       }
       __syncthreads();
+      stamp(r, 11);
       if (tid == 0) {  // segment offsets in rank order: range bins ascending, then b1
         int o = 0;
         for (int j = 0; j <= kCandBins; ++j) {
@@ -637,6 +638,7 @@ __global__ void __launch_bounds__(kPT, 1)
         cord[s_boff[ba == b1 ? kCandBins : ba - rlo] + rk] = ia;
       }
       __syncthreads();
+      stamp(r, 12);
       const int o1 = s_boff[kCandBins], n1c = s_bcnt[kCandBins];
       const int j1 = sel_cut(&s_sel, um, cord + o1, n1c, before1, thr1);
       cut1 = j1 < n1c ? j1 + 1 : n1c;
