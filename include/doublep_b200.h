@@ -280,7 +280,7 @@ int dp_debug_plan_clock(unsigned long long* out);
 int dp_debug_attn_timing(unsigned long long* out);
 /* Profiling switches: key 0 = attention flags (bit 0: skip the math, stream
  * K/V only); key 1 = force the plan cluster size (8 or 16; 0 = auto); key 3 = 1
- * runs k-means++ seeding on one CTA per head instead of a 16-CTA cluster.
+ * runs k-means++ seeding on one CTA per head instead of an 8-CTA cluster.
  * Never set on the product path. */
 int dp_debug_set(int key, int value);
 /* Profiling aid: co-resident plan clusters at this geometry for cluster size

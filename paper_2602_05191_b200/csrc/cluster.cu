@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(kPPThreads) kmeanspp_kernel(dp_cluster_params 
 }
 
 // -------------------------------------------------------------------------
-// k-means++ seeding with one 16-CTA thread-block cluster per head: CTA r owns
+// k-means++ seeding with one 8-CTA thread-block cluster per head: CTA r owns
 // a contiguous chunk of the points, each thread a contiguous segment of it.
 // Per step: dsq update of my segment (16-B key loads, the single-CTA
 // kernel's fp64 arithmetic), CTA sums pushed to every CTA over DSMEM
@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(kPPThreads) kmeanspp_kernel(dp_cluster_params 
 // pushed (barrier 2); the minimum is the next centre.  ~2 cluster barriers
 // per centre instead of one SM streaming every point.
 // -------------------------------------------------------------------------
-constexpr int kPPCL = 16;          // CTAs per head (non-portable cluster size)
+constexpr int kPPCL = 8;           // CTAs per head (16-CTA clusters: only 7 co-resident on B200)
 constexpr int kPPCThreads = 1024;
 
 template <typename T>
@@ -304,6 +304,8 @@ __global__ void __launch_bounds__(kPPCThreads) kmeanspp_cluster_kernel(
   __syncthreads();
   for (int i = 0; i < k; ++i) {
     const int idx = s_idx;
+    // this step's uniform, loaded while the centre row and the dsq update are in flight
+    const double u_next = i + 1 < k ? __ldg(&uniforms[(size_t)bh * (k - 1) + i]) : 0.0;
     if (r == 0 && tid == 0) picks[(size_t)bh * k + i] = idx;
     for (int j = tid; j < d; j += nt) {
       const double x = (double)to_float(X[(size_t)idx * d + j]);
@@ -369,7 +371,7 @@ __global__ void __launch_bounds__(kPPCThreads) kmeanspp_cluster_kernel(
     if (total > 0.0 && step < degen_in) {
       double last;
       const double off = block_exclusive_scan(loc, red, &last);
-      const double thr = uniforms[(size_t)bh * (k - 1) + (step - 1)] * total;
+      const double thr = u_next * total;
       if (tid == 0) s_mine = M;
       __syncthreads();
       double run = before + off;
@@ -583,7 +585,7 @@ constexpr int kTcRows = 128;                   // points per CTA = centroids per
 constexpr int kTcStages = 2;                   // ring of (tile, term) stages (2 CTAs per SM hide each other's tails)
 constexpr int kTcHalf = kTcRows * 128;         // one 64-column swizzle half: 128 rows x 128 B
 constexpr int kTcMaxK = 4096;
-constexpr int kTcThreads = 256;
+constexpr int kTcThreads = 384;  // warp 0 TMA, warp 1 MMA, warps 4-11 epilogue (two per TMEM lane quarter)
 
 __device__ __forceinline__ unsigned tc_smem(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
@@ -636,6 +638,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(cn + kTcMaxK);
   // bars: full[4], empty[4], afull, accf[2], acce[2]
   unsigned* tslot = reinterpret_cast<unsigned*>(bars + 16);
+  __shared__ float s_hb[kTcRows], s_hb2[kTcRows];
+  __shared__ int s_hi[kTcRows], s_hi2[kTcRows];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const unsigned b0 = tc_smem(bars);
   auto FULL = [&](int s) { return b0 + 8u * s; };
@@ -651,7 +655,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     tc_bar_init(AFULL, 1);
     for (int b = 0; b < 2; ++b) {
       tc_bar_init(ACCF(b), 1);
-      tc_bar_init(ACCE(b), 128);
+      tc_bar_init(ACCE(b), 256);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -710,8 +714,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                        : "memory");
       }
     }
-  } else if (warp >= 4) {  // epilogue: TMEM lanes 32*(warp-4) .. +31 = my points
-    const int ew = warp - 4, row = ew * 32 + lane, pt = p0 + row;
+  } else if (warp >= 4) {  // epilogue: TMEM lane quarter warp % 4 = my 32 points; column half (warp - 4) / 4
+    const int ew = (warp - 4) & 3, half = (warp - 4) >> 2, row = ew * 32 + lane, pt = p0 + row;
     const float xn = pt < M ? (float)w.xnorm[(size_t)bh * M + pt] : 0.f;
     // four independent (best, runner-up) trackers over columns q % 4: the
     // compare chain is the epilogue's critical path, so it gets ILP
@@ -728,7 +732,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       tc_bar_wait(ACCF(b), (j >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
 #pragma unroll 1
-      for (int c0 = 0; c0 < kTcRows; c0 += 32) {
+      for (int c0 = half * (kTcRows / 2); c0 < (half + 1) * (kTcRows / 2); c0 += 32) {
         unsigned v[32];
         const unsigned ta = tmem + ((unsigned)(ew * 32) << 16) + (unsigned)(b * kTcRows + c0);
         asm volatile(
@@ -781,6 +785,34 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         bi2 = ti[u];
       }
     }
+    // the two column halves of a row meet in shared memory (named barrier over
+    // the 8 epilogue warps); half 0 merges and finishes the row
+    if (half == 1) {
+      s_hb[row] = best;
+      s_hb2[row] = best2;
+      s_hi[row] = bi;
+      s_hi2[row] = bi2;
+    }
+    asm volatile("bar.sync 2, 256;\n" ::: "memory");
+    if (half == 1) goto epilogue_done;
+    {
+      const float ob = s_hb[row], ob2 = s_hb2[row];
+      const int oi = s_hi[row], oi2 = s_hi2[row];
+      if (ob < best || (ob == best && oi < bi)) {
+        if (best < ob2 || (best == ob2 && bi < oi2)) {
+          best2 = best;
+          bi2 = bi;
+        } else {
+          best2 = ob2;
+          bi2 = oi2;
+        }
+        best = ob;
+        bi = oi;
+      } else if (ob < best2 || (ob == best2 && oi < bi2)) {
+        best2 = ob;
+        bi2 = oi;
+      }
+    }
     if (bi == 0x7fffffff) bi = 0;
     if (pt < M) {
       // the winner is re-scored in fp64 (exact objective, the fp64 path's
@@ -822,6 +854,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       w.assign[(size_t)bh * M + pt] = bi;
       w.sqd[(size_t)bh * M + pt] = fmax(dbest, 0.0);
     }
+  epilogue_done:;
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
