@@ -276,7 +276,7 @@ template <typename T>
 __global__ void __launch_bounds__(kPPCThreads) kmeanspp_cluster_kernel(
     dp_cluster_params p, const T* __restrict__ src, const int* __restrict__ first_pick,
     const double* __restrict__ uniforms, const int* __restrict__ alt_picks, int* __restrict__ degenerate_from,
-    int* __restrict__ picks, KmWs w) {
+    int* __restrict__ picks, KmWs w, int use_smem) {
   cg::cluster_group cluster = cg::this_cluster();
   const int r = (int)cluster.block_rank();
   const int bh = blockIdx.x / kPPCL;
@@ -295,7 +295,10 @@ __global__ void __launch_bounds__(kPPCThreads) kmeanspp_cluster_kernel(
   __shared__ int s_idx, s_degen, s_mine;
   const T* X = src + ((size_t)bh * p.n_tokens + p.sink) * d;
   const double* xn = w.xnorm + (size_t)bh * M;
-  double* dsq = w.dsq + (size_t)bh * M;
+  // the chunk's dsq lives in shared memory when it fits (no global round trip
+  // per point per centre), else in the workspace
+  extern __shared__ double sdsq[];
+  double* D = use_smem ? sdsq : w.dsq + (size_t)bh * M + c0;  // indexed by pt - c0
   const int degen_in = degenerate_from ? degenerate_from[bh] : k;
   if (tid == 0) {
     s_degen = k;
@@ -353,8 +356,8 @@ __global__ void __launch_bounds__(kPPCThreads) kmeanspp_cluster_kernel(
         }
       }
       const double dist = fmax(xn[pt] - 2.0 * ((a0 + a1) + (a2 + a3)) + cn, 0.0);
-      const double nd = (i == 0) ? dist : fmin(dsq[pt], dist);
-      dsq[pt] = nd;
+      const double nd = (i == 0) ? dist : fmin(D[pt - c0], dist);
+      D[pt - c0] = nd;
       loc += nd;
     }
     if (i + 1 == k) break;
@@ -376,7 +379,7 @@ __global__ void __launch_bounds__(kPPCThreads) kmeanspp_cluster_kernel(
       __syncthreads();
       double run = before + off;
       for (int j = beg; j < end; ++j) {
-        run += dsq[j];
+        run += D[j - c0];
         if (run > thr) {
           atomicMin(&s_mine, j);
           break;
@@ -430,8 +433,13 @@ static cudaError_t launch_pp_cluster(const dp_cluster_params* p, const T* src, c
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaFuncSetAttribute(kmeanspp_cluster_kernel<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  return cudaLaunchKernelEx(&cfg, kmeanspp_cluster_kernel<T>, *p, src, first, u, alt, degen, picks, w);
+  const int M = p->n_tokens - p->sink - p->window;
+  const size_t dbytes = (size_t)((M + kPPCL - 1) / kPPCL) * sizeof(double);
+  const int use_smem = dbytes <= 200 * 1024;
+  cfg.dynamicSmemBytes = use_smem ? dbytes : 0;
+  if (use_smem)
+    cudaFuncSetAttribute(kmeanspp_cluster_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dbytes);
+  return cudaLaunchKernelEx(&cfg, kmeanspp_cluster_kernel<T>, *p, src, first, u, alt, degen, picks, w, use_smem);
 }
 
 static cudaError_t launch_kmeanspp(const dp_cluster_params* p, const void* src, const int* first,
