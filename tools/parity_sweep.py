@@ -1,7 +1,7 @@
 """Randomised parity sweep of the fused decode path against the CPU oracle
 (the §8c protocol of tests/test_gpu_parity.py, over many random geometries).
 
-    python tools/parity_sweep.py [cases] [seed]
+    python tools/parity_sweep.py [cases] [seed] [max_context]
 
 Each case draws (context, kv heads, G, head dim, dtype, tail profile, p1, p2,
 plan cluster size), builds the workload with the reference generator law,
@@ -32,12 +32,14 @@ TOL = {torch.float32: 1e-5, torch.bfloat16: 2e-3}
 def main():
     cases = int(sys.argv[1]) if len(sys.argv) > 1 else 40
     rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 1234)
+    nmax = int(sys.argv[3]) if len(sys.argv) > 3 else 40000
+    sizes = [x for x in (300, 700, 1500, 3000, 6000, 12000, 24000, 40000) if x <= nmax]
     totals = {"heads": 0, "exact": 0, "order_tie": 0, "threshold_tie": 0, "real": 0, "out_checked": 0,
               "out_fail": 0, "lm_fail": 0}
     worst = {torch.float32: 0.0, torch.bfloat16: 0.0}
     t0 = time.time()
     for c in range(cases):
-        n = int(rng.choice([300, 700, 1500, 3000, 6000, 12000, 24000, 40000]))
+        n = int(rng.choice(sizes))
         H = int(rng.choice([1, 2, 3]))
         G = int(rng.choice([1, 2, 3, 4, 6, 8]))
         d = int(rng.choice([32, 64, 128, 128]))
