@@ -238,7 +238,8 @@ typedef struct dp_cluster_params {
   int32_t n_tokens, sink, window;
   int32_t k;          /* requested clusters (already clamped to middle) */
   int32_t max_iters;
-  int32_t fp64_assign; /* 1: fp64 distances (reference-exact); 0: fp32 */
+  int32_t fp64_assign; /* 1: fp64 distances (reference-exact); 0: fp32 FFMA; 2: tcgen05 tensor cores
+                          (bf16 keys, head_dim 64/128, k <= 4096; winners re-scored in fp64) */
 } dp_cluster_params;
 
 /* Workspace for dp_cluster_build. */
