@@ -593,7 +593,7 @@ constexpr int kTcRows = 128;                   // points per CTA = centroids per
 constexpr int kTcStages = 2;                   // ring of (tile, term) stages (2 CTAs per SM hide each other's tails)
 constexpr int kTcHalf = kTcRows * 128;         // one 64-column swizzle half: 128 rows x 128 B
 constexpr int kTcMaxK = 4096;
-constexpr int kTcThreads = 384;  // warp 0 TMA, warp 1 MMA, warps 4-11 epilogue (two per TMEM lane quarter)
+constexpr int kTcThreads = 256;  // warp 0 TMA, warp 1 MMA, warps 4-7 epilogue (one per TMEM lane quarter)
 
 __device__ __forceinline__ unsigned tc_smem(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
@@ -626,7 +626,7 @@ __device__ __forceinline__ unsigned long long tc_desc(unsigned saddr) {
          (1ull << 46) | (2ull << 61);
 }
 
-__global__ void __launch_bounds__(kTcThreads, 1)
+__global__ void __launch_bounds__(kTcThreads, 2)
     assign_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmC,
                      dp_cluster_params p, KmWs w, const __nv_bfloat16* __restrict__ tc_keys) {
   const int bh = blockIdx.y;
@@ -642,12 +642,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tc_raw) + 1023) & ~uintptr_t(1023));
   unsigned char* As = base;                                      // keys tile [halves][128 x 128 B]
   unsigned char* Bs = As + 2 * kTcHalf;                          // ring [stages][halves][128 x 128 B]
-  float* cn = reinterpret_cast<float*>(Bs + kTcStages * 2 * kTcHalf);  // [kTcMaxK] centroid norms
-  unsigned long long* bars = reinterpret_cast<unsigned long long*>(cn + kTcMaxK);
+  float* cn = reinterpret_cast<float*>(Bs + kTcStages * 2 * kTcHalf);  // [kpad] centroid norms
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(cn + ((p.k + 31) & ~31));
   // bars: full[4], empty[4], afull, accf[2], acce[2]
   unsigned* tslot = reinterpret_cast<unsigned*>(bars + 16);
-  __shared__ float s_hb[kTcRows], s_hb2[kTcRows];
-  __shared__ int s_hi[kTcRows], s_hi2[kTcRows];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const unsigned b0 = tc_smem(bars);
   auto FULL = [&](int s) { return b0 + 8u * s; };
@@ -663,7 +661,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     tc_bar_init(AFULL, 1);
     for (int b = 0; b < 2; ++b) {
       tc_bar_init(ACCF(b), 1);
-      tc_bar_init(ACCE(b), 256);
+      tc_bar_init(ACCE(b), 128);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -722,8 +720,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                        : "memory");
       }
     }
-  } else if (warp >= 4) {  // epilogue: TMEM lane quarter warp % 4 = my 32 points; column half (warp - 4) / 4
-    const int ew = (warp - 4) & 3, half = (warp - 4) >> 2, row = ew * 32 + lane, pt = p0 + row;
+  } else if (warp >= 4) {  // epilogue: TMEM lane quarter warp % 4 = my 32 points
+    const int ew = warp - 4, row = ew * 32 + lane, pt = p0 + row;
     const float xn = pt < M ? (float)w.xnorm[(size_t)bh * M + pt] : 0.f;
     // four independent (best, runner-up) trackers over columns q % 4: the
     // compare chain is the epilogue's critical path, so it gets ILP
@@ -740,22 +738,18 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       tc_bar_wait(ACCF(b), (j >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
 #pragma unroll 1
-      for (int c0 = half * (kTcRows / 2); c0 < (half + 1) * (kTcRows / 2); c0 += 32) {
-        unsigned v[32];
+      for (int c0 = 0; c0 < kTcRows; c0 += 16) {
+        unsigned v[16];
         const unsigned ta = tmem + ((unsigned)(ew * 32) << 16) + (unsigned)(b * kTcRows + c0);
         asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
             : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
-              "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]),
-              "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
-              "=r"(v[30]), "=r"(v[31])
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
             : "r"(ta));
         asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
         const int cb = j * kTcRows + c0;
 #pragma unroll
-        for (int q = 0; q < 32; ++q) {
+        for (int q = 0; q < 16; ++q) {
           const int col = cb + q, u = q & 3;
           const float dist = col < kc ? fmaf(-2.f, __uint_as_float(v[q]), xn + cn[col]) : CUDART_INF_F;
           if (dist < tb[u]) {  // strict: within a tracker columns arrive in increasing order
@@ -791,34 +785,6 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       } else if (tb[u] < best2 || (tb[u] == best2 && ti[u] < bi2)) {
         best2 = tb[u];
         bi2 = ti[u];
-      }
-    }
-    // the two column halves of a row meet in shared memory (named barrier over
-    // the 8 epilogue warps); half 0 merges and finishes the row
-    if (half == 1) {
-      s_hb[row] = best;
-      s_hb2[row] = best2;
-      s_hi[row] = bi;
-      s_hi2[row] = bi2;
-    }
-    asm volatile("bar.sync 2, 256;\n" ::: "memory");
-    if (half == 1) goto epilogue_done;
-    {
-      const float ob = s_hb[row], ob2 = s_hb2[row];
-      const int oi = s_hi[row], oi2 = s_hi2[row];
-      if (ob < best || (ob == best && oi < bi)) {
-        if (best < ob2 || (best == ob2 && bi < oi2)) {
-          best2 = best;
-          bi2 = bi;
-        } else {
-          best2 = ob2;
-          bi2 = oi2;
-        }
-        best = ob;
-        bi = oi;
-      } else if (ob < best2 || (ob == best2 && oi < bi2)) {
-        best2 = ob;
-        bi2 = oi;
       }
     }
     if (bi == 0x7fffffff) bi = 0;
@@ -862,7 +828,6 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       w.assign[(size_t)bh * M + pt] = bi;
       w.sqd[(size_t)bh * M + pt] = fmax(dbest, 0.0);
     }
-  epilogue_done:;
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
@@ -911,8 +876,8 @@ static cudaError_t tc_map(CUtensorMap* m, const void* ptr, unsigned long long ro
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-static size_t tc_smem_bytes() {
-  return 1024 + 2 * kTcHalf + (size_t)kTcStages * 2 * kTcHalf + kTcMaxK * 4 + 16 * 8 + 16;
+static size_t tc_smem_bytes(int k) {  // ~101 KB at k = 1022: two CTAs per SM
+  return 1024 + 2 * kTcHalf + (size_t)kTcStages * 2 * kTcHalf + (size_t)((k + 31) & ~31) * 4 + 16 * 8 + 16;
 }
 
 static bool tc_supported(const dp_cluster_params* p) {
@@ -929,7 +894,7 @@ static cudaError_t launch_assign_tc(const dp_cluster_params* p, const void* src,
   e = tc_map(&mc, w.csplit, 3ull * BH * p->k, p->head_dim);
   if (e != cudaSuccess) return e;
   csplit_kernel<<<dim3((p->k * p->head_dim + 255) / 256, BH), 256, 0, st>>>(*p, w);
-  const size_t smem = tc_smem_bytes();
+  const size_t smem = tc_smem_bytes(p->k);
   cudaFuncSetAttribute(assign_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   assign_tc_kernel<<<dim3((M + kTcRows - 1) / kTcRows, BH), kTcThreads, smem, st>>>(
       mx, mc, *p, w, static_cast<const __nv_bfloat16*>(src));

@@ -181,3 +181,41 @@ def test_token_topk_ties_lower_position():
                                          v[0, 0].double().cpu().numpy(), budget)
         np.testing.assert_array_equal(got, np.sort(idx))
         np.testing.assert_allclose(out[0, 0].cpu().numpy(), o_out.output, rtol=1e-11, atol=1e-12)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_mixed_attention_f64_matches_oracle(dtype):
+    """dp_mixed_attention_f64 (the runner's fp64 evaluation path) on the fused
+    plan's states equals the oracle's mixed_attention fed the same GPU tables
+    to fp64 rounding (1e-12), and with no states equals full attention."""
+    from paper_2602_05191_b200 import cluster_layer, sparse_attention
+    from paper_2602_05191_b200 import metrics as M
+
+    B, H, G, n, d = 1, 2, 4, 2500, 64
+    spec = O.WorkloadSpec(context_len=n, head_dim=d, num_kv_heads=H, gqa_group=G, num_steps=1,
+                          tail_profile="mixed", seed=77)
+    keys, values, queries = O.generate(spec)
+    kd = torch.from_numpy(keys[0]).cuda().to(dtype).unsqueeze(0)
+    vd = torch.from_numpy(values[0]).cuda().to(dtype).unsqueeze(0)
+    q = torch.from_numpy(queries[0, 0]).cuda().to(dtype).unsqueeze(0)
+    layer = cluster_layer(kd, vd, fp64_assign=False)
+    _, ws = sparse_attention(q, layer, 0.9, 0.7, return_plan=True)
+    out, lse = M.mixed_attention_f64(q, layer, ws.state, ws.log_mass)
+    full, flse = M.mixed_attention_f64(q, layer)
+    kf, vf = kd[0].double().cpu().numpy(), vd[0].double().cpu().numpy()
+    st = ws.state[0].cpu().numpy()
+    lm = ws.log_mass[0].cpu().numpy()
+    for hq in range(H * G):
+        h = hq // G
+        t = oracle_tables(layer, 0, h)
+        K = len(t.members)
+        qv = q[0, hq].double().cpu().numpy()
+        exact = np.sort(np.concatenate([np.arange(layer.sink), np.arange(n - layer.window, n),
+                                        *[t.members[c] for c in range(K) if st[hq, c] == 2]]))
+        approx = np.array([c for c in range(K) if st[hq, c] == 1], dtype=np.int64)
+        est = O.Estimate(log_masses=lm[hq, :K], probs=None, order=None)
+        ref = O.mixed_attention(qv, kf[h], vf[h], t, exact, approx, est)
+        assert O.output_error(out[0, hq].cpu().numpy(), ref.output) <= 1e-12
+        assert float(lse[0, hq]) == pytest.approx(ref.log_normalizer, abs=1e-12)
+        dense = O.full_attention(qv, kf[h], vf[h])
+        assert O.output_error(full[0, hq].cpu().numpy(), dense.output) <= 1e-12
