@@ -20,6 +20,7 @@ from .engine import (
     PRESETS,
     AttentionOutput,
     ClusterEstimate,
+    DecodeGraph,
     DecodeWorkspace,
     DoublePConfig,
     SelectionPlan,
@@ -50,7 +51,7 @@ __version__ = "0.1.0"
 BACKEND = "b200"
 
 __all__ = [
-    "AttentionOutput", "BACKEND", "ClusterEstimate", "ClusteredCache", "ClusteredLayer", "DecodeWorkspace",
+    "AttentionOutput", "BACKEND", "ClusterEstimate", "ClusteredCache", "ClusteredLayer", "DecodeGraph", "DecodeWorkspace",
     "DoublePConfig", "KvCache", "PRESETS", "SelectionPlan", "TopPResult", "build_cache_for_config",
     "build_clustered_cache", "cluster_layer", "cluster_topk_attention", "decode_step", "default_cluster_count", "dense_attention",
     "estimate_cluster_distribution", "full_attention", "head_seed", "plan_selection", "sparse_attention",

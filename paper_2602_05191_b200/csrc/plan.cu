@@ -204,7 +204,11 @@ struct SelShared {
 __device__ __noinline__ int sel_find_bin(SelShared* sh, const unsigned long long* bm, const int* bc,
                                          unsigned long long mbase, int cbase, double thr, int limit) {
   const int tid = threadIdx.x;
-  if (tid == 0) sh->b = kBins;
+  if (tid == 0) {  // not found (no mass at all: a non-finite query) -> nothing ahead of the last bin
+    sh->b = kBins;
+    sh->before = 0;
+    sh->cbefore = 0;
+  }
   __syncthreads();
   unsigned long long m = mbase, hmass = 0;
   int c = cbase, hit = -1, hcnt = 0;
@@ -443,7 +447,10 @@ __global__ void __launch_bounds__(kPT, 1)
         for (int e = 0; e < 2; ++e) {
           const int h = 2 * (lane & 3) + e;
           if (h < G) {
-            const double val = ((c[0][e] + c[1][e]) + (c[2][e] + c[3][e])) * scale + ls;
+            double val = ((c[0][e] + c[1][e]) + (c[2][e] + c[3][e])) * scale + ls;
+            // a non-finite query must not break the selection's ordering: NaN
+            // ranks last (-inf), +inf first (the largest finite double)
+            val = val != val ? -CUDART_INF : fmin(val, 1.7976931348623157e308);
             lml[h * L.per + row] = val;
             remote(cluster, lmall, h)[k0 + row] = val;
             lmax[e] = fmax(lmax[e], val);
@@ -518,7 +525,7 @@ __global__ void __launch_bounds__(kPT, 1)
     stamp(r, 20);
 #pragma unroll 1
     for (int i = tid; i < K; i += kPT) {
-      const float xf = (float)(M - lmall[i]);  // >= 0
+      const float xf = M == -CUDART_INF ? CUDART_INF_F : (float)(M - lmall[i]);  // >= 0 (+inf: no mass)
       const unsigned long long u = __float2ull_rn(__expf(-xf) * (float)kFix);
       int b = (int)(xf * kBinScale);
       b = b < 0 ? 0 : (b >= kBins ? kBins - 1 : b);
@@ -551,7 +558,8 @@ __global__ void __launch_bounds__(kPT, 1)
     if (K > 0) {
       // stage 1 (selection.py:57-58): the bin where the mass crosses p1 * total
       const double thr1 = p1 * (double)total;
-      const int b1 = sel_find_bin(&s_sel, bm, bc, mbase, cbase, thr1, kBins);  // always found
+      // always found for finite scores; a non-finite query must not index out of range
+      const int b1 = min(sel_find_bin(&s_sel, bm, bc, mbase, cbase, thr1, kBins), kBins - 1);
       const unsigned long long before1 = s_sel.before;
       cbefore1 = s_sel.cbefore;
       stamp(r, 23);
@@ -671,7 +679,7 @@ __global__ void __launch_bounds__(kPT, 1)
             stown[i] = (uint8_t)(j < cut2 ? 2 : 1);
           }
         } else {  // wide range: rank b2 on its own after emitting b1's states
-          b2 = sel_find_bin(&s_sel, bm, bc, mbase, cbase, thr2, b1);
+          b2 = min(sel_find_bin(&s_sel, bm, bc, mbase, cbase, thr2, b1), b1);
           const unsigned long long before2 = s_sel.before;
           const int cbefore2 = s_sel.cbefore;
 #pragma unroll 1

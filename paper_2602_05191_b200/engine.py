@@ -131,6 +131,48 @@ def _sparse_layer(q, layer, p1=0.95, p2=0.7, *, workspace=None, return_plan=Fals
     return (out, ws) if return_plan else out
 
 
+class DecodeGraph:
+    """One decode step over several layers captured as a CUDA graph -- the
+    serving-engine form of the product path.  Every replay runs, for each
+    layer li, exactly the eager ``sparse_attention(q[li], layers[li], p1, p2)``
+    launches (plan + attend, PDL-chained) into ``out[li]``, without the
+    per-call host work.  ``q`` [L,B,Hq,d] and ``out`` [L,B,Hq,d] fp32 are fixed
+    device buffers: fill ``q`` (e.g. a non-blocking copy from pinned host
+    memory), ``replay()``, read ``out``.  Layers share one geometry (and one
+    workspace, reused layer after layer as in the eager path)."""
+
+    def __init__(self, layers, q, p1=0.95, p2=0.7, *, out=None, workspace=None):
+        for name, val in (("p1", p1), ("p2", p2)):
+            if not 0.0 < val <= 1.0:
+                raise ValueError(f"{name} must be in (0, 1], got {val}")
+        if q.dim() != 4 or q.shape[0] != len(layers):
+            raise ValueError(f"q must be [layers, B, Hq, d] with {len(layers)} layers, got {tuple(q.shape)}")
+        G = _group(q[0], layers[0])
+        ws = workspace if workspace is not None else DecodeWorkspace(layers[0], G)
+        for lay in layers:
+            if not ws.fits(lay, G):
+                raise ValueError("DecodeGraph layers must share one geometry (the workspace does not fit)")
+        dev = layers[0].device
+        self.layers, self.q, self.ws = list(layers), q, ws
+        self.out = out if out is not None else torch.empty(q.shape, dtype=torch.float32, device=dev)
+        if self.out.dtype != torch.float32 or self.out.shape != q.shape or not self.out.is_contiguous():
+            raise ValueError(f"out must be a contiguous float32 tensor of shape {tuple(q.shape)}")
+        self.p1, self.p2 = p1, p2
+        self._step()  # eager warm-up (allocates nothing): caches attributes, tensor maps, views
+        torch.cuda.synchronize(dev)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self._step()
+
+    def _step(self):
+        for li, lay in enumerate(self.layers):
+            _sparse_layer(self.q[li], lay, self.p1, self.p2, workspace=self.ws, out=self.out[li])
+
+    def replay(self):
+        self.graph.replay()
+        return self.out
+
+
 def cluster_topk_attention(q, layer, budget, *, workspace=None, stream=None, scale=None, return_plan=False):
     """Fixed cluster-budget baseline on the device (baseline_cluster_topk,
     engine.py:318-338): the `budget` clusters of largest estimated mass are

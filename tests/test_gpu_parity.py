@@ -466,3 +466,45 @@ def test_batched_sequences_parity(G):
             assert c1 != "real" and c2 != "real", (b, hq, c1, c2)
             if c1 == "exact" and c2 == "exact":
                 assert O.output_error(out[b, hq], o_out.output) <= TOL[torch.bfloat16], (b, hq)
+
+
+def test_decode_graph_matches_eager():
+    """DecodeGraph (the step's per-layer sparse_attention calls captured as one
+    CUDA graph, shared workspace) reproduces the eager calls layer by layer."""
+    from paper_2602_05191_b200 import DecodeGraph, DecodeWorkspace, cluster_layer, sparse_attention
+    from paper_2602_05191_b200.workload import generate_layer, generate_queries
+
+    L, H, G, n, d = 3, 2, 4, 4096, 128
+    layers, qs = [], []
+    for li in range(L):
+        k, v, c = generate_layer(1, H, n, d, layer=li)
+        layers.append(cluster_layer(k, v, fp64_assign=False, layer=li))
+        qs.append(torch.from_numpy(generate_queries(c, G, 1, layer=li)[0]).cuda().to(torch.bfloat16))
+    q = torch.stack(qs)  # [L, 1, Hq, d]
+    ws = DecodeWorkspace(layers[0], G)
+    want = torch.stack([sparse_attention(q[li], layers[li], 0.95, 0.7, workspace=ws).clone() for li in range(L)])
+    dg = DecodeGraph(layers, q.clone(), 0.95, 0.7, workspace=ws)
+    for _ in range(2):
+        got = dg.replay()
+        torch.cuda.synchronize()
+        err = ((got - want).norm(dim=-1) / want.norm(dim=-1)).max().item()
+        assert err <= 1e-5, err
+
+
+def test_nonfinite_query_does_not_fault():
+    """A NaN/Inf query (garbage in an uninitialised buffer) gives garbage
+    outputs but must not fault the plan or attention kernels."""
+    from paper_2602_05191_b200 import DecodeWorkspace, cluster_layer, sparse_attention
+    from paper_2602_05191_b200.workload import generate_layer
+
+    k, v, _ = generate_layer(1, 2, 4096, 128)
+    lay = cluster_layer(k, v, fp64_assign=False)
+    ws = DecodeWorkspace(lay, 4)
+    for bad in (float("nan"), float("inf"), -float("inf")):
+        q = torch.full((1, 8, 128), bad, dtype=torch.bfloat16, device="cuda")
+        sparse_attention(q, lay, 0.95, 0.7, workspace=ws)
+        torch.cuda.synchronize()
+    q = torch.randn((1, 8, 128), device="cuda").to(torch.bfloat16)
+    out = sparse_attention(q, lay, 0.95, 0.7, workspace=ws)  # the workspace is still usable
+    torch.cuda.synchronize()
+    assert torch.isfinite(out).all()
