@@ -20,6 +20,7 @@
 #include <cooperative_groups.h>
 #include <cuda.h>
 
+#include <algorithm>
 #include <string>
 
 #include "common.cuh"
@@ -75,7 +76,9 @@ static size_t km_layout(const dp_cluster_params* p, KmWs* w, char* base) {
   t.cursor = (int*)take(BH * k * 4);
   t.knum = (int*)take(BH * 4);
   t.done = (int*)take(BH * 4);
-  t.csplit = (__nv_bfloat16*)take(p->fp64_assign == 2 ? 3 * BH * k * d * 2 : 0);
+  // >= 128 rows so the tensor map's 128-row boxes never exceed it (rows past
+  // 3*BH*k only feed centroid columns >= k, which the argmin masks)
+  t.csplit = (__nv_bfloat16*)take(p->fp64_assign == 2 ? std::max<size_t>(3 * BH * k, 128) * d * 2 : 0);
   if (w) *w = t;
   return off;
 }
@@ -868,7 +871,8 @@ static cudaError_t tc_map(CUtensorMap* m, const void* ptr, unsigned long long ro
   }
   const cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)rows};
   const cuuint64_t strides[1] = {(cuuint64_t)d * 2};
-  const cuuint32_t box[2] = {64, (cuuint32_t)(rows < (unsigned long long)kTcRows ? rows : kTcRows)};
+  if (rows < (unsigned long long)kTcRows) return cudaErrorInvalidValue;  // the kernel expects full 128-row boxes
+  const cuuint32_t box[2] = {64, (cuuint32_t)kTcRows};
   const cuuint32_t es[2] = {1, 1};
   const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -891,7 +895,7 @@ static cudaError_t launch_assign_tc(const dp_cluster_params* p, const void* src,
   CUtensorMap mx, mc;
   cudaError_t e = tc_map(&mx, src, (unsigned long long)BH * p->n_tokens, p->head_dim);
   if (e != cudaSuccess) return e;
-  e = tc_map(&mc, w.csplit, 3ull * BH * p->k, p->head_dim);
+  e = tc_map(&mc, w.csplit, std::max(3ull * BH * p->k, (unsigned long long)kTcRows), p->head_dim);
   if (e != cudaSuccess) return e;
   csplit_kernel<<<dim3((p->k * p->head_dim + 255) / 256, BH), 256, 0, st>>>(*p, w);
   const size_t smem = tc_smem_bytes(p->k);

@@ -508,3 +508,17 @@ def test_nonfinite_query_does_not_fault():
     out = sparse_attention(q, lay, 0.95, 0.7, workspace=ws)  # the workspace is still usable
     torch.cuda.synchronize()
     assert torch.isfinite(out).all()
+
+
+def test_tensor_core_assign_tiny_tables():
+    """Tensor-core assignment with fewer than 128 centroid rows in the whole
+    split table (3 * B*H * k < 128): the TMA boxes must still complete (this
+    shape used to hang) and the result equals the fp64 path."""
+    from paper_2602_05191_b200 import cluster_layer
+    from paper_2602_05191_b200.workload import generate_layer
+
+    k, v, _ = generate_layer(2, 1, 700, 128)  # B=2, H=1, 20 clusters per head -> 120 split rows
+    tc = cluster_layer(k, v, fp64_assign=False, tensor_cores=True)
+    ref = cluster_layer(k, v, fp64_assign=True)
+    torch.cuda.synchronize()
+    assert torch.equal(tc.offs, ref.offs) and torch.equal(tc.perm, ref.perm)
