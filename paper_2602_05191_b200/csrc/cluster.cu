@@ -910,10 +910,11 @@ static cudaError_t launch_assign_tc(const dp_cluster_params* p, const void* src,
 // convergence test, member offsets and a stable counting sort.
 // -------------------------------------------------------------------------
 constexpr int kUpdThreads = 1024;
+constexpr int kSortSeg = 8;  // point segments (warps) of the member sort (fewer when k is large)
 
 __global__ void __launch_bounds__(kUpdThreads) update_kernel(dp_cluster_params p, KmWs w, int it,
                                                            double* __restrict__ objective,
-                                                           int* __restrict__ iters) {
+                                                           int* __restrict__ iters, int nseg) {
   const int bh = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
   if (w.done[bh]) return;
   const int M = p.n_tokens - p.sink - p.window;
@@ -977,21 +978,56 @@ __global__ void __launch_bounds__(kUpdThreads) update_kernel(dp_cluster_params p
     start[knew] = M;
   }
   __syncthreads();
-  if (tid < 32) {
-    int* sorted = w.sorted + (size_t)bh * M;
-    const int lane = tid;
-    for (int b0 = 0; b0 < M; b0 += 32) {
+  // stable counting sort of the members (ascending point index within each
+  // cluster): kSortSeg warps each own a contiguous segment of the points;
+  // per-segment cluster counts in shared memory, a per-cluster prefix over the
+  // segments, then every warp places its points with shared-memory cursors
+  // (no global read-modify-write on the dependent path)
+  extern __shared__ int segc[];  // [nseg][k]
+  int* sorted = w.sorted + (size_t)bh * M;
+  const int seg = (M + nseg - 1) / nseg;
+  const int warp = tid >> 5, lane = tid & 31;
+  for (int i = tid; i < nseg * knew; i += nt) segc[i] = 0;
+  __syncthreads();
+  if (warp < nseg) {
+    int* cnt = segc + warp * knew;
+    const int s0 = warp * seg, s1 = min(M, s0 + seg);
+    for (int b0 = s0; b0 < s1; b0 += 32) {
       const int i = b0 + lane;
-      const unsigned act = __ballot_sync(0xffffffffu, i < M);
-      if (i < M) {
+      const unsigned act = __ballot_sync(0xffffffffu, i < s1);
+      if (i < s1) {
+        const int a = assign[i];
+        const unsigned peers = __match_any_sync(act, a);
+        if (lane == __ffs(peers) - 1) cnt[a] += __popc(peers);
+      }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  for (int c = tid; c < knew; c += nt) {
+    int run = start[c];
+    for (int g = 0; g < nseg; ++g) {
+      const int t = segc[g * knew + c];
+      segc[g * knew + c] = run;
+      run += t;
+    }
+  }
+  __syncthreads();
+  if (warp < nseg) {
+    int* cur = segc + warp * knew;
+    const int s0 = warp * seg, s1 = min(M, s0 + seg);
+    for (int b0 = s0; b0 < s1; b0 += 32) {
+      const int i = b0 + lane;
+      const unsigned act = __ballot_sync(0xffffffffu, i < s1);
+      if (i < s1) {
         const int a = assign[i];
         const unsigned peers = __match_any_sync(act, a);
         const int leader = __ffs(peers) - 1;
         const int rank = __popc(peers & ((1u << lane) - 1u));
         int pos = 0;
         if (lane == leader) {
-          pos = cursor[a];
-          cursor[a] = pos + __popc(peers);
+          pos = cur[a];
+          cur[a] = pos + __popc(peers);
         }
         pos = __shfl_sync(peers, pos, leader);
         sorted[pos + rank] = i;
@@ -1210,6 +1246,12 @@ int dp_cluster_build(const dp_cluster_params* p, const void* src_keys, const voi
   e0 = launch_kmeanspp(p, src_keys, first_pick, uniforms, alt_picks, degenerate_from, w.sorted, w, st);
   if (e0 != cudaSuccess) return set_cuda_error(e0, "dp_cluster_build (kmeans++)");
   cnorm_kernel<<<dim3((p->k * 32 + 255) / 256, BH), 256, 0, st>>>(*p, w);
+  const int nseg = std::max(1, std::min(kSortSeg, (int)((200 * 1024) / ((size_t)p->k * sizeof(int)))));
+  const size_t upd_smem = (size_t)nseg * p->k * sizeof(int);
+  if ((size_t)p->k * sizeof(int) > 200 * 1024)
+    return set_error(DP_ERR_UNSUPPORTED, "more than 51200 clusters per head");
+  if (upd_smem > 48 * 1024)
+    cudaFuncSetAttribute(update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_smem);
   for (int it = 0; it < p->max_iters; ++it) {
     if (p->fp64_assign == 2) {
       const cudaError_t ea = launch_assign_tc(p, src_keys, w, st);
@@ -1218,7 +1260,7 @@ int dp_cluster_build(const dp_cluster_params* p, const void* src_keys, const voi
       assign_kernel<double><<<dim3((M + kAP - 1) / kAP, BH), 256, 0, st>>>(*p, src_keys, w);
     else
       assign_kernel<float><<<dim3((M + kAP - 1) / kAP, BH), 256, 0, st>>>(*p, src_keys, w);
-    update_kernel<<<BH, kUpdThreads, 0, st>>>(*p, w, it, objective, iters);
+    update_kernel<<<BH, kUpdThreads, upd_smem, st>>>(*p, w, it, objective, iters, nseg);
     means_kernel<<<dim3((p->k * 32 + 255) / 256, BH), 256, 0, st>>>(*p, src_keys, w);
   }
   cudaError_t e = cudaGetLastError();
