@@ -755,15 +755,13 @@ __global__ void __launch_bounds__(kTcThreads, 2)
         for (int q = 0; q < 16; ++q) {
           const int col = cb + q, u = q & 3;
           const float dist = col < kc ? fmaf(-2.f, __uint_as_float(v[q]), xn + cn[col]) : CUDART_INF_F;
-          if (dist < tb[u]) {  // strict: within a tracker columns arrive in increasing order
-            tb2[u] = tb[u];
-            ti2[u] = ti[u];
-            tb[u] = dist;
-            ti[u] = col;
-          } else if (dist < tb2[u]) {
-            tb2[u] = dist;
-            ti2[u] = col;
-          }
+          // branch-free (best, runner-up) update; strict: within a tracker the
+          // columns arrive in increasing order, so ties keep the lower index
+          const bool lt1 = dist < tb[u], lt2 = dist < tb2[u];
+          tb2[u] = lt1 ? tb[u] : (lt2 ? dist : tb2[u]);
+          ti2[u] = lt1 ? ti[u] : (lt2 ? col : ti2[u]);
+          tb[u] = lt1 ? dist : tb[u];
+          ti[u] = lt1 ? col : ti[u];
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
