@@ -522,3 +522,31 @@ def test_tensor_core_assign_tiny_tables():
     ref = cluster_layer(k, v, fp64_assign=True)
     torch.cuda.synchronize()
     assert torch.equal(tc.offs, ref.offs) and torch.equal(tc.perm, ref.perm)
+
+
+def test_nonfinite_query_other_entry_points():
+    """The unfused score/select/attend path, the cluster top-k baseline and the
+    measurement kernels also survive a NaN query (garbage out, no fault)."""
+    from paper_2602_05191_b200 import cluster_layer, cluster_topk_attention
+    from paper_2602_05191_b200 import metrics as M
+    from paper_2602_05191_b200 import _native as N
+    from paper_2602_05191_b200.workload import generate_layer
+
+    k, v, _ = generate_layer(1, 2, 3000, 128)
+    lay = cluster_layer(k, v, fp64_assign=False)
+    q = torch.full((1, 8, 128), float("nan"), dtype=torch.bfloat16, device="cuda")
+    cluster_topk_attention(q, lay, 5)
+    w, lse = M.token_weights(q, lay)
+    M.token_topk_attention(q, lay, 100, weights=w)
+    M.adaptive_token_budget_batched(lay, w, 0.9)
+    M.mixed_attention_f64(q, lay)
+    lm = torch.zeros((1, 8, lay.cluster_cap), dtype=torch.float64, device="cuda")
+    st = torch.zeros((1, 8, lay.cluster_cap), dtype=torch.uint8, device="cuda")
+    cnt = torch.zeros((1, 8, 2), dtype=torch.int32, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    N.check(N.lib().dp_score(lay.view(), N.ptr(q), 1, 4, 1 / 128 ** 0.5, N.ptr(lm), s))
+    N.check(N.lib().dp_select(lay.view(), 4, 0.95, 0.7, N.ptr(lm), N.ptr(st), N.ptr(cnt), None, None, None, None, 0,
+                              s))
+    torch.cuda.synchronize()
+    q2 = torch.randn((1, 8, 128), device="cuda").to(torch.bfloat16)
+    assert torch.isfinite(cluster_topk_attention(q2, lay, 5)).all()
