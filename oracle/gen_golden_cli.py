@@ -35,6 +35,8 @@ RUNS = [
     ("cli_figs_cluster_error", ["figs", "--table", "cluster-error", "--window", "32"]),
     ("cli_figs_tracking", ["figs", "--table", "tracking", "--window", "32"]),
 ]
+# the `cluster` subcommand writes JSON
+JSON_RUNS = [("cli_cluster", ["cluster", "--window", "32"])]
 
 
 def main():
@@ -42,6 +44,10 @@ def main():
                      "--profile", "mixed", "--seed", "6", "--out", DUMP]) == 0
     for name, argv in RUNS:
         out = os.path.join(OUT, name + ".csv")
+        assert cli.main([argv[0], "--input", DUMP, *argv[1:], "--out", out]) == 0, name
+        print("wrote", name)
+    for name, argv in JSON_RUNS:
+        out = os.path.join(OUT, name + ".json")
         assert cli.main([argv[0], "--input", DUMP, *argv[1:], "--out", out]) == 0, name
         print("wrote", name)
 

@@ -111,3 +111,18 @@ def test_cli_errors(capsys):
     assert "requires k" in capsys.readouterr().err
     assert main(["run", "--input", DUMP, "--method", "cluster_topk", "--m", "999", "--window", "32"]) == 1
     assert "cluster budget must be in" in capsys.readouterr().err
+
+
+def test_cli_cluster_report_matches_reference(tmp_path):
+    """`cluster` subcommand: the same JSON report as the reference CLI (the
+    default fp64 clustering reproduces the reference's clusters exactly)."""
+    import json
+
+    from paper_2602_05191_b200.cli import main
+
+    out = tmp_path / "c.json"
+    assert main(["cluster", "--input", DUMP, "--window", "32", "--out", str(out)]) == 0
+    got = json.loads(out.read_text())
+    with open(os.path.join(GOLDEN, "cli_cluster.json")) as f:
+        want = json.load(f)
+    assert got == want
