@@ -480,14 +480,14 @@ def run_b200(a):
             torch.cuda.current_stream(dev).synchronize()
 
         # the serving form of the same API: the 32 per-layer calls captured once
-        # (DecodeGraph), replayed per step between the pinned copies
+        # (DecodeGraph) with the pinned copies inside the graph -- one graph per
+        # distinct query step (each reads its own pinned slice), replayed per step
         qd.copy_(qh[0])  # real queries in the graph's input buffer before its eager warm-up
-        dg = DecodeGraph(layers, qd, a.p1, a.p2, out=od, workspace=wss[0])
+        graphs = [DecodeGraph(layers, qd, a.p1, a.p2, out=od, workspace=wss[0], host_q=qh[s], host_out=oh)
+                  for s in range(a.qsteps)]
 
         def e2e_graph(s):
-            qd.copy_(qh[s % a.qsteps], non_blocking=True)
-            dg.replay()
-            oh.copy_(od, non_blocking=True)
+            graphs[s % a.qsteps].replay()
             torch.cuda.current_stream(dev).synchronize()
 
         def timed_e2e(fn):
@@ -508,9 +508,10 @@ def run_b200(a):
         eager_ms = timed_e2e(e2e_eager)
         e2e = {"value": e2e_ms * 1e3, "unit": "us/step", "h2d_bytes_per_step": int(L * B * Hq_l * d * 2),
                "d2h_bytes_per_step": int(L * B * Hq_l * d * 4),
-               "path": "paper_2602_05191_b200.DecodeGraph (the step's 32 sparse_attention calls captured once as a "
-                       "CUDA graph, one shared workspace), replayed per step; all layers' q in from pinned host "
-                       "memory and all outputs back, one copy each per step",
+               "path": "paper_2602_05191_b200.DecodeGraph (the step's 32 sparse_attention calls and the pinned "
+                       "host copies captured once as a CUDA graph, one shared workspace), replayed per step: all "
+                       "layers' q in from pinned host memory (layer 0 first, the rest overlapping it), every "
+                       "layer's output back to pinned host memory as soon as it is ready, host sync per step",
                "eager_us_per_step": eager_ms * 1e3,
                "eager_path": "paper_2602_05191_b200.sparse_attention per layer, eager, same copies"}
 

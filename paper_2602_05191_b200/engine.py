@@ -137,11 +137,14 @@ class DecodeGraph:
     layer li, exactly the eager ``sparse_attention(q[li], layers[li], p1, p2)``
     launches (plan + attend, PDL-chained) into ``out[li]``, without the
     per-call host work.  ``q`` [L,B,Hq,d] and ``out`` [L,B,Hq,d] fp32 are fixed
-    device buffers: fill ``q`` (e.g. a non-blocking copy from pinned host
-    memory), ``replay()``, read ``out``.  Layers share one geometry (and one
-    workspace, reused layer after layer as in the eager path)."""
+    device buffers.  Optional pinned host buffers move inside the graph:
+    ``host_q`` is copied in (layer 0's slice first, the rest on a side stream
+    while layer 0 runs) and each layer's output is copied to ``host_out`` on a
+    side stream as soon as that layer finishes, so only the last layer's copy
+    is exposed.  Layers share one geometry (and one workspace, reused layer
+    after layer as in the eager path)."""
 
-    def __init__(self, layers, q, p1=0.95, p2=0.7, *, out=None, workspace=None):
+    def __init__(self, layers, q, p1=0.95, p2=0.7, *, out=None, workspace=None, host_q=None, host_out=None):
         for name, val in (("p1", p1), ("p2", p2)):
             if not 0.0 < val <= 1.0:
                 raise ValueError(f"{name} must be in (0, 1], got {val}")
@@ -157,7 +160,12 @@ class DecodeGraph:
         self.out = out if out is not None else torch.empty(q.shape, dtype=torch.float32, device=dev)
         if self.out.dtype != torch.float32 or self.out.shape != q.shape or not self.out.is_contiguous():
             raise ValueError(f"out must be a contiguous float32 tensor of shape {tuple(q.shape)}")
+        for name, t, dt in (("host_q", host_q, q.dtype), ("host_out", host_out, torch.float32)):
+            if t is not None and (t.shape != q.shape or t.dtype != dt or t.is_cuda or not t.is_pinned()):
+                raise ValueError(f"{name} must be a pinned host tensor of shape {tuple(q.shape)} and dtype {dt}")
+        self.host_q, self.host_out = host_q, host_out
         self.p1, self.p2 = p1, p2
+        self._s_in, self._s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
         self._step()  # eager warm-up (allocates nothing): caches attributes, tensor maps, views
         torch.cuda.synchronize(dev)
         self.graph = torch.cuda.CUDAGraph()
@@ -165,12 +173,28 @@ class DecodeGraph:
             self._step()
 
     def _step(self):
+        main = torch.cuda.current_stream(self.layers[0].device)
+        hq, ho = self.host_q, self.host_out
+        if hq is not None:
+            self.q[0].copy_(hq[0], non_blocking=True)
+            if len(self.layers) > 1:
+                self._s_in.wait_stream(main)
+                with torch.cuda.stream(self._s_in):
+                    self.q[1:].copy_(hq[1:], non_blocking=True)
         for li, lay in enumerate(self.layers):
+            if li == 1 and hq is not None:
+                main.wait_stream(self._s_in)
             _sparse_layer(self.q[li], lay, self.p1, self.p2, workspace=self.ws, out=self.out[li])
+            if ho is not None:
+                self._s_out.wait_stream(main)
+                with torch.cuda.stream(self._s_out):
+                    ho[li].copy_(self.out[li], non_blocking=True)
+        if ho is not None:
+            main.wait_stream(self._s_out)
 
     def replay(self):
         self.graph.replay()
-        return self.out
+        return self.host_out if self.host_out is not None else self.out
 
 
 def cluster_topk_attention(q, layer, budget, *, workspace=None, stream=None, scale=None, return_plan=False):

@@ -489,6 +489,17 @@ def test_decode_graph_matches_eager():
         torch.cuda.synchronize()
         err = ((got - want).norm(dim=-1) / want.norm(dim=-1)).max().item()
         assert err <= 1e-5, err
+    # pinned host buffers inside the graph: q in, every layer's output out
+    hq = q.cpu().pin_memory()
+    ho = torch.zeros(q.shape, dtype=torch.float32).pin_memory()
+    qbuf = torch.zeros_like(q)
+    dg2 = DecodeGraph(layers, qbuf, 0.95, 0.7, workspace=ws, host_q=hq, host_out=ho)
+    ho.zero_()
+    got = dg2.replay()
+    torch.cuda.synchronize()
+    assert got.data_ptr() == ho.data_ptr()
+    err = ((got - want.cpu()).norm(dim=-1) / want.cpu().norm(dim=-1)).max().item()
+    assert err <= 1e-5, err
 
 
 def test_nonfinite_query_does_not_fault():
