@@ -114,10 +114,16 @@ def lib():
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(LIB):
-        from .build import build
+    from .build import build
 
-        build()
+    try:
+        build()  # no-op when the library matches the sources' digest; rebuilds a stale one
+    except FileNotFoundError:  # no nvcc on this host: use the prebuilt library if there is one
+        if not os.path.exists(LIB):
+            raise
+        import warnings
+
+        warnings.warn("nvcc not found: loading the prebuilt libdoublep_b200.so without a digest check")
     handle = ctypes.CDLL(LIB)
     for name, (res, args) in _SIGS.items():
         fn = getattr(handle, name)

@@ -21,6 +21,8 @@ SOURCES = ["capi.cu", "decode.cu", "cluster.cu", "attn_tc.cu", "plan.cu", "metri
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-Xptxas", "-v"]
+if os.environ.get("DP_PROFILE"):  # %globaltimer phase stamps (tools/plan_timing.py, step_timing.py)
+    FLAGS = FLAGS + ["-DDP_PROFILE"]
 
 
 def _nvcc():
@@ -55,17 +57,20 @@ def build(force=False, verbose=False):
     nvcc = _nvcc()
     objs = []
     logs = []
-    for src in SOURCES:
+    procs = []
+    for src in SOURCES:  # compiled in parallel
         path = os.path.join(CSRC, src)
         if not os.path.exists(path):
             continue
         obj = os.path.join(LIBDIR, src.replace(".cu", ".o"))
         cmd = [nvcc, *ARCH, *FLAGS, "-I", INCLUDE, "-I", CSRC, "-c", path, "-o", obj]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        logs.append(r.stderr)
-        if r.returncode != 0:
-            raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
+        procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
         objs.append(obj)
+    for src, pr in procs:
+        _, err = pr.communicate()
+        logs.append(err)
+        if pr.returncode != 0:
+            raise RuntimeError(f"nvcc failed for {src}:\n{err}")
     cmd = [nvcc, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:

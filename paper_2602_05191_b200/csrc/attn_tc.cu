@@ -26,6 +26,7 @@
 #include <cuda_runtime.h>
 
 #include "common.cuh"
+#include "host_state.h"
 #include "decode_internal.h"
 
 namespace dp {
@@ -134,12 +135,20 @@ __device__ __forceinline__ int atom_add_acq_rel(int* p, int v) {
   return old;
 }
 
+// (compiled in only with -DDP_PROFILE)
 __device__ __forceinline__ void astamp(int ev) {
+#ifdef DP_PROFILE
   if (threadIdx.x == 0 && blockIdx.x < 512) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     g_attn_ts[blockIdx.x][ev] = t;
   }
+#endif
+}
+__device__ __forceinline__ void astamp_at(int ev, unsigned long long v) {
+#ifdef DP_PROFILE
+  if (blockIdx.x < 512) g_attn_ts[blockIdx.x][ev] = v;
+#endif
 }
 
 // owner CTA of global row j when T rows are split evenly over `grid` CTAs
@@ -295,11 +304,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
       if (w.more()) nr_nx = fetch(w, e_nx, bh_nx);
       if (idx >= kStages) mbar_wait(smem_u32(&empty_bar[s]), (unsigned)(((idx / kStages) + 1) & 1));
       rmask[s * kTcRows + pr0 + lane] = e == 0xFFFFFFFFu ? 0 : (int)(e >> 24);
+#ifdef DP_PROFILE
       if (idx == 0 && warp == kWarps && lane == 0 && blockIdx.x < 512) {  // profiling: first row entries in hand
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t) : "r"(e));
         g_attn_ts[blockIdx.x][9] = t;
       }
+#endif
       const size_t head_off = (size_t)bh * v.row_cap * d;
       const __nv_bfloat16* Kg = reinterpret_cast<const __nv_bfloat16*>(v.keys) + head_off;
       const __nv_bfloat16* Vg = reinterpret_cast<const __nv_bfloat16*>(v.values) + head_off;
@@ -322,11 +333,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
           cp16_zero(vd, Vg);
         }
       }
+#ifdef DP_PROFILE
       if (idx == 0 && warp == kWarps && lane == 0 && blockIdx.x < 512) {  // profiling: first tile issued
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         g_attn_ts[blockIdx.x][10] = t;
       }
+#endif
       cp_async_arrive(smem_u32(&full_bar[s]));  // completes when this lane's copies land
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&full_bar[s]));  // releases the rmask stores
@@ -655,9 +668,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
     if (lane == 0) mbar_arrive(smem_u32(&empty_bar[s]));  // stage s free for the producer
   }
   astamp(3);
-  if (tid == 0 && blockIdx.x < 512) {  // profiling: rows and head segments of this CTA
-    g_attn_ts[blockIdx.x][7] = (unsigned long long)(r1 - r0);
-    g_attn_ts[blockIdx.x][8] = (unsigned long long)nflushed;
+  if (tid == 0) {  // profiling: rows and head segments of this CTA
+    astamp_at(7, (unsigned long long)(r1 - r0));
+    astamp_at(8, (unsigned long long)nflushed);
   }
   consumers_sync();  // every partial of this CTA is written (CTA scope)
   if (tid == 0) {
@@ -837,19 +850,10 @@ size_t attn_tc_smem_bytes(int BH) { return TcSmem::fixed + (size_t)(BH + 1) * 8;
 template <bool kDense, bool kQF32>
 static cudaError_t launch_tc_t(const dp_cache_view& v, const void* q, int G, double scale, const double* lm,
                                WorkLists wl, Partials<float> pt, float* out, float* lse, cudaStream_t st) {
-  static size_t attr = 0;
-  static int sms = 0;
   const int BH = v.batch * v.kv_heads;
   const size_t smem = attn_tc_smem_bytes(BH);
-  if (attr < smem) {
-    cudaFuncSetAttribute(attn_tc_kernel<kDense, kQF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = smem;
-  }
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  ensure_smem(reinterpret_cast<const void*>(attn_tc_kernel<kDense, kQF32>), smem);
+  const int sms = sm_count();
   // one persistent CTA per SM (row ranges balanced to +-1 row)
   const int grid = sms < kMaxPartSlots ? sms : kMaxPartSlots;
   cudaLaunchConfig_t cfg = {};

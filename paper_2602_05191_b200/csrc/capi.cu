@@ -114,8 +114,13 @@ int dp_attend(const dp_cache_view* v, const void* q, int32_t q_dtype, int32_t G,
 int dp_sparse_attention(const dp_cache_view* v, const void* q, int32_t q_dtype, int32_t G, double scale,
                         const double* log_mass, const uint8_t* state, float* out, float* lse, int32_t* stats,
                         void* ws, size_t ws_bytes, void* stream) {
-  int r = dp_build_worklist(v, G, log_mass, state, stats, ws, ws_bytes, stream);
+  int r = check_view(v, G);
   if (r) return r;
+  if ((r = check_q(q_dtype))) return r;
+  if (ws_bytes < dp_decode_workspace_bytes(v, G)) return fail(DP_ERR_INVALID, "workspace too small");
+  // with the query: the sink/window logits join the attention's reference max
+  cudaError_t e = dp::launch_worklist(*v, G, state, stats, ws, (cudaStream_t)stream, log_mass, q, q_dtype, scale);
+  if (e != cudaSuccess) return cuda_fail(e, "dp_sparse_attention");
   return dp_attend(v, q, q_dtype, G, scale, log_mass, out, lse, ws, ws_bytes, stream);
 }
 

@@ -24,6 +24,7 @@
 #include <string>
 
 #include "common.cuh"
+#include "host_state.h"
 #include "doublep_b200.h"
 
 namespace cg = cooperative_groups;

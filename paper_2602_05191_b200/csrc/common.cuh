@@ -65,6 +65,18 @@ __device__ __forceinline__ T block_max(T v, T* red, T ident) {
   return r;
 }
 
+// Reference max (nats) of the tensor-core attention's shared accumulators:
+// the larger of the head's top cluster log-mass and its sink/window logits
+// (always-exact rows the plan never scores otherwise), plus a margin, so an
+// exact row up to ~70 nats above it cannot overflow the fp32 sums.  The top
+// cluster is always exact and carries >= e^(top log-mass) (Jensen), so the
+// margin costs nothing at the low end.
+constexpr double kRefMargin = 11.0;
+__device__ __forceinline__ double ref_max(double top, double sw) {
+  const double m = fmax(top, sw);  // fmax drops a NaN operand
+  return (m == -CUDART_INF || m != m) ? 0.0 : fmin(m, 1e30) + kRefMargin;
+}
+
 // Block-wide exclusive scan (fixed association order, so deterministic).
 // Returns the exclusive prefix; *total receives the block total.
 template <typename T>

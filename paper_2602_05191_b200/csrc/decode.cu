@@ -15,6 +15,7 @@
 #include <string>
 
 #include "common.cuh"
+#include "host_state.h"
 #include "decode_internal.h"
 
 namespace dp {
@@ -570,11 +571,7 @@ cudaError_t launch_score(const dp_cache_view& v, const void* q, int qdt, int G, 
                          cudaStream_t st) {
   const size_t smem = (size_t)G * v.head_dim * 8 + (size_t)kScoreTile * (v.head_dim + 4) * 4 +
                       (size_t)G * v.head_dim * 4;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr_set = true;
-  }
+  ensure_smem(reinterpret_cast<const void*>(score_kernel), 200 * 1024);
   dim3 grid((v.cluster_cap + kScoreTile - 1) / kScoreTile, v.batch * v.kv_heads);
   score_kernel<<<grid, kScoreTile, smem, st>>>(v, q, qdt, G, scale, lm);
   return cudaGetLastError();
@@ -609,11 +606,7 @@ cudaError_t launch_select(const dp_cache_view& v, int G, double p1, double p2, c
                           cudaStream_t st) {
   const int Kp = select_padded(std::max(1, v.cluster_cap));
   const size_t smem = (size_t)Kp * 12;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr_set = true;
-  }
+  ensure_smem(reinterpret_cast<const void*>(select_kernel), 200 * 1024);
   select_kernel<<<v.batch * v.kv_heads * G, kSelectThreads, smem, st>>>(v, G, p1, p2, lm, state, counts,
                                                                        order, cum, probs, Kp);
   return cudaGetLastError();
@@ -626,12 +619,7 @@ cudaError_t launch_attn_t(const dp_cache_view& v, const void* q, int qdt, int G,
   const size_t BH = (size_t)v.batch * v.kv_heads;
   Partials<Acc> pt = carve_partials<Acc>(parts, BH, wl.max_chunks, G, v.head_dim);
   const size_t smem = attn_smem_bytes(v.head_dim, G, sizeof(T), sizeof(Acc));
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(attn_chunk_kernel<T, Acc, kDense>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         200 * 1024);
-    attr_set = true;
-  }
+  ensure_smem(reinterpret_cast<const void*>(attn_chunk_kernel<T, Acc, kDense>), 200 * 1024);
   const int rows = kDense ? v.n_tokens : v.row_cap;
   dim3 grid((rows + kChunkRows - 1) / kChunkRows, (unsigned)BH);
   cudaError_t e;
@@ -656,7 +644,8 @@ cudaError_t launch_attn_t(const dp_cache_view& v, const void* q, int qdt, int G,
 // computes it in-cluster): over state==1 clusters, m = max log-mass,
 // l = sum e^(lm - m), o = sum e^(lm - m) * value_mean (engine.py:231-246)
 __global__ void __launch_bounds__(256) approx_partial_kernel(dp_cache_view v, int G, const double* __restrict__ lm,
-                                                            const uint8_t* __restrict__ state, WorkLists wl) {
+                                                            const uint8_t* __restrict__ state, WorkLists wl,
+                                                            const void* __restrict__ q, int qdt, double scale) {
   const int hq = blockIdx.x, bh = hq / G, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int K = v.nclusters[bh], cap = v.cluster_cap, d = v.head_dim;
   const double* x = lm + (size_t)hq * cap;
@@ -668,10 +657,25 @@ __global__ void __launch_bounds__(256) approx_partial_kernel(dp_cache_view v, in
     if (st[k] == 1) m = fmax(m, x[k]);
     mall = fmax(mall, x[k]);
   }
+  // sink/window rows are always exact: their logits join the reference max
+  // (q nullable: the dp_build_worklist entry point has no query)
+  double sw = -CUDART_INF;
+  if (q) {
+    const int nsw = v.sink + v.window;
+    for (int t = tid; t < nsw; t += blockDim.x) {
+      const int row = t < v.sink ? t : v.n_tokens - v.window + (t - v.sink);
+      double acc = 0.0;
+      for (int c = 0; c < d; ++c)
+        acc += load_elem_d(v.keys, v.dtype, ((size_t)bh * v.row_cap + row) * d + c) *
+               load_elem_d(q, qdt, (size_t)hq * d + c);
+      if (acc == acc) sw = fmax(sw, acc * scale);
+    }
+  }
   const double M = block_max(m, red, -CUDART_INF);
   const double Mall = block_max(mall, red, -CUDART_INF);
+  const double SW = block_max(sw, red, -CUDART_INF);
   // reference max of the tensor-core attention's accumulators (log2 units), as dp_plan writes it
-  if (tid == 0) wl.refm[hq] = K > 0 ? (float)(Mall * 1.4426950408889634) : 0.f;
+  if (tid == 0) wl.refm[hq] = (float)(ref_max(Mall, SW) * 1.4426950408889634);
   const float* vbar = v.value_means + (size_t)bh * cap * d;
   float acc[8];
 #pragma unroll
@@ -702,13 +706,13 @@ __global__ void __launch_bounds__(256) approx_partial_kernel(dp_cache_view v, in
 }
 
 cudaError_t launch_worklist(const dp_cache_view& v, int G, const uint8_t* state, int* stats, void* ws,
-                            cudaStream_t st, const double* lm) {
+                            cudaStream_t st, const double* lm, const void* q, int qdt, double scale) {
   WorkLists wl;
   decode_ws_layout(&v, G, &wl, nullptr, nullptr, reinterpret_cast<char*>(ws));
   wl.stats = stats;
   worklist_kernel<<<v.batch * v.kv_heads, kListThreads, 0, st>>>(v, G, state, wl);
   if (lm && v.head_dim <= 256)
-    approx_partial_kernel<<<v.batch * v.kv_heads * G, 256, 0, st>>>(v, G, lm, state, wl);
+    approx_partial_kernel<<<v.batch * v.kv_heads * G, 256, 0, st>>>(v, G, lm, state, wl, q, qdt, scale);
   return cudaGetLastError();
 }
 

@@ -70,7 +70,8 @@ cudaError_t launch_select(const dp_cache_view& v, int G, double p1, double p2, c
                           uint8_t* state, int* counts, int* order, double* cum, double* probs,
                           cudaStream_t st);
 cudaError_t launch_worklist(const dp_cache_view& v, int G, const uint8_t* state, int* stats, void* ws,
-                            cudaStream_t st, const double* lm);
+                            cudaStream_t st, const double* lm, const void* q = nullptr, int qdt = 0,
+                            double scale = 0.0);
 cudaError_t launch_attend(const dp_cache_view& v, const void* q, int qdt, int G, double scale, const double* lm,
                           float* out, float* lse, void* ws, bool dense, cudaStream_t st);
 cudaError_t launch_attn_tc(const dp_cache_view& v, const void* q, int qdt, int G, double scale, const double* lm,

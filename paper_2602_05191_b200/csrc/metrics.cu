@@ -27,6 +27,7 @@
 #include <cuda_runtime.h>
 
 #include "common.cuh"
+#include "host_state.h"
 #include "decode_internal.h"
 
 namespace dp {

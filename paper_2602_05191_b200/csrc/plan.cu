@@ -37,6 +37,7 @@
 #include <cuda_runtime.h>
 
 #include "common.cuh"
+#include "host_state.h"
 #include "decode_internal.h"
 
 namespace cg = cooperative_groups;
@@ -61,13 +62,16 @@ constexpr int kCandBins = 8;      // stage-2 candidate bins ranked together with
 // dp_debug_plan_timing() -- profiling aid only
 __device__ unsigned long long g_plan_ts[16][24];
 __device__ unsigned long long g_plan_clk[16][2];
+// (compiled in only with -DDP_PROFILE: DP_PROFILE=1 python -m paper_2602_05191_b200.build)
 __device__ __forceinline__ void stamp(int r, int ev) {
+#ifdef DP_PROFILE
   if (blockIdx.x < 16 && threadIdx.x == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     g_plan_ts[r][ev] = t;
     if (ev == 0 || ev == 9) g_plan_clk[r][ev == 9] = clock64();
   }
+#endif
 }
 
 __device__ __forceinline__ void cl_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory"); }
@@ -323,6 +327,8 @@ __global__ void __launch_bounds__(kPT, 1)
 
   __shared__ __align__(8) unsigned long long s_tbar[2];  // TMA tile barriers
   __shared__ double s_max[kMaxCL][kG];  // pushed slice maxima (owners)
+  __shared__ double s_swx[kMaxCL][kG];  // pushed sink/window logit maxima (owners)
+  __shared__ double s_sw[kPW][kG];
   __shared__ int s_cnt[kMaxCL][4];      // pushed slice counts (rows, exact clusters, approx clusters)
   __shared__ double s_Mg[kG];           // pushed head maxima (every CTA)
   __shared__ double s_wm[kPW][kG];
@@ -477,6 +483,34 @@ __global__ void __launch_bounds__(kPT, 1)
       }
     }
   }
+  // sink/window logits of my share of those rows (always exact; never scored
+  // otherwise): their max joins the attention's reference max (ref_max)
+  {
+    double swl[kG];
+#pragma unroll
+    for (int g = 0; g < kG; ++g) swl[g] = -CUDART_INF;
+    const int nsw = v.sink + v.window, s0 = r * nsw / CL, s1 = (r + 1) * nsw / CL;
+#pragma unroll 1
+    for (int t = s0 + warp; t < s1; t += kPW) {
+      const int row = t < v.sink ? t : v.n_tokens - v.window + (t - v.sink);
+      const size_t kb = ((size_t)bh * v.row_cap + row) * d;
+      float kx[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) kx[j] = lane + 32 * j < d ? load_elem_f(v.keys, v.dtype, kb + lane + 32 * j) : 0.f;
+#pragma unroll
+      for (int g = 0; g < kG; ++g) {
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (lane + 32 * j < d) acc += (double)kx[j] * qd[g * qP + lane + 32 * j];
+        acc = warp_sum(acc) * scale;
+        if (g < G && acc == acc) swl[g] = fmax(swl[g], acc);
+      }
+    }
+    if (lane == 0)
+#pragma unroll
+      for (int g = 0; g < kG; ++g) s_sw[warp][g] = swl[g];
+  }
   stamp(r, 10);
 #pragma unroll
   for (int e = 0; e < 2; ++e) {
@@ -493,6 +527,10 @@ __global__ void __launch_bounds__(kPT, 1)
 #pragma unroll 1
     for (int w = 0; w < kPW; ++w) mm = fmax(mm, s_wm[w][tid]);
     remote(cluster, &s_max[0][0], tid)[r * kG + tid] = mm;
+    double sm = -CUDART_INF;
+#pragma unroll 1
+    for (int w = 0; w < kPW; ++w) sm = fmax(sm, s_sw[w][tid]);
+    remote(cluster, &s_swx[0][0], tid)[r * kG + tid] = sm;
   }
   if (r < G) {  // owners: zero the histogram now (the tile buffers it overlays are consumed)
     unsigned* hz = reinterpret_cast<unsigned*>(smem + L.hm);
@@ -739,7 +777,12 @@ __global__ void __launch_bounds__(kPT, 1)
       counts[2 * hq + 1] = K > 0 ? n2 : 0;
     }
     (void)ctot;
-    if (tid < CL) remote(cluster, s_Mg, tid)[g] = K > 0 ? M : 0.0;
+    if (tid < CL) {
+      double SW = -CUDART_INF;
+#pragma unroll 1
+      for (int rr = 0; rr < CL; ++rr) SW = fmax(SW, s_swx[rr][g]);
+      remote(cluster, s_Mg, tid)[g] = ref_max(K > 0 ? M : -CUDART_INF, SW);
+    }
   }
   stamp(r, 5);
   cl_sync();  // (B) every cluster state and head max is in place
@@ -898,6 +941,7 @@ static cudaError_t centroid_tmap(const dp_cache_view& v, CUtensorMap* m) {
   };
   static Entry cache[64];
   static int next = 0;
+  std::lock_guard<std::recursive_mutex> lock(host_mutex());
   const long long rows = (long long)v.batch * v.kv_heads * v.cluster_cap;
   for (const Entry& e : cache)
     if (e.ptr == v.centroids && e.rows == rows && e.d == v.head_dim) {
@@ -944,20 +988,15 @@ static void* plan_fn_for(int kG) {
 // the kernel's dynamic shared-memory limit only ever grows (the occupancy
 // queries below and the launches share it; lowering it for a query would
 // make a later, larger launch fail)
-static void ensure_smem_attr(int kG, size_t smem) {
-  static size_t cur[9] = {};
-  if (cur[kG] >= smem) return;
-  void* fn = plan_fn_for(kG);
-  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  cur[kG] = smem;
-}
+static void ensure_smem_attr(int kG, size_t smem) { ensure_smem(plan_fn_for(kG), smem, true); }
 
 // co-resident clusters of size cl at this shared-memory footprint
 static int max_active_clusters(int kG, int cl, size_t smem) {
-  static int cache[9][17] = {};
-  static size_t cache_smem[9][17] = {};
-  if (cache_smem[kG][cl] == smem) return cache[kG][cl];
+  static int cache[kMaxDevices][9][17] = {};
+  static size_t cache_smem[kMaxDevices][9][17] = {};
+  const int dev = current_device();
+  std::lock_guard<std::recursive_mutex> lock(host_mutex());
+  if (cache_smem[dev][kG][cl] == smem) return cache[dev][kG][cl];
   void* fn = plan_fn_for(kG);
   ensure_smem_attr(kG, smem);
   cudaLaunchConfig_t cfg = {};
@@ -976,8 +1015,8 @@ static int max_active_clusters(int kG, int cl, size_t smem) {
     cudaGetLastError();
     n = 0;
   }
-  cache[kG][cl] = n;
-  cache_smem[kG][cl] = smem;
+  cache[dev][kG][cl] = n;
+  cache_smem[dev][kG][cl] = smem;
   return n;
 }
 

@@ -142,7 +142,11 @@ class DecodeGraph:
     while layer 0 runs) and each layer's output is copied to ``host_out`` on a
     side stream as soon as that layer finishes, so only the last layer's copy
     is exposed.  Layers share one geometry (and one workspace, reused layer
-    after layer as in the eager path)."""
+    after layer as in the eager path).
+
+    The captured launches hold each layer's token count, so a graph is valid
+    for one cache state: after ``ClusteredLayer.append`` (decode-time growth)
+    ``replay()`` raises -- rebuild the graph (or call ``recapture()``)."""
 
     def __init__(self, layers, q, p1=0.95, p2=0.7, *, out=None, workspace=None, host_q=None, host_out=None):
         for name, val in (("p1", p1), ("p2", p2)):
@@ -168,9 +172,18 @@ class DecodeGraph:
         self._s_in, self._s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
         self._step()  # eager warm-up (allocates nothing): caches attributes, tensor maps, views
         torch.cuda.synchronize(dev)
+        self._capture()
+
+    def _capture(self):
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph):
             self._step()
+        self._ntok = [lay.n_tokens for lay in self.layers]
+
+    def recapture(self):
+        """Re-record the graph for the layers' current token counts."""
+        torch.cuda.synchronize(self.layers[0].device)
+        self._capture()
 
     def _step(self):
         main = torch.cuda.current_stream(self.layers[0].device)
@@ -193,6 +206,9 @@ class DecodeGraph:
             main.wait_stream(self._s_out)
 
     def replay(self):
+        if [lay.n_tokens for lay in self.layers] != self._ntok:
+            raise ValueError("DecodeGraph is stale: a layer's token count changed since capture "
+                             "(append_tokens); call recapture()")
         self.graph.replay()
         return self.host_out if self.host_out is not None else self.out
 

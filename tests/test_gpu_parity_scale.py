@@ -1,0 +1,216 @@
+"""GPU parity at the benchmarked configurations (SURVEY.md §8c protocol,
+VERDICT r1 "next round" item 1).
+
+Every test here runs the PRODUCT path (``sparse_attention(q[B,Hq,d], layer,
+p1, p2)`` -> ``dp_decode_step``, the same call the bench times) on the bench's
+own synthetic workload and checks every (sequence, q head) against the oracle
+fed the GPU's clustered tables:
+
+  * log-masses within 1e-9 (fp64 scoring over fp32 centroids),
+  * stage-1 / stage-2 cluster sets bit-exact, or a classified score tie
+    (order tie / threshold tie within 1e-6); a "real" mismatch fails,
+  * outputs rel-L2 <= 2e-3 (bf16 cache) / 1e-5 (fp32 cache), lse within 1e-4,
+  * the exact-token set (sink + window + members of C_exact) equal to the
+    oracle's (engine.py:196-205).
+
+Each test prints its exact / tie counts.  Shapes:
+  (i)   128K, 8 kv heads, G=4, p=(0.95, 0.7), auto plan cluster size (K ~ 4094)
+        -- the bench's long_context layer;
+  (ii)  70B shape (64 q / 8 kv, G=8) at 128K, p1 in {0.9, 0.95, 0.99};
+  (iii) batch 16 at 32K (config 3's batching), one layer;
+  (iv)  config 1 exactly: 8K, 32 q / 8 kv, d=128, fp32 cache, peaked and mixed,
+        inputs from the reference generator law (oracle.generate);
+  (v)   decode-time growth through the fused plan + attention path: d=128
+        bf16, appends across the window edge, then sparse_attention.
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import doublep_oracle as O
+from parity import classify_sets, oracle_tables
+
+pytestmark = pytest.mark.gpu
+
+TOL = {torch.float32: 1e-5, torch.bfloat16: 2e-3}
+
+
+def _host_head(t, b, h):
+    return t[b, h].double().cpu().numpy()
+
+
+def check_layer(layer, kpos, vpos, q, p1, p2, dtype, label, ntokens=None):
+    """Product path on a whole layer vs the oracle, every (b, q head).
+    kpos/vpos: position-ordered rows [B,H,N,d] (device or host tensors)."""
+    from paper_2602_05191_b200 import sparse_attention
+
+    B, Hq, d = q.shape
+    H = layer.kv_heads
+    G = Hq // H
+    out, ws = sparse_attention(q, layer, p1, p2, return_plan=True)
+    out = out.double().cpu().numpy()
+    lse = ws.lse.double().cpu().numpy()
+    lm = ws.log_mass.cpu().numpy()
+    st = ws.state.cpu().numpy()
+    cnt = ws.counts.cpu().numpy()
+    n = layer.n_tokens if ntokens is None else ntokens
+    classes = {"exact": 0, "order_tie": 0, "threshold_tie": 0, "real": 0}
+    worst = 0.0
+    for b in range(B):
+        for h in range(H):
+            t = oracle_tables(layer, b, h)
+            K = len(t.members)
+            kf = _host_head(kpos, b, h)[:n]
+            vf = _host_head(vpos, b, h)[:n]
+            for g in range(G):
+                hq = h * G + g
+                qv = q[b, hq].double().cpu().numpy()
+                o_out, o_plan, o_est = O.decode_step(qv, kf, vf, t, p1, p2, layer.sink, layer.window)
+                np.testing.assert_allclose(lm[b, hq, :K], o_est.log_masses, rtol=0, atol=1e-9)
+                c1, c2 = classify_sets(o_est, o_plan, st[b, hq], p1, p2)
+                classes[c1] += 1
+                classes[c2] += 1
+                assert c1 != "real" and c2 != "real", (label, b, hq, c1, c2)
+                assert int(cnt[b, hq, 0]) == int((st[b, hq, :K] >= 1).sum())
+                assert int(cnt[b, hq, 1]) == int((st[b, hq, :K] == 2).sum())
+                if c1 == "exact" and c2 == "exact":
+                    exact_ids = np.flatnonzero(st[b, hq, :K] == 2)
+                    np.testing.assert_array_equal(np.sort(exact_ids), np.sort(o_plan.exact_clusters))
+                    err = O.output_error(out[b, hq], o_out.output)
+                    worst = max(worst, err)
+                    assert err <= TOL[dtype], (label, b, hq, err)
+                    assert abs(lse[b, hq] - o_out.log_normalizer) <= 1e-4 * max(1.0, abs(o_out.log_normalizer))
+    print(f"[PARITY] {label}: p=({p1},{p2}) stage classes {classes} worst rel err {worst:.2e}")
+    assert classes["real"] == 0
+    return classes
+
+
+def _bench_layer(B, H, n, G, profile="peaked", layer=0, steps=1):
+    """The bench's workload: device generator, batched GPU k-means."""
+    from paper_2602_05191_b200 import cluster_layer
+    from paper_2602_05191_b200.workload import generate_layer, generate_queries
+
+    k, v, c = generate_layer(B, H, n, 128, layer=layer)
+    lay = cluster_layer(k, v, fp64_assign=False, layer=layer)
+    q = torch.from_numpy(generate_queries(c, G, steps, profile=profile, layer=layer)).cuda().to(torch.bfloat16)
+    return lay, k, v, q
+
+
+def test_parity_128k_g4_bench_long_context():
+    """(i) the bench's long_context layer: 128K, 8 kv heads, G=4, (0.95, 0.7)."""
+    lay, k, v, q = _bench_layer(1, 8, 131072, 4)
+    assert int(lay.nclusters.max()) > 4000  # K ~ 4094: the plan's widest table
+    check_layer(lay, k, v, q[0], 0.95, 0.7, torch.bfloat16, "128K G=4 8kv")
+
+
+@pytest.mark.parametrize("p1", [0.9, 0.95, 0.99])
+def test_parity_128k_g8_70b_shape(p1):
+    """(ii) 70B shape: 64 q / 8 kv heads at 128K, p1 sweep (p2 = 0.7)."""
+    lay, k, v, q = _bench_layer(1, 8, 131072, 8)
+    check_layer(lay, k, v, q[0], p1, 0.7, torch.bfloat16, "128K G=8 70B-shape")
+
+
+def test_parity_batch16_32k():
+    """(iii) batch 16 at 32K, one layer, 8 kv heads, G=4."""
+    lay, k, v, q = _bench_layer(16, 8, 32768, 4)
+    check_layer(lay, k, v, q[0], 0.95, 0.7, torch.bfloat16, "B=16 32K")
+
+
+@pytest.mark.parametrize("profile", ["peaked", "mixed"])
+def test_parity_config1_exact(profile):
+    """(iv) config 1 exactly: 8K tokens, 32 q / 8 kv heads, d=128, fp32 cache,
+    reference generator law (host), p=(0.95, 0.7)."""
+    from paper_2602_05191_b200 import cluster_layer
+
+    spec = O.WorkloadSpec(context_len=8192, head_dim=128, num_kv_heads=8, gqa_group=4, num_steps=2,
+                          tail_profile=profile, seed=0)
+    keys, values, queries = O.generate(spec)
+    kd = torch.from_numpy(keys[0]).cuda().unsqueeze(0)  # [1,8,8192,128] fp32
+    vd = torch.from_numpy(values[0]).cuda().unsqueeze(0)
+    lay = cluster_layer(kd, vd)
+    for s in range(2):
+        q = torch.from_numpy(queries[s, 0]).cuda().unsqueeze(0)  # [1,32,128] fp32
+        check_layer(lay, kd, vd, q, 0.95, 0.7, torch.float32, f"config1 8K fp32 {profile} step {s}")
+
+
+def test_growth_through_fused_path():
+    """(v) decode-time growth at the product shape: 8 kv heads, d=128, bf16,
+    G=4; 200 appended tokens (the window slides past 136 former window rows,
+    which become residual singleton clusters), then the fused product step."""
+    from paper_2602_05191_b200 import cluster_layer, sparse_attention
+    from paper_2602_05191_b200.workload import generate_layer, generate_queries
+
+    H, n, d, G, T = 8, 8192, 128, 4, 200
+    k, v, c = generate_layer(1, H, n, d)
+    lay = cluster_layer(k, v, fp64_assign=False, row_cap=n + T, extra_clusters=T)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(5)
+    app_k = (torch.randn((T, 1, H, d), generator=g, device="cuda") * 1.2).to(torch.bfloat16)
+    app_v = torch.randn((T, 1, H, d), generator=g, device="cuda").to(torch.bfloat16)
+    q = torch.from_numpy(generate_queries(c, G, 1)[0]).cuda().to(torch.bfloat16)
+    kf_all = torch.cat([k, app_k.permute(1, 2, 0, 3)], dim=2)  # [1,H,n+T,d] position order
+    vf_all = torch.cat([v, app_v.permute(1, 2, 0, 3)], dim=2)
+    for t in range(T):
+        lay.append(app_k[t], app_v[t])
+        if t in (30, 63, 64, 65, T - 1):  # before, at and past the window edge
+            sparse_attention(q, lay, 0.95, 0.7)  # the fused path between appends must stay sane
+    torch.cuda.synchronize()
+    assert lay.n_tokens == n + T
+    # oracle: prefill tables (first _prefill_k clusters) + its own residual pool
+    for p1, p2 in [(0.95, 0.7), (1.0, 1.0)]:
+        out, ws = sparse_attention(q, lay, p1, p2, return_plan=True)
+        out = out.double().cpu().numpy()
+        st = ws.state.cpu().numpy()
+        classes = {"exact": 0, "order_tie": 0, "threshold_tie": 0, "real": 0}
+        worst = 0.0
+        for h in range(H):
+            full = oracle_tables(lay, 0, h)
+            kp = int(lay.nclusters[0, h]) - (T)  # clusters present before growth
+            base = O.HeadTables(members=full.members[:kp], centroids=full.centroids[:kp],
+                                value_means=full.value_means[:kp])
+            kh = kf_all[0, h].double().cpu().numpy()
+            vh = vf_all[0, h].double().cpu().numpy()
+            tab = O.grow_tables(base, kh, vh, n, n + T, lay.window)
+            assert len(tab.members) == len(full.members)
+            for a_, b_ in zip(tab.members, full.members):
+                assert np.array_equal(a_, b_)
+            for gg in range(G):
+                hq = h * G + gg
+                qv = q[0, hq].double().cpu().numpy()
+                o_out, o_plan, o_est = O.decode_step(qv, kh, vh, tab, p1, p2, lay.sink, lay.window)
+                c1, c2 = classify_sets(o_est, o_plan, st[0, hq], p1, p2)
+                classes[c1] += 1
+                classes[c2] += 1
+                assert c1 != "real" and c2 != "real", (h, gg, c1, c2)
+                if c1 == "exact" and c2 == "exact":
+                    err = O.output_error(out[0, hq], o_out.output)
+                    worst = max(worst, err)
+                    assert err <= TOL[torch.bfloat16], (hq, err)
+        print(f"[PARITY] growth +{T} d128 bf16 fused: p=({p1},{p2}) classes {classes} worst {worst:.2e}")
+
+
+def test_dominant_sink_logit_is_finite():
+    """a sink/window logit far (>= 80 nats) above every cluster's
+    log-mass must not overflow the attention accumulators.  The output must
+    match the oracle (the sink dominates)."""
+    from paper_2602_05191_b200 import cluster_layer
+
+    H, n, d, G = 2, 4096, 128, 4
+    rng = np.random.default_rng(3)
+    keys = rng.normal(size=(1, H, n, d)).astype(np.float32) * 0.3
+    values = rng.normal(size=(1, H, n, d)).astype(np.float32)
+    q = rng.normal(size=(1, H * G, d)).astype(np.float32)
+    q /= np.linalg.norm(q, axis=-1, keepdims=True)
+    # sink token 0 aligned with every query: logit ~ 120 nats above the rest
+    for h in range(H):
+        keys[0, h, 0] = q[0, h * G] * (120.0 * math.sqrt(d))
+        q[0, h * G + 1:h * G + G] = q[0, h * G]
+    for dtype in (torch.bfloat16, torch.float32):
+        kd = torch.from_numpy(keys).cuda().to(dtype)
+        vd = torch.from_numpy(values).cuda().to(dtype)
+        lay = cluster_layer(kd, vd, fp64_assign=dtype == torch.float32)
+        qd = torch.from_numpy(q).cuda().to(dtype)
+        check_layer(lay, kd, vd, qd, 0.95, 0.7, dtype, f"dominant sink {dtype}")
