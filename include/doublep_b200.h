@@ -141,9 +141,17 @@ int dp_plan(const dp_cache_view* v, const void* q, int32_t q_dtype, int32_t gqa_
             void* stream);
 
 /* score + select + sparse attention in one call (decode_step,
- * engine.py:267-278): dp_plan + dp_attend when supported, else the separate
- * dp_score / dp_select / dp_sparse_attention kernels.  log_mass/state/counts are caller buffers so the plan
- * stays inspectable. */
+ * engine.py:267-278).  Implementations, chosen by geometry:
+ *   - dp_plan + dp_attend (fused plan, then a persistent attention grid
+ *     balanced over every head's rows) when the plan supports the shape;
+ *   - the separate dp_score / dp_select / dp_sparse_attention kernels;
+ *   - opt-in (dp_debug_set(6, 0)): ONE launch when one thread-block cluster
+ *     per (sequence, kv head) fits on the GPU in a single wave (bf16 cache,
+ *     head_dim 128, G <= 8, cluster_cap <= 4096): score, select, attention
+ *     over the cluster-contiguous runs (TMA) and the LSE merge, with
+ *     distributed shared memory between the cluster's CTAs.
+ * log_mass (required) / state / counts / stats are caller buffers so the
+ * plan stays inspectable. */
 int dp_decode_step(const dp_cache_view* v, const void* q, int32_t q_dtype, int32_t gqa_group,
                    double scale, double p1, double p2, double* log_mass, uint8_t* state,
                    int32_t* counts, float* out, float* lse, int32_t* stats, void* workspace,
@@ -281,9 +289,22 @@ int dp_debug_plan_clock(unsigned long long* out);
 int dp_debug_attn_timing(unsigned long long* out);
 /* Profiling switches: key 0 = attention flags (bit 0: skip the math, stream
  * K/V only); key 1 = force the plan cluster size (8 or 16; 0 = auto); key 3 = 1
- * runs k-means++ seeding on one CTA per head instead of an 8-CTA cluster.
+ * runs k-means++ seeding on one CTA per head instead of an 8-CTA cluster;
+ * key 4 = the one-launch step's L2 prefetch margin in 0.1-nat units (0 = off);
+ * key 5 = force the one-launch step's cluster size (0 = auto); key 6 = 0
+ * enables the one-launch step in dp_decode_step (default 1: off -- measured
+ * slower than dp_plan + dp_attend at 32K and 128K); key 7 = the
+ * one-launch step's profiling bits (1: skip the attention math, 2: skip the
+ * K/V loads).
  * Never set on the product path. */
 int dp_debug_set(int key, int value);
+/* Profiling aid: %globaltimer stamps of the last one-launch step (cluster 0),
+ * [16 ranks][16 events] followed by the selection's [16 CTAs][8 events]
+ * (out must hold 384 values; built with DP_PROFILE=1). */
+int dp_debug_step_timing(unsigned long long* out);
+/* The thread-block cluster size the one-launch step uses at this geometry
+ * (0: not supported -- dp_decode_step runs dp_plan + dp_attend). */
+int dp_debug_step_cluster_size(const dp_cache_view* v, int G);
 /* Profiling aid: co-resident plan clusters at this geometry for cluster size
  * cl (cudaOccupancyMaxActiveClusters). */
 int dp_debug_plan_occupancy(const dp_cache_view* v, int G, int cl);

@@ -66,6 +66,8 @@ _SIGS = {
     "dp_debug_plan_clock": (ctypes.c_int, [_vp]),
     "dp_debug_attn_timing": (ctypes.c_int, [_vp]),
     "dp_debug_set": (ctypes.c_int, [ctypes.c_int, ctypes.c_int]),
+    "dp_debug_step_timing": (ctypes.c_int, [_vp]),
+    "dp_debug_step_cluster_size": (ctypes.c_int, [ctypes.POINTER(CacheView), ctypes.c_int]),
     "dp_debug_plan_occupancy": (ctypes.c_int, [ctypes.POINTER(CacheView), ctypes.c_int, ctypes.c_int]),
     "dp_decode_step": (ctypes.c_int, [ctypes.POINTER(CacheView), _vp, ctypes.c_int32, ctypes.c_int32,
                                       ctypes.c_double, ctypes.c_double, ctypes.c_double, _vp, _vp,

@@ -28,6 +28,7 @@
 #include "common.cuh"
 #include "host_state.h"
 #include "decode_internal.h"
+#include "tc_common.cuh"
 
 namespace dp {
 
@@ -40,100 +41,12 @@ constexpr int kStages = 3;
 constexpr int kSegCost = 256;  // rows' worth of time a head segment start costs a CTA (range balancing)
 constexpr int kStageElems = kTcRows * kRowStride;  // one K (or V) tile
 int g_attn_debug = 0;  // profiling switches (dp_debug_set)
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-// K/V rows are read once per step: evict-first in L2, so the streamed cache
-// does not push out what is reused (code, work lists, partials, tables)
-__device__ __forceinline__ unsigned long long evict_first_policy() {
-  unsigned long long p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ void cp16(unsigned dst, const void* src, unsigned long long pol) {
-  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "l"(pol));
-}
-__device__ __forceinline__ void ldsm_x4(unsigned addr, unsigned& r0, unsigned& r1, unsigned& r2, unsigned& r3) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
-               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-               : "r"(addr));
-}
-__device__ __forceinline__ void ldsm_x4_t(unsigned addr, unsigned& r0, unsigned& r1, unsigned& r2, unsigned& r3) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
-               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-               : "r"(addr));
-}
-// D += A * B, m16n8k16 bf16 -> f32 (a1 = a3 = 0: rows 8..15 of A are unused heads)
-__device__ __forceinline__ void mma_bf16(float (&d)[4], unsigned a0, unsigned a2, unsigned b0, unsigned b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};\n"
-      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-      : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
-}
-__device__ __forceinline__ unsigned pack_bf16(float lo, float hi) {
-  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
-  return *reinterpret_cast<unsigned*>(&v);
-}
-// split (x, y) into a bf16 hi pair + a bf16 lo pair
-__device__ __forceinline__ void split2(float x, float y, unsigned& hi, unsigned& lo) {
-  const __nv_bfloat16 hx = __float2bfloat16_rn(x), hy = __float2bfloat16_rn(y);
-  __nv_bfloat162 h;
-  h.x = hx;
-  h.y = hy;
-  hi = *reinterpret_cast<unsigned*>(&h);
-  lo = pack_bf16(x - __bfloat162float(hx), y - __bfloat162float(hy));
-}
-
-// ---- bulk-copy engine (TMA, non-tensor) + mbarrier helpers -------------
-__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(unsigned bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
-}
-// the mbarrier tracks completion of this thread's prior cp.async copies
-__device__ __forceinline__ void cp_async_arrive(unsigned bar) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
-}
-// 16-byte cp.async that writes zeros (src-size 0)
-__device__ __forceinline__ void cp16_zero(unsigned dst, const void* any) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, 0;\n" ::"r"(dst), "l"(any));
-}
 // barrier over the 8 compute warps only (the producer warp never joins)
 __device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;\n" ::"n"(kConsumers) : "memory"); }
-
-__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n"
-      "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(bar),
-      "r"(parity)
-      : "memory");
-}
-// one contiguous row (bytes multiple of 16) global -> shared, completing on bar
-__device__ __forceinline__ void bulk_row(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
-               "l"(src), "r"(bytes), "r"(bar)
-               : "memory");
-}
 
 // per-CTA phase stamps (%globaltimer ns) of the last launch; profiling aid,
 // read with dp_debug_attn_timing()
 __device__ unsigned long long g_attn_ts[512][12];
-__device__ __forceinline__ void red_add_v4(float* p, float4 v) {  // p 16-B aligned
-  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
-               : "memory");
-}
-
-__device__ __forceinline__ int atom_add_acq_rel(int* p, int v) {
-  int old;
-  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;\n" : "=r"(old) : "l"(p), "r"(v) : "memory");
-  return old;
-}
 
 // (compiled in only with -DDP_PROFILE)
 __device__ __forceinline__ void astamp(int ev) {
@@ -832,11 +745,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
 }
 
 }  // namespace dp
-namespace dp { extern int g_plan_cl, g_pp_single; }
+namespace dp { extern int g_plan_cl, g_pp_single, g_step_cl, g_step_off, g_step_dbg; extern float g_step_tau; }
 extern "C" int dp_debug_set(int key, int value) {
   if (key == 0) dp::g_attn_debug = value;
   if (key == 1) dp::g_plan_cl = value;
   if (key == 3) dp::g_pp_single = value;
+  if (key == 4) dp::g_step_tau = 0.1f * (float)value;
+  if (key == 5) dp::g_step_cl = value;
+  if (key == 6) dp::g_step_off = value;
+  if (key == 7) dp::g_step_dbg = value;
   return 0;
 }
 extern "C" int dp_debug_attn_timing(unsigned long long* out) {

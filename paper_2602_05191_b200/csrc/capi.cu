@@ -143,6 +143,13 @@ int dp_decode_step(const dp_cache_view* v, const void* q, int32_t q_dtype, int32
                    int32_t* stats, void* ws, size_t ws_bytes, void* stream) {
   int r = check_view(v, G);
   if (r) return r;
+  if (dp::step_supported(*v, G, q_dtype)) {  // the whole step in one launch (every head's cluster co-resident)
+    if ((r = check_q(q_dtype)) || (r = check_p(p1, "p1")) || (r = check_p(p2, "p2"))) return r;
+    if (!log_mass) return fail(DP_ERR_INVALID, "log_mass buffer required");
+    cudaError_t e = dp::launch_step(*v, q, q_dtype, G, scale, p1, p2, log_mass, state, counts, stats, out, lse, ws,
+                                    (cudaStream_t)stream);
+    return e == cudaSuccess ? DP_OK : cuda_fail(e, "dp_decode_step");
+  }
   if (dp::plan_supported(*v, G)) {  // fused score + select + worklist (one launch) -> attend
     r = dp_plan(v, q, q_dtype, G, scale, p1, p2, log_mass, state, counts, stats, ws, ws_bytes, stream);
     if (r) return r;

@@ -1,6 +1,7 @@
 // Internal declarations shared by the decode translation units.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -79,6 +80,14 @@ cudaError_t launch_attn_tc(const dp_cache_view& v, const void* q, int qdt, int G
 cudaError_t launch_plan(const dp_cache_view& v, const void* q, int qdt, int G, double scale, double p1, double p2,
                         double* lm, uint8_t* state, int* counts, int* stats, void* ws, cudaStream_t st);
 bool plan_supported(const dp_cache_view& v, int G);
+// 2-D TMA map over all centroid rows [B*H*cap, d] fp32 (32-float x 128-row boxes, 128B swizzle), cached
+cudaError_t centroid_tmap(const dp_cache_view& v, CUtensorMap* m);
+// step.cu: the whole decode step (score + select + attention + merge) in ONE launch when every
+// (sequence, kv head) thread-block cluster is co-resident (batch-1 latency path)
+bool step_supported(const dp_cache_view& v, int G, int qdt);
+cudaError_t launch_step(const dp_cache_view& v, const void* q, int qdt, int G, double scale, double p1, double p2,
+                        double* lm, uint8_t* state, int* counts, int* stats, float* out, float* lse, void* ws,
+                        cudaStream_t st);
 cudaError_t launch_topk_state(const dp_cache_view& v, int G, int budget, const int* order, uint8_t* state,
                               int* counts, cudaStream_t st);
 cudaError_t launch_append(const dp_cache_view& v, const void* nk, const void* nv, cudaStream_t st);

@@ -38,6 +38,7 @@
 
 #include "common.cuh"
 #include "host_state.h"
+#include "select.cuh"
 #include "decode_internal.h"
 
 namespace cg = cooperative_groups;
@@ -47,16 +48,11 @@ namespace dp {
 constexpr int kPT = 512;          // threads per CTA
 constexpr int kPW = kPT / 32;     // warps per CTA
 constexpr int kBins = 2048;       // log-mass bins of width 1/32 nat (span 64 nats)
-constexpr float kBinScale = 32.f;
-constexpr int kBinsPT = kBins / kPT;  // 4 bins per thread
-constexpr double kFix = 549755813888.0;  // 2^39 fixed-point scale of e = exp(lm - max) <= 1
-// (mass below 2^-39 of the max rounds to zero: <= 4096 * 2^-39 < 1e-8 of the total)
 constexpr int kPlanMaxCap = 4096;
 constexpr int kCh = 128;          // centroid rows per shared-memory tile (P1)
 constexpr int kTileBytes = kCh * 128 * 4;  // one tile: kCh rows x 128 fp32 (4 swizzled column blocks)
 constexpr int kMaxPer = 1024;     // clusters per CTA slice (cap 4096 / 4)
 constexpr int kMaxCL = 16;
-constexpr int kCandBins = 8;      // stage-2 candidate bins ranked together with the stage-1 bin        // cluster size is chosen at launch (<= 16, non-portable above 8)
 
 // phase timestamps (%globaltimer, ns) of cluster 0: [rank][event]; read with
 // dp_debug_plan_timing() -- profiling aid only
@@ -140,169 +136,6 @@ __device__ __forceinline__ T* remote(cg::cluster_group& c, T* p, int rank) {
   return c.map_shared_rank(p, rank);
 }
 
-// block-wide exclusive scan of (mass u64, count int) pairs; totals to mt / ct.
-// Warp scans, then warp 0 scans the 16 warp totals (so no thread reads all
-// of them).  sm/sc need 2 * kPW + 1 slots; callers separate consecutive uses
-// with a barrier.
-__device__ __forceinline__ void scan_pair(unsigned long long m, int c, unsigned long long* sm, int* sc,
-                                          unsigned long long& mex, int& cex, unsigned long long& mt, int& ct) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  unsigned long long mi = m;
-  int ci = c;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const unsigned long long tm = __shfl_up_sync(0xffffffffu, mi, o);
-    const int tc = __shfl_up_sync(0xffffffffu, ci, o);
-    if (lane >= o) {
-      mi += tm;
-      ci += tc;
-    }
-  }
-  if (lane == 31) {
-    sm[warp] = mi;
-    sc[warp] = ci;
-  }
-  __syncthreads();
-  if (warp == 0) {
-    const unsigned long long wv = lane < kPW ? sm[lane] : 0ull;
-    const int wc = lane < kPW ? sc[lane] : 0;
-    unsigned long long wi = wv;
-    int wci = wc;
-#pragma unroll
-    for (int o = 1; o < kPW; o <<= 1) {
-      const unsigned long long tm = __shfl_up_sync(0xffffffffu, wi, o);
-      const int tc = __shfl_up_sync(0xffffffffu, wci, o);
-      if (lane >= o) {
-        wi += tm;
-        wci += tc;
-      }
-    }
-    if (lane < kPW) {
-      sm[kPW + lane] = wi - wv;
-      sc[kPW + lane] = wci - wc;
-    }
-    if (lane == kPW - 1) {
-      sm[2 * kPW] = wi;
-      sc[2 * kPW] = wci;
-    }
-  }
-  __syncthreads();
-  mex = sm[kPW + warp] + mi - m;
-  cex = sc[kPW + warp] + ci - c;
-  mt = sm[2 * kPW];
-  ct = sc[2 * kPW];
-}
-
-// ---------------------------------------------------------------------------
-// P2 pieces, one copy each (__noinline__): this code runs once per launch on
-// a cold instruction cache, so its footprint -- not its instruction count --
-// is what costs time.  All threads of the CTA call them.
-// ---------------------------------------------------------------------------
-struct SelShared {
-  unsigned long long before, at;
-  int b, n, nc, cbefore;
-};
-
-// first bin (< limit) whose inclusive mass reaches thr; before / cbefore =
-// mass / count of the bins ahead of it.  bm/bc: this thread's kBinsPT bins.
-__device__ __noinline__ int sel_find_bin(SelShared* sh, const unsigned long long* bm, const int* bc,
-                                         unsigned long long mbase, int cbase, double thr, int limit) {
-  const int tid = threadIdx.x;
-  if (tid == 0) {  // not found (no mass at all: a non-finite query) -> nothing ahead of the last bin
-    sh->b = kBins;
-    sh->before = 0;
-    sh->cbefore = 0;
-  }
-  __syncthreads();
-  unsigned long long m = mbase, hmass = 0;
-  int c = cbase, hit = -1, hcnt = 0;
-#pragma unroll
-  for (int j = 0; j < kBinsPT; ++j) {
-    const int b = tid * kBinsPT + j;
-    if (hit < 0 && b < limit && bm[j] && (double)(m + bm[j]) >= thr) {
-      hit = b;
-      hmass = m;
-      hcnt = c;
-    }
-    m += bm[j];
-    c += bc[j];
-  }
-  if (hit >= 0) atomicMin(&sh->b, hit);
-  __syncthreads();
-  const int bb = sh->b;
-  if (hit == bb) {
-    sh->before = hmass;
-    sh->cbefore = hcnt;
-  }
-  __syncthreads();
-  return bb;
-}
-
-// members of bin b -> clist (any order), then cord[rank] = member with the
-// exact (log-mass desc, cluster id asc) rank; returns the member count
-__device__ __noinline__ int sel_rank_bin(SelShared* sh, const uint16_t* binI, const double* lmall, int* clist,
-                                         int* cord, int K, int b) {
-  const int tid = threadIdx.x;
-  if (tid == 0) sh->nc = 0;
-  __syncthreads();
-#pragma unroll 1
-  for (int i = tid; i < K; i += kPT)
-    if (binI[i] == b) clist[atomicAdd(&sh->nc, 1)] = i;
-  __syncthreads();
-  const int n = sh->nc;
-#pragma unroll 1
-  for (int a = tid; a < n; a += kPT) {
-    const int ia = clist[a];
-    const double la = lmall[ia];
-    int rk = 0;
-#pragma unroll 1
-    for (int j = 0; j < n; ++j) {
-      const int ij = clist[j];
-      const double lj = lmall[ij];
-      rk += lj > la || (lj == la && ij < ia);
-    }
-    cord[rk] = ia;
-  }
-  __syncthreads();
-  return n;
-}
-
-// warp 0: first j < n with base + sum_{t<=j} u[cord[t]] >= thr (n if none);
-// sh->at = that inclusive sum
-__device__ __noinline__ int sel_cut(SelShared* sh, const unsigned long long* um, const int* cord, int n,
-                                    unsigned long long base, double thr) {
-  const int lane = threadIdx.x & 31;
-  if ((threadIdx.x >> 5) == 0) {
-    int res = n;
-    unsigned long long at = base;
-#pragma unroll 1
-    for (int j0 = 0; j0 < n; j0 += 32) {
-      const int j = j0 + lane;
-      unsigned long long inc = j < n ? um[cord[j]] : 0ull;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned long long t = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += t;
-      }
-      const unsigned long long cum = base + inc;
-      const unsigned hit = __ballot_sync(0xffffffffu, j < n && (double)cum >= thr);
-      if (hit) {
-        const int f = __ffs(hit) - 1;
-        res = j0 + f;
-        at = __shfl_sync(0xffffffffu, cum, f);
-        break;
-      }
-      base += __shfl_sync(0xffffffffu, inc, 31);
-      at = base;
-    }
-    if (lane == 0) {
-      sh->n = res;
-      sh->at = at;
-    }
-  }
-  __syncthreads();
-  return sh->n;
-}
 
 template <int kG>
 __global__ void __launch_bounds__(kPT, 1)
@@ -332,12 +165,9 @@ __global__ void __launch_bounds__(kPT, 1)
   __shared__ int s_cnt[kMaxCL][4];      // pushed slice counts (rows, exact clusters, approx clusters)
   __shared__ double s_Mg[kG];           // pushed head maxima (every CTA)
   __shared__ double s_wm[kPW][kG];
-  __shared__ unsigned long long s_redu[2 * kPW + 1];
-  __shared__ int s_redi[kPW * 4];
-  __shared__ SelShared s_sel;
-  __shared__ int s_lo, s_hi, s_bcnt[kCandBins + 1], s_boff[kCandBins + 1];
-  __shared__ unsigned long long s_pre_m[kCandBins];
-  __shared__ int s_pre_c[kCandBins];
+  __shared__ SelScratch<kPT> s_selx;
+  unsigned long long* s_redu = s_selx.redu;
+  int* s_redi = s_selx.redi;
 
   // Before griddepcontrol.wait only the cache tables are touched (centroid
   // tiles, offsets): the previous grid in the stream (the last layer's
@@ -489,7 +319,9 @@ __global__ void __launch_bounds__(kPT, 1)
     double swl[kG];
 #pragma unroll
     for (int g = 0; g < kG; ++g) swl[g] = -CUDART_INF;
-    const int nsw = v.sink + v.window, s0 = r * nsw / CL, s1 = (r + 1) * nsw / CL;
+    // with idle CTAs in P2 (CL > G) they take these rows after barrier A
+    // (sw_late below); otherwise every CTA takes a share here
+    const int nsw = CL > G ? 0 : v.sink + v.window, s0 = r * nsw / CL, s1 = (r + 1) * nsw / CL;
 #pragma unroll 1
     for (int t = s0 + warp; t < s1; t += kPW) {
       const int row = t < v.sink ? t : v.n_tokens - v.window + (t - v.sink);
@@ -533,13 +365,7 @@ __global__ void __launch_bounds__(kPT, 1)
     remote(cluster, &s_swx[0][0], tid)[r * kG + tid] = sm;
   }
   if (r < G) {  // owners: zero the histogram now (the tile buffers it overlays are consumed)
-    unsigned* hz = reinterpret_cast<unsigned*>(smem + L.hm);
-#pragma unroll
-    for (int j = 0; j < kBinsPT; ++j) {
-      hz[tid * kBinsPT + j] = 0u;
-      hz[kBins + tid * kBinsPT + j] = 0u;
-      reinterpret_cast<int*>(smem + L.hc)[tid * kBinsPT + j] = 0;
-    }
+    select_zero_hist<kPT, kBins>(reinterpret_cast<unsigned*>(smem + L.hm), reinterpret_cast<int*>(smem + L.hc));
   }
   stamp(r, 3);
   cl_sync();  // (A) every score is in its owner's shared memory
@@ -553,7 +379,6 @@ __global__ void __launch_bounds__(kPT, 1)
     uint8_t* stown = reinterpret_cast<uint8_t*>(smem + L.stown);  // this head's states, then packed out
     uint16_t* binI = reinterpret_cast<uint16_t*>(smem + L.bin);
     unsigned* hmh = reinterpret_cast<unsigned*>(smem + L.hm);  // [kBins] high 19 bits of the mass
-    unsigned* hml = hmh + kBins;                               // [kBins] low 20 bits
     int* hc = reinterpret_cast<int*>(smem + L.hc);
     int* clist = reinterpret_cast<int*>(smem + L.clist);
     int* cord = reinterpret_cast<int*>(smem + L.cord);
@@ -561,206 +386,9 @@ __global__ void __launch_bounds__(kPT, 1)
 #pragma unroll 1
     for (int rr = 0; rr < CL; ++rr) M = fmax(M, s_max[rr][g]);
     stamp(r, 20);
-#pragma unroll 1
-    for (int i = tid; i < K; i += kPT) {
-      const float xf = M == -CUDART_INF ? CUDART_INF_F : (float)(M - lmall[i]);  // >= 0 (+inf: no mass)
-      const unsigned long long u = __float2ull_rn(__expf(-xf) * (float)kFix);
-      int b = (int)(xf * kBinScale);
-      b = b < 0 ? 0 : (b >= kBins ? kBins - 1 : b);
-      um[i] = u;
-      binI[i] = (uint16_t)b;
-      if (u) {  // native 32-bit shared atomics (a 64-bit add is a CAS loop)
-        atomicAdd(&hmh[b], (unsigned)(u >> 20));
-        atomicAdd(&hml[b], (unsigned)(u & 0xFFFFFu));
-        atomicAdd(&hc[b], 1);  // zero-mass members only ever sit at or past the stage-1 bin
-      }
-    }
-    __syncthreads();
-    stamp(r, 21);
-    unsigned long long bm[kBinsPT];
-    int bc[kBinsPT];
-    unsigned long long msum = 0;
-    int csum = 0;
-#pragma unroll
-    for (int j = 0; j < kBinsPT; ++j) {
-      bm[j] = ((unsigned long long)hmh[tid * kBinsPT + j] << 20) + hml[tid * kBinsPT + j];
-      bc[j] = hc[tid * kBinsPT + j];
-      msum += bm[j];
-      csum += bc[j];
-    }
-    unsigned long long mbase, total;
-    int cbase, ctot;
-    scan_pair(msum, csum, s_redu, s_redi, mbase, cbase, total, ctot);
-    stamp(r, 22);
-    int cut1 = 0, cbefore1 = 0, n2 = 0;
+    int n1 = 0, n2 = 0;
+    select_two_stage<kPT, kBins>(K, M, lmall, p1, p2, um, binI, hmh, hc, clist, cord, stown, &s_selx, n1, n2);
     if (K > 0) {
-      // stage 1 (selection.py:57-58): the bin where the mass crosses p1 * total
-      const double thr1 = p1 * (double)total;
-      // always found for finite scores; a non-finite query must not index out of range
-      const int b1 = min(sel_find_bin(&s_sel, bm, bc, mbase, cbase, thr1, kBins), kBins - 1);
-      const unsigned long long before1 = s_sel.before;
-      cbefore1 = s_sel.cbefore;
-      stamp(r, 23);
-      // stage 2 (engine.py:191-194) crosses p2 * sub with sub in [before1, before1 + mass(b1)]:
-      // its bin lies in [blo, bhi] (or inside b1), so every candidate bin is ranked in ONE pass
-      const unsigned long long mb1 = ((unsigned long long)hmh[b1] << 20) + hml[b1];
-      if (tid == 0) {
-        s_lo = kBins;
-        s_hi = kBins;
-      }
-      __syncthreads();
-      {
-        const double tlo = p2 * (double)before1, thi = p2 * (double)(before1 + mb1);
-        unsigned long long m = mbase;
-        int hlo = -1, hhi = -1;
-#pragma unroll
-        for (int j = 0; j < kBinsPT; ++j) {
-          const int b = tid * kBinsPT + j;
-          if (b < b1 && bm[j]) {
-            if (hlo < 0 && (double)(m + bm[j]) >= tlo) hlo = b;
-            if (hhi < 0 && (double)(m + bm[j]) >= thi) hhi = b;
-          }
-          m += bm[j];
-        }
-        if (hlo >= 0) atomicMin(&s_lo, hlo);
-        if (hhi >= 0) atomicMin(&s_hi, hhi);
-      }
-      __syncthreads();
-      const int blo = s_lo;                              // kBins: every stage-2 crossing is inside b1
-      const int bhi = min(s_hi, b1 - 1);                 // s_hi = kBins: up to the bin before b1
-      const int nrange = blo <= bhi ? bhi - blo + 1 : 0;  // candidate bins below b1
-      const bool wide = nrange > kCandBins;             // rare: fall back to ranking b2 separately
-      const int rlo = wide ? kBins : blo, rhi = wide ? -1 : bhi;
-      {  // exclusive (mass, count) prefix of the candidate range bins
-        unsigned long long m = mbase;
-        int c = cbase;
-#pragma unroll
-        for (int j = 0; j < kBinsPT; ++j) {
-          const int b = tid * kBinsPT + j;
-          if (b >= blo && b < blo + kCandBins) {
-            s_pre_m[b - blo] = m;
-            s_pre_c[b - blo] = c;
-          }
-          m += bm[j];
-          c += bc[j];
-        }
-      }
-      // compaction: members of b1 and of [rlo, rhi]; per-bin counts -> segment offsets
-      if (tid <= kCandBins) s_bcnt[tid] = 0;
-      if (tid == 0) s_sel.nc = 0;
-      __syncthreads();
-#pragma unroll 1
-      for (int i = tid; i < K; i += kPT) {
-        const int b = binI[i];
-        if (b == b1 || (b >= rlo && b <= rhi)) {
-          clist[atomicAdd(&s_sel.nc, 1)] = i;
-          atomicAdd(&s_bcnt[b == b1 ? kCandBins : b - rlo], 1);
-        }
-      }
-      __syncthreads();
-      stamp(r, 11);
-      if (tid == 0) {  // segment offsets in rank order: range bins ascending, then b1
-        int o = 0;
-        for (int j = 0; j <= kCandBins; ++j) {
-          const int c = s_bcnt[j];
-          s_boff[j] = o;
-          o += c;
-        }
-      }
-      __syncthreads();
-      const int ncand = s_sel.nc;
-#pragma unroll 1
-      for (int a = tid; a < ncand; a += kPT) {  // exact rank (log-mass desc, id asc) within the bin
-        const int ia = clist[a], ba = binI[ia];
-        const double la = lmall[ia];
-        int rk = 0;
-#pragma unroll 1
-        for (int j = 0; j < ncand; ++j) {
-          const int ij = clist[j];
-          if (binI[ij] != ba) continue;
-          const double lj = lmall[ij];
-          rk += lj > la || (lj == la && ij < ia);
-        }
-        cord[s_boff[ba == b1 ? kCandBins : ba - rlo] + rk] = ia;
-      }
-      __syncthreads();
-      stamp(r, 12);
-      const int o1 = s_boff[kCandBins], n1c = s_bcnt[kCandBins];
-      const int j1 = sel_cut(&s_sel, um, cord + o1, n1c, before1, thr1);
-      cut1 = j1 < n1c ? j1 + 1 : n1c;
-      const double thr2 = p2 * (double)s_sel.at;  // retained mass (engine.py:191)
-      stamp(r, 13);
-      int b2 = b1, cut2;
-      if ((double)before1 >= thr2 && cbefore1 > 0) {  // crossing strictly below bin b1
-        if (!wide) {
-          // first range bin whose inclusive mass reaches thr2 (it exists: thr2 in [tlo, thi])
-          if (tid == 0) {
-            int bb = bhi;
-            for (int b = blo; b <= bhi; ++b) {
-              const unsigned long long mm = ((unsigned long long)hmh[b] << 20) + hml[b];
-              if (mm && (double)(s_pre_m[b - blo] + mm) >= thr2) {
-                bb = b;
-                break;
-              }
-            }
-            s_lo = bb;
-          }
-          __syncthreads();
-          b2 = s_lo;
-          const int n2c = s_bcnt[b2 - rlo], o2 = s_boff[b2 - rlo];
-          const int j2 = sel_cut(&s_sel, um, cord + o2, n2c, s_pre_m[b2 - blo], thr2);
-          cut2 = j2 < n2c ? j2 + 1 : n2c;
-          n2 = s_pre_c[b2 - blo] + cut2;
-#pragma unroll 1
-          for (int j = tid; j < n2c; j += kPT) {
-            const int i = cord[o2 + j];
-            stown[i] = (uint8_t)(j < cut2 ? 2 : 1);
-          }
-        } else {  // wide range: rank b2 on its own after emitting b1's states
-          b2 = min(sel_find_bin(&s_sel, bm, bc, mbase, cbase, thr2, b1), b1);
-          const unsigned long long before2 = s_sel.before;
-          const int cbefore2 = s_sel.cbefore;
-#pragma unroll 1
-          for (int j = tid; j < n1c; j += kPT) {
-            const int i = cord[o1 + j];
-            stown[i] = (uint8_t)(j < cut1 ? 1 : 0);
-          }
-          __syncthreads();
-          const int n2c = sel_rank_bin(&s_sel, binI, lmall, clist, cord, K, b2);
-          const int j2 = sel_cut(&s_sel, um, cord, n2c, before2, thr2);
-          cut2 = j2 < n2c ? j2 + 1 : n2c;
-          n2 = cbefore2 + cut2;
-#pragma unroll 1
-          for (int j = tid; j < n2c; j += kPT) {
-            const int i = cord[j];
-            stown[i] = (uint8_t)(j < cut2 ? 2 : 1);
-          }
-        }
-        if (!wide)
-#pragma unroll 1
-          for (int j = tid; j < n1c; j += kPT) {
-            const int i = cord[o1 + j];
-            stown[i] = (uint8_t)(j < cut1 ? 1 : 0);
-          }
-      } else {  // crossing inside b1's ranked prefix
-        const int j2 = sel_cut(&s_sel, um, cord + o1, cut1, before1, thr2);
-        cut2 = j2 < cut1 ? j2 + 1 : cut1;
-        n2 = cbefore1 + cut2;
-#pragma unroll 1
-        for (int j = tid; j < n1c; j += kPT) {
-          const int i = cord[o1 + j];
-          stown[i] = (uint8_t)(j < cut2 ? 2 : (j < cut1 ? 1 : 0));
-        }
-      }
-      // everything outside the boundary bins: bins < b2 exact, [b2, b1) approx, > b1 dropped
-#pragma unroll 1
-      for (int i = tid; i < K; i += kPT) {
-        const int b = binI[i];
-        if (b != b1 && b != b2) {
-          stown[i] = (uint8_t)(b < b2 ? 2 : (b < b1 ? 1 : 0));
-        }
-      }
-      __syncthreads();
       // states travel to the slice owners as packed 4-byte words (slices are 4-aligned)
 #pragma unroll 1
       for (int i = 4 * tid; i < K; i += 4 * kPT) {
@@ -773,15 +401,49 @@ __global__ void __launch_bounds__(kPT, 1)
       }
     }
     if (tid == 0) {
-      counts[2 * hq] = K > 0 ? cbefore1 + cut1 : 0;
-      counts[2 * hq + 1] = K > 0 ? n2 : 0;
+      counts[2 * hq] = n1;
+      counts[2 * hq + 1] = n2;
     }
-    (void)ctot;
     if (tid < CL) {
       double SW = -CUDART_INF;
+      if (CL <= G)
 #pragma unroll 1
-      for (int rr = 0; rr < CL; ++rr) SW = fmax(SW, s_swx[rr][g]);
-      remote(cluster, s_Mg, tid)[g] = ref_max(K > 0 ? M : -CUDART_INF, SW);
+        for (int rr = 0; rr < CL; ++rr) SW = fmax(SW, s_swx[rr][g]);
+      remote(cluster, s_Mg, tid)[g] = CL > G ? (K > 0 ? M : -CUDART_INF) : ref_max(K > 0 ? M : -CUDART_INF, SW);
+    }
+  }
+  if (CL > G && r >= G) {  // sw_late: the CTAs idle in P2 score the sink/window rows -> CTA 0
+    const int nid = CL - G, nsw = v.sink + v.window;
+    const int s0 = (r - G) * nsw / nid, s1 = (r - G + 1) * nsw / nid;
+    double swl[kG];
+#pragma unroll
+    for (int g = 0; g < kG; ++g) swl[g] = -CUDART_INF;
+#pragma unroll 1
+    for (int t = s0 + warp; t < s1; t += kPW) {
+      const int row = t < v.sink ? t : v.n_tokens - v.window + (t - v.sink);
+      const size_t kb = ((size_t)bh * v.row_cap + row) * d;
+      float kx[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) kx[j] = lane + 32 * j < d ? load_elem_f(v.keys, v.dtype, kb + lane + 32 * j) : 0.f;
+#pragma unroll
+      for (int g = 0; g < kG; ++g) {
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (lane + 32 * j < d) acc += (double)kx[j] * qd[g * qP + lane + 32 * j];
+        acc = warp_sum(acc) * scale;
+        if (g < G && acc == acc) swl[g] = fmax(swl[g], acc);
+      }
+    }
+    if (lane == 0)
+#pragma unroll
+      for (int g = 0; g < kG; ++g) s_sw[warp][g] = swl[g];
+    __syncthreads();
+    if (tid < G) {
+      double sm = -CUDART_INF;
+#pragma unroll 1
+      for (int w = 0; w < kPW; ++w) sm = fmax(sm, s_sw[w][tid]);
+      remote(cluster, &s_swx[0][0], 0)[r * kG + tid] = sm;
     }
   }
   stamp(r, 5);
@@ -879,7 +541,7 @@ __global__ void __launch_bounds__(kPT, 1)
     }
     unsigned long long ro64, trr64;
     int ao, taa;
-    scan_pair((unsigned long long)len, ma != 0 ? 1 : 0, s_redu, s_redi, ro64, ao, trr64, taa);
+    scan_pair<kPT>((unsigned long long)len, ma != 0 ? 1 : 0, s_redu, s_redi, ro64, ao, trr64, taa);
     const int ro = (int)ro64 + row_base;
     if (i0 == 0) stamp(r, 18);
     if (ma) apx[ao + apx_base] = make_int2(k0 + i, ma);
@@ -903,7 +565,16 @@ __global__ void __launch_bounds__(kPT, 1)
   }
   if (r == 0) {
     if (tid < G)  // reference max of the attention accumulators: the head's top log-mass (log2 units)
-      wl.refm[(size_t)bh * G + tid] = (float)(s_Mg[tid] * 1.4426950408889634);
+    {
+      double Mref = s_Mg[tid];
+      if (CL > G) {  // sink/window maxima pushed by the CTAs idle in P2
+        double SW = -CUDART_INF;
+#pragma unroll 1
+        for (int rr = G; rr < CL; ++rr) SW = fmax(SW, s_swx[rr][tid]);
+        Mref = ref_max(Mref, SW);
+      }
+      wl.refm[(size_t)bh * G + tid] = (float)(Mref * 1.4426950408889634);
+    }
     if (tid == 0) {
       const int all_r = tot_r + sw_rows;
       wl.nrows[bh] = all_r;
@@ -932,7 +603,7 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
 static cudaError_t centroid_tmap_encode(const dp_cache_view& v, CUtensorMap* m);
 // a few recent maps, keyed by (centroid pointer, rows, d): encoding costs host
 // microseconds on every layer of every step otherwise
-static cudaError_t centroid_tmap(const dp_cache_view& v, CUtensorMap* m) {
+cudaError_t centroid_tmap(const dp_cache_view& v, CUtensorMap* m) {
   struct Entry {
     const void* ptr;
     long long rows;

@@ -1,0 +1,447 @@
+// Two-stage top-p of one q head on one CTA (engine.py:180-213,
+// selection.py:36-65), shared by the plan kernel (plan.cu, 512 threads) and
+// the fused decode-step kernel (step.cu, 384 threads).
+//
+// e_k = exp(lm_k - max) as a 2^-39 fixed-point integer (exact,
+// order-independent sums); a mass histogram over 1/32-nat bins finds the bin
+// holding the p1 crossing (then p2 of the retained mass); only the boundary
+// bins are ranked exactly (log-mass desc, cluster id asc == the reference's
+// stable argsort order).  Cut semantics follow the reference: the first
+// prefix whose cumsum/total >= p (searchsorted left + 1, clamped to n).
+// Masses below 2^-39 of the max round to zero (<= 4096 * 2^-39 < 1e-8 of
+// the total): such clusters sit past the stage-1 cut for every p1 < 1.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <math_constants.h>
+#include <stdint.h>
+
+namespace dp {
+
+constexpr float kBinScale = 32.f;           // bins of 1/32 nat
+constexpr double kFix = 549755813888.0;     // 2^39 fixed-point scale of e = exp(lm - max) <= 1
+constexpr int kCandBins = 8;                // stage-2 candidate bins ranked together with the stage-1 bin
+
+// phase stamps of the first 16 CTAs' selections (profiling builds only, -DDP_PROFILE)
+static __device__ unsigned long long g_sel_ts[16][8];
+__device__ __forceinline__ void sel_stamp(int ev) {
+#ifdef DP_PROFILE
+  if (blockIdx.x < 16 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_sel_ts[blockIdx.x][ev] = t;
+  }
+#endif
+}
+
+// block-wide exclusive scan of (mass u64, count int) pairs; totals to mt / ct.
+// Warp scans, then warp 0 scans the 16 warp totals (so no thread reads all
+// of them).  sm/sc need 2 * (kT / 32) + 1 slots; callers separate consecutive uses
+// with a barrier.
+template <int kT>
+__device__ __forceinline__ void scan_pair(unsigned long long m, int c, unsigned long long* sm, int* sc,
+                                          unsigned long long& mex, int& cex, unsigned long long& mt, int& ct) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned long long mi = m;
+  int ci = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long tm = __shfl_up_sync(0xffffffffu, mi, o);
+    const int tc = __shfl_up_sync(0xffffffffu, ci, o);
+    if (lane >= o) {
+      mi += tm;
+      ci += tc;
+    }
+  }
+  if (lane == 31) {
+    sm[warp] = mi;
+    sc[warp] = ci;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const unsigned long long wv = lane < (kT / 32) ? sm[lane] : 0ull;
+    const int wc = lane < (kT / 32) ? sc[lane] : 0;
+    unsigned long long wi = wv;
+    int wci = wc;
+#pragma unroll
+    for (int o = 1; o < (kT / 32); o <<= 1) {
+      const unsigned long long tm = __shfl_up_sync(0xffffffffu, wi, o);
+      const int tc = __shfl_up_sync(0xffffffffu, wci, o);
+      if (lane >= o) {
+        wi += tm;
+        wci += tc;
+      }
+    }
+    if (lane < (kT / 32)) {
+      sm[(kT / 32) + lane] = wi - wv;
+      sc[(kT / 32) + lane] = wci - wc;
+    }
+    if (lane == (kT / 32) - 1) {
+      sm[2 * (kT / 32)] = wi;
+      sc[2 * (kT / 32)] = wci;
+    }
+  }
+  __syncthreads();
+  mex = sm[(kT / 32) + warp] + mi - m;
+  cex = sc[(kT / 32) + warp] + ci - c;
+  mt = sm[2 * (kT / 32)];
+  ct = sc[2 * (kT / 32)];
+}
+
+// ---------------------------------------------------------------------------
+// P2 pieces, one copy each (__noinline__): this code runs once per launch on
+// a cold instruction cache, so its footprint -- not its instruction count --
+// is what costs time.  All threads of the CTA call them.
+// ---------------------------------------------------------------------------
+struct SelShared {
+  unsigned long long before, at;
+  int b, n, nc, cbefore;
+};
+
+// first bin (< limit) whose inclusive mass reaches thr; before / cbefore =
+// mass / count of the bins ahead of it.  bm/bc: this thread's (NB / kT) bins.
+template <int kT, int NB>
+__device__ __noinline__ int sel_find_bin(SelShared* sh, const unsigned long long* bm, const int* bc,
+                                         unsigned long long mbase, int cbase, double thr, int limit) {
+  const int tid = threadIdx.x;
+  if (tid == 0) {  // not found (no mass at all: a non-finite query) -> nothing ahead of the last bin
+    sh->b = NB;
+    sh->before = 0;
+    sh->cbefore = 0;
+  }
+  __syncthreads();
+  unsigned long long m = mbase, hmass = 0;
+  int c = cbase, hit = -1, hcnt = 0;
+#pragma unroll
+  for (int j = 0; j < (NB / kT); ++j) {
+    const int b = tid * (NB / kT) + j;
+    if (hit < 0 && b < limit && bm[j] && (double)(m + bm[j]) >= thr) {
+      hit = b;
+      hmass = m;
+      hcnt = c;
+    }
+    m += bm[j];
+    c += bc[j];
+  }
+  if (hit >= 0) atomicMin(&sh->b, hit);
+  __syncthreads();
+  const int bb = sh->b;
+  if (hit == bb) {
+    sh->before = hmass;
+    sh->cbefore = hcnt;
+  }
+  __syncthreads();
+  return bb;
+}
+
+// members of bin b -> clist (any order), then cord[rank] = member with the
+// exact (log-mass desc, cluster id asc) rank; returns the member count
+template <int kT>
+__device__ __noinline__ int sel_rank_bin(SelShared* sh, const uint16_t* binI, const double* lmall, int* clist,
+                                         int* cord, int K, int b) {
+  const int tid = threadIdx.x;
+  if (tid == 0) sh->nc = 0;
+  __syncthreads();
+#pragma unroll 1
+  for (int i = tid; i < K; i += kT)
+    if (binI[i] == b) clist[atomicAdd(&sh->nc, 1)] = i;
+  __syncthreads();
+  const int n = sh->nc;
+#pragma unroll 1
+  for (int a = tid; a < n; a += kT) {
+    const int ia = clist[a];
+    const double la = lmall[ia];
+    int rk = 0;
+#pragma unroll 1
+    for (int j = 0; j < n; ++j) {
+      const int ij = clist[j];
+      const double lj = lmall[ij];
+      rk += lj > la || (lj == la && ij < ia);
+    }
+    cord[rk] = ia;
+  }
+  __syncthreads();
+  return n;
+}
+
+// warp 0: first j < n with base + sum_{t<=j} u[cord[t]] >= thr (n if none);
+// sh->at = that inclusive sum
+static __device__ __noinline__ int sel_cut(SelShared* sh, const unsigned long long* um, const int* cord, int n,
+                                    unsigned long long base, double thr) {
+  const int lane = threadIdx.x & 31;
+  if ((threadIdx.x >> 5) == 0) {
+    int res = n;
+    unsigned long long at = base;
+#pragma unroll 1
+    for (int j0 = 0; j0 < n; j0 += 32) {
+      const int j = j0 + lane;
+      unsigned long long inc = j < n ? um[cord[j]] : 0ull;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+      }
+      const unsigned long long cum = base + inc;
+      const unsigned hit = __ballot_sync(0xffffffffu, j < n && (double)cum >= thr);
+      if (hit) {
+        const int f = __ffs(hit) - 1;
+        res = j0 + f;
+        at = __shfl_sync(0xffffffffu, cum, f);
+        break;
+      }
+      base += __shfl_sync(0xffffffffu, inc, 31);
+      at = base;
+    }
+    if (lane == 0) {
+      sh->n = res;
+      sh->at = at;
+    }
+  }
+  __syncthreads();
+  return sh->n;
+}
+
+template <int kT>
+struct SelScratch {
+  SelShared sel;
+  unsigned long long redu[2 * (kT / 32) + 1];
+  int redi[(kT / 32) * 4];
+  int lo, hi, bcnt[kCandBins + 1], boff[kCandBins + 1];
+  unsigned long long pre_m[kCandBins];
+  int pre_c[kCandBins];
+};
+
+// zero the [2 * NB] mass halves and [NB] counts (callers do it early, off the
+// critical path; every thread of the CTA)
+template <int kT, int NB>
+__device__ __forceinline__ void select_zero_hist(unsigned* hm, int* hc) {
+#pragma unroll
+  for (int j = 0; j < NB / kT; ++j) {
+    hm[threadIdx.x * (NB / kT) + j] = 0u;
+    hm[NB + threadIdx.x * (NB / kT) + j] = 0u;
+    hc[threadIdx.x * (NB / kT) + j] = 0;
+  }
+}
+
+// Selection of one q head: lmall[K] log-masses (shared), M = their max.
+// Writes stown[i] = 2 exact / 1 approx / 0 dropped for i < K and returns the
+// stage-1 / stage-2 counts.  Scratch arrays (shared): um [K] u64, binI [K],
+// hm [2 * NB] (zeroed by select_zero_hist), hc [NB] (zeroed), clist [K],
+// cord [K].  Every thread of the CTA calls it.
+template <int kT, int NB>
+__device__ void select_two_stage(const int K, const double M, const double* lmall, const double p1,
+                                 const double p2, unsigned long long* um, uint16_t* binI, unsigned* hmh, int* hc,
+                                 int* clist, int* cord, uint8_t* stown, SelScratch<kT>* S, int& n1_out,
+                                 int& n2_out) {
+  static_assert(NB % kT == 0, "bins per thread");
+  const int tid = threadIdx.x;
+  unsigned* hml = hmh + NB;  // [NB] low 20 bits of the bin masses (hmh: high 19 bits)
+  sel_stamp(0);
+#pragma unroll 1
+    for (int i = tid; i < K; i += kT) {
+      const float xf = M == -CUDART_INF ? CUDART_INF_F : (float)(M - lmall[i]);  // >= 0 (+inf: no mass)
+      const unsigned long long u = __float2ull_rn(__expf(-xf) * (float)kFix);
+      int b = (int)(xf * kBinScale);
+      b = b < 0 ? 0 : (b >= NB ? NB - 1 : b);
+      um[i] = u;
+      binI[i] = (uint16_t)b;
+      if (u) {  // native 32-bit shared atomics (a 64-bit add is a CAS loop)
+        atomicAdd(&hmh[b], (unsigned)(u >> 20));
+        atomicAdd(&hml[b], (unsigned)(u & 0xFFFFFu));
+        atomicAdd(&hc[b], 1);  // zero-mass members only ever sit at or past the stage-1 bin
+      }
+    }
+    __syncthreads();
+    sel_stamp(1);
+    unsigned long long bm[(NB / kT)];
+    int bc[(NB / kT)];
+    unsigned long long msum = 0;
+    int csum = 0;
+#pragma unroll
+    for (int j = 0; j < (NB / kT); ++j) {
+      bm[j] = ((unsigned long long)hmh[tid * (NB / kT) + j] << 20) + hml[tid * (NB / kT) + j];
+      bc[j] = hc[tid * (NB / kT) + j];
+      msum += bm[j];
+      csum += bc[j];
+    }
+    unsigned long long mbase, total;
+    int cbase, ctot;
+    scan_pair<kT>(msum, csum, S->redu, S->redi, mbase, cbase, total, ctot);
+    sel_stamp(2);
+    int cut1 = 0, cbefore1 = 0, n2 = 0;
+    if (K > 0) {
+      // stage 1 (selection.py:57-58): the bin where the mass crosses p1 * total
+      const double thr1 = p1 * (double)total;
+      // always found for finite scores; a non-finite query must not index out of range
+      const int b1 = min(sel_find_bin<kT, NB>(&S->sel, bm, bc, mbase, cbase, thr1, NB), NB - 1);
+      sel_stamp(3);
+      const unsigned long long before1 = S->sel.before;
+      cbefore1 = S->sel.cbefore;
+      // stage 2 (engine.py:191-194) crosses p2 * sub with sub in [before1, before1 + mass(b1)]:
+      // its bin lies in [blo, bhi] (or inside b1), so every candidate bin is ranked in ONE pass
+      const unsigned long long mb1 = ((unsigned long long)hmh[b1] << 20) + hml[b1];
+      if (tid == 0) {
+        S->lo = NB;
+        S->hi = NB;
+      }
+      __syncthreads();
+      {
+        const double tlo = p2 * (double)before1, thi = p2 * (double)(before1 + mb1);
+        unsigned long long m = mbase;
+        int hlo = -1, hhi = -1;
+#pragma unroll
+        for (int j = 0; j < (NB / kT); ++j) {
+          const int b = tid * (NB / kT) + j;
+          if (b < b1 && bm[j]) {
+            if (hlo < 0 && (double)(m + bm[j]) >= tlo) hlo = b;
+            if (hhi < 0 && (double)(m + bm[j]) >= thi) hhi = b;
+          }
+          m += bm[j];
+        }
+        if (hlo >= 0) atomicMin(&S->lo, hlo);
+        if (hhi >= 0) atomicMin(&S->hi, hhi);
+      }
+      __syncthreads();
+      const int blo = S->lo;                              // NB: every stage-2 crossing is inside b1
+      const int bhi = min(S->hi, b1 - 1);                 // S->hi = NB: up to the bin before b1
+      const int nrange = blo <= bhi ? bhi - blo + 1 : 0;  // candidate bins below b1
+      const bool wide = nrange > kCandBins;             // rare: fall back to ranking b2 separately
+      const int rlo = wide ? NB : blo, rhi = wide ? -1 : bhi;
+      {  // exclusive (mass, count) prefix of the candidate range bins
+        unsigned long long m = mbase;
+        int c = cbase;
+#pragma unroll
+        for (int j = 0; j < (NB / kT); ++j) {
+          const int b = tid * (NB / kT) + j;
+          if (b >= blo && b < blo + kCandBins) {
+            S->pre_m[b - blo] = m;
+            S->pre_c[b - blo] = c;
+          }
+          m += bm[j];
+          c += bc[j];
+        }
+      }
+      // compaction: members of b1 and of [rlo, rhi]; per-bin counts -> segment offsets
+      if (tid <= kCandBins) S->bcnt[tid] = 0;
+      if (tid == 0) S->sel.nc = 0;
+      __syncthreads();
+#pragma unroll 1
+      for (int i = tid; i < K; i += kT) {
+        const int b = binI[i];
+        if (b == b1 || (b >= rlo && b <= rhi)) {
+          clist[atomicAdd(&S->sel.nc, 1)] = i;
+          atomicAdd(&S->bcnt[b == b1 ? kCandBins : b - rlo], 1);
+        }
+      }
+      __syncthreads();
+      sel_stamp(4);
+      if (tid == 0) {  // segment offsets in rank order: range bins ascending, then b1
+        int o = 0;
+        for (int j = 0; j <= kCandBins; ++j) {
+          const int c = S->bcnt[j];
+          S->boff[j] = o;
+          o += c;
+        }
+      }
+      __syncthreads();
+      const int ncand = S->sel.nc;
+#pragma unroll 1
+      for (int a = tid; a < ncand; a += kT) {  // exact rank (log-mass desc, id asc) within the bin
+        const int ia = clist[a], ba = binI[ia];
+        const double la = lmall[ia];
+        int rk = 0;
+#pragma unroll 1
+        for (int j = 0; j < ncand; ++j) {
+          const int ij = clist[j];
+          if (binI[ij] != ba) continue;
+          const double lj = lmall[ij];
+          rk += lj > la || (lj == la && ij < ia);
+        }
+        cord[S->boff[ba == b1 ? kCandBins : ba - rlo] + rk] = ia;
+      }
+      __syncthreads();
+      sel_stamp(5);
+      const int o1 = S->boff[kCandBins], n1c = S->bcnt[kCandBins];
+      const int j1 = sel_cut(&S->sel, um, cord + o1, n1c, before1, thr1);
+      sel_stamp(6);
+      cut1 = j1 < n1c ? j1 + 1 : n1c;
+      const double thr2 = p2 * (double)S->sel.at;  // retained mass (engine.py:191)
+      int b2 = b1, cut2;
+      if ((double)before1 >= thr2 && cbefore1 > 0) {  // crossing strictly below bin b1
+        if (!wide) {
+          // first range bin whose inclusive mass reaches thr2 (it exists: thr2 in [tlo, thi])
+          if (tid == 0) {
+            int bb = bhi;
+            for (int b = blo; b <= bhi; ++b) {
+              const unsigned long long mm = ((unsigned long long)hmh[b] << 20) + hml[b];
+              if (mm && (double)(S->pre_m[b - blo] + mm) >= thr2) {
+                bb = b;
+                break;
+              }
+            }
+            S->lo = bb;
+          }
+          __syncthreads();
+          b2 = S->lo;
+          const int n2c = S->bcnt[b2 - rlo], o2 = S->boff[b2 - rlo];
+          const int j2 = sel_cut(&S->sel, um, cord + o2, n2c, S->pre_m[b2 - blo], thr2);
+          cut2 = j2 < n2c ? j2 + 1 : n2c;
+          n2 = S->pre_c[b2 - blo] + cut2;
+#pragma unroll 1
+          for (int j = tid; j < n2c; j += kT) {
+            const int i = cord[o2 + j];
+            stown[i] = (uint8_t)(j < cut2 ? 2 : 1);
+          }
+        } else {  // wide range: rank b2 on its own after emitting b1's states
+          b2 = min(sel_find_bin<kT, NB>(&S->sel, bm, bc, mbase, cbase, thr2, b1), b1);
+          const unsigned long long before2 = S->sel.before;
+          const int cbefore2 = S->sel.cbefore;
+#pragma unroll 1
+          for (int j = tid; j < n1c; j += kT) {
+            const int i = cord[o1 + j];
+            stown[i] = (uint8_t)(j < cut1 ? 1 : 0);
+          }
+          __syncthreads();
+          const int n2c = sel_rank_bin<kT>(&S->sel, binI, lmall, clist, cord, K, b2);
+          const int j2 = sel_cut(&S->sel, um, cord, n2c, before2, thr2);
+          cut2 = j2 < n2c ? j2 + 1 : n2c;
+          n2 = cbefore2 + cut2;
+#pragma unroll 1
+          for (int j = tid; j < n2c; j += kT) {
+            const int i = cord[j];
+            stown[i] = (uint8_t)(j < cut2 ? 2 : 1);
+          }
+        }
+        if (!wide)
+#pragma unroll 1
+          for (int j = tid; j < n1c; j += kT) {
+            const int i = cord[o1 + j];
+            stown[i] = (uint8_t)(j < cut1 ? 1 : 0);
+          }
+      } else {  // crossing inside b1's ranked prefix
+        const int j2 = sel_cut(&S->sel, um, cord + o1, cut1, before1, thr2);
+        cut2 = j2 < cut1 ? j2 + 1 : cut1;
+        n2 = cbefore1 + cut2;
+#pragma unroll 1
+        for (int j = tid; j < n1c; j += kT) {
+          const int i = cord[o1 + j];
+          stown[i] = (uint8_t)(j < cut2 ? 2 : (j < cut1 ? 1 : 0));
+        }
+      }
+      // everything outside the boundary bins: bins < b2 exact, [b2, b1) approx, > b1 dropped
+#pragma unroll 1
+      for (int i = tid; i < K; i += kT) {
+        const int b = binI[i];
+        if (b != b1 && b != b2) {
+          stown[i] = (uint8_t)(b < b2 ? 2 : (b < b1 ? 1 : 0));
+        }
+      }
+      __syncthreads();
+    }
+  sel_stamp(7);
+  (void)ctot;
+  n1_out = K > 0 ? cbefore1 + cut1 : 0;
+  n2_out = K > 0 ? n2 : 0;
+}
+
+}  // namespace dp

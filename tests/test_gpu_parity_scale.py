@@ -214,3 +214,21 @@ def test_dominant_sink_logit_is_finite():
         lay = cluster_layer(kd, vd, fp64_assign=dtype == torch.float32)
         qd = torch.from_numpy(q).cuda().to(dtype)
         check_layer(lay, kd, vd, qd, 0.95, 0.7, dtype, f"dominant sink {dtype}")
+
+
+@pytest.mark.parametrize("n,H,G", [(32768, 8, 4), (2048, 2, 4), (8192, 2, 8)])
+def test_one_launch_step_parity(n, H, G):
+    """The opt-in one-launch decode step (step.cu: score + select + TMA-staged
+    attention + DSMEM merge in one kernel) against the oracle, including the
+    tiny-table shapes whose last tile is partial."""
+    from paper_2602_05191_b200 import _native as N
+
+    lib = N.lib()
+    lay, k, v, q = _bench_layer(1, H, n, G)
+    lib.dp_debug_set(6, 0)
+    try:
+        assert lib.dp_debug_step_cluster_size(lay.view(), G) > 0
+        check_layer(lay, k, v, q[0], 0.95, 0.7, torch.bfloat16, f"one-launch step {n} H{H} G{G}")
+        check_layer(lay, k, v, q[0], 1.0, 1.0, torch.bfloat16, f"one-launch step {n} H{H} G{G}")
+    finally:
+        lib.dp_debug_set(6, 1)
