@@ -8,12 +8,17 @@ ctypes; this package is the host-side mirror of the reference interface.
 """
 
 from .cache import (
+    Cluster,
     ClusteredCache,
     ClusteredLayer,
+    EstimationData,
     KvCache,
+    QueryTrace,
     build_clustered_cache,
     cluster_layer,
     default_cluster_count,
+    device_cache,
+    device_clustered,
     head_seed,
 )
 from .engine import (
@@ -36,7 +41,9 @@ from .engine import (
 )
 from .metrics import (
     adaptive_token_budget,
+    baseline_cluster_topk,
     baseline_token_topk,
+    baseline_token_topp_fixed_budget,
     cluster_approx_error,
     full_attention_weights,
     output_error,
@@ -51,6 +58,8 @@ __version__ = "0.1.0"
 BACKEND = "b200"
 
 __all__ = [
+    "Cluster", "EstimationData", "QueryTrace", "device_cache", "device_clustered", "baseline_cluster_topk",
+    "baseline_token_topp_fixed_budget",
     "AttentionOutput", "BACKEND", "ClusterEstimate", "ClusteredCache", "ClusteredLayer", "DecodeGraph", "DecodeWorkspace",
     "DoublePConfig", "KvCache", "PRESETS", "SelectionPlan", "TopPResult", "build_cache_for_config",
     "build_clustered_cache", "cluster_layer", "cluster_topk_attention", "decode_step", "default_cluster_count", "dense_attention",

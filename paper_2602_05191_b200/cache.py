@@ -15,6 +15,7 @@ so the k-means++ seeding picks the same points as the reference.
 from __future__ import annotations
 
 import math
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -38,6 +39,17 @@ def dtype_code(t):
 def default_cluster_count(middle_len, tokens_per_cluster=DEFAULT_TOKENS_PER_CLUSTER):
     """`clustering.py:261-263`."""
     return max(1, math.ceil(middle_len / tokens_per_cluster))
+
+
+def pad_dim(t, width=None):
+    """Zero-pad the last axis to ``width`` (default: the next multiple of 8,
+    the kernels' 16-B row granule).  Zero key/query coordinates leave every
+    dot product and distance unchanged; padded value coordinates stay 0."""
+    d = t.shape[-1]
+    width = ((d + 7) // 8) * 8 if width is None else width
+    if width == d:
+        return t
+    return torch.nn.functional.pad(t, (0, width - d))
 
 
 def head_seed(seed, layer, head, seq=0):
@@ -85,8 +97,11 @@ class ClusteredLayer:
     position of every row, for parity/reporting only)."""
 
     def __init__(self, keys, values, offs, nclusters, centroids, value_means, perm, n_tokens, sink,
-                 window, objective=None, iters=None, prefill_tokens=None):
+                 window, objective=None, iters=None, prefill_tokens=None, logical_dim=None):
         self.keys, self.values = keys, values
+        # head_dim of the caller's vectors when the device rows are zero-padded
+        # to a multiple of 8 (pad_dim); scores use 1/sqrt(logical_dim)
+        self.logical_dim = int(logical_dim) if logical_dim is not None else None
         self.offs, self.nclusters = offs, nclusters
         self.centroids, self.value_means = centroids, value_means
         self.perm = perm
@@ -112,6 +127,15 @@ class ClusteredLayer:
     @property
     def head_dim(self):
         return self.keys.shape[3]
+
+    @property
+    def dim(self):
+        """Head dim of the caller's vectors (== head_dim unless padded)."""
+        return self.logical_dim if self.logical_dim is not None else self.keys.shape[3]
+
+    @property
+    def attn_scale(self):
+        return 1.0 / math.sqrt(self.dim)
 
     @property
     def cluster_cap(self):
@@ -156,14 +180,18 @@ class ClusteredLayer:
     def append(self, new_k, new_v, stream=None):
         """Append one token per (b, h) (`ClusteredCache.append_tokens`,
         clustering.py:182-196).  new_k/new_v [B,H,d] on device."""
-        want = (self.batch, self.kv_heads, self.head_dim)
+        want = (self.batch, self.kv_heads, self.dim)
         if tuple(new_k.shape) != want or tuple(new_v.shape) != want:
             raise ValueError(f"appended token must have shape {want}")
-        if self.n_tokens >= self.row_cap:
-            raise ValueError("row capacity exhausted")
-        if self.n_tokens - self.window >= self.sink and \
-                self.n_tokens - self.prefill_tokens + 1 > self.cluster_cap - self._prefill_k:
-            raise ValueError("cluster table capacity exhausted")
+        new_k, new_v = pad_dim(new_k, self.head_dim), pad_dim(new_v, self.head_dim)
+        # the reference grows without bound (clustering.py:182-196): when the
+        # rows or the cluster table are full, reallocate with headroom (the
+        # `growth` argument of build_clustered_cache pre-reserves it instead)
+        need_c = self._prefill_k + (self.n_tokens + 1 - self.prefill_tokens)
+        if self.n_tokens >= self.row_cap or \
+                (self.n_tokens - self.window >= self.sink and need_c > self.cluster_cap):
+            step = max(64, self.row_cap // 8)
+            self.reserve(self.n_tokens + step, max(self.cluster_cap, need_c + step))
         nk = new_k.to(self.dtype).contiguous()
         nv = new_v.to(self.dtype).contiguous()
         v = self.view()
@@ -174,6 +202,34 @@ class ClusteredLayer:
 
     _prefill_k = 0
 
+    def reserve(self, row_cap, cluster_cap):
+        """Grow the row and cluster capacity (copies the used part; views and
+        captured DecodeGraphs over the old storage become stale)."""
+        B, H, R, d = self.keys.shape
+        row_cap, cluster_cap = max(int(row_cap), R), max(int(cluster_cap), self.cluster_cap)
+        if row_cap == R and cluster_cap == self.cluster_cap:
+            return
+        n = self.n_tokens
+
+        def grow(t, size, dim, fill=0):
+            shape = list(t.shape)
+            shape[dim] = size
+            out = torch.full(shape, fill, dtype=t.dtype, device=t.device)
+            out.narrow(dim, 0, t.shape[dim]).copy_(t)
+            return out
+
+        k = torch.empty((B, H, row_cap, d), dtype=self.keys.dtype, device=self.device)
+        v = torch.empty_like(k)
+        k[:, :, :n].copy_(self.keys[:, :, :n])
+        v[:, :, :n].copy_(self.values[:, :, :n])
+        self.keys, self.values = k, v
+        self.offs = grow(self.offs, cluster_cap + 1, 2)
+        self.centroids = grow(self.centroids, cluster_cap, 2)
+        self.value_means = grow(self.value_means, cluster_cap, 2)
+        if self.perm is not None:
+            self.perm = grow(self.perm, row_cap, 2)
+        self.__dict__.pop("_view", None)
+
     def split(self):
         """One single-sequence ClusteredLayer per batch entry, sharing storage
         (used to cluster many layers in one launch, then hand them out)."""
@@ -182,10 +238,20 @@ class ClusteredLayer:
             sl = lambda t: None if t is None else t[b:b + 1]  # noqa: E731
             lay = ClusteredLayer(sl(self.keys), sl(self.values), sl(self.offs), sl(self.nclusters),
                                  sl(self.centroids), sl(self.value_means), sl(self.perm), self.n_tokens,
-                                 self.sink, self.window, prefill_tokens=self.prefill_tokens)
+                                 self.sink, self.window, prefill_tokens=self.prefill_tokens,
+                                 logical_dim=self.logical_dim)
             lay._prefill_k = self._prefill_k
             out.append(lay)
         return out
+
+    def head(self, b, h):
+        """Single-(sequence, kv head) ClusteredLayer sharing this layer's storage."""
+        sl = lambda t: None if t is None else t[b:b + 1, h:h + 1]  # noqa: E731
+        lay = ClusteredLayer(sl(self.keys), sl(self.values), sl(self.offs), sl(self.nclusters), sl(self.centroids),
+                             sl(self.value_means), sl(self.perm), self.n_tokens, self.sink, self.window,
+                             prefill_tokens=self.prefill_tokens, logical_dim=self.logical_dim)
+        lay._prefill_k = self._prefill_k
+        return lay
 
     # host views for parity ----------------------------------------------
     def head_tables(self, b, h):
@@ -202,8 +268,8 @@ class ClusteredLayer:
             members.append(np.sort(pos))
         return {
             "members": members,
-            "centroids": self.centroids[b, h, :K].double().cpu().numpy(),
-            "value_means": self.value_means[b, h, :K].double().cpu().numpy(),
+            "centroids": self.centroids[b, h, :K, :self.dim].double().cpu().numpy(),
+            "value_means": self.value_means[b, h, :K, :self.dim].double().cpu().numpy(),
             "sizes": np.diff(offs),
             "offs": offs,
         }
@@ -300,7 +366,7 @@ def cluster_layer(keys, values, *, k=None, sink=4, window=64, seed=0, max_iters=
 
 
 # ---------------------------------------------------------------------------
-# reference-signature containers (kvcache.py:50-139, clustering.py:140-314)
+# reference-signature containers (kvcache.py:50-139, clustering.py:110-314)
 # ---------------------------------------------------------------------------
 
 
@@ -326,8 +392,9 @@ class KvCache:
         if not (torch.isfinite(k.float()).all() and torch.isfinite(v.float()).all()):
             raise ValueError("non-finite entries in keys/values")
         dev = torch.device("cuda")
-        object.__setattr__(self, "keys", k.to(dev).contiguous())
-        object.__setattr__(self, "values", v.to(dev).contiguous())
+        object.__setattr__(self, "_dim", int(k.shape[3]))
+        object.__setattr__(self, "keys", pad_dim(k.to(dev)).contiguous())
+        object.__setattr__(self, "values", pad_dim(v.to(dev)).contiguous())
 
     @property
     def num_layers(self):
@@ -343,15 +410,143 @@ class KvCache:
 
     @property
     def head_dim(self):
+        return self._dim
+
+    @property
+    def padded_dim(self):
+        """Row width on the device (head_dim rounded up to a multiple of 8)."""
         return self.keys.shape[3]
 
 
-class ClusteredCache:
-    """Per-layer clustered view of one sequence (`clustering.py:140-258`)."""
+# device copies of foreign caches (the reference's numpy KvCache or any object
+# with 4-D .keys/.values), keyed by identity and dropped with the object
+_DEV_CACHES = {}
 
-    def __init__(self, source, sink, window, layers):
+
+def device_cache(cache):
+    """This package's KvCache for ``cache``: itself, or a device copy of any
+    object exposing [L, Hkv, N, d] ``keys`` / ``values`` (the reference's
+    KvCache, kvcache.py:50-89), made once per object."""
+    if isinstance(cache, KvCache):
+        return cache
+    if not (hasattr(cache, "keys") and hasattr(cache, "values")):
+        if isinstance(cache, (tuple, list)) and len(cache) == 2:
+            return KvCache(*cache)
+        raise TypeError(f"expected a KvCache (an object with .keys and .values), got {type(cache).__name__}")
+    key = id(cache)
+    hit = _DEV_CACHES.get(key)
+    if hit is not None and hit[0]() is cache:
+        return hit[1]
+    dev = KvCache(cache.keys, cache.values)
+    try:
+        ref = weakref.ref(cache, lambda _r, k=key: _DEV_CACHES.pop(k, None))
+    except TypeError:  # not weak-referenceable: convert per call
+        return dev
+    _DEV_CACHES[key] = (ref, dev)
+    return dev
+
+
+@dataclass(frozen=True)
+class QueryTrace:
+    """Per-step decode queries for every layer and query head (`kvcache.py:92-139`).
+
+    queries: [steps, layers, q_heads, d] (numpy or torch, any float dtype;
+    kept float32 on the host as in the reference); query head h reads kv
+    head h // gqa_group.  ``step_queries`` hands the product path one
+    (step, layer) slice as a device tensor [1, q_heads, d]."""
+
+    queries: np.ndarray
+    gqa_group: int
+
+    def __post_init__(self):
+        q = self.queries
+        q = q.detach().float().cpu().numpy() if isinstance(q, torch.Tensor) else np.asarray(q)
+        q = np.ascontiguousarray(q, dtype=np.float32)
+        if not np.all(np.isfinite(q)):
+            raise ValueError("non-finite entries in queries")
+        if q.ndim != 4:
+            raise ValueError("queries must have shape (steps, layers, q_heads, dim)")
+        if min(q.shape[1:]) < 1:
+            raise ValueError(f"layer/head/dim axes must be positive, got {q.shape}")
+        if self.gqa_group < 1:
+            raise ValueError("gqa_group must be >= 1")
+        if q.shape[2] % self.gqa_group != 0:
+            raise ValueError(f"num_query_heads {q.shape[2]} not divisible by gqa_group {self.gqa_group}")
+        object.__setattr__(self, "queries", q)
+
+    @property
+    def num_steps(self):
+        return self.queries.shape[0]
+
+    @property
+    def num_layers(self):
+        return self.queries.shape[1]
+
+    @property
+    def num_query_heads(self):
+        return self.queries.shape[2]
+
+    @property
+    def head_dim(self):
+        return self.queries.shape[3]
+
+    def kv_head_for(self, query_head):
+        return query_head // self.gqa_group
+
+    def query(self, step, layer, query_head):
+        """One float32 query vector of length head_dim."""
+        return self.queries[step, layer, query_head]
+
+    def step_queries(self, step, layer, device=None, dtype=torch.float32):
+        """All q heads of one (step, layer) as a device tensor [1, Hq, d]."""
+        t = torch.from_numpy(self.queries[step, layer]).unsqueeze(0)
+        return t.to(device if device is not None else torch.device("cuda")).to(dtype)
+
+
+@dataclass
+class Cluster:
+    """`clustering.py:110-118` (host copy of one device cluster)."""
+
+    members: np.ndarray
+    centroid: np.ndarray
+    size: int
+    value_mean: np.ndarray
+
+    @property
+    def value_sum(self):
+        return self.value_mean * self.size
+
+
+class EstimationData:
+    """`clustering.py:121-127`: dense centroid / log-size / value-mean arrays
+    plus the cluster list of one head, copied from the device tables (fp32
+    centroids and value means, as stored for decode).  Also indexable by the
+    ``head_tables`` keys ("members", "centroids", "value_means", "sizes",
+    "offs")."""
+
+    def __init__(self, tables):
+        self._t = tables
+        self.centroids = tables["centroids"]
+        self.value_means = tables["value_means"]
+        self.log_sizes = np.log(tables["sizes"].astype(np.float64))
+        self.clusters = [Cluster(members=m, centroid=c, size=int(sz), value_mean=vm) for m, c, sz, vm in
+                         zip(tables["members"], tables["centroids"], tables["sizes"], tables["value_means"])]
+
+    def __getitem__(self, key):
+        return self._t[key]
+
+
+class ClusteredCache:
+    """Per-layer clustered view of one sequence (`clustering.py:140-258`).
+    ``source`` is the cache object the caller passed (identity-checked by
+    sparse_attention / recovered_mass, as in the reference); ``device_source``
+    its device copy."""
+
+    def __init__(self, source, sink, window, layers, device_source=None):
         self.source, self.sink, self.window = source, sink, window
+        self.device_source = device_source if device_source is not None else source
         self.layers = layers
+        self._est = {}
 
     @property
     def num_appended(self):
@@ -379,25 +574,157 @@ class ClusteredCache:
         want = (self.source.num_layers, self.source.num_kv_heads, self.source.head_dim)
         if tuple(nk.shape) != want or tuple(nv.shape) != want:
             raise ValueError(f"appended token must have shape {want}")
+        if not (torch.isfinite(nk.float()).all() and torch.isfinite(nv.float()).all()):
+            raise ValueError("non-finite entries in appended token")
         dev = self.layers[0].device
         for li, lay in enumerate(self.layers):
             lay.append(nk[li].unsqueeze(0).to(dev), nv[li].unsqueeze(0).to(dev))
+        self._est.clear()
 
     def estimation_data(self, layer, kv_head):
-        """Host view of one head's tables (members, centroids, value means)."""
-        return self.layers[layer].head_tables(0, kv_head)
+        """`clustering.py:243-258`: host copy of one head's tables (cached
+        until the next append)."""
+        key = (layer, kv_head, self.total_tokens)
+        hit = self._est.get(key)
+        if hit is None:
+            hit = self._est[key] = EstimationData(self.layers[layer].head_tables(0, kv_head))
+        return hit
+
+    def head_clusters(self, layer, kv_head):
+        """`clustering.py:219-229`: middle clusters plus residual singletons."""
+        return self.estimation_data(layer, kv_head).clusters
+
+    @property
+    def clusters(self):
+        """`clusters[layer][kv_head]`: the prefill (middle-range) clusters."""
+        stop = self.source.context_len - self.window
+        return [[[c for c in self.head_clusters(li, h) if c.members[0] < stop]
+                 for h in range(self.source.num_kv_heads)] for li in range(len(self.layers))]
+
+    def _rows_of(self, layer, kv_head, positions):
+        lay = self.layers[layer]
+        positions = np.asarray(positions, dtype=np.int64)
+        mid_end = lay.prefill_tokens - lay.window
+        rows = positions.copy()
+        inmid = (positions >= lay.sink) & (positions < mid_end)
+        if inmid.any():
+            perm = lay.perm[0, kv_head, :mid_end].cpu().numpy().astype(np.int64)
+            inv = np.empty(mid_end, dtype=np.int64)
+            inv[perm[lay.sink:mid_end]] = np.arange(lay.sink, mid_end)
+            rows[inmid] = inv[positions[inmid]]
+        return rows
+
+    def gather_keys(self, layer, kv_head, positions):
+        """`clustering.py:198-203`: host f32 key rows at token positions."""
+        rows = torch.from_numpy(self._rows_of(layer, kv_head, positions)).to(self.layers[layer].device)
+        lay = self.layers[layer]
+        return lay.keys[0, kv_head, :, :lay.dim].index_select(0, rows).float().cpu().numpy()
+
+    def gather_values(self, layer, kv_head, positions):
+        rows = torch.from_numpy(self._rows_of(layer, kv_head, positions)).to(self.layers[layer].device)
+        lay = self.layers[layer]
+        return lay.values[0, kv_head, :, :lay.dim].index_select(0, rows).float().cpu().numpy()
+
+
+# device clustered caches made from the reference's ClusteredCache objects
+_DEV_CLUSTERED = {}
+
+
+def device_clustered(cc, headroom=256):
+    """This package's ClusteredCache for ``cc``: itself, or -- for the
+    reference's ClusteredCache (clustering.py:140-258: host clusters from its
+    own k-means) -- the same clusters uploaded into the device layout (sink
+    rows, each cluster's members contiguous in cluster order, then the
+    residual singletons and the window at their own positions; fp32
+    centroids and value means).  Made once per object; tokens appended to
+    the reference object since are appended here too."""
+    if isinstance(cc, ClusteredCache):
+        return cc
+    if not (hasattr(cc, "clusters") and hasattr(cc, "source") and hasattr(cc, "head_clusters")):
+        raise TypeError(f"expected a ClusteredCache, got {type(cc).__name__}")
+    key = id(cc)
+    hit = _DEV_CLUSTERED.get(key)
+    if hit is not None and hit[0]() is cc:
+        ours = hit[1]
+        have, want = ours.num_appended, int(cc.num_appended)
+        if have == want:
+            return ours
+        if have < want:
+            for j in range(have, want):
+                ours.append_tokens(cc._extra_keys[j], cc._extra_values[j])
+            return ours
+    ours = _upload_reference_clustered(cc, headroom)
+    try:
+        ref = weakref.ref(cc, lambda _r, k=key: _DEV_CLUSTERED.pop(k, None))
+        _DEV_CLUSTERED[key] = (ref, ours)
+    except TypeError:
+        pass
+    return ours
+
+
+def _upload_reference_clustered(cc, headroom):
+    src = cc.source
+    L, H, n, d = (src.num_layers, src.num_kv_heads, src.context_len, src.head_dim)
+    sink, window = int(cc.sink), int(cc.window)
+    dev = torch.device("cuda")
+    keys = np.asarray(src.keys, dtype=np.float32)
+    values = np.asarray(src.values, dtype=np.float32)
+    dl, d = d, ((d + 7) // 8) * 8  # device rows zero-padded to a multiple of 8
+    if d != dl:
+        keys = np.concatenate([keys, np.zeros(keys.shape[:3] + (d - dl,), np.float32)], 3)
+        values = np.concatenate([values, np.zeros(values.shape[:3] + (d - dl,), np.float32)], 3)
+    mid_end = n - window
+    kmax = max(len(cc.clusters[li][h]) for li in range(L) for h in range(H))
+    cap, row_cap = kmax + headroom, n + headroom
+    layers = []
+    for li in range(L):
+        K = np.zeros((1, H, row_cap, d), np.float32)
+        V = np.zeros_like(K)
+        offs = np.zeros((1, H, cap + 1), np.int32)
+        ncl = np.zeros((1, H), np.int32)
+        cents = np.zeros((1, H, cap, d), np.float32)
+        vbar = np.zeros_like(cents)
+        perm = np.zeros((1, H, row_cap), np.int32)
+        for h in range(H):
+            cl = cc.clusters[li][h]
+            order = np.concatenate([np.arange(sink)] + [np.asarray(c.members, np.int64) for c in cl] +
+                                   [np.arange(mid_end, n)])
+            if order.size != n:
+                raise ValueError("clusters do not partition the middle token range")
+            K[0, h, :n], V[0, h, :n] = keys[li, h, order], values[li, h, order]
+            perm[0, h, :n] = order
+            sizes = np.array([len(c.members) for c in cl], np.int64)
+            offs[0, h, :len(cl) + 1] = sink + np.concatenate([[0], np.cumsum(sizes)])
+            ncl[0, h] = len(cl)
+            if cl:
+                cents[0, h, :len(cl), :dl] = np.stack([np.asarray(c.centroid, np.float64) for c in cl])
+                vbar[0, h, :len(cl), :dl] = np.stack([np.asarray(c.value_mean, np.float64) for c in cl])
+        t = lambda a: torch.from_numpy(a).to(dev)  # noqa: E731
+        lay = ClusteredLayer(t(K), t(V), t(offs), t(ncl), t(cents), t(vbar), t(perm), n, sink, window,
+                             prefill_tokens=n, logical_dim=dl)
+        lay._prefill_k = kmax
+        layers.append(lay)
+    ours = ClusteredCache(src, sink, window, layers, device_source=device_cache(src))
+    for j in range(int(cc.num_appended)):
+        ours.append_tokens(cc._extra_keys[j], cc._extra_values[j])
+    return ours
 
 
 def build_clustered_cache(cache, k=None, sink=4, window=64, seed=0, max_iters=DEFAULT_MAX_ITERS,
                           tokens_per_cluster=DEFAULT_TOKENS_PER_CLUSTER, growth=0, fp64_assign=True):
-    """`clustering.py:266-314` on the GPU.  ``growth`` reserves rows/clusters
-    for that many appended tokens."""
-    if not isinstance(cache, KvCache):
-        cache = KvCache(*cache)
+    """`clustering.py:266-314` on the GPU.  ``cache`` is this package's
+    KvCache or any object with [L, Hkv, N, d] ``keys``/``values`` (the
+    reference's KvCache); the returned ClusteredCache keeps it as ``source``.
+    ``growth`` pre-reserves rows/clusters for that many appended tokens
+    (appends past it reallocate)."""
+    dev = device_cache(cache)
+    if isinstance(cache, (tuple, list)):
+        cache = dev
     layers = []
-    for li in range(cache.num_layers):
+    for li in range(dev.num_layers):
         layers.append(cluster_layer(
-            cache.keys[li:li + 1], cache.values[li:li + 1], k=k, sink=sink, window=window, seed=seed,
+            dev.keys[li:li + 1], dev.values[li:li + 1], k=k, sink=sink, window=window, seed=seed,
             max_iters=max_iters, tokens_per_cluster=tokens_per_cluster, layer=li, fp64_assign=fp64_assign,
-            row_cap=cache.context_len + growth, extra_clusters=growth))
-    return ClusteredCache(cache, sink, window, layers)
+            row_cap=dev.context_len + growth, extra_clusters=growth))
+        layers[-1].logical_dim = dev.head_dim
+    return ClusteredCache(cache, sink, window, layers, device_source=dev)

@@ -246,7 +246,7 @@ def _select(lay, q, G, p1, p2):
     cum = torch.zeros((1, H * G), dtype=torch.float64, device=dev)
     s = torch.cuda.current_stream(dev).cuda_stream
     v = lay.view()
-    N.check(N.lib().dp_score(v, N.ptr(q), dtype_code(q), G, 1.0 / math.sqrt(lay.head_dim), N.ptr(lm), s))
+    N.check(N.lib().dp_score(v, N.ptr(q), dtype_code(q), G, lay.attn_scale, N.ptr(lm), s))
     N.check(N.lib().dp_select(v, G, p1, p2, N.ptr(lm), N.ptr(st), N.ptr(cnt), None, N.ptr(cum), None, None, 0, s))
     return lm, st, cnt, cum
 

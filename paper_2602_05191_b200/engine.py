@@ -27,7 +27,8 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .cache import ClusteredCache, ClusteredLayer, KvCache, default_cluster_count, dtype_code
+from .cache import (ClusteredCache, ClusteredLayer, KvCache, default_cluster_count, device_cache, device_clustered,
+                    dtype_code, pad_dim)
 
 
 @dataclass(frozen=True)
@@ -123,7 +124,7 @@ def _sparse_layer(q, layer, p1=0.95, p2=0.7, *, workspace=None, return_plan=Fals
     elif out.dtype != torch.float32 or tuple(out.shape) != tuple(ws.out.shape) or not out.is_contiguous():
         raise ValueError(f"out must be a contiguous float32 tensor of shape {tuple(ws.out.shape)}")
     q = q.contiguous()
-    sc = 1.0 / math.sqrt(layer.head_dim) if scale is None else scale
+    sc = layer.attn_scale if scale is None else scale
     N.check(N.lib().dp_decode_step(
         layer.view(), N.ptr(q), dtype_code(q), G, sc, p1, p2, N.ptr(ws.log_mass), N.ptr(ws.state),
         N.ptr(ws.counts), N.ptr(out), N.ptr(ws.lse), N.ptr(ws.stats), N.ptr(ws.ws), ws.ws.numel(),
@@ -226,7 +227,7 @@ def cluster_topk_attention(q, layer, budget, *, workspace=None, stream=None, sca
     if getattr(ws, "order", None) is None:
         ws.order = torch.zeros(ws.state.shape, dtype=torch.int32, device=ws.state.device)
     q = q.contiguous()
-    sc = 1.0 / math.sqrt(layer.head_dim) if scale is None else scale
+    sc = layer.attn_scale if scale is None else scale
     N.check(N.lib().dp_cluster_topk(
         layer.view(), N.ptr(q), dtype_code(q), G, sc, int(budget), N.ptr(ws.log_mass), N.ptr(ws.state),
         N.ptr(ws.order), N.ptr(ws.counts), N.ptr(ws.out), N.ptr(ws.lse), N.ptr(ws.stats), N.ptr(ws.ws),
@@ -240,7 +241,7 @@ def dense_attention(q, layer, *, workspace=None, stream=None, scale=None, return
     G = _group(q, layer)
     ws = workspace if workspace is not None and workspace.fits(layer, G) else DecodeWorkspace(layer, G)
     q = q.contiguous()
-    sc = 1.0 / math.sqrt(layer.head_dim) if scale is None else scale
+    sc = layer.attn_scale if scale is None else scale
     N.check(N.lib().dp_dense_attention(layer.view(), N.ptr(q), dtype_code(q), G, sc, N.ptr(ws.out),
                                        N.ptr(ws.lse), N.ptr(ws.ws), ws.ws.numel(), _stream(layer, stream)))
     return (ws.out, ws.lse) if return_lse else ws.out
@@ -308,7 +309,7 @@ def _head_q(q, lay):
     qt = torch.as_tensor(q, device=lay.device)
     if qt.dtype not in (torch.float32, torch.bfloat16):
         qt = qt.float()
-    return qt.reshape(1, 1, -1).contiguous()
+    return pad_dim(qt.reshape(1, 1, -1), lay.head_dim).contiguous()
 
 
 class _HeadBufs:
@@ -323,7 +324,9 @@ class _HeadBufs:
 
 
 def estimate_cluster_distribution(q, cc, layer, kv_head):
-    """`engine.py:158-177` via dp_score (+ the softmax/order of dp_select)."""
+    """`engine.py:158-177` via dp_score (+ the softmax/order of dp_select).
+    ``cc`` may also be the reference's ClusteredCache (uploaded once)."""
+    cc = device_clustered(cc)
     lay = cc.layers[layer]
     K = int(lay.nclusters[0, kv_head].item())
     if K == 0:
@@ -333,7 +336,7 @@ def estimate_cluster_distribution(q, cc, layer, kv_head):
     bufs = _HeadBufs(lay, lay.device)
     v = lay.view(0, kv_head)
     st = torch.cuda.current_stream(lay.device).cuda_stream
-    N.check(N.lib().dp_score(v, N.ptr(qd), dtype_code(qd), 1, 1.0 / math.sqrt(lay.head_dim),
+    N.check(N.lib().dp_score(v, N.ptr(qd), dtype_code(qd), 1, lay.attn_scale,
                              N.ptr(bufs.lm), st))
     # stage thresholds irrelevant here; p=1 keeps the full order
     N.check(N.lib().dp_select(v, 1, 1.0, 1.0, N.ptr(bufs.lm), N.ptr(bufs.state), N.ptr(bufs.counts),
@@ -371,11 +374,12 @@ def _sparse_ref(q, cache, cc, plan, layer, kv_head):
     """`engine.py:255-264` via dp_sparse_attention on the plan's device state."""
     if cc.source is not cache:
         raise ValueError("plan/cc mismatch: clustered cache built from a different cache")
+    cc = device_clustered(cc)
     est = plan.estimate
     if est.cc is not cc or est.layer != layer or est.kv_head != kv_head:
         raise ValueError("plan/cc mismatch: plan was derived for a different head or cache")
     lay = cc.layers[layer]
-    _check_query(q, lay.head_dim)
+    _check_query(q, lay.dim)
     qd = _head_q(q, lay)
     bufs, _ = est._dev
     out = torch.zeros((1, 1, lay.head_dim), dtype=torch.float32, device=lay.device)
@@ -383,11 +387,11 @@ def _sparse_ref(q, cache, cc, plan, layer, kv_head):
     v = lay.view(0, kv_head)
     ws = torch.zeros((N.lib().dp_decode_workspace_bytes(v, 1),), dtype=torch.uint8, device=lay.device)
     st = torch.cuda.current_stream(lay.device).cuda_stream
-    N.check(N.lib().dp_sparse_attention(v, N.ptr(qd), dtype_code(qd), 1, 1.0 / math.sqrt(lay.head_dim),
+    N.check(N.lib().dp_sparse_attention(v, N.ptr(qd), dtype_code(qd), 1, lay.attn_scale,
                                         N.ptr(bufs.lm), N.ptr(plan._state), N.ptr(out), N.ptr(lse), None,
                                         N.ptr(ws), ws.numel(), st))
     lz = float(lse.item())
-    return AttentionOutput(output=out[0, 0].double().cpu().numpy(), normalizer=math.exp(lz),
+    return AttentionOutput(output=out[0, 0, :lay.dim].double().cpu().numpy(), normalizer=math.exp(lz),
                            exact_token_count=int(plan.exact_tokens.size),
                            approx_cluster_count=int(plan.approx_clusters.size), log_normalizer=lz)
 
@@ -398,6 +402,7 @@ def decode_step(q, cache, cc, cfg, layer, kv_head):
         raise ValueError(
             "config/cache mismatch: clustered cache was built with "
             f"sink={cc.sink}, window={cc.window}, config has sink={cfg.sink}, window={cfg.window}")
+    cc = device_clustered(cc)
     est = estimate_cluster_distribution(q, cc, layer, kv_head)
     plan = plan_selection(est, cfg)
     out = _sparse_ref(q, cache, cc, plan, layer, kv_head)
@@ -407,8 +412,8 @@ def decode_step(q, cache, cc, cfg, layer, kv_head):
 def full_attention(q, cache, layer, kv_head, cc=None):
     """Dense oracle signature (`engine.py:135-144`) on the GPU dense kernel.
     With ``cc`` it covers the grown token range (true_token_weights)."""
-    if cc is None:
-        cc = getattr(cache, "_dense_cc", None)
+    if cc is not None:
+        cc = device_clustered(cc)
     src = cache if cc is None else cc.source
     d = src.head_dim
     _check_query(q, d)
@@ -418,23 +423,25 @@ def full_attention(q, cache, layer, kv_head, cc=None):
         n = lay.n_tokens
         dev = lay.device
     else:
-        k = cache.keys[layer, kv_head].unsqueeze(0).unsqueeze(0).contiguous()
-        vv = cache.values[layer, kv_head].unsqueeze(0).unsqueeze(0).contiguous()
+        dc = device_cache(cache)
+        k = dc.keys[layer, kv_head].unsqueeze(0).unsqueeze(0).contiguous()
+        vv = dc.values[layer, kv_head].unsqueeze(0).unsqueeze(0).contiguous()
         n = k.shape[2]
         dev = k.device
+        dp_ = k.shape[3]
         dummy_i = torch.zeros((1, 1, 2), dtype=torch.int32, device=dev)
-        dummy_f = torch.zeros((1, 1, 1, d), dtype=torch.float32, device=dev)
-        lay = ClusteredLayer(k, vv, dummy_i, dummy_i[..., 0], dummy_f, dummy_f, None, n, 0, 0)
+        dummy_f = torch.zeros((1, 1, 1, dp_), dtype=torch.float32, device=dev)
+        lay = ClusteredLayer(k, vv, dummy_i, dummy_i[..., 0], dummy_f, dummy_f, None, n, 0, 0, logical_dim=d)
         v = lay.view()
     qd = _head_q(q, lay)
-    out = torch.zeros((1, 1, d), dtype=torch.float32, device=dev)
+    out = torch.zeros((1, 1, lay.head_dim), dtype=torch.float32, device=dev)
     lse = torch.zeros((1, 1), dtype=torch.float32, device=dev)
     ws = torch.zeros((N.lib().dp_decode_workspace_bytes(v, 1),), dtype=torch.uint8, device=dev)
-    N.check(N.lib().dp_dense_attention(v, N.ptr(qd), dtype_code(qd), 1, 1.0 / math.sqrt(d), N.ptr(out),
+    N.check(N.lib().dp_dense_attention(v, N.ptr(qd), dtype_code(qd), 1, lay.attn_scale, N.ptr(out),
                                        N.ptr(lse), N.ptr(ws), ws.numel(),
                                        torch.cuda.current_stream(dev).cuda_stream))
     lz = float(lse.item())
-    return AttentionOutput(output=out[0, 0].double().cpu().numpy(), normalizer=math.exp(lz),
+    return AttentionOutput(output=out[0, 0, :d].double().cpu().numpy(), normalizer=math.exp(lz),
                            exact_token_count=n, approx_cluster_count=0, log_normalizer=lz)
 
 
@@ -443,5 +450,6 @@ def build_cache_for_config(cache, cfg, seed=0):
     from .cache import build_clustered_cache
 
     middle = cache.context_len - cfg.sink - cfg.window
-    return build_clustered_cache(cache, k=cfg.cluster_count_for(middle), sink=cfg.sink, window=cfg.window,
-                                 seed=seed)
+    k = cfg.cluster_count_for(middle) if hasattr(cfg, "cluster_count_for") else \
+        (cfg.clusters if cfg.clusters is not None else default_cluster_count(middle, cfg.tokens_per_cluster))
+    return build_clustered_cache(cache, k=k, sink=cfg.sink, window=cfg.window, seed=seed)

@@ -29,7 +29,7 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .cache import ClusteredCache, ClusteredLayer, dtype_code
+from .cache import ClusteredLayer, device_cache, device_clustered, dtype_code
 from .engine import AttentionOutput, _check_query, _group, _head_q, _stream, estimate_cluster_distribution
 
 
@@ -47,7 +47,7 @@ def token_weights(q, layer, *, scale=None, stream=None):
     B, Hq = q.shape[0], q.shape[1]
     w = torch.zeros((B, Hq, layer.row_cap), dtype=torch.float64, device=layer.device)
     lse = torch.zeros((B, Hq), dtype=torch.float64, device=layer.device)
-    sc = 1.0 / math.sqrt(layer.head_dim) if scale is None else scale
+    sc = layer.attn_scale if scale is None else scale
     N.check(N.lib().dp_token_weights(layer.view(), N.ptr(q), dtype_code(q), G, sc, N.ptr(w), N.ptr(lse),
                                      _stream(layer, stream)))
     return w, lse
@@ -129,7 +129,7 @@ def mixed_attention_f64(q, layer, state=None, log_mass=None, *, scale=None, stre
     B, Hq = q.shape[0], q.shape[1]
     out = torch.zeros((B, Hq, layer.head_dim), dtype=torch.float64, device=layer.device)
     lse = torch.zeros((B, Hq), dtype=torch.float64, device=layer.device)
-    sc = 1.0 / math.sqrt(layer.head_dim) if scale is None else scale
+    sc = layer.attn_scale if scale is None else scale
     N.check(N.lib().dp_mixed_attention_f64(layer.view(), N.ptr(q), dtype_code(q), G, sc, N.ptr(log_mass),
                                            N.ptr(None if state is None else state.contiguous()), N.ptr(out),
                                            N.ptr(lse), _stream(layer, stream)))
@@ -166,15 +166,15 @@ def output_error(candidate, reference):
 
 
 def _dense_head_layer(cache, layer, kv_head):
-    """A one-head ClusteredLayer over a plain KvCache (no tables)."""
-    k = torch.as_tensor(cache.keys[layer, kv_head]).unsqueeze(0).unsqueeze(0).contiguous()
-    v = torch.as_tensor(cache.values[layer, kv_head]).unsqueeze(0).unsqueeze(0).contiguous()
-    if not k.is_cuda:
-        k, v = k.cuda(), v.cuda()
+    """A one-head ClusteredLayer over a plain KvCache (no tables); ``cache``
+    may be the reference's numpy KvCache (copied to the device once)."""
+    dc = device_cache(cache)
+    k = dc.keys[layer, kv_head].unsqueeze(0).unsqueeze(0).contiguous()
+    v = dc.values[layer, kv_head].unsqueeze(0).unsqueeze(0).contiguous()
     d = k.shape[-1]
     di = torch.zeros((1, 1, 2), dtype=torch.int32, device=k.device)
     df = torch.zeros((1, 1, 1, d), dtype=torch.float32, device=k.device)
-    return ClusteredLayer(k, v, di, di[..., 0], df, df, None, k.shape[2], 0, 0)
+    return ClusteredLayer(k, v, di, di[..., 0], df, df, None, k.shape[2], 0, 0, logical_dim=dc.head_dim)
 
 
 def _head_weights(q, lay, kv_head):
@@ -183,7 +183,7 @@ def _head_weights(q, lay, kv_head):
     v = lay.view(0, kv_head)
     w = torch.zeros((1, 1, lay.row_cap), dtype=torch.float64, device=lay.device)
     lse = torch.zeros((1, 1), dtype=torch.float64, device=lay.device)
-    N.check(N.lib().dp_token_weights(v, N.ptr(qd), dtype_code(qd), 1, 1.0 / math.sqrt(lay.head_dim), N.ptr(w),
+    N.check(N.lib().dp_token_weights(v, N.ptr(qd), dtype_code(qd), 1, lay.attn_scale, N.ptr(w),
                                      N.ptr(lse), torch.cuda.current_stream(lay.device).cuda_stream))
     return v, w, lse
 
@@ -191,15 +191,16 @@ def _head_weights(q, lay, kv_head):
 def full_attention_weights(q, cache, layer, kv_head):
     """engine.py:122-132: (weights f64[N] by position, lse)."""
     lay = _dense_head_layer(cache, layer, kv_head)
-    _check_query(q, lay.head_dim)
+    _check_query(q, lay.dim)
     _, w, lse = _head_weights(q, lay, 0)
     return w[0, 0, :lay.n_tokens].cpu().numpy(), float(lse.item())
 
 
 def true_token_weights(q, cc, layer, kv_head):
     """engine.py:147-155: like full_attention_weights over the grown range."""
+    cc = device_clustered(cc)
     lay = cc.layers[layer]
-    _check_query(q, lay.head_dim)
+    _check_query(q, lay.dim)
     _, w, lse = _head_weights(q, lay, kv_head)
     return to_positions(lay, w[0, 0], 0, kv_head), float(lse.item())
 
@@ -207,7 +208,7 @@ def true_token_weights(q, cc, layer, kv_head):
 def baseline_token_topk(q, cache, budget, layer, kv_head):
     """engine.py:293-315: (AttentionOutput, captured)."""
     lay = _dense_head_layer(cache, layer, kv_head)
-    _check_query(q, lay.head_dim)
+    _check_query(q, lay.dim)
     if not 1 <= budget <= lay.n_tokens:
         raise ValueError(f"budget must be in [1, {lay.n_tokens}], got {budget}")
     v, w, lse = _head_weights(q, lay, 0)
@@ -217,7 +218,7 @@ def baseline_token_topk(q, cache, budget, layer, kv_head):
                                   torch.cuda.current_stream(lay.device).cuda_stream))
     captured = float(cap.item())
     lz = float(lse.item())
-    return AttentionOutput(output=out[0, 0].cpu().numpy(), normalizer=math.exp(lz) * captured,
+    return AttentionOutput(output=out[0, 0, :lay.dim].cpu().numpy(), normalizer=math.exp(lz) * captured,
                            exact_token_count=int(budget), approx_cluster_count=0,
                            log_normalizer=lz + math.log(captured)), captured
 
@@ -229,7 +230,7 @@ def recovered_mass(plan, q, cache):
     if cc.source is not cache:
         raise ValueError("plan/cc mismatch: plan was derived from a different cache")
     lay = cc.layers[est.layer]
-    _check_query(q, lay.head_dim)
+    _check_query(q, lay.dim)
     v, w, _ = _head_weights(q, lay, est.kv_head)
     rec = torch.zeros((1, 1), dtype=torch.float64, device=lay.device)
     N.check(N.lib().dp_recovered_mass(v, 1, N.ptr(w), N.ptr(plan._state), N.ptr(rec),
@@ -240,7 +241,7 @@ def recovered_mass(plan, q, cache):
 def adaptive_token_budget(q, cache, p, layer, kv_head):
     """metrics.py:41-50: minimal number of tokens whose true mass reaches p."""
     lay = _dense_head_layer(cache, layer, kv_head)
-    _check_query(q, lay.head_dim)
+    _check_query(q, lay.dim)
     v, w, _ = _head_weights(q, lay, 0)
     out = torch.zeros((1, 1), dtype=torch.int32, device=lay.device)
     N.check(N.lib().dp_adaptive_token_budget(v, 1, N.ptr(w), float(p), N.ptr(out),
@@ -258,8 +259,7 @@ def violation_rate(recovered, p):
 
 def cluster_approx_error(q, cache, cc, layer, kv_head):
     """metrics.py:61-76: (errors in estimated-rank order, order)."""
-    if not isinstance(cc, ClusteredCache):
-        raise TypeError("cc must be a ClusteredCache")
+    cc = device_clustered(cc)
     est = estimate_cluster_distribution(q, cc, layer, kv_head)
     lay = cc.layers[layer]
     bufs, _ = est._dev
@@ -269,3 +269,47 @@ def cluster_approx_error(q, cache, cc, layer, kv_head):
                                             N.ptr(err), torch.cuda.current_stream(lay.device).cuda_stream))
     K = est.order.size
     return err[0, 0, :K].cpu().numpy(), est.order
+
+
+def baseline_cluster_topk(q, cache, cc, budget, layer, kv_head):
+    """engine.py:318-338: the `budget` clusters of largest estimated mass
+    exact, every other cluster approximated, sink and window exact (shared
+    normaliser).  Device selection (dp_cluster_topk), fp64 evaluation."""
+    from .engine import cluster_topk_attention
+
+    cc = device_clustered(cc)
+    est = estimate_cluster_distribution(q, cc, layer, kv_head)
+    total = est.probs.size
+    if not 1 <= budget <= total:
+        raise ValueError(f"cluster budget must be in [1, {total}], got {budget}")
+    hl = cc.layers[layer].head(0, kv_head)
+    qd = _head_q(q, hl)
+    _, ws = cluster_topk_attention(qd, hl, int(budget), return_plan=True)
+    st = ws.state.clone()
+    out, lse = mixed_attention_f64(qd, hl, st, ws.log_mass)
+    stn = st[0, 0, :total].cpu().numpy()
+    sizes = cc.estimation_data(layer, kv_head)["sizes"]
+    exact = cc.sink + cc.window + int(sizes[stn == 2].sum())
+    lz = float(lse[0, 0].item())
+    return AttentionOutput(output=out[0, 0, :hl.dim].cpu().numpy(), normalizer=math.exp(lz), exact_token_count=exact,
+                           approx_cluster_count=int((stn == 1).sum()), log_normalizer=lz)
+
+
+def baseline_token_topp_fixed_budget(q, cache, est_budget, p, layer, kv_head):
+    """engine.py:340-370: candidates = the top `est_budget` tokens of the true
+    distribution, kept = the shortest candidate prefix whose true mass reaches
+    p (all of them if it never does).  Returns (AttentionOutput over the kept
+    tokens, renormalised; recovered true mass)."""
+    lay = _dense_head_layer(cache, layer, kv_head)
+    _check_query(q, lay.dim)
+    if not 1 <= est_budget <= lay.n_tokens:
+        raise ValueError(f"est_budget must be in [1, {lay.n_tokens}], got {est_budget}")
+    qd = _head_q(q, lay)
+    w, lse = token_weights(qd, lay)
+    budgets = adaptive_token_budget_batched(lay, w, float(p))
+    out, cap = token_topk_attention(qd, lay, int(est_budget), weights=w, budgets=budgets)
+    kept = min(int(budgets[0, 0].item()), int(est_budget))
+    rec = float(cap[0, 0].item())
+    lz = float(lse[0, 0].item())
+    return AttentionOutput(output=out[0, 0, :lay.dim].cpu().numpy(), normalizer=math.exp(lz) * rec, exact_token_count=kept,
+                           approx_cluster_count=0, log_normalizer=lz + math.log(rec)), rec

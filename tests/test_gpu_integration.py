@@ -1,0 +1,244 @@
+"""The drop-in boundary, exercised with the REAL reference package.
+
+baseline/_ref holds the unmodified reference (tools/install_reference.sh:
+`doublep` 0.1.0 with its Cython kernels, plus its tests/).  These tests bind
+the reference's operator API to the B200 path exactly as INTEGRATION.md §1(a)
+describes (paper_2602_05191_b200.integration.install) and then run
+  * the reference's own tests/test_engine.py, test_metrics.py and
+    test_acceptance.py (unchanged files, through tests/b200_ref_plugin.py), and
+  * the reference CLI's `run` end to end, compared record by record with the
+    same run on the reference's own CPU path.
+Reference objects go in unchanged: numpy KvCache / QueryTrace, the reference
+DoublePConfig, and a ClusteredCache built by the reference's CPU k-means.
+"""
+
+import os
+import subprocess
+import sys
+import xml.etree.ElementTree as ET
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF = os.path.join(ROOT, "baseline", "_ref")
+HAVE_REF = os.path.isdir(os.path.join(REF, "doublep"))
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not HAVE_REF, reason="reference not installed "
+                                                  "(tools/install_reference.sh)")]
+
+# Reference tests whose assertions demand float64 agreement (1e-9 absolute)
+# from arithmetic the B200 path does on an fp32 query (the reference feeds
+# these two tests float64 numpy queries; QueryTrace and the C ABI carry fp32):
+# measured 2.0e-9 (captured mass) and 1.25e-8 (output error).  Everything
+# else in test_engine / test_metrics / test_acceptance passes unchanged.  Both
+# properties are re-asserted below at the north-star fp32 tolerance (1e-5).
+FP64_BOUND = {
+    "test_engine.py::test_decode_after_append_attends_new_tokens",
+    "test_engine.py::test_token_topk_captured_matches_oracle",
+}
+
+
+def _env():
+    env = dict(os.environ)
+    env["PYTHONPATH"] = os.pathsep.join([REF, ROOT, os.path.join(ROOT, "tests")] +
+                                        [p for p in env.get("PYTHONPATH", "").split(os.pathsep) if p])
+    return env
+
+
+def _run_reference_tests(files, tmp_path):
+    xml = tmp_path / "ref.xml"
+    cmd = [sys.executable, "-m", "pytest", "-p", "b200_ref_plugin", "-q", "-p", "no:cacheprovider",
+           f"--junitxml={xml}", "--rootdir", os.path.join(REF, "tests")] + \
+          [os.path.join(REF, "tests", f) for f in files]
+    r = subprocess.run(cmd, cwd=os.path.join(REF, "tests"), env=_env(), capture_output=True, text=True,
+                       timeout=900)
+    res = {}
+    for tc in ET.parse(xml).getroot().iter("testcase"):
+        name = f"{tc.get('classname').split('.')[-1]}.py::{tc.get('name')}"
+        fail = tc.find("failure") if tc.find("failure") is not None else tc.find("error")
+        res[name] = "skipped" if tc.find("skipped") is not None else ("failed" if fail is not None else "passed")
+        if fail is not None:
+            res[name + "#msg"] = (fail.get("message") or "")[:300]
+    return r, res
+
+
+def test_reference_test_suite_on_b200(tmp_path):
+    r, res = _run_reference_tests(["test_engine.py", "test_metrics.py", "test_acceptance.py"], tmp_path)
+    outcomes = {k: v for k, v in res.items() if "#" not in k}
+    assert outcomes, r.stdout[-3000:] + r.stderr[-3000:]
+    passed = sorted(k for k, v in outcomes.items() if v == "passed")
+    failed = sorted(k for k, v in outcomes.items() if v == "failed")
+    print(f"\n[REF-SUITE] {len(passed)} passed, {len(failed)} failed of {len(outcomes)} reference tests on B200")
+    for k in failed:
+        print(f"[REF-SUITE] failed {k}: {res.get(k + '#msg', '')[:200]}")
+    unexpected = [k for k in failed if k not in FP64_BOUND]
+    assert not unexpected, f"reference tests failing beyond fp64-only tolerances: {unexpected}\n" + \
+        "\n".join(res.get(k + "#msg", "") for k in unexpected)
+    assert len(passed) >= len(outcomes) - len(FP64_BOUND)
+
+
+def _ref():
+    if REF not in sys.path:
+        sys.path.insert(0, REF)
+    import doublep
+
+    return doublep
+
+
+class _Bound:
+    def __init__(self):
+        from paper_2602_05191_b200 import integration
+
+        self.pkg = _ref()
+        self._integration = integration
+        self.handle = integration.install(self.pkg)
+
+    def original(self, qualname):
+        """The reference's own function behind a rebound name ("doublep.engine.decode_step")."""
+        return self.handle.original(qualname)
+
+    def cpu_run(self, fn, *a):
+        """fn(*a) with the reference unbound (its own CPU path), then rebind."""
+        self.handle.uninstall()
+        try:
+            return fn(*a)
+        finally:
+            self.handle = self._integration.install(self.pkg)
+
+
+@pytest.fixture
+def bound():
+    b = _Bound()
+    yield b
+    b.handle.uninstall()
+
+
+def _make_cache(doublep, n, d, seed, layers=1, kv_heads=1):  # tests/conftest.py:7-15 of the reference
+    rng = np.random.default_rng(seed)
+    return doublep.KvCache(keys=rng.normal(size=(layers, kv_heads, n, d)),
+                           values=rng.normal(size=(layers, kv_heads, n, d)))
+
+
+def test_fp64_bound_semantics_at_north_star_tolerance(bound):
+    """The FP64_BOUND reference tests' properties at the fp32 tolerance."""
+    import math
+
+    doublep = bound.pkg
+    from doublep import engine, metrics
+
+    # exact collapse (test_engine.py:128-136): p1 = p2 = 1 over singleton clusters == dense
+    cache = _make_cache(doublep, 48, 16, 5)
+    cc = doublep.build_clustered_cache(cache, k=48 - 6, sink=2, window=4, seed=0)
+    cfg = engine.DoublePConfig(p1=1.0, p2=1.0, sink=2, window=4)
+    q = np.random.default_rng(6).normal(size=16)
+    out, plan, _ = engine.decode_step(q, cache, cc, cfg, 0, 0)
+    ref = engine.full_attention(q, cache, 0, 0)
+    assert metrics.output_error(out, ref) <= 1e-5
+    assert out.normalizer == pytest.approx(ref.normalizer, rel=1e-5)
+    # logits 0 and 2 in one cluster: estimate 2e, exact 1 + e^2 (test_engine.py:113-125)
+    cache2 = doublep.KvCache(keys=np.array([[0.0], [2.0]]).reshape(1, 1, 2, 1), values=np.ones((1, 1, 2, 1)))
+    cc2 = doublep.build_clustered_cache(cache2, k=1, sink=0, window=0, seed=0)
+    est = engine.estimate_cluster_distribution(np.ones(1), cc2, 0, 0)
+    approx = math.exp(est.log_masses[0])
+    assert approx == pytest.approx(2.0 * math.e, rel=1e-6)
+    assert approx < math.exp(0.0) + math.exp(2.0)
+    # growth (test_engine.py:274-291): exact over everything == dense over the grown range
+    cache3 = _make_cache(doublep, 64, 32, 28)
+    cc3 = doublep.build_clustered_cache(cache3, k=4, sink=2, window=8, seed=0)
+    rng = np.random.default_rng(29)
+    for _ in range(3):
+        cc3.append_tokens(rng.normal(size=(1, 1, 32)).astype(np.float32),
+                          rng.normal(size=(1, 1, 32)).astype(np.float32))
+    q3 = rng.normal(size=32)
+    out3, plan3, _ = engine.decode_step(q3, cache3, cc3, engine.DoublePConfig(p1=1.0, p2=1.0, sink=2, window=8),
+                                        0, 0)
+    assert plan3.exact_tokens.size == cc3.total_tokens == 67
+    w, _ = engine.true_token_weights(q3, cc3, 0, 0)
+    oracle = w @ cc3.gather_values(0, 0, np.arange(67)).astype(np.float64)
+    assert metrics.output_error(out3.output, oracle) <= 1e-5
+    # captured mass of token top-k == the oracle's top-k weight sum (test_engine.py:210-216)
+    kk = np.asarray(cache.keys[0, 0], np.float64)
+    lg = kk @ q / math.sqrt(16)
+    w = np.exp(lg - lg.max())
+    w /= w.sum()
+    for k in (1, 5, 20):
+        _, cap_k = engine.baseline_token_topk(q, cache, k, 0, 0)
+        assert cap_k == pytest.approx(np.sort(w)[::-1][:k].sum(), abs=1e-7)
+    # token top-k with the full budget is dense (test_engine.py:191-197)
+    out4, captured = engine.baseline_token_topk(q, cache, 48, 0, 0)
+    assert captured == pytest.approx(1.0, abs=1e-9)
+    np.testing.assert_allclose(out4.output, ref.output, atol=1e-5)
+
+
+def _records_equal(a, b, tol_err=2e-4):
+    """Integer columns identical; float columns within the fp32-table tolerance."""
+    assert len(a) == len(b)
+    worst = 0.0
+    for ra, rb in zip(a, b):
+        for col in ("layer", "head", "step", "method", "p1", "p2", "k", "m", "B", "clusters_total"):
+            assert getattr(ra, col) == getattr(rb, col), (col, ra, rb)
+        for col in ("recovered_mass", "est_mass"):
+            x, y = getattr(ra, col), getattr(rb, col)
+            assert (x is None) == (y is None)
+            if x is not None:
+                assert abs(x - y) <= 1e-5, (col, ra, rb)
+        worst = max(worst, abs(ra.rel_err - rb.rel_err))
+    assert worst <= tol_err, worst
+    return worst
+
+
+def test_reference_cli_run_end_to_end(bound):
+    """doublep.cli.run (cli.py:93-124) on the B200 path vs the same run on the
+    reference's CPU path: every record's selection counts and exact tokens
+    identical, masses within 1e-5, errors within 2e-4."""
+    from doublep import cli
+    from doublep.workload import WorkloadSpec
+
+    spec = WorkloadSpec(context_len=2048, head_dim=64, num_kv_heads=2, gqa_group=4, num_layers=1, num_steps=2,
+                        tail_profile="peaked", seed=0)
+    worst = {}
+    for method, extra in (("doublep", {}), ("token_topk", {"k": 128}), ("cluster_topk", {"m": 8}),
+                          ("token_topp_fixed", {"B": 256}), ("full", {})):
+        cfgr = cli.RunConfig(workload=spec, input_path=None, method=method, **extra)
+        gpu = cli.run(cfgr)
+        cpu = bound.cpu_run(cli.run, cfgr)
+        mism = [(g, c) for g, c in zip(gpu, cpu) if (g.clusters_selected, g.clusters_exact, g.exact_tokens) !=
+                (c.clusters_selected, c.clusters_exact, c.exact_tokens)]
+        # selection counts may differ only at a score tie (fp32 centroid tables): none at this seed
+        assert not mism, mism[:3]
+        worst[method] = _records_equal(gpu, cpu)
+    print("\n[REF-CLI] worst |rel_err(gpu) - rel_err(cpu)| per method:", {k: f"{v:.2e}" for k, v in worst.items()})
+
+
+def test_reference_clustered_cache_and_trace_accepted(bound):
+    """A ClusteredCache built by the reference's CPU k-means, its QueryTrace
+    and DoublePConfig drive the B200 decode directly (uploaded once); the
+    outputs match the reference's own decode_step on the same clusters."""
+    from doublep import engine, metrics
+    from doublep.workload import WorkloadSpec, generate
+
+    import paper_2602_05191_b200 as P
+
+    spec = WorkloadSpec(context_len=1024, head_dim=32, num_kv_heads=2, gqa_group=2, num_layers=1, num_steps=1,
+                        tail_profile="mixed", seed=3)
+    cache, trace = generate(spec)
+    ref_build = bound.original("doublep.clustering.build_clustered_cache")
+    ref_decode = bound.original("doublep.engine.decode_step")
+    cc = ref_build(cache, sink=4, window=64, seed=0)  # CPU k-means, reference object
+    cfg = engine.DoublePConfig(p1=0.95, p2=0.7)
+    worst = 0.0
+    for hq in range(trace.num_query_heads):
+        q = trace.query(0, 0, hq)
+        h = trace.kv_head_for(hq)
+        out_g, plan_g, _ = engine.decode_step(q, cache, cc, cfg, 0, h)     # B200 on reference clusters
+        out_c, plan_c, _ = ref_decode(q, cache, cc, cfg, 0, h)             # reference CPU
+        assert np.array_equal(plan_g.exact_clusters, plan_c.exact_clusters)
+        assert np.array_equal(plan_g.exact_tokens, plan_c.exact_tokens)
+        worst = max(worst, metrics.output_error(out_g, out_c))
+    assert worst <= 1e-5, worst
+    # our QueryTrace mirror reads the same trace
+    qt = P.QueryTrace(queries=trace.queries, gqa_group=trace.gqa_group)
+    assert qt.kv_head_for(5) == trace.kv_head_for(5)
+    np.testing.assert_array_equal(qt.query(0, 0, 3), trace.query(0, 0, 3))
+    assert tuple(qt.step_queries(0, 0).shape) == (1, trace.num_query_heads, trace.head_dim)
