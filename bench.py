@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--no-fi-dense", action="store_true", help="skip the flashinfer trtllm-gen dense comparator")
+    ap.add_argument("--mixed-layers", type=int, default=8,
+                    help="layers of the 'mixed' stress-profile line at the headline context (0: off)")
     ap.add_argument("--cpu-sample-heads", type=int, default=2)
     ap.add_argument("--long-context", type=int, default=131072,
                     help="secondary workload context (0: off); reported under long_context")
@@ -166,78 +169,181 @@ def barrier(world):
 
 
 # ---------------------------------------------------------------------------
-# CPU reference (the oracle port of doublep.decode_step) -- baseline only
+# CPU reference: the UNMODIFIED reference package (doublep 0.1.0, installed at
+# baseline/_ref by tools/install_reference.sh) timed on the host cores -- a
+# reported baseline only.  Each backend configuration runs in its own process
+# (the backend is chosen at import, kernels.py:17-29; BLAS threads at load).
 # ---------------------------------------------------------------------------
-def oracle_head_from_layer(layer, h):
-    """Position-ordered keys/values + tables of one head of a GPU-built layer."""
-    from oracle import doublep_oracle as O
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+_REF_WORKER = r"""
+import json, pickle, sys, time
+sys.path.insert(0, sys.argv[1])
+import doublep
+from doublep import engine
+with open(sys.argv[2], "rb") as f:
+    job = pickle.load(f)
+cache, cc, calls = job["cache"], job["cc"], job["calls"]
+cfg = engine.DoublePConfig(job["p1"], job["p2"], sink=cc.sink, window=cc.window)
+try:
+    from threadpoolctl import threadpool_info
+    blas = [[i.get("internal_api"), i.get("num_threads")] for i in threadpool_info() if i.get("user_api") == "blas"]
+except Exception:
+    blas = None
+for layer, kv, q in calls[: min(4, len(calls))]:  # warm-up (first-call allocations, caches)
+    engine.decode_step(q, cache, cc, cfg, layer, kv)
+times = []
+for rep in range(job["reps"]):
+    for layer, kv, q in calls:
+        t0 = time.perf_counter()
+        engine.decode_step(q, cache, cc, cfg, layer, kv)
+        times.append(time.perf_counter() - t0)
+print(json.dumps({"backend": doublep.BACKEND, "blas": blas, "times": times}))
+"""
+
+# (label, DOUBLEP_KERNELS, BLAS threads: None = all cores)
+REF_CONFIGS = (("cython", "cython", None), ("numpy-blas1", "python", 1), ("numpy-blasN", "python", None))
+
+
+def ref_available():
+    return os.path.isdir(os.path.join(REF_DIR, "doublep"))
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def ref_decode_times(cache, cc, calls, p1, p2, reps, configs=REF_CONFIGS):
+    """Per-call seconds of the reference's decode_step (engine.py:267-278) for
+    each backend configuration: {label: {"times": [...], "backend", "blas", "threads"}}."""
+    import pickle
+    import subprocess
+    import tempfile
+
+    with tempfile.NamedTemporaryFile(suffix=".pkl", delete=False) as f:
+        pickle.dump({"cache": cache, "cc": cc, "calls": calls, "p1": p1, "p2": p2, "reps": reps}, f)
+        job = f.name
+    out = {}
+    try:
+        for label, kern, thr in configs:
+            n = str(thr if thr is not None else os.cpu_count())
+            env = dict(os.environ, DOUBLEP_KERNELS=kern, OPENBLAS_NUM_THREADS=n, OMP_NUM_THREADS=n,
+                       MKL_NUM_THREADS=n)
+            r = subprocess.run([sys.executable, "-c", _REF_WORKER, REF_DIR, job], env=env, capture_output=True,
+                               text=True, timeout=1800)
+            if r.returncode != 0:
+                out[label] = {"error": r.stderr.strip().splitlines()[-1:] or ["failed"]}
+                continue
+            res = json.loads(r.stdout.strip().splitlines()[-1])
+            res["threads"] = 1 if kern == "cython" else int(n)  # the Cython kernels never release the GIL
+            out[label] = res
+    finally:
+        os.unlink(job)
+    return out
+
+
+def _ref_import():
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    import doublep
+
+    return doublep
+
+
+def ref_cache_from_layer(layer, heads):
+    """The reference's KvCache + ClusteredCache (kvcache.py:50, clustering.py:140)
+    for kv heads `heads` of a GPU-built single-sequence layer: position-ordered
+    f32 keys/values and the device clusters as reference Cluster objects."""
+    doublep = _ref_import()
+    from doublep.clustering import Cluster, ClusteredCache
 
     n = layer.n_tokens
-    rows_k = layer.keys[0, h, :n].float().cpu().numpy()
-    rows_v = layer.values[0, h, :n].float().cpu().numpy()
-    perm = layer.perm[0, h, :n].cpu().numpy()
-    kp = np.empty_like(rows_k)
-    vp = np.empty_like(rows_v)
-    kp[perm] = rows_k
-    vp[perm] = rows_v
-    t = layer.head_tables(0, h)
-    return kp, vp, O.HeadTables(members=t["members"], centroids=t["centroids"], value_means=t["value_means"])
+    ks, vs, cls = [], [], []
+    for h in heads:
+        rows_k = layer.keys[0, h, :n].float().cpu().numpy()
+        rows_v = layer.values[0, h, :n].float().cpu().numpy()
+        perm = layer.perm[0, h, :n].cpu().numpy()
+        kp = np.empty_like(rows_k)
+        vp = np.empty_like(rows_v)
+        kp[perm] = rows_k
+        vp[perm] = rows_v
+        ks.append(kp)
+        vs.append(vp)
+        t = layer.head_tables(0, h)
+        cls.append([Cluster(members=np.asarray(m, np.int64), centroid=c, size=int(len(m)),
+                            value_sum=vm * len(m), value_mean=vm)
+                    for m, c, vm in zip(t["members"], t["centroids"], t["value_means"])])
+    cache = doublep.KvCache(keys=np.stack(ks)[None], values=np.stack(vs)[None])
+    cc = ClusteredCache(source=cache, sink=layer.sink, window=layer.window, clusters=[cls])
+    return cache, cc
 
 
-def cpu_decode_sample(heads, queries_for_head, a, steps):
-    """Time oracle.decode_step per (q head, step); returns per-call seconds."""
-    from oracle import doublep_oracle as O
-
-    times = []
-    for (kp, vp, tab), qs in zip(heads, queries_for_head):
-        for s in range(steps):
-            for g in range(qs.shape[1]):
-                q = qs[s % qs.shape[0], g].astype(np.float64)
-                t0 = time.perf_counter()
-                O.decode_step(q, kp, vp, tab, a.p1, a.p2, 4, 64)
-                times.append(time.perf_counter() - t0)
-    return times
+def summarize_ref(res, scale_up):
+    """Pick the fastest configuration; per-step us = median per call x scale_up."""
+    rows = {}
+    for label, r in res.items():
+        if "times" in r:
+            med = float(statistics.median(r["times"]))
+            rows[label] = {"ms_per_call": med * 1e3, "us_per_step": med * scale_up * 1e6, "calls": len(r["times"]),
+                           "backend": r["backend"], "blas": r["blas"], "threads": r["threads"]}
+        else:
+            rows[label] = r
+    ok = {k: v for k, v in rows.items() if "us_per_step" in v}
+    best = min(ok, key=lambda k: ok[k]["us_per_step"]) if ok else None
+    return best, rows
 
 
 def run_reference(a):
-    """--impl reference: the reference algorithm (oracle port of doublep
-    0.1.0's NumPy path) on the host cores, same metric/config, bounded
-    sample: one KV head of one layer (host-generated with the reference law,
-    clustered with the reference k-means), G q heads per step, extrapolated
-    to all heads and layers."""
+    """--impl reference: the unmodified reference's decode_step (doublep 0.1.0,
+    baseline/_ref) on the host cores, same metric and config, on a bounded
+    sample: one kv head of layer 0 generated by the reference's generator
+    (workload.py:154-194) and clustered by the reference's own
+    build_clustered_cache (NumPy backend, all cores; not timed), then every
+    step times decode_step for that head's G q heads under each backend
+    configuration; value = the fastest configuration's median per-call time
+    x (kv heads x layers x batch x G)."""
     world, rank, _ = dist_setup()
     if rank != 0:
         return
-    from oracle import doublep_oracle as O
+    if not ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "baseline/_ref missing (tools/install_reference.sh)"}))
+        return
+    os.environ["DOUBLEP_KERNELS"] = "python"  # prefill k-means in this process: NumPy (Cython is ~4x slower)
+    doublep = _ref_import()
+    from doublep.workload import WorkloadSpec, generate
 
     n, d, G = a.context, a.head_dim, a.gqa
-    spec = O.WorkloadSpec(context_len=n, head_dim=d, num_kv_heads=1, gqa_group=G, num_steps=max(a.qsteps, 1),
-                          tail_profile=a.profile, seed=0)
+    spec = WorkloadSpec(context_len=n, head_dim=d, num_kv_heads=1, gqa_group=G, num_layers=1,
+                        num_steps=max(a.qsteps, 1), tail_profile=a.profile, seed=0)
     t0 = time.perf_counter()
-    keys, values, centers = O.generate_head(spec, 0, 0)
-    qs = np.stack([O.generate_queries(spec, 0, g, centers) for g in range(G)], axis=1)  # [S, G, d]
-    k = O.clamp_k(n, 4, 64)
-    tables, _ = O.build_head_tables(keys, values, k, 4, 64, seed_for_head=O.head_seed(0, 0, 0))
+    cache, trace = generate(spec)
+    cc = doublep.build_clustered_cache(cache, sink=4, window=64, seed=0)
     prefill = time.perf_counter() - t0
-    scale_up = a.kv_heads * a.layers * a.batch  # (q-head group steps) per full decode step
-    per_step = []
-    for s in range(a.warmup + a.steps):
-        t0 = time.perf_counter()
-        for g in range(G):
-            O.decode_step(qs[s % qs.shape[0], g].astype(np.float64), keys, values, tables, a.p1, a.p2, 4, 64)
-        dt = time.perf_counter() - t0
-        if s >= a.warmup:
-            per_step.append(dt * scale_up * 1e6)
-    val = float(statistics.median(per_step))
+    steps = a.warmup + a.steps
+    calls = [(0, 0, trace.query(s % trace.num_steps, 0, g)) for s in range(steps) for g in range(G)]
+    res = ref_decode_times(cache, cc, calls, a.p1, a.p2, reps=1)
+    scale_up = a.kv_heads * a.layers * a.batch * G
+    best, rows = summarize_ref(res, scale_up)
+    val = rows[best]["us_per_step"] if best else None
     line = {
         "impl": "reference", "metric": "decode_us_per_step", "value": val, "unit": "us/step",
-        "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": val / 1e3,
+        "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": None if val is None else val / 1e3,
         "higher_is_better": False, "scaling": "strong" if a.gpus > 1 else "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic (reference generator law, host)", "config": workload_config(a, 1),
-        "cpu_baseline": {"value": val, "unit": "us/step", "cores": os.cpu_count(), "kind": "port",
-                         "sample": f"1 layer x 1 kv head x {G} q heads per step at N={n}, extrapolated "
-                                   f"x{scale_up} (kv heads x layers x batch); oracle port of doublep "
-                                   f"0.1.0 NumPy path; prefill clustering {prefill:.1f}s not timed"},
+        "dtype": "f64", "data": "synthetic (the reference's own generator, host)", "config": workload_config(a, 1),
+        "cpu_baseline": {"value": val, "unit": "us/step", "cores": None if best is None else rows[best]["threads"],
+                         "kind": "reference", "cpu_model": cpu_model(), "host_cores": os.cpu_count(),
+                         "backend": best, "configs": rows,
+                         "sample": f"doublep 0.1.0 decode_step (unmodified, baseline/_ref) for 1 kv head x {G} q "
+                                   f"heads per step at N={n}, {a.warmup}+{a.steps} steps per backend configuration; "
+                                   f"median per call x{scale_up} (q heads x layers x batch), labelled extrapolation; "
+                                   f"clusters from the reference's build_clustered_cache ({prefill:.1f}s, not timed)"},
         "e2e": {"value": val, "unit": "us/step", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -246,7 +352,38 @@ def run_reference(a):
 # ---------------------------------------------------------------------------
 # the B200 arm
 # ---------------------------------------------------------------------------
-def _measure(a, context, L, dev, world, rank, sampler=None):
+def _fi_dense(a, layers, qdev, scale, B, hl, G, d, context):
+    """The fastest installed dense decode kernel: flashinfer's trtllm-gen
+    `trtllm_batch_decode_with_kv_cache` (Blackwell fmhaSm100a cubins; library
+    code) over a strided 64-row page view of the same caches (row order does
+    not matter to dense attention).  Returns fn(li, s) for graph capture."""
+    import torch
+    from flashinfer.decode import trtllm_batch_decode_with_kv_cache
+
+    P = 64
+    rc = layers[0].row_cap
+    if context % P or rc % P:
+        raise ValueError("context not a multiple of the page size")
+    dev = layers[0].device
+    ws = torch.zeros(256 << 20, dtype=torch.uint8, device=dev)
+    bt = (torch.arange(B, device=dev)[:, None] * (hl * rc // P) +
+          torch.arange(context // P, device=dev)[None]).to(torch.int32)
+    sl = torch.full((B,), context, dtype=torch.int32, device=dev)
+    npg = B * hl * rc // P - (hl - 1) * rc // P
+
+    def pages(t):
+        return torch.as_strided(t, (npg, hl, P, d), (P * d, rc * d, d, 1))
+
+    kv = [(pages(lay.keys), pages(lay.values)) for lay in layers]
+
+    def fn(li, s):
+        q = qdev[li][s % a.qsteps]
+        return trtllm_batch_decode_with_kv_cache(q, kv[li], ws, bt, sl, context, bmm1_scale=scale)
+
+    return fn
+
+
+def _measure(a, context, L, dev, world, rank, sampler=None, profile=None, with_dense=True):
     """Build L synthetic layers at `context` (GPU k-means prefill, not timed)
     and time CUDA graphs of the full sparse decode step (plan + attend per
     layer) and of the dense comparator over the same caches."""
@@ -272,7 +409,7 @@ def _measure(a, context, L, dev, world, rank, sampler=None):
         ks[li * B:(li + 1) * B] = k[:, h0:h0 + hl]
         vs[li * B:(li + 1) * B] = v[:, h0:h0 + hl]
         del k, v
-        q = generate_queries(centers[:, h0:h0 + hl], G, a.qsteps, profile=a.profile, layer=li)
+        q = generate_queries(centers[:, h0:h0 + hl], G, a.qsteps, profile=profile or a.profile, layer=li)
         qdev.append(torch.from_numpy(q).to(dev).to(torch.bfloat16))  # [S,B,Hq,d]
     torch.cuda.synchronize(dev)
     gen_s = time.perf_counter() - t0
@@ -426,12 +563,27 @@ def _measure(a, context, L, dev, world, rank, sampler=None):
     attend_graph_bytes = float((((stats_np[0, :, :, :, 0] * 2 * d * s_kv + stats_np[0, :, :, :, 1] * d * 4)
                                  .sum(axis=(1, 2))) + qo).mean())
     del agraphs, wsl
-    dense_ms = None
-    if not a.no_dense:
+    dense_ms = fi_ms = None
+    fi_note = "skipped"
+    if not a.no_dense and with_dense:
         dgraphs = capture(dense_step)
         dense_ms = max_over_ranks(timed(dgraphs, a.steps, a.warmup), world, dev)
         del dgraphs
-    return dict(layers=layers, wss=wss, qdev=qdev, ms=ms, dense_ms=dense_ms, stage_ms=stage_ms,
+        if not a.no_fi_dense:
+            try:
+                fi = _fi_dense(a, layers, qdev, scale, B, hl, G, d, context)
+                dense_step(0, 0)
+                ref = wss[0].out.clone()
+                chk = fi(0, 0).float()
+                rel = float((chk - ref).norm() / ref.norm())
+                fgraphs = capture(lambda li, s: fi(li, s))
+                fi_ms = max_over_ranks(timed(fgraphs, a.steps, a.warmup), world, dev)
+                del fgraphs
+                fi_note = f"rel-L2 vs dp_dense_attention on layer 0: {rel:.1e}"
+            except Exception as e:  # library comparator only; never the product path
+                fi_note = f"unavailable: {repr(e)[:160]}"
+    return dict(layers=layers, wss=wss, qdev=qdev, ms=ms, dense_ms=dense_ms, fi_ms=fi_ms, fi_note=fi_note,
+                stage_ms=stage_ms,
                 dense_kernel_ms=dense_kernel_ms, attend_bytes=attend_bytes, step_bytes=step_bytes,
                 dense_bytes=dense_bytes, union_frac=float(U.mean() / context), prefill_s=prefill_s, gen_s=gen_s,
                 hl=hl, Hq_l=Hq_l, attend_graph_ms=attend_graph_ms, attend_graph_bytes=attend_graph_bytes)
@@ -515,26 +667,49 @@ def run_b200(a):
                "eager_us_per_step": eager_ms * 1e3,
                "eager_path": "paper_2602_05191_b200.sparse_attention per layer, eager, same copies"}
 
-    # ---- CPU baseline (rank 0, N=1 only) ---------------------------------
+    # ---- CPU baseline (rank 0, N=1 only): the reference's own decode_step --
     cpu = None
-    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+    if rank == 0 and world == 1 and not a.no_cpu_baseline and ref_available():
         nh = min(a.cpu_sample_heads, hl)
-        heads = [oracle_head_from_layer(layers[0], h) for h in range(nh)]
-        qsets = [qdev[0][:, 0, h * G:(h + 1) * G].float().cpu().numpy() for h in range(nh)]
-        times = cpu_decode_sample(heads, qsets, a, steps=2)
-        per_call = statistics.median(times)
-        cpu_us = per_call * a.kv_heads * G * L * B * 1e6
-        cpu = {"value": cpu_us, "unit": "us/step", "cores": os.cpu_count(), "kind": "port",
-               "sample": f"layer 0, {nh} kv heads x {G} q heads x 2 steps of the same cache (GPU-built "
-                         f"clusters), oracle decode_step median {per_call * 1e3:.2f} ms per q-head-step, "
-                         f"extrapolated x{a.kv_heads * G * L * B} (all q heads, layers, batch); NumPy/"
-                         f"OpenBLAS threads = cores"}
+        rcache, rcc = ref_cache_from_layer(layers[0], range(nh))
+        qs = qdev[0][:4, 0].float().cpu().numpy()  # [4 steps, Hq, d]
+        calls = [(0, h, qs[s, h * G + g]) for s in range(qs.shape[0]) for h in range(nh) for g in range(G)]
+        res_ref = ref_decode_times(rcache, rcc, calls, a.p1, a.p2, reps=1,
+                                   configs=(REF_CONFIGS[0], REF_CONFIGS[2]))
+        scale_up = a.kv_heads * G * L * B
+        best, rows = summarize_ref(res_ref, scale_up)
+        if best is not None:
+            cpu = {"value": rows[best]["us_per_step"], "unit": "us/step", "cores": rows[best]["threads"],
+                   "kind": "reference", "cpu_model": cpu_model(), "host_cores": os.cpu_count(), "backend": best,
+                   "configs": rows,
+                   "sample": f"doublep 0.1.0 decode_step (unmodified, baseline/_ref) on layer 0, {nh} kv heads x "
+                             f"{G} q heads x 4 query steps of the GPU-built clusters (as reference Cluster objects); "
+                             f"median {rows[best]['ms_per_call']:.2f} ms per q-head-step, labelled extrapolation "
+                             f"x{scale_up} (all q heads, layers, batch)"}
+
+    fi_ms, fi_note = res["fi_ms"], res["fi_note"]
+    # ---- the 'mixed' stress profile (workload.py:83-89) at the same context --
+    mixed = None
+    del layers, wss, qdev, res
+    torch.cuda.empty_cache()
+    if a.mixed_layers and a.profile != "mixed":
+        rm = _measure(a, a.context, a.mixed_layers, dev, world, rank, profile="mixed")
+        mixed = {"profile": "mixed", "context": a.context, "layers_timed": a.mixed_layers,
+                 "us_per_layer": rm["ms"] * 1e3 / a.mixed_layers,
+                 "us_per_step_32_layers": rm["ms"] * 1e3 / a.mixed_layers * 32,
+                 "dense_us_per_layer": None if rm["dense_ms"] is None else rm["dense_ms"] * 1e3 / a.mixed_layers,
+                 "fi_dense_us_per_layer": None if rm["fi_ms"] is None else rm["fi_ms"] * 1e3 / a.mixed_layers,
+                 "union_exact_rows_frac": rm["union_frac"],
+                 "stage_us_per_layer": {"plan": rm["stage_ms"][0] * 1e3, "attend": rm["stage_ms"][1] * 1e3},
+                 "attend_gbs": float(rm["attend_bytes"].mean() / (rm["stage_ms"][1] * 1e-3) / 1e9)}
+        dm = [x for x in (rm["dense_ms"], rm["fi_ms"]) if x is not None]
+        mixed["speedup_vs_fastest_dense"] = min(dm) / rm["ms"] if dm else None
+        del rm
+        torch.cuda.empty_cache()
 
     # ---- secondary workload: the same step at 128K context (fewer layers) --
     long_ctx = None
     if a.long_context and a.long_context != a.context:
-        del layers, wss, qdev, res
-        torch.cuda.empty_cache()
         r2 = _measure(a, a.long_context, a.long_layers, dev, world, rank)
         a_ms = r2["stage_ms"][1]
         long_ctx = {
@@ -542,7 +717,10 @@ def run_b200(a):
             "us_per_layer": r2["ms"] * 1e3 / a.long_layers,
             "us_per_step_32_layers": r2["ms"] * 1e3 / a.long_layers * 32,
             "dense_us_per_layer": None if r2["dense_ms"] is None else r2["dense_ms"] * 1e3 / a.long_layers,
-            "speedup_vs_dense": None if r2["dense_ms"] is None else r2["dense_ms"] / r2["ms"],
+            "fi_dense_us_per_layer": None if r2["fi_ms"] is None else r2["fi_ms"] * 1e3 / a.long_layers,
+            "speedup_vs_dense": None if r2["dense_ms"] is None else
+            min(x for x in (r2["dense_ms"], r2["fi_ms"]) if x is not None) / r2["ms"],
+            "speedup_vs": "the fastest of dp_dense_attention and flashinfer trtllm-gen",
             "stage_us_per_layer": {"plan": r2["stage_ms"][0] * 1e3, "attend": a_ms * 1e3},
             "attend_algorithmic_bytes": float(r2["attend_bytes"].mean()),
             "attend_gbs": float(r2["attend_bytes"].mean() / (a_ms * 1e-3) / 1e9),
@@ -577,7 +755,7 @@ def run_b200(a):
             "data": "synthetic (reference blob law on device, Philox); random-init caches, no checkpoint",
             "config": workload_config(a, world),
             "roofline": {"bound": "hbm", "achieved": attend_gbs, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": attend_gbs / hbm_peak, "traffic": traffic,
+                         "frac": attend_gbs / hbm_peak, "frac_vs_8tbs": attend_gbs / 8000.0, "traffic": traffic,
                          "traffic_source": "profiles/traffic.json (ncu --set full, dram read+write per launch)",
                          "kernel": "dp_attend = attn_tc_kernel (gathered split-KV attention + fused LSE merge), one launch per layer",
                          "peak_source": peak_src,
@@ -597,15 +775,23 @@ def run_b200(a):
             "step_algorithmic_bytes": step_bytes,
             "step_roofline_frac": step_bytes / (ms * 1e-3) / 1e9 / hbm_peak,
             "union_exact_rows_frac": union_frac,
-            "dense_us_per_step": None if dense_ms is None else dense_ms * 1e3,
+            "dense_us_per_step": None if dense_ms is None else min(x for x in (dense_ms, fi_ms) if x is not None) * 1e3,
+            "dense_comparators_us_per_step": {
+                "dp_dense_attention": None if dense_ms is None else dense_ms * 1e3,
+                "flashinfer_trtllm_gen": None if fi_ms is None else fi_ms * 1e3,
+                "flashinfer_note": fi_note},
             "dense_roofline_frac": None if dense_ms is None else dense_bytes / (dense_ms * 1e-3) / 1e9 / hbm_peak,
-            "speedup_vs_dense": None if dense_ms is None else dense_ms / ms,
+            "speedup_vs_dense": None if dense_ms is None else min(x for x in (dense_ms, fi_ms) if x is not None) / ms,
+            "speedup_vs": "the fastest dense kernel measured in this run (dp_dense_attention, flashinfer trtllm-gen)",
+            "mixed_profile": mixed,
             "prefill_s": prefill_s, "generate_s": gen_s,
             "long_context": long_ctx,
         }
+        line["attend_in_graph"]["frac_vs_8tbs"] = line["attend_in_graph"]["gbs"] / 8000.0
         if long_ctx is not None:
             long_ctx["attend_roofline_frac"] = long_ctx["attend_gbs"] / hbm_peak
             long_ctx["attend_in_graph"]["frac"] = long_ctx["attend_in_graph"]["gbs"] / hbm_peak
+            long_ctx["attend_in_graph"]["frac_vs_8tbs"] = long_ctx["attend_in_graph"]["gbs"] / 8000.0
             long_ctx["dense_kernel_roofline_frac"] = long_ctx["dense_kernel_gbs"] / hbm_peak
         print(json.dumps(line), flush=True)
 
