@@ -58,6 +58,7 @@ constexpr int kMaxCL = 16;
 // dp_debug_plan_timing() -- profiling aid only
 __device__ unsigned long long g_plan_ts[16][24];
 __device__ unsigned long long g_plan_clk[16][2];
+__device__ unsigned long long g_plan_cyc[16][24];
 // (compiled in only with -DDP_PROFILE: DP_PROFILE=1 python -m paper_2602_05191_b200.build)
 __device__ __forceinline__ void stamp(int r, int ev) {
 #ifdef DP_PROFILE
@@ -65,6 +66,7 @@ __device__ __forceinline__ void stamp(int r, int ev) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     g_plan_ts[r][ev] = t;
+    g_plan_cyc[r][ev] = clock64();  // SM cycles: phase durations within one CTA
     if (ev == 0 || ev == 9) g_plan_clk[r][ev == 9] = clock64();
   }
 #endif
@@ -766,6 +768,9 @@ int plan_cluster_size(const dp_cache_view& v, int G) { return pick_cl(v, G); }
 extern "C" int dp_debug_plan_clock(unsigned long long* out) {
   return cudaMemcpyFromSymbol(out, dp::g_plan_clk, sizeof(dp::g_plan_clk)) == cudaSuccess ? 0 : 2;  // [16][2]
 }
+extern "C" int dp_debug_plan_cycles(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, dp::g_plan_cyc, sizeof(dp::g_plan_cyc)) == cudaSuccess ? 0 : 2;  // [16][24]
+}
 extern "C" int dp_debug_plan_timing(unsigned long long* out) {
   return cudaMemcpyFromSymbol(out, dp::g_plan_ts, sizeof(dp::g_plan_ts)) == cudaSuccess ? 0 : 2;  // [16][24]
 }
@@ -780,4 +785,7 @@ int plan_occupancy(const dp_cache_view& v, int G, int cl) {
 extern "C" int dp_debug_plan_occupancy(const dp_cache_view* v, int G, int cl) {
   if (cl == 0) return dp::plan_cluster_size(*v, G);  // the size launch_plan picks
   return dp::plan_occupancy(*v, G, cl);
+}
+extern "C" int dp_debug_sel_cycles(unsigned long long* out) {  // [16][8] select phase cycles (plan.cu's copy)
+  return cudaMemcpyFromSymbol(out, dp::g_sel_ts, sizeof(dp::g_sel_ts)) == cudaSuccess ? 0 : 2;
 }

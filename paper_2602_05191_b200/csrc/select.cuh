@@ -27,9 +27,7 @@ static __device__ unsigned long long g_sel_ts[16][8];
 __device__ __forceinline__ void sel_stamp(int ev) {
 #ifdef DP_PROFILE
   if (blockIdx.x < 16 && threadIdx.x == 0) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    g_sel_ts[blockIdx.x][ev] = t;
+    g_sel_ts[blockIdx.x][ev] = clock64();  // SM cycles
   }
 #endif
 }

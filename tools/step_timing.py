@@ -38,6 +38,8 @@ if os.environ.get("DP_SHARED_WS"):  # one workspace reused by every layer (a ser
     wss = [wss[0]] * L
 views = [lay.view() for lay in layers]
 lib = N.lib()
+if os.environ.get("DP_HINT_TAU") is not None:  # L2 warm-up threshold (nats); 0 disables
+    lib.dp_debug_set(8, int(round(10 * float(os.environ["DP_HINT_TAU"]))))
 sc = 1.0 / math.sqrt(d)
 
 
@@ -94,6 +96,7 @@ print(f"context {n}, layers {L}, G {G}: us per layer")
 print(f"  plan (same layer)     {timed(lambda: [plan(0) for _ in range(L)]):8.2f}")
 print(f"  plan (layers cycled)  {timed(lambda: [plan(j) for j in range(L)]):8.2f}")
 print(f"  attend (cycled)       {timed(lambda: [attend(j) for j in range(L)]):8.2f}")
+print(f"  attend (same layer)   {timed(lambda: [attend(0) for j in range(L)]):8.2f}   (rows L2-resident)")
 print(f"  plan+attend (cycled)  {timed(lambda: [(plan(j), attend(j)) for j in range(L)]):8.2f}")
 print(f"  dense (cycled)        {timed(lambda: [dense(j) for j in range(L)]):8.2f}")
 lib.dp_debug_set(0, 1)
@@ -121,6 +124,13 @@ for name, col in (("start", 0), ("prefix", 1), ("data0", 2), ("loop", 3), ("flus
     x = x[(x > -1e6) & (x < 1e6)]
     if x.size:
         print(f"  {name:7s} min {x.min():7.2f} med {np.median(x):7.2f} max {x.max():7.2f}  (n={x.size})")
+pbuf = (ctypes.c_ulonglong * 384)()
+lib.dp_debug_plan_timing(ctypes.cast(pbuf, ctypes.c_void_p))
+pt = np.array(pbuf[:], dtype=np.float64).reshape(16, 24)
+pend = pt[:, 9][pt[:, 9] > 0]
+pstart = pt[:, 0][pt[:, 0] > 0]
+if pend.size:
+    print(f"  plan cluster 0 (same layer): start {(pstart.min() - a0) / 1e3:.2f}, end max {(pend.max() - a0) / 1e3:.2f} us")
 pe_rel = (pe - a0) / 1e3
 pi_rel = (pi - a0) / 1e3
 print(f"  producer: first row entries med {np.median(pe_rel):.2f}, first tile issued med {np.median(pi_rel):.2f}")
