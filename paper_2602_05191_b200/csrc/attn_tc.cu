@@ -38,7 +38,7 @@ constexpr int kProducers = 4;  // producer warps, 32 rows each
 constexpr int kTcThreads = kConsumers + 32 * kProducers;
 constexpr int kRowStride = 136;      // bf16 elements per staged row (272 B: conflict-free ldmatrix)
 constexpr int kStages = 3;
-constexpr int kSegCost = 256;  // rows' worth of time a head segment start costs a CTA (range balancing)
+int g_seg_cost = 768;  // rows' worth of time a head segment start costs a CTA (range balancing; dp_debug_set(9, .))
 constexpr int kStageElems = kTcRows * kRowStride;  // one K (or V) tile
 int g_attn_debug = 0;  // profiling switches (dp_debug_set)
 // barrier over the 8 compute warps only (the producer warp never joins)
@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
                                                                float scale_log2, const double* __restrict__ lm,
                                                                WorkLists wl, Partials<float> pt,
                                                                float* __restrict__ out, float* __restrict__ lse,
-                                                               int dbg) {
+                                                               int dbg, int kSegCost) {
   constexpr int d = 128;
   constexpr int kWarps = kConsumers / 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -262,9 +262,55 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
 
   // Q^T B-fragments (registers): b0 = Q[head g8][k*16 + 2tq ..], b1 = Q[head g8][k*16 + 8 + 2tq ..]
   unsigned qa[8][2], qb[8][2];  // hi, lo
+  // ---- consumer prologue: the first two head segments of this CTA's range get
+  // their q staged in shared memory and their approx-list shares computed
+  // now, while the producers fetch row entries and the first tiles -- a head
+  // switch inside the loop then costs no global round trip
+  constexpr int kQes = kQF32 ? 4 : 2;
+  __shared__ __align__(16) unsigned char s_qseg[2][8 * d * 4];
+  int seg_bh[2] = {-1, -1}, ap_pb[2] = {0, 0}, ap_pn[2] = {0, 0};
+  int2 ap_pd[2] = {make_int2(0, 0), make_int2(0, 0)};
+  {
+    TileWalk w0;
+    w0.init(rp, BH, r0, r1);
+    if (w0.more()) {
+      seg_bh[0] = w0.bh;
+      const long long e0 = rp[w0.bh + 1] < r1 ? rp[w0.bh + 1] : r1;
+      if (e0 < r1) {
+        w0.next(rp, BH, (int)(e0 - w0.s));
+        if (w0.more()) seg_bh[1] = w0.bh;
+      }
+    }
+    const int qchunks = G * d * kQes / 16;
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+      if (seg_bh[k] >= 0)
+        for (int i = tid; i < qchunks; i += kConsumers)
+          reinterpret_cast<uint4*>(s_qseg[k])[i] =
+              __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(q) + (size_t)seg_bh[k] * G * d * kQes) + i);
+    if (!kDense) {
+      long long na[2];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) na[k] = seg_bh[k] >= 0 ? __ldcg(&wl.napprox[seg_bh[k]]) : 0;
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int bh = seg_bh[k];
+        if (bh < 0) continue;
+        const long long hr = rp[bh + 1] - rp[bh];
+        const long long lo = (r0 > rp[bh] ? r0 : rp[bh]) - rp[bh], hi = (r1 < rp[bh + 1] ? r1 : rp[bh + 1]) - rp[bh];
+        const int j0 = hr > 0 ? (int)(na[k] * lo / hr) : 0, j1 = hr > 0 ? (int)(na[k] * hi / hr) : 0;
+        ap_pb[k] = j0 + (j1 - j0) * warp / kWarps;
+        ap_pn[k] = j0 + (j1 - j0) * (warp + 1) / kWarps - ap_pb[k];
+        if (lane < ap_pn[k]) ap_pd[k] = __ldcg(&wl.approx[(size_t)bh * v.cluster_cap + ap_pb[k] + lane]);
+      }
+    }
+    consumers_sync();  // staged q visible to every consumer warp
+  }
   auto load_q = [&](int bh) {
     const bool valid = g8 < G;
+    const int sk = bh == seg_bh[0] ? 0 : (bh == seg_bh[1] ? 1 : -1);
     const size_t qoff = ((size_t)bh * G + (valid ? g8 : 0)) * d;
+    const unsigned char* qs = sk >= 0 ? s_qseg[sk] + (size_t)(valid ? g8 : 0) * d * kQes : nullptr;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
 #pragma unroll
@@ -274,10 +320,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
           qa[k][h] = 0u;
           qb[k][h] = 0u;
         } else if (kQF32) {
-          const float2 f = *reinterpret_cast<const float2*>(reinterpret_cast<const float*>(q) + qoff + col);
+          const float2 f = qs ? *reinterpret_cast<const float2*>(qs + (size_t)col * 4)
+                              : *reinterpret_cast<const float2*>(reinterpret_cast<const float*>(q) + qoff + col);
           split2(f.x, f.y, qa[k][h], qb[k][h]);
         } else {
-          qa[k][h] = *reinterpret_cast<const unsigned*>(reinterpret_cast<const __nv_bfloat16*>(q) + qoff + col);
+          qa[k][h] = qs ? *reinterpret_cast<const unsigned*>(qs + (size_t)col * 2)
+                        : *reinterpret_cast<const unsigned*>(reinterpret_cast<const __nv_bfloat16*>(q) + qoff + col);
           qb[k][h] = 0u;
         }
       }
@@ -468,7 +516,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
       // plan's approx list, each warp takes a share and trickles it into its
       // online softmax one entry per tile, loads issued a tile ahead (so the
       // fold never waits on memory); the flush drains what is left.
-      if (!kDense) {
+      if (!kDense && (bh == seg_bh[0] || bh == seg_bh[1])) {  // precomputed in the prologue
+        const int sk = bh == seg_bh[0] ? 0 : 1;
+        ap_base = ap_pb[sk];
+        ap_n = ap_pn[sk];
+        ap_desc = ap_pd[sk];
+        ap_k = 0;
+        ap_ready = false;
+      } else if (!kDense) {
         // this CTA's share of the head's approx list is proportional to the
         // rows of the head it covers (a short head segment gets few entries)
         const long long na = __ldcg(&wl.napprox[bh]);
@@ -745,7 +800,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
 }
 
 }  // namespace dp
-namespace dp { extern int g_plan_cl, g_pp_single, g_step_cl, g_step_off, g_step_dbg; extern float g_step_tau; }
+namespace dp { extern int g_plan_cl, g_pp_single, g_step_cl, g_step_off, g_step_dbg, g_seg_cost; extern float g_step_tau; }
 extern "C" int dp_debug_set(int key, int value) {
   if (key == 0) dp::g_attn_debug = value;
   if (key == 1) dp::g_plan_cl = value;
@@ -754,6 +809,7 @@ extern "C" int dp_debug_set(int key, int value) {
   if (key == 5) dp::g_step_cl = value;
   if (key == 6) dp::g_step_off = value;
   if (key == 7) dp::g_step_dbg = value;
+  if (key == 9) dp::g_seg_cost = value;
   return 0;
 }
 extern "C" int dp_debug_attn_timing(unsigned long long* out) {
@@ -784,7 +840,7 @@ static cudaError_t launch_tc_t(const dp_cache_view& v, const void* q, int G, dou
   cfg.attrs = at;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, attn_tc_kernel<kDense, kQF32>, v, q, G, (float)(scale * 1.4426950408889634), lm,
-                            wl, pt, out, lse, g_attn_debug);
+                            wl, pt, out, lse, g_attn_debug, g_seg_cost);
 }
 
 cudaError_t launch_attn_tc(const dp_cache_view& v, const void* q, int qdt, int G, double scale, const double* lm,

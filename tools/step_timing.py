@@ -40,6 +40,8 @@ views = [lay.view() for lay in layers]
 lib = N.lib()
 if os.environ.get("DP_HINT_TAU") is not None:  # L2 warm-up threshold (nats); 0 disables
     lib.dp_debug_set(8, int(round(10 * float(os.environ["DP_HINT_TAU"]))))
+if os.environ.get("DP_SEG_COST") is not None:  # attention range balancing: rows per head-segment start
+    lib.dp_debug_set(9, int(os.environ["DP_SEG_COST"]))
 sc = 1.0 / math.sqrt(d)
 
 
