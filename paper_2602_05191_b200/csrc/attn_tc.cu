@@ -268,6 +268,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
   // switch inside the loop then costs no global round trip
   constexpr int kQes = kQF32 ? 4 : 2;
   __shared__ __align__(16) unsigned char s_qseg[2][8 * d * 4];
+  __shared__ float s_refm[2][8];  // the plan's reference maxima of those segments' q heads
   int seg_bh[2] = {-1, -1}, ap_pb[2] = {0, 0}, ap_pn[2] = {0, 0};
   int2 ap_pd[2] = {make_int2(0, 0), make_int2(0, 0)};
   {
@@ -289,6 +290,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
           reinterpret_cast<uint4*>(s_qseg[k])[i] =
               __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(q) + (size_t)seg_bh[k] * G * d * kQes) + i);
     if (!kDense) {
+      if (tid < 2 * G && seg_bh[tid / G] >= 0) s_refm[tid / G][tid % G] = __ldcg(&wl.refm[(size_t)seg_bh[tid / G] * G + tid % G]);
       long long na[2];
 #pragma unroll
       for (int k = 0; k < 2; ++k) na[k] = seg_bh[k] >= 0 ? __ldcg(&wl.napprox[seg_bh[k]]) : 0;
@@ -457,7 +459,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
 #pragma unroll 1
       for (int i = tid; i < G * d4; i += kConsumers) {
         const int h = i / d4, c = (i - h * d4) * 4;
-        const float Mr = __ldcg(&wl.refm[(size_t)bh * G + h]);
+        const float Mr = bh == seg_bh[0] ? s_refm[0][h] : (bh == seg_bh[1] ? s_refm[1][h]
+                                                                            : __ldcg(&wl.refm[(size_t)bh * G + h]));
         bool any = false;
         float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
         float L = 0.f;

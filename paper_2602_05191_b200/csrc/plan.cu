@@ -230,10 +230,36 @@ __global__ void __launch_bounds__(kPT, 1)
       for (int t = tid; t < v.sink + v.window; t += kPT)
         rw[t] = tag | (unsigned)(t < v.sink ? t : v.n_tokens - v.window + (t - v.sink));
     }
+    // the group's queries -> fp64 rows: one 16-B load per thread (a single
+    // round trip; the scalar loop took two dependent ones per thread)
+    if ((reinterpret_cast<uintptr_t>(q) & 15) != 0) {  // unaligned caller buffer: scalar loads
 #pragma unroll 1
-    for (int i = tid; i < 8 * d; i += kPT) {
-      const int h = i / d, c = i - h * d;
-      qd[h * qP + c] = h < G ? (double)load_elem_f(q, qdt, ((size_t)bh * G + h) * d + c) : 0.0;
+      for (int i = tid; i < 8 * d; i += kPT) {
+        const int h = i / d, c = i - h * d;
+        qd[h * qP + c] = h < G ? (double)load_elem_f(q, qdt, ((size_t)bh * G + h) * d + c) : 0.0;
+      }
+    } else {
+      const int es = qdt == DP_F32 ? 4 : 2, per16 = 16 / es, nchunk = 8 * d / per16;
+      for (int i = tid; i < nchunk; i += kPT) {
+        const int h = (i * per16) / d, c0 = (i * per16) - h * d;
+        if (h < G) {
+          const uint4 raw = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(q) +
+                                                                 (((size_t)bh * G + h) * d + c0) * es));
+          const unsigned w[4] = {raw.x, raw.y, raw.z, raw.w};
+          if (es == 4) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) qd[h * qP + c0 + j] = (double)__uint_as_float(w[j]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              qd[h * qP + c0 + 2 * j] = (double)__uint_as_float(w[j] << 16);
+              qd[h * qP + c0 + 2 * j + 1] = (double)__uint_as_float(w[j] & 0xFFFF0000u);
+            }
+          }
+        } else {
+          for (int j = 0; j < per16; ++j) qd[h * qP + c0 + j] = 0.0;
+        }
+      }
     }
   }
   __syncthreads();  // qd, offs, barrier init
