@@ -57,6 +57,11 @@ def parse():
     ap.add_argument("--long-context", type=int, default=131072,
                     help="secondary workload context (0: off); reported under long_context")
     ap.add_argument("--long-layers", type=int, default=4)
+    ap.add_argument("--prefill-group-gib", type=float, default=16.0,
+                    help="position-ordered KV clustered per launch (bounds the prefill's transient memory)")
+    ap.add_argument("--sim-world", type=int, default=1,
+                    help="measure ONE rank's KV-head shard of a P-GPU run on this GPU (no collectives)")
+    ap.add_argument("--sim-rank", type=int, default=0)
     return ap.parse_args()
 
 
@@ -71,7 +76,9 @@ def workload_config(a, world):
         "layers": a.layers, "batch": a.batch, "context": a.context, "kv_heads": a.kv_heads,
         "q_heads": a.kv_heads * a.gqa, "head_dim": a.head_dim, "p1": a.p1, "p2": a.p2,
         "tail_profile": a.profile, "sink": 4, "window": 64, "tokens_per_cluster": 32,
-        "parallelism": f"kv-head shard x{world}" if world > 1 else "single GPU",
+        "parallelism": (f"kv-head shard x{world}" if world > 1 else
+                        (f"kv-head shard {a.sim_rank}/{a.sim_world} measured alone on one GPU (per-GPU share of a "
+                         f"{a.sim_world}-GPU run)" if a.sim_world > 1 else "single GPU")),
         "l2": "inputs larger than L2 (each layer's KV > 126 MB; layers cycled)",
     }
 
@@ -133,14 +140,19 @@ class ClockSampler:
 # distributed plumbing
 # ---------------------------------------------------------------------------
 def dist_setup():
+    """(world, rank, local device).  DP_SAME_DEVICE=1 runs every rank on
+    cuda:0 over gloo -- a plumbing dry run of an N-GPU launch on one GPU."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    same = os.environ.get("DP_SAME_DEVICE") == "1"
+    if same:
+        local = 0
     if world > 1:
         import torch.distributed as dist
 
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl" if _cuda() else "gloo")
+        dist.init_process_group("nccl" if _cuda() and not same else "gloo")
     return world, rank, local
 
 
@@ -156,7 +168,8 @@ def max_over_ranks(x, world, device):
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device=device)
+    on_dev = dist.get_backend() == "nccl"
+    t = torch.tensor([x], dtype=torch.float64, device=device if on_dev else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -394,44 +407,55 @@ def _measure(a, context, L, dev, world, rank, sampler=None, profile=None, with_d
     from paper_2602_05191_b200.cache import dtype_code, head_seed
     from paper_2602_05191_b200.workload import generate_layer, generate_queries
 
-    hl = a.kv_heads // world
-    h0 = rank * hl
+    P, r = (a.sim_world, a.sim_rank) if a.sim_world > 1 else (world, rank)
+    hl = a.kv_heads // P
+    h0 = r * hl
     G, d, B = a.gqa, a.head_dim, a.batch
     lib = N.lib()
 
     # ---- prefill: synthetic caches + GPU k-means (not timed) -------------
-    t0 = time.perf_counter()
-    qdev = []
-    ks = torch.empty((L * B, hl, context, d), dtype=torch.bfloat16, device=dev)
-    vs = torch.empty_like(ks)
-    for li in range(L):
-        k, v, centers = generate_layer(B, a.kv_heads, context, d, layer=li, device=dev)
-        ks[li * B:(li + 1) * B] = k[:, h0:h0 + hl]
-        vs[li * B:(li + 1) * B] = v[:, h0:h0 + hl]
-        del k, v
-        q = generate_queries(centers[:, h0:h0 + hl], G, a.qsteps, profile=profile or a.profile, layer=li)
-        qdev.append(torch.from_numpy(q).to(dev).to(torch.bfloat16))  # [S,B,Hq,d]
-    torch.cuda.synchronize(dev)
-    gen_s = time.perf_counter() - t0
-    # every (layer, sequence, kv head) of the model clustered in ONE batched
-    # GPU k-means (seeds as build_clustered_cache: SeedSequence([0, layer, head]))
-    seeds = [[head_seed(0, li, h0 + h, b) for h in range(hl)] for li in range(L) for b in range(B)]
-    big = cluster_layer(ks, vs, fp64_assign=bool(a.fp64_assign), head_seeds=seeds)
-    del ks, vs
-    torch.cuda.synchronize(dev)
-    prefill_s = time.perf_counter() - t0 - gen_s
-    per_seq = big.split()
-    layers = []
-    for li in range(L):
-        if B == 1:
-            layers.append(per_seq[li])
-        else:  # re-slice [L*B] -> per layer [B]
-            sl = lambda t: t[li * B:(li + 1) * B]  # noqa: E731
+    # Layers are generated and clustered in groups (one batched k-means launch
+    # per group, every (layer, sequence, kv head) of the group at once); each
+    # group's position-ordered KV is freed as soon as its clustered copy
+    # exists, so the resident cache is ONE copy (config 3 at 2 GPUs: 128 GiB
+    # per rank) plus one group in flight.  Sequence b of layer li comes from
+    # the device generator seeded (layer li, seed b); seeds of the k-means as
+    # build_clustered_cache: SeedSequence([0, layer, head]).
+    gen_s = prefill_s = 0.0
+    per_layer = B * hl * context * d * 2 * 2
+    group = max(1, min(L, int(a.prefill_group_gib * (1 << 30)) // max(per_layer, 1)))
+    qdev, layers = [], []
+    for g0 in range(0, L, group):
+        ng = min(group, L - g0)
+        t0 = time.perf_counter()
+        ks = torch.empty((ng * B, hl, context, d), dtype=torch.bfloat16, device=dev)
+        vs = torch.empty_like(ks)
+        for li in range(g0, g0 + ng):
+            cents = []
+            for b in range(B):
+                k, v, c = generate_layer(1, a.kv_heads, context, d, layer=li, seed=b, device=dev)
+                ks[(li - g0) * B + b] = k[0, h0:h0 + hl]
+                vs[(li - g0) * B + b] = v[0, h0:h0 + hl]
+                cents.append(c[0, h0:h0 + hl])
+                del k, v
+            q = generate_queries(np.stack(cents), G, a.qsteps, profile=profile or a.profile, layer=li)
+            qdev.append(torch.from_numpy(q).to(dev).to(torch.bfloat16))  # [S,B,Hq,d]
+        torch.cuda.synchronize(dev)
+        t1 = time.perf_counter()
+        seeds = [[head_seed(0, li, h0 + h, b) for h in range(hl)] for li in range(g0, g0 + ng) for b in range(B)]
+        big = cluster_layer(ks, vs, fp64_assign=bool(a.fp64_assign), head_seeds=seeds)
+        del ks, vs
+        torch.cuda.synchronize(dev)
+        gen_s += t1 - t0
+        prefill_s += time.perf_counter() - t1
+        for j in range(ng):  # [ng*B] -> per layer [B]
+            sl = lambda t: t[j * B:(j + 1) * B]  # noqa: E731
             lay = ClusteredLayer(sl(big.keys), sl(big.values), sl(big.offs), sl(big.nclusters),
                                  sl(big.centroids), sl(big.value_means), sl(big.perm), big.n_tokens,
                                  big.sink, big.window)
             lay._prefill_k = big._prefill_k
             layers.append(lay)
+        del big
 
     # one workspace reused by every layer, as a serving engine holds it (all
     # layers share the geometry; each plan waits for the previous attention)
