@@ -23,6 +23,8 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxe
          "-Xptxas", "-v"]
 if os.environ.get("DP_PROFILE"):  # %globaltimer phase stamps (tools/plan_timing.py, step_timing.py)
     FLAGS = FLAGS + ["-DDP_PROFILE"]
+if os.environ.get("DP_EXTRA_FLAGS"):  # experiment switches, e.g. "-DDP_SEL_REPEAT"
+    FLAGS = FLAGS + os.environ["DP_EXTRA_FLAGS"].split()
 
 
 def _nvcc():

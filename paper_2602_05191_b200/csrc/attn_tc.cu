@@ -803,7 +803,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
 }
 
 }  // namespace dp
-namespace dp { extern int g_plan_cl, g_pp_single, g_step_cl, g_step_off, g_step_dbg, g_seg_cost; extern float g_step_tau; }
+namespace dp { extern int g_plan_dbg; extern int g_plan_cl, g_pp_single, g_step_cl, g_step_off, g_step_dbg, g_seg_cost; extern float g_step_tau; }
 extern "C" int dp_debug_set(int key, int value) {
   if (key == 0) dp::g_attn_debug = value;
   if (key == 1) dp::g_plan_cl = value;
@@ -813,6 +813,7 @@ extern "C" int dp_debug_set(int key, int value) {
   if (key == 6) dp::g_step_off = value;
   if (key == 7) dp::g_step_dbg = value;
   if (key == 9) dp::g_seg_cost = value;
+  if (key == 10) dp::g_plan_dbg = value;
   return 0;
 }
 extern "C" int dp_debug_attn_timing(unsigned long long* out) {

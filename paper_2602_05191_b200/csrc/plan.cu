@@ -59,6 +59,7 @@ constexpr int kMaxCL = 16;
 __device__ unsigned long long g_plan_ts[16][24];
 __device__ unsigned long long g_plan_clk[16][2];
 __device__ unsigned long long g_plan_cyc[16][24];
+__device__ unsigned long long g_sel_ts2[16][8];  // DP_SEL_REPEAT: the first pass's select stamps
 // (compiled in only with -DDP_PROFILE: DP_PROFILE=1 python -m paper_2602_05191_b200.build)
 __device__ __forceinline__ void stamp(int r, int ev) {
 #ifdef DP_PROFILE
@@ -82,10 +83,51 @@ __device__ __forceinline__ void cl_sync() {
   cl_wait();
 }
 
+// DSMEM pushes that signal the receiver's mbarrier (st.async ... complete_tx):
+// the receiver waits for exactly the bytes it expects, the sender never
+// waits (no cluster-wide barrier, no release fence on the sender's side)
+__device__ __forceinline__ unsigned cl_map(const void* p, int rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"((unsigned)__cvta_generic_to_shared(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void push_f64(const double* dst, int rank, double v, const unsigned long long* bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];\n" ::"r"(cl_map(dst, rank)),
+               "l"(__double_as_longlong(v)), "r"(cl_map(bar, rank))
+               : "memory");
+}
+__device__ __forceinline__ void push_u32(const void* dst, int rank, unsigned v, const unsigned long long* bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];\n" ::"r"(cl_map(dst, rank)),
+               "r"(v), "r"(cl_map(bar, rank))
+               : "memory");
+}
+__device__ __forceinline__ void push_v4(const void* dst, int rank, int a, int b, int c, int e,
+                                        const unsigned long long* bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];\n" ::"r"(
+                   cl_map(dst, rank)),
+               "r"(a), "r"(b), "r"(c), "r"(e), "r"(cl_map(bar, rank))
+               : "memory");
+}
+__device__ __forceinline__ void mb_expect(const unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mb_wait0(const unsigned long long* bar) {  // phase 0 complete (acquire, cluster)
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  unsigned done = 0;
+  while (!done)
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], 0;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(a)
+        : "memory");
+}
+
 struct PlanLayout {
   int per;                 // centroid rows per CTA (capacity)
   size_t cs;               // P1: [per][d + 4] fp32 centroid slice | P2 (owners): select arrays | P3 scratch
-  size_t um, bin, hm, hc, clist, cord, stown;  // P2 arrays (inside the cs region)
+  size_t um, bin, hm, hc, clist, cord, stown;  // P2 arrays (inside the cs region; bin = cursors, cord unused)
   size_t lmall;            // [cap] fp64 log-masses of my head (owners; pushed by every CTA)
   size_t lml;              // [kG][per] fp64 log-masses of my slice
   size_t qd;               // [8][d + 4] fp64 queries (padded rows)
@@ -110,16 +152,16 @@ __host__ __device__ inline PlanLayout plan_layout(int CL, int kG, int d, int cap
     return r;
   };
   L.um = take2((size_t)cap * 8);
-  L.bin = take2((size_t)cap * 2);
+  L.bin = take2((size_t)kBins * 4);  // select_fast: per-bin cursors
   L.hm = take2((size_t)kBins * 8);
-  L.hc = take2((size_t)kBins * 4);
+  L.hc = take2((size_t)(kBins + 1) * 4);
   L.clist = take2((size_t)cap * 4);
-  L.cord = take2((size_t)cap * 4);
+  L.cord = 0;
   L.stown = take2((size_t)cap + 4);
   const size_t csb = (size_t)2 * kTileBytes;  // two TMA tiles (128B swizzle) to d + 4 floats (conflict-free A loads)
   const size_t big = csb > p2 ? csb : p2;
   L.cs = take(big);
-  L.um += L.cs; L.bin += L.cs; L.hm += L.cs; L.hc += L.cs; L.clist += L.cs; L.cord += L.cs; L.stown += L.cs;
+  L.um += L.cs; L.bin += L.cs; L.hm += L.cs; L.hc += L.cs; L.clist += L.cs; L.stown += L.cs;
   L.lmall = take((size_t)cap * 8);
   L.lml = take((size_t)kG * L.per * 8);
   L.qd = take((size_t)8 * (d + 4) * 8);
@@ -143,7 +185,7 @@ template <int kG>
 __global__ void __launch_bounds__(kPT, 1)
     plan_kernel(const __grid_constant__ CUtensorMap tmC, dp_cache_view v, const void* __restrict__ q, int qdt, int G,
                 double scale, double p1, double p2, double* __restrict__ lm_out, uint8_t* __restrict__ state_out,
-                int* __restrict__ counts, WorkLists wl, int CL, int boxr) {
+                int* __restrict__ counts, WorkLists wl, int CL, int boxr, int dbg) {
   cg::cluster_group cluster = cg::this_cluster();
   const int r = (int)cluster.block_rank();
   const int bh = blockIdx.x / CL;
@@ -161,13 +203,18 @@ __global__ void __launch_bounds__(kPT, 1)
   int* offs = reinterpret_cast<int*>(smem + L.offs);
 
   __shared__ __align__(8) unsigned long long s_tbar[2];  // TMA tile barriers
+  // hand-off barriers: A (owner g <- every slice's scores of head g, maxima),
+  // B (slice r <- every owner's states of the slice; CTA 0 also the head
+  // maxima and late sink/window maxima), C (every CTA <- every slice's counts)
+  __shared__ __align__(8) unsigned long long s_mb[3];
   __shared__ double s_max[kMaxCL][kG];  // pushed slice maxima (owners)
   __shared__ double s_swx[kMaxCL][kG];  // pushed sink/window logit maxima (owners)
   __shared__ double s_sw[kPW][kG];
-  __shared__ int s_cnt[kMaxCL][4];      // pushed slice counts (rows, exact clusters, approx clusters)
+  __shared__ __align__(16) int s_cnt[kMaxCL][4];  // pushed slice counts (rows, exact clusters, approx clusters)
   __shared__ double s_Mg[kG];           // pushed head maxima (every CTA)
   __shared__ double s_wm[kPW][kG];
   __shared__ SelScratch<kPT> s_selx;
+  __shared__ SelFastShared s_self;
   unsigned long long* s_redu = s_selx.redu;
   int* s_redi = s_selx.redi;
 
@@ -176,7 +223,14 @@ __global__ void __launch_bounds__(kPT, 1)
   // attention) never writes them, and anything that does (dp_append_token,
   // prefill) completed before that grid started.  So the centroid TMA and the
   // offset loads overlap the previous layer's tail; q and every output wait.
-  cl_arrive_relaxed();  // (S) every CTA of the cluster has started before DSMEM is touched
+  if (tid == 0) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"((unsigned)__cvta_generic_to_shared(&s_mb[i])));
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  cl_arrive_relaxed();  // (S) every CTA of the cluster has started (and initialised its barriers) before DSMEM is touched
   stamp(r, 0);
 
   const int K = __ldg(&v.nclusters[bh]);
@@ -194,6 +248,12 @@ __global__ void __launch_bounds__(kPT, 1)
   const int ntile = (nloc + kCh - 1) / kCh;
   const int ncb = d / 32;  // 128-B column blocks per row
   if (tid == 0) {
+    // bytes each hand-off barrier of this CTA receives
+    if (r < G) mb_expect(&s_mb[0], (unsigned)(K * 8 + CL * 16));
+    unsigned eb = (unsigned)(G * 4 * ((nloc + 3) / 4));
+    if (r == 0) eb += (unsigned)(G * 8 + (CL > G ? (CL - G) * G * 8 : 0));
+    mb_expect(&s_mb[1], eb);
+    mb_expect(&s_mb[2], (unsigned)(CL * 16));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar0));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar0 + 8));
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -315,8 +375,8 @@ __global__ void __launch_bounds__(kPT, 1)
             // a non-finite query must not break the selection's ordering: NaN
             // ranks last (-inf), +inf first (the largest finite double)
             val = val != val ? -CUDART_INF : fmin(val, 1.7976931348623157e308);
-            lml[h * L.per + row] = val;
-            remote(cluster, lmall, h)[k0 + row] = val;
+            push_f64(lmall + k0 + row, h, val, &s_mb[0]);
+            if (lm_out) lm_out[((size_t)bh * G + h) * cap + k0 + row] = val;  // (read by the attention kernel)
             lmax[e] = fmax(lmax[e], val);
           }
         }
@@ -382,21 +442,31 @@ __global__ void __launch_bounds__(kPT, 1)
     if (lane < 4 && h < kG) s_wm[warp][h] = m;
   }
   __syncthreads();
-  if (tid < G) {
-    double mm = -CUDART_INF;
-#pragma unroll 1
-    for (int w = 0; w < kPW; ++w) mm = fmax(mm, s_wm[w][tid]);
-    remote(cluster, &s_max[0][0], tid)[r * kG + tid] = mm;
-    double sm = -CUDART_INF;
-#pragma unroll 1
-    for (int w = 0; w < kPW; ++w) sm = fmax(sm, s_sw[w][tid]);
-    remote(cluster, &s_swx[0][0], tid)[r * kG + tid] = sm;
+  if (tid < G) {  // (independent loads, then a tree: no serial chain of shared loads)
+    double mm[kPW], sm[kPW];
+#pragma unroll
+    for (int w = 0; w < kPW; ++w) {
+      mm[w] = s_wm[w][tid];
+      sm[w] = s_sw[w][tid];
+    }
+#pragma unroll
+    for (int h = kPW / 2; h > 0; h >>= 1)
+#pragma unroll
+      for (int w = 0; w < h; ++w) {
+        mm[w] = fmax(mm[w], mm[w + h]);
+        sm[w] = fmax(sm[w], sm[w + h]);
+      }
+    push_f64(&s_max[r][tid], tid, mm[0], &s_mb[0]);
+    push_f64(&s_swx[r][tid], tid, sm[0], &s_mb[0]);
   }
   if (r < G) {  // owners: zero the histogram now (the tile buffers it overlays are consumed)
-    select_zero_hist<kPT, kBins>(reinterpret_cast<unsigned*>(smem + L.hm), reinterpret_cast<int*>(smem + L.hc));
+    select_fast_zero<kPT, kBins>(reinterpret_cast<unsigned*>(smem + L.hm), reinterpret_cast<int*>(smem + L.hc), &s_self);
   }
   stamp(r, 3);
-  cl_sync();  // (A) every score is in its owner's shared memory
+  if (r < G) {  // (A) every score of my head is in my shared memory
+    mb_wait0(&s_mb[0]);
+    __syncthreads();  // (the zeroed histogram too)
+  }
   stamp(r, 4);
 
   // ---------------- P2: two-stage top-p, owner CTA g = r -------------------
@@ -405,17 +475,36 @@ __global__ void __launch_bounds__(kPT, 1)
     const int hq = bh * G + g;
     unsigned long long* um = reinterpret_cast<unsigned long long*>(smem + L.um);
     uint8_t* stown = reinterpret_cast<uint8_t*>(smem + L.stown);  // this head's states, then packed out
-    uint16_t* binI = reinterpret_cast<uint16_t*>(smem + L.bin);
-    unsigned* hmh = reinterpret_cast<unsigned*>(smem + L.hm);  // [kBins] high 19 bits of the mass
+    int* cur = reinterpret_cast<int*>(smem + L.bin);
+    unsigned* hm = reinterpret_cast<unsigned*>(smem + L.hm);
     int* hc = reinterpret_cast<int*>(smem + L.hc);
     int* clist = reinterpret_cast<int*>(smem + L.clist);
-    int* cord = reinterpret_cast<int*>(smem + L.cord);
     double M = -CUDART_INF;
-#pragma unroll 1
-    for (int rr = 0; rr < CL; ++rr) M = fmax(M, s_max[rr][g]);
+    {  // max of the pushed slice maxima (independent loads, then a tree)
+      double mm[kMaxCL];
+#pragma unroll
+      for (int rr = 0; rr < kMaxCL; ++rr) mm[rr] = rr < CL ? s_max[rr][g] : -CUDART_INF;
+#pragma unroll
+      for (int w = kMaxCL / 2; w > 0; w >>= 1)
+#pragma unroll
+        for (int rr = 0; rr < w; ++rr) mm[rr] = fmax(mm[rr], mm[rr + w]);
+      M = mm[0];
+    }
     stamp(r, 20);
     int n1 = 0, n2 = 0;
-    select_two_stage<kPT, kBins>(K, M, lmall, p1, p2, um, binI, hmh, hc, clist, cord, stown, &s_selx, n1, n2);
+    if (dbg & 2) {  // timing experiment: no selection (nothing but sink/window selected)
+      for (int i = tid; i < K; i += kPT) stown[i] = 0;
+      __syncthreads();
+    } else {
+      select_fast<kPT, kBins, kPlanMaxCap / kPT>(K, M, lmall, p1, p2, um, hm, hc, cur, clist, stown, &s_self, n1, n2);
+    }
+#ifdef DP_SEL_REPEAT
+    // experiment: the same selection again with a warm instruction cache
+    if (blockIdx.x < 16 && tid < 8) g_sel_ts2[blockIdx.x][tid] = g_sel_ts[blockIdx.x][tid];
+    select_fast_zero<kPT, kBins>(hm, hc, &s_self);
+    __syncthreads();
+    select_fast<kPT, kBins, kPlanMaxCap / kPT>(K, M, lmall, p1, p2, um, hm, hc, cur, clist, stown, &s_self, n1, n2);
+#endif
     if (K > 0) {
       // states travel to the slice owners as packed 4-byte words (slices are 4-aligned)
 #pragma unroll 1
@@ -425,19 +514,19 @@ __global__ void __launch_bounds__(kPT, 1)
         for (int t = 0; t < 4; ++t)
           if (i + t < K) w |= (unsigned)stown[i + t] << (8 * t);
         const int rr = i / per;
-        *reinterpret_cast<unsigned*>(remote(cluster, stl, rr) + g * L.per + (i - rr * per)) = w;
+        push_u32(stl + g * L.per + (i - rr * per), rr, w, &s_mb[1]);
       }
     }
     if (tid == 0) {
       counts[2 * hq] = n1;
       counts[2 * hq + 1] = n2;
     }
-    if (tid < CL) {
+    if (tid == 0) {
       double SW = -CUDART_INF;
       if (CL <= G)
 #pragma unroll 1
         for (int rr = 0; rr < CL; ++rr) SW = fmax(SW, s_swx[rr][g]);
-      remote(cluster, s_Mg, tid)[g] = CL > G ? (K > 0 ? M : -CUDART_INF) : ref_max(K > 0 ? M : -CUDART_INF, SW);
+      push_f64(&s_Mg[g], 0, CL > G ? (K > 0 ? M : -CUDART_INF) : ref_max(K > 0 ? M : -CUDART_INF, SW), &s_mb[1]);
     }
   }
   if (CL > G && r >= G) {  // sw_late: the CTAs idle in P2 score the sink/window rows -> CTA 0
@@ -468,15 +557,20 @@ __global__ void __launch_bounds__(kPT, 1)
       for (int g = 0; g < kG; ++g) s_sw[warp][g] = swl[g];
     __syncthreads();
     if (tid < G) {
-      double sm = -CUDART_INF;
-#pragma unroll 1
-      for (int w = 0; w < kPW; ++w) sm = fmax(sm, s_sw[w][tid]);
-      remote(cluster, &s_swx[0][0], 0)[r * kG + tid] = sm;
+      double sm[kPW];
+#pragma unroll
+      for (int w = 0; w < kPW; ++w) sm[w] = s_sw[w][tid];
+#pragma unroll
+      for (int h = kPW / 2; h > 0; h >>= 1)
+#pragma unroll
+        for (int w = 0; w < h; ++w) sm[w] = fmax(sm[w], sm[w + h]);
+      push_f64(&s_swx[r][tid], 0, sm[0], &s_mb[1]);
     }
   }
   stamp(r, 5);
-  cl_sync();  // (B) every cluster state and head max is in place
+  mb_wait0(&s_mb[1]);  // (B) every cluster state of my slice (CTA 0: and the head maxima) is in place
   stamp(r, 6);
+  if (dbg & 4) return;  // timing experiment: no work lists
 
   // ---------------- P3: union counts + approx partial of my slice --------
   int e_rows = 0, e_cl = 0, a_cl = 0;
@@ -507,43 +601,36 @@ __global__ void __launch_bounds__(kPT, 1)
   stamp(r, 15);
   if (tid < CL) {
     int t0 = 0, t1 = 0, t2 = 0;
-#pragma unroll 1
-    for (int w = 0; w < kPW; ++w) {
+#pragma unroll
+    for (int w = 0; w < kPW; ++w) {  // independent loads (unrolled): no serial shared-load chain
       t0 += s_redi[w * 4 + 0];
       t1 += s_redi[w * 4 + 1];
       t2 += s_redi[w * 4 + 2];
     }
-    int* dst = remote(cluster, &s_cnt[0][0], tid) + r * 4;
-    dst[0] = t0;
-    dst[1] = t1;
-    dst[2] = t2;
+    push_v4(&s_cnt[r][0], tid, t0, t1, t2, 0, &s_mb[2]);
   }
   stamp(r, 7);
-  cl_sync();  // (C) slice counts published; no remote access after this
+  mb_wait0(&s_mb[2]);  // (C) every slice's counts are in place; no remote access after this
   stamp(r, 8);
 
   // ---------------- P4: work lists -----------------------------------------
   const int sw_rows = v.sink + v.window;
   int row_base = sw_rows, apx_base = 0, tot_r = 0, tot_e = 0, tot_a = 0;
-#pragma unroll 1
-  for (int rr = 0; rr < CL; ++rr) {
+#pragma unroll
+  for (int rr = 0; rr < kMaxCL; ++rr) {
+    if (rr >= CL) break;
+    const int c0 = s_cnt[rr][0], c1 = s_cnt[rr][1], c2 = s_cnt[rr][2];
     if (rr < r) {
-      row_base += s_cnt[rr][0];
-      apx_base += s_cnt[rr][2];
+      row_base += c0;
+      apx_base += c2;
     }
-    tot_r += s_cnt[rr][0];
-    tot_e += s_cnt[rr][1];
-    tot_a += s_cnt[rr][2];
+    tot_r += c0;
+    tot_e += c1;
+    tot_a += c2;
   }
   stamp(r, 16);
   // log-masses (the attention kernel reads the approximated clusters' ones)
   // and the debug states of my slice, kept off the barrier-release paths above
-  if (lm_out)
-#pragma unroll 1
-    for (int i = tid; i < G * nloc; i += kPT) {
-      const int g = i / nloc, k = i - g * nloc;
-      lm_out[((size_t)bh * G + g) * cap + k0 + k] = lml[g * L.per + k];
-    }
   if (state_out)
 #pragma unroll 1
     for (int i = tid; i < G * nloc; i += kPT) {
@@ -621,6 +708,7 @@ __global__ void __launch_bounds__(kPT, 1)
 }
 
 int g_plan_cl = 0;  // 0: auto; 2..16 forces the cluster size (dp_debug_set(1, .))
+int g_plan_dbg = 0;  // timing experiments (dp_debug_set(10, .)): bit 1 skips the selection, bit 2 the work lists
 size_t plan_smem_bytes(int d, int cap, int CL, int kG) { return plan_layout(CL, kG, d, cap).total + 1024; }
 
 // 2-D tensor map over all centroid rows [B*H*cap, d] fp32: 32-float x kCh-row
@@ -780,10 +868,10 @@ cudaError_t launch_plan(const dp_cache_view& v, const void* q, int qdt, int G, d
   const long long rows = (long long)v.batch * v.kv_heads * v.cluster_cap;
   const int boxr = rows < kCh ? (int)rows : kCh;  // rows per TMA box (the tile is never fuller than that)
   switch (kG) {
-    case 1: return cudaLaunchKernelEx(&cfg, plan_kernel<1>, tm, v, q, qdt, G, scale, p1, p2, lm, state, counts, wl, CL, boxr);
-    case 2: return cudaLaunchKernelEx(&cfg, plan_kernel<2>, tm, v, q, qdt, G, scale, p1, p2, lm, state, counts, wl, CL, boxr);
-    case 4: return cudaLaunchKernelEx(&cfg, plan_kernel<4>, tm, v, q, qdt, G, scale, p1, p2, lm, state, counts, wl, CL, boxr);
-    default: return cudaLaunchKernelEx(&cfg, plan_kernel<8>, tm, v, q, qdt, G, scale, p1, p2, lm, state, counts, wl, CL, boxr);
+    case 1: return cudaLaunchKernelEx(&cfg, plan_kernel<1>, tm, v, q, qdt, G, scale, p1, p2, lm, state, counts, wl, CL, boxr, g_plan_dbg);
+    case 2: return cudaLaunchKernelEx(&cfg, plan_kernel<2>, tm, v, q, qdt, G, scale, p1, p2, lm, state, counts, wl, CL, boxr, g_plan_dbg);
+    case 4: return cudaLaunchKernelEx(&cfg, plan_kernel<4>, tm, v, q, qdt, G, scale, p1, p2, lm, state, counts, wl, CL, boxr, g_plan_dbg);
+    default: return cudaLaunchKernelEx(&cfg, plan_kernel<8>, tm, v, q, qdt, G, scale, p1, p2, lm, state, counts, wl, CL, boxr, g_plan_dbg);
   }
 }
 
@@ -811,6 +899,12 @@ int plan_occupancy(const dp_cache_view& v, int G, int cl) {
 extern "C" int dp_debug_plan_occupancy(const dp_cache_view* v, int G, int cl) {
   if (cl == 0) return dp::plan_cluster_size(*v, G);  // the size launch_plan picks
   return dp::plan_occupancy(*v, G, cl);
+}
+extern "C" int dp_debug_sel_sub(unsigned long long* out) {  // [16][8] stamps inside a select phase
+  return cudaMemcpyFromSymbol(out, dp::g_sel_sub, sizeof(dp::g_sel_sub)) == cudaSuccess ? 0 : 2;
+}
+extern "C" int dp_debug_sel_cycles2(unsigned long long* out) {  // [16][8] first pass (DP_SEL_REPEAT builds)
+  return cudaMemcpyFromSymbol(out, dp::g_sel_ts2, sizeof(dp::g_sel_ts2)) == cudaSuccess ? 0 : 2;
 }
 extern "C" int dp_debug_sel_cycles(unsigned long long* out) {  // [16][8] select phase cycles (plan.cu's copy)
   return cudaMemcpyFromSymbol(out, dp::g_sel_ts, sizeof(dp::g_sel_ts)) == cudaSuccess ? 0 : 2;

@@ -24,6 +24,12 @@ constexpr int kCandBins = 8;                // stage-2 candidate bins ranked tog
 
 // phase stamps of the first 16 CTAs' selections (profiling builds only, -DDP_PROFILE)
 static __device__ unsigned long long g_sel_ts[16][8];
+static __device__ unsigned long long g_sel_sub[16][8];  // finer stamps inside a phase (profiling builds)
+__device__ __forceinline__ void sel_sub(int ev) {
+#ifdef DP_PROFILE
+  if (blockIdx.x < 16 && threadIdx.x == 0) g_sel_sub[blockIdx.x][ev] = clock64();
+#endif
+}
 __device__ __forceinline__ void sel_stamp(int ev) {
 #ifdef DP_PROFILE
   if (blockIdx.x < 16 && threadIdx.x == 0) {
@@ -442,4 +448,264 @@ __device__ void select_two_stage(const int K, const double M, const double* lmal
   n2_out = K > 0 ? n2 : 0;
 }
 
+// ---------------------------------------------------------------------------
+// select_fast: the same two-stage top-p with a short dependent chain (7 CTA
+// barriers, no single-thread loops) and little shared-memory traffic per
+// warp (on B200 the shared-memory pipe, not latency, bounds a 512-thread
+// CTA doing small per-element steps).  Every element keeps its bin, mass and
+// sorted position in registers (kEPT slots per thread, K <= kEPT * kT); the
+// per-bin (mass, count) histogram is scanned once into exclusive prefixes
+// (pm, pc: in place over the histogram), which gives
+//   * the stage-1 boundary bin b1 (the unique bin with excl < p1 T <= incl),
+//   * the bins that can hold the stage-2 cut without knowing the exact
+//     stage-1 cut: p2 * at1 lies in (p2 * before1, p2 * (before1 + mass b1)],
+//     so only the bins whose (excl, incl] meets that range (usually one) and
+//     b1 itself need an exact order -- every other element's state follows
+//     from its bin alone,
+//   * each of those candidates' slot in the global sorted order: pc[b] + its
+//     rank inside bin b (log-mass desc, id asc), and its exclusive cumulative
+//     mass pm[b] + the masses ranked ahead of it.
+// Both cuts are then found by the unique candidate whose (excl, incl] holds
+// the threshold: no scan over the sorted order.  Cumulative masses are
+// 2^-38 fixed-point integers (exact, order-independent sums); a cluster
+// whose mass rounds to zero sits past the stage-1 cut unless p1 >= 1 (then
+// everything is kept, as the reference's clamp does).
+// ---------------------------------------------------------------------------
+constexpr double kFixF = 274877906944.0;  // 2^38
+
+struct SelFastShared {
+  unsigned long long wm[33];  // warp totals of the bin scan (mass) -> exclusive prefixes, [32] = total
+  int wc[33];                 // (count)
+  unsigned long long before1, mass1, at1;
+  int b1, n1, n2, pad;
+};
+
+// zero the histogram (hm: [2 NB] mass halves, hc: [NB + 1] counts) and the
+// shared results; every thread, early, followed by a barrier before use
+template <int kT, int NB>
+__device__ __forceinline__ void select_fast_zero(unsigned* hm, int* hc, SelFastShared* S) {
+  for (int j = threadIdx.x; j < 2 * NB; j += kT) hm[j] = 0u;
+  for (int j = threadIdx.x; j <= NB; j += kT) hc[j] = 0;
+  if (threadIdx.x == 0) {
+    S->b1 = NB;
+    S->n1 = 0;
+    S->n2 = 0;
+    S->at1 = 0ull;
+  }
+}
+
+// lmall [K] log-masses, M their max.  Scratch (shared): um [K] u64, hm
+// [2 NB] u32 (zeroed), hc [NB + 1] int (zeroed), cur [NB] int, clist [K] int.
+// Writes stown[i] (2 exact / 1 approx / 0 dropped).  Every thread calls it.
+template <int kT, int NB, int kEPT>
+__device__ void select_fast(const int K, const double M, const double* lmall, const double p1, const double p2,
+                            unsigned long long* um, unsigned* hm, int* hc, int* cur, int* clist, uint8_t* stown,
+                            SelFastShared* S, int& n1_out, int& n2_out) {
+  static_assert(NB % kT == 0, "bins per thread");
+  constexpr int kBPT = NB / kT;
+  constexpr int kW = kT / 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  unsigned* hmh = hm;       // high bits (u >> 20) per bin
+  unsigned* hml = hm + NB;  // low 20 bits per bin
+  unsigned long long* pm = reinterpret_cast<unsigned long long*>(hm);  // after the scan: exclusive mass prefix
+  int* pc = hc;                                                         // after the scan: exclusive count prefix
+  int eb[kEPT];
+  unsigned long long eu[kEPT];
+  sel_stamp(0);
+  // (1) masses, bins, histogram
+#pragma unroll
+  for (int s = 0; s < kEPT; ++s) {
+    eb[s] = NB;
+    eu[s] = 0ull;
+    if (s * kT >= K) break;
+    const int i = tid + s * kT;
+    if (i < K) {
+      const float xf = M == -CUDART_INF ? CUDART_INF_F : (float)(M - lmall[i]);  // >= 0 (+inf: no mass)
+      const unsigned long long u = __float2ull_rn(__expf(-xf) * (float)kFixF);
+      int b = (int)(xf * kBinScale);
+      b = b < 0 ? 0 : (b >= NB ? NB - 1 : b);
+      um[i] = u;
+      eb[s] = b;
+      eu[s] = u;
+      if (u) {  // native 32-bit shared atomics (a 64-bit add is a CAS loop)
+        atomicAdd(&hmh[b], (unsigned)(u >> 20));
+        atomicAdd(&hml[b], (unsigned)(u & 0xFFFFFu));
+        atomicAdd(&hc[b], 1);
+      }
+    }
+  }
+  __syncthreads();
+  sel_stamp(1);
+  // (2) exclusive bin prefixes, total, the stage-1 boundary bin
+  unsigned long long bm[kBPT], mloc = 0ull;
+  int bc[kBPT], cloc = 0;
+#pragma unroll
+  for (int j = 0; j < kBPT; ++j) {
+    const int b = tid * kBPT + j;
+    bm[j] = ((unsigned long long)hmh[b] << 20) + hml[b];
+    bc[j] = hc[b];
+    mloc += bm[j];
+    cloc += bc[j];
+  }
+  sel_sub(0);
+  unsigned long long mi = mloc;
+  int ci = cloc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long tm = __shfl_up_sync(0xffffffffu, mi, o);
+    const int tc = __shfl_up_sync(0xffffffffu, ci, o);
+    if (lane >= o) {
+      mi += tm;
+      ci += tc;
+    }
+  }
+  sel_sub(1);
+  if (lane == 31) {
+    S->wm[warp] = mi;
+    S->wc[warp] = ci;
+  }
+  __syncthreads();  // (every histogram read is done: the prefixes below overwrite it in place)
+  sel_sub(2);
+  if (warp == 0) {  // exclusive prefix of the warp totals
+    const unsigned long long w = lane < kW ? S->wm[lane] : 0ull;
+    const int wc = lane < kW ? S->wc[lane] : 0;
+    unsigned long long wi = w;
+    int wci = wc;
+#pragma unroll
+    for (int o = 1; o < kW; o <<= 1) {
+      const unsigned long long tm = __shfl_up_sync(0xffffffffu, wi, o);
+      const int tc = __shfl_up_sync(0xffffffffu, wci, o);
+      if (lane >= o) {
+        wi += tm;
+        wci += tc;
+      }
+    }
+    if (lane < kW) {
+      S->wm[lane] = wi - w;
+      S->wc[lane] = wci - wc;
+    }
+    if (lane == kW - 1) {
+      S->wm[32] = wi;
+      S->wc[32] = wci;
+    }
+  }
+  __syncthreads();
+  sel_sub(3);
+  const unsigned long long T = S->wm[32];
+  unsigned long long mex = S->wm[warp] + mi - mloc;
+  int cex = S->wc[warp] + ci - cloc;
+  const double thr1 = p1 * (double)T;
+#pragma unroll
+  for (int j = 0; j < kBPT; ++j) {
+    const int b = tid * kBPT + j;
+    const unsigned long long inc = mex + bm[j];
+    if (bm[j] && (double)mex < thr1 && thr1 <= (double)inc) {  // the unique crossing bin
+      S->b1 = b;
+      S->before1 = mex;
+      S->mass1 = bm[j];
+    }
+    pm[b] = mex;
+    pc[b] = cex;
+    cur[b] = 0;
+    mex = inc;
+    cex += bc[j];
+  }
+  if (tid == kT - 1) pc[NB] = S->wc[32];
+  sel_sub(4);
+  __syncthreads();
+  sel_stamp(2);
+  const int b1 = S->b1;
+  if (T == 0ull || b1 >= NB) {  // no mass at all (a non-finite query)
+    const uint8_t st = p1 >= 1.0 ? (p2 >= 1.0 ? 2 : 1) : 0;
+    for (int i = tid; i < K; i += kT) stown[i] = st;
+    n1_out = p1 >= 1.0 ? K : 0;
+    n2_out = p1 >= 1.0 && p2 >= 1.0 ? K : 0;
+    __syncthreads();
+    return;
+  }
+  // (3) candidates: b1 and the bins whose (excl, incl] meets (tlo, thi]
+  const double tlo = p2 * (double)S->before1, thi = p2 * (double)(S->before1 + S->mass1);
+  int cls[kEPT];  // 0 exact by bin, 1 approx by bin, 2 dropped by bin, 3 candidate
+#pragma unroll
+  for (int s = 0; s < kEPT; ++s) {
+    cls[s] = 2;
+    if (s * kT >= K) break;
+    const int b = eb[s];
+    if (eu[s] && b <= b1) {
+      const unsigned long long inc = b + 1 < NB ? pm[b + 1] : T;
+      if (b == b1 || ((double)inc >= tlo && (double)pm[b] < thi)) {
+        cls[s] = 3;
+        clist[pc[b] + atomicAdd(&cur[b], 1)] = tid + s * kT;
+      } else {
+        cls[s] = (double)inc < tlo ? 0 : 1;
+      }
+    }
+  }
+  __syncthreads();
+  sel_stamp(3);
+  // (4) rank inside the bin -> sorted position and exclusive cumulative mass;
+  //     the stage-1 crossing element
+  int pos[kEPT];
+  unsigned long long ex[kEPT];
+#pragma unroll
+  for (int s = 0; s < kEPT; ++s) {
+    pos[s] = 0;
+    ex[s] = 0ull;
+    if (s * kT >= K) break;
+    if (cls[s] == 3) {
+      const int ia = tid + s * kT, b = eb[s];
+      const double la = lmall[ia];
+      const int j0 = pc[b], j1 = pc[b + 1];
+      int rk = 0;
+      unsigned long long pre = 0ull;
+#pragma unroll 4
+      for (int j = j0; j < j1; ++j) {
+        const int ij = clist[j];
+        const double lj = lmall[ij];
+        const bool ahead = lj > la || (lj == la && ij < ia);
+        rk += ahead;
+        pre += ahead ? um[ij] : 0ull;
+      }
+      pos[s] = j0 + rk;
+      ex[s] = pm[b] + pre;
+      const unsigned long long inc = ex[s] + eu[s];
+      if ((double)ex[s] < thr1 && thr1 <= (double)inc) {
+        S->n1 = pos[s] + 1;
+        S->at1 = inc;
+      }
+    }
+  }
+  __syncthreads();
+  sel_stamp(4);
+  // (5) the stage-2 crossing element (p2 of the retained mass, engine.py:191)
+  const int n1 = p1 >= 1.0 ? K : S->n1;
+  const double thr2 = p2 * (double)S->at1;
+#pragma unroll
+  for (int s = 0; s < kEPT; ++s) {
+    if (s * kT >= K) break;
+    if (cls[s] == 3 && (double)ex[s] < thr2 && thr2 <= (double)(ex[s] + eu[s])) S->n2 = pos[s] + 1;
+  }
+  __syncthreads();
+  sel_stamp(5);
+  const int n2 = p1 >= 1.0 && p2 >= 1.0 ? K : S->n2;
+  // (6) states: candidates by position; the others by bin; zero-mass ones
+  //     past every cut
+  const uint8_t zst = p1 >= 1.0 ? (p2 >= 1.0 ? 2 : 1) : 0;
+#pragma unroll
+  for (int s = 0; s < kEPT; ++s) {
+    if (s * kT >= K) break;
+    const int i = tid + s * kT;
+    if (i < K) {
+      uint8_t st;
+      if (!eu[s]) st = zst;
+      else if (cls[s] == 3) st = pos[s] < n2 ? 2 : (pos[s] < n1 ? 1 : 0);
+      else st = cls[s] == 0 ? 2 : (cls[s] == 1 ? 1 : 0);
+      stown[i] = st;
+    }
+  }
+  __syncthreads();
+  sel_stamp(6);
+  n1_out = n1;
+  n2_out = n2;
+}
 }  // namespace dp

@@ -48,8 +48,21 @@ for r in range(min(CL, 16)):
 sb = (ctypes.c_ulonglong * 128)()
 lib.dp_debug_sel_cycles(ctypes.cast(sb, ctypes.c_void_p))
 s = np.array(sb[:], dtype=np.float64).reshape(16, 8)
-sn = ["hist", "scan", "b1", "cmpct", "rank", "cut1", "states"]
+sn = ["hist", "scan", "cand", "rank", "cut2", "states"]
 print("select phases of the owner CTAs (us): " + " ".join(f"{x:>6s}" for x in sn))
 for r in range(G):
-    d = np.diff(s[r]) / 1965
+    d = np.diff(s[r][:7]) / 1965
     print(f"{r:4d} " + " ".join(f"{x:6.2f}" for x in d))
+if os.environ.get("DP_EXTRA_FLAGS", "").find("DP_SEL_REPEAT") >= 0:
+    lib.dp_debug_sel_cycles2(ctypes.cast(sb, ctypes.c_void_p))
+    s = np.array(sb[:], dtype=np.float64).reshape(16, 8)
+    print("first (cold) pass of the repeated selection (us):")
+    for r in range(G):
+        d = np.diff(s[r][:7]) / 1965
+        print(f"{r:4d} " + " ".join(f"{x:6.2f}" for x in d) + f"  total {(s[r,7]-s[r,0])/1965:6.2f}")
+sb2 = (ctypes.c_ulonglong * 128)()
+lib.dp_debug_sel_sub(ctypes.cast(sb2, ctypes.c_void_p))
+s2 = np.array(sb2[:], dtype=np.float64).reshape(16, 8)
+print("select phase-2 sub-steps (us from the phase start): loads, warp scan, sync1, warp0 scan+sync2, bins")
+for r in range(G):
+    print(f"{r:4d} " + " ".join(f"{(x - s[r][1]) / 1965:6.2f}" for x in s2[r][:5]))
