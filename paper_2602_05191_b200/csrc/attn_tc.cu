@@ -634,11 +634,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
       if (ap_ready) ap_fold();
       if (ap_k < ap_n) ap_issue(bh);
     }
-    if (seg_end) flush(bh, reinterpret_cast<float*>(Ks));  // this stage's K buffer is the scratch
+    if (seg_end && !(dbg & 2)) flush(bh, reinterpret_cast<float*>(Ks));  // this stage's K buffer is the scratch
     __syncwarp();
     if (lane == 0) mbar_arrive(smem_u32(&empty_bar[s]));  // stage s free for the producer
   }
   astamp(3);
+  if (dbg & 10) return;  // timing experiments: no flush / merge (2), no counters / merge (8)
   if (tid == 0) {  // profiling: rows and head segments of this CTA
     astamp_at(7, (unsigned long long)(r1 - r0));
     astamp_at(8, (unsigned long long)nflushed);
@@ -648,14 +649,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
     // release: this CTA's reductions (observed through the barrier) are visible
     // at gpu scope before its count; acquire: the last CTA's merge reads, ordered
     // after the barrier below, see every other CTA's reductions
-    for (int i = 0; i < nflushed; ++i)
-      if (atom_add_acq_rel(&wl.counters[flushed[i]], 1) == head_parts(flushed[i]) - 1)
-        s_merge[s_nmerge++] = flushed[i];
     // heads with no rows at all (no sink/window, nothing exact): merged by CTA bh % grid
     if (!kDense)
       for (int bh = me; bh < BH; bh += grid)
-        if (rp[bh + 1] == rp[bh]) s_merge[s_nmerge++] = bh;
+        if (rp[bh + 1] == rp[bh]) s_merge[atomicAdd(&s_nmerge, 1)] = bh;
   }
+  if (tid < nflushed)  // the (<= 2) completion counters in parallel, one round trip
+    if (atom_add_acq_rel(&wl.counters[flushed[tid]], 1) == head_parts(flushed[tid]) - 1)
+      s_merge[atomicAdd(&s_nmerge, 1)] = flushed[tid];
   consumers_sync();
   astamp(4);
 
@@ -664,7 +665,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
   // (approximated clusters: logit = log-mass, value = value mean).  One
   // round trip: warp w streams partials w, w+8, ... with an online rescale,
   // then the 8 warp states are combined in shared memory.
-  const int nm = s_nmerge;
+  const int nm = (dbg & 4) ? 0 : s_nmerge;  // (4: timing experiment, no merge)
   if (nm == 0) {
     astamp(5);
     return;
@@ -673,25 +674,29 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
   float* ored = reinterpret_cast<float*>(KV);  // [warps][8 heads][d]
   if (tid < nm) wl.counters[s_merge[tid]] = 0;  // self-reset for the next launch
   if (!kDense) {
-    // sparse heads with rows: out = o / l from the accumulators (one round
-    // trip), which are zeroed again for the next launch
-    const int nq = nm * G;
+    // sparse heads with rows: out = o / l from the accumulators, one float4
+    // per thread (a single L2 round trip); each thread clears the float4 it
+    // read, the shared l words are cleared after the barrier below
+    const int nq = nm * G, d4 = d >> 2;
 #pragma unroll 1
-    for (int i = tid; i < nq * d; i += kConsumers) {
-      const int qi = i / d, c = i - qi * d, mi = qi / G, g = qi - mi * G, bh = s_merge[mi];
+    for (int i = tid; i < nq * d4; i += kConsumers) {
+      const int qi = i / d4, c = (i - qi * d4) * 4, mi = qi / G, g = qi - mi * G, bh = s_merge[mi];
       if (rp[bh + 1] == rp[bh]) continue;  // no rows: slow path below
       float* ac = wl.acc + ((size_t)bh * G + g) * acc_stride(d);
-      const float o_ = __ldcg(ac + c), l_ = __ldcg(ac + d);
-      out[((size_t)bh * G + g) * d + c] = l_ > 0.f ? o_ / l_ : 0.f;
+      const float4 o4 = __ldcg(reinterpret_cast<const float4*>(ac + c));
+      const float l_ = __ldcg(ac + d);
+      const float rl = l_ > 0.f ? 1.f / l_ : 0.f;
+      *reinterpret_cast<float4*>(ac + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+      *reinterpret_cast<float4*>(out + ((size_t)bh * G + g) * d + c) =
+          make_float4(o4.x * rl, o4.y * rl, o4.z * rl, o4.w * rl);
       if (c == 0)
         lse[(size_t)bh * G + g] =
             l_ > 0.f ? __ldcg(&wl.refm[(size_t)bh * G + g]) * 0.69314718055994531f + __logf(l_) : -INFINITY;
     }
-    consumers_sync();  // every accumulator read before any is cleared
-#pragma unroll 1
-    for (int i = tid; i < nq * (d + 1); i += kConsumers) {
-      const int qi = i / (d + 1), c = i - qi * (d + 1), mi = qi / G, g = qi - mi * G;
-      wl.acc[((size_t)s_merge[mi] * G + g) * acc_stride(d) + c] = 0.f;
+    consumers_sync();  // every l read before it is cleared
+    for (int i = tid; i < nq; i += kConsumers) {
+      const int mi = i / G, g = i - mi * G;
+      wl.acc[((size_t)s_merge[mi] * G + g) * acc_stride(d) + d] = 0.f;
     }
     // keep only the row-less heads for the slow path
     consumers_sync();

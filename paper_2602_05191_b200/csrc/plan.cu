@@ -572,45 +572,41 @@ __global__ void __launch_bounds__(kPT, 1)
   stamp(r, 6);
   if (dbg & 4) return;  // timing experiment: no work lists
 
-  // ---------------- P3: union counts + approx partial of my slice --------
-  int e_rows = 0, e_cl = 0, a_cl = 0;
+  // ---------------- P3: union rows of my slice ----------------------------
+  // Slice-local exclusive offsets (rows; approx | exact << 16 cluster counts)
+  // are scanned BEFORE the count exchange, so only the slice bases remain
+  // after it.  Scratch: the P1/P2 region (tiles / selection arrays), free now.
+  int* s_ro = reinterpret_cast<int*>(smem + L.cs);   // [per] local row offset
+  int* s_ao = s_ro + L.per;                          // [per] local approx offset
+  int t_rows = 0, t_pk = 0;
 #pragma unroll 1
-  for (int i = tid; i < nloc; i += kPT) {
-    int me = 0, ma = 0;
+  for (int i0 = 0; i0 < nloc; i0 += kPT) {
+    const int i = i0 + tid;
+    int me = 0, ma = 0, len = 0;
+    if (i < nloc) {
 #pragma unroll 1
-    for (int g = 0; g < G; ++g) {
-      const uint8_t s = stl[g * L.per + i];
-      me |= (s == 2) << g;
-      ma |= (s == 1) << g;
+      for (int g = 0; g < G; ++g) {
+        const uint8_t st = stl[g * L.per + i];
+        me |= (st == 2) << g;
+        ma |= (st == 1) << g;
+      }
+      len = me ? offs[i + 1] - offs[i] : 0;
     }
-    if (me) {
-      e_rows += offs[i + 1] - offs[i];
-      e_cl += 1;
+    unsigned long long ro64, trr64;
+    int pk, tpk;
+    scan_pair<kPT>((unsigned long long)len, (ma != 0) | ((me != 0) << 16), s_redu, s_redi, ro64, pk, trr64, tpk);
+    if (i < nloc) {
+      s_ro[i] = t_rows + (int)ro64;
+      s_ao[i] = (t_pk & 0xFFFF) + (pk & 0xFFFF);
     }
-    a_cl += ma != 0;
+    t_rows += (int)trr64;
+    t_pk += tpk;
+    __syncthreads();  // s_redu / s_redi reuse
   }
-  {  // (rows, exact clusters, approx clusters) of my slice -> every CTA
-    const int v0 = warp_sum(e_rows), v1 = warp_sum(e_cl), v2 = warp_sum(a_cl);
-    if (lane == 0) {
-      s_redi[warp * 4 + 0] = v0;
-      s_redi[warp * 4 + 1] = v1;
-      s_redi[warp * 4 + 2] = v2;
-    }
-  }
-  __syncthreads();
   stamp(r, 15);
-  if (tid < CL) {
-    int t0 = 0, t1 = 0, t2 = 0;
-#pragma unroll
-    for (int w = 0; w < kPW; ++w) {  // independent loads (unrolled): no serial shared-load chain
-      t0 += s_redi[w * 4 + 0];
-      t1 += s_redi[w * 4 + 1];
-      t2 += s_redi[w * 4 + 2];
-    }
-    push_v4(&s_cnt[r][0], tid, t0, t1, t2, 0, &s_mb[2]);
-  }
+  if (tid < CL) push_v4(&s_cnt[r][0], tid, t_rows, t_pk >> 16, t_pk & 0xFFFF, 0, &s_mb[2]);
   stamp(r, 7);
-  mb_wait0(&s_mb[2]);  // (C) every slice's counts are in place; no remote access after this
+  if (!(dbg & 16)) mb_wait0(&s_mb[2]);  // (C) every slice's counts are in place; no remote access after this
   stamp(r, 8);
 
   // ---------------- P4: work lists -----------------------------------------
@@ -629,9 +625,7 @@ __global__ void __launch_bounds__(kPT, 1)
     tot_a += c2;
   }
   stamp(r, 16);
-  // log-masses (the attention kernel reads the approximated clusters' ones)
-  // and the debug states of my slice, kept off the barrier-release paths above
-  if (state_out)
+  if (state_out)  // debug states of my slice
 #pragma unroll 1
     for (int i = tid; i < G * nloc; i += kPT) {
       const int g = i / nloc, k = i - g * nloc;
@@ -643,25 +637,21 @@ __global__ void __launch_bounds__(kPT, 1)
 #pragma unroll 1
   for (int i0 = 0; i0 < nloc; i0 += kPT) {
     const int i = i0 + tid;
-    int me = 0, ma = 0, len = 0, st0 = 0;
+    int me = 0, ma = 0, len = 0, st0 = 0, ro = 0;
     if (i < nloc) {
 #pragma unroll 1
       for (int g = 0; g < G; ++g) {
-        const uint8_t s = stl[g * L.per + i];
-        me |= (s == 2) << g;
-        ma |= (s == 1) << g;
+        const uint8_t st = stl[g * L.per + i];
+        me |= (st == 2) << g;
+        ma |= (st == 1) << g;
       }
       st0 = offs[i];
       len = me ? offs[i + 1] - st0 : 0;
+      ro = row_base + s_ro[i];
+      if (ma) apx[apx_base + s_ao[i]] = make_int2(k0 + i, ma);
     }
-    unsigned long long ro64, trr64;
-    int ao, taa;
-    scan_pair<kPT>((unsigned long long)len, ma != 0 ? 1 : 0, s_redu, s_redi, ro64, ao, trr64, taa);
-    const int ro = (int)ro64 + row_base;
-    if (i0 == 0) stamp(r, 18);
-    if (ma) apx[ao + apx_base] = make_int2(k0 + i, ma);
     // warp-cooperative expansion of the warp's 32 clusters: lanes write consecutive rows
-    unsigned todo = __ballot_sync(0xffffffffu, len > 0);
+    unsigned todo = __ballot_sync(0xffffffffu, len > 0 && !(dbg & 8));
 #pragma unroll 1
     while (todo) {
       const int t = __ffs(todo) - 1;
@@ -673,11 +663,8 @@ __global__ void __launch_bounds__(kPT, 1)
 #pragma unroll 1
       for (int x = lane; x < tl; x += 32) rowidx[to + x] = tag | (unsigned)(ts + x);
     }
-    row_base += (int)trr64;
-    apx_base += taa;
-    if (i0 == 0) stamp(r, 19);
-    __syncthreads();  // s_redu / s_redi reuse
   }
+  stamp(r, 19);
   if (r == 0) {
     if (tid < G)  // reference max of the attention accumulators: the head's top log-mass (log2 units)
     {

@@ -103,9 +103,7 @@ __device__ __forceinline__ void tma_box(unsigned dst, const CUtensorMap* map, in
       "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(row), "r"(bar), "l"(pol)
       : "memory");
 }
-__device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
-}
+
 
 struct StepLayout {
   int per;  // slice capacity (cap / CL rounded up to 4)

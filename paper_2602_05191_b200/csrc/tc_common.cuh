@@ -86,6 +86,10 @@ __device__ __forceinline__ void bulk_row(unsigned dst, const void* src, unsigned
                : "memory");
 }
 
+__device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {  // bulk L2 prefetch (16-B multiple)
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ void red_add_v4(float* p, float4 v) {  // p 16-B aligned
   asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
                : "memory");

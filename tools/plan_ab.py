@@ -60,8 +60,15 @@ plan()
 attend()
 torch.cuda.synchronize()
 print(f"context {n} G {G}: plan cluster size {lib.dp_debug_plan_occupancy(view, G, 0)}; us per launch in graph")
-for bits, name in ((0, "full plan"), (4, "no work lists"), (2, "no selection"), (6, "no selection, no lists")):
+for bits, name in ((0, "full plan"), (16, "no count-exchange wait"), (8, "no row expansion"), (4, "no work lists"), (2, "no selection"),
+                   (6, "no selection, no lists")):
     lib.dp_debug_set(10, bits)
     print(f"  {name:28s} {timed(lambda: [plan() for _ in range(L)]):7.2f}")
 lib.dp_debug_set(10, 0)
 print(f"  {'plan + attend':28s} {timed(lambda: [(plan(), attend()) for _ in range(L)]):7.2f}")
+for bits, name in ((1, "attend: no math"), (4, "attend: no merge"), (8, "attend: no counters/merge"),
+                   (2, "attend: no flush/merge"), (3, "attend: neither")):
+    lib.dp_debug_set(0, bits)
+    print(f"  plan + {name:28s} {timed(lambda: [(plan(), attend()) for _ in range(L)]):7.2f}")
+lib.dp_debug_set(0, 0)
+print(f"  {'attend alone':28s} {timed(lambda: [attend() for _ in range(L)]):7.2f}")
