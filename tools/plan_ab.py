@@ -72,3 +72,8 @@ for bits, name in ((1, "attend: no math"), (4, "attend: no merge"), (8, "attend:
     print(f"  plan + {name:28s} {timed(lambda: [(plan(), attend()) for _ in range(L)]):7.2f}")
 lib.dp_debug_set(0, 0)
 print(f"  {'attend alone':28s} {timed(lambda: [attend() for _ in range(L)]):7.2f}")
+for cl in (6, 8, 10):
+    lib.dp_debug_set(1, cl)
+    print(f"  CL {cl:2d}: plan {timed(lambda: [plan() for _ in range(L)]):7.2f}  plan + attend "
+          f"{timed(lambda: [(plan(), attend()) for _ in range(L)]):7.2f}")
+lib.dp_debug_set(1, 0)
