@@ -322,6 +322,57 @@ int dp_nearest_centroid(const void* points, int32_t dtype, int32_t n, int32_t d,
                         const double* centroids, int32_t k, int32_t fp64, int32_t* assign,
                         double* sqdist, void* stream);
 
+/* ---------------------------------------------------------------------- */
+/* sequence sharding with the reference's GLOBAL semantics (config 5,     */
+/* >= 512K tokens over P GPUs).  The host layer             */
+/* (paper_2602_05191_b200/seqshard.py) runs the collectives between them. */
+/* ---------------------------------------------------------------------- */
+
+/* One k-means++ step's distance update (clustering.py:45,53) over this
+ * rank's middle points [units, n, d]: dsq = |x - centre|^2 (first != 0) or
+ * min(dsq, |x - centre|^2), fp64; sums[u] = the local sum (fixed order). */
+int dp_kmpp_shard_dsq(const void* points, int32_t dtype, int32_t units, int32_t n, int32_t d, const double* centre,
+                      int32_t first, double* dsq, double* sums, void* stream);
+
+/* The step's pick (clustering.py:49, Generator.choice(p = dsq / total)): with
+ * all_sums [world, units] the all-gathered local sums, the centre is the first
+ * GLOBAL point whose running dsq sum exceeds uniforms[u] * total; pick_in
+ * (nullable) forces a global index per unit (the first centre,
+ * clustering.py:42).  This rank holds global middle indices
+ * [global_base, global_base + n).  centre_out [units, d] fp64 = the row on
+ * the owning rank, zeros elsewhere (an all-reduce sum hands it to every
+ * rank); pick_out [units] = the global index on the owner, -1 elsewhere, -2
+ * when the total mass is zero (the reference then draws rng.integers). */
+int dp_kmpp_shard_pick(const void* points, int32_t dtype, int32_t units, int32_t n, int32_t d, const double* dsq,
+                       const double* all_sums, int32_t world, int32_t rank, const double* uniforms,
+                       const int32_t* pick_in, int64_t global_base, double* centre_out, int32_t* pick_out,
+                       void* stream);
+
+/* Lloyd's local half (clustering.py:100-106): fp64 sums [units, k, d] and
+ * member counts [units, k] of this rank's points per cluster, each cluster's
+ * members added in ascending position order (deterministic; an all-reduce
+ * of [k, d + 1] gives the global means).  assign [units, n] int32. */
+size_t dp_lloyd_shard_workspace_bytes(int32_t units, int32_t n, int32_t k);
+int dp_lloyd_shard_sums(const void* points, int32_t dtype, int32_t units, int32_t n, int32_t d,
+                        const int32_t* assign, int32_t k, double* sums, int64_t* counts, void* workspace,
+                        size_t workspace_bytes, void* stream);
+
+/* Two-stage top-p (engine.py:180-213, selection.py:36-65) over log-mass rows
+ * of ANY length -- the all-gathered per-shard slices of one global cluster
+ * table (K = 32,766 at 1M tokens).  log_mass [rows, ld] fp64, nclusters
+ * [rows] the valid length of each row; state [rows, ld] (2 exact / 1 approx
+ * / 0 dropped), counts [rows, 2] = (|C_p|, |C_exact|).  One CTA per row. */
+size_t dp_select_global_workspace_bytes(int32_t rows, int32_t ld);
+int dp_select_global(const double* log_mass, int32_t rows, int32_t ld, const int32_t* nclusters, double p1,
+                     double p2, uint8_t* state, int32_t* counts, void* workspace, size_t workspace_bytes,
+                     void* stream);
+
+/* The exchange step's merge (engine.py:234-246 across shards): partials
+ * out_parts [parts, rows, d] fp32 with lse_parts [parts, rows] (-inf: empty)
+ * -> out [rows, d], lse [rows]; fp64 weights. */
+int dp_lse_merge(const float* out_parts, const float* lse_parts, int32_t parts, int32_t rows, int32_t d, float* out,
+                 float* lse, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -98,6 +98,18 @@ _SIGS = {
                                    ctypes.c_size_t, _vp]),
     "dp_nearest_centroid": (ctypes.c_int, [_vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _vp,
                                            ctypes.c_int32, ctypes.c_int32, _vp, _vp, _vp]),
+    "dp_kmpp_shard_dsq": (ctypes.c_int, [_vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _vp,
+                                         ctypes.c_int32, _vp, _vp, _vp]),
+    "dp_kmpp_shard_pick": (ctypes.c_int, [_vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _vp,
+                                          _vp, ctypes.c_int32, ctypes.c_int32, _vp, _vp, ctypes.c_int64, _vp, _vp,
+                                          _vp]),
+    "dp_lloyd_shard_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]),
+    "dp_lloyd_shard_sums": (ctypes.c_int, [_vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _vp,
+                                           ctypes.c_int32, _vp, _vp, _vp, ctypes.c_size_t, _vp]),
+    "dp_select_global_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int32, ctypes.c_int32]),
+    "dp_select_global": (ctypes.c_int, [_vp, ctypes.c_int32, ctypes.c_int32, _vp, ctypes.c_double, ctypes.c_double,
+                                        _vp, _vp, _vp, ctypes.c_size_t, _vp]),
+    "dp_lse_merge": (ctypes.c_int, [_vp, _vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _vp, _vp, _vp]),
 }
 
 _lib = None

@@ -259,6 +259,64 @@ int dp_mixed_attention_f64(const dp_cache_view* v, const void* q, int32_t q_dtyp
   return e == cudaSuccess ? DP_OK : cuda_fail(e, "dp_mixed_attention_f64");
 }
 
+/* ---- sequence-sharded Double-P with global semantics (shard.cu) ---- */
+
+int dp_kmpp_shard_dsq(const void* points, int32_t dtype, int32_t units, int32_t n, int32_t d, const double* centre,
+                      int32_t first, double* dsq, double* sums, void* stream) {
+  if (!points || !centre || !dsq || !sums) return fail(DP_ERR_INVALID, "dp_kmpp_shard_dsq: null buffer");
+  if (dtype != DP_F32 && dtype != DP_BF16) return fail(DP_ERR_INVALID, "unknown points dtype");
+  if (units < 1 || n < 1 || d < 1) return fail(DP_ERR_INVALID, "dp_kmpp_shard_dsq: empty shard");
+  cudaError_t e = dp::launch_kmpp_dsq(points, dtype, units, n, d, centre, first, dsq, sums, (cudaStream_t)stream);
+  return e == cudaSuccess ? DP_OK : cuda_fail(e, "dp_kmpp_shard_dsq");
+}
+
+int dp_kmpp_shard_pick(const void* points, int32_t dtype, int32_t units, int32_t n, int32_t d, const double* dsq,
+                       const double* all_sums, int32_t world, int32_t rank, const double* uniforms,
+                       const int32_t* pick_in, int64_t global_base, double* centre_out, int32_t* pick_out,
+                       void* stream) {
+  if (!points || !centre_out || !pick_out) return fail(DP_ERR_INVALID, "dp_kmpp_shard_pick: null buffer");
+  if (!pick_in && (!dsq || !all_sums || !uniforms)) return fail(DP_ERR_INVALID, "dp_kmpp_shard_pick: null buffer");
+  if (world < 1 || rank < 0 || rank >= world) return fail(DP_ERR_INVALID, "rank outside [0, world)");
+  cudaError_t e = dp::launch_kmpp_pick(points, dtype, units, n, d, dsq, all_sums, world, rank, uniforms, pick_in,
+                                       (long long)global_base, centre_out, pick_out, (cudaStream_t)stream);
+  return e == cudaSuccess ? DP_OK : cuda_fail(e, "dp_kmpp_shard_pick");
+}
+
+size_t dp_lloyd_shard_workspace_bytes(int32_t units, int32_t n, int32_t k) { return dp::lloyd_sums_ws_bytes(units, n, k); }
+
+int dp_lloyd_shard_sums(const void* points, int32_t dtype, int32_t units, int32_t n, int32_t d,
+                        const int32_t* assign, int32_t k, double* sums, int64_t* counts, void* workspace,
+                        size_t workspace_bytes, void* stream) {
+  if (!points || !assign || !sums || !counts) return fail(DP_ERR_INVALID, "dp_lloyd_shard_sums: null buffer");
+  if (workspace_bytes < dp::lloyd_sums_ws_bytes(units, n, k)) return fail(DP_ERR_INVALID, "workspace too small");
+  cudaError_t e = dp::launch_lloyd_sums(points, dtype, units, n, d, assign, k, sums,
+                                        reinterpret_cast<long long*>(counts), workspace, (cudaStream_t)stream);
+  return e == cudaSuccess ? DP_OK : cuda_fail(e, "dp_lloyd_shard_sums");
+}
+
+size_t dp_select_global_workspace_bytes(int32_t rows, int32_t ld) { return dp::select_global_ws_bytes(rows, ld); }
+
+int dp_select_global(const double* log_mass, int32_t rows, int32_t ld, const int32_t* nclusters, double p1,
+                     double p2, uint8_t* state, int32_t* counts, void* workspace, size_t workspace_bytes,
+                     void* stream) {
+  int r;
+  if ((r = check_p(p1, "p1")) || (r = check_p(p2, "p2"))) return r;
+  if (!log_mass || !nclusters || !state || !counts) return fail(DP_ERR_INVALID, "dp_select_global: null buffer");
+  if (rows < 1 || ld < 1) return fail(DP_ERR_INVALID, "dp_select_global: empty input");
+  if (workspace_bytes < dp::select_global_ws_bytes(rows, ld)) return fail(DP_ERR_INVALID, "workspace too small");
+  cudaError_t e = dp::launch_select_global(log_mass, rows, ld, nclusters, p1, p2, state, counts, workspace,
+                                           (cudaStream_t)stream);
+  return e == cudaSuccess ? DP_OK : cuda_fail(e, "dp_select_global");
+}
+
+int dp_lse_merge(const float* out_parts, const float* lse_parts, int32_t parts, int32_t rows, int32_t d, float* out,
+                 float* lse, void* stream) {
+  if (!out_parts || !lse_parts || !out || !lse) return fail(DP_ERR_INVALID, "dp_lse_merge: null buffer");
+  if (parts < 1 || rows < 1 || d < 1) return fail(DP_ERR_INVALID, "dp_lse_merge: empty input");
+  cudaError_t e = dp::launch_lse_merge(out_parts, lse_parts, parts, rows, d, out, lse, (cudaStream_t)stream);
+  return e == cudaSuccess ? DP_OK : cuda_fail(e, "dp_lse_merge");
+}
+
 }  // extern "C"
 
 // error helper used by the clustering TU

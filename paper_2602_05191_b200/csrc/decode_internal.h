@@ -104,5 +104,19 @@ cudaError_t launch_mixed_f64(const dp_cache_view& v, const void* q, int qdt, int
                              const uint8_t* state, double* out, double* lse, cudaStream_t st);
 cudaError_t launch_adaptive_budget(const dp_cache_view& v, int G, const double* w, double p, int* budget,
                                    cudaStream_t st);
+// shard.cu: sequence-sharded Double-P with global semantics (config 5)
+cudaError_t launch_kmpp_dsq(const void* pts, int dtype, int units, int n, int d, const double* centre, int first,
+                            double* dsq, double* sums, cudaStream_t st);
+cudaError_t launch_kmpp_pick(const void* pts, int dtype, int units, int n, int d, const double* dsq,
+                             const double* all_sums, int P, int rank, const double* u_draw, const int* pick_in,
+                             long long gbase, double* centre_out, int* pick_out, cudaStream_t st);
+size_t lloyd_sums_ws_bytes(int units, int n, int k);
+cudaError_t launch_lloyd_sums(const void* pts, int dtype, int units, int n, int d, const int* assign, int k,
+                              double* sums, long long* counts, void* ws, cudaStream_t st);
+size_t select_global_ws_bytes(int rows, int ld);
+cudaError_t launch_select_global(const double* lm, int rows, int ld, const int* Ks, double p1, double p2,
+                                 uint8_t* state, int* counts, void* ws, cudaStream_t st);
+cudaError_t launch_lse_merge(const float* out_parts, const float* lse_parts, int P, int rows, int d, float* out,
+                             float* lse, cudaStream_t st);
 
 }  // namespace dp

@@ -1,0 +1,489 @@
+// Sequence-sharded Double-P with the reference's GLOBAL semantics (SURVEY.md
+// section 8e, config 5): the per-rank device pieces.  The host layer
+// (paper_2602_05191_b200/seqshard.py) strings them together with
+// torch.distributed collectives (NCCL over NVLink; gloo in the tests).
+//
+//   * global k-means++ (clustering.py:36-55) over position-sharded points:
+//     kmpp_dsq_kernel folds the newest centre into every local point's
+//     squared distance and reduces the local sum; after an all-gather of the
+//     P local sums, kmpp_pick_kernel finds whether this rank owns the point
+//     where the GLOBAL running sum first exceeds u * total (the reference's
+//     Generator.choice(p = dsq / total) in unnormalised form, the same rule
+//     as the single-GPU seeding kernel) and writes that row; an all-reduce
+//     of the (owner row, zeros elsewhere) buffer hands the centre to all.
+//   * global Lloyd (clustering.py:58-107): nearest-centroid assignment of
+//     the local points (dp_nearest_centroid), then lloyd_sums_kernel -- fp64
+//     per-cluster sums of the local members in ascending position order
+//     (deterministic) -- whose [K, d + 1] results are all-reduced.
+//   * global two-stage top-p (engine.py:180-213) over the all-gathered
+//     per-shard log-mass slices: select_global_kernel, one CTA per q head,
+//     any cluster count (the 1M-token config has K = 32,766): the same
+//     histogram / boundary-candidate algorithm as the fused plan's select
+//     (select.cuh), with per-element data recomputed from the log-masses or
+//     kept in global scratch instead of registers.
+//   * lse_merge_kernel: the exchange step's log-sum-exp merge of the P
+//     partial (out, lse) (engine.py:234-246 across shards).
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+#include "common.cuh"
+#include "decode_internal.h"
+#include "select.cuh"
+
+namespace dp {
+
+// ---------------------------------------------------------------------------
+// global k-means++
+// ---------------------------------------------------------------------------
+constexpr int kKT = 256;
+
+// dsq[u, i] = |x_i - c_u|^2 (first) or min(dsq, |x_i - c_u|^2); sums[u] =
+// sum_i dsq[u, i] in a fixed association order (thread segments, then a
+// fixed tree), fp64 throughout (clustering.py:45,53)
+__global__ void __launch_bounds__(kKT) kmpp_dsq_kernel(const void* __restrict__ pts, int dtype, int n, int d,
+                                                      const double* __restrict__ centre, int first,
+                                                      double* __restrict__ dsq, double* __restrict__ sums) {
+  const int u = blockIdx.x, tid = threadIdx.x;
+  extern __shared__ double s_c[];  // [d] the centre
+  __shared__ double s_red[kKT];
+  for (int j = tid; j < d; j += kKT) s_c[j] = centre[(size_t)u * d + j];
+  __syncthreads();
+  const int per = (n + kKT - 1) / kKT, i0 = min(n, tid * per), i1 = min(n, i0 + per);
+  double acc = 0.0;
+  for (int i = i0; i < i1; ++i) {
+    const size_t base = ((size_t)u * n + i) * d;
+    double s = 0.0;
+    for (int j = 0; j < d; ++j) {
+      const double x = load_elem_d(pts, dtype, base + j) - s_c[j];
+      s += x * x;
+    }
+    double* p = dsq + (size_t)u * n + i;
+    const double v = first ? s : fmin(*p, s);
+    *p = v;
+    acc += v;
+  }
+  s_red[tid] = acc;
+  __syncthreads();
+  for (int w = kKT / 2; w > 0; w >>= 1) {
+    if (tid < w) s_red[tid] += s_red[tid + w];
+    __syncthreads();
+  }
+  if (tid == 0) sums[u] = s_red[0];
+}
+
+// Centre pick of one step.  all_sums [P, U] (rank order); u_draw [U]; an
+// explicit global index (pick_in[u] >= 0: the first centre, or an
+// rng.integers draw once the mass is zero) takes precedence.  This rank owns
+// global middle indices [gbase, gbase + n).  Writes centre_out[u] (the row
+// in fp64 on the owner, zeros elsewhere) and pick_out[u] (global index on
+// the owner, -1 elsewhere).  One CTA per unit.
+__global__ void __launch_bounds__(kKT) kmpp_pick_kernel(const void* __restrict__ pts, int dtype, int n, int d,
+                                                       const double* __restrict__ dsq,
+                                                       const double* __restrict__ all_sums, int P, int rank,
+                                                       const double* __restrict__ u_draw,
+                                                       const int* __restrict__ pick_in, long long gbase,
+                                                       double* __restrict__ centre_out, int* __restrict__ pick_out) {
+  const int u = blockIdx.x, U = gridDim.x, tid = threadIdx.x;
+  __shared__ double s_part[kKT];
+  __shared__ int s_pick;
+  if (tid == 0) s_pick = -1;
+  long long gpick = pick_in ? pick_in[u] : -1;
+  double target = 0.0, before = 0.0, total = 0.0;
+  if (gpick < 0) {
+    for (int r = 0; r < P; ++r) {
+      const double s = all_sums[(size_t)r * U + u];
+      if (r < rank) before += s;
+      total += s;
+    }
+    if (!(total > 0.0)) gpick = -2;  // degenerate: the host replays rng.integers (pick_in)
+    target = u_draw[u] * total;
+  }
+  const bool mine_explicit = gpick >= gbase && gpick < gbase + n;
+  const double mysum = gpick == -1 ? all_sums[(size_t)rank * U + u] : 0.0;
+  const bool owner = gpick >= 0 ? mine_explicit
+                                : (gpick == -1 && before <= target && target < before + mysum);
+  __syncthreads();
+  if (owner) {
+    if (gpick >= 0) {
+      if (tid == 0) s_pick = (int)(gpick - gbase);
+    } else {
+      // first local index whose running sum exceeds target - before: thread
+      // segments, their sums scanned in a fixed order
+      const double t = target - before;
+      const int per = (n + kKT - 1) / kKT, i0 = min(n, tid * per), i1 = min(n, i0 + per);
+      double acc = 0.0;
+      for (int i = i0; i < i1; ++i) acc += dsq[(size_t)u * n + i];
+      s_part[tid] = acc;
+      __syncthreads();
+      if (tid == 0) {
+        double run = 0.0;
+        int seg = kKT - 1;
+        for (int s = 0; s < kKT; ++s) {
+          if (run + s_part[s] > t) {
+            seg = s;
+            break;
+          }
+          run += s_part[s];
+        }
+        const int j0 = min(n, seg * per), j1 = min(n, j0 + per);
+        int pick = j1 > j0 ? j1 - 1 : n - 1;
+        for (int i = j0; i < j1; ++i) {
+          run += dsq[(size_t)u * n + i];
+          if (run > t) {
+            pick = i;
+            break;
+          }
+        }
+        s_pick = pick;
+      }
+    }
+  }
+  __syncthreads();
+  const int lp = s_pick;
+  for (int j = tid; j < d; j += kKT)
+    centre_out[(size_t)u * d + j] = lp >= 0 ? load_elem_d(pts, dtype, ((size_t)u * n + lp) * d + j) : 0.0;
+  if (tid == 0) pick_out[u] = lp >= 0 ? (int)(gbase + lp) : (gpick == -2 ? -2 : -1);
+}
+
+// ---------------------------------------------------------------------------
+// global Lloyd: local per-cluster sums in ascending position order
+// ---------------------------------------------------------------------------
+// One CTA per unit: counting sort of the local points by cluster (stable:
+// ascending local index), then warp w sums clusters w, w + 8, ... member by
+// member (lane j covers dims j, j + 32, ...).  sums [U, k, d] fp64, counts
+// [U, k] int64 (a point with assign < 0 is skipped).  Scratch: cnt/cur [U, k]
+// int, order [U, n] int.
+constexpr int kLT = 256;
+__global__ void __launch_bounds__(kLT) lloyd_sums_kernel(const void* __restrict__ pts, int dtype, int n, int d,
+                                                        const int* __restrict__ assign, int k,
+                                                        double* __restrict__ sums, long long* __restrict__ counts,
+                                                        int* __restrict__ cnt, int* __restrict__ order) {
+  const int u = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int* a = assign + (size_t)u * n;
+  int* c = cnt + (size_t)u * k;
+  int* o = order + (size_t)u * n;
+  for (int j = tid; j < k; j += kLT) c[j] = 0;
+  __syncthreads();
+  for (int i = tid; i < n; i += kLT)
+    if (a[i] >= 0 && a[i] < k) atomicAdd(&c[a[i]], 1);
+  __syncthreads();
+  if (tid == 0) {  // exclusive offsets (serial: prefill-only, k is small per unit)
+    int run = 0;
+    for (int j = 0; j < k; ++j) {
+      const int x = c[j];
+      c[j] = run;
+      run += x;
+    }
+  }
+  __syncthreads();
+  if (tid == 0)  // stable placement (ascending index inside each cluster)
+    for (int i = 0; i < n; ++i)
+      if (a[i] >= 0 && a[i] < k) o[c[a[i]]++] = i;
+  __syncthreads();
+  for (int j = warp; j < k; j += kLT / 32) {
+    const int e = c[j], s = j == 0 ? 0 : c[j - 1];  // c now holds inclusive ends
+    for (int dd = lane; dd < d; dd += 32) {
+      double acc = 0.0;
+      for (int m = s; m < e; ++m) acc += load_elem_d(pts, dtype, ((size_t)u * n + o[m]) * d + dd);
+      sums[((size_t)u * k + j) * d + dd] = acc;
+    }
+    if (lane == 0) counts[(size_t)u * k + j] = e - s;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// global two-stage top-p over a log-mass row of any length
+// ---------------------------------------------------------------------------
+constexpr int kGT = 1024;
+constexpr int kGB = 2048;
+
+__device__ __forceinline__ double gsel_sanitise(double x) { return x != x ? -CUDART_INF : fmin(x, 1.7976931348623157e308); }
+
+// u = exp(lm - M) as a 2^-38 fixed-point integer and its 1/32-nat bin
+__device__ __forceinline__ void gsel_elem(double M, double lm, unsigned long long& u, int& b) {
+  const float xf = M == -CUDART_INF ? CUDART_INF_F : (float)(M - lm);
+  u = __float2ull_rn(__expf(-xf) * (float)kFixF);
+  b = (int)(xf * kBinScale);
+  b = b < 0 ? 0 : (b >= kGB ? kGB - 1 : b);
+}
+
+// rows: one per (sequence, q head); K[row] clusters at lm + row * ld.
+// Scratch per row (ld entries each): pos int, ex u64, cand int.
+__global__ void __launch_bounds__(kGT, 1) select_global_kernel(const double* __restrict__ lm_all, int ld,
+                                                              const int* __restrict__ Ks, double p1, double p2,
+                                                              uint8_t* __restrict__ state_all,
+                                                              int* __restrict__ counts, int* __restrict__ pos_ws,
+                                                              unsigned long long* __restrict__ ex_ws,
+                                                              int* __restrict__ cand_ws) {
+  const int row = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int K = Ks[row];
+  const double* lm = lm_all + (size_t)row * ld;
+  uint8_t* state = state_all + (size_t)row * ld;
+  int* pos = pos_ws + (size_t)row * ld;
+  unsigned long long* ex = ex_ws + (size_t)row * ld;
+  int* cand = cand_ws + (size_t)row * ld;
+  __shared__ unsigned s_hh[kGB], s_hl[kGB];
+  __shared__ int s_hc[kGB + 1];
+  unsigned* s_cur = s_hh;  // after the bin scan: per-bin cursors of the candidate placement
+  __shared__ unsigned long long s_pm[kGB];
+  __shared__ unsigned long long s_wm[33];
+  __shared__ int s_wc[33];
+  __shared__ double s_red[32];
+  __shared__ unsigned long long s_before1, s_mass1, s_at1;
+  __shared__ int s_b1, s_n1, s_n2;
+  for (int j = tid; j < kGB; j += kGT) {
+    s_hh[j] = 0u;
+    s_hl[j] = 0u;
+    s_hc[j] = 0;
+  }
+  if (tid == 0) {
+    s_b1 = kGB;
+    s_n1 = 0;
+    s_n2 = 0;
+    s_at1 = 0ull;
+  }
+  // (0) the row's maximum
+  double m = -CUDART_INF;
+  for (int i = tid; i < K; i += kGT) m = fmax(m, gsel_sanitise(lm[i]));
+  m = warp_max(m);
+  if (lane == 0) s_red[warp] = m;
+  __syncthreads();
+  double M = -CUDART_INF;
+#pragma unroll
+  for (int w = 0; w < kGT / 32; ++w) M = fmax(M, s_red[w]);
+  // (1) histogram
+  for (int i = tid; i < K; i += kGT) {
+    unsigned long long u;
+    int b;
+    gsel_elem(M, gsel_sanitise(lm[i]), u, b);
+    if (u) {
+      atomicAdd(&s_hh[b], (unsigned)(u >> 20));
+      atomicAdd(&s_hl[b], (unsigned)(u & 0xFFFFFu));
+      atomicAdd(&s_hc[b], 1);
+    }
+  }
+  __syncthreads();
+  // (2) exclusive bin prefixes (2 bins per thread), total, stage-1 bin
+  constexpr int kBPT = kGB / kGT;
+  unsigned long long bm[kBPT], mloc = 0ull;
+  int bc[kBPT], cloc = 0;
+#pragma unroll
+  for (int j = 0; j < kBPT; ++j) {
+    const int b = tid * kBPT + j;
+    bm[j] = ((unsigned long long)s_hh[b] << 20) + s_hl[b];
+    bc[j] = s_hc[b];
+    mloc += bm[j];
+    cloc += bc[j];
+  }
+  unsigned long long mi = mloc;
+  int ci = cloc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long tm = __shfl_up_sync(0xffffffffu, mi, o);
+    const int tc = __shfl_up_sync(0xffffffffu, ci, o);
+    if (lane >= o) {
+      mi += tm;
+      ci += tc;
+    }
+  }
+  if (lane == 31) {
+    s_wm[warp] = mi;
+    s_wc[warp] = ci;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const unsigned long long w = s_wm[lane];
+    const int wc = s_wc[lane];
+    unsigned long long wi = w;
+    int wci = wc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long tm = __shfl_up_sync(0xffffffffu, wi, o);
+      const int tc = __shfl_up_sync(0xffffffffu, wci, o);
+      if (lane >= o) {
+        wi += tm;
+        wci += tc;
+      }
+    }
+    s_wm[lane] = wi - w;
+    s_wc[lane] = wci - wc;
+    if (lane == 31) {
+      s_wm[32] = wi;
+      s_wc[32] = wci;
+    }
+  }
+  __syncthreads();
+  const unsigned long long T = s_wm[32];
+  unsigned long long mex = s_wm[warp] + mi - mloc;
+  int cex = s_wc[warp] + ci - cloc;
+  const double thr1 = p1 * (double)T;
+#pragma unroll
+  for (int j = 0; j < kBPT; ++j) {
+    const int b = tid * kBPT + j;
+    const unsigned long long inc = mex + bm[j];
+    if (bm[j] && (double)mex < thr1 && thr1 <= (double)inc) {
+      s_b1 = b;
+      s_before1 = mex;
+      s_mass1 = bm[j];
+    }
+    s_pm[b] = mex;
+    s_hc[b] = cex;  // -> exclusive count prefix
+    s_cur[b] = 0u;
+    mex = inc;
+    cex += bc[j];
+  }
+  if (tid == kGT - 1) s_hc[kGB] = s_wc[32];
+  __syncthreads();
+  const int b1 = s_b1;
+  if (T == 0ull || b1 >= kGB) {  // no mass (a non-finite query)
+    const uint8_t st = p1 >= 1.0 ? (p2 >= 1.0 ? 2 : 1) : 0;
+    for (int i = tid; i < K; i += kGT) state[i] = st;
+    if (tid == 0) {
+      counts[2 * row] = p1 >= 1.0 ? K : 0;
+      counts[2 * row + 1] = p1 >= 1.0 && p2 >= 1.0 ? K : 0;
+    }
+    return;
+  }
+  const double tlo = p2 * (double)s_before1, thi = p2 * (double)(s_before1 + s_mass1);
+  auto is_cand = [&](int b) {
+    const unsigned long long inc = b + 1 < kGB ? s_pm[b + 1] : T;
+    return b == b1 || (b < b1 && (double)inc >= tlo && (double)s_pm[b] < thi);
+  };
+  // (3) candidates -> their bin segments of the global sorted order
+  for (int i = tid; i < K; i += kGT) {
+    unsigned long long u;
+    int b;
+    gsel_elem(M, gsel_sanitise(lm[i]), u, b);
+    if (u && b <= b1 && is_cand(b)) cand[s_hc[b] + (int)atomicAdd(&s_cur[b], 1u)] = i;
+  }
+  __syncthreads();
+  // (4) rank inside the bin (log-mass desc, id asc); stage-1 crossing
+  for (int i = tid; i < K; i += kGT) {
+    unsigned long long u;
+    int b;
+    const double la = gsel_sanitise(lm[i]);
+    gsel_elem(M, la, u, b);
+    if (!(u && b <= b1 && is_cand(b))) continue;
+    const int j0 = s_hc[b], j1 = s_hc[b + 1];
+    int rk = 0;
+    unsigned long long pre = 0ull;
+    for (int j = j0; j < j1; ++j) {
+      const int ij = cand[j];
+      const double lj = gsel_sanitise(lm[ij]);
+      const bool ahead = lj > la || (lj == la && ij < i);
+      if (ahead) {
+        unsigned long long uj;
+        int bj;
+        gsel_elem(M, lj, uj, bj);
+        ++rk;
+        pre += uj;
+      }
+    }
+    pos[i] = j0 + rk;
+    ex[i] = s_pm[b] + pre;
+    const unsigned long long inc = ex[i] + u;
+    if ((double)ex[i] < thr1 && thr1 <= (double)inc) {
+      s_n1 = j0 + rk + 1;
+      s_at1 = inc;
+    }
+  }
+  __syncthreads();
+  // (5) stage-2 crossing
+  const int n1 = p1 >= 1.0 ? K : s_n1;
+  const double thr2 = p2 * (double)s_at1;
+  for (int i = tid; i < K; i += kGT) {
+    unsigned long long u;
+    int b;
+    gsel_elem(M, gsel_sanitise(lm[i]), u, b);
+    if (u && b <= b1 && is_cand(b) && (double)ex[i] < thr2 && thr2 <= (double)(ex[i] + u)) s_n2 = pos[i] + 1;
+  }
+  __syncthreads();
+  const int n2 = p1 >= 1.0 && p2 >= 1.0 ? K : s_n2;
+  // (6) states
+  const uint8_t zst = p1 >= 1.0 ? (p2 >= 1.0 ? 2 : 1) : 0;
+  for (int i = tid; i < K; i += kGT) {
+    unsigned long long u;
+    int b;
+    gsel_elem(M, gsel_sanitise(lm[i]), u, b);
+    uint8_t st;
+    if (!u) {
+      st = zst;
+    } else if (b <= b1 && is_cand(b)) {
+      st = pos[i] < n2 ? 2 : (pos[i] < n1 ? 1 : 0);
+    } else if (b > b1) {
+      st = 0;
+    } else {
+      const unsigned long long inc = b + 1 < kGB ? s_pm[b + 1] : T;
+      st = (double)inc < tlo ? 2 : 1;
+    }
+    state[i] = st;
+  }
+  if (tid == 0) {
+    counts[2 * row] = n1;
+    counts[2 * row + 1] = n2;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// LSE merge of P partials: out_parts [P, rows, d], lse_parts [P, rows]
+// ---------------------------------------------------------------------------
+__global__ void lse_merge_kernel(const float* __restrict__ out_parts, const float* __restrict__ lse_parts, int P,
+                                 int rows, int d, float* __restrict__ out, float* __restrict__ lse) {
+  const int row = blockIdx.x;
+  float M = -INFINITY;
+  for (int p = 0; p < P; ++p) M = fmaxf(M, lse_parts[(size_t)p * rows + row]);
+  double L = 0.0;
+  for (int p = 0; p < P; ++p) {
+    const float l = lse_parts[(size_t)p * rows + row];
+    if (l != -INFINITY) L += exp((double)l - (double)M);
+  }
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    double acc = 0.0;
+    for (int p = 0; p < P; ++p) {
+      const float l = lse_parts[(size_t)p * rows + row];
+      if (l != -INFINITY) acc += exp((double)l - (double)M) * (double)out_parts[((size_t)p * rows + row) * d + c];
+    }
+    out[(size_t)row * d + c] = L > 0.0 ? (float)(acc / L) : 0.f;
+  }
+  if (threadIdx.x == 0) lse[row] = L > 0.0 ? (float)((double)M + log(L)) : -INFINITY;
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+cudaError_t launch_kmpp_dsq(const void* pts, int dtype, int units, int n, int d, const double* centre, int first,
+                            double* dsq, double* sums, cudaStream_t st) {
+  kmpp_dsq_kernel<<<units, kKT, (size_t)d * sizeof(double), st>>>(pts, dtype, n, d, centre, first, dsq, sums);
+  return cudaGetLastError();
+}
+cudaError_t launch_kmpp_pick(const void* pts, int dtype, int units, int n, int d, const double* dsq,
+                             const double* all_sums, int P, int rank, const double* u_draw, const int* pick_in,
+                             long long gbase, double* centre_out, int* pick_out, cudaStream_t st) {
+  kmpp_pick_kernel<<<units, kKT, 0, st>>>(pts, dtype, n, d, dsq, all_sums, P, rank, u_draw, pick_in, gbase,
+                                          centre_out, pick_out);
+  return cudaGetLastError();
+}
+size_t lloyd_sums_ws_bytes(int units, int n, int k) { return ((size_t)units * k + (size_t)units * n) * sizeof(int); }
+cudaError_t launch_lloyd_sums(const void* pts, int dtype, int units, int n, int d, const int* assign, int k,
+                              double* sums, long long* counts, void* ws, cudaStream_t st) {
+  int* cnt = reinterpret_cast<int*>(ws);
+  int* order = cnt + (size_t)units * k;
+  lloyd_sums_kernel<<<units, kLT, 0, st>>>(pts, dtype, n, d, assign, k, sums, counts, cnt, order);
+  return cudaGetLastError();
+}
+size_t select_global_ws_bytes(int rows, int ld) { return (size_t)rows * ld * (4 + 8 + 4); }
+cudaError_t launch_select_global(const double* lm, int rows, int ld, const int* Ks, double p1, double p2,
+                                 uint8_t* state, int* counts, void* ws, cudaStream_t st) {
+  unsigned long long* ex = reinterpret_cast<unsigned long long*>(ws);
+  int* pos = reinterpret_cast<int*>(ex + (size_t)rows * ld);
+  int* cand = pos + (size_t)rows * ld;
+  select_global_kernel<<<rows, kGT, 0, st>>>(lm, ld, Ks, p1, p2, state, counts, pos, ex, cand);
+  return cudaGetLastError();
+}
+cudaError_t launch_lse_merge(const float* out_parts, const float* lse_parts, int P, int rows, int d, float* out,
+                             float* lse, cudaStream_t st) {
+  lse_merge_kernel<<<rows, 128, 0, st>>>(out_parts, lse_parts, P, rows, d, out, lse);
+  return cudaGetLastError();
+}
+
+}  // namespace dp
