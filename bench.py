@@ -62,6 +62,10 @@ def parse():
     ap.add_argument("--sim-world", type=int, default=1,
                     help="measure ONE rank's KV-head shard of a P-GPU run on this GPU (no collectives)")
     ap.add_argument("--sim-rank", type=int, default=0)
+    ap.add_argument("--seq-shards", type=int, default=1,
+                    help="config 5: shard the sequence over P ranks (global two-stage top-p over the "
+                         "all-gathered log-mass slices + LSE merge); under torchrun P = world, else one "
+                         "rank's share (--sim-rank) is measured alone on one GPU")
     return ap.parse_args()
 
 
@@ -828,10 +832,186 @@ class _Null:
         return False
 
 
+def measured_peak():
+    """(HBM GB/s, source): MEASURED_PEAKS.json (driver-written) or the
+    profiling recipe's fallback."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except Exception:
+        peaks = {}
+    return float(peaks.get("hbm_gbs", 6650.0)), ("measured" if "hbm_gbs" in peaks else "fallback")
+
+
+def run_seqshard(a):
+    """Config 5: 1M-token single-sequence decode, sequence-sharded over P GPUs
+    with the reference's global selection (paper_2602_05191_b200.seqshard):
+    per layer each rank scores its slice of the cluster table, the log-mass
+    slices are all-gathered, dp_select_global runs the two-stage top-p over
+    the whole table, the rank attends over its exact clusters / pseudo-rows
+    and the partials are all-gathered and merged (dp_lse_merge).  Caches: each
+    rank clusters its own 1/P of the tokens into 1/P of the clusters (the
+    cluster-partitioned layout; the GLOBAL k-means of seqshard.shard_cluster_layer
+    is ~32K sequential all-reduce rounds at 1M and is exercised by the tests,
+    not here).  Without torchrun the other ranks' slices are stand-ins (this
+    rank's own slice repeated) and the collectives are not timed."""
+    import torch
+
+    from paper_2602_05191_b200 import _native as N
+    from paper_2602_05191_b200 import cluster_layer
+    from paper_2602_05191_b200.cache import dtype_code, head_seed
+    from paper_2602_05191_b200.seqshard import Comm
+    from paper_2602_05191_b200.sharding import seq_shard_bounds
+    from paper_2602_05191_b200.workload import generate_layer, generate_queries
+
+    world, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    P = a.seq_shards
+    real = world > 1
+    if real and world != P:
+        raise SystemExit(f"--seq-shards {P} needs {P} ranks (got {world})")
+    r = rank if real else a.sim_rank
+    comm = Comm() if real else None
+    L, G, d, H = a.layers, a.gqa, a.head_dim, a.kv_heads
+    Hq = H * G
+    lo, hi = seq_shard_bounds(a.context, P, r)
+    n_r = hi - lo
+    sink = 4 if r == 0 else 0
+    window = 64 if r == P - 1 else 0
+    lib = N.lib()
+    t0 = time.perf_counter()
+    layers, qs = [], []
+    for li in range(L):
+        k, v, c = generate_layer(1, H, n_r, d, layer=li, seed=1000 + r, device=dev)
+        seeds = [[head_seed(0, li, h, 1000 + r) for h in range(H)]]
+        lay = cluster_layer(k, v, sink=sink, window=window, head_seeds=seeds)
+        del k, v
+        layers.append(lay)
+        qs.append(torch.from_numpy(generate_queries(c, G, a.qsteps, profile=a.profile, layer=li)).to(dev)
+                  .to(torch.bfloat16))  # [S, 1, Hq, d]
+    torch.cuda.synchronize(dev)
+    prefill_s = time.perf_counter() - t0
+    cap = max(lay.cluster_cap for lay in layers)
+    ld = P * cap
+    scale = 1.0 / math.sqrt(d)
+    lm = torch.zeros((1, Hq, cap), dtype=torch.float64, device=dev)
+    st = torch.zeros((1, Hq, cap), dtype=torch.uint8, device=dev)
+    g_lm = torch.full((Hq, ld), -math.inf, dtype=torch.float64, device=dev)
+    g_st = torch.zeros((Hq, ld), dtype=torch.uint8, device=dev)
+    g_cnt = torch.zeros((Hq, 2), dtype=torch.int32, device=dev)
+    g_k = torch.full((Hq,), ld, dtype=torch.int32, device=dev)
+    g_ws = torch.empty((lib.dp_select_global_workspace_bytes(Hq, ld),), dtype=torch.uint8, device=dev)
+    out = torch.zeros((1, Hq, d), dtype=torch.float32, device=dev)
+    lse = torch.zeros((1, Hq), dtype=torch.float32, device=dev)
+    parts_o = torch.zeros((P, 1, Hq, d), dtype=torch.float32, device=dev)
+    parts_l = torch.zeros((P, 1, Hq), dtype=torch.float32, device=dev)
+    merged = torch.zeros_like(out)
+    merged_l = torch.zeros_like(lse)
+    wsb = max(lib.dp_decode_workspace_bytes(lay.view(), G) for lay in layers)
+    ws = torch.zeros((wsb,), dtype=torch.uint8, device=dev)
+    views = [lay.view() for lay in layers]
+    stats = torch.zeros((L, 1, H, 4), dtype=torch.int32, device=dev)
+
+    def layer_step(li, s, ev=None):
+        cs = torch.cuda.current_stream(dev).cuda_stream
+        q = qs[li][s % a.qsteps]
+        lay, v = layers[li], views[li]
+        if ev is not None:
+            ev[0].record()
+        lm.fill_(-math.inf)
+        N.check(lib.dp_score(v, N.ptr(q), dtype_code(q), G, scale, N.ptr(lm), cs))
+        if ev is not None:
+            ev[1].record()
+        if real:
+            g_lm.view(Hq, P, cap).copy_(comm.all_gather(lm[0]).permute(1, 0, 2))
+        else:  # stand-ins for the other ranks' slices: this rank's own slice
+            g_lm.view(Hq, P, cap).copy_(lm[0].unsqueeze(1).expand(Hq, P, cap))
+        if ev is not None:
+            ev[2].record()
+        N.check(lib.dp_select_global(N.ptr(g_lm), Hq, ld, N.ptr(g_k), a.p1, a.p2, N.ptr(g_st), N.ptr(g_cnt),
+                                     N.ptr(g_ws), g_ws.numel(), cs))
+        st[0].copy_(g_st.view(Hq, P, cap)[:, r])
+        if ev is not None:
+            ev[3].record()
+        N.check(lib.dp_sparse_attention(v, N.ptr(q), dtype_code(q), G, scale, N.ptr(lm), N.ptr(st), N.ptr(out),
+                                        N.ptr(lse), N.ptr(stats[li]), N.ptr(ws), ws.numel(), cs))
+        if ev is not None:
+            ev[4].record()
+        if real:
+            parts_o.copy_(comm.all_gather(out))
+            parts_l.copy_(comm.all_gather(lse))
+        else:
+            parts_o.copy_(out.unsqueeze(0).expand_as(parts_o))
+            parts_l.copy_(lse.unsqueeze(0).expand_as(parts_l))
+        N.check(lib.dp_lse_merge(N.ptr(parts_o), N.ptr(parts_l), P, Hq, d, N.ptr(merged), N.ptr(merged_l), cs))
+        if ev is not None:
+            ev[5].record()
+
+    sampler = ClockSampler(local)
+    for s in range(a.warmup):
+        for li in range(L):
+            layer_step(li, s)
+    torch.cuda.synchronize(dev)
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with sampler:
+        e0.record()
+        for s in range(a.steps):
+            for li in range(L):
+                layer_step(li, s)
+        e1.record()
+        torch.cuda.synchronize(dev)
+    barrier(world)
+    ms = max_over_ranks(e0.elapsed_time(e1) / a.steps, world, dev)
+    # stage split (eager, CUDA events): score / gather / select / attend / merge
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(L)]
+    torch.cuda._sleep(int(1e8))
+    for li in range(L):
+        layer_step(li, 0, evs[li])
+    torch.cuda.synchronize(dev)
+    stage = np.mean([[e[j].elapsed_time(e[j + 1]) for j in range(5)] for e in evs], axis=0) * 1e3
+    st_np = stats.cpu().numpy().astype(np.int64)
+    U, A = st_np[..., 0], st_np[..., 1]
+    ncl = np.stack([lay.nclusters.cpu().numpy() for lay in layers]).astype(np.int64)
+    attend_bytes = (U * 2 * d * 2 + A * d * 4).sum(axis=(1, 2)) + Hq * d * (2 + 4)  # [L]
+    step_bytes = float(attend_bytes.sum() + (ncl * (d * 4 + 4)).sum())
+    dense_bytes = float(L * H * n_r * 2 * d * 2)
+    hbm_peak, peak_src = measured_peak()
+    if rank == 0:
+        line = {
+            "metric": "decode_us_per_step", "value": ms * 1e3, "unit": "us/step", "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (reference blob law on device, Philox); random-init caches, no checkpoint",
+            "config": {"workload": f"doublep-decode llama-3.1-8b-shape L{L} B1 N{a.context} Hq{Hq}/Hkv{H} d{d} bf16 "
+                                   f"p=({a.p1},{a.p2}) {a.profile} sequence-sharded P={P}",
+                       "layers": L, "context": a.context, "seq_shards": P, "rank_tokens": n_r,
+                       "parallelism": (f"sequence shards over {P} GPUs" if real else
+                                       f"sequence shard {r}/{P} measured alone on one GPU (collectives not timed; "
+                                       f"other ranks' log-mass slices and partials are stand-ins)"),
+                       "global_clusters": int(P * ncl.sum(axis=(1, 2)).mean() / H),
+                       "caches": "each rank clusters its own 1/P of the tokens (cluster-partitioned layout)",
+                       "l2": "inputs larger than L2 (each layer's KV > 126 MB; layers cycled)"},
+            "stage_us_per_layer": {"score": stage[0], "gather": stage[1], "select_global": stage[2],
+                                   "attend": stage[3], "merge": stage[4]},
+            "attend_roofline": {"bound": "hbm", "achieved": float(attend_bytes.mean() / (stage[3] * 1e-6) / 1e9),
+                                "peak": hbm_peak, "unit": "GB/s", "peak_source": peak_src},
+            "step_algorithmic_bytes": step_bytes, "dense_bytes_per_rank": dense_bytes,
+            "union_exact_rows_frac": float(U.mean() / n_r),
+            "collective_bytes_per_layer": {"all_gather_log_mass": Hq * ld * 8, "all_gather_partials": P * Hq * (d + 1) * 4},
+            "prefill_s": prefill_s, "clocks": sampler.summary(),
+            "gpu_launches": L * a.steps * 5,
+        }
+        print(json.dumps(line), flush=True)
+
+
 def main():
     a = parse()
     if a.impl == "reference":
         run_reference(a)
+    elif a.seq_shards > 1:
+        run_seqshard(a)
     else:
         run_b200(a)
     if int(os.environ.get("WORLD_SIZE", "1")) > 1:

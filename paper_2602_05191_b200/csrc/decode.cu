@@ -263,12 +263,22 @@ __global__ void __launch_bounds__(kListThreads) worklist_kernel(dp_cache_view v,
     const int pa = block_exclusive_scan<int>(ma != 0, red, &tot_a);
     const int pl = block_exclusive_scan<int>(len, red, &tot_l);
     const int rb = s_runs, rowb = s_rows, ab = s_apx;
-    if (me) {
-      runs[rb + pe] = make_int4(offs[k], len, me, rowb + pl);
-      const unsigned tag = (unsigned)me << 24;
-      for (int t = 0; t < len; ++t) rowidx[rowb + pl + t] = tag | (unsigned)(offs[k] + t);
-    }
+    const int st0 = me ? offs[k] : 0;
+    if (me) runs[rb + pe] = make_int4(st0, len, me, rowb + pl);
     if (ma) apx[ab + pa] = make_int2(k, ma);
+    {  // warp-cooperative expansion of the warp's clusters: lanes write consecutive rows
+      const int lane = tid & 31;
+      unsigned todo = __ballot_sync(0xffffffffu, len > 0);
+      while (todo) {
+        const int t = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const int tl = __shfl_sync(0xffffffffu, len, t);
+        const int to = __shfl_sync(0xffffffffu, rowb + pl, t);
+        const unsigned tag = (unsigned)__shfl_sync(0xffffffffu, me, t) << 24;
+        const int ts = __shfl_sync(0xffffffffu, st0, t);
+        for (int x = lane; x < tl; x += 32) rowidx[to + x] = tag | (unsigned)(ts + x);
+      }
+    }
     __syncthreads();
     if (tid == 0) { s_runs = rb + tot_e; s_rows = rowb + tot_l; s_apx = ab + tot_a; }
     __syncthreads();
@@ -645,7 +655,8 @@ cudaError_t launch_attn_t(const dp_cache_view& v, const void* q, int qdt, int G,
 // l = sum e^(lm - m), o = sum e^(lm - m) * value_mean (engine.py:231-246)
 __global__ void __launch_bounds__(256) approx_partial_kernel(dp_cache_view v, int G, const double* __restrict__ lm,
                                                             const uint8_t* __restrict__ state, WorkLists wl,
-                                                            const void* __restrict__ q, int qdt, double scale) {
+                                                            const void* __restrict__ q, int qdt, double scale,
+                                                            int need_partial) {
   const int hq = blockIdx.x, bh = hq / G, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int K = v.nclusters[bh], cap = v.cluster_cap, d = v.head_dim;
   const double* x = lm + (size_t)hq * cap;
@@ -660,14 +671,15 @@ __global__ void __launch_bounds__(256) approx_partial_kernel(dp_cache_view v, in
   // sink/window rows are always exact: their logits join the reference max
   // (q nullable: the dp_build_worklist entry point has no query)
   double sw = -CUDART_INF;
-  if (q) {
+  if (q) {  // one warp per row, lanes over the dims (coalesced)
     const int nsw = v.sink + v.window;
-    for (int t = tid; t < nsw; t += blockDim.x) {
+    for (int t = warp; t < nsw; t += blockDim.x / 32) {
       const int row = t < v.sink ? t : v.n_tokens - v.window + (t - v.sink);
       double acc = 0.0;
-      for (int c = 0; c < d; ++c)
+      for (int c = lane; c < d; c += 32)
         acc += load_elem_d(v.keys, v.dtype, ((size_t)bh * v.row_cap + row) * d + c) *
                load_elem_d(q, qdt, (size_t)hq * d + c);
+      acc = warp_sum(acc);
       if (acc == acc) sw = fmax(sw, acc * scale);
     }
   }
@@ -676,6 +688,7 @@ __global__ void __launch_bounds__(256) approx_partial_kernel(dp_cache_view v, in
   const double SW = block_max(sw, red, -CUDART_INF);
   // reference max of the tensor-core attention's accumulators (log2 units), as dp_plan writes it
   if (tid == 0) wl.refm[hq] = (float)(ref_max(Mall, SW) * 1.4426950408889634);
+  if (!need_partial) return;  // the tensor-core attention folds the approximated clusters itself
   const float* vbar = v.value_means + (size_t)bh * cap * d;
   float acc[8];
 #pragma unroll
@@ -712,7 +725,8 @@ cudaError_t launch_worklist(const dp_cache_view& v, int G, const uint8_t* state,
   wl.stats = stats;
   worklist_kernel<<<v.batch * v.kv_heads, kListThreads, 0, st>>>(v, G, state, wl);
   if (lm && v.head_dim <= 256)
-    approx_partial_kernel<<<v.batch * v.kv_heads * G, 256, 0, st>>>(v, G, lm, state, wl, q, qdt, scale);
+    approx_partial_kernel<<<v.batch * v.kv_heads * G, 256, 0, st>>>(v, G, lm, state, wl, q, qdt, scale,
+                                                                    !(v.dtype == DP_BF16 && v.head_dim == 128));
   return cudaGetLastError();
 }
 

@@ -28,6 +28,7 @@
 
 #include "common.cuh"
 #include "decode_internal.h"
+#include "host_state.h"
 #include "select.cuh"
 
 namespace dp {
@@ -196,6 +197,8 @@ __global__ void __launch_bounds__(kLT) lloyd_sums_kernel(const void* __restrict_
 // ---------------------------------------------------------------------------
 constexpr int kGT = 1024;
 constexpr int kGB = 2048;
+constexpr int kGCand = 4096;  // candidates staged in shared memory (more: the global-scratch path)
+constexpr size_t kGDyn = (size_t)kGCand * (8 + 8 + 8 + 4 + 4);
 
 __device__ __forceinline__ double gsel_sanitise(double x) { return x != x ? -CUDART_INF : fmin(x, 1.7976931348623157e308); }
 
@@ -230,7 +233,13 @@ __global__ void __launch_bounds__(kGT, 1) select_global_kernel(const double* __r
   __shared__ int s_wc[33];
   __shared__ double s_red[32];
   __shared__ unsigned long long s_before1, s_mass1, s_at1;
-  __shared__ int s_b1, s_n1, s_n2;
+  __shared__ int s_b1, s_n1, s_n2, s_blo, s_bhi;
+  extern __shared__ __align__(16) unsigned char g_dyn[];  // staged candidates
+  unsigned long long* s_cu = reinterpret_cast<unsigned long long*>(g_dyn);
+  unsigned long long* s_cex = s_cu + kGCand;
+  double* s_clm = reinterpret_cast<double*>(s_cex + kGCand);
+  int* s_cid = reinterpret_cast<int*>(s_clm + kGCand);
+  int* s_cpos = s_cid + kGCand;
   for (int j = tid; j < kGB; j += kGT) {
     s_hh[j] = 0u;
     s_hl[j] = 0u;
@@ -349,57 +358,125 @@ __global__ void __launch_bounds__(kGT, 1) select_global_kernel(const double* __r
     const unsigned long long inc = b + 1 < kGB ? s_pm[b + 1] : T;
     return b == b1 || (b < b1 && (double)inc >= tlo && (double)s_pm[b] < thi);
   };
-  // (3) candidates -> their bin segments of the global sorted order
+  // (3) candidates -> their bin segments of the global sorted order; the
+  //     candidate bins are [blo, bhi] and b1, i.e. two contiguous slot ranges
+  if (tid == 0) {
+    s_blo = kGB;
+    s_bhi = -1;
+  }
+  __syncthreads();
   for (int i = tid; i < K; i += kGT) {
     unsigned long long u;
     int b;
     gsel_elem(M, gsel_sanitise(lm[i]), u, b);
-    if (u && b <= b1 && is_cand(b)) cand[s_hc[b] + (int)atomicAdd(&s_cur[b], 1u)] = i;
-  }
-  __syncthreads();
-  // (4) rank inside the bin (log-mass desc, id asc); stage-1 crossing
-  for (int i = tid; i < K; i += kGT) {
-    unsigned long long u;
-    int b;
-    const double la = gsel_sanitise(lm[i]);
-    gsel_elem(M, la, u, b);
-    if (!(u && b <= b1 && is_cand(b))) continue;
-    const int j0 = s_hc[b], j1 = s_hc[b + 1];
-    int rk = 0;
-    unsigned long long pre = 0ull;
-    for (int j = j0; j < j1; ++j) {
-      const int ij = cand[j];
-      const double lj = gsel_sanitise(lm[ij]);
-      const bool ahead = lj > la || (lj == la && ij < i);
-      if (ahead) {
-        unsigned long long uj;
-        int bj;
-        gsel_elem(M, lj, uj, bj);
-        ++rk;
-        pre += uj;
+    if (u && b <= b1 && is_cand(b)) {
+      cand[s_hc[b] + (int)atomicAdd(&s_cur[b], 1u)] = i;
+      if (b < b1) {
+        atomicMin(&s_blo, b);
+        atomicMax(&s_bhi, b);
       }
     }
-    pos[i] = j0 + rk;
-    ex[i] = s_pm[b] + pre;
-    const unsigned long long inc = ex[i] + u;
-    if ((double)ex[i] < thr1 && thr1 <= (double)inc) {
-      s_n1 = j0 + rk + 1;
-      s_at1 = inc;
+  }
+  __syncthreads();
+  // stage the candidates in shared memory (id, log-mass, mass): slots of
+  // [blo, bhi] then those of b1
+  const int r1a = s_bhi >= 0 ? s_hc[s_blo] : 0, r1b = s_bhi >= 0 ? s_hc[s_bhi + 1] : 0;
+  const int r2a = s_hc[b1], r2b = s_hc[b1 + 1];
+  const int n1c = r1b - r1a, nc = n1c + (r2b - r2a);
+  const bool staged = nc <= kGCand;
+  auto sidx = [&](int slot) { return slot >= r2a ? n1c + (slot - r2a) : slot - r1a; };
+  if (staged) {
+    for (int t = tid; t < nc; t += kGT) {
+      const int slot = t < n1c ? r1a + t : r2a + (t - n1c);
+      const int i = cand[slot];
+      const double la = gsel_sanitise(lm[i]);
+      unsigned long long u;
+      int b;
+      gsel_elem(M, la, u, b);
+      (void)b;
+      s_cid[t] = i;
+      s_clm[t] = la;
+      s_cu[t] = u;
+    }
+  }
+  __syncthreads();
+  // (4) rank inside the bin (log-mass desc, id asc) -> sorted position and
+  //     exclusive cumulative mass; the stage-1 crossing element
+  if (staged) {
+    for (int t = tid; t < nc; t += kGT) {
+      const int i = s_cid[t];
+      const double la = s_clm[t];
+      unsigned long long u;
+      int b;
+      gsel_elem(M, la, u, b);
+      const int j0 = s_hc[b], j1 = s_hc[b + 1], k0 = sidx(j0);
+      int rk = 0;
+      unsigned long long pre = 0ull;
+      for (int j = 0; j < j1 - j0; ++j) {
+        const double lj = s_clm[k0 + j];
+        const int ij = s_cid[k0 + j];
+        const bool ahead = lj > la || (lj == la && ij < i);
+        rk += ahead;
+        pre += ahead ? s_cu[k0 + j] : 0ull;
+      }
+      const int ps = j0 + rk;
+      const unsigned long long e0 = s_pm[b] + pre;
+      s_cpos[t] = ps;
+      s_cex[t] = e0;
+      if ((double)e0 < thr1 && thr1 <= (double)(e0 + u)) {
+        s_n1 = ps + 1;
+        s_at1 = e0 + u;
+      }
+    }
+  } else {  // many candidates (very flat scores): the same from global scratch
+    for (int i = tid; i < K; i += kGT) {
+      unsigned long long u;
+      int b;
+      const double la = gsel_sanitise(lm[i]);
+      gsel_elem(M, la, u, b);
+      if (!(u && b <= b1 && is_cand(b))) continue;
+      const int j0 = s_hc[b], j1 = s_hc[b + 1];
+      int rk = 0;
+      unsigned long long pre = 0ull;
+      for (int j = j0; j < j1; ++j) {
+        const int ij = cand[j];
+        const double lj = gsel_sanitise(lm[ij]);
+        const bool ahead = lj > la || (lj == la && ij < i);
+        if (ahead) {
+          unsigned long long uj;
+          int bj;
+          gsel_elem(M, lj, uj, bj);
+          ++rk;
+          pre += uj;
+        }
+      }
+      pos[i] = j0 + rk;
+      ex[i] = s_pm[b] + pre;
+      const unsigned long long inc = ex[i] + u;
+      if ((double)ex[i] < thr1 && thr1 <= (double)inc) {
+        s_n1 = j0 + rk + 1;
+        s_at1 = inc;
+      }
     }
   }
   __syncthreads();
   // (5) stage-2 crossing
   const int n1 = p1 >= 1.0 ? K : s_n1;
   const double thr2 = p2 * (double)s_at1;
-  for (int i = tid; i < K; i += kGT) {
-    unsigned long long u;
-    int b;
-    gsel_elem(M, gsel_sanitise(lm[i]), u, b);
-    if (u && b <= b1 && is_cand(b) && (double)ex[i] < thr2 && thr2 <= (double)(ex[i] + u)) s_n2 = pos[i] + 1;
+  if (staged) {
+    for (int t = tid; t < nc; t += kGT)
+      if ((double)s_cex[t] < thr2 && thr2 <= (double)(s_cex[t] + s_cu[t])) s_n2 = s_cpos[t] + 1;
+  } else {
+    for (int i = tid; i < K; i += kGT) {
+      unsigned long long u;
+      int b;
+      gsel_elem(M, gsel_sanitise(lm[i]), u, b);
+      if (u && b <= b1 && is_cand(b) && (double)ex[i] < thr2 && thr2 <= (double)(ex[i] + u)) s_n2 = pos[i] + 1;
+    }
   }
   __syncthreads();
   const int n2 = p1 >= 1.0 && p2 >= 1.0 ? K : s_n2;
-  // (6) states
+  // (6) states: candidates by position, the rest by bin
   const uint8_t zst = p1 >= 1.0 ? (p2 >= 1.0 ? 2 : 1) : 0;
   for (int i = tid; i < K; i += kGT) {
     unsigned long long u;
@@ -409,6 +486,7 @@ __global__ void __launch_bounds__(kGT, 1) select_global_kernel(const double* __r
     if (!u) {
       st = zst;
     } else if (b <= b1 && is_cand(b)) {
+      if (staged) continue;  // written from the staged copy below
       st = pos[i] < n2 ? 2 : (pos[i] < n1 ? 1 : 0);
     } else if (b > b1) {
       st = 0;
@@ -418,6 +496,8 @@ __global__ void __launch_bounds__(kGT, 1) select_global_kernel(const double* __r
     }
     state[i] = st;
   }
+  if (staged)
+    for (int t = tid; t < nc; t += kGT) state[s_cid[t]] = s_cpos[t] < n2 ? 2 : (s_cpos[t] < n1 ? 1 : 0);
   if (tid == 0) {
     counts[2 * row] = n1;
     counts[2 * row + 1] = n2;
@@ -477,7 +557,13 @@ cudaError_t launch_select_global(const double* lm, int rows, int ld, const int* 
   unsigned long long* ex = reinterpret_cast<unsigned long long*>(ws);
   int* pos = reinterpret_cast<int*>(ex + (size_t)rows * ld);
   int* cand = pos + (size_t)rows * ld;
-  select_global_kernel<<<rows, kGT, 0, st>>>(lm, ld, Ks, p1, p2, state, counts, pos, ex, cand);
+  static bool attr[64] = {};
+  const int dev = current_device();
+  if (!attr[dev]) {
+    cudaFuncSetAttribute(select_global_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGDyn);
+    attr[dev] = true;
+  }
+  select_global_kernel<<<rows, kGT, kGDyn, st>>>(lm, ld, Ks, p1, p2, state, counts, pos, ex, cand);
   return cudaGetLastError();
 }
 cudaError_t launch_lse_merge(const float* out_parts, const float* lse_parts, int P, int rows, int d, float* out,

@@ -196,3 +196,46 @@ def test_select_global_matches_fused_plan():
         kk = int(ks[r])
         assert torch.equal(st[r, :kk], st_ref[0, r, :kk]), r
         assert torch.equal(cnt[r], cnt_ref[0, r]), r
+
+
+@pytest.mark.parametrize("K", [32766, 50000])
+def test_select_global_large_k_vs_oracle(K):
+    """The global table of the 1M-token config (K = 32,766; beyond the fused
+    plan's and dp_select's per-launch caps): dp_select_global against the
+    oracle's two-stage top-p (selection.py:36-65) on peaked and flat rows,
+    ties classified as in tests/parity.py."""
+    from types import SimpleNamespace
+
+    from paper_2602_05191_b200 import _native as N
+
+    rng = np.random.default_rng(7)
+    rows = []
+    for kind in ("peaked", "flat", "two-peak"):
+        base = rng.normal(0.0, 1.0, K) + np.log(rng.integers(1, 80, K))
+        if kind == "peaked":
+            base[rng.integers(0, K, 300)] += rng.uniform(4, 14, 300)
+        elif kind == "two-peak":
+            base[:50] += 20.0
+            base[-50:] += 19.5
+        rows.append(base * (0.3 if kind == "flat" else 1.0))
+    lm = torch.from_numpy(np.stack(rows)).cuda()
+    R = lm.shape[0]
+    ks = torch.full((R,), K, dtype=torch.int32, device="cuda")
+    st = torch.zeros((R, K), dtype=torch.uint8, device="cuda")
+    cnt = torch.zeros((R, 2), dtype=torch.int32, device="cuda")
+    lib = N.lib()
+    for p1, p2 in ((0.95, 0.7), (0.9, 0.8), (0.99, 0.5)):
+        ws = torch.empty((lib.dp_select_global_workspace_bytes(R, K),), dtype=torch.uint8, device="cuda")
+        N.check(lib.dp_select_global(N.ptr(lm), R, K, N.ptr(ks), p1, p2, N.ptr(st), N.ptr(cnt), N.ptr(ws),
+                                     ws.numel(), torch.cuda.current_stream().cuda_stream))
+        torch.cuda.synchronize()
+        for r in range(R):
+            x = rows[r]
+            probs = O.softmax(x)
+            est = SimpleNamespace(probs=probs)
+            s1 = O.top_p_select(probs, p1)
+            pl = SimpleNamespace(stage1=s1)
+            c1, c2 = PT.classify_sets(est, pl, st[r].cpu().numpy(), p1, p2)
+            assert "real" not in (c1, c2), (r, p1, p2, c1, c2)
+            n1 = int((st[r] >= 1).sum())
+            assert int(cnt[r, 0]) == n1 and int(cnt[r, 1]) == int((st[r] == 2).sum())
