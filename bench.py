@@ -953,16 +953,32 @@ def run_seqshard(a):
         for li in range(L):
             layer_step(li, s)
     torch.cuda.synchronize(dev)
+    graphs = None
+    if not real:  # one CUDA graph per distinct query step (the collectives of a real run stay eager)
+        graphs = []
+        for s in range(a.qsteps):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                for li in range(L):
+                    layer_step(li, s)
+            graphs.append(g)
+        for s in range(a.warmup):
+            graphs[s % len(graphs)].replay()
+        torch.cuda.synchronize(dev)
     barrier(world)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with sampler:
         e0.record()
         for s in range(a.steps):
-            for li in range(L):
-                layer_step(li, s)
+            if graphs is not None:
+                graphs[s % len(graphs)].replay()
+            else:
+                for li in range(L):
+                    layer_step(li, s)
         e1.record()
         torch.cuda.synchronize(dev)
     barrier(world)
+    del graphs
     ms = max_over_ranks(e0.elapsed_time(e1) / a.steps, world, dev)
     # stage split (eager, CUDA events): score / gather / select / attend / merge
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(L)]
@@ -1001,7 +1017,8 @@ def run_seqshard(a):
             "union_exact_rows_frac": float(U.mean() / n_r),
             "collective_bytes_per_layer": {"all_gather_log_mass": Hq * ld * 8, "all_gather_partials": P * Hq * (d + 1) * 4},
             "prefill_s": prefill_s, "clocks": sampler.summary(),
-            "gpu_launches": L * a.steps * 5,
+            "timing": "CUDA graph of the L-layer step" if not real else "eager (NCCL collectives in the step)",
+            "gpu_launches": L * a.steps * 7,
         }
         print(json.dumps(line), flush=True)
 

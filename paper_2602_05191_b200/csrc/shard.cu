@@ -217,7 +217,8 @@ __global__ void __launch_bounds__(kGT, 1) select_global_kernel(const double* __r
                                                               uint8_t* __restrict__ state_all,
                                                               int* __restrict__ counts, int* __restrict__ pos_ws,
                                                               unsigned long long* __restrict__ ex_ws,
-                                                              int* __restrict__ cand_ws) {
+                                                              int* __restrict__ cand_ws,
+                                                              unsigned long long* __restrict__ pk_ws) {
   const int row = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int K = Ks[row];
   const double* lm = lm_all + (size_t)row * ld;
@@ -225,6 +226,9 @@ __global__ void __launch_bounds__(kGT, 1) select_global_kernel(const double* __r
   int* pos = pos_ws + (size_t)row * ld;
   unsigned long long* ex = ex_ws + (size_t)row * ld;
   int* cand = cand_ws + (size_t)row * ld;
+  // (u, bin) of every element, packed once in pass (1) and re-read by the
+  // later passes instead of recomputing exp / conversions: u << 11 | bin
+  unsigned long long* pk = pk_ws + (size_t)row * ld;
   __shared__ unsigned s_hh[kGB], s_hl[kGB];
   __shared__ int s_hc[kGB + 1];
   unsigned* s_cur = s_hh;  // after the bin scan: per-bin cursors of the candidate placement
@@ -265,6 +269,7 @@ __global__ void __launch_bounds__(kGT, 1) select_global_kernel(const double* __r
     unsigned long long u;
     int b;
     gsel_elem(M, gsel_sanitise(lm[i]), u, b);
+    pk[i] = (u << 11) | (unsigned long long)b;
     if (u) {
       atomicAdd(&s_hh[b], (unsigned)(u >> 20));
       atomicAdd(&s_hl[b], (unsigned)(u & 0xFFFFFu));
@@ -366,9 +371,9 @@ __global__ void __launch_bounds__(kGT, 1) select_global_kernel(const double* __r
   }
   __syncthreads();
   for (int i = tid; i < K; i += kGT) {
-    unsigned long long u;
-    int b;
-    gsel_elem(M, gsel_sanitise(lm[i]), u, b);
+    const unsigned long long w = pk[i];
+    const unsigned long long u = w >> 11;
+    const int b = (int)(w & 2047u);
     if (u && b <= b1 && is_cand(b)) {
       cand[s_hc[b] + (int)atomicAdd(&s_cur[b], 1u)] = i;
       if (b < b1) {
@@ -389,14 +394,9 @@ __global__ void __launch_bounds__(kGT, 1) select_global_kernel(const double* __r
     for (int t = tid; t < nc; t += kGT) {
       const int slot = t < n1c ? r1a + t : r2a + (t - n1c);
       const int i = cand[slot];
-      const double la = gsel_sanitise(lm[i]);
-      unsigned long long u;
-      int b;
-      gsel_elem(M, la, u, b);
-      (void)b;
       s_cid[t] = i;
-      s_clm[t] = la;
-      s_cu[t] = u;
+      s_clm[t] = gsel_sanitise(lm[i]);
+      s_cu[t] = pk[i] >> 11;
     }
   }
   __syncthreads();
@@ -406,9 +406,8 @@ __global__ void __launch_bounds__(kGT, 1) select_global_kernel(const double* __r
     for (int t = tid; t < nc; t += kGT) {
       const int i = s_cid[t];
       const double la = s_clm[t];
-      unsigned long long u;
-      int b;
-      gsel_elem(M, la, u, b);
+      const unsigned long long u = s_cu[t];
+      const int b = (int)(pk[i] & 2047u);
       const int j0 = s_hc[b], j1 = s_hc[b + 1], k0 = sidx(j0);
       int rk = 0;
       unsigned long long pre = 0ull;
@@ -479,9 +478,9 @@ __global__ void __launch_bounds__(kGT, 1) select_global_kernel(const double* __r
   // (6) states: candidates by position, the rest by bin
   const uint8_t zst = p1 >= 1.0 ? (p2 >= 1.0 ? 2 : 1) : 0;
   for (int i = tid; i < K; i += kGT) {
-    unsigned long long u;
-    int b;
-    gsel_elem(M, gsel_sanitise(lm[i]), u, b);
+    const unsigned long long w = pk[i];
+    const unsigned long long u = w >> 11;
+    const int b = (int)(w & 2047u);
     uint8_t st;
     if (!u) {
       st = zst;
@@ -551,11 +550,12 @@ cudaError_t launch_lloyd_sums(const void* pts, int dtype, int units, int n, int 
   lloyd_sums_kernel<<<units, kLT, 0, st>>>(pts, dtype, n, d, assign, k, sums, counts, cnt, order);
   return cudaGetLastError();
 }
-size_t select_global_ws_bytes(int rows, int ld) { return (size_t)rows * ld * (4 + 8 + 4); }
+size_t select_global_ws_bytes(int rows, int ld) { return (size_t)rows * ld * (8 + 8 + 4 + 4); }
 cudaError_t launch_select_global(const double* lm, int rows, int ld, const int* Ks, double p1, double p2,
                                  uint8_t* state, int* counts, void* ws, cudaStream_t st) {
   unsigned long long* ex = reinterpret_cast<unsigned long long*>(ws);
-  int* pos = reinterpret_cast<int*>(ex + (size_t)rows * ld);
+  unsigned long long* pk = ex + (size_t)rows * ld;
+  int* pos = reinterpret_cast<int*>(pk + (size_t)rows * ld);
   int* cand = pos + (size_t)rows * ld;
   static bool attr[64] = {};
   const int dev = current_device();
@@ -563,7 +563,7 @@ cudaError_t launch_select_global(const double* lm, int rows, int ld, const int* 
     cudaFuncSetAttribute(select_global_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGDyn);
     attr[dev] = true;
   }
-  select_global_kernel<<<rows, kGT, kGDyn, st>>>(lm, ld, Ks, p1, p2, state, counts, pos, ex, cand);
+  select_global_kernel<<<rows, kGT, kGDyn, st>>>(lm, ld, Ks, p1, p2, state, counts, pos, ex, cand, pk);
   return cudaGetLastError();
 }
 cudaError_t launch_lse_merge(const float* out_parts, const float* lse_parts, int P, int rows, int d, float* out,
