@@ -275,6 +275,17 @@ __global__ void __launch_bounds__(kPT, 1)
             : "memory");
     }
   }
+  // the slice's later tiles (only two fit in shared memory) are requested
+  // into L2 now: the centroid tables are layer-static, so this also overlaps
+  // the previous grid's tail, and the refills after the wait hit L2
+  if (tid == 0 && ntile > 2 && !(dbg & 32)) {
+    const char* cbase = reinterpret_cast<const char*>(v.centroids) + ((size_t)bh * cap + k0) * d * 4;
+    const size_t rest = (size_t)(nloc - 2 * kCh) * d * 4;
+    for (size_t o = 0; o < rest; o += 65536)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(cbase + (size_t)2 * kCh * d * 4 + o),
+                   "r"((unsigned)(rest - o < 65536 ? rest - o : 65536))
+                   : "memory");
+  }
   {
     const int* goffs = v.offs + (size_t)bh * (cap + 1) + k0;
 #pragma unroll 1
