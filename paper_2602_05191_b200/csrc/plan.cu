@@ -507,7 +507,12 @@ __global__ void __launch_bounds__(kPT, 1)
       for (int i = tid; i < K; i += kPT) stown[i] = 0;
       __syncthreads();
     } else {
-      select_fast<kPT, kBins, kPlanMaxCap / kPT>(K, M, lmall, p1, p2, um, hm, hc, cur, clist, stown, &s_self, n1, n2);
+      // register slots per thread sized to the table: 2 up to 1024 clusters (32K contexts), else 8
+      if (K <= 2 * kPT)
+        select_fast<kPT, kBins, 2>(K, M, lmall, p1, p2, um, hm, hc, cur, clist, stown, &s_self, n1, n2);
+      else
+        select_fast<kPT, kBins, kPlanMaxCap / kPT>(K, M, lmall, p1, p2, um, hm, hc, cur, clist, stown, &s_self, n1,
+                                                   n2);
     }
 #ifdef DP_SEL_REPEAT
     // experiment: the same selection again with a warm instruction cache

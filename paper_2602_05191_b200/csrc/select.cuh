@@ -473,9 +473,20 @@ __device__ void select_two_stage(const int K, const double M, const double* lmal
 // ---------------------------------------------------------------------------
 constexpr double kFixF = 274877906944.0;  // 2^38
 
+#ifdef SEL_PROBE
+__device__ long long g_sel_probe[16];
+#define SELP(k, S)                                                   \
+  if (threadIdx.x == 0) {                                            \
+    volatile int _x = *reinterpret_cast<volatile int*>(&(S)->n1);    \
+    (void)_x;                                                        \
+    g_sel_probe[k] = clock64();                                      \
+  }
+#else
+#define SELP(k, S)
+#endif
 struct SelFastShared {
-  unsigned long long wm[33];  // warp totals of the bin scan (mass) -> exclusive prefixes, [32] = total
-  int wc[33];                 // (count)
+  unsigned long long wm[33], wx[33];  // warp totals of the bin scan (mass); their exclusive prefixes, [kW] = total
+  int wc[33], wcx[33];                // (count)
   unsigned long long before1, mass1, at1;
   int b1, n1, n2, pad;
 };
@@ -497,6 +508,16 @@ __device__ __forceinline__ void select_fast_zero(unsigned* hm, int* hc, SelFastS
 // lmall [K] log-masses, M their max.  Scratch (shared): um [K] u64, hm
 // [2 NB] u32 (zeroed), hc [NB + 1] int (zeroed), cur [NB] int, clist [K] int.
 // Writes stown[i] (2 exact / 1 approx / 0 dropped).  Every thread calls it.
+// smallest integer >= t (t a non-negative double): "x >= t" <=> "x >= ceil_u64(t)"
+// for an integer x, so every threshold test below is an integer compare (a
+// u64 -> fp64 conversion per bin / element costs more than the rest of the
+// phase on sm_100)
+__device__ __forceinline__ unsigned long long ceil_u64(double t) {
+  if (!(t > 0.0)) return 0ull;
+  const double c = ceil(t);
+  return c >= 1.8e19 ? ~0ull : (unsigned long long)c;
+}
+
 template <int kT, int NB, int kEPT>
 __device__ void select_fast(const int K, const double M, const double* lmall, const double p1, const double p2,
                             unsigned long long* um, unsigned* hm, int* hc, int* cur, int* clist, uint8_t* stown,
@@ -512,12 +533,12 @@ __device__ void select_fast(const int K, const double M, const double* lmall, co
   int eb[kEPT];
   unsigned long long eu[kEPT];
   sel_stamp(0);
+  SELP(0, S);
   // (1) masses, bins, histogram
 #pragma unroll
   for (int s = 0; s < kEPT; ++s) {
     eb[s] = NB;
     eu[s] = 0ull;
-    if (s * kT >= K) break;
     const int i = tid + s * kT;
     if (i < K) {
       const float xf = M == -CUDART_INF ? CUDART_INF_F : (float)(M - lmall[i]);  // >= 0 (+inf: no mass)
@@ -535,17 +556,25 @@ __device__ void select_fast(const int K, const double M, const double* lmall, co
     }
   }
   __syncthreads();
+  SELP(1, S);
   sel_stamp(1);
   // (2) exclusive bin prefixes, total, the stage-1 boundary bin
+  static_assert(kBPT == 4, "bins are read and written as 16-byte vectors (4 per thread)");
   unsigned long long bm[kBPT], mloc = 0ull;
   int bc[kBPT], cloc = 0;
+  {  // one 16-B vector per array per thread: contiguous across the warp, no bank conflicts
+    const uint4 h4 = *reinterpret_cast<const uint4*>(hmh + tid * kBPT);
+    const uint4 l4 = *reinterpret_cast<const uint4*>(hml + tid * kBPT);
+    const int4 c4 = *reinterpret_cast<const int4*>(hc + tid * kBPT);
+    const unsigned hh[4] = {h4.x, h4.y, h4.z, h4.w}, ll[4] = {l4.x, l4.y, l4.z, l4.w};
+    const int cc[4] = {c4.x, c4.y, c4.z, c4.w};
 #pragma unroll
-  for (int j = 0; j < kBPT; ++j) {
-    const int b = tid * kBPT + j;
-    bm[j] = ((unsigned long long)hmh[b] << 20) + hml[b];
-    bc[j] = hc[b];
-    mloc += bm[j];
-    cloc += bc[j];
+    for (int j = 0; j < kBPT; ++j) {
+      bm[j] = ((unsigned long long)hh[j] << 20) + ll[j];
+      bc[j] = cc[j];
+      mloc += bm[j];
+      cloc += bc[j];
+    }
   }
   sel_sub(0);
   unsigned long long mi = mloc;
@@ -565,54 +594,52 @@ __device__ void select_fast(const int K, const double M, const double* lmall, co
     S->wc[warp] = ci;
   }
   __syncthreads();  // (every histogram read is done: the prefixes below overwrite it in place)
+  SELP(2, S);
   sel_sub(2);
-  if (warp == 0) {  // exclusive prefix of the warp totals
-    const unsigned long long w = lane < kW ? S->wm[lane] : 0ull;
-    const int wc = lane < kW ? S->wc[lane] : 0;
-    unsigned long long wi = w;
-    int wci = wc;
+  if (tid <= kW) {  // thread w: exclusive prefix of the warp totals (independent loads, no shuffles)
+    unsigned long long e = 0ull;
+    int ec = 0;
 #pragma unroll
-    for (int o = 1; o < kW; o <<= 1) {
-      const unsigned long long tm = __shfl_up_sync(0xffffffffu, wi, o);
-      const int tc = __shfl_up_sync(0xffffffffu, wci, o);
-      if (lane >= o) {
-        wi += tm;
-        wci += tc;
+    for (int w = 0; w < kW; ++w)
+      if (w < tid) {
+        e += S->wm[w];
+        ec += S->wc[w];
       }
-    }
-    if (lane < kW) {
-      S->wm[lane] = wi - w;
-      S->wc[lane] = wci - wc;
-    }
-    if (lane == kW - 1) {
-      S->wm[32] = wi;
-      S->wc[32] = wci;
-    }
+    S->wx[tid] = e;  // wx[kW] = the total
+    S->wcx[tid] = ec;
   }
   __syncthreads();
   sel_sub(3);
-  const unsigned long long T = S->wm[32];
-  unsigned long long mex = S->wm[warp] + mi - mloc;
-  int cex = S->wc[warp] + ci - cloc;
+  SELP(3, S);
+  const unsigned long long T = S->wx[kW];
+  unsigned long long mex = S->wx[warp] + mi - mloc;
+  int cex = S->wcx[warp] + ci - cloc;
   const double thr1 = p1 * (double)T;
+  const unsigned long long T1 = ceil_u64(thr1);
+  unsigned long long pmv[kBPT];
+  int pcv[kBPT];
 #pragma unroll
   for (int j = 0; j < kBPT; ++j) {
     const int b = tid * kBPT + j;
     const unsigned long long inc = mex + bm[j];
-    if (bm[j] && (double)mex < thr1 && thr1 <= (double)inc) {  // the unique crossing bin
+    if (bm[j] && mex < T1 && T1 <= inc) {  // the unique crossing bin
       S->b1 = b;
       S->before1 = mex;
       S->mass1 = bm[j];
     }
-    pm[b] = mex;
-    pc[b] = cex;
-    cur[b] = 0;
+    pmv[j] = mex;
+    pcv[j] = cex;
     mex = inc;
     cex += bc[j];
   }
-  if (tid == kT - 1) pc[NB] = S->wc[32];
+  reinterpret_cast<ulonglong2*>(pm + tid * kBPT)[0] = make_ulonglong2(pmv[0], pmv[1]);
+  reinterpret_cast<ulonglong2*>(pm + tid * kBPT)[1] = make_ulonglong2(pmv[2], pmv[3]);
+  *reinterpret_cast<int4*>(pc + tid * kBPT) = make_int4(pcv[0], pcv[1], pcv[2], pcv[3]);
+  *reinterpret_cast<int4*>(cur + tid * kBPT) = make_int4(0, 0, 0, 0);
+  if (tid == kT - 1) pc[NB] = S->wcx[kW];
   sel_sub(4);
   __syncthreads();
+  SELP(4, S);
   sel_stamp(2);
   const int b1 = S->b1;
   if (T == 0ull || b1 >= NB) {  // no mass at all (a non-finite query)
@@ -624,24 +651,32 @@ __device__ void select_fast(const int K, const double M, const double* lmall, co
     return;
   }
   // (3) candidates: b1 and the bins whose (excl, incl] meets (tlo, thi]
-  const double tlo = p2 * (double)S->before1, thi = p2 * (double)(S->before1 + S->mass1);
-  int cls[kEPT];  // 0 exact by bin, 1 approx by bin, 2 dropped by bin, 3 candidate
+  const unsigned long long Tlo = ceil_u64(p2 * (double)S->before1), Thi = ceil_u64(p2 * (double)(S->before1 + S->mass1));
+  // every non-candidate's state follows from its bin and is written now;
+  // the later passes touch only this thread's candidates (bit s of cmask)
+  const uint8_t zst = p1 >= 1.0 ? (p2 >= 1.0 ? 2 : 1) : 0;
+  unsigned cmask = 0u;
 #pragma unroll
   for (int s = 0; s < kEPT; ++s) {
-    cls[s] = 2;
-    if (s * kT >= K) break;
+    const int i = tid + s * kT;
+    if (i >= K) continue;
     const int b = eb[s];
-    if (eu[s] && b <= b1) {
+    uint8_t st = 0;
+    if (!eu[s]) {
+      st = zst;
+    } else if (b <= b1) {
       const unsigned long long inc = b + 1 < NB ? pm[b + 1] : T;
-      if (b == b1 || ((double)inc >= tlo && (double)pm[b] < thi)) {
-        cls[s] = 3;
-        clist[pc[b] + atomicAdd(&cur[b], 1)] = tid + s * kT;
+      if (b == b1 || (inc >= Tlo && pm[b] < Thi)) {
+        cmask |= 1u << s;
+        clist[pc[b] + atomicAdd(&cur[b], 1)] = i;
       } else {
-        cls[s] = (double)inc < tlo ? 0 : 1;
+        st = inc < Tlo ? 2 : 1;  // before the candidate range: exact; between it and b1: approx
       }
     }
+    if (!((cmask >> s) & 1u)) stown[i] = st;
   }
   __syncthreads();
+  SELP(5, S);
   sel_stamp(3);
   // (4) rank inside the bin -> sorted position and exclusive cumulative mass;
   //     the stage-1 crossing element
@@ -651,8 +686,7 @@ __device__ void select_fast(const int K, const double M, const double* lmall, co
   for (int s = 0; s < kEPT; ++s) {
     pos[s] = 0;
     ex[s] = 0ull;
-    if (s * kT >= K) break;
-    if (cls[s] == 3) {
+    if ((cmask >> s) & 1u) {
       const int ia = tid + s * kT, b = eb[s];
       const double la = lmall[ia];
       const int j0 = pc[b], j1 = pc[b + 1];
@@ -669,41 +703,33 @@ __device__ void select_fast(const int K, const double M, const double* lmall, co
       pos[s] = j0 + rk;
       ex[s] = pm[b] + pre;
       const unsigned long long inc = ex[s] + eu[s];
-      if ((double)ex[s] < thr1 && thr1 <= (double)inc) {
+      if (ex[s] < T1 && T1 <= inc) {
         S->n1 = pos[s] + 1;
         S->at1 = inc;
       }
     }
   }
   __syncthreads();
+  SELP(6, S);
   sel_stamp(4);
   // (5) the stage-2 crossing element (p2 of the retained mass, engine.py:191)
   const int n1 = p1 >= 1.0 ? K : S->n1;
-  const double thr2 = p2 * (double)S->at1;
+  const unsigned long long T2 = ceil_u64(p2 * (double)S->at1);
 #pragma unroll
   for (int s = 0; s < kEPT; ++s) {
-    if (s * kT >= K) break;
-    if (cls[s] == 3 && (double)ex[s] < thr2 && thr2 <= (double)(ex[s] + eu[s])) S->n2 = pos[s] + 1;
+    if (((cmask >> s) & 1u) && ex[s] < T2 && T2 <= ex[s] + eu[s]) S->n2 = pos[s] + 1;
   }
   __syncthreads();
+  SELP(7, S);
   sel_stamp(5);
   const int n2 = p1 >= 1.0 && p2 >= 1.0 ? K : S->n2;
-  // (6) states: candidates by position; the others by bin; zero-mass ones
-  //     past every cut
-  const uint8_t zst = p1 >= 1.0 ? (p2 >= 1.0 ? 2 : 1) : 0;
+  // (6) the candidates' states (the others were written in (3))
 #pragma unroll
   for (int s = 0; s < kEPT; ++s) {
-    if (s * kT >= K) break;
-    const int i = tid + s * kT;
-    if (i < K) {
-      uint8_t st;
-      if (!eu[s]) st = zst;
-      else if (cls[s] == 3) st = pos[s] < n2 ? 2 : (pos[s] < n1 ? 1 : 0);
-      else st = cls[s] == 0 ? 2 : (cls[s] == 1 ? 1 : 0);
-      stown[i] = st;
-    }
+    if ((cmask >> s) & 1u) stown[tid + s * kT] = pos[s] < n2 ? 2 : (pos[s] < n1 ? 1 : 0);
   }
   __syncthreads();
+  SELP(8, S);
   sel_stamp(6);
   n1_out = n1;
   n2_out = n2;
