@@ -452,40 +452,47 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
         }
       }
     } else {
-      // sparse: scale to the plan's reference max and add into the head's
-      // accumulators with 4-wide fire-and-forget reductions (the merge then
-      // reads one (o, l) per q head instead of every CTA's partial)
-      const int d4 = d >> 2;
+      // sparse: scale to the plan's reference max and fold into the head's
+      // self-completing accumulators.  Each 16-B vector holds (o[c], o[c+1],
+      // l, count); every CTA of the head adds (its o, its l, 1) with ONE
+      // returning vector atomic, and the CTA whose add brings the count to
+      // the head's CTA total holds the complete sums in the returned value
+      // plus its own: it writes out[c..c+1] (and the lse) and clears the
+      // vector.  Atomics on one address are totally ordered, so no fence,
+      // completion counter or second round trip is needed.
+      const int d2 = d >> 1;
+      const float parts = (float)head_parts(bh);
 #pragma unroll 1
-      for (int i = tid; i < G * d4; i += kConsumers) {
-        const int h = i / d4, c = (i - h * d4) * 4;
+      for (int i = tid; i < G * d2; i += kConsumers) {
+        const int h = i / d2, c = (i - h * d2) * 2;
         const float Mr = bh == seg_bh[0] ? s_refm[0][h] : (bh == seg_bh[1] ? s_refm[1][h]
                                                                             : __ldcg(&wl.refm[(size_t)bh * G + h]));
-        bool any = false;
-        float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
-        float L = 0.f;
+        float o0 = 0.f, o1 = 0.f, L = 0.f;
 #pragma unroll
         for (int ww = 0; ww < kWarps; ++ww) {
           const float wm = s_wm[ww][h];
           if (wm != -INFINITY) {
-            any = true;
             const float f = exp2f(wm - Mr);
-            const float4 x = *reinterpret_cast<const float4*>(scratch + ((size_t)ww * 8 + h) * d + c);
-            sum.x += f * x.x;
-            sum.y += f * x.y;
-            sum.z += f * x.z;
-            sum.w += f * x.w;
+            const float2 x = *reinterpret_cast<const float2*>(scratch + ((size_t)ww * 8 + h) * d + c);
+            o0 += f * x.x;
+            o1 += f * x.y;
             L += f * s_wl[ww][h];
           }
         }
-        if (any) {
-          float* ac = wl.acc + ((size_t)bh * G + h) * acc_stride(d);
-          red_add_v4(ac + c, sum);
-          if (c == 0) atomicAdd(ac + d, L);
+        float* ac = wl.acc + ((size_t)bh * G + h) * acc_stride(d) + 2 * c;
+        const float4 old = atom_add_v4(ac, make_float4(o0, o1, L, 1.f));
+        if (old.w == parts - 1.f) {  // the last contribution: the sums are complete
+          const float lt = old.z + L;
+          const float rl = lt > 0.f ? 1.f / lt : 0.f;
+          *reinterpret_cast<float2*>(out + ((size_t)bh * G + h) * d + c) = make_float2((old.x + o0) * rl,
+                                                                                      (old.y + o1) * rl);
+          if (c == 0) lse[(size_t)bh * G + h] = lt > 0.f ? Mr * 0.69314718055994531f + __logf(lt) : -INFINITY;
+          *reinterpret_cast<float4*>(ac) = make_float4(0.f, 0.f, 0.f, 0.f);  // zero for the next launch
         }
       }
     }
     consumers_sync();  // scratch (this stage) and s_wm/s_wl free again
+    if (!kDense) return;  // sparse heads complete inside the flush
     if (nflushed < 2) {
       flushed[nflushed++] = bh;
     } else {  // many tiny heads in one range: publish the oldest now
@@ -654,7 +661,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
       for (int bh = me; bh < BH; bh += grid)
         if (rp[bh + 1] == rp[bh]) s_merge[atomicAdd(&s_nmerge, 1)] = bh;
   }
-  if (tid < nflushed)  // the (<= 2) completion counters in parallel, one round trip
+  if (kDense && tid < nflushed)  // the (<= 2) completion counters in parallel, one round trip
     if (atom_add_acq_rel(&wl.counters[flushed[tid]], 1) == head_parts(flushed[tid]) - 1)
       s_merge[atomicAdd(&s_nmerge, 1)] = flushed[tid];
   consumers_sync();
@@ -673,41 +680,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
   astamp(6);
   float* ored = reinterpret_cast<float*>(KV);  // [warps][8 heads][d]
   if (tid < nm) wl.counters[s_merge[tid]] = 0;  // self-reset for the next launch
-  if (!kDense) {
-    // sparse heads with rows: out = o / l from the accumulators, one float4
-    // per thread (a single L2 round trip); each thread clears the float4 it
-    // read, the shared l words are cleared after the barrier below
-    const int nq = nm * G, d4 = d >> 2;
-#pragma unroll 1
-    for (int i = tid; i < nq * d4; i += kConsumers) {
-      const int qi = i / d4, c = (i - qi * d4) * 4, mi = qi / G, g = qi - mi * G, bh = s_merge[mi];
-      if (rp[bh + 1] == rp[bh]) continue;  // no rows: slow path below
-      float* ac = wl.acc + ((size_t)bh * G + g) * acc_stride(d);
-      const float4 o4 = __ldcg(reinterpret_cast<const float4*>(ac + c));
-      const float l_ = __ldcg(ac + d);
-      const float rl = l_ > 0.f ? 1.f / l_ : 0.f;
-      *reinterpret_cast<float4*>(ac + c) = make_float4(0.f, 0.f, 0.f, 0.f);
-      *reinterpret_cast<float4*>(out + ((size_t)bh * G + g) * d + c) =
-          make_float4(o4.x * rl, o4.y * rl, o4.z * rl, o4.w * rl);
-      if (c == 0)
-        lse[(size_t)bh * G + g] =
-            l_ > 0.f ? __ldcg(&wl.refm[(size_t)bh * G + g]) * 0.69314718055994531f + __logf(l_) : -INFINITY;
-    }
-    consumers_sync();  // every l read before it is cleared
-    for (int i = tid; i < nq; i += kConsumers) {
-      const int mi = i / G, g = i - mi * G;
-      wl.acc[((size_t)s_merge[mi] * G + g) * acc_stride(d) + d] = 0.f;
-    }
-    // keep only the row-less heads for the slow path
-    consumers_sync();
-    if (tid == 0) {
-      int k = 0;
-      for (int mi = 0; mi < nm; ++mi)
-        if (rp[s_merge[mi] + 1] == rp[s_merge[mi]]) s_merge[k++] = s_merge[mi];
-      s_nmerge = k;
-    }
-    consumers_sync();
-  }
+  // (sparse heads with rows completed in their flushes; s_merge holds only
+  // the dense heads and the sparse heads without any row)
   const int nm2 = s_nmerge;
   // (merged head, q head) pairs are spread over all 8 warps, so a CTA that
   // closes two heads merges them side by side.  Warp w takes pair

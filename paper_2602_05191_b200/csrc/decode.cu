@@ -540,7 +540,7 @@ size_t decode_ws_layout(const dp_cache_view* v, int G, WorkLists* wl, void** par
   char* cpre = take((BH + 1) * sizeof(int));
   char* dn = take(sizeof(int));
   char* ap = take(BH * (size_t)G * (4 + (size_t)v->head_dim) * sizeof(float));  // [m, l, -, -, o]
-  char* ac = take(BH * (size_t)G * acc_stride(v->head_dim) * sizeof(float));  // [o, l, pad]
+  char* ac = take(BH * (size_t)G * acc_stride(v->head_dim) * sizeof(float));  // (o, o, l, count) vectors
   char* rm = take(BH * (size_t)G * sizeof(float));
   const size_t pbytes = BH * max_chunks * G * (2 + (size_t)v->head_dim) * acc;
   char* p = take(pbytes);

@@ -15,7 +15,7 @@ constexpr int kMaxPartSlots = 256;  // persistent attention grid cap (partials p
 
 // Row stride of the sparse accumulators: o[d], l, 3 pad floats (16-B aligned rows
 // for vector reductions).
-__host__ __device__ constexpr int acc_stride(int d) { return d + 4; }
+__host__ __device__ constexpr int acc_stride(int d) { return 2 * d; }  // d/2 vectors (o[c], o[c+1], l, count)
 
 // Device work lists (one set per (b, kv head)), carved from the workspace.
 struct WorkLists {
@@ -31,7 +31,7 @@ struct WorkLists {
   int* chunk_prefix;  // [BH+1] exclusive prefix of nchunks over heads (+ total)
   int* done;      // [1] producer-completion counter (zero between launches)
   float* apart;   // [BH][G][4+d] approx pseudo-row partial per q head (m, l, -, -, o[d]); m = -inf: none
-  float* acc;     // [BH][G][acc_stride(d)] sparse attention accumulators (o[d], l, pad) scaled by 2^-ref (zero between launches)
+  float* acc;     // [BH][G][acc_stride(d)] sparse attention accumulators: d/2 vectors (o[c], o[c+1], l, count) scaled by 2^-ref (zero between launches)
   float* refm;    // [BH][G] reference max (log2 units) of those accumulators, written by the plan
   int max_chunks;
 };

@@ -95,6 +95,16 @@ __device__ __forceinline__ void red_add_v4(float* p, float4 v) {  // p 16-B alig
                : "memory");
 }
 
+// returning 4-wide fp32 atomic add (ATOMG.ADD.F32x4): the old vector
+__device__ __forceinline__ float4 atom_add_v4(float* p, float4 v) {  // p 16-B aligned
+  float4 o;
+  asm volatile("atom.global.v4.f32.add {%0, %1, %2, %3}, [%4], {%5, %6, %7, %8};\n"
+               : "=f"(o.x), "=f"(o.y), "=f"(o.z), "=f"(o.w)
+               : "l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+  return o;
+}
+
 __device__ __forceinline__ int atom_add_acq_rel(int* p, int v) {
   int old;
   asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;\n" : "=r"(old) : "l"(p), "r"(v) : "memory");
