@@ -313,6 +313,7 @@ int dp_lse_merge(const float* out_parts, const float* lse_parts, int32_t parts, 
                  float* lse, void* stream) {
   if (!out_parts || !lse_parts || !out || !lse) return fail(DP_ERR_INVALID, "dp_lse_merge: null buffer");
   if (parts < 1 || rows < 1 || d < 1) return fail(DP_ERR_INVALID, "dp_lse_merge: empty input");
+  if (parts > 64) return fail(DP_ERR_UNSUPPORTED, "dp_lse_merge: at most 64 partials");
   cudaError_t e = dp::launch_lse_merge(out_parts, lse_parts, parts, rows, d, out, lse, (cudaStream_t)stream);
   return e == cudaSuccess ? DP_OK : cuda_fail(e, "dp_lse_merge");
 }

@@ -664,9 +664,20 @@ __global__ void __launch_bounds__(256) approx_partial_kernel(dp_cache_view v, in
   __shared__ double red[33];
   __shared__ float part[8][256];
   double m = -CUDART_INF, mall = -CUDART_INF;
-  for (int k = tid; k < K; k += blockDim.x) {
-    if (st[k] == 1) m = fmax(m, x[k]);
-    mall = fmax(mall, x[k]);
+  for (int k0 = tid; k0 < K; k0 += blockDim.x * 8) {  // 8 loads in flight per thread
+    double xv[8];
+    uint8_t sv[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int k = k0 + j * blockDim.x;
+      xv[j] = k < K ? x[k] : -CUDART_INF;
+      sv[j] = k < K ? st[k] : 0;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (sv[j] == 1) m = fmax(m, xv[j]);
+      mall = fmax(mall, xv[j]);
+    }
   }
   // sink/window rows are always exact: their logits join the reference max
   // (q nullable: the dp_build_worklist entry point has no query)

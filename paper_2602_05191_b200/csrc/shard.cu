@@ -197,6 +197,7 @@ __global__ void __launch_bounds__(kLT) lloyd_sums_kernel(const void* __restrict_
 // ---------------------------------------------------------------------------
 constexpr int kGT = 1024;
 constexpr int kGB = 2048;
+constexpr int kGU = 8;        // element loads in flight per thread
 constexpr int kGCand = 4096;  // candidates staged in shared memory (more: the global-scratch path)
 constexpr size_t kGDyn = (size_t)kGCand * (8 + 8 + 8 + 4 + 4);
 
@@ -256,8 +257,16 @@ __global__ void __launch_bounds__(kGT, 1) select_global_kernel(const double* __r
     s_at1 = 0ull;
   }
   // (0) the row's maximum
+  // every element loop below issues kGU loads before using any of them
+  // (one load per iteration would serialise L2 round trips: 32 per thread)
   double m = -CUDART_INF;
-  for (int i = tid; i < K; i += kGT) m = fmax(m, gsel_sanitise(lm[i]));
+  for (int i0 = tid; i0 < K; i0 += kGT * kGU) {
+    double x[kGU];
+#pragma unroll
+    for (int j = 0; j < kGU; ++j) x[j] = i0 + j * kGT < K ? lm[i0 + j * kGT] : -CUDART_INF;
+#pragma unroll
+    for (int j = 0; j < kGU; ++j) m = fmax(m, gsel_sanitise(x[j]));
+  }
   m = warp_max(m);
   if (lane == 0) s_red[warp] = m;
   __syncthreads();
@@ -265,15 +274,23 @@ __global__ void __launch_bounds__(kGT, 1) select_global_kernel(const double* __r
 #pragma unroll
   for (int w = 0; w < kGT / 32; ++w) M = fmax(M, s_red[w]);
   // (1) histogram
-  for (int i = tid; i < K; i += kGT) {
-    unsigned long long u;
-    int b;
-    gsel_elem(M, gsel_sanitise(lm[i]), u, b);
-    pk[i] = (u << 11) | (unsigned long long)b;
-    if (u) {
-      atomicAdd(&s_hh[b], (unsigned)(u >> 20));
-      atomicAdd(&s_hl[b], (unsigned)(u & 0xFFFFFu));
-      atomicAdd(&s_hc[b], 1);
+  for (int i0 = tid; i0 < K; i0 += kGT * kGU) {
+    double x[kGU];
+#pragma unroll
+    for (int j = 0; j < kGU; ++j) x[j] = i0 + j * kGT < K ? lm[i0 + j * kGT] : -CUDART_INF;
+#pragma unroll
+    for (int j = 0; j < kGU; ++j) {
+      const int i = i0 + j * kGT;
+      if (i >= K) break;
+      unsigned long long u;
+      int b;
+      gsel_elem(M, gsel_sanitise(x[j]), u, b);
+      pk[i] = (u << 11) | (unsigned long long)b;
+      if (u) {
+        atomicAdd(&s_hh[b], (unsigned)(u >> 20));
+        atomicAdd(&s_hl[b], (unsigned)(u & 0xFFFFFu));
+        atomicAdd(&s_hc[b], 1);
+      }
     }
   }
   __syncthreads();
@@ -358,10 +375,11 @@ __global__ void __launch_bounds__(kGT, 1) select_global_kernel(const double* __r
     }
     return;
   }
-  const double tlo = p2 * (double)s_before1, thi = p2 * (double)(s_before1 + s_mass1);
+  // integer thresholds (a u64 -> fp64 conversion per element costs more than the test)
+  const unsigned long long Tlo = ceil_u64(p2 * (double)s_before1), Thi = ceil_u64(p2 * (double)(s_before1 + s_mass1));
   auto is_cand = [&](int b) {
     const unsigned long long inc = b + 1 < kGB ? s_pm[b + 1] : T;
-    return b == b1 || (b < b1 && (double)inc >= tlo && (double)s_pm[b] < thi);
+    return b == b1 || (b < b1 && inc >= Tlo && s_pm[b] < Thi);
   };
   // (3) candidates -> their bin segments of the global sorted order; the
   //     candidate bins are [blo, bhi] and b1, i.e. two contiguous slot ranges
@@ -370,15 +388,21 @@ __global__ void __launch_bounds__(kGT, 1) select_global_kernel(const double* __r
     s_bhi = -1;
   }
   __syncthreads();
-  for (int i = tid; i < K; i += kGT) {
-    const unsigned long long w = pk[i];
-    const unsigned long long u = w >> 11;
-    const int b = (int)(w & 2047u);
-    if (u && b <= b1 && is_cand(b)) {
-      cand[s_hc[b] + (int)atomicAdd(&s_cur[b], 1u)] = i;
-      if (b < b1) {
-        atomicMin(&s_blo, b);
-        atomicMax(&s_bhi, b);
+  for (int i0 = tid; i0 < K; i0 += kGT * kGU) {
+    unsigned long long wv[kGU];
+#pragma unroll
+    for (int j = 0; j < kGU; ++j) wv[j] = i0 + j * kGT < K ? pk[i0 + j * kGT] : 0ull;
+#pragma unroll
+    for (int j = 0; j < kGU; ++j) {
+      const int i = i0 + j * kGT;
+      const unsigned long long u = wv[j] >> 11;
+      const int b = (int)(wv[j] & 2047u);
+      if (u && b <= b1 && is_cand(b)) {
+        cand[s_hc[b] + (int)atomicAdd(&s_cur[b], 1u)] = i;
+        if (b < b1) {
+          atomicMin(&s_blo, b);
+          atomicMax(&s_bhi, b);
+        }
       }
     }
   }
@@ -477,23 +501,30 @@ __global__ void __launch_bounds__(kGT, 1) select_global_kernel(const double* __r
   const int n2 = p1 >= 1.0 && p2 >= 1.0 ? K : s_n2;
   // (6) states: candidates by position, the rest by bin
   const uint8_t zst = p1 >= 1.0 ? (p2 >= 1.0 ? 2 : 1) : 0;
-  for (int i = tid; i < K; i += kGT) {
-    const unsigned long long w = pk[i];
-    const unsigned long long u = w >> 11;
-    const int b = (int)(w & 2047u);
-    uint8_t st;
-    if (!u) {
-      st = zst;
-    } else if (b <= b1 && is_cand(b)) {
-      if (staged) continue;  // written from the staged copy below
-      st = pos[i] < n2 ? 2 : (pos[i] < n1 ? 1 : 0);
-    } else if (b > b1) {
-      st = 0;
-    } else {
-      const unsigned long long inc = b + 1 < kGB ? s_pm[b + 1] : T;
-      st = (double)inc < tlo ? 2 : 1;
+  for (int i0 = tid; i0 < K; i0 += kGT * kGU) {
+    unsigned long long wv[kGU];
+#pragma unroll
+    for (int j = 0; j < kGU; ++j) wv[j] = i0 + j * kGT < K ? pk[i0 + j * kGT] : 0ull;
+#pragma unroll
+    for (int j = 0; j < kGU; ++j) {
+      const int i = i0 + j * kGT;
+      if (i >= K) break;
+      const unsigned long long u = wv[j] >> 11;
+      const int b = (int)(wv[j] & 2047u);
+      uint8_t st;
+      if (!u) {
+        st = zst;
+      } else if (b <= b1 && is_cand(b)) {
+        if (staged) continue;  // written from the staged copy below
+        st = pos[i] < n2 ? 2 : (pos[i] < n1 ? 1 : 0);
+      } else if (b > b1) {
+        st = 0;
+      } else {
+        const unsigned long long inc = b + 1 < kGB ? s_pm[b + 1] : T;
+        st = inc < Tlo ? 2 : 1;
+      }
+      state[i] = st;
     }
-    state[i] = st;
   }
   if (staged)
     for (int t = tid; t < nc; t += kGT) state[s_cid[t]] = s_cpos[t] < n2 ? 2 : (s_cpos[t] < n1 ? 1 : 0);
@@ -509,22 +540,29 @@ __global__ void __launch_bounds__(kGT, 1) select_global_kernel(const double* __r
 __global__ void lse_merge_kernel(const float* __restrict__ out_parts, const float* __restrict__ lse_parts, int P,
                                  int rows, int d, float* __restrict__ out, float* __restrict__ lse) {
   const int row = blockIdx.x;
-  float M = -INFINITY;
-  for (int p = 0; p < P; ++p) M = fmaxf(M, lse_parts[(size_t)p * rows + row]);
-  double L = 0.0;
-  for (int p = 0; p < P; ++p) {
-    const float l = lse_parts[(size_t)p * rows + row];
-    if (l != -INFINITY) L += exp((double)l - (double)M);
-  }
-  for (int c = threadIdx.x; c < d; c += blockDim.x) {
-    double acc = 0.0;
+  __shared__ double s_w[64];
+  __shared__ double s_L;
+  if (threadIdx.x == 0) {  // the P weights once per row (fp64), then every dim reuses them
+    float M = -INFINITY;
+    for (int p = 0; p < P; ++p) M = fmaxf(M, lse_parts[(size_t)p * rows + row]);
+    double L = 0.0;
     for (int p = 0; p < P; ++p) {
       const float l = lse_parts[(size_t)p * rows + row];
-      if (l != -INFINITY) acc += exp((double)l - (double)M) * (double)out_parts[((size_t)p * rows + row) * d + c];
+      const double w = l != -INFINITY ? exp((double)l - (double)M) : 0.0;
+      s_w[p] = w;
+      L += w;
     }
+    s_L = L;
+    lse[row] = L > 0.0 ? (float)((double)M + log(L)) : -INFINITY;
+  }
+  __syncthreads();
+  const double L = s_L;
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    double acc = 0.0;
+    for (int p = 0; p < P; ++p)
+      if (s_w[p] > 0.0) acc += s_w[p] * (double)out_parts[((size_t)p * rows + row) * d + c];
     out[(size_t)row * d + c] = L > 0.0 ? (float)(acc / L) : 0.f;
   }
-  if (threadIdx.x == 0) lse[row] = L > 0.0 ? (float)((double)M + log(L)) : -INFINITY;
 }
 
 // ---------------------------------------------------------------------------
