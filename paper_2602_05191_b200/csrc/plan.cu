@@ -294,6 +294,10 @@ __global__ void __launch_bounds__(kPT, 1)
     // let the attention grid become resident on the SMs this launch leaves free
     // (its CTAs wait for our completion before reading anything we write)
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    if (dbg & 64) {  // timing experiment: the launch + dependency-wait floor
+      cl_wait();
+      return;
+    }
     if (r == 0) {  // sink and window rows open every head's union list (plan-independent)
       const unsigned tag = (unsigned)((1 << G) - 1) << 24;
       unsigned* rw = reinterpret_cast<unsigned*>(wl.rowidx) + (size_t)bh * v.row_cap;
@@ -334,6 +338,10 @@ __global__ void __launch_bounds__(kPT, 1)
     }
   }
   __syncthreads();  // qd, offs, barrier init
+  if (dbg & 128) {  // timing experiment: + the query load
+    cl_wait();
+    return;
+  }
   stamp(r, 1);
   cl_wait();  // (S)
   stamp(r, 2);
@@ -652,7 +660,10 @@ __global__ void __launch_bounds__(kPT, 1)
   int2* apx = wl.approx + (size_t)bh * cap;
 #pragma unroll 1
   for (int i0 = 0; i0 < nloc; i0 += kPT) {
-    const int i = i0 + tid;
+    // lane l of warp w takes cluster i0 + l * kPW + w: a slice's clusters
+    // spread over all 16 warps (a small slice would otherwise leave most
+    // warps idle while 4 of them expand every row)
+    const int i = i0 + lane * kPW + warp;
     int me = 0, ma = 0, len = 0, st0 = 0, ro = 0;
     if (i < nloc) {
 #pragma unroll 1

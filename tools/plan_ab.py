@@ -61,7 +61,7 @@ attend()
 torch.cuda.synchronize()
 print(f"context {n} G {G}: plan cluster size {lib.dp_debug_plan_occupancy(view, G, 0)}; us per launch in graph")
 for bits, name in ((0, "full plan"), (32, "no centroid L2 prefetch"), (16, "no count-exchange wait"), (8, "no row expansion"), (4, "no work lists"), (2, "no selection"),
-                   (6, "no selection, no lists")):
+                   (6, "no selection, no lists"), (128, "launch + wait + q load only"), (64, "launch + wait only")):
     lib.dp_debug_set(10, bits)
     print(f"  {name:28s} {timed(lambda: [plan() for _ in range(L)]):7.2f}")
 lib.dp_debug_set(10, 0)
