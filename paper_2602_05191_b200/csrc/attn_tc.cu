@@ -491,8 +491,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
         }
       }
     }
-    consumers_sync();  // scratch (this stage) and s_wm/s_wl free again
+    // No barrier here: the scratch (this stage's K buffer) is handed back by
+    // each warp's empty-barrier arrive after the flush, and the producer
+    // refills it only once all 8 warps arrived, i.e. finished reading it;
+    // s_wm/s_wl are rewritten only after the next flush's first barrier.
     if (!kDense) return;  // sparse heads complete inside the flush
+    consumers_sync();
     if (nflushed < 2) {
       flushed[nflushed++] = bh;
     } else {  // many tiny heads in one range: publish the oldest now

@@ -140,16 +140,17 @@ class DecodeGraph:
     per-call host work.  ``q`` [L,B,Hq,d] and ``out`` [L,B,Hq,d] fp32 are fixed
     device buffers.  Optional pinned host buffers move inside the graph:
     ``host_q`` is copied in (layer 0's slice first, the rest on a side stream
-    while layer 0 runs) and each layer's output is copied to ``host_out`` on a
-    side stream as soon as that layer finishes, so only the last layer's copy
-    is exposed.  Layers share one geometry (and one workspace, reused layer
+    while layer 0 runs) and the outputs are copied to ``host_out`` on a side
+    stream every ``out_every`` layers, so only the last batch's copy is
+    exposed.  Layers share one geometry (and one workspace, reused layer
     after layer as in the eager path).
 
     The captured launches hold each layer's token count, so a graph is valid
     for one cache state: after ``ClusteredLayer.append`` (decode-time growth)
     ``replay()`` raises -- rebuild the graph (or call ``recapture()``)."""
 
-    def __init__(self, layers, q, p1=0.95, p2=0.7, *, out=None, workspace=None, host_q=None, host_out=None):
+    def __init__(self, layers, q, p1=0.95, p2=0.7, *, out=None, workspace=None, host_q=None, host_out=None,
+                 out_every=8):
         for name, val in (("p1", p1), ("p2", p2)):
             if not 0.0 < val <= 1.0:
                 raise ValueError(f"{name} must be in (0, 1], got {val}")
@@ -169,6 +170,10 @@ class DecodeGraph:
             if t is not None and (t.shape != q.shape or t.dtype != dt or t.is_cuda or not t.is_pinned()):
                 raise ValueError(f"{name} must be a pinned host tensor of shape {tuple(q.shape)} and dtype {dt}")
         self.host_q, self.host_out = host_q, host_out
+        # layers per device->host output copy: every copy forks a side-stream
+        # branch off the layer chain, which breaks the programmatic (PDL)
+        # overlap of the next layer's launch, so copies are batched
+        self.out_every = max(1, int(out_every))
         self.p1, self.p2 = p1, p2
         self._s_in, self._s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
         self._step()  # eager warm-up (allocates nothing): caches attributes, tensor maps, views
@@ -199,10 +204,11 @@ class DecodeGraph:
             if li == 1 and hq is not None:
                 main.wait_stream(self._s_in)
             _sparse_layer(self.q[li], lay, self.p1, self.p2, workspace=self.ws, out=self.out[li])
-            if ho is not None:
+            if ho is not None and ((li + 1) % self.out_every == 0 or li + 1 == len(self.layers)):
+                l0 = (li // self.out_every) * self.out_every
                 self._s_out.wait_stream(main)
                 with torch.cuda.stream(self._s_out):
-                    ho[li].copy_(self.out[li], non_blocking=True)
+                    ho[l0:li + 1].copy_(self.out[l0:li + 1], non_blocking=True)
         if ho is not None:
             main.wait_stream(self._s_out)
 
