@@ -232,3 +232,41 @@ def test_one_launch_step_parity(n, H, G):
         check_layer(lay, k, v, q[0], 1.0, 1.0, torch.bfloat16, f"one-launch step {n} H{H} G{G}")
     finally:
         lib.dp_debug_set(6, 1)
+
+
+def test_parity_beyond_fused_plan_cap_200k():
+    """(vi) contexts past the fused plan's 4096-cluster table (131K-524K):
+    dp_decode_step falls back to score -> select -> worklist -> attention.
+    200K tokens, 2 kv heads (K ~ 6250), G=4."""
+    lay, k, v, q = _bench_layer(1, 2, 200000, 4)
+    assert int(lay.nclusters.max()) > 4096
+    check_layer(lay, k, v, q[0], 0.95, 0.7, torch.bfloat16, "200K G=4 (unfused, K>4096)")
+
+
+@pytest.mark.parametrize("kind", ["zero", "uniform"])
+def test_flat_scores_at_the_widest_table(kind):
+    """Flat score profiles at K ~ 4094 put many clusters in one 1/32-nat bin
+    (the boundary ranking's worst case): a zero query (log-mass = log|C|
+    only) and the reference's `uniform` tail profile; parity and no
+    pathological slowdown (the plan must stay within 3x its peaked time)."""
+    import time
+
+    from paper_2602_05191_b200 import sparse_attention
+
+    prof = "uniform" if kind == "uniform" else "peaked"
+    lay, k, v, q = _bench_layer(1, 2, 131072, 4, profile=prof)
+    q0 = torch.zeros_like(q[0]) if kind == "zero" else q[0]
+    check_layer(lay, k, v, q0, 0.95, 0.7, torch.bfloat16, f"128K flat ({kind})")
+
+    def t(qq):
+        sparse_attention(qq, lay, 0.95, 0.7)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(20):
+            sparse_attention(qq, lay, 0.95, 0.7)
+        torch.cuda.synchronize()
+        return (time.perf_counter() - t0) / 20
+
+    flat, peaked = t(q0), t(_bench_layer(1, 2, 131072, 4)[3][0])
+    print(f"[FLAT] {kind}: {flat * 1e6:.1f} us per step vs peaked {peaked * 1e6:.1f} us")
+    assert flat < 3 * peaked + 200e-6
