@@ -535,6 +535,387 @@ __global__ void __launch_bounds__(kGT, 1) select_global_kernel(const double* __r
 }
 
 // ---------------------------------------------------------------------------
+// The same selection split over many CTAs per row (large K: the single-CTA
+// kernel is instruction-bound on ONE SM per q head, ~45 us at K = 32,766).
+// Five launches: max -> histogram -> bin scan -> candidates/states ->
+// candidate ranking; per-row state lives in global scratch (GSelRow).
+// ---------------------------------------------------------------------------
+struct GSelRow {
+  unsigned long long mkey;  // ordered-int max of the row (atomicMax); 0 = unset
+  unsigned long long T, before1, mass1, Tlo, Thi;
+  int b1, blo, bhi, pad;
+};
+__device__ __forceinline__ unsigned long long dkey(double x) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double dfromkey(unsigned long long k) {
+  return __longlong_as_double((long long)((k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k));
+}
+constexpr int kST2 = 256;  // threads of the split kernels
+
+__global__ void __launch_bounds__(kST2) gs_max_kernel(const double* __restrict__ lm, int ld, const int* __restrict__ Ks,
+                                                     GSelRow* __restrict__ rd, unsigned long long* __restrict__ hm,
+                                                     int* __restrict__ hc, int* __restrict__ cur) {
+  const int row = blockIdx.y, S = gridDim.x, sp = blockIdx.x, tid = threadIdx.x;
+  const int K = Ks[row];
+  // zero my share of the row's histogram, counts and cursors
+  for (int b = sp * (kGB / S) + tid; b < (sp + 1) * (kGB / S); b += kST2) {
+    hm[(size_t)row * kGB + b] = 0ull;
+    hc[(size_t)row * (kGB + 1) + b] = 0;
+    cur[(size_t)row * kGB + b] = 0;
+  }
+  const int i0 = (int)((long long)K * sp / S), i1 = (int)((long long)K * (sp + 1) / S);
+  double m = -CUDART_INF;
+  for (int i = i0 + tid; i < i1; i += kST2 * kGU) {
+    double x[kGU];
+#pragma unroll
+    for (int j = 0; j < kGU; ++j) x[j] = i + j * kST2 < i1 ? lm[(size_t)row * ld + i + j * kST2] : -CUDART_INF;
+#pragma unroll
+    for (int j = 0; j < kGU; ++j) m = fmax(m, gsel_sanitise(x[j]));
+  }
+  m = warp_max(m);
+  if ((tid & 31) == 0) atomicMax(&rd[row].mkey, dkey(m));
+}
+
+__global__ void __launch_bounds__(kST2) gs_hist_kernel(const double* __restrict__ lm, int ld, const int* __restrict__ Ks,
+                                                      const GSelRow* __restrict__ rd,
+                                                      unsigned long long* __restrict__ hm, int* __restrict__ hc,
+                                                      unsigned long long* __restrict__ pk_ws) {
+  const int row = blockIdx.y, S = gridDim.x, sp = blockIdx.x, tid = threadIdx.x;
+  const int K = Ks[row];
+  __shared__ unsigned s_h[kGB], s_l[kGB];
+  __shared__ int s_c[kGB];
+  for (int b = tid; b < kGB; b += kST2) {
+    s_h[b] = 0u;
+    s_l[b] = 0u;
+    s_c[b] = 0;
+  }
+  __syncthreads();
+  const double M = dfromkey(rd[row].mkey);
+  unsigned long long* pk = pk_ws + (size_t)row * ld;
+  const int i0 = (int)((long long)K * sp / S), i1 = (int)((long long)K * (sp + 1) / S);
+  for (int i = i0 + tid; i < i1; i += kST2 * kGU) {
+    double x[kGU];
+#pragma unroll
+    for (int j = 0; j < kGU; ++j) x[j] = i + j * kST2 < i1 ? lm[(size_t)row * ld + i + j * kST2] : -CUDART_INF;
+#pragma unroll
+    for (int j = 0; j < kGU; ++j) {
+      const int ii = i + j * kST2;
+      if (ii >= i1) break;
+      unsigned long long u;
+      int b;
+      gsel_elem(M, gsel_sanitise(x[j]), u, b);
+      pk[ii] = (u << 11) | (unsigned long long)b;
+      if (u) {
+        atomicAdd(&s_h[b], (unsigned)(u >> 20));
+        atomicAdd(&s_l[b], (unsigned)(u & 0xFFFFFu));
+        atomicAdd(&s_c[b], 1);
+      }
+    }
+  }
+  __syncthreads();
+  for (int b = tid; b < kGB; b += kST2)
+    if (s_c[b]) {
+      atomicAdd(&hm[(size_t)row * kGB + b], ((unsigned long long)s_h[b] << 20) + s_l[b]);
+      atomicAdd(&hc[(size_t)row * (kGB + 1) + b], s_c[b]);
+    }
+}
+
+// one CTA (1024 threads) per row: exclusive bin prefixes (in place: hm -> pm,
+// hc -> pc), total, the stage-1 bin and the stage-2 candidate range
+__global__ void __launch_bounds__(kGT) gs_scan_kernel(const int* __restrict__ Ks, double p1, double p2,
+                                                     GSelRow* __restrict__ rd, unsigned long long* __restrict__ hm,
+                                                     int* __restrict__ hc) {
+  const int row = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int kBPT = kGB / kGT;
+  __shared__ unsigned long long s_wm[33];
+  __shared__ int s_wc[33];
+  unsigned long long* pm = hm + (size_t)row * kGB;
+  int* pc = hc + (size_t)row * (kGB + 1);
+  unsigned long long bm[kBPT], mloc = 0ull;
+  int bc[kBPT], cloc = 0;
+#pragma unroll
+  for (int j = 0; j < kBPT; ++j) {
+    bm[j] = pm[tid * kBPT + j];
+    bc[j] = pc[tid * kBPT + j];
+    mloc += bm[j];
+    cloc += bc[j];
+  }
+  unsigned long long mi = mloc;
+  int ci = cloc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long tm = __shfl_up_sync(0xffffffffu, mi, o);
+    const int tc = __shfl_up_sync(0xffffffffu, ci, o);
+    if (lane >= o) {
+      mi += tm;
+      ci += tc;
+    }
+  }
+  if (lane == 31) {
+    s_wm[warp] = mi;
+    s_wc[warp] = ci;
+  }
+  if (tid == 0) {
+    rd[row].b1 = kGB;
+    rd[row].blo = kGB;
+    rd[row].bhi = -1;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const unsigned long long w = s_wm[lane];
+    const int wc = s_wc[lane];
+    unsigned long long wi = w;
+    int wci = wc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long tm = __shfl_up_sync(0xffffffffu, wi, o);
+      const int tc = __shfl_up_sync(0xffffffffu, wci, o);
+      if (lane >= o) {
+        wi += tm;
+        wci += tc;
+      }
+    }
+    s_wm[lane] = wi - w;
+    s_wc[lane] = wci - wc;
+    if (lane == 31) {
+      s_wm[32] = wi;
+      s_wc[32] = wci;
+    }
+  }
+  __syncthreads();
+  const unsigned long long T = s_wm[32];
+  unsigned long long mex = s_wm[warp] + mi - mloc;
+  int cex = s_wc[warp] + ci - cloc;
+  const unsigned long long T1 = ceil_u64(p1 * (double)T);
+#pragma unroll
+  for (int j = 0; j < kBPT; ++j) {
+    const int b = tid * kBPT + j;
+    const unsigned long long inc = mex + bm[j];
+    if (bm[j] && mex < T1 && T1 <= inc) {
+      rd[row].b1 = b;
+      rd[row].before1 = mex;
+      rd[row].mass1 = bm[j];
+      rd[row].Tlo = ceil_u64(p2 * (double)mex);
+      rd[row].Thi = ceil_u64(p2 * (double)inc);
+    }
+    pm[b] = mex;
+    pc[b] = cex;
+    mex = inc;
+    cex += bc[j];
+  }
+  if (tid == kGT - 1) pc[kGB] = s_wc[32];
+  if (tid == 0) rd[row].T = T;
+}
+
+// candidates -> their global slots; every other element's state from its bin
+__global__ void __launch_bounds__(kST2) gs_cand_kernel(const int* __restrict__ Ks, int ld, double p1, double p2,
+                                                      GSelRow* __restrict__ rd,
+                                                      const unsigned long long* __restrict__ hm,
+                                                      const int* __restrict__ hc, int* __restrict__ cur,
+                                                      const unsigned long long* __restrict__ pk_ws,
+                                                      int* __restrict__ cand_ws, uint8_t* __restrict__ state_all) {
+  const int row = blockIdx.y, S = gridDim.x, sp = blockIdx.x, tid = threadIdx.x;
+  const int K = Ks[row];
+  const int b1 = rd[row].b1;
+  const unsigned long long T = rd[row].T, Tlo = rd[row].Tlo, Thi = rd[row].Thi;
+  const unsigned long long* pm = hm + (size_t)row * kGB;
+  const int* pc = hc + (size_t)row * (kGB + 1);
+  const unsigned long long* pk = pk_ws + (size_t)row * ld;
+  int* cand = cand_ws + (size_t)row * ld;
+  uint8_t* state = state_all + (size_t)row * ld;
+  const uint8_t zst = p1 >= 1.0 ? (p2 >= 1.0 ? 2 : 1) : 0;
+  const bool none = T == 0ull || b1 >= kGB;
+  const int i0 = (int)((long long)K * sp / S), i1 = (int)((long long)K * (sp + 1) / S);
+  int lo = kGB, hi = -1;
+  for (int i = i0 + tid; i < i1; i += kST2 * kGU) {
+    unsigned long long wv[kGU];
+#pragma unroll
+    for (int j = 0; j < kGU; ++j) wv[j] = i + j * kST2 < i1 ? pk[i + j * kST2] : 0ull;
+#pragma unroll
+    for (int j = 0; j < kGU; ++j) {
+      const int ii = i + j * kST2;
+      if (ii >= i1) break;
+      const unsigned long long u = wv[j] >> 11;
+      const int b = (int)(wv[j] & 2047u);
+      uint8_t st = 0;
+      if (none) {
+        st = zst;
+      } else if (!u) {
+        st = zst;
+      } else if (b <= b1) {
+        const unsigned long long inc = b + 1 < kGB ? pm[b + 1] : T;
+        if (b == b1 || (inc >= Tlo && pm[b] < Thi)) {
+          cand[pc[b] + atomicAdd(&cur[(size_t)row * kGB + b], 1)] = ii;
+          if (b < b1) {
+            lo = min(lo, b);
+            hi = max(hi, b);
+          }
+          continue;  // ranked by the last kernel
+        }
+        st = inc < Tlo ? 2 : 1;
+      }
+      state[ii] = st;
+    }
+  }
+  if (hi >= 0) {
+    atomicMin(&rd[row].blo, lo);
+    atomicMax(&rd[row].bhi, hi);
+  }
+}
+
+// one CTA per row: stage the candidates, rank them, both cuts, their states
+__global__ void __launch_bounds__(kGT, 1) gs_rank_kernel(const double* __restrict__ lm, int ld, const int* __restrict__ Ks,
+                                                        double p1, double p2, GSelRow* __restrict__ rd,
+                                                        const unsigned long long* __restrict__ hm,
+                                                        const int* __restrict__ hc,
+                                                        const unsigned long long* __restrict__ pk_ws,
+                                                        const int* __restrict__ cand_ws,
+                                                        uint8_t* __restrict__ state_all, int* __restrict__ counts,
+                                                        int* __restrict__ fail) {
+  const int row = blockIdx.x, tid = threadIdx.x;
+  const int K = Ks[row];
+  extern __shared__ __align__(16) unsigned char g_dyn[];
+  unsigned long long* s_cu = reinterpret_cast<unsigned long long*>(g_dyn);
+  unsigned long long* s_cex = s_cu + kGCand;
+  double* s_clm = reinterpret_cast<double*>(s_cex + kGCand);
+  int* s_cid = reinterpret_cast<int*>(s_clm + kGCand);
+  int* s_cpos = s_cid + kGCand;
+  __shared__ int s_n1, s_n2;
+  __shared__ unsigned long long s_at1;
+  const unsigned long long* pm = hm + (size_t)row * kGB;
+  const int* pc = hc + (size_t)row * (kGB + 1);
+  const unsigned long long* pk = pk_ws + (size_t)row * ld;
+  const int* cand = cand_ws + (size_t)row * ld;
+  uint8_t* state = state_all + (size_t)row * ld;
+  const int b1 = rd[row].b1, blo = rd[row].blo, bhi = rd[row].bhi;
+  const unsigned long long T = rd[row].T;
+  if (tid == 0) {
+    s_n1 = 0;
+    s_n2 = 0;
+    s_at1 = 0ull;
+  }
+  __syncthreads();
+  if (T == 0ull || b1 >= kGB) {
+    if (tid == 0) {
+      counts[2 * row] = p1 >= 1.0 ? K : 0;
+      counts[2 * row + 1] = p1 >= 1.0 && p2 >= 1.0 ? K : 0;
+      rd[row].mkey = 0ull;
+    }
+    return;
+  }
+  const int r1a = bhi >= 0 ? pc[blo] : 0, r1b = bhi >= 0 ? pc[bhi + 1] : 0;
+  const int r2a = pc[b1], r2b = pc[b1 + 1];
+  const int n1c = r1b - r1a, nc = n1c + (r2b - r2a);
+  const unsigned long long T1 = ceil_u64(p1 * (double)T);
+  if (nc > kGCand) {  // very flat rows: rank straight from global scratch (slow, rare)
+    if (tid == 0) *fail = 1;
+    for (int t = tid; t < nc; t += kGT) {
+      const int slot = t < n1c ? r1a + t : r2a + (t - n1c);
+      const int i = cand[slot];
+      const double la = gsel_sanitise(lm[(size_t)row * ld + i]);
+      const unsigned long long u = pk[i] >> 11;
+      const int b = (int)(pk[i] & 2047u);
+      int rk = 0;
+      unsigned long long pre = 0ull;
+      for (int j = pc[b]; j < pc[b + 1]; ++j) {
+        const int ij = cand[j];
+        const double lj = gsel_sanitise(lm[(size_t)row * ld + ij]);
+        if (lj > la || (lj == la && ij < i)) {
+          ++rk;
+          pre += pk[ij] >> 11;
+        }
+      }
+      const unsigned long long e0 = pm[b] + pre;
+      if (e0 < T1 && T1 <= e0 + u) {
+        s_n1 = pc[b] + rk + 1;
+        s_at1 = e0 + u;
+      }
+    }
+    __syncthreads();
+    const int n1 = p1 >= 1.0 ? K : s_n1;
+    const unsigned long long T2 = ceil_u64(p2 * (double)s_at1);
+    for (int pass = 0; pass < 2; ++pass) {  // pass 0: the stage-2 cut; pass 1: states
+      const int n2 = p1 >= 1.0 && p2 >= 1.0 ? K : s_n2;
+      for (int t = tid; t < nc; t += kGT) {
+        const int slot = t < n1c ? r1a + t : r2a + (t - n1c);
+        const int i = cand[slot];
+        const double la = gsel_sanitise(lm[(size_t)row * ld + i]);
+        const unsigned long long u = pk[i] >> 11;
+        const int b = (int)(pk[i] & 2047u);
+        int rk = 0;
+        unsigned long long pre = 0ull;
+        for (int j = pc[b]; j < pc[b + 1]; ++j) {
+          const int ij = cand[j];
+          const double lj = gsel_sanitise(lm[(size_t)row * ld + ij]);
+          if (lj > la || (lj == la && ij < i)) {
+            ++rk;
+            pre += pk[ij] >> 11;
+          }
+        }
+        const int ps = pc[b] + rk;
+        const unsigned long long e0 = pm[b] + pre;
+        if (pass == 0 && e0 < T2 && T2 <= e0 + u) s_n2 = ps + 1;
+        if (pass == 1) state[i] = ps < n2 ? 2 : (ps < n1 ? 1 : 0);
+      }
+      __syncthreads();
+    }
+    if (tid == 0) {
+      counts[2 * row] = n1;
+      counts[2 * row + 1] = p1 >= 1.0 && p2 >= 1.0 ? K : s_n2;
+      rd[row].mkey = 0ull;
+    }
+    return;
+  }
+  auto sidx = [&](int slot) { return slot >= r2a ? n1c + (slot - r2a) : slot - r1a; };
+  for (int t = tid; t < nc; t += kGT) {
+    const int slot = t < n1c ? r1a + t : r2a + (t - n1c);
+    const int i = cand[slot];
+    s_cid[t] = i;
+    s_clm[t] = gsel_sanitise(lm[(size_t)row * ld + i]);
+    s_cu[t] = pk[i] >> 11;
+  }
+  __syncthreads();
+  for (int t = tid; t < nc; t += kGT) {
+    const int i = s_cid[t];
+    const double la = s_clm[t];
+    const unsigned long long u = s_cu[t];
+    const int b = (int)(pk[i] & 2047u);
+    const int j0 = pc[b], j1 = pc[b + 1], k0 = sidx(j0);
+    int rk = 0;
+    unsigned long long pre = 0ull;
+    for (int j = 0; j < j1 - j0; ++j) {
+      const double lj = s_clm[k0 + j];
+      const int ij = s_cid[k0 + j];
+      const bool ahead = lj > la || (lj == la && ij < i);
+      rk += ahead;
+      pre += ahead ? s_cu[k0 + j] : 0ull;
+    }
+    const unsigned long long e0 = pm[b] + pre;
+    s_cpos[t] = j0 + rk;
+    s_cex[t] = e0;
+    if (e0 < T1 && T1 <= e0 + u) {
+      s_n1 = j0 + rk + 1;
+      s_at1 = e0 + u;
+    }
+  }
+  __syncthreads();
+  const int n1 = p1 >= 1.0 ? K : s_n1;
+  const unsigned long long T2 = ceil_u64(p2 * (double)s_at1);
+  for (int t = tid; t < nc; t += kGT)
+    if (s_cex[t] < T2 && T2 <= s_cex[t] + s_cu[t]) s_n2 = s_cpos[t] + 1;
+  __syncthreads();
+  const int n2 = p1 >= 1.0 && p2 >= 1.0 ? K : s_n2;
+  for (int t = tid; t < nc; t += kGT) state[s_cid[t]] = s_cpos[t] < n2 ? 2 : (s_cpos[t] < n1 ? 1 : 0);
+  if (tid == 0) {
+    counts[2 * row] = n1;
+    counts[2 * row + 1] = n2;
+    rd[row].mkey = 0ull;  // ready for the next call
+  }
+}
+
+// ---------------------------------------------------------------------------
 // LSE merge of P partials: out_parts [P, rows, d], lse_parts [P, rows]
 // ---------------------------------------------------------------------------
 __global__ void lse_merge_kernel(const float* __restrict__ out_parts, const float* __restrict__ lse_parts, int P,
@@ -588,7 +969,10 @@ cudaError_t launch_lloyd_sums(const void* pts, int dtype, int units, int n, int 
   lloyd_sums_kernel<<<units, kLT, 0, st>>>(pts, dtype, n, d, assign, k, sums, counts, cnt, order);
   return cudaGetLastError();
 }
-size_t select_global_ws_bytes(int rows, int ld) { return (size_t)rows * ld * (8 + 8 + 4 + 4); }
+size_t select_global_ws_bytes(int rows, int ld) {
+  return (size_t)rows * ld * (8 + 8 + 4 + 4) +
+         (size_t)rows * (sizeof(GSelRow) + kGB * 8 + (kGB + 1) * 4 + kGB * 4) + 64;
+}
 cudaError_t launch_select_global(const double* lm, int rows, int ld, const int* Ks, double p1, double p2,
                                  uint8_t* state, int* counts, void* ws, cudaStream_t st) {
   unsigned long long* ex = reinterpret_cast<unsigned long long*>(ws);
@@ -599,7 +983,26 @@ cudaError_t launch_select_global(const double* lm, int rows, int ld, const int* 
   const int dev = current_device();
   if (!attr[dev]) {
     cudaFuncSetAttribute(select_global_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGDyn);
+    cudaFuncSetAttribute(gs_rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGDyn);
     attr[dev] = true;
+  }
+  // split over several CTAs per row when one SM per row would be the bound
+  const int S = ld >= 8192 ? (rows * 8 <= 2 * sm_count() ? 8 : (rows * 4 <= 2 * sm_count() ? 4 : 1)) : 1;
+  if (S > 1) {
+    char* x = reinterpret_cast<char*>(cand + (size_t)rows * ld);
+    x += (16 - (reinterpret_cast<uintptr_t>(x) & 15)) & 15;
+    GSelRow* rd = reinterpret_cast<GSelRow*>(x);
+    unsigned long long* hm = reinterpret_cast<unsigned long long*>(rd + rows);
+    int* hc = reinterpret_cast<int*>(hm + (size_t)rows * kGB);
+    int* cur = hc + (size_t)rows * (kGB + 1);
+    int* fail = reinterpret_cast<int*>(&rd[0].pad);  // (row 0's pad word) set when candidates overflow
+    const dim3 g(S, rows);
+    gs_max_kernel<<<g, kST2, 0, st>>>(lm, ld, Ks, rd, hm, hc, cur);
+    gs_hist_kernel<<<g, kST2, 0, st>>>(lm, ld, Ks, rd, hm, hc, pk);
+    gs_scan_kernel<<<rows, kGT, 0, st>>>(Ks, p1, p2, rd, hm, hc);
+    gs_cand_kernel<<<g, kST2, 0, st>>>(Ks, ld, p1, p2, rd, hm, hc, cur, pk, cand, state);
+    gs_rank_kernel<<<rows, kGT, kGDyn, st>>>(lm, ld, Ks, p1, p2, rd, hm, hc, pk, cand, state, counts, fail);
+    return cudaGetLastError();
   }
   select_global_kernel<<<rows, kGT, kGDyn, st>>>(lm, ld, Ks, p1, p2, state, counts, pos, ex, cand, pk);
   return cudaGetLastError();
