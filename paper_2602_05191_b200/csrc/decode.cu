@@ -544,6 +544,8 @@ size_t decode_ws_layout(const dp_cache_view* v, int G, WorkLists* wl, void** par
   char* rm = take(BH * (size_t)G * sizeof(float));
   const size_t pbytes = BH * max_chunks * G * (2 + (size_t)v->head_dim) * acc;
   char* p = take(pbytes);
+  char* wlp = take(BH * (size_t)kWlMaxChunks * 4 * sizeof(int));  // split worklist: per-chunk totals
+  char* wkey = take(BH * (size_t)G * 2 * sizeof(unsigned long long));  // per q head: lm max key, sink/window max
   if (wl) {
     wl->runs = reinterpret_cast<int4*>(runs);
     wl->approx = reinterpret_cast<int2*>(apx);
@@ -560,6 +562,8 @@ size_t decode_ws_layout(const dp_cache_view* v, int G, WorkLists* wl, void** par
     wl->apart = reinterpret_cast<float*>(ap);
     wl->acc = reinterpret_cast<float*>(ac);
     wl->refm = reinterpret_cast<float*>(rm);
+    wl->wlp = reinterpret_cast<int*>(wlp);
+    wl->wkey = reinterpret_cast<unsigned long long*>(wkey);
     wl->max_chunks = max_chunks;
   }
   if (parts) *parts = p;
@@ -729,11 +733,169 @@ __global__ void __launch_bounds__(256) approx_partial_kernel(dp_cache_view v, in
   }
 }
 
+// ---------------------------------------------------------------------------
+// Split worklist for the tensor-core attention (bf16, d = 128): the one-CTA-
+// per-head worklist_kernel + approx_partial_kernel take ~35 us at K ~ 4K
+// (8 CTAs).  Two launches over (256-cluster chunk, kv head) CTAs instead:
+// wl_count (union lengths, chunk totals, the q heads' log-mass maxima and the
+// sink/window logit maxima) and wl_write (chunk bases from the totals, the
+// packed union rows, runs and approx lists; chunk 0 writes the head's
+// counts and the accumulators' reference maxima).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long wl_dkey(double x) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double wl_dfromkey(unsigned long long k) {
+  return __longlong_as_double((long long)((k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k));
+}
+
+__device__ __forceinline__ void wl_masks(const uint8_t* __restrict__ state, int bh, int G, int cap, int k, int K,
+                                         const int* __restrict__ offs, int& me, int& ma, int& len) {
+  me = ma = len = 0;
+  if (k < K) {
+    for (int g = 0; g < G; ++g) {
+      const uint8_t st = state[((size_t)bh * G + g) * cap + k];
+      me |= (st == 2) << g;
+      ma |= (st == 1) << g;
+    }
+    if (me) len = offs[k + 1] - offs[k];
+  }
+}
+
+__global__ void __launch_bounds__(kWlThreads) wl_count_kernel(dp_cache_view v, int G, const uint8_t* __restrict__ state,
+                                                             const double* __restrict__ lm, const void* __restrict__ q,
+                                                             int qdt, double scale, WorkLists wl) {
+  const int ch = blockIdx.x, bh = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int K = v.nclusters[bh], cap = v.cluster_cap, d = v.head_dim;
+  const int* offs = v.offs + (size_t)bh * (cap + 1);
+  const int k = ch * kWlThreads + tid;
+  int me, ma, len;
+  wl_masks(state, bh, G, cap, k, K, offs, me, ma, len);
+  __shared__ int red[3][kWlThreads / 32];
+  const int r0 = warp_sum(len), r1 = warp_sum(ma != 0 ? 1 : 0), r2 = warp_sum(me != 0 ? 1 : 0);
+  if (lane == 0) {
+    red[0][warp] = r0;
+    red[1][warp] = r1;
+    red[2][warp] = r2;
+  }
+  // the q heads' log-mass maxima over my clusters (reference max of the attention accumulators)
+  for (int g = 0; g < G; ++g) {
+    double x = k < K ? lm[((size_t)bh * G + g) * cap + k] : -CUDART_INF;
+    x = x != x ? -CUDART_INF : x;
+    x = warp_max(x);
+    if (lane == 0 && x != -CUDART_INF) atomicMax(&wl.wkey[((size_t)bh * G + g) * 2], wl_dkey(x));
+  }
+  __syncthreads();
+  if (tid < 3) {
+    int t = 0;
+    for (int w = 0; w < kWlThreads / 32; ++w) t += red[tid][w];
+    wl.wlp[((size_t)bh * kWlMaxChunks + ch) * 4 + tid] = t;
+  }
+  if (ch == 0 && q) {  // sink/window logits (always exact rows): one warp per row, lanes over dims
+    const int nsw = v.sink + v.window;
+    for (int g = 0; g < G; ++g) {
+      double sw = -CUDART_INF;
+      for (int t = warp; t < nsw; t += kWlThreads / 32) {
+        const int row = t < v.sink ? t : v.n_tokens - v.window + (t - v.sink);
+        double acc = 0.0;
+        for (int c = lane; c < d; c += 32)
+          acc += load_elem_d(v.keys, v.dtype, ((size_t)bh * v.row_cap + row) * d + c) *
+                 load_elem_d(q, qdt, ((size_t)bh * G + g) * d + c);
+        acc = warp_sum(acc);
+        if (acc == acc) sw = fmax(sw, acc * scale);
+      }
+      if (lane == 0 && sw != -CUDART_INF) atomicMax(&wl.wkey[((size_t)bh * G + g) * 2 + 1], wl_dkey(sw));
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kWlThreads) wl_write_kernel(dp_cache_view v, int G, const uint8_t* __restrict__ state,
+                                                             WorkLists wl, int nch) {
+  const int ch = blockIdx.x, bh = blockIdx.y, tid = threadIdx.x, lane = tid & 31;
+  const int K = v.nclusters[bh], cap = v.cluster_cap;
+  const int* offs = v.offs + (size_t)bh * (cap + 1);
+  __shared__ int s_base[3], s_tot[3];
+  __shared__ int red[33];
+  if (tid < 3) {  // my chunk's bases: the totals of the chunks before it
+    int b = 0, t = 0;
+    for (int c = 0; c < nch; ++c) {
+      const int x = wl.wlp[((size_t)bh * kWlMaxChunks + c) * 4 + tid];
+      if (c < ch) b += x;
+      t += x;
+    }
+    s_base[tid] = b;
+    s_tot[tid] = t;
+  }
+  const int k = ch * kWlThreads + tid;
+  int me, ma, len;
+  wl_masks(state, bh, G, cap, k, K, offs, me, ma, len);
+  const int full = (1 << G) - 1;
+  const int nsw_runs = (v.sink > 0) + (v.window > 0), sw_rows = v.sink + v.window;
+  int tl, ta, te;
+  const int pl = block_exclusive_scan<int>(len, red, &tl);
+  const int pa = block_exclusive_scan<int>(ma != 0, red, &ta);
+  const int pe = block_exclusive_scan<int>(me != 0, red, &te);
+  const int rowb = sw_rows + s_base[0] + pl;
+  unsigned* rowidx = reinterpret_cast<unsigned*>(wl.rowidx) + (size_t)bh * v.row_cap;
+  if (ma) wl.approx[(size_t)bh * cap + s_base[1] + pa] = make_int2(k, ma);
+  const int st0 = me ? offs[k] : 0;
+  if (me) wl.runs[(size_t)bh * (cap + 2) + nsw_runs + s_base[2] + pe] = make_int4(st0, len, me, rowb);
+  unsigned todo = __ballot_sync(0xffffffffu, len > 0);
+  while (todo) {  // warp-cooperative expansion: lanes write consecutive rows
+    const int t = __ffs(todo) - 1;
+    todo &= todo - 1;
+    const int tlen = __shfl_sync(0xffffffffu, len, t);
+    const int to = __shfl_sync(0xffffffffu, rowb, t);
+    const unsigned tag = (unsigned)__shfl_sync(0xffffffffu, me, t) << 24;
+    const int ts = __shfl_sync(0xffffffffu, st0, t);
+    for (int x = lane; x < tlen; x += 32) rowidx[to + x] = tag | (unsigned)(ts + x);
+  }
+  if (ch == 0) {
+    const unsigned ftag = (unsigned)full << 24;
+    for (int t = tid; t < v.sink; t += kWlThreads) rowidx[t] = ftag | (unsigned)t;
+    for (int t = tid; t < v.window; t += kWlThreads) rowidx[v.sink + t] = ftag | (unsigned)(v.n_tokens - v.window + t);
+    if (tid == 0) {
+      int r = 0;
+      if (v.sink > 0) wl.runs[(size_t)bh * (cap + 2) + r++] = make_int4(0, v.sink, full, 0);
+      if (v.window > 0) wl.runs[(size_t)bh * (cap + 2) + r++] = make_int4(v.n_tokens - v.window, v.window, full, v.sink);
+      const int all_r = sw_rows + s_tot[0];
+      wl.nrows[bh] = all_r;
+      wl.napprox[bh] = s_tot[1];
+      wl.nruns[bh] = nsw_runs + s_tot[2];
+      wl.nchunks[bh] = (all_r + kChunkRows - 1) / kChunkRows;
+      if (wl.stats) {
+        wl.stats[4 * bh + 0] = all_r;
+        wl.stats[4 * bh + 1] = s_tot[1];
+        wl.stats[4 * bh + 2] = (all_r + kChunkRows - 1) / kChunkRows;
+        wl.stats[4 * bh + 3] = s_tot[2];
+      }
+    }
+    if (tid < G) {  // reference max (log2 units) as dp_plan writes it; keys re-armed for the next call
+      unsigned long long* kk = wl.wkey + ((size_t)bh * G + tid) * 2;
+      const double M = kk[0] ? wl_dfromkey(kk[0]) : -CUDART_INF;
+      const double SW = kk[1] ? wl_dfromkey(kk[1]) : -CUDART_INF;
+      wl.refm[(size_t)bh * G + tid] = (float)(ref_max(M, SW) * 1.4426950408889634);
+      kk[0] = 0ull;
+      kk[1] = 0ull;
+    }
+  }
+}
+
 cudaError_t launch_worklist(const dp_cache_view& v, int G, const uint8_t* state, int* stats, void* ws,
                             cudaStream_t st, const double* lm, const void* q, int qdt, double scale) {
   WorkLists wl;
   decode_ws_layout(&v, G, &wl, nullptr, nullptr, reinterpret_cast<char*>(ws));
   wl.stats = stats;
+  const int nch = (v.cluster_cap + kWlThreads - 1) / kWlThreads;
+  if (lm && v.dtype == DP_BF16 && v.head_dim == 128 && nch <= kWlMaxChunks) {
+    // the tensor-core attention folds the approximated clusters itself: the
+    // split two-launch worklist (no per-q-head approx partial needed)
+    const dim3 g((unsigned)nch, (unsigned)(v.batch * v.kv_heads));
+    wl_count_kernel<<<g, kWlThreads, 0, st>>>(v, G, state, lm, q, qdt, scale, wl);
+    wl_write_kernel<<<g, kWlThreads, 0, st>>>(v, G, state, wl, nch);
+    return cudaGetLastError();
+  }
   worklist_kernel<<<v.batch * v.kv_heads, kListThreads, 0, st>>>(v, G, state, wl);
   if (lm && v.head_dim <= 256)
     approx_partial_kernel<<<v.batch * v.kv_heads * G, 256, 0, st>>>(v, G, lm, state, wl, q, qdt, scale,

@@ -18,6 +18,9 @@ constexpr int kMaxPartSlots = 256;  // persistent attention grid cap (partials p
 __host__ __device__ constexpr int acc_stride(int d) { return 2 * d; }  // d/2 vectors (o[c], o[c+1], l, count)
 
 // Device work lists (one set per (b, kv head)), carved from the workspace.
+constexpr int kWlThreads = 256;    // split worklist: clusters per chunk CTA
+constexpr int kWlMaxChunks = 64;   // up to 16384 clusters per head
+
 struct WorkLists {
   int4* runs;     // [BH][cap+2] {row start, len, head mask, virtual row prefix}
   int2* approx;   // [BH][cap]   {cluster id, head mask}
@@ -33,6 +36,8 @@ struct WorkLists {
   float* apart;   // [BH][G][4+d] approx pseudo-row partial per q head (m, l, -, -, o[d]); m = -inf: none
   float* acc;     // [BH][G][acc_stride(d)] sparse attention accumulators: d/2 vectors (o[c], o[c+1], l, count) scaled by 2^-ref (zero between launches)
   float* refm;    // [BH][G] reference max (log2 units) of those accumulators, written by the plan
+  int* wlp;       // [BH][kWlMaxChunks][4] split worklist: per-chunk (rows, approx, exact) totals
+  unsigned long long* wkey;  // [BH][G][2] split worklist: ordered keys of the log-mass / sink-window maxima (0 = unset)
   int max_chunks;
 };
 
