@@ -559,15 +559,27 @@ __device__ void select_fast(const int K, const double M, const double* lmall, co
   SELP(1, S);
   sel_stamp(1);
   // (2) exclusive bin prefixes, total, the stage-1 boundary bin
-  static_assert(kBPT == 4, "bins are read and written as 16-byte vectors (4 per thread)");
+  static_assert(kBPT == 4 || kBPT == 2, "bins are read and written as vectors (2 or 4 per thread)");
   unsigned long long bm[kBPT], mloc = 0ull;
   int bc[kBPT], cloc = 0;
-  {  // one 16-B vector per array per thread: contiguous across the warp, no bank conflicts
-    const uint4 h4 = *reinterpret_cast<const uint4*>(hmh + tid * kBPT);
-    const uint4 l4 = *reinterpret_cast<const uint4*>(hml + tid * kBPT);
-    const int4 c4 = *reinterpret_cast<const int4*>(hc + tid * kBPT);
-    const unsigned hh[4] = {h4.x, h4.y, h4.z, h4.w}, ll[4] = {l4.x, l4.y, l4.z, l4.w};
-    const int cc[4] = {c4.x, c4.y, c4.z, c4.w};
+  {  // one vector per array per thread: contiguous across the warp, no bank conflicts
+    unsigned hh[kBPT], ll[kBPT];
+    int cc[kBPT];
+    if constexpr (kBPT == 4) {
+      const uint4 h4 = *reinterpret_cast<const uint4*>(hmh + tid * kBPT);
+      const uint4 l4 = *reinterpret_cast<const uint4*>(hml + tid * kBPT);
+      const int4 c4 = *reinterpret_cast<const int4*>(hc + tid * kBPT);
+      hh[0] = h4.x; hh[1] = h4.y; hh[2] = h4.z; hh[3] = h4.w;
+      ll[0] = l4.x; ll[1] = l4.y; ll[2] = l4.z; ll[3] = l4.w;
+      cc[0] = c4.x; cc[1] = c4.y; cc[2] = c4.z; cc[3] = c4.w;
+    } else {
+      const uint2 h2 = *reinterpret_cast<const uint2*>(hmh + tid * kBPT);
+      const uint2 l2 = *reinterpret_cast<const uint2*>(hml + tid * kBPT);
+      const int2 c2 = *reinterpret_cast<const int2*>(hc + tid * kBPT);
+      hh[0] = h2.x; hh[1] = h2.y;
+      ll[0] = l2.x; ll[1] = l2.y;
+      cc[0] = c2.x; cc[1] = c2.y;
+    }
 #pragma unroll
     for (int j = 0; j < kBPT; ++j) {
       bm[j] = ((unsigned long long)hh[j] << 20) + ll[j];
@@ -633,9 +645,14 @@ __device__ void select_fast(const int K, const double M, const double* lmall, co
     cex += bc[j];
   }
   reinterpret_cast<ulonglong2*>(pm + tid * kBPT)[0] = make_ulonglong2(pmv[0], pmv[1]);
-  reinterpret_cast<ulonglong2*>(pm + tid * kBPT)[1] = make_ulonglong2(pmv[2], pmv[3]);
-  *reinterpret_cast<int4*>(pc + tid * kBPT) = make_int4(pcv[0], pcv[1], pcv[2], pcv[3]);
-  *reinterpret_cast<int4*>(cur + tid * kBPT) = make_int4(0, 0, 0, 0);
+  if constexpr (kBPT == 4) {
+    reinterpret_cast<ulonglong2*>(pm + tid * kBPT)[1] = make_ulonglong2(pmv[2], pmv[3]);
+    *reinterpret_cast<int4*>(pc + tid * kBPT) = make_int4(pcv[0], pcv[1], pcv[2], pcv[3]);
+    *reinterpret_cast<int4*>(cur + tid * kBPT) = make_int4(0, 0, 0, 0);
+  } else {
+    *reinterpret_cast<int2*>(pc + tid * kBPT) = make_int2(pcv[0], pcv[1]);
+    *reinterpret_cast<int2*>(cur + tid * kBPT) = make_int2(0, 0);
+  }
   if (tid == kT - 1) pc[NB] = S->wcx[kW];
   sel_sub(4);
   __syncthreads();

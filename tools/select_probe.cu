@@ -10,7 +10,10 @@
 #include "select.cuh"
 
 using namespace dp;
-constexpr int kT = 512, kNB = 2048, kCap = 4096;
+#ifndef PROBE_NB
+#define PROBE_NB 2048
+#endif
+constexpr int kT = 512, kNB = PROBE_NB, kCap = 4096;
 
 __global__ void __launch_bounds__(kT, 1) probe(const double* lm_g, int K, int reps, long long* cyc, int* out) {
   extern __shared__ __align__(16) unsigned char sm[];
