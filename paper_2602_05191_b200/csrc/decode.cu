@@ -377,12 +377,15 @@ __global__ void __launch_bounds__(kAttnThreads) attn_chunk_kernel(dp_cache_view 
     if ((rmask[r] >> g) & 1) {
       const T* kr = reinterpret_cast<const T*>(ks + r * rowb);
       const Acc* qg = qs + g * d;
-      Acc a = 0;
-      for (int j = 0; j < d; ++j) {
-        if constexpr (sizeof(T) == 4) a = fma((Acc)kr[j], qg[j], a);
-        else a = fma((Acc)bf2f(kr[j]), qg[j], a);
+      Acc a[4] = {0, 0, 0, 0};  // four independent chains (d % 8 == 0): latency / 4
+      for (int j = 0; j < d; j += 4) {
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          if constexpr (sizeof(T) == 4) a[t] = fma((Acc)kr[j + t], qg[j + t], a[t]);
+          else a[t] = fma((Acc)bf2f(kr[j + t]), qg[j + t], a[t]);
+        }
       }
-      s = a * sc_scale;
+      s = ((a[0] + a[1]) + (a[2] + a[3])) * sc_scale;
     }
     sc[g * kChunkRows + r] = s;
   }
@@ -410,15 +413,26 @@ __global__ void __launch_bounds__(kAttnThreads) attn_chunk_kernel(dp_cache_view 
   for (int i = tid; i < G * d; i += nt) {
     const int g = i / d, j = i - g * d;
     const Acc* pg = sc + g * kChunkRows;
-    Acc o = 0;
-    for (int r = 0; r < nr; ++r) {
+    Acc o[4] = {0, 0, 0, 0};  // four independent chains over the rows
+    int r = 0;
+    for (; r + 4 <= nr; r += 4) {
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const T* vr = reinterpret_cast<const T*>(vs + (r + t) * rowb);
+        Acc val;
+        if constexpr (sizeof(T) == 4) val = (Acc)vr[j];
+        else val = (Acc)bf2f(vr[j]);
+        o[t] = fma(pg[r + t], val, o[t]);
+      }
+    }
+    for (; r < nr; ++r) {
       const T* vr = reinterpret_cast<const T*>(vs + r * rowb);
       Acc val;
       if constexpr (sizeof(T) == 4) val = (Acc)vr[j];
       else val = (Acc)bf2f(vr[j]);
-      o = fma(pg[r], val, o);
+      o[0] = fma(pg[r], val, o[0]);
     }
-    pt.o[(((size_t)bh * pt.max_chunks + c) * G + g) * d + j] = o;
+    pt.o[(((size_t)bh * pt.max_chunks + c) * G + g) * d + j] = (o[0] + o[1]) + (o[2] + o[3]);
   }
 }
 
