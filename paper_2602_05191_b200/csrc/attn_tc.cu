@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
   };
 
   auto flush = [&](int bh, float* scratch) {
-    if (!kDense) {  // drain this warp's remaining approx entries
+    if (!kDense && !(dbg & 64)) {  // drain this warp's remaining approx entries
       if (ap_ready) ap_fold();
 #pragma unroll 1
       while (ap_k < ap_n) {
@@ -642,8 +642,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
               : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(bl0), "r"(bl1));
       }
     }
-    if (!kDense) {  // one approx pseudo-row per tile: fold the loaded one, issue the next
-      if (ap_ready) ap_fold();
+    if (!kDense && !(dbg & 64)) {  // one approx pseudo-row per tile: fold the loaded one, issue the next
+      if (ap_ready) ap_fold();       // (64: timing experiment, no approx pseudo-rows)
       if (ap_k < ap_n) ap_issue(bh);
     }
     if (seg_end && !(dbg & 2)) flush(bh, reinterpret_cast<float*>(Ks));  // this stage's K buffer is the scratch

@@ -66,7 +66,7 @@ for bits, name in ((0, "full plan"), (32, "no centroid L2 prefetch"), (16, "no c
     print(f"  {name:28s} {timed(lambda: [plan() for _ in range(L)]):7.2f}")
 lib.dp_debug_set(10, 0)
 print(f"  {'plan + attend':28s} {timed(lambda: [(plan(), attend()) for _ in range(L)]):7.2f}")
-for bits, name in ((32, "attend: P hi only"), (1, "attend: no math"), (4, "attend: no merge"), (8, "attend: no counters/merge"),
+for bits, name in ((64, "attend: no approx rows"), (32, "attend: P hi only"), (1, "attend: no math"), (4, "attend: no merge"), (8, "attend: no counters/merge"),
                    (2, "attend: no flush/merge"), (3, "attend: neither")):
     lib.dp_debug_set(0, bits)
     print(f"  plan + {name:28s} {timed(lambda: [(plan(), attend()) for _ in range(L)]):7.2f}")
