@@ -373,6 +373,41 @@ int dp_select_global(const double* log_mass, int32_t rows, int32_t ld, const int
 int dp_lse_merge(const float* out_parts, const float* lse_parts, int32_t parts, int32_t rows, int32_t d, float* out,
                  float* lse, void* stream);
 
+/* ---------------------------------------------------------------------- */
+/* the reference's per-query kernel plugin seam (kernels.py:47-96) as     */
+/* HOST-pointer calls: the eight operations a DOUBLEP_KERNELS backend     */
+/* provides (_kernels_cy.pyx:21-157), computed on the current device      */
+/* (csrc/seam.cu).  Synchronous; matrices DP_F32 or DP_F64 row-major      */
+/* [rows, d]; idx (int64, NULL = all rows) must lie in [0, rows).  These  */
+/* replace the Cython backend one call at a time; the decode path above   */
+/* does not use them.                                                     */
+/* ---------------------------------------------------------------------- */
+#define DP_F64 2 /* seam matrices only */
+
+/* scaled_logits / gather_scaled_logits (kernels.py:47-57): out[i] =
+ * (keys[idx[i]] . q) * scale, fp64 sequential over d -- bit-identical to
+ * _kernels_cy.pyx:21-50. */
+int dp_kn_scaled_logits(const void* keys, int32_t dtype, int64_t rows, int32_t d, const int64_t* idx, int64_t n_idx,
+                        const double* q, double scale, double* out);
+/* logsumexp (kernels.py:60-62, _kernels_cy.pyx:53-65): n >= 1 (else
+ * DP_ERR_INVALID); exact max for one element. */
+int dp_kn_logsumexp(const double* x, int64_t n, double* out);
+/* softmax (kernels.py:65-67, _kernels_cy.pyx:68-83): out [n]. */
+int dp_kn_softmax(const double* x, int64_t n, double* out);
+/* weighted_sum / gather_weighted_sum (kernels.py:70-76): out[d] =
+ * sum_i w[i] * mat[idx[i]], fp64. */
+int dp_kn_weighted_sum(const double* w, const void* mat, int32_t dtype, int64_t rows, int32_t d, const int64_t* idx,
+                       int64_t n_idx, double* out);
+/* nearest_centroid (kernels.py:79-87, _kernels_cy.pyx:115-140): direct
+ * difference in fp64, strict '<' (ties -> lowest index); assign int64 [n],
+ * sqdist fp64 [n]; k >= 1. */
+int dp_kn_nearest_centroid(const void* points, int32_t dtype, int64_t n, int32_t d, const double* centroids,
+                           int32_t k, int64_t* assign, double* sqdist);
+/* sorted_prefix_count (kernels.py:90-96, _kernels_cy.pyx:143-157): smallest
+ * prefix with running fp64 sum >= p (n if never); DP_ERR_INVALID "input not
+ * sorted" on an ascent among the scanned entries. */
+int dp_kn_sorted_prefix_count(const double* sorted_probs, int64_t n, double p, int64_t* count);
+
 #ifdef __cplusplus
 }
 #endif

@@ -95,6 +95,43 @@ def sorted_prefix_count(sorted_probs, p):
     return sp.shape[0]
 
 
+def scaled_logits_seq(keys, idx, q, scale):
+    """The compiled backend's loop order (`_kernels_cy.pyx:21-50`): per row, a
+    float64 running sum over j of keys[row, j] * q[j] (each product and add
+    rounded separately), then one multiply by ``scale``.  Vectorised over
+    rows; bit-identical to the Cython backend (pinned against its outputs in
+    tests/golden/kernels_seam.npz)."""
+    keys = np.asarray(keys)
+    rows = keys if idx is None else keys[np.asarray(idx, dtype=np.intp)]
+    rows = rows.astype(np.float64, copy=False)
+    q = np.asarray(q, dtype=np.float64)
+    acc = np.zeros(rows.shape[0], dtype=np.float64)
+    for j in range(rows.shape[1]):
+        acc = acc + rows[:, j] * q[j]
+    return acc * scale
+
+
+def nearest_centroid_direct(points, centroids):
+    """The compiled backend's formulation (`_kernels_cy.pyx:115-140`): direct
+    differences, float64 running sum over j, strict ``<`` over centroids in
+    index order (ties -> lowest index).  Differs from the NumPy backend's
+    expansion (:func:`nearest_centroid`) in the last bits of the distance."""
+    x = np.asarray(points).astype(np.float64, copy=False)
+    c = np.asarray(centroids, dtype=np.float64)
+    n = x.shape[0]
+    best = np.full(n, np.inf)
+    assign = np.zeros(n, dtype=np.int64)
+    for ci in range(c.shape[0]):
+        dist = np.zeros(n, dtype=np.float64)
+        for j in range(x.shape[1]):
+            diff = x[:, j] - c[ci, j]
+            dist = dist + diff * diff
+        better = dist < best
+        best = np.where(better, dist, best)
+        assign = np.where(better, ci, assign)
+    return assign, best
+
+
 def output_error(candidate, reference):
     """Relative L2 error -- `metrics.py:15-23`."""
     a = candidate.output if isinstance(candidate, AttentionOutput) else np.asarray(candidate)

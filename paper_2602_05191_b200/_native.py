@@ -12,7 +12,7 @@ import re
 from .build import INCLUDE, LIB
 
 DP_OK, DP_ERR_INVALID, DP_ERR_CUDA, DP_ERR_UNSUPPORTED = 0, 1, 2, 3
-DP_F32, DP_BF16 = 0, 1
+DP_F32, DP_BF16, DP_F64 = 0, 1, 2
 
 _c_int_p = ctypes.POINTER(ctypes.c_int32)
 _c_dbl_p = ctypes.POINTER(ctypes.c_double)
@@ -110,6 +110,15 @@ _SIGS = {
     "dp_select_global": (ctypes.c_int, [_vp, ctypes.c_int32, ctypes.c_int32, _vp, ctypes.c_double, ctypes.c_double,
                                         _vp, _vp, _vp, ctypes.c_size_t, _vp]),
     "dp_lse_merge": (ctypes.c_int, [_vp, _vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _vp, _vp, _vp]),
+    "dp_kn_scaled_logits": (ctypes.c_int, [_vp, ctypes.c_int32, ctypes.c_int64, ctypes.c_int32, _vp, ctypes.c_int64,
+                                           _vp, ctypes.c_double, _vp]),
+    "dp_kn_logsumexp": (ctypes.c_int, [_vp, ctypes.c_int64, _vp]),
+    "dp_kn_softmax": (ctypes.c_int, [_vp, ctypes.c_int64, _vp]),
+    "dp_kn_weighted_sum": (ctypes.c_int, [_vp, _vp, ctypes.c_int32, ctypes.c_int64, ctypes.c_int32, _vp,
+                                          ctypes.c_int64, _vp]),
+    "dp_kn_nearest_centroid": (ctypes.c_int, [_vp, ctypes.c_int32, ctypes.c_int64, ctypes.c_int32, _vp, ctypes.c_int32,
+                                              _vp, _vp]),
+    "dp_kn_sorted_prefix_count": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_double, _vp]),
 }
 
 _lib = None

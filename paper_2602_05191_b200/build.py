@@ -17,7 +17,7 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIBDIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIBDIR, "libdoublep_b200.so")
-SOURCES = ["capi.cu", "decode.cu", "cluster.cu", "attn_tc.cu", "plan.cu", "step.cu", "metrics.cu", "shard.cu"]
+SOURCES = ["capi.cu", "decode.cu", "cluster.cu", "attn_tc.cu", "plan.cu", "step.cu", "metrics.cu", "shard.cu", "seam.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-Xptxas", "-v"]

@@ -152,3 +152,24 @@ def install(pkg=None):
             if n is not None and k == n:
                 h._set(mod, k, repl[n])
     return h
+
+
+def install_kernels(pkg=None):
+    """Make ``paper_2602_05191_b200.kernels`` the reference's kernel backend:
+    the one-level-lower binding (the reference's own plugin seam,
+    kernels.py:17-29) -- every ``kernels.X`` call the reference makes
+    (engine.py:128-361, clustering.py:85, numerics.py:35-44,
+    selection.py:82) then runs on the GPU through dp_kn_*.  ``BACKEND`` reads
+    "b200".  Returns a Handle whose ``uninstall()`` restores the previous
+    backend."""
+    from . import kernels as b200_kernels
+
+    name = pkg.__name__ if pkg is not None else "doublep"
+    base = pkg if pkg is not None else importlib.import_module(name)
+    ref_kernels = importlib.import_module(f"{name}.kernels")
+    h = Handle()
+    h._set(ref_kernels, "_impl", b200_kernels)
+    h._set(ref_kernels, "BACKEND", b200_kernels.BACKEND)
+    if hasattr(base, "BACKEND"):
+        h._set(base, "BACKEND", b200_kernels.BACKEND)
+    return h

@@ -39,19 +39,23 @@ FP64_BOUND = {
 }
 
 
-def _env():
+def _env(bind="ops", counts=None):
     env = dict(os.environ)
+    env["B200_REF_BIND"] = bind
+    if counts:
+        env["B200_REF_SEAM_COUNTS"] = str(counts)
     env["PYTHONPATH"] = os.pathsep.join([REF, ROOT, os.path.join(ROOT, "tests")] +
                                         [p for p in env.get("PYTHONPATH", "").split(os.pathsep) if p])
     return env
 
 
-def _run_reference_tests(files, tmp_path):
+def _run_reference_tests(files, tmp_path, bind="ops"):
+    counts = tmp_path / "seam_counts.json"
     xml = tmp_path / "ref.xml"
     cmd = [sys.executable, "-m", "pytest", "-p", "b200_ref_plugin", "-q", "-p", "no:cacheprovider",
            f"--junitxml={xml}", "--rootdir", os.path.join(REF, "tests")] + \
           [os.path.join(REF, "tests", f) for f in files]
-    r = subprocess.run(cmd, cwd=os.path.join(REF, "tests"), env=_env(), capture_output=True, text=True,
+    r = subprocess.run(cmd, cwd=os.path.join(REF, "tests"), env=_env(bind, counts), capture_output=True, text=True,
                        timeout=900)
     res = {}
     for tc in ET.parse(xml).getroot().iter("testcase"):
@@ -76,6 +80,35 @@ def test_reference_test_suite_on_b200(tmp_path):
     assert not unexpected, f"reference tests failing beyond fp64-only tolerances: {unexpected}\n" + \
         "\n".join(res.get(k + "#msg", "") for k in unexpected)
     assert len(passed) >= len(outcomes) - len(FP64_BOUND)
+
+
+def test_reference_full_suite_on_kernel_seam(tmp_path):
+    """One level lower: the reference's kernel plugin seam bound to the GPU
+    (integration.install_kernels -- the DOUBLEP_KERNELS=b200 backend of
+    INTEGRATION.md), the reference's engine, clustering, selection and CLI
+    unchanged above it.  Its WHOLE test suite must pass: the seam is
+    bit-identical to the Cython backend where the reference's tests compare
+    exactly, and within its 1e-12 elsewhere."""
+    files = sorted(f for f in os.listdir(os.path.join(REF, "tests")) if f.startswith("test_") and f.endswith(".py"))
+    r, res = _run_reference_tests(files, tmp_path, bind="kernels")
+    outcomes = {k: v for k, v in res.items() if "#" not in k}
+    assert outcomes, r.stdout[-3000:] + r.stderr[-3000:]
+    failed = sorted(k for k, v in outcomes.items() if v == "failed")
+    passed = sum(v == "passed" for v in outcomes.values())
+    print(f"\n[REF-SEAM] {passed} passed, {len(failed)} failed of {len(outcomes)} reference tests, kernels on B200")
+    import json
+
+    calls = json.loads((tmp_path / "seam_counts.json").read_text())
+    print(f"[REF-SEAM] GPU seam calls: {calls}")
+    for name in ("scaled_logits", "logsumexp", "softmax", "weighted_sum", "gather_weighted_sum",
+                 "nearest_centroid", "sorted_prefix_count"):
+        assert calls.get(name, 0) > 0, (name, calls)
+    # the one test that enumerates the reference's two backends by name
+    # (tests/test_kernels.py:23-26 asserts BACKEND in ("python", "cython"));
+    # a maintainer adding "b200" extends that tuple
+    unexpected = [k for k in failed if k != "test_kernels.py::test_backend_is_reported"]
+    assert not unexpected, "\n".join(f"{k}: {res.get(k + '#msg', '')}" for k in unexpected)
+    assert passed >= len(outcomes) - 1
 
 
 def _ref():

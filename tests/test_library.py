@@ -67,3 +67,30 @@ def test_workspace_sizes_are_host_computable():
     p.batch, p.kv_heads, p.head_dim, p.dtype = 1, 8, 128, 1
     p.n_tokens, p.sink, p.window, p.k, p.max_iters = 32768, 4, 64, 1022, 25
     assert lib.dp_cluster_workspace_bytes(p) > 8 * 32700 * 8
+
+
+def test_kernel_seam_validation_without_device():
+    """dp_kn_* (the reference's kernels.py seam) reject bad arguments on the
+    host, before any device work, with the reference's error classes."""
+    from paper_2602_05191_b200 import kernels as K
+
+    assert K.BACKEND == "b200"
+    with pytest.raises(ValueError, match="zero-size"):
+        K.logsumexp([])
+    with pytest.raises(ValueError, match="zero-size"):
+        K.softmax(np.zeros(0))
+    with pytest.raises(IndexError):
+        K.gather_scaled_logits(np.zeros((4, 2), np.float32), [4], np.zeros(2), 1.0)
+    with pytest.raises(ValueError, match="empty sequence"):
+        K.nearest_centroid(np.zeros((3, 2)), np.zeros((0, 2)))
+    with pytest.raises(ValueError, match="not aligned"):
+        K.weighted_sum(np.ones(3), np.ones((4, 2)))
+    assert K.sorted_prefix_count([], 0.5) == 0
+    assert K.scaled_logits(np.zeros((0, 3)), np.zeros(3), 1.0).shape == (0,)
+    lib = N.lib()
+    out = np.zeros(2)
+    idx = np.array([0, 9], dtype=np.int64)
+    with pytest.raises(ValueError, match="index out of range"):
+        N.check(lib.dp_kn_scaled_logits(None, N.DP_F32, 4, 2, idx.ctypes.data, 2, None, 1.0, out.ctypes.data))
+    with pytest.raises(ValueError, match="float32 or float64"):
+        N.check(lib.dp_kn_scaled_logits(None, N.DP_BF16, 4, 2, None, 0, None, 1.0, out.ctypes.data))

@@ -181,3 +181,41 @@ def test_lse_merge_matches_whole():
     M, L, o = O.lse_merge(*zip(*parts))
     np.testing.assert_allclose(o, whole, rtol=1e-12)
     assert M + math.log(L) == pytest.approx(lse, rel=1e-12)
+
+
+def _seam():
+    return np.load(os.path.join(GOLDEN, "kernels_seam.npz"))
+
+
+def test_oracle_seam_matches_compiled_reference_backend():
+    """The Cython-order restatements are bit-identical to the reference's
+    compiled backend (_kernels_cy.pyx, tests/golden/kernels_seam.npz from
+    oracle/gen_golden_seam.py); the reductions agree to the reference's own
+    backend-parity tolerance (tests/test_kernels.py:30-67)."""
+    g = _seam()
+    for t in "abcde":
+        keys, q, s = g[f"sl_{t}_keys"], g[f"sl_{t}_q"], float(g[f"sl_{t}_scale"])
+        np.testing.assert_array_equal(O.scaled_logits_seq(keys, None, q, s), g[f"sl_{t}_out"])
+        np.testing.assert_array_equal(O.scaled_logits_seq(keys, g[f"sl_{t}_idx"], q, s), g[f"sl_{t}_gout"])
+        np.testing.assert_allclose(O.scaled_logits(keys, q, s), g[f"sl_{t}_out"], rtol=1e-12, atol=1e-12)
+    for t in "abcd":
+        x = g[f"lse_{t}_x"]
+        assert O.logsumexp(x) == pytest.approx(float(g[f"lse_{t}_out"]), rel=1e-12, abs=1e-12)
+        np.testing.assert_allclose(O.softmax(x), g[f"sm_{t}_out"], rtol=1e-12, atol=1e-15)
+    assert O.logsumexp(g["lse_b_x"]) == float(g["lse_b_out"])  # exact for one element
+    for t in "abc":
+        w, mat, idx = g[f"ws_{t}_w"], g[f"ws_{t}_mat"], g[f"ws_{t}_idx"]
+        np.testing.assert_allclose(O.weighted_sum(w, mat), g[f"ws_{t}_out"], rtol=1e-12, atol=1e-12)
+        np.testing.assert_allclose(O.weighted_sum(w[: len(idx)], mat[idx]), g[f"ws_{t}_gout"], rtol=1e-12,
+                                   atol=1e-12)
+    for t in "abcde":
+        a, b = O.nearest_centroid_direct(g[f"nc_{t}_pts"], g[f"nc_{t}_cents"])
+        np.testing.assert_array_equal(a, g[f"nc_{t}_assign"])
+        np.testing.assert_array_equal(b, g[f"nc_{t}_dsq"])
+    assert g["nc_d_assign"][0] == 0 and not np.any(g["nc_e_assign"] == 5)  # ties -> lower index
+    off = 0
+    for n, p, c in zip(g["spc_lens"], g["spc_p"], g["spc_count"]):
+        assert O.sorted_prefix_count(g["spc_vals"][off:off + n], p) == c
+        off += n
+    for p, c in zip(g["spc_big_p"], g["spc_big_count"]):
+        assert O.sorted_prefix_count(g["spc_big"], p) == c
