@@ -953,6 +953,8 @@ def run_seqshard(a):
         for li in range(L):
             layer_step(li, s)
     torch.cuda.synchronize(dev)
+    if os.environ.get("DP_DUMP_GLM"):  # tools/gsel_probe.py: the last layer's global log-mass table
+        torch.save(g_lm.cpu(), os.environ["DP_DUMP_GLM"])
     graphs = None
     if not real:  # one CUDA graph per distinct query step (the collectives of a real run stay eager)
         graphs = []

@@ -798,6 +798,8 @@ extern "C" int dp_debug_set(int key, int value) {
   if (key == 7) dp::g_step_dbg = value;
   if (key == 9) dp::g_seg_cost = value;
   if (key == 10) dp::g_plan_dbg = value;
+  if (key == 11) dp::g_gsel_path = value;
+  if (key == 12) return dp::set_gsel_dbg(value);
   return 0;
 }
 extern "C" int dp_debug_attn_timing(unsigned long long* out) {

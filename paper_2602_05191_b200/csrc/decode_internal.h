@@ -119,6 +119,8 @@ size_t lloyd_sums_ws_bytes(int units, int n, int k);
 cudaError_t launch_lloyd_sums(const void* pts, int dtype, int units, int n, int d, const int* assign, int k,
                               double* sums, long long* counts, void* ws, cudaStream_t st);
 size_t select_global_ws_bytes(int rows, int ld);
+extern int g_gsel_path;  // dp_debug_set(11, .)
+int set_gsel_dbg(int v);  // dp_debug_set(12, .)
 cudaError_t launch_select_global(const double* lm, int rows, int ld, const int* Ks, double p1, double p2,
                                  uint8_t* state, int* counts, void* ws, cudaStream_t st);
 cudaError_t launch_lse_merge(const float* out_parts, const float* lse_parts, int P, int rows, int d, float* out,

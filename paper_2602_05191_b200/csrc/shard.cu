@@ -23,6 +23,7 @@
 //     kept in global scratch instead of registers.
 //   * lse_merge_kernel: the exchange step's log-sum-exp merge of the P
 //     partial (out, lse) (engine.py:234-246 across shards).
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
@@ -30,6 +31,9 @@
 #include "decode_internal.h"
 #include "host_state.h"
 #include "select.cuh"
+#include "dsmem.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace dp {
 
@@ -230,9 +234,9 @@ __global__ void __launch_bounds__(kGT, 1) select_global_kernel(const double* __r
   // (u, bin) of every element, packed once in pass (1) and re-read by the
   // later passes instead of recomputing exp / conversions: u << 11 | bin
   unsigned long long* pk = pk_ws + (size_t)row * ld;
-  __shared__ unsigned s_hh[kGB], s_hl[kGB];
+  __shared__ unsigned long long s_hm[kGB];  // exact u64 bin masses (u32 halves overflow on flat rows)
   __shared__ int s_hc[kGB + 1];
-  unsigned* s_cur = s_hh;  // after the bin scan: per-bin cursors of the candidate placement
+  unsigned* s_cur = reinterpret_cast<unsigned*>(s_hm);  // after the bin scan: per-bin cursors of the candidate placement
   __shared__ unsigned long long s_pm[kGB];
   __shared__ unsigned long long s_wm[33];
   __shared__ int s_wc[33];
@@ -246,8 +250,7 @@ __global__ void __launch_bounds__(kGT, 1) select_global_kernel(const double* __r
   int* s_cid = reinterpret_cast<int*>(s_clm + kGCand);
   int* s_cpos = s_cid + kGCand;
   for (int j = tid; j < kGB; j += kGT) {
-    s_hh[j] = 0u;
-    s_hl[j] = 0u;
+    s_hm[j] = 0ull;
     s_hc[j] = 0;
   }
   if (tid == 0) {
@@ -287,8 +290,7 @@ __global__ void __launch_bounds__(kGT, 1) select_global_kernel(const double* __r
       gsel_elem(M, gsel_sanitise(x[j]), u, b);
       pk[i] = (u << 11) | (unsigned long long)b;
       if (u) {
-        atomicAdd(&s_hh[b], (unsigned)(u >> 20));
-        atomicAdd(&s_hl[b], (unsigned)(u & 0xFFFFFu));
+        atomicAdd(&s_hm[b], u);
         atomicAdd(&s_hc[b], 1);
       }
     }
@@ -301,7 +303,7 @@ __global__ void __launch_bounds__(kGT, 1) select_global_kernel(const double* __r
 #pragma unroll
   for (int j = 0; j < kBPT; ++j) {
     const int b = tid * kBPT + j;
-    bm[j] = ((unsigned long long)s_hh[b] << 20) + s_hl[b];
+    bm[j] = s_hm[b];
     bc[j] = s_hc[b];
     mloc += bm[j];
     cloc += bc[j];
@@ -584,11 +586,10 @@ __global__ void __launch_bounds__(kST2) gs_hist_kernel(const double* __restrict_
                                                       unsigned long long* __restrict__ pk_ws) {
   const int row = blockIdx.y, S = gridDim.x, sp = blockIdx.x, tid = threadIdx.x;
   const int K = Ks[row];
-  __shared__ unsigned s_h[kGB], s_l[kGB];
+  __shared__ unsigned long long s_h[kGB];
   __shared__ int s_c[kGB];
   for (int b = tid; b < kGB; b += kST2) {
-    s_h[b] = 0u;
-    s_l[b] = 0u;
+    s_h[b] = 0ull;
     s_c[b] = 0;
   }
   __syncthreads();
@@ -608,8 +609,7 @@ __global__ void __launch_bounds__(kST2) gs_hist_kernel(const double* __restrict_
       gsel_elem(M, gsel_sanitise(x[j]), u, b);
       pk[ii] = (u << 11) | (unsigned long long)b;
       if (u) {
-        atomicAdd(&s_h[b], (unsigned)(u >> 20));
-        atomicAdd(&s_l[b], (unsigned)(u & 0xFFFFFu));
+        atomicAdd(&s_h[b], u);
         atomicAdd(&s_c[b], 1);
       }
     }
@@ -617,7 +617,7 @@ __global__ void __launch_bounds__(kST2) gs_hist_kernel(const double* __restrict_
   __syncthreads();
   for (int b = tid; b < kGB; b += kST2)
     if (s_c[b]) {
-      atomicAdd(&hm[(size_t)row * kGB + b], ((unsigned long long)s_h[b] << 20) + s_l[b]);
+      atomicAdd(&hm[(size_t)row * kGB + b], s_h[b]);
       atomicAdd(&hc[(size_t)row * (kGB + 1) + b], s_c[b]);
     }
 }
@@ -916,6 +916,421 @@ __global__ void __launch_bounds__(kGT, 1) gs_rank_kernel(const double* __restric
 }
 
 // ---------------------------------------------------------------------------
+// The same selection in ONE launch: a thread-block cluster of CS CTAs
+// (1024 threads each) per row, each CTA holding up to 8192 of the row's
+// elements in registers (K <= CS * 8192, CS <= 8).  Every exchange is a
+// distributed-shared-memory PUSH that completes a transaction on the
+// receiver's mbarrier (st.async, dsmem.cuh) -- no cluster-wide barrier and
+// no remote load after the start-up one, the plan kernel's protocol:
+//   A  CTA maxima -> every CTA;
+//   B  local histograms (1/32-nat bins; masses as three 13-bit pieces so
+//      native 32-bit shared atomics stay exact) -> the bin-slice owners
+//      (CTA s owns 2048/CS bins);
+//   C  owners sum their slice over the sources, push slice totals to every
+//      CTA, then (knowing the slice's global offset) push every CTA the
+//      slice's exclusive mass / count prefixes and that CTA's own offset
+//      inside each bin, plus the stage-1 bin if it lies in the slice;
+//   D  every CTA classifies its elements: the candidates (stage-1 bin, the
+//      stage-2 range) are pushed to CTA 0 at their bin slots, everything
+//      else takes its state from its bin;
+//   E  CTA 0 ranks the candidates (log-mass desc, index asc), finds both
+//      cuts and writes their states.
+// Same arithmetic as select_global_kernel (u, bins, double thresholds), so
+// the states are identical (tests/test_gpu_seqshard.py).  More candidates
+// than kGCand go through global scratch and one cluster barrier instead.
+// ---------------------------------------------------------------------------
+__device__ int g_gsel_dbg;  // timing experiments (dp_debug_set(12, .)): exit after phase n
+constexpr int kGCT = 1024;  // threads per CTA
+constexpr int kGCE = 8;     // elements per thread
+constexpr int kGCMaxCS = 8;
+struct GcLayout {
+  // region 1: local histogram + receive buffer, later (CTA 0) the staged candidates
+  static constexpr size_t h0 = 0;                          // u32[kGB] mass bits [0, 13)
+  static constexpr size_t h1 = h0 + (size_t)kGB * 4;       // u32[kGB] mass bits [13, 26)
+  static constexpr size_t h2 = h1 + (size_t)kGB * 4;       // u32[kGB] mass bits [26, 39)
+  static constexpr size_t hc = h2 + (size_t)kGB * 4;       // u32[kGB] counts
+  static constexpr size_t recv = hc + (size_t)kGB * 4;     // uint4[kGB]: [source][slice bin] pieces + count
+  static constexpr size_t cu = 0;                          // u64[kGCand] staged candidates: mass
+  static constexpr size_t clm = cu + (size_t)kGCand * 8;   //   log-mass
+  static constexpr size_t cex = clm + (size_t)kGCand * 8;  //   exclusive cumulative mass (CTA 0's ranking)
+  static constexpr size_t cid = cex + (size_t)kGCand * 8;  //   index
+  static constexpr size_t cpos = cid + (size_t)kGCand * 4; //   sorted position
+  static constexpr size_t r1 = cpos + (size_t)kGCand * 4;
+  // region 2: the row's bin table (every CTA) and candidate cursors
+  static constexpr size_t tab = r1;                        // uint4[kGB]: pm lo, pm hi, pc, my base in the bin
+  static constexpr size_t cur = tab + (size_t)kGB * 16;    // int[kGB] local candidate cursors
+  static constexpr size_t bytes = cur + (size_t)kGB * 4;
+  static_assert(recv + (size_t)kGB * 16 <= r1, "histogram region overlaps the bin table");
+};
+
+template <int CS>
+__global__ void __launch_bounds__(kGCT, 1)
+    gsel_cluster_kernel(const double* __restrict__ lm_all, int ld, const int* __restrict__ Ks, double p1, double p2,
+                        uint8_t* __restrict__ state_all, int* __restrict__ counts, int* __restrict__ gcid,
+                        double* __restrict__ gclm, unsigned long long* __restrict__ gcu,
+                        unsigned long long* __restrict__ gcex, int* __restrict__ gcpos) {
+  constexpr int W = kGB / CS;                      // bins per slice owner
+  constexpr int BPT = W > kGCT ? W / kGCT : 1;     // slice bins per thread
+  constexpr int NT = W / BPT;                      // threads holding slice bins
+  const int c = (int)cg::this_cluster().block_rank();
+  const int row = blockIdx.x / CS, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int K = Ks[row];
+  const double* lm = lm_all + (size_t)row * ld;
+  uint8_t* state = state_all + (size_t)row * ld;
+  extern __shared__ __align__(16) unsigned char g_dyn[];
+  unsigned* h0 = reinterpret_cast<unsigned*>(g_dyn + GcLayout::h0);
+  unsigned* h1 = reinterpret_cast<unsigned*>(g_dyn + GcLayout::h1);
+  unsigned* h2 = reinterpret_cast<unsigned*>(g_dyn + GcLayout::h2);
+  unsigned* hc = reinterpret_cast<unsigned*>(g_dyn + GcLayout::hc);
+  uint4* recv = reinterpret_cast<uint4*>(g_dyn + GcLayout::recv);
+  uint4* tab = reinterpret_cast<uint4*>(g_dyn + GcLayout::tab);
+  int* lcur = reinterpret_cast<int*>(g_dyn + GcLayout::cur);
+  __shared__ __align__(8) unsigned long long s_mb[5];  // A maxima, B histograms, C slice totals, D table, E candidates
+  __shared__ __align__(8) double s_cmax[kGCMaxCS];
+  __shared__ __align__(8) unsigned long long s_sm[kGCMaxCS];
+  __shared__ unsigned s_sc[kGCMaxCS];
+  __shared__ int s_rb1[kGCMaxCS];
+  __shared__ __align__(16) unsigned long long s_rbm[kGCMaxCS][2];
+  __shared__ double s_red[32];
+  __shared__ unsigned long long s_wm[33];
+  __shared__ unsigned s_wc[33];
+  __shared__ unsigned long long s_at1;
+  __shared__ int s_myb1, s_n1, s_n2, s_blo, s_bhi;
+  __shared__ __align__(16) unsigned long long s_myb1m[2];
+  if (tid == 0) {
+#pragma unroll
+    for (int i = 0; i < 5; ++i) mb_init(&s_mb[i]);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    mb_expect(&s_mb[0], CS * 8);
+    mb_expect(&s_mb[1], (unsigned)(CS * W * 16));
+    mb_expect(&s_mb[2], CS * 12);
+    mb_expect(&s_mb[3], (unsigned)(kGB * 16 + CS * 20));
+    s_myb1 = kGB;
+    s_n1 = 0;
+    s_n2 = 0;
+    s_at1 = 0ull;
+    s_blo = kGB;
+    s_bhi = -1;
+  }
+  for (int j = tid; j < kGB; j += kGCT) {
+    h0[j] = 0u;
+    h1[j] = 0u;
+    h2[j] = 0u;
+    hc[j] = 0u;
+    lcur[j] = 0;
+  }
+  // my elements: [e0, e1), thread tid holds e0 + tid + j * kGCT
+  const int per = (K + CS - 1) / CS;
+  const int e0 = min(K, c * per), e1 = min(K, e0 + per);
+  double x[kGCE];
+#pragma unroll
+  for (int j = 0; j < kGCE; ++j) {
+    const int i = e0 + tid + j * kGCT;
+    x[j] = i < e1 ? gsel_sanitise(lm[i]) : -CUDART_INF;
+  }
+  double m = x[0];
+#pragma unroll
+  for (int j = 1; j < kGCE; ++j) m = fmax(m, x[j]);
+  m = warp_max(m);
+  if (lane == 0) s_red[warp] = m;
+  __syncthreads();  // barrier init, zeroed histogram, warp maxima
+  cl_arrive_relaxed();  // (S) every CTA has started and initialised its barriers
+  const int dbg = g_gsel_dbg;
+  // ---- A: maxima
+  double cmax = -CUDART_INF;
+  if (tid < CS) {
+    double mm[32];
+#pragma unroll
+    for (int w = 0; w < 32; ++w) mm[w] = s_red[w];
+#pragma unroll
+    for (int h = 16; h > 0; h >>= 1)
+#pragma unroll
+      for (int w = 0; w < h; ++w) mm[w] = fmax(mm[w], mm[w + h]);
+    cmax = mm[0];
+  }
+  cl_wait();  // (S) -- .aligned: every thread, outside any divergent branch
+  if (tid < CS) push_f64(&s_cmax[c], tid, cmax, &s_mb[0]);
+  mb_wait0(&s_mb[0]);
+  double M = s_cmax[0];
+#pragma unroll
+  for (int r = 1; r < CS; ++r) M = fmax(M, s_cmax[r]);
+  if (dbg == 1) return;
+  // ---- B: local histogram -> the slice owners
+  unsigned long long pk[kGCE];
+#pragma unroll
+  for (int j = 0; j < kGCE; ++j) {
+    const int i = e0 + tid + j * kGCT;
+    pk[j] = 0ull;
+    if (i < e1) {
+      unsigned long long u;
+      int b;
+      gsel_elem(M, x[j], u, b);
+      pk[j] = (u << 11) | (unsigned long long)b;
+      if (u) {
+        atomicAdd(&h0[b], (unsigned)(u & 0x1FFFu));
+        if (u >> 13) atomicAdd(&h1[b], (unsigned)((u >> 13) & 0x1FFFu));
+        if (u >> 26) atomicAdd(&h2[b], (unsigned)(u >> 26));
+        atomicAdd(&hc[b], 1u);
+      }
+    }
+  }
+  __syncthreads();
+  for (int b = tid; b < kGB; b += kGCT) {
+    const int s = b / W;
+    push_v4(&recv[c * W + (b - s * W)], s, (int)h0[b], (int)h1[b], (int)h2[b], (int)hc[b], &s_mb[1]);
+  }
+  mb_wait0(&s_mb[1]);
+  if (dbg == 2) return;
+  // ---- C: my slice [c W, (c + 1) W): sums over the sources, slice totals
+  unsigned long long bm[BPT];
+  unsigned bc[BPT];
+  unsigned long long mloc = 0ull;
+  unsigned cloc = 0u;
+#pragma unroll
+  for (int k = 0; k < BPT; ++k) {
+    bm[k] = 0ull;
+    bc[k] = 0u;
+    if (tid < NT) {
+      const int lb = tid * BPT + k;
+#pragma unroll
+      for (int r = 0; r < CS; ++r) {
+        const uint4 v = recv[r * W + lb];
+        bm[k] += (unsigned long long)v.x + ((unsigned long long)v.y << 13) + ((unsigned long long)v.z << 26);
+        bc[k] += v.w;
+      }
+    }
+    mloc += bm[k];
+    cloc += bc[k];
+  }
+  unsigned long long mi = mloc;
+  unsigned ci = cloc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long tm = __shfl_up_sync(0xffffffffu, mi, o);
+    const unsigned tc = __shfl_up_sync(0xffffffffu, ci, o);
+    if (lane >= o) {
+      mi += tm;
+      ci += tc;
+    }
+  }
+  if (lane == 31) {
+    s_wm[warp] = mi;
+    s_wc[warp] = ci;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const unsigned long long w = s_wm[lane];
+    const unsigned wc = s_wc[lane];
+    unsigned long long wi = w;
+    unsigned wci = wc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long tm = __shfl_up_sync(0xffffffffu, wi, o);
+      const unsigned tc = __shfl_up_sync(0xffffffffu, wci, o);
+      if (lane >= o) {
+        wi += tm;
+        wci += tc;
+      }
+    }
+    s_wm[lane] = wi - w;
+    s_wc[lane] = wci - wc;
+    if (lane == 31) {
+      s_wm[32] = wi;
+      s_wc[32] = wci;
+    }
+  }
+  __syncthreads();
+  if (tid < CS) {
+    push_u64(&s_sm[c], tid, s_wm[32], &s_mb[2]);
+    push_u32(&s_sc[c], tid, s_wc[32], &s_mb[2]);
+  }
+  mb_wait0(&s_mb[2]);
+  unsigned long long T = 0ull, before = 0ull;
+  unsigned cbefore = 0u, ctot = 0u;
+#pragma unroll
+  for (int r = 0; r < CS; ++r) {
+    if (r < c) {
+      before += s_sm[r];
+      cbefore += s_sc[r];
+    }
+    T += s_sm[r];
+    ctot += s_sc[r];
+  }
+  const double thr1 = p1 * (double)T;
+  {
+    unsigned long long mex = before + s_wm[warp] + mi - mloc;
+    unsigned cex = cbefore + s_wc[warp] + ci - cloc;
+#pragma unroll
+    for (int k = 0; k < BPT; ++k) {
+      if (tid < NT) {
+        const int lb = tid * BPT + k, b = c * W + lb;
+        const unsigned long long inc = mex + bm[k];
+        if (bm[k] && (double)mex < thr1 && thr1 <= (double)inc) {
+          s_myb1 = b;
+          s_myb1m[0] = mex;
+          s_myb1m[1] = bm[k];
+        }
+        // every CTA: this bin's prefixes and that CTA's offset inside the bin
+        unsigned base = 0u;
+#pragma unroll
+        for (int r = 0; r < CS; ++r) {
+          push_v4(&tab[b], r, (int)(unsigned)mex, (int)(unsigned)(mex >> 32), (int)cex, (int)base, &s_mb[3]);
+          base += recv[r * W + lb].w;
+        }
+      }
+      mex += bm[k];
+      cex += bc[k];
+    }
+  }
+  __syncthreads();
+  if (tid < CS) {
+    push_u32(&s_rb1[c], tid, (unsigned)s_myb1, &s_mb[3]);
+    push_v2u64(&s_rbm[c][0], tid, s_myb1m[0], s_myb1m[1], &s_mb[3]);
+  }
+  mb_wait0(&s_mb[3]);
+  if (dbg == 3) return;
+  // ---- D: classify; candidates -> CTA 0
+  int b1 = kGB;
+  unsigned long long before1 = 0ull, mass1 = 0ull;
+#pragma unroll
+  for (int r = 0; r < CS; ++r)
+    if (s_rb1[r] < b1) {
+      b1 = s_rb1[r];
+      before1 = s_rbm[r][0];
+      mass1 = s_rbm[r][1];
+    }
+  auto pm_of = [&](int b) {
+    const uint4 t = tab[b];
+    return (unsigned long long)t.x | ((unsigned long long)t.y << 32);
+  };
+  auto pc_of = [&](int b) { return b < kGB ? (int)tab[b].z : (int)ctot; };
+  const bool none = T == 0ull || b1 >= kGB;  // no mass (a non-finite query)
+  const uint8_t zst = p1 >= 1.0 ? (p2 >= 1.0 ? 2 : 1) : 0;
+  const unsigned long long Tlo = none ? 0ull : ceil_u64(p2 * (double)before1),
+                           Thi = none ? 0ull : ceil_u64(p2 * (double)(before1 + mass1));
+  auto is_cand = [&](int b) {
+    const unsigned long long inc = b + 1 < kGB ? pm_of(b + 1) : T;
+    return b == b1 || (b < b1 && inc >= Tlo && pm_of(b) < Thi);
+  };
+  if (!none) {  // the stage-2 candidate bins below b1 form one range [blo, bhi] (prefixes are monotone)
+    int lo = kGB, hi = -1;
+    for (int b = tid; b < b1; b += kGCT)
+      if (is_cand(b)) {
+        lo = min(lo, b);
+        hi = max(hi, b);
+      }
+    lo = __reduce_min_sync(0xffffffffu, lo);
+    hi = __reduce_max_sync(0xffffffffu, hi);
+    if (lane == 0 && hi >= 0) {
+      atomicMin(&s_blo, lo);
+      atomicMax(&s_bhi, hi);
+    }
+  }
+  __syncthreads();
+  const int r1a = s_bhi >= 0 ? pc_of(s_blo) : 0, r1b = s_bhi >= 0 ? pc_of(s_bhi + 1) : 0;
+  const int r2a = none ? 0 : pc_of(b1), r2b = none ? 0 : pc_of(b1 + 1);
+  const int n1c = r1b - r1a, nc = n1c + (r2b - r2a);
+  const bool staged = nc <= kGCand;
+  auto sidx = [&](int slot) { return slot >= r2a ? n1c + (slot - r2a) : slot - r1a; };
+  if (c == 0 && tid == 0) mb_expect(&s_mb[4], staged ? (unsigned)nc * 20u : 0u);
+  unsigned long long* s_cu = reinterpret_cast<unsigned long long*>(g_dyn + GcLayout::cu);
+  double* s_clm = reinterpret_cast<double*>(g_dyn + GcLayout::clm);
+  int* s_cid = reinterpret_cast<int*>(g_dyn + GcLayout::cid);
+#pragma unroll
+  for (int j = 0; j < kGCE; ++j) {
+    const int i = e0 + tid + j * kGCT;
+    if (i >= e1) continue;
+    const unsigned long long u = pk[j] >> 11;
+    const int b = (int)(pk[j] & 2047u);
+    uint8_t st;
+    if (none || !u) {
+      st = zst;
+    } else if (b > b1) {
+      st = 0;
+    } else if (is_cand(b)) {
+      const int t = sidx(pc_of(b) + (int)tab[b].w + atomicAdd(&lcur[b], 1));
+      const double li = gsel_sanitise(lm[i]);  // (re-read: x[] is not kept live across the exchanges)
+      if (staged) {
+        push_u64(&s_cu[t], 0, u, &s_mb[4]);
+        push_f64(&s_clm[t], 0, li, &s_mb[4]);
+        push_u32(&s_cid[t], 0, (unsigned)i, &s_mb[4]);
+      } else {
+        gcu[(size_t)row * ld + t] = u;
+        gclm[(size_t)row * ld + t] = li;
+        gcid[(size_t)row * ld + t] = i;
+      }
+      continue;  // ranked by CTA 0
+    } else {
+      const unsigned long long inc = b + 1 < kGB ? pm_of(b + 1) : T;
+      st = inc < Tlo ? 2 : 1;
+    }
+    state[i] = st;
+  }
+  if (!staged) cl_sync();  // the global-scratch candidates are visible to CTA 0
+  if (c != 0) return;
+  if (staged) mb_wait0(&s_mb[4]);  // every candidate push has landed (CTA 0 must not exit before)
+  if (dbg == 4) return;
+  if (none) {
+    if (tid == 0) {
+      counts[2 * row] = p1 >= 1.0 ? K : 0;
+      counts[2 * row + 1] = p1 >= 1.0 && p2 >= 1.0 ? K : 0;
+    }
+    return;
+  }
+  // ---- E: CTA 0 ranks the candidates inside their bins (log-mass desc, index asc)
+  unsigned long long* a_cu = s_cu;
+  double* a_clm = s_clm;
+  int* a_cid = s_cid;
+  unsigned long long* a_cex = reinterpret_cast<unsigned long long*>(g_dyn + GcLayout::cex);
+  int* a_cpos = reinterpret_cast<int*>(g_dyn + GcLayout::cpos);
+  if (!staged) {
+    a_cu = gcu + (size_t)row * ld;
+    a_clm = gclm + (size_t)row * ld;
+    a_cid = gcid + (size_t)row * ld;
+    a_cex = gcex + (size_t)row * ld;
+    a_cpos = gcpos + (size_t)row * ld;
+  }
+  for (int t = tid; t < nc; t += kGCT) {
+    const int i = a_cid[t];
+    const double la = a_clm[t];
+    const unsigned long long u = a_cu[t];
+    unsigned long long uu;
+    int b;
+    gsel_elem(M, la, uu, b);
+    const int j0 = pc_of(b), j1 = pc_of(b + 1), k0 = sidx(j0);
+    int rk = 0;
+    unsigned long long pre = 0ull;
+    for (int j = 0; j < j1 - j0; ++j) {
+      const double lj = a_clm[k0 + j];
+      const int ij = a_cid[k0 + j];
+      const bool ahead = lj > la || (lj == la && ij < i);
+      rk += ahead;
+      pre += ahead ? a_cu[k0 + j] : 0ull;
+    }
+    const int ps = j0 + rk;
+    const unsigned long long ex = pm_of(b) + pre;
+    a_cpos[t] = ps;
+    a_cex[t] = ex;
+    if ((double)ex < thr1 && thr1 <= (double)(ex + u)) {
+      s_n1 = ps + 1;
+      s_at1 = ex + u;
+    }
+  }
+  __syncthreads();
+  const int n1 = p1 >= 1.0 ? K : s_n1;
+  const double thr2 = p2 * (double)s_at1;
+  for (int t = tid; t < nc; t += kGCT)
+    if ((double)a_cex[t] < thr2 && thr2 <= (double)(a_cex[t] + a_cu[t])) s_n2 = a_cpos[t] + 1;
+  __syncthreads();
+  const int n2 = p1 >= 1.0 && p2 >= 1.0 ? K : s_n2;
+  for (int t = tid; t < nc; t += kGCT) state[a_cid[t]] = a_cpos[t] < n2 ? 2 : (a_cpos[t] < n1 ? 1 : 0);
+  if (tid == 0) {
+    counts[2 * row] = n1;
+    counts[2 * row + 1] = n2;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // LSE merge of P partials: out_parts [P, rows, d], lse_parts [P, rows]
 // ---------------------------------------------------------------------------
 __global__ void lse_merge_kernel(const float* __restrict__ out_parts, const float* __restrict__ lse_parts, int P,
@@ -970,8 +1385,20 @@ cudaError_t launch_lloyd_sums(const void* pts, int dtype, int units, int n, int 
   return cudaGetLastError();
 }
 size_t select_global_ws_bytes(int rows, int ld) {
-  return (size_t)rows * ld * (8 + 8 + 4 + 4) +
-         (size_t)rows * (sizeof(GSelRow) + kGB * 8 + (kGB + 1) * 4 + kGB * 4) + 64;
+  const size_t split = (size_t)rows * ld * (8 + 8 + 4 + 4) +
+                       (size_t)rows * (sizeof(GSelRow) + kGB * 8 + (kGB + 1) * 4 + kGB * 4) + 64;
+  const size_t clustered = (size_t)rows * ld * (4 + 8 + 8 + 8 + 4) + 64;  // candidate overflow scratch
+  return split > clustered ? split : clustered;
+}
+
+int g_gsel_path = 0;
+int set_gsel_dbg(int v) { return cudaMemcpyToSymbol(g_gsel_dbg, &v, sizeof(int)) == cudaSuccess ? 0 : 2; }  // dp_debug_set(11, .): 0 auto, 1 split launches, 2 one CTA per row, 3 clustered
+
+// cluster size for the one-launch form: 8192 elements per CTA, power of two <= 8
+static int gsel_cluster_size(int ld) {
+  int cs = 1;
+  while (cs < kGCMaxCS && (long long)cs * kGCT * kGCE < ld) cs <<= 1;
+  return (long long)cs * kGCT * kGCE >= ld ? cs : 0;
 }
 cudaError_t launch_select_global(const double* lm, int rows, int ld, const int* Ks, double p1, double p2,
                                  uint8_t* state, int* counts, void* ws, cudaStream_t st) {
@@ -986,8 +1413,43 @@ cudaError_t launch_select_global(const double* lm, int rows, int ld, const int* 
     cudaFuncSetAttribute(gs_rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGDyn);
     attr[dev] = true;
   }
+  const int CS = gsel_cluster_size(ld);
+  if ((g_gsel_path == 0 || g_gsel_path == 3) && CS > 0) {
+    const void* fn = CS == 1 ? reinterpret_cast<const void*>(gsel_cluster_kernel<1>)
+                     : CS == 2 ? reinterpret_cast<const void*>(gsel_cluster_kernel<2>)
+                     : CS == 4 ? reinterpret_cast<const void*>(gsel_cluster_kernel<4>)
+                               : reinterpret_cast<const void*>(gsel_cluster_kernel<8>);
+    cudaError_t e = ensure_smem(fn, GcLayout::bytes);
+    if (e != cudaSuccess) return e;
+    int* gcid = reinterpret_cast<int*>(ws);
+    double* gclm = reinterpret_cast<double*>(gcid + ((size_t)rows * ld + 1) / 2 * 2);
+    unsigned long long* gcu = reinterpret_cast<unsigned long long*>(gclm + (size_t)rows * ld);
+    unsigned long long* gcex = gcu + (size_t)rows * ld;
+    int* gcpos = reinterpret_cast<int*>(gcex + (size_t)rows * ld);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(rows * CS);
+    cfg.blockDim = dim3(kGCT);
+    cfg.dynamicSmemBytes = GcLayout::bytes;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CS;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    switch (CS) {
+      case 1: return cudaLaunchKernelEx(&cfg, gsel_cluster_kernel<1>, lm, ld, Ks, p1, p2, state, counts, gcid, gclm, gcu, gcex, gcpos);
+      case 2: return cudaLaunchKernelEx(&cfg, gsel_cluster_kernel<2>, lm, ld, Ks, p1, p2, state, counts, gcid, gclm, gcu, gcex, gcpos);
+      case 4: return cudaLaunchKernelEx(&cfg, gsel_cluster_kernel<4>, lm, ld, Ks, p1, p2, state, counts, gcid, gclm, gcu, gcex, gcpos);
+      default: return cudaLaunchKernelEx(&cfg, gsel_cluster_kernel<8>, lm, ld, Ks, p1, p2, state, counts, gcid, gclm, gcu, gcex, gcpos);
+    }
+  }
   // split over several CTAs per row when one SM per row would be the bound
-  const int S = ld >= 8192 ? (rows * 8 <= 2 * sm_count() ? 8 : (rows * 4 <= 2 * sm_count() ? 4 : 1)) : 1;
+  const int S = g_gsel_path == 2 ? 1
+                : (ld >= 8192 || g_gsel_path == 1)
+                    ? (rows * 8 <= 2 * sm_count() ? 8 : (rows * 4 <= 2 * sm_count() ? 4 : 1))
+                    : 1;
   if (S > 1) {
     char* x = reinterpret_cast<char*>(cand + (size_t)rows * ld);
     x += (16 - (reinterpret_cast<uintptr_t>(x) & 15)) & 15;

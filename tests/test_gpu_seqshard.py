@@ -239,3 +239,58 @@ def test_select_global_large_k_vs_oracle(K):
             assert "real" not in (c1, c2), (r, p1, p2, c1, c2)
             n1 = int((st[r] >= 1).sum())
             assert int(cnt[r, 0]) == n1 and int(cnt[r, 1]) == int((st[r] == 2).sum())
+
+
+@pytest.mark.parametrize("K", [700, 8192, 20000, 32766, 50000])
+def test_select_global_paths_identical(K):
+    """The one-launch clustered selection (DSMEM exchanges, the default up to
+    K = 65,536), the five-launch split form and the one-CTA-per-row kernel
+    give bit-identical states and counts -- including rows so flat that the
+    candidates overflow shared memory into global scratch, rows with -inf /
+    NaN entries, exact ties and ragged per-row K."""
+    from paper_2602_05191_b200 import _native as N
+
+    rng = np.random.default_rng(K)
+    rows = []
+    for kind in ("peaked", "flat", "ties", "nonfinite", "tiny"):
+        base = rng.normal(0.0, 1.0, K) + np.log(rng.integers(1, 80, K))
+        if kind == "peaked":
+            base[rng.integers(0, K, max(1, K // 100))] += rng.uniform(4, 14, max(1, K // 100))
+        elif kind == "flat":
+            base = base * 0.01
+        elif kind == "ties":
+            base = np.round(base * 4) / 4
+        elif kind == "nonfinite":
+            base[rng.integers(0, K, 50)] = -np.inf
+            base[rng.integers(0, K, 5)] = np.nan
+        else:
+            base = np.full(K, -np.inf)
+        rows.append(base)
+    lm = torch.from_numpy(np.stack(rows)).cuda()
+    R = lm.shape[0]
+    ks = torch.tensor([K, K, max(1, K - 3), K, K], dtype=torch.int32, device="cuda")
+    lib = N.lib()
+    s = torch.cuda.current_stream().cuda_stream
+    ws = torch.empty((lib.dp_select_global_workspace_bytes(R, K),), dtype=torch.uint8, device="cuda")
+    res = {}
+    try:
+        for path in (3, 1, 2):
+            if path == 3 and K > 65536:
+                continue
+            lib.dp_debug_set(11, path)
+            for p1, p2 in ((0.95, 0.7), (0.5, 0.9), (1.0, 0.7), (1.0, 1.0)):
+                st = torch.full((R, K), 9, dtype=torch.uint8, device="cuda")
+                cnt = torch.zeros((R, 2), dtype=torch.int32, device="cuda")
+                N.check(lib.dp_select_global(N.ptr(lm), R, K, N.ptr(ks), p1, p2, N.ptr(st), N.ptr(cnt), N.ptr(ws),
+                                             ws.numel(), s))
+                torch.cuda.synchronize()
+                res[(path, p1, p2)] = (st.cpu(), cnt.cpu())
+    finally:
+        lib.dp_debug_set(11, 0)
+    for (path, p1, p2), (st, cnt) in res.items():
+        ref_st, ref_cnt = res[(2, p1, p2)]
+        for r in range(R):
+            kk = int(ks[r])
+            assert torch.equal(st[r, :kk], ref_st[r, :kk]), (path, p1, p2, r)
+            assert int(cnt[r, 0]) == int((st[r, :kk] >= 1).sum()) and int(cnt[r, 1]) == int((st[r, :kk] == 2).sum())
+        assert torch.equal(cnt, ref_cnt), (path, p1, p2)
