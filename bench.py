@@ -860,6 +860,8 @@ def run_seqshard(a):
     from paper_2602_05191_b200 import _native as N
     from paper_2602_05191_b200 import cluster_layer
     from paper_2602_05191_b200.cache import dtype_code, head_seed
+    import torch.distributed as dist
+
     from paper_2602_05191_b200.seqshard import Comm
     from paper_2602_05191_b200.sharding import seq_shard_bounds
     from paper_2602_05191_b200.workload import generate_layer, generate_queries
@@ -912,6 +914,11 @@ def run_seqshard(a):
     ws = torch.zeros((wsb,), dtype=torch.uint8, device=dev)
     views = [lay.view() for lay in layers]
     stats = torch.zeros((L, 1, H, 4), dtype=torch.int32, device=dev)
+    # dp_plan's shape limit; the in-place selection's (P * cap <= 65536)
+    use_plan = cap <= 4096 and P * cap <= 65536 and os.environ.get("DP_SEQ_UNFUSED") is None
+    parts_lm = torch.full((P, Hq, cap), -math.inf, dtype=torch.float64, device=dev)
+    h_st = torch.zeros((Hq, P * cap), dtype=torch.uint8, device=dev)
+    h_k = torch.full((Hq,), P * cap, dtype=torch.int32, device=dev)
 
     def layer_step(li, s, ev=None):
         cs = torch.cuda.current_stream(dev).cuda_stream
@@ -919,10 +926,34 @@ def run_seqshard(a):
         lay, v = layers[li], views[li]
         if ev is not None:
             ev[0].record()
-        lm.fill_(-math.inf)
-        N.check(lib.dp_score(v, N.ptr(q), dtype_code(q), G, scale, N.ptr(lm), cs))
+        if use_plan:  # the fused plan's scoring phase (-inf past K); its work-list phase runs on the global states below
+            N.check(lib.dp_plan_score(v, N.ptr(q), dtype_code(q), G, scale, N.ptr(lm), N.ptr(ws), ws.numel(), cs))
+        else:
+            lm.fill_(-math.inf)
+            N.check(lib.dp_score(v, N.ptr(q), dtype_code(q), G, scale, N.ptr(lm), cs))
         if ev is not None:
             ev[1].record()
+        if use_plan:  # in place: the selection reads the gathered [P, Hq, cap] slices, the plan its slice of states
+            if real:
+                dist.all_gather_into_tensor(parts_lm, lm[0])
+            else:  # stand-ins for the other ranks' slices: this rank's own slice
+                parts_lm.copy_(lm[0].unsqueeze(0).expand(P, Hq, cap))
+            if ev is not None:
+                ev[2].record()
+            N.check(lib.dp_select_global_parts(N.ptr(parts_lm), Hq, P, cap, N.ptr(h_k), a.p1, a.p2, N.ptr(h_st),
+                                               N.ptr(g_cnt), N.ptr(g_ws), g_ws.numel(), cs))
+            if ev is not None:
+                ev[3].record()
+            N.check(lib.dp_plan_given(v, N.ptr(q), dtype_code(q), G, scale, N.ptr(lm), N.ptr(h_st[:, r * cap:]),
+                                      P * cap, N.ptr(stats[li]), N.ptr(ws), ws.numel(), cs))
+            N.check(lib.dp_attend(v, N.ptr(q), dtype_code(q), G, scale, N.ptr(lm), N.ptr(out), N.ptr(lse), N.ptr(ws),
+                                  ws.numel(), cs))
+            if ev is not None:
+                ev[4].record()
+            merge_step()
+            if ev is not None:
+                ev[5].record()
+            return
         if real:
             g_lm.view(Hq, P, cap).copy_(comm.all_gather(lm[0]).permute(1, 0, 2))
         else:  # stand-ins for the other ranks' slices: this rank's own slice
@@ -938,15 +969,19 @@ def run_seqshard(a):
                                         N.ptr(lse), N.ptr(stats[li]), N.ptr(ws), ws.numel(), cs))
         if ev is not None:
             ev[4].record()
+        merge_step()
+        if ev is not None:
+            ev[5].record()
+
+    def merge_step():
+        cs = torch.cuda.current_stream(dev).cuda_stream
         if real:
-            parts_o.copy_(comm.all_gather(out))
-            parts_l.copy_(comm.all_gather(lse))
+            dist.all_gather_into_tensor(parts_o, out)
+            dist.all_gather_into_tensor(parts_l, lse)
         else:
             parts_o.copy_(out.unsqueeze(0).expand_as(parts_o))
             parts_l.copy_(lse.unsqueeze(0).expand_as(parts_l))
         N.check(lib.dp_lse_merge(N.ptr(parts_o), N.ptr(parts_l), P, Hq, d, N.ptr(merged), N.ptr(merged_l), cs))
-        if ev is not None:
-            ev[5].record()
 
     sampler = ClockSampler(local)
     for s in range(a.warmup):

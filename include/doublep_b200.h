@@ -140,6 +140,22 @@ int dp_plan(const dp_cache_view* v, const void* q, int32_t q_dtype, int32_t gqa_
             int32_t* counts, int32_t* stats, void* workspace, size_t workspace_bytes,
             void* stream);
 
+/* The fused plan split around an OUTSIDE selection (config 5: the two-stage
+ * top-p runs over the global, all-gathered log-mass table, dp_select_global):
+ *   dp_plan_score: phase 1 only -- log_mass [B, H, G, cluster_cap] of this
+ *     cache's clusters (-inf past each head's cluster count), then exit;
+ *   dp_plan_given: the plan with the states READ from `state` ([B, H, G]
+ *     rows of stride state_ld, 0 = cluster_cap; 0 dropped / 1 approximated /
+ *     2 exact) instead of
+ *     selected; builds the work lists dp_attend consumes (log_mass as
+ *     written by dp_plan_score for the same q).
+ * Same shape limits as dp_plan. */
+int dp_plan_score(const dp_cache_view* v, const void* q, int32_t q_dtype, int32_t gqa_group, double scale,
+                  double* log_mass, void* workspace, size_t workspace_bytes, void* stream);
+int dp_plan_given(const dp_cache_view* v, const void* q, int32_t q_dtype, int32_t gqa_group, double scale,
+                  double* log_mass, const uint8_t* state, int32_t state_ld, int32_t* stats, void* workspace,
+                  size_t workspace_bytes, void* stream);
+
 /* score + select + sparse attention in one call (decode_step,
  * engine.py:267-278).  Implementations, chosen by geometry:
  *   - dp_plan + dp_attend (fused plan, then a persistent attention grid
@@ -370,6 +386,15 @@ int dp_select_global(const double* log_mass, int32_t rows, int32_t ld, const int
 /* The exchange step's merge (engine.py:234-246 across shards): partials
  * out_parts [parts, rows, d] fp32 with lse_parts [parts, rows] (-inf: empty)
  * -> out [rows, d], lse [rows]; fp64 weights. */
+/* dp_select_global over the all-gathered slices read IN PLACE:
+ * log_mass_parts [parts, rows, part_len] (slot k of part p is global entry
+ * p * part_len + k; holes hold -inf), state [rows, parts * part_len].  The
+ * one-launch cluster form only: parts * part_len <= 65536 (else
+ * DP_ERR_UNSUPPORTED). */
+int dp_select_global_parts(const double* log_mass_parts, int32_t rows, int32_t parts, int32_t part_len,
+                           const int32_t* nclusters, double p1, double p2, uint8_t* state, int32_t* counts,
+                           void* workspace, size_t workspace_bytes, void* stream);
+
 int dp_lse_merge(const float* out_parts, const float* lse_parts, int32_t parts, int32_t rows, int32_t d, float* out,
                  float* lse, void* stream);
 

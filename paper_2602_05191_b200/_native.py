@@ -62,6 +62,10 @@ _SIGS = {
                                  ctypes.c_double, _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp]),
     "dp_plan": (ctypes.c_int, [ctypes.POINTER(CacheView), _vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_double,
                                ctypes.c_double, ctypes.c_double, _vp, _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp]),
+    "dp_plan_score": (ctypes.c_int, [ctypes.POINTER(CacheView), _vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_double,
+                                     _vp, _vp, ctypes.c_size_t, _vp]),
+    "dp_plan_given": (ctypes.c_int, [ctypes.POINTER(CacheView), _vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_double,
+                                     _vp, _vp, ctypes.c_int32, _vp, _vp, ctypes.c_size_t, _vp]),
     "dp_debug_plan_timing": (ctypes.c_int, [_vp]),
     "dp_debug_plan_clock": (ctypes.c_int, [_vp]),
     "dp_debug_attn_timing": (ctypes.c_int, [_vp]),
@@ -109,6 +113,8 @@ _SIGS = {
     "dp_select_global_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int32, ctypes.c_int32]),
     "dp_select_global": (ctypes.c_int, [_vp, ctypes.c_int32, ctypes.c_int32, _vp, ctypes.c_double, ctypes.c_double,
                                         _vp, _vp, _vp, ctypes.c_size_t, _vp]),
+    "dp_select_global_parts": (ctypes.c_int, [_vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _vp,
+                                              ctypes.c_double, ctypes.c_double, _vp, _vp, _vp, ctypes.c_size_t, _vp]),
     "dp_lse_merge": (ctypes.c_int, [_vp, _vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _vp, _vp, _vp]),
     "dp_kn_scaled_logits": (ctypes.c_int, [_vp, ctypes.c_int32, ctypes.c_int64, ctypes.c_int32, _vp, ctypes.c_int64,
                                            _vp, ctypes.c_double, _vp]),

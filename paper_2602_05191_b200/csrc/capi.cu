@@ -138,6 +138,35 @@ int dp_plan(const dp_cache_view* v, const void* q, int32_t q_dtype, int32_t G, d
   return e == cudaSuccess ? DP_OK : cuda_fail(e, "dp_plan");
 }
 
+int dp_plan_score(const dp_cache_view* v, const void* q, int32_t q_dtype, int32_t G, double scale, double* log_mass,
+                  void* ws, size_t ws_bytes, void* stream) {
+  int r = check_view(v, G);
+  if (r) return r;
+  if ((r = check_q(q_dtype))) return r;
+  if (!log_mass) return fail(DP_ERR_INVALID, "log_mass buffer required");
+  if (ws_bytes < dp_decode_workspace_bytes(v, G)) return fail(DP_ERR_INVALID, "workspace too small");
+  if (!dp::plan_supported(*v, G))
+    return fail(DP_ERR_UNSUPPORTED, "fused plan needs cluster_cap <= 4096 and row_cap < 2^24");
+  cudaError_t e = dp::launch_plan(*v, q, q_dtype, G, scale, 1.0, 1.0, log_mass, nullptr, nullptr, nullptr, ws,
+                                  (cudaStream_t)stream, 1 << 8);
+  return e == cudaSuccess ? DP_OK : cuda_fail(e, "dp_plan_score");
+}
+
+int dp_plan_given(const dp_cache_view* v, const void* q, int32_t q_dtype, int32_t G, double scale, double* log_mass,
+                  const uint8_t* state, int32_t state_ld, int32_t* stats, void* ws, size_t ws_bytes, void* stream) {
+  int r = check_view(v, G);
+  if (r) return r;
+  if ((r = check_q(q_dtype))) return r;
+  if (!log_mass || !state) return fail(DP_ERR_INVALID, "log_mass and state buffers required");
+  if (ws_bytes < dp_decode_workspace_bytes(v, G)) return fail(DP_ERR_INVALID, "workspace too small");
+  if (!dp::plan_supported(*v, G))
+    return fail(DP_ERR_UNSUPPORTED, "fused plan needs cluster_cap <= 4096 and row_cap < 2^24");
+  if (state_ld != 0 && state_ld < v->cluster_cap) return fail(DP_ERR_INVALID, "state_ld below cluster_cap");
+  cudaError_t e = dp::launch_plan(*v, q, q_dtype, G, scale, 1.0, 1.0, log_mass, const_cast<uint8_t*>(state), nullptr,
+                                  stats, ws, (cudaStream_t)stream, 1 << 9, state_ld);
+  return e == cudaSuccess ? DP_OK : cuda_fail(e, "dp_plan_given");
+}
+
 int dp_decode_step(const dp_cache_view* v, const void* q, int32_t q_dtype, int32_t G, double scale, double p1,
                    double p2, double* log_mass, uint8_t* state, int32_t* counts, float* out, float* lse,
                    int32_t* stats, void* ws, size_t ws_bytes, void* stream) {
@@ -307,6 +336,22 @@ int dp_select_global(const double* log_mass, int32_t rows, int32_t ld, const int
   cudaError_t e = dp::launch_select_global(log_mass, rows, ld, nclusters, p1, p2, state, counts, workspace,
                                            (cudaStream_t)stream);
   return e == cudaSuccess ? DP_OK : cuda_fail(e, "dp_select_global");
+}
+
+int dp_select_global_parts(const double* log_mass_parts, int32_t rows, int32_t parts, int32_t part_len,
+                           const int32_t* nclusters, double p1, double p2, uint8_t* state, int32_t* counts,
+                           void* workspace, size_t workspace_bytes, void* stream) {
+  int r;
+  if ((r = check_p(p1, "p1")) || (r = check_p(p2, "p2"))) return r;
+  if (!log_mass_parts || !nclusters || !state || !counts) return fail(DP_ERR_INVALID, "dp_select_global: null buffer");
+  if (rows < 1 || parts < 1 || part_len < 1) return fail(DP_ERR_INVALID, "dp_select_global: empty input");
+  if (!dp::select_global_parts_supported(parts, part_len))
+    return fail(DP_ERR_UNSUPPORTED, "dp_select_global_parts: parts * part_len must be <= 65536");
+  const int ld = parts * part_len;
+  if (workspace_bytes < dp::select_global_ws_bytes(rows, ld)) return fail(DP_ERR_INVALID, "workspace too small");
+  cudaError_t e = dp::launch_select_global(log_mass_parts, rows, ld, nclusters, p1, p2, state, counts, workspace,
+                                           (cudaStream_t)stream, part_len);
+  return e == cudaSuccess ? DP_OK : cuda_fail(e, "dp_select_global_parts");
 }
 
 int dp_lse_merge(const float* out_parts, const float* lse_parts, int32_t parts, int32_t rows, int32_t d, float* out,

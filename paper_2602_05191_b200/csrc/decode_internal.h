@@ -83,7 +83,8 @@ cudaError_t launch_attend(const dp_cache_view& v, const void* q, int qdt, int G,
 cudaError_t launch_attn_tc(const dp_cache_view& v, const void* q, int qdt, int G, double scale, const double* lm,
                            WorkLists wl, Partials<float> pt, float* out, float* lse, bool dense, cudaStream_t st);
 cudaError_t launch_plan(const dp_cache_view& v, const void* q, int qdt, int G, double scale, double p1, double p2,
-                        double* lm, uint8_t* state, int* counts, int* stats, void* ws, cudaStream_t st);
+                        double* lm, uint8_t* state, int* counts, int* stats, void* ws, cudaStream_t st, int mode = 0,
+                        int state_ld = 0);
 bool plan_supported(const dp_cache_view& v, int G);
 // 2-D TMA map over all centroid rows [B*H*cap, d] fp32 (32-float x 128-row boxes, 128B swizzle), cached
 cudaError_t centroid_tmap(const dp_cache_view& v, CUtensorMap* m);
@@ -122,7 +123,8 @@ size_t select_global_ws_bytes(int rows, int ld);
 extern int g_gsel_path;  // dp_debug_set(11, .)
 int set_gsel_dbg(int v);  // dp_debug_set(12, .)
 cudaError_t launch_select_global(const double* lm, int rows, int ld, const int* Ks, double p1, double p2,
-                                 uint8_t* state, int* counts, void* ws, cudaStream_t st);
+                                 uint8_t* state, int* counts, void* ws, cudaStream_t st, int part_len = 0);
+bool select_global_parts_supported(int parts, int part_len);
 cudaError_t launch_lse_merge(const float* out_parts, const float* lse_parts, int P, int rows, int d, float* out,
                              float* lse, cudaStream_t st);
 

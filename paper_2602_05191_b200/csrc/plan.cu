@@ -47,6 +47,8 @@ namespace cg = cooperative_groups;
 
 namespace dp {
 
+constexpr int kPlanScoreOnly = 1 << 8;     // mode: score only (log-masses out, then exit)
+constexpr int kPlanGivenStates = 1 << 9;  // mode: states read from state_out (an outside selection), not selected
 constexpr int kPT = 512;          // threads per CTA
 constexpr int kPW = kPT / 32;     // warps per CTA
 constexpr int kBins = 1024;       // log-mass bins of width 1/32 nat: span 32 nats, past the 27 nats where a 2^-38 mass rounds to 0
@@ -136,7 +138,7 @@ template <int kG>
 __global__ void __launch_bounds__(kPT, 1)
     plan_kernel(const __grid_constant__ CUtensorMap tmC, dp_cache_view v, const void* __restrict__ q, int qdt, int G,
                 double scale, double p1, double p2, double* __restrict__ lm_out, uint8_t* __restrict__ state_out,
-                int* __restrict__ counts, WorkLists wl, int CL, int boxr, int dbg) {
+                int* __restrict__ counts, WorkLists wl, int CL, int boxr, int dbg, int sld) {
   cg::cluster_group cluster = cg::this_cluster();
   const int r = (int)cluster.block_rank();
   const int bh = blockIdx.x / CL;
@@ -196,11 +198,13 @@ __global__ void __launch_bounds__(kPT, 1)
   // zero), K = 4 dims; fp32 centroids and queries are exact in fp64.
   const int qP = d + 4;  // padded fp64 query rows: conflict-free B-fragment loads
   const unsigned bar0 = (unsigned)__cvta_generic_to_shared(&s_tbar[0]);
-  const int ntile = (nloc + kCh - 1) / kCh;
+  // given states: the log-masses are already written (dp_plan_score) -- no scoring pass
+  const int ntile = dbg & kPlanGivenStates ? 0 : (nloc + kCh - 1) / kCh;
   const int ncb = d / 32;  // 128-B column blocks per row
   if (tid == 0) {
     // bytes each hand-off barrier of this CTA receives
-    if (r < G) mb_expect(&s_mb[0], (unsigned)(K * 8 + CL * 16));
+    // (given states: no scores travel, only the slice maxima)
+    if (r < G) mb_expect(&s_mb[0], (unsigned)((dbg & kPlanGivenStates ? 0 : K * 8) + CL * 16));
     unsigned eb = (unsigned)(G * 4 * ((nloc + 3) / 4));
     if (r == 0) eb += (unsigned)(G * 8 + (CL > G ? (CL - G) * G * 8 : 0));
     mb_expect(&s_mb[1], eb);
@@ -298,6 +302,15 @@ __global__ void __launch_bounds__(kPT, 1)
   stamp(r, 2);
   double lmax[2] = {-CUDART_INF, -CUDART_INF};  // heads 2(l%4), 2(l%4)+1
   const double* qrow = qd + (lane >> 2) * qP + (lane & 3);  // B fragment: q[head l/4][4 kk + l%4]
+  if (dbg & kPlanGivenStates) {  // my slice's maxima from the written log-masses (same lane -> head map as below)
+#pragma unroll 1
+    for (int row = tid >> 2; row < nloc; row += kPT / 4)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int h = 2 * (lane & 3) + e;
+        if (h < G) lmax[e] = fmax(lmax[e], lm_out[((size_t)bh * G + h) * cap + k0 + row]);
+      }
+  }
 #pragma unroll 1
   for (int t = 0; t < ntile; ++t) {
     const int row0 = t * kCh;
@@ -438,6 +451,14 @@ __global__ void __launch_bounds__(kPT, 1)
     __syncthreads();  // (the zeroed histogram too)
   }
   stamp(r, 4);
+  if (dbg & kPlanScoreOnly) {  // log-masses written; every push into an owner has landed (A)
+    // slots [K, cap) read -inf (a table of several slices has holes there)
+#pragma unroll 1
+    for (int i = K + r * kPT + tid; i < cap; i += CL * kPT)
+#pragma unroll 1
+      for (int h = 0; h < G; ++h) lm_out[((size_t)bh * G + h) * cap + i] = -CUDART_INF;
+    return;
+  }
 
   // ---------------- P2: two-stage top-p, owner CTA g = r -------------------
   if (r < G) {
@@ -462,7 +483,11 @@ __global__ void __launch_bounds__(kPT, 1)
     }
     stamp(r, 20);
     int n1 = 0, n2 = 0;
-    if (dbg & 2) {  // timing experiment: no selection (nothing but sink/window selected)
+    if (dbg & kPlanGivenStates) {  // the states come from outside (a global selection): load them
+      const uint8_t* sin = state_out + (size_t)hq * sld;  // row stride sld (>= cap)
+      for (int i = tid; i < K; i += kPT) stown[i] = sin[i];
+      __syncthreads();
+    } else if (dbg & 2) {  // timing experiment: no selection (nothing but sink/window selected)
       for (int i = tid; i < K; i += kPT) stown[i] = 0;
       __syncthreads();
     } else {
@@ -492,7 +517,7 @@ __global__ void __launch_bounds__(kPT, 1)
         push_u32(stl + g * L.per + (i - rr * per), rr, w, &s_mb[1]);
       }
     }
-    if (tid == 0) {
+    if (tid == 0 && !(dbg & kPlanGivenStates)) {
       counts[2 * hq] = n1;
       counts[2 * hq + 1] = n2;
     }
@@ -600,7 +625,7 @@ __global__ void __launch_bounds__(kPT, 1)
     tot_a += c2;
   }
   stamp(r, 16);
-  if (state_out)  // debug states of my slice
+  if (state_out && !(dbg & kPlanGivenStates))  // debug states of my slice
 #pragma unroll 1
     for (int i = tid; i < G * nloc; i += kPT) {
       const int g = i / nloc, k = i - g * nloc;
@@ -808,7 +833,8 @@ bool plan_supported(const dp_cache_view& v, int G) {
 }
 
 cudaError_t launch_plan(const dp_cache_view& v, const void* q, int qdt, int G, double scale, double p1, double p2,
-                        double* lm, uint8_t* state, int* counts, int* stats, void* ws, cudaStream_t st) {
+                        double* lm, uint8_t* state, int* counts, int* stats, void* ws, cudaStream_t st, int mode,
+                        int state_ld) {
   WorkLists wl;
   decode_ws_layout(&v, G, &wl, nullptr, nullptr, reinterpret_cast<char*>(ws));
   wl.stats = stats;
@@ -837,10 +863,10 @@ cudaError_t launch_plan(const dp_cache_view& v, const void* q, int qdt, int G, d
   const long long rows = (long long)v.batch * v.kv_heads * v.cluster_cap;
   const int boxr = rows < kCh ? (int)rows : kCh;  // rows per TMA box (the tile is never fuller than that)
   switch (kG) {
-    case 1: return cudaLaunchKernelEx(&cfg, plan_kernel<1>, tm, v, q, qdt, G, scale, p1, p2, lm, state, counts, wl, CL, boxr, g_plan_dbg);
-    case 2: return cudaLaunchKernelEx(&cfg, plan_kernel<2>, tm, v, q, qdt, G, scale, p1, p2, lm, state, counts, wl, CL, boxr, g_plan_dbg);
-    case 4: return cudaLaunchKernelEx(&cfg, plan_kernel<4>, tm, v, q, qdt, G, scale, p1, p2, lm, state, counts, wl, CL, boxr, g_plan_dbg);
-    default: return cudaLaunchKernelEx(&cfg, plan_kernel<8>, tm, v, q, qdt, G, scale, p1, p2, lm, state, counts, wl, CL, boxr, g_plan_dbg);
+    case 1: return cudaLaunchKernelEx(&cfg, plan_kernel<1>, tm, v, q, qdt, G, scale, p1, p2, lm, state, counts, wl, CL, boxr, g_plan_dbg | mode, state_ld > 0 ? state_ld : v.cluster_cap);
+    case 2: return cudaLaunchKernelEx(&cfg, plan_kernel<2>, tm, v, q, qdt, G, scale, p1, p2, lm, state, counts, wl, CL, boxr, g_plan_dbg | mode, state_ld > 0 ? state_ld : v.cluster_cap);
+    case 4: return cudaLaunchKernelEx(&cfg, plan_kernel<4>, tm, v, q, qdt, G, scale, p1, p2, lm, state, counts, wl, CL, boxr, g_plan_dbg | mode, state_ld > 0 ? state_ld : v.cluster_cap);
+    default: return cudaLaunchKernelEx(&cfg, plan_kernel<8>, tm, v, q, qdt, G, scale, p1, p2, lm, state, counts, wl, CL, boxr, g_plan_dbg | mode, state_ld > 0 ? state_ld : v.cluster_cap);
   }
 }
 

@@ -965,7 +965,8 @@ struct GcLayout {
 
 template <int CS>
 __global__ void __launch_bounds__(kGCT, 1)
-    gsel_cluster_kernel(const double* __restrict__ lm_all, int ld, const int* __restrict__ Ks, double p1, double p2,
+    gsel_cluster_kernel(const double* __restrict__ lm_all, int ld, int part_len, long long part_stride,
+                        const int* __restrict__ Ks, double p1, double p2,
                         uint8_t* __restrict__ state_all, int* __restrict__ counts, int* __restrict__ gcid,
                         double* __restrict__ gclm, unsigned long long* __restrict__ gcu,
                         unsigned long long* __restrict__ gcex, int* __restrict__ gcpos) {
@@ -975,7 +976,12 @@ __global__ void __launch_bounds__(kGCT, 1)
   const int c = (int)cg::this_cluster().block_rank();
   const int row = blockIdx.x / CS, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int K = Ks[row];
-  const double* lm = lm_all + (size_t)row * ld;
+  // element i of the row: part i / part_len, slot i % part_len (one part: the row itself;
+  // several: the all-gathered [parts, rows, part_len] slices read in place)
+  const double* lm = lm_all + (size_t)row * (part_stride ? part_len : ld);
+  auto lm_at = [&](int i) {
+    return part_stride ? lm[(long long)(i / part_len) * part_stride + (i % part_len)] : lm[i];
+  };
   uint8_t* state = state_all + (size_t)row * ld;
   extern __shared__ __align__(16) unsigned char g_dyn[];
   unsigned* h0 = reinterpret_cast<unsigned*>(g_dyn + GcLayout::h0);
@@ -1026,7 +1032,7 @@ __global__ void __launch_bounds__(kGCT, 1)
 #pragma unroll
   for (int j = 0; j < kGCE; ++j) {
     const int i = e0 + tid + j * kGCT;
-    x[j] = i < e1 ? gsel_sanitise(lm[i]) : -CUDART_INF;
+    x[j] = i < e1 ? gsel_sanitise(lm_at(i)) : -CUDART_INF;
   }
   double m = x[0];
 #pragma unroll
@@ -1249,7 +1255,7 @@ __global__ void __launch_bounds__(kGCT, 1)
       st = 0;
     } else if (is_cand(b)) {
       const int t = sidx(pc_of(b) + (int)tab[b].w + atomicAdd(&lcur[b], 1));
-      const double li = gsel_sanitise(lm[i]);  // (re-read: x[] is not kept live across the exchanges)
+      const double li = gsel_sanitise(lm_at(i));  // (re-read: x[] is not kept live across the exchanges)
       if (staged) {
         push_u64(&s_cu[t], 0, u, &s_mb[4]);
         push_f64(&s_clm[t], 0, li, &s_mb[4]);
@@ -1400,21 +1406,24 @@ static int gsel_cluster_size(int ld) {
   while (cs < kGCMaxCS && (long long)cs * kGCT * kGCE < ld) cs <<= 1;
   return (long long)cs * kGCT * kGCE >= ld ? cs : 0;
 }
+bool select_global_parts_supported(int parts, int part_len) {
+  return gsel_cluster_size((int)((long long)parts * part_len)) > 0 && (long long)parts * part_len < (1ll << 31);
+}
 cudaError_t launch_select_global(const double* lm, int rows, int ld, const int* Ks, double p1, double p2,
-                                 uint8_t* state, int* counts, void* ws, cudaStream_t st) {
+                                 uint8_t* state, int* counts, void* ws, cudaStream_t st, int part_len) {
   unsigned long long* ex = reinterpret_cast<unsigned long long*>(ws);
   unsigned long long* pk = ex + (size_t)rows * ld;
   int* pos = reinterpret_cast<int*>(pk + (size_t)rows * ld);
   int* cand = pos + (size_t)rows * ld;
-  static bool attr[64] = {};
-  const int dev = current_device();
-  if (!attr[dev]) {
-    cudaFuncSetAttribute(select_global_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGDyn);
-    cudaFuncSetAttribute(gs_rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGDyn);
-    attr[dev] = true;
-  }
+  cudaError_t ea = ensure_smem(reinterpret_cast<const void*>(select_global_kernel), kGDyn);
+  if (ea == cudaSuccess) ea = ensure_smem(reinterpret_cast<const void*>(gs_rank_kernel), kGDyn);
+  if (ea != cudaSuccess) return ea;
+  // part_len > 0: lm is [ld / part_len, rows, part_len] (the one-launch form reads it in place)
+  const long long part_stride = part_len > 0 ? (long long)rows * part_len : 0;
+  if (part_len <= 0) part_len = ld;
   const int CS = gsel_cluster_size(ld);
-  if ((g_gsel_path == 0 || g_gsel_path == 3) && CS > 0) {
+  if (part_stride && !(CS > 0)) return cudaErrorInvalidValue;
+  if ((g_gsel_path == 0 || g_gsel_path == 3 || part_stride) && CS > 0) {
     const void* fn = CS == 1 ? reinterpret_cast<const void*>(gsel_cluster_kernel<1>)
                      : CS == 2 ? reinterpret_cast<const void*>(gsel_cluster_kernel<2>)
                      : CS == 4 ? reinterpret_cast<const void*>(gsel_cluster_kernel<4>)
@@ -1439,10 +1448,10 @@ cudaError_t launch_select_global(const double* lm, int rows, int ld, const int* 
     cfg.attrs = at;
     cfg.numAttrs = 1;
     switch (CS) {
-      case 1: return cudaLaunchKernelEx(&cfg, gsel_cluster_kernel<1>, lm, ld, Ks, p1, p2, state, counts, gcid, gclm, gcu, gcex, gcpos);
-      case 2: return cudaLaunchKernelEx(&cfg, gsel_cluster_kernel<2>, lm, ld, Ks, p1, p2, state, counts, gcid, gclm, gcu, gcex, gcpos);
-      case 4: return cudaLaunchKernelEx(&cfg, gsel_cluster_kernel<4>, lm, ld, Ks, p1, p2, state, counts, gcid, gclm, gcu, gcex, gcpos);
-      default: return cudaLaunchKernelEx(&cfg, gsel_cluster_kernel<8>, lm, ld, Ks, p1, p2, state, counts, gcid, gclm, gcu, gcex, gcpos);
+      case 1: return cudaLaunchKernelEx(&cfg, gsel_cluster_kernel<1>, lm, ld, part_len, part_stride, Ks, p1, p2, state, counts, gcid, gclm, gcu, gcex, gcpos);
+      case 2: return cudaLaunchKernelEx(&cfg, gsel_cluster_kernel<2>, lm, ld, part_len, part_stride, Ks, p1, p2, state, counts, gcid, gclm, gcu, gcex, gcpos);
+      case 4: return cudaLaunchKernelEx(&cfg, gsel_cluster_kernel<4>, lm, ld, part_len, part_stride, Ks, p1, p2, state, counts, gcid, gclm, gcu, gcex, gcpos);
+      default: return cudaLaunchKernelEx(&cfg, gsel_cluster_kernel<8>, lm, ld, part_len, part_stride, Ks, p1, p2, state, counts, gcid, gclm, gcu, gcex, gcpos);
     }
   }
   // split over several CTAs per row when one SM per row would be the bound

@@ -375,12 +375,24 @@ class SeqShardState:
                     c0, c1 = int(info.c_lo[info.rank, b, h]), int(info.c_lo[info.rank + 1, b, h])
                     mine_dst[row, :c1 - c0] = np.arange(c0, c1)
         valid = src >= 0
+        # the same entries in the in-place form's [rows, P * cap] table (slot rr * cap + k)
+        self.hole_idx = torch.from_numpy(np.where(valid, (src // cap // self.rows) * cap + src % cap, 0)).to(dev)
         self.src_idx = torch.from_numpy(np.where(valid, src, 0)).to(dev)
         self.src_valid = torch.from_numpy(valid).to(dev)
         mv = mine_dst >= 0
         self.mine_idx = torch.from_numpy(np.where(mv, mine_dst, 0)).to(dev)
         self.mine_valid = torch.from_numpy(mv).to(dev)
         self.cap = cap
+        self.use_plan = True  # the fused plan split around the global selection (falls back by shape)
+        # in-place form: the selection reads the all-gathered [P, rows, cap] slices directly and the
+        # plan reads this rank's states out of the [rows, P * cap] table (no gather / scatter copies)
+        self.P = P
+        self.in_place = P * cap <= 65536
+        self.h_state = torch.zeros((self.rows, P * cap), dtype=torch.uint8, device=dev) if self.in_place else None
+        self.h_k = torch.full((self.rows,), P * cap, dtype=torch.int32, device=dev)
+        if self.in_place:
+            self.h_ws = torch.empty((max(N.lib().dp_select_global_workspace_bytes(self.rows, P * cap), 1),),
+                                    dtype=torch.uint8, device=dev)
 
 
 def seqshard_decode(q, lay: ClusteredLayer, info: ShardInfo, comm: Comm, p1=0.95, p2=0.7, *, state=None,
@@ -401,8 +413,32 @@ def seqshard_decode(q, lay: ClusteredLayer, info: ShardInfo, comm: Comm, p1=0.95
     st = torch.cuda.current_stream(dev).cuda_stream
     lib = N.lib()
     view = lay.view()
-    # 1. scores of my cluster slice
-    N.check(lib.dp_score(view, N.ptr(q), dtype_code(q), G, lay.attn_scale, N.ptr(S.log_mass), st))
+    # 1. scores of my cluster slice: the fused plan's scoring phase (dp_plan_score), or
+    #    the standalone kernel where the plan does not take the shape
+    if S.use_plan:
+        rc = lib.dp_plan_score(view, N.ptr(q), dtype_code(q), G, lay.attn_scale, N.ptr(S.log_mass), N.ptr(S.ws),
+                               S.ws.numel(), st)
+        if rc == N.DP_ERR_UNSUPPORTED:
+            S.use_plan = False
+        else:
+            N.check(rc)
+    if not S.use_plan:
+        N.check(lib.dp_score(view, N.ptr(q), dtype_code(q), G, lay.attn_scale, N.ptr(S.log_mass), st))
+    # 2.-4. in place: the selection reads the all-gathered slices where they landed, the plan reads
+    #    my slice's states out of the holey [rows, P * cap] table (dp_plan_score left -inf in the holes)
+    if S.use_plan and S.in_place:
+        parts = comm.all_gather(S.log_mass.reshape(S.rows, S.cap))  # [P, rows, cap]
+        N.check(lib.dp_select_global_parts(N.ptr(parts), S.rows, S.P, S.cap, N.ptr(S.h_k), p1, p2, N.ptr(S.h_state),
+                                           N.ptr(S.g_counts), N.ptr(S.h_ws), S.h_ws.numel(), st))
+        mine = S.h_state[:, info.rank * S.cap:]
+        N.check(lib.dp_plan_given(view, N.ptr(q), dtype_code(q), G, lay.attn_scale, N.ptr(S.log_mass), N.ptr(mine),
+                                  S.P * S.cap, None, N.ptr(S.ws), S.ws.numel(), st))
+        N.check(lib.dp_attend(view, N.ptr(q), dtype_code(q), G, lay.attn_scale, N.ptr(S.log_mass), N.ptr(S.out),
+                              N.ptr(S.lse), N.ptr(S.ws), S.ws.numel(), st))
+        if return_plan:  # the global table in global cluster order (as the copying form keeps it)
+            S.g_state.copy_(torch.where(S.src_valid, torch.gather(S.h_state, 1, S.hole_idx),
+                                        torch.zeros_like(S.g_state)))
+        return _merge(S, lay, comm, lib, st, return_plan)
     # 2. the global log-mass table (all-gathered slices, global cluster order)
     parts = comm.all_gather(S.log_mass.reshape(S.rows, S.cap))  # [P, rows, cap]
     flat = parts.reshape(-1)
@@ -413,8 +449,19 @@ def seqshard_decode(q, lay: ClusteredLayer, info: ShardInfo, comm: Comm, p1=0.95
     # 4. my slice's states -> local attention over my exact clusters and pseudo-rows
     S.state.reshape(S.rows, S.cap).copy_(torch.where(S.mine_valid, torch.gather(S.g_state, 1, S.mine_idx),
                                                      torch.zeros_like(S.mine_idx, dtype=torch.uint8)))
-    N.check(lib.dp_sparse_attention(view, N.ptr(q), dtype_code(q), G, lay.attn_scale, N.ptr(S.log_mass),
-                                    N.ptr(S.state), N.ptr(S.out), N.ptr(S.lse), None, N.ptr(S.ws), S.ws.numel(), st))
+    if S.use_plan:  # work lists from the given states (cluster-distributed, DSMEM), then the attention grid
+        N.check(lib.dp_plan_given(view, N.ptr(q), dtype_code(q), G, lay.attn_scale, N.ptr(S.log_mass), N.ptr(S.state),
+                                  0, None, N.ptr(S.ws), S.ws.numel(), st))
+        N.check(lib.dp_attend(view, N.ptr(q), dtype_code(q), G, lay.attn_scale, N.ptr(S.log_mass), N.ptr(S.out),
+                              N.ptr(S.lse), N.ptr(S.ws), S.ws.numel(), st))
+    else:
+        N.check(lib.dp_sparse_attention(view, N.ptr(q), dtype_code(q), G, lay.attn_scale, N.ptr(S.log_mass),
+                                        N.ptr(S.state), N.ptr(S.out), N.ptr(S.lse), None, N.ptr(S.ws), S.ws.numel(),
+                                        st))
+    return _merge(S, lay, comm, lib, st, return_plan)
+
+
+def _merge(S, lay, comm, lib, st, return_plan):
     # 5. the exchange step: all-gather of the partials + the LSE merge kernel
     outs = comm.all_gather(S.out)   # [P, B, Hq, d]
     lses = comm.all_gather(S.lse)   # [P, B, Hq]
