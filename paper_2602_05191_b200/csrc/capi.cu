@@ -148,7 +148,7 @@ int dp_plan_score(const dp_cache_view* v, const void* q, int32_t q_dtype, int32_
   if (!dp::plan_supported(*v, G))
     return fail(DP_ERR_UNSUPPORTED, "fused plan needs cluster_cap <= 4096 and row_cap < 2^24");
   cudaError_t e = dp::launch_plan(*v, q, q_dtype, G, scale, 1.0, 1.0, log_mass, nullptr, nullptr, nullptr, ws,
-                                  (cudaStream_t)stream, 1 << 8);
+                                  (cudaStream_t)stream, 1);
   return e == cudaSuccess ? DP_OK : cuda_fail(e, "dp_plan_score");
 }
 
@@ -163,7 +163,7 @@ int dp_plan_given(const dp_cache_view* v, const void* q, int32_t q_dtype, int32_
     return fail(DP_ERR_UNSUPPORTED, "fused plan needs cluster_cap <= 4096 and row_cap < 2^24");
   if (state_ld != 0 && state_ld < v->cluster_cap) return fail(DP_ERR_INVALID, "state_ld below cluster_cap");
   cudaError_t e = dp::launch_plan(*v, q, q_dtype, G, scale, 1.0, 1.0, log_mass, const_cast<uint8_t*>(state), nullptr,
-                                  stats, ws, (cudaStream_t)stream, 1 << 9, state_ld);
+                                  stats, ws, (cudaStream_t)stream, 2, state_ld);
   return e == cudaSuccess ? DP_OK : cuda_fail(e, "dp_plan_given");
 }
 

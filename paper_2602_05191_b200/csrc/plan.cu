@@ -47,8 +47,9 @@ namespace cg = cooperative_groups;
 
 namespace dp {
 
-constexpr int kPlanScoreOnly = 1 << 8;     // mode: score only (log-masses out, then exit)
-constexpr int kPlanGivenStates = 1 << 9;  // mode: states read from state_out (an outside selection), not selected
+// kMode (compile time, so the normal plan carries none of it): 0 the plan; 1 score only
+// (log-masses out, then exit); 2 states read from state_out (an outside selection), not selected
+constexpr int kModePlan = 0, kModeScore = 1, kModeGiven = 2;
 constexpr int kPT = 512;          // threads per CTA
 constexpr int kPW = kPT / 32;     // warps per CTA
 constexpr int kBins = 1024;       // log-mass bins of width 1/32 nat: span 32 nats, past the 27 nats where a 2^-38 mass rounds to 0
@@ -134,7 +135,7 @@ __device__ __forceinline__ T* remote(cg::cluster_group& c, T* p, int rank) {
 }
 
 
-template <int kG>
+template <int kG, int kMode>
 __global__ void __launch_bounds__(kPT, 1)
     plan_kernel(const __grid_constant__ CUtensorMap tmC, dp_cache_view v, const void* __restrict__ q, int qdt, int G,
                 double scale, double p1, double p2, double* __restrict__ lm_out, uint8_t* __restrict__ state_out,
@@ -199,12 +200,12 @@ __global__ void __launch_bounds__(kPT, 1)
   const int qP = d + 4;  // padded fp64 query rows: conflict-free B-fragment loads
   const unsigned bar0 = (unsigned)__cvta_generic_to_shared(&s_tbar[0]);
   // given states: the log-masses are already written (dp_plan_score) -- no scoring pass
-  const int ntile = dbg & kPlanGivenStates ? 0 : (nloc + kCh - 1) / kCh;
+  const int ntile = kMode == kModeGiven ? 0 : (nloc + kCh - 1) / kCh;
   const int ncb = d / 32;  // 128-B column blocks per row
   if (tid == 0) {
     // bytes each hand-off barrier of this CTA receives
     // (given states: no scores travel, only the slice maxima)
-    if (r < G) mb_expect(&s_mb[0], (unsigned)((dbg & kPlanGivenStates ? 0 : K * 8) + CL * 16));
+    if (r < G) mb_expect(&s_mb[0], (unsigned)((kMode == kModeGiven ? 0 : K * 8) + CL * 16));
     unsigned eb = (unsigned)(G * 4 * ((nloc + 3) / 4));
     if (r == 0) eb += (unsigned)(G * 8 + (CL > G ? (CL - G) * G * 8 : 0));
     mb_expect(&s_mb[1], eb);
@@ -302,7 +303,7 @@ __global__ void __launch_bounds__(kPT, 1)
   stamp(r, 2);
   double lmax[2] = {-CUDART_INF, -CUDART_INF};  // heads 2(l%4), 2(l%4)+1
   const double* qrow = qd + (lane >> 2) * qP + (lane & 3);  // B fragment: q[head l/4][4 kk + l%4]
-  if (dbg & kPlanGivenStates) {  // my slice's maxima from the written log-masses (same lane -> head map as below)
+  if (kMode == kModeGiven) {  // my slice's maxima from the written log-masses (same lane -> head map as below)
 #pragma unroll 1
     for (int row = tid >> 2; row < nloc; row += kPT / 4)
 #pragma unroll
@@ -451,7 +452,7 @@ __global__ void __launch_bounds__(kPT, 1)
     __syncthreads();  // (the zeroed histogram too)
   }
   stamp(r, 4);
-  if (dbg & kPlanScoreOnly) {  // log-masses written; every push into an owner has landed (A)
+  if (kMode == kModeScore) {  // log-masses written; every push into an owner has landed (A)
     // slots [K, cap) read -inf (a table of several slices has holes there)
 #pragma unroll 1
     for (int i = K + r * kPT + tid; i < cap; i += CL * kPT)
@@ -483,7 +484,7 @@ __global__ void __launch_bounds__(kPT, 1)
     }
     stamp(r, 20);
     int n1 = 0, n2 = 0;
-    if (dbg & kPlanGivenStates) {  // the states come from outside (a global selection): load them
+    if (kMode == kModeGiven) {  // the states come from outside (a global selection): load them
       const uint8_t* sin = state_out + (size_t)hq * sld;  // row stride sld (>= cap)
       for (int i = tid; i < K; i += kPT) stown[i] = sin[i];
       __syncthreads();
@@ -517,7 +518,7 @@ __global__ void __launch_bounds__(kPT, 1)
         push_u32(stl + g * L.per + (i - rr * per), rr, w, &s_mb[1]);
       }
     }
-    if (tid == 0 && !(dbg & kPlanGivenStates)) {
+    if (tid == 0 && kMode != kModeGiven) {
       counts[2 * hq] = n1;
       counts[2 * hq + 1] = n2;
     }
@@ -625,7 +626,7 @@ __global__ void __launch_bounds__(kPT, 1)
     tot_a += c2;
   }
   stamp(r, 16);
-  if (state_out && !(dbg & kPlanGivenStates))  // debug states of my slice
+  if (state_out && kMode != kModeGiven)  // debug states of my slice
 #pragma unroll 1
     for (int i = tid; i < G * nloc; i += kPT) {
       const int g = i / nloc, k = i - g * nloc;
@@ -755,17 +756,21 @@ static cudaError_t centroid_tmap_encode(const dp_cache_view& v, CUtensorMap* m) 
 static int group_bound(int G) { return G <= 1 ? 1 : (G <= 2 ? 2 : (G <= 4 ? 4 : 8)); }
 
 template <int kG>
-static void* plan_fn() {
-  return reinterpret_cast<void*>(plan_kernel<kG>);
+static void* plan_fn(int mode) {
+  return mode == kModeScore ? reinterpret_cast<void*>(plan_kernel<kG, kModeScore>)
+         : mode == kModeGiven ? reinterpret_cast<void*>(plan_kernel<kG, kModeGiven>)
+                              : reinterpret_cast<void*>(plan_kernel<kG, kModePlan>);
 }
-static void* plan_fn_for(int kG) {
-  return kG == 1 ? plan_fn<1>() : kG == 2 ? plan_fn<2>() : kG == 4 ? plan_fn<4>() : plan_fn<8>();
+static void* plan_fn_for(int kG, int mode = kModePlan) {
+  return kG == 1 ? plan_fn<1>(mode) : kG == 2 ? plan_fn<2>(mode) : kG == 4 ? plan_fn<4>(mode) : plan_fn<8>(mode);
 }
 
 // the kernel's dynamic shared-memory limit only ever grows (the occupancy
 // queries below and the launches share it; lowering it for a query would
 // make a later, larger launch fail)
-static void ensure_smem_attr(int kG, size_t smem) { ensure_smem(plan_fn_for(kG), smem, true); }
+static void ensure_smem_attr(int kG, size_t smem) {
+  for (int mode = 0; mode < 3; ++mode) ensure_smem(plan_fn_for(kG, mode), smem, true);
+}
 
 // co-resident clusters of size cl at this shared-memory footprint
 static int max_active_clusters(int kG, int cl, size_t smem) {
@@ -832,6 +837,21 @@ bool plan_supported(const dp_cache_view& v, int G) {
          v.row_cap < (1 << 24) && cl_fits(v, G, 8);
 }
 
+template <int kG>
+static cudaError_t launch_plan_mode(const cudaLaunchConfig_t& cfg, int mode, const CUtensorMap& tm,
+                                    const dp_cache_view& v, const void* q, int qdt, int G, double scale, double p1,
+                                    double p2, double* lm, uint8_t* state, int* counts, WorkLists wl, int CL, int boxr,
+                                    int sld) {
+  if (mode == kModeScore)
+    return cudaLaunchKernelEx(&cfg, plan_kernel<kG, kModeScore>, tm, v, q, qdt, G, scale, p1, p2, lm, state, counts, wl,
+                              CL, boxr, g_plan_dbg, sld);
+  if (mode == kModeGiven)
+    return cudaLaunchKernelEx(&cfg, plan_kernel<kG, kModeGiven>, tm, v, q, qdt, G, scale, p1, p2, lm, state, counts, wl,
+                              CL, boxr, g_plan_dbg, sld);
+  return cudaLaunchKernelEx(&cfg, plan_kernel<kG, kModePlan>, tm, v, q, qdt, G, scale, p1, p2, lm, state, counts, wl, CL,
+                            boxr, g_plan_dbg, sld);
+}
+
 cudaError_t launch_plan(const dp_cache_view& v, const void* q, int qdt, int G, double scale, double p1, double p2,
                         double* lm, uint8_t* state, int* counts, int* stats, void* ws, cudaStream_t st, int mode,
                         int state_ld) {
@@ -862,11 +882,12 @@ cudaError_t launch_plan(const dp_cache_view& v, const void* q, int qdt, int G, d
   if (e != cudaSuccess) return e;
   const long long rows = (long long)v.batch * v.kv_heads * v.cluster_cap;
   const int boxr = rows < kCh ? (int)rows : kCh;  // rows per TMA box (the tile is never fuller than that)
+  const int sld = state_ld > 0 ? state_ld : v.cluster_cap;
   switch (kG) {
-    case 1: return cudaLaunchKernelEx(&cfg, plan_kernel<1>, tm, v, q, qdt, G, scale, p1, p2, lm, state, counts, wl, CL, boxr, g_plan_dbg | mode, state_ld > 0 ? state_ld : v.cluster_cap);
-    case 2: return cudaLaunchKernelEx(&cfg, plan_kernel<2>, tm, v, q, qdt, G, scale, p1, p2, lm, state, counts, wl, CL, boxr, g_plan_dbg | mode, state_ld > 0 ? state_ld : v.cluster_cap);
-    case 4: return cudaLaunchKernelEx(&cfg, plan_kernel<4>, tm, v, q, qdt, G, scale, p1, p2, lm, state, counts, wl, CL, boxr, g_plan_dbg | mode, state_ld > 0 ? state_ld : v.cluster_cap);
-    default: return cudaLaunchKernelEx(&cfg, plan_kernel<8>, tm, v, q, qdt, G, scale, p1, p2, lm, state, counts, wl, CL, boxr, g_plan_dbg | mode, state_ld > 0 ? state_ld : v.cluster_cap);
+    case 1: return launch_plan_mode<1>(cfg, mode, tm, v, q, qdt, G, scale, p1, p2, lm, state, counts, wl, CL, boxr, sld);
+    case 2: return launch_plan_mode<2>(cfg, mode, tm, v, q, qdt, G, scale, p1, p2, lm, state, counts, wl, CL, boxr, sld);
+    case 4: return launch_plan_mode<4>(cfg, mode, tm, v, q, qdt, G, scale, p1, p2, lm, state, counts, wl, CL, boxr, sld);
+    default: return launch_plan_mode<8>(cfg, mode, tm, v, q, qdt, G, scale, p1, p2, lm, state, counts, wl, CL, boxr, sld);
   }
 }
 

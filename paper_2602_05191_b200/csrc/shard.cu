@@ -1341,28 +1341,37 @@ __global__ void __launch_bounds__(kGCT, 1)
 // ---------------------------------------------------------------------------
 __global__ void lse_merge_kernel(const float* __restrict__ out_parts, const float* __restrict__ lse_parts, int P,
                                  int rows, int d, float* __restrict__ out, float* __restrict__ lse) {
-  const int row = blockIdx.x;
+  const int row = blockIdx.x, tid = threadIdx.x;
   __shared__ double s_w[64];
   __shared__ double s_L;
-  if (threadIdx.x == 0) {  // the P weights once per row (fp64), then every dim reuses them
-    float M = -INFINITY;
-    for (int p = 0; p < P; ++p) M = fmaxf(M, lse_parts[(size_t)p * rows + row]);
-    double L = 0.0;
-    for (int p = 0; p < P; ++p) {
-      const float l = lse_parts[(size_t)p * rows + row];
-      const double w = l != -INFINITY ? exp((double)l - (double)M) : 0.0;
-      s_w[p] = w;
-      L += w;
+  if (tid < 32) {  // the P weights once per row (fp64, one lane per part), then every dim reuses them
+    const float l = tid < P ? lse_parts[(size_t)tid * rows + row] : -INFINITY;
+    const float l2 = tid + 32 < P ? lse_parts[(size_t)(tid + 32) * rows + row] : -INFINITY;
+    float M = fmaxf(l, l2);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+    const double w = l != -INFINITY ? exp((double)l - (double)M) : 0.0;
+    const double w2 = l2 != -INFINITY ? exp((double)l2 - (double)M) : 0.0;
+    if (tid < P) s_w[tid] = w;
+    if (tid + 32 < P) s_w[tid + 32] = w2;
+    double L = w + w2;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+    if (tid == 0) {
+      s_L = L;
+      lse[row] = L > 0.0 ? (float)((double)M + log(L)) : -INFINITY;
     }
-    s_L = L;
-    lse[row] = L > 0.0 ? (float)((double)M + log(L)) : -INFINITY;
   }
   __syncthreads();
   const double L = s_L;
-  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+  for (int c = tid; c < d; c += blockDim.x) {
     double acc = 0.0;
-    for (int p = 0; p < P; ++p)
-      if (s_w[p] > 0.0) acc += s_w[p] * (double)out_parts[((size_t)p * rows + row) * d + c];
+#pragma unroll 8
+    for (int p = 0; p < P; ++p) {  // (unrolled: the part loads are independent and go out together)
+      const float x = out_parts[((size_t)p * rows + row) * d + c];
+      const double w = s_w[p];
+      if (w > 0.0) acc += w * (double)x;
+    }
     out[(size_t)row * d + c] = L > 0.0 ? (float)(acc / L) : 0.f;
   }
 }
