@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
   };
 
   auto flush = [&](int bh, float* scratch) {
-    if (!kDense && !(dbg & 64)) {  // drain this warp's remaining approx entries
+    if (!kDense && !DP_AB(dbg, 64)) {  // drain this warp's remaining approx entries
       if (ap_ready) ap_fold();
 #pragma unroll 1
       while (ap_k < ap_n) {
@@ -555,7 +555,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
     if (idx == 0) astamp(2);
     __nv_bfloat16* Ks = KV + (size_t)s * 2 * kStageElems;
     const __nv_bfloat16* Vs = Ks + kStageElems;
-    if (!(dbg & 1) && r0w < nr) {
+    if (!DP_AB(dbg, 1) && r0w < nr) {
       // ---- S = K Q^T for this warp's 16 rows (two accumulators: short chains)
       float sa[4] = {0.f, 0.f, 0.f, 0.f}, sb[4] = {0.f, 0.f, 0.f, 0.f};
       {
@@ -634,7 +634,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
             "{%0,%1,%2,%3};\n"
             : "+f"(o[mb][0]), "+f"(o[mb][1]), "+f"(o[mb][2]), "+f"(o[mb][3])
             : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(bh0), "r"(bh1));
-        if (!(dbg & 32))  // (32: timing experiment -- P's low half dropped)
+        if (!DP_AB(dbg, 32))  // (32: timing experiment -- P's low half dropped)
           asm volatile(
               "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
               "{%0,%1,%2,%3};\n"
@@ -642,16 +642,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
               : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(bl0), "r"(bl1));
       }
     }
-    if (!kDense && !(dbg & 64)) {  // one approx pseudo-row per tile: fold the loaded one, issue the next
+    if (!kDense && !DP_AB(dbg, 64)) {  // one approx pseudo-row per tile: fold the loaded one, issue the next
       if (ap_ready) ap_fold();       // (64: timing experiment, no approx pseudo-rows)
       if (ap_k < ap_n) ap_issue(bh);
     }
-    if (seg_end && !(dbg & 2)) flush(bh, reinterpret_cast<float*>(Ks));  // this stage's K buffer is the scratch
+    if (seg_end && !DP_AB(dbg, 2)) flush(bh, reinterpret_cast<float*>(Ks));  // this stage's K buffer is the scratch
     __syncwarp();
     if (lane == 0) mbar_arrive(smem_u32(&empty_bar[s]));  // stage s free for the producer
   }
   astamp(3);
-  if (dbg & 10) return;  // timing experiments: no flush / merge (2), no counters / merge (8)
+  if DP_AB(dbg, 10) return;  // timing experiments: no flush / merge (2), no counters / merge (8)
   if (tid == 0) {  // profiling: rows and head segments of this CTA
     astamp_at(7, (unsigned long long)(r1 - r0));
     astamp_at(8, (unsigned long long)nflushed);
@@ -677,7 +677,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(dp_cache_view v,
   // (approximated clusters: logit = log-mass, value = value mean).  One
   // round trip: warp w streams partials w, w+8, ... with an online rescale,
   // then the 8 warp states are combined in shared memory.
-  const int nm = (dbg & 4) ? 0 : s_nmerge;  // (4: timing experiment, no merge)
+  const int nm = DP_AB(dbg, 4) ? 0 : s_nmerge;  // (4: timing experiment, no merge)
   if (nm == 0) {
     astamp(5);
     return;

@@ -8,6 +8,17 @@
 
 #include "doublep_b200.h"
 
+// Timing-experiment switches (dp_debug_set 0 / 10: skip a phase, drop P's low
+// half, ...) are compiled in only with -DDP_AB_KNOBS
+// (DP_EXTRA_FLAGS=-DDP_AB_KNOBS python -m paper_2602_05191_b200.build; the A/B
+// tools need it).  The product build carries none of their branches: runtime
+// mode checks in the plan cost ~0.27 us per layer at 32K (measured).
+#ifdef DP_AB_KNOBS
+#define DP_AB(dbg, mask) (((dbg) & (mask)) != 0)
+#else
+#define DP_AB(dbg, mask) (false)
+#endif
+
 namespace dp {
 
 constexpr int kMaxGroup = 8;  // GQA group sizes the decode kernels are built for

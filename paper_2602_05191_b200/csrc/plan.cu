@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(kPT, 1)
   // the slice's later tiles (only two fit in shared memory) are requested
   // into L2 now: the centroid tables are layer-static, so this also overlaps
   // the previous grid's tail, and the refills after the wait hit L2
-  if (tid == 0 && ntile > 2 && !(dbg & 32)) {
+  if (tid == 0 && ntile > 2 && !DP_AB(dbg, 32)) {
     const char* cbase = reinterpret_cast<const char*>(v.centroids) + ((size_t)bh * cap + k0) * d * 4;
     const size_t rest = (size_t)(nloc - 2 * kCh) * d * 4;
     for (size_t o = 0; o < rest; o += 65536)
@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(kPT, 1)
     // let the attention grid become resident on the SMs this launch leaves free
     // (its CTAs wait for our completion before reading anything we write)
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
-    if (dbg & 64) {  // timing experiment: the launch + dependency-wait floor
+    if DP_AB(dbg, 64) {  // timing experiment: the launch + dependency-wait floor
       cl_wait();
       return;
     }
@@ -294,7 +294,7 @@ __global__ void __launch_bounds__(kPT, 1)
     }
   }
   __syncthreads();  // qd, offs, barrier init
-  if (dbg & 128) {  // timing experiment: + the query load
+  if DP_AB(dbg, 128) {  // timing experiment: + the query load
     cl_wait();
     return;
   }
@@ -488,7 +488,7 @@ __global__ void __launch_bounds__(kPT, 1)
       const uint8_t* sin = state_out + (size_t)hq * sld;  // row stride sld (>= cap)
       for (int i = tid; i < K; i += kPT) stown[i] = sin[i];
       __syncthreads();
-    } else if (dbg & 2) {  // timing experiment: no selection (nothing but sink/window selected)
+    } else if DP_AB(dbg, 2) {  // timing experiment: no selection (nothing but sink/window selected)
       for (int i = tid; i < K; i += kPT) stown[i] = 0;
       __syncthreads();
     } else {
@@ -571,7 +571,7 @@ __global__ void __launch_bounds__(kPT, 1)
   stamp(r, 5);
   mb_wait0(&s_mb[1]);  // (B) every cluster state of my slice (CTA 0: and the head maxima) is in place
   stamp(r, 6);
-  if (dbg & 4) return;  // timing experiment: no work lists
+  if DP_AB(dbg, 4) return;  // timing experiment: no work lists
 
   // ---------------- P3: union rows of my slice ----------------------------
   // Slice-local exclusive offsets (rows; approx | exact << 16 cluster counts)
@@ -607,7 +607,7 @@ __global__ void __launch_bounds__(kPT, 1)
   stamp(r, 15);
   if (tid < CL) push_v4(&s_cnt[r][0], tid, t_rows, t_pk >> 16, t_pk & 0xFFFF, 0, &s_mb[2]);
   stamp(r, 7);
-  if (!(dbg & 16)) mb_wait0(&s_mb[2]);  // (C) every slice's counts are in place; no remote access after this
+  if (!DP_AB(dbg, 16)) mb_wait0(&s_mb[2]);  // (C) every slice's counts are in place; no remote access after this
   stamp(r, 8);
 
   // ---------------- P4: work lists -----------------------------------------
@@ -655,7 +655,7 @@ __global__ void __launch_bounds__(kPT, 1)
       if (ma) apx[apx_base + s_ao[i]] = make_int2(k0 + i, ma);
     }
     // warp-cooperative expansion of the warp's 32 clusters: lanes write consecutive rows
-    unsigned todo = __ballot_sync(0xffffffffu, len > 0 && !(dbg & 8));
+    unsigned todo = __ballot_sync(0xffffffffu, len > 0 && !DP_AB(dbg, 8));
 #pragma unroll 1
     while (todo) {
       const int t = __ffs(todo) - 1;

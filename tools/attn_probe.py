@@ -1,6 +1,8 @@
 """Time dense / sparse attention of one 32K layer (events, no profiler),
 with and without the math (dp_debug_set(0, 1)): separates streaming from
-compute.  python tools/attn_probe.py"""
+compute.  python tools/attn_probe.py
+(The phase-skip switches exist only in a knob build:
+    DP_EXTRA_FLAGS=-DDP_AB_KNOBS python -m paper_2602_05191_b200.build --force)"""
 import math
 import os
 import sys

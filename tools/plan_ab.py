@@ -1,6 +1,8 @@
 """A/B timing of the plan kernel's parts (dp_debug_set(10, bits): 2 skips the
 selection, 4 the work lists) in a CUDA graph of back-to-back plan launches:
-    python tools/plan_ab.py [context] [G]"""
+    python tools/plan_ab.py [context] [G]
+(The phase-skip switches exist only in a knob build:
+    DP_EXTRA_FLAGS=-DDP_AB_KNOBS python -m paper_2602_05191_b200.build --force)"""
 import math
 import os
 import sys

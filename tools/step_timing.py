@@ -1,6 +1,8 @@
 """Per-kernel in-graph timing of the decode step (profiling aid).
 
     python tools/step_timing.py [context] [layers] [G]
+(The phase-skip switches exist only in a knob build:
+    DP_EXTRA_FLAGS=-DDP_AB_KNOBS python -m paper_2602_05191_b200.build --force)
 
 Builds `layers` synthetic layers, then times CUDA graphs of: the plan alone
 (one layer repeated / layers cycled), the attention alone (cycled), the full
