@@ -353,20 +353,28 @@ __global__ void __launch_bounds__(kAttnThreads) attn_chunk_kernel(dp_cache_view 
   const T* Kg = reinterpret_cast<const T*>(v.keys) + head_off;
   const T* Vg = reinterpret_cast<const T*>(v.values) + head_off;
   const int ch = d * (int)sizeof(T) / 16;
+  // K rows in one cp.async group, V rows in a second: the logits and the
+  // softmax below run while the V group is still in flight
   for (int i = tid; i < kChunkRows * ch; i += nt) {
     const int r = i / ch, cc = i - r * ch;
     const int phys = rphys[r];
     unsigned char* kd = ks + r * rowb + cc * 16;
-    unsigned char* vd = vs + r * rowb + cc * 16;
-    if (phys >= 0) {
+    if (phys >= 0)
       cp_async16<T>(kd, reinterpret_cast<const unsigned char*>(Kg + (size_t)phys * d) + cc * 16);
-      cp_async16<T>(vd, reinterpret_cast<const unsigned char*>(Vg + (size_t)phys * d) + cc * 16);
-    } else {
+    else
       *reinterpret_cast<int4*>(kd) = make_int4(0, 0, 0, 0);
-      *reinterpret_cast<int4*>(vd) = make_int4(0, 0, 0, 0);
-    }
   }
-  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+  for (int i = tid; i < kChunkRows * ch; i += nt) {
+    const int r = i / ch, cc = i - r * ch;
+    const int phys = rphys[r];
+    unsigned char* vd = vs + r * rowb + cc * 16;
+    if (phys >= 0)
+      cp_async16<T>(vd, reinterpret_cast<const unsigned char*>(Vg + (size_t)phys * d) + cc * 16);
+    else
+      *reinterpret_cast<int4*>(vd) = make_int4(0, 0, 0, 0);
+  }
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 1;\n" ::: "memory");  // K landed
   __syncthreads();
 
   // logits: thread per (head, row); lanes share the head -> q broadcast
@@ -409,6 +417,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_chunk_kernel(dp_cache_view 
       pt.l[pi] = l;
     }
   }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");  // V landed
   __syncthreads();
   for (int i = tid; i < G * d; i += nt) {
     const int g = i / d, j = i - g * d;

@@ -10,7 +10,7 @@
 namespace dp {
 
 constexpr int kChunkRows = 128;   // rows per split-KV work item
-constexpr int kAttnThreads = 256;
+constexpr int kAttnThreads = 512;  // one (head, row) logit / (head, dim) output per thread at G = 4
 constexpr int kMaxPartSlots = 256;  // persistent attention grid cap (partials per head)
 
 // Row stride of the sparse accumulators: o[d], l, 3 pad floats (16-B aligned rows
