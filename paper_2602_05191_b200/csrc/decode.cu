@@ -326,9 +326,11 @@ __global__ void __launch_bounds__(kAttnThreads) attn_chunk_kernel(dp_cache_view 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Acc* qs = reinterpret_cast<Acc*>(smem_raw);
   Acc* sc = qs + G * d;                                   // [G][R]
+  // ONE row buffer: K, then (once the logits are taken) V -- half the shared memory, so two or
+  // three CTAs share an SM and one's loads overlap another's arithmetic
   unsigned char* ks = reinterpret_cast<unsigned char*>(sc + G * kChunkRows);
-  unsigned char* vs = ks + kChunkRows * rowb;
-  int* rphys = reinterpret_cast<int*>(vs + kChunkRows * rowb);
+  unsigned char* vs = ks;
+  int* rphys = reinterpret_cast<int*>(ks + kChunkRows * rowb);
   int* rmask = rphys + kChunkRows;
 
   for (int i = tid; i < G * d; i += nt) qs[i] = (Acc)load_elem_d(q, qdt, (size_t)bh * G * d + i);
@@ -353,29 +355,20 @@ __global__ void __launch_bounds__(kAttnThreads) attn_chunk_kernel(dp_cache_view 
   const T* Kg = reinterpret_cast<const T*>(v.keys) + head_off;
   const T* Vg = reinterpret_cast<const T*>(v.values) + head_off;
   const int ch = d * (int)sizeof(T) / 16;
-  // K rows in one cp.async group, V rows in a second: the logits and the
-  // softmax below run while the V group is still in flight
-  for (int i = tid; i < kChunkRows * ch; i += nt) {
-    const int r = i / ch, cc = i - r * ch;
-    const int phys = rphys[r];
-    unsigned char* kd = ks + r * rowb + cc * 16;
-    if (phys >= 0)
-      cp_async16<T>(kd, reinterpret_cast<const unsigned char*>(Kg + (size_t)phys * d) + cc * 16);
-    else
-      *reinterpret_cast<int4*>(kd) = make_int4(0, 0, 0, 0);
-  }
-  asm volatile("cp.async.commit_group;\n" ::: "memory");
-  for (int i = tid; i < kChunkRows * ch; i += nt) {
-    const int r = i / ch, cc = i - r * ch;
-    const int phys = rphys[r];
-    unsigned char* vd = vs + r * rowb + cc * 16;
-    if (phys >= 0)
-      cp_async16<T>(vd, reinterpret_cast<const unsigned char*>(Vg + (size_t)phys * d) + cc * 16);
-    else
-      *reinterpret_cast<int4*>(vd) = make_int4(0, 0, 0, 0);
-  }
-  asm volatile("cp.async.commit_group;\ncp.async.wait_group 1;\n" ::: "memory");  // K landed
-  __syncthreads();
+  auto load_rows = [&](const T* G0, unsigned char* dst) {
+    for (int i = tid; i < kChunkRows * ch; i += nt) {
+      const int r = i / ch, cc = i - r * ch;
+      const int phys = rphys[r];
+      unsigned char* kd = dst + r * rowb + cc * 16;
+      if (phys >= 0)
+        cp_async16<T>(kd, reinterpret_cast<const unsigned char*>(G0 + (size_t)phys * d) + cc * 16);
+      else
+        *reinterpret_cast<int4*>(kd) = make_int4(0, 0, 0, 0);
+    }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();
+  };
+  load_rows(Kg, ks);
 
   // logits: thread per (head, row); lanes share the head -> q broadcast
   const Acc sc_scale = (Acc)scale;
@@ -417,8 +410,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_chunk_kernel(dp_cache_view 
       pt.l[pi] = l;
     }
   }
-  asm volatile("cp.async.wait_group 0;\n" ::: "memory");  // V landed
-  __syncthreads();
+  load_rows(Vg, vs);  // (the softmax barrier above: every logit read of K is done)
   for (int i = tid; i < G * d; i += nt) {
     const int g = i / d, j = i - g * d;
     const Acc* pg = sc + g * kChunkRows;
@@ -532,7 +524,7 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(dp_cache_view v, i
 // ---------------------------------------------------------------------------
 size_t attn_smem_bytes(int d, int G, int elem, int acc) {
   const int rowb = d * elem + 16;
-  return (size_t)acc * (G * d + G * kChunkRows) + 2 * (size_t)kChunkRows * rowb + 2 * kChunkRows * 4;
+  return (size_t)acc * (G * d + G * kChunkRows) + (size_t)kChunkRows * rowb + 2 * kChunkRows * 4;
 }
 
 int select_padded(int K) {
