@@ -294,3 +294,40 @@ def test_select_global_paths_identical(K):
             assert torch.equal(st[r, :kk], ref_st[r, :kk]), (path, p1, p2, r)
             assert int(cnt[r, 0]) == int((st[r, :kk] >= 1).sum()) and int(cnt[r, 1]) == int((st[r, :kk] == 2).sum())
         assert torch.equal(cnt, ref_cnt), (path, p1, p2)
+
+
+@pytest.mark.parametrize("P,part_len", [(2, 700), (8, 4096), (5, 3000)])
+def test_select_global_parts_in_place(P, part_len):
+    """dp_select_global_parts reads the all-gathered [P, rows, part_len]
+    slices in place (holes at -inf, as dp_plan_score leaves them): the same
+    states and counts as dp_select_global on the flattened global table."""
+    from paper_2602_05191_b200 import _native as N
+
+    rng = np.random.default_rng(P * 1000 + part_len)
+    R = 6
+    parts = rng.normal(0.0, 1.0, (P, R, part_len)) + np.log(rng.integers(1, 80, (P, R, part_len)))
+    parts[:, :, rng.integers(0, part_len, 40)] += 9.0
+    for p in range(P):  # ragged slices: each rank holds fewer clusters than the slot count
+        n_p = int(rng.integers(part_len // 2, part_len + 1))
+        parts[p, :, n_p:] = -np.inf
+    parts[:, 3] = np.round(parts[:, 3] * 2) / 2  # exact ties across slices
+    flat = np.ascontiguousarray(parts.transpose(1, 0, 2).reshape(R, P * part_len))
+    lib = N.lib()
+    s = torch.cuda.current_stream().cuda_stream
+    K = P * part_len
+    t_parts = torch.from_numpy(np.ascontiguousarray(parts)).cuda()
+    t_flat = torch.from_numpy(flat).cuda()
+    ks = torch.full((R,), K, dtype=torch.int32, device="cuda")
+    ws = torch.empty((lib.dp_select_global_workspace_bytes(R, K),), dtype=torch.uint8, device="cuda")
+    for p1, p2 in ((0.95, 0.7), (0.6, 0.9), (1.0, 0.5)):
+        st_a = torch.zeros((R, K), dtype=torch.uint8, device="cuda")
+        st_b = torch.zeros((R, K), dtype=torch.uint8, device="cuda")
+        c_a = torch.zeros((R, 2), dtype=torch.int32, device="cuda")
+        c_b = torch.zeros((R, 2), dtype=torch.int32, device="cuda")
+        N.check(lib.dp_select_global(N.ptr(t_flat), R, K, N.ptr(ks), p1, p2, N.ptr(st_a), N.ptr(c_a), N.ptr(ws),
+                                     ws.numel(), s))
+        N.check(lib.dp_select_global_parts(N.ptr(t_parts), R, P, part_len, N.ptr(ks), p1, p2, N.ptr(st_b),
+                                           N.ptr(c_b), N.ptr(ws), ws.numel(), s))
+        torch.cuda.synchronize()
+        assert torch.equal(st_a, st_b), (p1, p2)
+        assert torch.equal(c_a, c_b), (p1, p2)
