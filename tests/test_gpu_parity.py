@@ -561,3 +561,58 @@ def test_nonfinite_query_other_entry_points():
     torch.cuda.synchronize()
     q2 = torch.randn((1, 8, 128), device="cuda").to(torch.bfloat16)
     assert torch.isfinite(cluster_topk_attention(q2, lay, 5)).all()
+
+
+@pytest.mark.parametrize("n,dtype", [(32768, torch.bfloat16), (8192, torch.float32), (131072, torch.bfloat16)])
+def test_plan_split_equals_fused_plan(n, dtype):
+    """dp_plan_score + dp_plan_given (config 5's split around an outside
+    selection) fed the fused plan's OWN states reproduce the fused plan:
+    identical log-masses and states, the same attention output."""
+    from paper_2602_05191_b200 import _native as N
+    from paper_2602_05191_b200 import cluster_layer
+    from paper_2602_05191_b200.cache import dtype_code
+    from paper_2602_05191_b200.workload import generate_layer, generate_queries
+
+    H, G = (8, 4) if n <= 32768 else (2, 4)
+    k, v, c = generate_layer(1, H, n, 128)
+    lay = cluster_layer(k.to(dtype), v.to(dtype), fp64_assign=False)
+    q = torch.from_numpy(generate_queries(c, G, 1)[0]).cuda().to(torch.bfloat16).contiguous()
+    lib = N.lib()
+    s = torch.cuda.current_stream().cuda_stream
+    view = lay.view()
+    cap = lay.cluster_cap
+    wsb = lib.dp_decode_workspace_bytes(view, G)
+
+    def run(split):
+        lm = torch.full((1, H * G, cap), 7.0, dtype=torch.float64, device="cuda")
+        st = torch.zeros((1, H * G, cap), dtype=torch.uint8, device="cuda")
+        cnt = torch.zeros((1, H * G, 2), dtype=torch.int32, device="cuda")
+        out = torch.zeros((1, H * G, 128), dtype=torch.float32, device="cuda")
+        lse = torch.zeros((1, H * G), dtype=torch.float32, device="cuda")
+        ws = torch.zeros((wsb,), dtype=torch.uint8, device="cuda")
+        if split:
+            N.check(lib.dp_plan_score(view, N.ptr(q), dtype_code(q), G, lay.attn_scale, N.ptr(lm), N.ptr(ws), wsb, s))
+            st.copy_(ref_state)
+            N.check(lib.dp_plan_given(view, N.ptr(q), dtype_code(q), G, lay.attn_scale, N.ptr(lm), N.ptr(st), 0, None,
+                                      N.ptr(ws), wsb, s))
+        else:
+            N.check(lib.dp_plan(view, N.ptr(q), dtype_code(q), G, lay.attn_scale, 0.95, 0.7, N.ptr(lm), N.ptr(st),
+                                N.ptr(cnt), None, N.ptr(ws), wsb, s))
+        N.check(lib.dp_attend(view, N.ptr(q), dtype_code(q), G, lay.attn_scale, N.ptr(lm), N.ptr(out), N.ptr(lse),
+                              N.ptr(ws), wsb, s))
+        torch.cuda.synchronize()
+        return lm, st, out, lse
+
+    lm_a, st_a, out_a, lse_a = run(False)
+    ref_state = st_a.clone()
+    lm_b, st_b, out_b, lse_b = run(True)
+    kk = lay.nclusters.reshape(-1).repeat_interleave(G)
+    for r in range(H * G):
+        K = int(kk[r])
+        assert torch.equal(lm_a[0, r, :K], lm_b[0, r, :K]), r
+        assert torch.all(lm_b[0, r, K:] == -math.inf), r  # score-only leaves -inf past K
+    assert torch.equal(st_a, st_b)
+    # the attention's cross-CTA accumulators are float atomics (order varies run to run)
+    err = ((out_a - out_b).norm(dim=-1) / out_a.norm(dim=-1)).max().item()
+    assert err <= 1e-6, err
+    assert torch.allclose(lse_a, lse_b, rtol=0, atol=1e-5)
