@@ -200,12 +200,12 @@ __global__ void __launch_bounds__(kPT, 1)
   const int qP = d + 4;  // padded fp64 query rows: conflict-free B-fragment loads
   const unsigned bar0 = (unsigned)__cvta_generic_to_shared(&s_tbar[0]);
   // given states: the log-masses are already written (dp_plan_score) -- no scoring pass
-  const int ntile = kMode == kModeGiven ? 0 : (nloc + kCh - 1) / kCh;
+  const int ntile = kMode == kModeGiven || DP_AB(dbg, 8192) ? 0 : (nloc + kCh - 1) / kCh;
   const int ncb = d / 32;  // 128-B column blocks per row
   if (tid == 0) {
     // bytes each hand-off barrier of this CTA receives
     // (given states: no scores travel, only the slice maxima)
-    if (r < G) mb_expect(&s_mb[0], (unsigned)((kMode == kModeGiven ? 0 : K * 8) + CL * 16));
+    if (r < G) mb_expect(&s_mb[0], (unsigned)((kMode == kModeGiven || DP_AB(dbg, 512) ? 0 : K * 8) + CL * 16));
     unsigned eb = (unsigned)(G * 4 * ((nloc + 3) / 4));
     if (r == 0) eb += (unsigned)(G * 8 + (CL > G ? (CL - G) * G * 8 : 0));
     mb_expect(&s_mb[1], eb);
@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(kPT, 1)
 #pragma unroll 1
   for (int t = 0; t < ntile; ++t) {
     const int row0 = t * kCh;
-    {
+    if (!(DP_AB(dbg, 1024) && t >= 2)) {
       const unsigned b = bar0 + (unsigned)(t & 1) * 8;
       unsigned done = 0;
       while (!done)
@@ -325,6 +325,8 @@ __global__ void __launch_bounds__(kPT, 1)
             : "r"(b), "r"((unsigned)((t >> 1) & 1))
             : "memory");
     }
+    if (t < 2) stamp(r, t == 0 ? 14 : 21);  // tile arrived (profiling builds)
+    if (t == 3) stamp(r, 23);
     const unsigned char* tileC = reinterpret_cast<const unsigned char*>(Cs) + (size_t)(t & 1) * kTileBytes;
     const int nrb = (min(kCh, nloc - row0) + 7) >> 3;
 #pragma unroll 1
@@ -341,16 +343,21 @@ __global__ void __launch_bounds__(kPT, 1)
 #pragma unroll
         for (int tt = 0; tt < 4; ++tt) {
           const int kq = kk + tt;
-          const double a =
-              (double)*reinterpret_cast<const float*>(arow + (size_t)(kq >> 3) * kCh * 128 + (((kq & 7) ^ sw) << 4));
+          const float af = DP_AB(dbg, 32768) ? (float)(kq + ia)
+                                             : *reinterpret_cast<const float*>(arow + (size_t)(kq >> 3) * kCh * 128 + (((kq & 7) ^ sw) << 4));
+          const double a = DP_AB(dbg, 2048) ? __longlong_as_double((long long)__float_as_uint(af) << 29) : (double)af;
+          if DP_AB(dbg, 256) {  // timing experiment: no MMA (the A loads stay)
+            c[tt][0] += a;
+          } else {
           asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                        : "+d"(c[tt][0]), "+d"(c[tt][1])
                        : "d"(a), "d"(qrow[kq * 4]));
+          }
         }
       }
       const int row = row0 + ia;
       if (row < nloc) {
-        const double ls = log((double)(offs[row + 1] - offs[row]));
+        const double ls = DP_AB(dbg, 4096) ? (double)(offs[row + 1] - offs[row]) : log((double)(offs[row + 1] - offs[row]));
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int h = 2 * (lane & 3) + e;
@@ -359,14 +366,15 @@ __global__ void __launch_bounds__(kPT, 1)
             // a non-finite query must not break the selection's ordering: NaN
             // ranks last (-inf), +inf first (the largest finite double)
             val = val != val ? -CUDART_INF : fmin(val, 1.7976931348623157e308);
-            push_f64(lmall + k0 + row, h, val, &s_mb[0]);
-            if (lm_out) lm_out[((size_t)bh * G + h) * cap + k0 + row] = val;  // (read by the attention kernel)
+            if (!DP_AB(dbg, 512)) push_f64(lmall + k0 + row, h, val, &s_mb[0]);
+            if (lm_out && !DP_AB(dbg, 16384)) lm_out[((size_t)bh * G + h) * cap + k0 + row] = val;  // (read by the attention kernel)
             lmax[e] = fmax(lmax[e], val);
           }
         }
       }
     }
-    if (t + 2 < ntile) {  // refill this buffer once every warp is done with it
+    if (t < 2) stamp(r, t == 0 ? 11 : 12);  // tile computed (warp 0)
+    if (t + 2 < ntile && !DP_AB(dbg, 1024)) {  // refill this buffer once every warp is done with it
       __syncthreads();
       if (tid == 0) {
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -818,8 +826,12 @@ static int pick_cl(const dp_cache_view& v, int G) {
   const int kG = group_bound(G);
   // 8 when every cluster fits in one wave: wider clusters shorten the slices
   // but leave fewer SMs for the attention CTAs that become resident during
-  // the plan (measured: 8 vs 10 at 32K 25.6 vs 25.8 us per plan + attend,
-  // equal at 128K); wider only when 8 does not fit the table
+  // the plan (measured: 8 vs 10 at 32K 25.6 vs 25.8 us per plan + attend; at
+  // 128K: 10 is 0.6 us per plan + attend faster, tools/plan_ab.py r2o); wider
+  // only when the narrowest does not fit the table
+  if (v.cluster_cap > 2048 && cl_fits(v, G, 10) &&
+      max_active_clusters(kG, 10, plan_smem_bytes(v.head_dim, v.cluster_cap, 10, kG)) >= units)
+    return 10;
   for (int cl = 8; cl <= kMaxCL; ++cl)
     if (cl_fits(v, G, cl) &&
         max_active_clusters(kG, cl, plan_smem_bytes(v.head_dim, v.cluster_cap, cl, kG)) >= units)

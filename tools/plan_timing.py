@@ -22,6 +22,8 @@ k, v, c = generate_layer(1, 8, n, 128)
 lay = cluster_layer(k, v)
 q = torch.from_numpy(generate_queries(c, G, 1)[0]).cuda().to(torch.bfloat16)
 ws = DecodeWorkspace(lay, G)
+if os.environ.get('PLAN_DBG'):
+    N.lib().dp_debug_set(10, int(os.environ['PLAN_DBG']))  # knob builds: A/B switches
 lib = N.lib()
 view = lay.view()
 warm()
@@ -33,11 +35,11 @@ for it in range(3):
 torch.cuda.synchronize()
 buf = (ctypes.c_ulonglong * 384)()
 lib.dp_debug_plan_timing(ctypes.cast(buf, ctypes.c_void_p))
-t = np.array(buf[:], dtype=np.float64).reshape(16, 24)[:, [0, 1, 2, 10, 3, 4, 20, 21, 22, 23, 11, 12, 13, 5, 6, 15, 7, 8, 16, 17, 18, 19, 9]]
+t = np.array(buf[:], dtype=np.float64).reshape(16, 24)[:, [0, 1, 2, 14, 11, 21, 12, 23, 10, 3, 4, 20, 5, 6, 15, 7, 8, 16, 17, 18, 19, 9]]
 nr = 16 if t[8:, 0].min() > 0 else 8
 t = t[:nr]
 t0 = t[:, 0].min()
-names = ["start", "loads", "S", "score", "P1", "A", "hist0", "hist", "scan", "b1", "cmpct", "rank", "cut1", "P2", "B", "cnts", "P3", "C", "offs", "lmst", "scan4", "rows", "P4"]
+names = ["start", "loads", "S", "t0in", "t0done", "t1in", "t1done", "t3in", "score", "P1", "A", "selin", "P2", "B", "cnts", "P3", "C", "offs", "lmst", "scan4", "rows", "P4"]
 print("ncand (stats unavailable); see counts")
 print("rank " + " ".join(f"{x:>6s}" for x in names))
 for r in range(nr):
@@ -46,6 +48,6 @@ cbuf = (ctypes.c_ulonglong * 32)()
 lib.dp_debug_plan_clock(ctypes.cast(cbuf, ctypes.c_void_p))
 cl = np.array(cbuf[:], dtype=np.float64).reshape(16, 2)
 tt = np.array(buf[:], dtype=np.float64).reshape(16, 24)
-print("SM clock inside the kernel (MHz):", [round((cl[r, 1] - cl[r, 0]) / (tt[r, 9] - tt[r, 0]) * 1e3) for r in range(nr)])
+print("SM clock inside the kernel (MHz):", [float((cl[r, 1] - cl[r, 0]) / (tt[r, 9] - tt[r, 0]) * 1e3) for r in range(nr)])
 print("counts", ws.counts[0, :G].tolist(), "stats", ws.stats[0, 0].tolist())
 
