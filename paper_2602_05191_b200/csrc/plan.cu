@@ -83,7 +83,7 @@ struct PlanLayout {
   size_t cs;               // P1: [per][d + 4] fp32 centroid slice | P2 (owners): select arrays | P3 scratch
   size_t um, bin, hm, hc, clist, cord, stown;  // P2 arrays (inside the cs region; bin = cursors, cord unused)
   size_t lmall;            // [cap] fp64 log-masses of my head (owners; pushed by every CTA)
-  size_t lml;              // [kG][per] fp64 log-masses of my slice
+  size_t lml;              // [per] fp64 log cluster sizes of my slice (sized kG * per)
   size_t qd;               // [8][d + 4] fp64 queries (padded rows)
   size_t stl;              // [kG][per] u8 states of my slice (pushed by the owners)
   size_t offs;             // [per + 1] int row offsets of my slice
@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(kPT, 1)
   unsigned char* smem = smem_raw + ((1024u - ((unsigned)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u);
   float* Cs = reinterpret_cast<float*>(smem + L.cs);
   double* lmall = reinterpret_cast<double*>(smem + L.lmall);
-  double* lml = reinterpret_cast<double*>(smem + L.lml);
+  double* lsz = reinterpret_cast<double*>(smem + L.lml);  // [nloc] log cluster sizes of my slice
   double* qd = reinterpret_cast<double*>(smem + L.qd);
   uint8_t* stl = reinterpret_cast<uint8_t*>(smem + L.stl);
   int* offs = reinterpret_cast<int*>(smem + L.offs);
@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(kPT, 1)
   // S[row, head] = sum_k C[row, k] q[head, k] on the fp64 tensor pipe:
   // mma.m8n8k4.f64 with M = 8 centroid rows, N = 8 heads (G <= 8, the rest
   // zero), K = 4 dims; fp32 centroids and queries are exact in fp64.
-  const int qP = d + 4;  // padded fp64 query rows: conflict-free B-fragment loads
+  const int qP = d + 2;  // padded fp64 query rows: a row is 16 B past a 128-B multiple -> conflict-free 16-B B-fragment loads
   const unsigned bar0 = (unsigned)__cvta_generic_to_shared(&s_tbar[0]);
   // given states: the log-masses are already written (dp_plan_score) -- no scoring pass
   const int ntile = kMode == kModeGiven || DP_AB(dbg, 8192) ? 0 : (nloc + kCh - 1) / kCh;
@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(kPT, 1)
   if (tid == 0) {
     // bytes each hand-off barrier of this CTA receives
     // (given states: no scores travel, only the slice maxima)
-    if (r < G) mb_expect(&s_mb[0], (unsigned)((kMode == kModeGiven || DP_AB(dbg, 512) ? 0 : K * 8) + CL * 16));
+    if (r < G) mb_expect(&s_mb[0], (unsigned)((kMode == kModeGiven ? 0 : K * 8) + CL * 16));
     unsigned eb = (unsigned)(G * 4 * ((nloc + 3) / 4));
     if (r == 0) eb += (unsigned)(G * 8 + (CL > G ? (CL - G) * G * 8 : 0));
     mb_expect(&s_mb[1], eb);
@@ -246,6 +246,10 @@ __global__ void __launch_bounds__(kPT, 1)
     const int* goffs = v.offs + (size_t)bh * (cap + 1) + k0;
 #pragma unroll 1
     for (int i = tid; i <= nloc; i += kPT) offs[i] = __ldg(&goffs[i]);
+    // log cluster sizes of the slice (engine.py:165, the size weight): layer-static, so
+    // they are taken here, overlapping the previous grid, not in P1's epilogue
+#pragma unroll 1
+    for (int i = tid; i < nloc; i += kPT) lsz[i] = log((double)(__ldg(&goffs[i + 1]) - __ldg(&goffs[i])));
     asm volatile("griddepcontrol.wait;\n" ::: "memory");  // PDL: inputs of the previous grid are visible
     // let the attention grid become resident on the SMs this launch leaves free
     // (its CTAs wait for our completion before reading anything we write)
@@ -302,7 +306,18 @@ __global__ void __launch_bounds__(kPT, 1)
   cl_wait();  // (S)
   stamp(r, 2);
   double lmax[2] = {-CUDART_INF, -CUDART_INF};  // heads 2(l%4), 2(l%4)+1
-  const double* qrow = qd + (lane >> 2) * qP + (lane & 3);  // B fragment: q[head l/4][4 kk + l%4]
+  // B fragment (m8n8k4 .col): lane holds q[head l/4][dim]; MMA step 4m + u takes dims
+  // 16m + 4(l%4) + u, so a lane's A and B operands of four steps are one 16-B
+  // (A: 4 fp32) / two 16-B (B: 4 fp64) shared loads
+  const double* qrow = qd + (lane >> 2) * qP + 4 * (lane & 3);
+  // DSMEM targets of my two heads' scores (owners h = 2(l%4) + e), mapped once
+  unsigned lm_cl[2] = {0u, 0u}, mb_cl[2] = {0u, 0u};
+#pragma unroll
+  for (int e = 0; e < 2; ++e)
+    if (2 * (lane & 3) + e < G) {
+      lm_cl[e] = cl_map(lmall + k0, 2 * (lane & 3) + e);
+      mb_cl[e] = cl_map(&s_mb[0], 2 * (lane & 3) + e);
+    }
   if (kMode == kModeGiven) {  // my slice's maxima from the written log-masses (same lane -> head map as below)
 #pragma unroll 1
     for (int row = tid >> 2; row < nloc; row += kPT / 4)
@@ -315,7 +330,7 @@ __global__ void __launch_bounds__(kPT, 1)
 #pragma unroll 1
   for (int t = 0; t < ntile; ++t) {
     const int row0 = t * kCh;
-    if (!(DP_AB(dbg, 1024) && t >= 2)) {
+    {
       const unsigned b = bar0 + (unsigned)(t & 1) * 8;
       unsigned done = 0;
       while (!done)
@@ -331,33 +346,34 @@ __global__ void __launch_bounds__(kPT, 1)
     const int nrb = (min(kCh, nloc - row0) + 7) >> 3;
 #pragma unroll 1
     for (int rb = warp; rb < nrb; rb += kPW) {
-      // row i = rb*8 + lane/4, dim = 4 kk + lane%4: column block kk/8, 16-B
-      // chunk kk%8 stored at chunk (kk%8) ^ (i%8) (128B swizzle) -> 32 banks
-      const int ia = rb * 8 + (lane >> 2);
-      const unsigned char* arow = tileC + (size_t)ia * 128 + (lane & 3) * 4;
+      // MMA row l/4 is tile row ia = rb*8 + perm(l/4), perm = 0,4,1,5,2,6,3,7: the two
+      // rows of a quarter-warp then differ in bit 2, so their 128B-swizzled 16-B
+      // chunks (logical chunk ^ (row % 8)) fall in disjoint bank groups
+      const int mr = lane >> 2;
+      const int ia = rb * 8 + (((mr & 1) << 2) | (mr >> 1));
+      const unsigned char* arow = tileC + (size_t)ia * 128;
       const int sw = ia & 7;
+      if (t == 0 && rb == 0) stamp(r, 22);  // (profiling builds) tile 0, warp 0: row block start
       double c[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
-      for (int kk = 0; kk < 32; kk += 4) {
-        if (kk * 4 >= d) break;
+      for (int m = 0; m < 8; ++m) {
+        if (m * 16 >= d) break;
+        const int lc = 4 * m + (lane & 3);  // logical 16-B chunk of the row: column block lc / 8
+        const float4 a4 = *reinterpret_cast<const float4*>(arow + (size_t)(lc >> 3) * kCh * 128 + (((lc & 7) ^ sw) << 4));
+        const double2 b01 = *reinterpret_cast<const double2*>(qrow + 16 * m);
+        const double2 b23 = *reinterpret_cast<const double2*>(qrow + 16 * m + 2);
+        const double av[4] = {(double)a4.x, (double)a4.y, (double)a4.z, (double)a4.w};
+        const double bv[4] = {b01.x, b01.y, b23.x, b23.y};
 #pragma unroll
-        for (int tt = 0; tt < 4; ++tt) {
-          const int kq = kk + tt;
-          const float af = DP_AB(dbg, 32768) ? (float)(kq + ia)
-                                             : *reinterpret_cast<const float*>(arow + (size_t)(kq >> 3) * kCh * 128 + (((kq & 7) ^ sw) << 4));
-          const double a = DP_AB(dbg, 2048) ? __longlong_as_double((long long)__float_as_uint(af) << 29) : (double)af;
-          if DP_AB(dbg, 256) {  // timing experiment: no MMA (the A loads stay)
-            c[tt][0] += a;
-          } else {
+        for (int u = 0; u < 4; ++u)
           asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-                       : "+d"(c[tt][0]), "+d"(c[tt][1])
-                       : "d"(a), "d"(qrow[kq * 4]));
-          }
-        }
+                       : "+d"(c[u][0]), "+d"(c[u][1])
+                       : "d"(av[u]), "d"(bv[u]));
       }
+      if (t == 0 && rb == 0) stamp(r, 13);  // (profiling builds) tile 0, warp 0: MMA loop done
       const int row = row0 + ia;
       if (row < nloc) {
-        const double ls = DP_AB(dbg, 4096) ? (double)(offs[row + 1] - offs[row]) : log((double)(offs[row + 1] - offs[row]));
+        const double ls = lsz[row];
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int h = 2 * (lane & 3) + e;
@@ -366,15 +382,18 @@ __global__ void __launch_bounds__(kPT, 1)
             // a non-finite query must not break the selection's ordering: NaN
             // ranks last (-inf), +inf first (the largest finite double)
             val = val != val ? -CUDART_INF : fmin(val, 1.7976931348623157e308);
-            if (!DP_AB(dbg, 512)) push_f64(lmall + k0 + row, h, val, &s_mb[0]);
-            if (lm_out && !DP_AB(dbg, 16384)) lm_out[((size_t)bh * G + h) * cap + k0 + row] = val;  // (read by the attention kernel)
+            asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];\n" ::"r"(
+                             lm_cl[e] + (unsigned)row * 8u),
+                         "l"(__double_as_longlong(val)), "r"(mb_cl[e])
+                         : "memory");
+            if (lm_out) lm_out[((size_t)bh * G + h) * cap + k0 + row] = val;  // (read by the attention kernel)
             lmax[e] = fmax(lmax[e], val);
           }
         }
       }
     }
     if (t < 2) stamp(r, t == 0 ? 11 : 12);  // tile computed (warp 0)
-    if (t + 2 < ntile && !DP_AB(dbg, 1024)) {  // refill this buffer once every warp is done with it
+    if (t + 2 < ntile) {  // refill this buffer once every warp is done with it
       __syncthreads();
       if (tid == 0) {
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");

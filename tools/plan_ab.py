@@ -63,11 +63,7 @@ attend()
 torch.cuda.synchronize()
 print(f"context {n} G {G}: plan cluster size {lib.dp_debug_plan_occupancy(view, G, 0)}; us per launch in graph")
 for bits, name in ((0, "full plan"), (32, "no centroid L2 prefetch"), (8, "no row expansion"), (4, "no work lists"), (2, "no selection"),
-                   (6, "no selection, no lists"), (6 | 256, "  + no score MMA"), (6 | 512, "  + no score pushes"),
-                   (6 | 1024, "  + no tile refills"), (6 | 256 | 512 | 1024, "  + none of the three"),
-                   (6 | 256 | 512 | 1024 | 2048, "  + no f32->f64 cvt"), (6 | 256 | 512 | 1024 | 4096, "  + no log"),
-                   (6 | 256 | 512 | 1024 | 2048 | 4096, "  + neither"), (6 | 512 | 8192, "  no scoring at all"),
-                   (7942 | 16384, "  + no lm_out stores"), (7942 | 32768, "  + no A loads"), (7942 | 16384 | 32768, "  + no stores, no A loads"), (128, "launch + wait + q load only"), (64, "launch + wait only")):
+                   (6, "no selection, no lists"), (128, "launch + wait + q load only"), (64, "launch + wait only")):
     lib.dp_debug_set(10, bits)
     print(f"  {name:28s} {timed(lambda: [plan() for _ in range(L)]):7.2f}")
 lib.dp_debug_set(10, 0)
