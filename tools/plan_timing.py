@@ -35,11 +35,11 @@ for it in range(3):
 torch.cuda.synchronize()
 buf = (ctypes.c_ulonglong * 384)()
 lib.dp_debug_plan_timing(ctypes.cast(buf, ctypes.c_void_p))
-t = np.array(buf[:], dtype=np.float64).reshape(16, 24)[:, [0, 1, 2, 14, 11, 21, 12, 23, 10, 3, 4, 20, 5, 6, 15, 7, 8, 16, 17, 18, 19, 9]]
+t = np.array(buf[:], dtype=np.float64).reshape(16, 24)[:, [0, 1, 2, 14, 22, 13, 11, 21, 12, 23, 10, 3, 4, 20, 5, 6, 15, 7, 8, 16, 17, 18, 19, 9]]
 nr = 16 if t[8:, 0].min() > 0 else 8
 t = t[:nr]
 t0 = t[:, 0].min()
-names = ["start", "loads", "S", "t0in", "t0done", "t1in", "t1done", "t3in", "score", "P1", "A", "selin", "P2", "B", "cnts", "P3", "C", "offs", "lmst", "scan4", "rows", "P4"]
+names = ["start", "loads", "S", "t0in", "rb0", "mma0", "t0done", "t1in", "t1done", "t3in", "score", "P1", "A", "selin", "P2", "B", "cnts", "P3", "C", "offs", "lmst", "scan4", "rows", "P4"]
 print("ncand (stats unavailable); see counts")
 print("rank " + " ".join(f"{x:>6s}" for x in names))
 for r in range(nr):
