@@ -144,6 +144,10 @@ for sg in (1, 2):
     if sel.any():
         print(f"  CTAs with {sg} head segment(s): n={int(sel.sum())} rows med {np.median(rows[sel]):.0f} "
               f"loop(data0->done) med {np.median(loop_end[sel]):.2f} max {loop_end[sel].max():.2f} us")
+if os.environ.get("ATTN_PER_CTA"):  # every CTA: id, segments, rows, data0, loop done (cumulative rows -> head)
+    cum = np.cumsum(rows)
+    for c in range(rows.size):
+        print(f"    cta {c:3d} seg {int(segs[c])} rows {int(rows[c]):5d} cum {int(cum[c]):7d} data0 {rel[c, 2]:7.2f} done {rel[c, 3]:7.2f} loop {rel[c, 3] - rel[c, 2]:6.2f}")
 slow = np.argsort(-rel[:, 3])[:6]
 print("  slowest CTAs (id, segments, rows, data0, loop done):",
       [(int(c), int(segs[c]), int(rows[c]), round(rel[c, 2], 2), round(rel[c, 3], 2)) for c in slow])
