@@ -605,27 +605,31 @@ __device__ void select_fast(const int K, const double M, const double* lmall, co
     S->wm[warp] = mi;
     S->wc[warp] = ci;
   }
-  __syncthreads();  // (every histogram read is done: the prefixes below overwrite it in place)
+  __syncthreads();  // warp totals in place (and every histogram read is done: the prefixes below overwrite it in place)
   SELP(2, S);
   sel_sub(2);
-  if (tid <= kW) {  // thread w: exclusive prefix of the warp totals (independent loads, no shuffles)
-    unsigned long long e = 0ull;
-    int ec = 0;
+  // every warp scans the kW warp totals itself (one load per lane + shuffles):
+  // no single-warp serial prefix and no second barrier
+  static_assert(kW <= 32, "warp totals fit one warp");
+  unsigned long long wsum = lane < kW ? S->wm[lane] : 0ull;
+  int csum = lane < kW ? S->wc[lane] : 0;
 #pragma unroll
-    for (int w = 0; w < kW; ++w)
-      if (w < tid) {
-        e += S->wm[w];
-        ec += S->wc[w];
-      }
-    S->wx[tid] = e;  // wx[kW] = the total
-    S->wcx[tid] = ec;
+  for (int o = 1; o < kW; o <<= 1) {
+    const unsigned long long tm = __shfl_up_sync(0xffffffffu, wsum, o);
+    const int tc = __shfl_up_sync(0xffffffffu, csum, o);
+    if (lane >= o) {
+      wsum += tm;
+      csum += tc;
+    }
   }
-  __syncthreads();
+  const unsigned long long T = __shfl_sync(0xffffffffu, wsum, kW - 1);  // total mass
+  const int CT = __shfl_sync(0xffffffffu, csum, kW - 1);                // total count
+  const unsigned long long wex = __shfl_sync(0xffffffffu, wsum, warp > 0 ? warp - 1 : 0);
+  const int wcex = __shfl_sync(0xffffffffu, csum, warp > 0 ? warp - 1 : 0);
   sel_sub(3);
   SELP(3, S);
-  const unsigned long long T = S->wx[kW];
-  unsigned long long mex = S->wx[warp] + mi - mloc;
-  int cex = S->wcx[warp] + ci - cloc;
+  unsigned long long mex = (warp > 0 ? wex : 0ull) + mi - mloc;
+  int cex = (warp > 0 ? wcex : 0) + ci - cloc;
   const double thr1 = p1 * (double)T;
   const unsigned long long T1 = ceil_u64(thr1);
   unsigned long long pmv[kBPT];
@@ -653,7 +657,7 @@ __device__ void select_fast(const int K, const double M, const double* lmall, co
     *reinterpret_cast<int2*>(pc + tid * kBPT) = make_int2(pcv[0], pcv[1]);
     *reinterpret_cast<int2*>(cur + tid * kBPT) = make_int2(0, 0);
   }
-  if (tid == kT - 1) pc[NB] = S->wcx[kW];
+  if (tid == kT - 1) pc[NB] = CT;
   sel_sub(4);
   __syncthreads();
   SELP(4, S);
