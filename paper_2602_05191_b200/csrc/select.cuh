@@ -489,6 +489,8 @@ struct SelFastShared {
   int wc[33], wcx[33];                // (count)
   unsigned long long before1, mass1, at1;
   int b1, n1, n2, pad;
+  int ba, bb;  // stage-2 candidate bins [ba, bb]: exact below, approx above (up to b1)
+  int pad2[2];
 };
 
 // zero the histogram (hm: [2 NB] mass halves, hc: [NB + 1] counts) and the
@@ -499,6 +501,8 @@ __device__ __forceinline__ void select_fast_zero(unsigned* hm, int* hc, SelFastS
   for (int j = threadIdx.x; j <= NB; j += kT) hc[j] = 0;
   if (threadIdx.x == 0) {
     S->b1 = NB;
+    S->ba = 0;   // (kept when the stage-2 lower threshold is 0)
+    S->bb = -1;  // (kept when the upper one is 0: no candidate range)
     S->n1 = 0;
     S->n2 = 0;
     S->at1 = 0ull;
@@ -673,6 +677,19 @@ __device__ void select_fast(const int K, const double M, const double* lmall, co
   }
   // (3) candidates: b1 and the bins whose (excl, incl] meets (tlo, thi]
   const unsigned long long Tlo = ceil_u64(p2 * (double)S->before1), Thi = ceil_u64(p2 * (double)(S->before1 + S->mass1));
+  // the prefix is monotone in the bin, so the bins meeting (Tlo, Thi] are one
+  // range [ba, bb]: ba holds the Tlo crossing (first inclusive prefix >= Tlo),
+  // bb the Thi crossing (last exclusive prefix < Thi).  Found from this
+  // thread's bins (still in registers), so the element pass below compares
+  // bin indices instead of loading two prefixes per element
+#pragma unroll
+  for (int j = 0; j < kBPT; ++j) {
+    const unsigned long long ex = pmv[j], in = pmv[j] + bm[j];
+    if (ex < Tlo && Tlo <= in) S->ba = tid * kBPT + j;
+    if (ex < Thi && Thi <= in) S->bb = tid * kBPT + j;
+  }
+  __syncthreads();
+  const int ba = S->ba, bb = S->bb;
   // every non-candidate's state follows from its bin and is written now;
   // the later passes touch only this thread's candidates (bit s of cmask)
   const uint8_t zst = p1 >= 1.0 ? (p2 >= 1.0 ? 2 : 1) : 0;
@@ -686,12 +703,11 @@ __device__ void select_fast(const int K, const double M, const double* lmall, co
     if (!eu[s]) {
       st = zst;
     } else if (b <= b1) {
-      const unsigned long long inc = b + 1 < NB ? pm[b + 1] : T;
-      if (b == b1 || (inc >= Tlo && pm[b] < Thi)) {
+      if (b == b1 || (b >= ba && b <= bb)) {
         cmask |= 1u << s;
         clist[pc[b] + atomicAdd(&cur[b], 1)] = i;
       } else {
-        st = inc < Tlo ? 2 : 1;  // before the candidate range: exact; between it and b1: approx
+        st = b < ba ? 2 : 1;  // before the candidate range: exact; between it and b1: approx
       }
     }
     if (!((cmask >> s) & 1u)) stown[i] = st;
