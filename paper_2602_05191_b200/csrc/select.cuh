@@ -750,24 +750,26 @@ __device__ void select_fast(const int K, const double M, const double* lmall, co
   SELP(6, S);
   sel_stamp(4);
   // (5) the stage-2 crossing element (p2 of the retained mass, engine.py:191)
+  //     and the candidates' states in one pass: along the sorted order the
+  //     exclusive cumulative mass of an element with mass > 0 is strictly
+  //     increasing, so "position < n2" is "ex < T2" and "position < n1" is
+  //     "ex < T1" -- no barrier between finding the cuts and applying them
+  //     (the others' states were written in (3))
   const int n1 = p1 >= 1.0 ? K : S->n1;
   const unsigned long long T2 = ceil_u64(p2 * (double)S->at1);
+  const bool all2 = p1 >= 1.0 && p2 >= 1.0;
 #pragma unroll
   for (int s = 0; s < kEPT; ++s) {
-    if (((cmask >> s) & 1u) && ex[s] < T2 && T2 <= ex[s] + eu[s]) S->n2 = pos[s] + 1;
+    if ((cmask >> s) & 1u) {
+      if (ex[s] < T2 && T2 <= ex[s] + eu[s]) S->n2 = pos[s] + 1;
+      stown[tid + s * kT] = all2 || ex[s] < T2 ? 2 : (p1 >= 1.0 || ex[s] < T1 ? 1 : 0);
+    }
   }
   __syncthreads();
   SELP(7, S);
   sel_stamp(5);
-  const int n2 = p1 >= 1.0 && p2 >= 1.0 ? K : S->n2;
-  // (6) the candidates' states (the others were written in (3))
-#pragma unroll
-  for (int s = 0; s < kEPT; ++s) {
-    if ((cmask >> s) & 1u) stown[tid + s * kT] = pos[s] < n2 ? 2 : (pos[s] < n1 ? 1 : 0);
-  }
-  __syncthreads();
-  SELP(8, S);
   sel_stamp(6);
+  const int n2 = all2 ? K : S->n2;
   n1_out = n1;
   n2_out = n2;
 }
