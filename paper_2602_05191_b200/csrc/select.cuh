@@ -39,12 +39,14 @@ __device__ __forceinline__ void sel_stamp(int ev) {
 }
 
 // block-wide exclusive scan of (mass u64, count int) pairs; totals to mt / ct.
-// Warp scans, then warp 0 scans the 16 warp totals (so no thread reads all
-// of them).  sm/sc need 2 * (kT / 32) + 1 slots; callers separate consecutive uses
-// with a barrier.
+// Warp scans, one barrier, then every warp scans the kT / 32 warp totals
+// itself with shuffles (no serial warp-0 step, no second barrier).  sm/sc need
+// kT / 32 slots; callers separate consecutive uses with a barrier.
 template <int kT>
 __device__ __forceinline__ void scan_pair(unsigned long long m, int c, unsigned long long* sm, int* sc,
                                           unsigned long long& mex, int& cex, unsigned long long& mt, int& ct) {
+  constexpr int kW = kT / 32;
+  static_assert(kW <= 32, "warp totals fit one warp");
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   unsigned long long mi = m;
   int ci = c;
@@ -62,34 +64,23 @@ __device__ __forceinline__ void scan_pair(unsigned long long m, int c, unsigned 
     sc[warp] = ci;
   }
   __syncthreads();
-  if (warp == 0) {
-    const unsigned long long wv = lane < (kT / 32) ? sm[lane] : 0ull;
-    const int wc = lane < (kT / 32) ? sc[lane] : 0;
-    unsigned long long wi = wv;
-    int wci = wc;
+  unsigned long long wi = lane < kW ? sm[lane] : 0ull;
+  int wci = lane < kW ? sc[lane] : 0;
 #pragma unroll
-    for (int o = 1; o < (kT / 32); o <<= 1) {
-      const unsigned long long tm = __shfl_up_sync(0xffffffffu, wi, o);
-      const int tc = __shfl_up_sync(0xffffffffu, wci, o);
-      if (lane >= o) {
-        wi += tm;
-        wci += tc;
-      }
-    }
-    if (lane < (kT / 32)) {
-      sm[(kT / 32) + lane] = wi - wv;
-      sc[(kT / 32) + lane] = wci - wc;
-    }
-    if (lane == (kT / 32) - 1) {
-      sm[2 * (kT / 32)] = wi;
-      sc[2 * (kT / 32)] = wci;
+  for (int o = 1; o < kW; o <<= 1) {
+    const unsigned long long tm = __shfl_up_sync(0xffffffffu, wi, o);
+    const int tc = __shfl_up_sync(0xffffffffu, wci, o);
+    if (lane >= o) {
+      wi += tm;
+      wci += tc;
     }
   }
-  __syncthreads();
-  mex = sm[(kT / 32) + warp] + mi - m;
-  cex = sc[(kT / 32) + warp] + ci - c;
-  mt = sm[2 * (kT / 32)];
-  ct = sc[2 * (kT / 32)];
+  mt = __shfl_sync(0xffffffffu, wi, kW - 1);
+  ct = __shfl_sync(0xffffffffu, wci, kW - 1);
+  const unsigned long long wex = __shfl_sync(0xffffffffu, wi, warp > 0 ? warp - 1 : 0);
+  const int wcex = __shfl_sync(0xffffffffu, wci, warp > 0 ? warp - 1 : 0);
+  mex = (warp > 0 ? wex : 0ull) + mi - m;
+  cex = (warp > 0 ? wcex : 0) + ci - c;
 }
 
 // ---------------------------------------------------------------------------
