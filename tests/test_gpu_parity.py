@@ -93,7 +93,9 @@ def _check_decode(layer, kdev, vdev, queries, G, p1, p2, dtype, counts=None):
 def test_decode_parity(dtype, profile, n, d, H, G, seed):
     spec, keys, values, queries = _workload(n, d, H, G, profile, seed, steps=2)
     layer, kd, vd = _layer(keys, values, dtype)
-    for p1, p2 in [(0.95, 0.7), (0.99, 0.8), (0.9, 0.7), (1.0, 1.0), (0.5, 0.95)]:
+    # (1.0, 0.7) and (0.8, 1.0): the clamped stage 1 with a real stage-2 cut, and a
+    # stage 2 that keeps the whole retained set (select.cuh's p >= 1 branches)
+    for p1, p2 in [(0.95, 0.7), (0.99, 0.8), (0.9, 0.7), (1.0, 1.0), (0.5, 0.95), (1.0, 0.7), (0.8, 1.0)]:
         for s in range(2):
             _check_decode(layer, layer_rows(kd), layer_rows(vd), queries[s, 0], G, p1, p2, dtype)
 
