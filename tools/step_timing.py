@@ -92,7 +92,7 @@ for j in range(L):
     plan(j)
     attend(j)
 torch.cuda.synchronize()
-print("max active plan clusters by size:", {c: lib.dp_debug_plan_occupancy(views[0], G, c) for c in (8, 10, 12, 14, 16)},
+print("max active plan clusters by size:", {c: lib.dp_debug_plan_occupancy(views[0], G, c) for c in (8, 9, 10, 11, 12, 14, 16)},
       "picked:", lib.dp_debug_plan_occupancy(views[0], G, 0))
 if len(sys.argv) > 4:
     lib.dp_debug_set(1, int(sys.argv[4]))
