@@ -33,7 +33,7 @@ def main():
     cases = int(sys.argv[1]) if len(sys.argv) > 1 else 40
     rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 1234)
     nmax = int(sys.argv[3]) if len(sys.argv) > 3 else 40000
-    sizes = [x for x in (300, 700, 1500, 3000, 6000, 12000, 24000, 40000) if x <= nmax]
+    sizes = [x for x in (300, 700, 1500, 3000, 6000, 12000, 24000, 40000, 80000, 131072) if x <= nmax]
     totals = {"heads": 0, "exact": 0, "order_tie": 0, "threshold_tie": 0, "real": 0, "out_checked": 0,
               "out_fail": 0, "lm_fail": 0}
     worst = {torch.float32: 0.0, torch.bfloat16: 0.0}
